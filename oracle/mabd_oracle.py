@@ -1,0 +1,389 @@
+"""Plain CPU fp64 oracle of one M-ABD implicit step with linear joints.
+
+TEST INFRASTRUCTURE ONLY. Only ``tests/``, ``__graft_entry__.smoke()`` and
+``bench.py`` (cpu_baseline / ``--impl reference``) may import this module. The
+CUDA product path never imports it and shares no code with it.
+
+What it computes ("Plain definition"): with linear joints and one
+Newton iteration a step is exactly the solution of ONE linear KKT system,
+PAPER.md P:460-474 (Eq. kkt) with the footnote P:459 residual term:
+
+    [ H̃   ∇C̃ᵀ ] [ δq ]   [ f̃_A     ]
+    [ ∇C̃  0   ] [ λ  ] = [ −C̃(qⁿ) ]
+
+H̃ = diag_M(H_A^j), H_A^j = diag₄(R_j) H̄_j diag₄(R_jᵀ)
+H̄_j = M_A/h² + K̄_A
+f_A = (1/h) M_A q̇ⁿ + M_A [0₉; g] − [V vec(R Π(RᵀA)); 0₃]
+qⁿ⁺¹ = qⁿ + δq,  q̇ⁿ⁺¹ = δq / h
+
+Each function cites the passage it follows. The KKT is solved by a library
+solver (dense LU, SuperLU on the full KKT, or block LU in a fixed bodies-first
+pivot order: SURVEY §8(c) O3). The specialised CPU solvers at the bottom (block
+Thomas, leaf-to-root elimination) exist only for pin P7 (agreement with the
+brute-force KKT on ≤ 16 bodies).
+
+Readings of the paper used here are listed in DESIGN.md ("Readings") and
+SURVEY §8(c) A1-A21; each is referenced where used.
+"""
+from __future__ import annotations
+
+import numpy as np
+import scipy.sparse as sp
+import scipy.sparse.linalg as spla
+
+__all__ = [
+    "lame", "unpack_mbar", "mass_A", "kbar_A", "hbar_A", "polar", "elastic_force_A", "affine_force",
+    "body_hessians", "constraint_system", "constraint_residual", "predict", "step", "simulate",
+    "block_thomas", "leaf_to_root_solve", "dual_matrix", "rel_err", "T9", "vec", "unvec",
+]
+
+# --------------------------------------------------------------------------
+# conventions
+# --------------------------------------------------------------------------
+
+def vec(A: np.ndarray) -> np.ndarray:
+    """Column-major vec of [...,3,3] → [...,9] (stack the three columns of A)."""
+    A = np.asarray(A)
+    return np.swapaxes(A, -1, -2).reshape(A.shape[:-2] + (9,))
+
+
+def unvec(v: np.ndarray) -> np.ndarray:
+    """Inverse of ``vec``: [...,9] → [...,3,3] with A[:, c] = v[3c:3c+3] (vec⁻¹)."""
+    v = np.asarray(v)
+    return np.swapaxes(v.reshape(v.shape[:-1] + (3, 3)), -1, -2)
+
+
+def _t9() -> np.ndarray:
+    """T₉: the 9×9 permutation with T₉ vec(A) = vec(Aᵀ) (SPEC S:48 'H_lin = μ(I₉+T₉)+…')."""
+    T = np.zeros((9, 9))
+    for r in range(3):
+        for c in range(3):
+            T[3 * c + r, 3 * r + c] = 1.0
+    return T
+
+
+T9 = _t9()
+
+
+def lame(E, nu):
+    """Lamé parameters from (E, ν), standard formulas (P:267-269 names μ, λ)."""
+    E = np.asarray(E, dtype=np.float64)
+    nu = np.asarray(nu, dtype=np.float64)
+    mu = E / (2.0 * (1.0 + nu))
+    lam = E * nu / ((1.0 + nu) * (1.0 - 2.0 * nu))
+    return mu, lam
+
+
+_PACK = [(0, 0), (0, 1), (0, 2), (0, 3), (1, 1), (1, 2), (1, 3), (2, 2), (2, 3), (3, 3)]
+
+
+def unpack_mbar(mbar: np.ndarray) -> np.ndarray:
+    """Packed [...,10] upper triangle (row-major) → symmetric [...,4,4] M̄."""
+    mbar = np.asarray(mbar, dtype=np.float64)
+    M = np.zeros(mbar.shape[:-1] + (4, 4))
+    for k, (i, j) in enumerate(_PACK):
+        M[..., i, j] = mbar[..., k]
+        M[..., j, i] = mbar[..., k]
+    return M
+
+
+def mass_A(mbar: np.ndarray) -> np.ndarray:
+    """Generalized mass M_A = JᵀMJ = M̄ ⊗ I₃ (P:182-184 with P:215).
+
+    With x_i = [x̄_iᵀ ⊗ I₃, I₃] q, JᵀMJ = Σ m_i [x̄_i;1][x̄_i;1]ᵀ ⊗ I₃ = M̄ ⊗ I₃.
+    """
+    return np.kron(unpack_mbar(mbar), np.eye(3)) if np.ndim(mbar) == 1 else \
+        np.einsum("...ij,kl->...ikjl", unpack_mbar(mbar), np.eye(3)).reshape(np.shape(mbar)[:-1] + (12, 12))
+
+
+def kbar_A(V, mu, lam) -> np.ndarray:
+    """Rest-shape generalized stiffness K̄_A = V[μ(I₉+T₉) + λ vec(I)vec(I)ᵀ] ⊕ 0₃.
+
+    The Hessian w.r.t. vec(A) of V·Ψ with ∂Ψ/∂A = μ(A+Aᵀ−2I) + λ tr(A−I) I; the translation
+    block is zero (the energy does not depend on t).
+    """
+    V = np.asarray(V, dtype=np.float64)
+    mu = np.asarray(mu, dtype=np.float64)
+    lam = np.asarray(lam, dtype=np.float64)
+    vI = vec(np.eye(3))
+    Klin = mu[..., None, None] * (np.eye(9) + T9) + lam[..., None, None] * np.outer(vI, vI)
+    K = np.zeros(V.shape + (12, 12))
+    K[..., :9, :9] = V[..., None, None] * Klin
+    return K
+
+
+def hbar_A(mbar, V, E, nu, h) -> np.ndarray:
+    """H̄_A = M_A/h² + K̄_A, the constant (pre-factorizable) body matrix (Eq. abd_final)."""
+    mu, lam = lame(E, nu)
+    return mass_A(mbar) / (h * h) + kbar_A(V, mu, lam)
+
+
+def polar(A: np.ndarray, det_min: float = 1e-9) -> np.ndarray:
+    """Rotation factor R = A(AᵀA)^{-1/2} of the polar decomposition, via the SVD A = UΣVᵀ, R = UVᵀ.
+
+    Raises if det A ≤ det_min (near-singular / inverted bodies are errors).
+    """
+    A = np.asarray(A, dtype=np.float64)
+    d = np.linalg.det(A)
+    if np.any(~np.isfinite(d)) or np.any(d <= det_min):
+        raise FloatingPointError("polar: det(A) <= %g (degenerate or inverted body)" % det_min)
+    U, _, Vt = np.linalg.svd(A)
+    return U @ Vt   # det(A) > 0 ⇒ det(UVᵀ) = +1
+
+
+def elastic_force_A(A, V, mu, lam) -> np.ndarray:
+    """Co-rotated linear-elastic force on the A-DOFs: V vec(R Π(F)), F = RᵀA.
+
+    Π(F) = μ(F+Fᵀ−2I) + λ tr(F−I) I is ∂Ψ/∂A of P:269 evaluated in the co-rotated frame; the volume weight
+    is the J̄ of P:263-265 for F_e = A (constant over the body).
+    """
+    A = np.asarray(A, dtype=np.float64)
+    R = polar(A)
+    F = np.swapaxes(R, -1, -2) @ A
+    I = np.eye(3)
+    trF = np.trace(F, axis1=-2, axis2=-1)
+    Pi = np.asarray(mu)[..., None, None] * (F + np.swapaxes(F, -1, -2) - 2 * I) + \
+        (np.asarray(lam) * (trF - 3.0))[..., None, None] * I
+    return np.asarray(V)[..., None] * vec(R @ Pi)
+
+
+def affine_force(q, qd, mbar, V, E, nu, g, h) -> np.ndarray:
+    """Newton r.h.s. f_A = −∇E at qⁿ for one iteration from q⁽⁰⁾ = qⁿ.
+
+    E(q) = (1/2h²)(q−q̂)ᵀM_A(q−q̂) + VΨ (P:193-199 projected by P:211-215), q̂ = qⁿ + hq̇ⁿ + h²M_A⁻¹f_ext,
+    and f_ext = M_A[0₉; g] for gravity (the projected mass-weighted gravity field). At q = qⁿ:
+    f_A = (1/h) M_A q̇ⁿ + M_A[0₉; g] − [V vec(RΠ); 0₃] (elastic term: SURVEY A3 reads P:260-271 as included).
+    """
+    q = np.asarray(q, dtype=np.float64)
+    MA = mass_A(mbar)
+    mu, lam = lame(E, nu)
+    grav = np.zeros(q.shape)
+    grav[..., 9:12] = g
+    f = np.einsum("...ij,...j->...i", MA, np.asarray(qd) / h + grav)
+    f[..., :9] -= elastic_force_A(unvec(q[..., :9]), V, mu, lam)
+    return f
+
+
+def body_hessians(R, Hbar) -> np.ndarray:
+    """H_A^j = diag₄(R) H̄ diag₄(Rᵀ) (P:256-258 with P:243-254), as dense 12×12 per body."""
+    R = np.asarray(R)
+    D4 = np.zeros(R.shape[:-2] + (12, 12))
+    for k in range(4):
+        D4[..., 3 * k:3 * k + 3, 3 * k:3 * k + 3] = R
+    return D4 @ Hbar @ np.swapaxes(D4, -1, -2)
+
+
+# --------------------------------------------------------------------------
+# constraints (ball = 1 point, linear hinge = 2 points: P:368)
+# --------------------------------------------------------------------------
+
+def constraint_system(scene):
+    """Constant Jacobian ∇C̃ (sparse, 3 rows per joint point) of the point-coincidence constraints.
+
+    A point ȳ on body j sits at x = Aȳ + t = (ȳ_augᵀ ⊗ I₃) q_j, ȳ_aug = [ȳ; 1] (P:182, P:368 with one control
+    point placed at the joint). Row block of point p: +(ȳ_a,augᵀ ⊗ I₃) on body a, −(ȳ_b,augᵀ ⊗ I₃) on body b
+    (the ball constraint S_B^α T^α q^α − S_B^β T^β q^β = 0), or nothing on the world side of an anchor.
+    Returns (J, world) with world[p] the fixed world point of anchors (else 0), so C(q) = J q − world.
+    """
+    n = scene.n
+    P = int(scene.npts.sum())
+    ra = np.repeat(scene.body_a, scene.npts)
+    rb = np.repeat(scene.body_b, scene.npts)
+    rows, cols, vals = [], [], []
+    for side, bodies, ys, sgn in ((0, ra, scene.ybar_a, 1.0), (1, rb, scene.ybar_b, -1.0)):
+        m = bodies >= 0
+        idx = np.nonzero(m)[0]
+        b = bodies[m]
+        y = ys[m]
+        yaug = np.concatenate([y, np.ones((len(idx), 1))], 1)    # [p,4]
+        for c in range(4):
+            for r in range(3):
+                rows.append(3 * idx + r)
+                cols.append(12 * b + 3 * c + r)
+                vals.append(sgn * yaug[:, c])
+    J = sp.csr_matrix((np.concatenate(vals), (np.concatenate(rows), np.concatenate(cols))), shape=(3 * P, 12 * n))
+    world = np.zeros((P, 3))
+    wm = rb < 0
+    world[wm] = scene.ybar_b[wm]
+    return J, world.reshape(-1)
+
+
+def constraint_residual(scene, q) -> float:
+    """max_k ‖C_k(q)‖∞ over all joint points (pin P3, BASELINE north star 'residual below 1e-10')."""
+    J, w = constraint_system(scene)
+    if J.shape[0] == 0:
+        return 0.0
+    return float(np.max(np.abs(J @ np.asarray(q).reshape(-1) - w)))
+
+
+# --------------------------------------------------------------------------
+# one step
+# --------------------------------------------------------------------------
+
+def predict(scene, q, qd, h):
+    """Per-body stages 1-2: R, f_A, H_j, and δq̃ = H_j⁻¹ f_A (Alg. 1 with exact R)."""
+    q = np.asarray(q, dtype=np.float64)
+    A = unvec(q[:, :9])
+    R = polar(A)
+    f = affine_force(q, qd, scene.mbar, scene.volume, scene.youngs, scene.poisson, scene.gravity, h)
+    Hbar = hbar_A(scene.mbar, scene.volume, scene.youngs, scene.poisson, h)
+    H = body_hessians(R, Hbar)
+    dq_tilde = np.linalg.solve(H, f[..., None])[..., 0]
+    return R, f, H, dq_tilde
+
+
+def _natural_order(scene) -> bool:
+    return scene.meta.get("topology") == "chain"
+
+
+def step(scene, q, qd, h, route: str = "auto", return_info: bool = False):
+    """One implicit step = one KKT solve, then qⁿ⁺¹ = qⁿ + δq, q̇ⁿ⁺¹ = δq/h (A6).
+
+    route: 'dense' (LAPACK dgesv on the full KKT), 'superlu' (SuperLU on the full KKT, COLAMD),
+    'blocklu' (bodies first: δq̃ = H⁻¹f, S = ∇C̃H̃⁻¹∇C̃ᵀ, SuperLU on S without pivoting,
+    λ = S⁻¹(∇C̃δq̃ + C(qⁿ)), δq = δq̃ − H̃⁻¹∇C̃ᵀλ), or 'auto' (SURVEY §8(c) O3 size rule).
+    """
+    q = np.asarray(q, dtype=np.float64)
+    qd = np.asarray(qd, dtype=np.float64)
+    n = scene.n
+    R, f, H, dq_tilde = predict(scene, q, qd, h)
+    J, world = constraint_system(scene)
+    m = J.shape[0]
+    c = J @ q.reshape(-1) - world                      # C̃(qⁿ), footnote P:459
+    N = 12 * n + m
+    if route == "auto":
+        route = "dense" if N <= 6000 else ("superlu" if n <= 4096 else "blocklu")
+    if m == 0:
+        dq = dq_tilde.reshape(-1)
+        lam = np.zeros(0)
+    elif route == "dense":
+        K = np.zeros((N, N))
+        for j in range(n):
+            K[12 * j:12 * j + 12, 12 * j:12 * j + 12] = H[j]
+        Jd = J.toarray()
+        K[12 * n:, :12 * n] = Jd
+        K[:12 * n, 12 * n:] = Jd.T
+        rhs = np.concatenate([f.reshape(-1), -c])
+        sol = np.linalg.solve(K, rhs)
+        dq, lam = sol[:12 * n], sol[12 * n:]
+    elif route == "superlu":
+        Hs = sp.bsr_matrix((H, np.arange(n), np.arange(n + 1)), shape=(12 * n, 12 * n)).tocsr()
+        K = sp.bmat([[Hs, J.T], [J, None]], format="csc")
+        rhs = np.concatenate([f.reshape(-1), -c])
+        sol = spla.splu(K).solve(rhs)
+        dq, lam = sol[:12 * n], sol[12 * n:]
+    elif route == "blocklu":
+        Hinv = np.linalg.inv(H)
+        Hinv = 0.5 * (Hinv + np.swapaxes(Hinv, 1, 2))
+        Hi = sp.bsr_matrix((Hinv, np.arange(n), np.arange(n + 1)), shape=(12 * n, 12 * n)).tocsr()
+        S = (J @ Hi @ J.T).tocsc()
+        r = J @ dq_tilde.reshape(-1) + c                # = C(q̃) (P:563-566 plus the footnote term)
+        permc = "NATURAL" if _natural_order(scene) else "MMD_AT_PLUS_A"
+        lu = spla.splu(S, permc_spec=permc, diag_pivot_thresh=0.0, options=dict(SymmetricMode=True))
+        lam = lu.solve(r)
+        dq = dq_tilde.reshape(-1) - Hi @ (J.T @ lam)
+    else:
+        raise ValueError(route)
+    dq = dq.reshape(n, 12)
+    q1 = q + dq
+    qd1 = dq / h
+    if return_info:
+        return q1, qd1, {"q_tilde": q + dq_tilde, "lam": lam, "R": R, "route": route, "f": f}
+    return q1, qd1
+
+
+def simulate(scene, nsteps=None, route: str = "auto", q=None, qd=None, callback=None):
+    q = scene.q0.copy() if q is None else q
+    qd = scene.qd0.copy() if qd is None else qd
+    for k in range(scene.nsteps if nsteps is None else nsteps):
+        q, qd = step(scene, q, qd, scene.h, route=route)
+        if callback is not None:
+            callback(k, q, qd)
+    return q, qd
+
+
+def rel_err(x, ref) -> float:
+    """Parity metric: max_{j,i} |x − ref| / max(|ref|, 1), per entry, SI units."""
+    x = np.asarray(x, dtype=np.float64)
+    ref = np.asarray(ref, dtype=np.float64)
+    if x.size == 0:
+        return 0.0
+    return float(np.max(np.abs(x - ref) / np.maximum(np.abs(ref), 1.0)))
+
+
+# --------------------------------------------------------------------------
+# specialised CPU solvers, only for pin P7 (agreement with the brute-force KKT)
+# --------------------------------------------------------------------------
+
+def dual_matrix(scene, q, qd, h):
+    """Dense dual S = ∇C̃ H̃⁻¹ ∇C̃ᵀ and r = C(q̃) (P:483 with the footnote P:459 term)."""
+    R, f, H, dq_tilde = predict(scene, q, qd, h)
+    J, world = constraint_system(scene)
+    Jd = J.toarray()
+    Hinv = np.zeros((12 * scene.n, 12 * scene.n))
+    for j in range(scene.n):
+        Hinv[12 * j:12 * j + 12, 12 * j:12 * j + 12] = np.linalg.inv(H[j])
+    S = Jd @ Hinv @ Jd.T
+    r = Jd @ (q.reshape(-1) + dq_tilde.reshape(-1)) - world
+    return S, r, Jd, Hinv, dq_tilde
+
+
+def block_thomas(D, B, b):
+    """Block Thomas algorithm for the block-tridiagonal chain dual.
+
+    Solves B_{k-1}ᵀ λ_{k-1} + D_k λ_k + B_k λ_{k+1} = b_k for k = 0..K-1 (P:570-583 layout).
+    D: [K,c,c], B: [K-1,c,c], b: [K,c].
+    """
+    K = len(D)
+    Dp = [None] * K
+    bp = [None] * K
+    Dp[0] = D[0].copy()
+    bp[0] = b[0].copy()
+    for k in range(1, K):                 # forward elimination
+        L = B[k - 1].T @ np.linalg.inv(Dp[k - 1])
+        Dp[k] = D[k] - L @ B[k - 1]
+        bp[k] = b[k] - L @ bp[k - 1]
+    lam = [None] * K
+    lam[K - 1] = np.linalg.solve(Dp[K - 1], bp[K - 1])
+    for k in range(K - 2, -1, -1):        # back substitution
+        lam[k] = np.linalg.solve(Dp[k], bp[k] - B[k] @ lam[k + 1])
+    return np.array(lam)
+
+
+def leaf_to_root_solve(S, r, joint_rows, joint_child, joint_parent, depth):
+    """Exact leaf-to-root elimination of the tree dual (the exact form of P:626-643).
+
+    Block Gaussian elimination of S (dense) where, body by body from the deepest level up, all joints whose
+    child side is that body's children ("child joints of b") are eliminated together; anchors count as child
+    joints of their body. Returns (λ, fill) where ``fill`` is the largest |update| written outside the
+    original block pattern of S (zero for a tree: its dual graph is chordal in this order).
+    joint_rows[k]: row indices of joint k; joint_child[k]: child body (−1 for an anchor);
+    joint_parent[k]: the body the joint hangs from; depth[b]: body depth.
+    """
+    S = np.array(S, dtype=np.float64)
+    r = np.array(r, dtype=np.float64)
+    pattern = np.abs(S) > 0
+    n_b = len(depth)
+    order = sorted(range(n_b), key=lambda b: -depth[b])
+    kids = {b: [k for k in range(len(joint_rows)) if joint_parent[k] == b] for b in range(n_b)}
+    remaining = np.ones(S.shape[0], bool)
+    elim = []
+    fill = 0.0
+    for b in order:
+        X = np.concatenate([joint_rows[k] for k in kids[b]]) if kids[b] else np.zeros(0, int)
+        if len(X) == 0:
+            continue
+        remaining[X] = False
+        Y = np.nonzero(remaining)[0]
+        SXX = S[np.ix_(X, X)]
+        SXY = S[np.ix_(X, Y)]
+        W = np.linalg.solve(SXX, SXY)
+        upd = SXY.T @ W
+        fill = max(fill, float(np.max(np.abs(upd[~pattern[np.ix_(Y, Y)]]), initial=0.0)))
+        S[np.ix_(Y, Y)] -= upd
+        r[Y] -= SXY.T @ np.linalg.solve(SXX, r[X])
+        elim.append((X, Y, SXX, SXY, r[X].copy()))
+    lam = np.zeros_like(r)
+    for X, Y, SXX, SXY, rX in reversed(elim):   # root-to-leaf back substitution
+        lam[X] = np.linalg.solve(SXX, rX - SXY @ lam[Y])
+    return lam, fill

@@ -1,0 +1,384 @@
+"""Pins of the CPU oracle against what the paper and the mathematics fix.
+
+None of these re-type the oracle's formulas: each compares against an independent definition
+(quadrature of JᵀMJ, finite differences of an energy, closed-form trajectories, invariants,
+brute-force KKT) chosen so that a dropped term, a sign or an index error fails one of them.
+"""
+import os
+
+import numpy as np
+import pytest
+import scipy.linalg
+
+import oracle as O
+from mabd_scenes import generators as G
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+
+
+# ----------------------------------------------------------------------------- per-body algebra
+
+def test_polar_examples():
+    """P8 / SPEC S:59-62: R(I)=I, R(2I)=I, R(R₀ diag(1.01,1,0.99)) = R₀, RᵀR = I, det R = 1."""
+    assert np.allclose(O.polar(np.eye(3)), np.eye(3), atol=1e-15)
+    assert np.allclose(O.polar(2 * np.eye(3)), np.eye(3), atol=1e-15)
+    R0 = G.random_rotations(np.random.default_rng(1), 20)
+    A = R0 @ np.diag([1.01, 1.0, 0.99])
+    R = O.polar(A)
+    assert np.max(np.abs(R - R0)) < 1e-12
+    assert np.max(np.abs(np.swapaxes(R, 1, 2) @ R - np.eye(3))) < 1e-13
+    assert np.allclose(np.linalg.det(R), 1.0, atol=1e-13)
+    # symmetric stretch: RᵀA is symmetric positive definite (definition of the polar factor)
+    S = np.swapaxes(R, 1, 2) @ A
+    assert np.max(np.abs(S - np.swapaxes(S, 1, 2))) < 1e-13
+    with pytest.raises(FloatingPointError):
+        O.polar(np.diag([1.0, 1.0, -1.0]))
+
+
+def _gauss_box_points(a, b, c, rho):
+    """2×2×2 Gauss-Legendre points/weights of a box: exact for the quadratic moments of M̄."""
+    g = np.array([-1.0, 1.0]) / np.sqrt(3.0)
+    pts = np.array([[a / 2 * x, b / 2 * y, c / 2 * z] for x in g for y in g for z in g])
+    w = np.full(8, rho * a * b * c / 8.0)
+    return pts, w
+
+
+def test_mass_matrix_is_JtMJ():
+    """M_A = Σ m_i J_iᵀJ_i with J_i = [x̄_iᵀ⊗I₃, I₃], by exact quadrature of a box."""
+    a, b, c, rho = 0.3, 0.1, 0.2, 700.0
+    pts, w = _gauss_box_points(a, b, c, rho)
+    M = np.zeros((12, 12))
+    for x, m in zip(pts, w):
+        Ji = np.hstack([np.kron(x[None, :], np.eye(3)), np.eye(3)])
+        M += m * Ji.T @ Ji
+    assert np.allclose(O.mass_A(G.box_mbar(a, b, c, rho)), M, rtol=0, atol=1e-13 * np.abs(M).max())
+    # 0.1 m cube at ρ = 1000 has translational mass block 1 kg · I₃
+    assert np.allclose(O.mass_A(G.box_mbar(0.1, 0.1, 0.1, 1000.0))[9:, 9:], np.eye(3), atol=1e-15)
+
+
+def _psi_lin(A, mu, lam):
+    """Linear elasticity Ψ = μ‖ε‖² + (λ/2) tr(ε)², ε = ½(A+Aᵀ) − I; its A-gradient is P:269."""
+    e = 0.5 * (A + A.T) - np.eye(3)
+    return mu * np.sum(e * e) + 0.5 * lam * np.trace(e) ** 2
+
+
+def test_kbar_is_fd_hessian_and_nullspace():
+    """K̄_A = Hessian of VΨ by central differences; null space dim 6."""
+    V, mu, lam = 0.002, 3.0e6, 5.0e6
+    K = O.kbar_A(V, mu, lam)
+    A0 = np.eye(3) + 0.01 * np.random.default_rng(2).standard_normal((3, 3))
+    eps = 1e-4
+    Kfd = np.zeros((9, 9))
+    for i in range(9):
+        for j in range(9):
+            def E(di, dj):
+                v = O.vec(A0).copy()
+                v[i] += di
+                v[j] += dj
+                return V * _psi_lin(O.unvec(v), mu, lam)
+            Kfd[i, j] = (E(eps, eps) - E(eps, -eps) - E(-eps, eps) + E(-eps, -eps)) / (4 * eps * eps)
+    assert np.allclose(K[:9, :9], Kfd, rtol=1e-6, atol=1e-6 * np.abs(Kfd).max())
+    assert np.all(K[9:, :] == 0) and np.all(K[:, 9:] == 0)
+    w = np.linalg.eigvalsh(K)
+    assert np.sum(np.abs(w) < 1e-9 * w.max()) == 6
+    # the rigid infinitesimal rotations vec(W), W skew, are in the null space
+    W = np.array([[0, -1, 2], [1, 0, -3], [-2, 3, 0]], float)
+    assert np.max(np.abs(K[:9, :9] @ O.vec(W))) < 1e-9 * np.abs(K).max()
+
+
+def _corot_energy(A, V, mu, lam):
+    """E(A) = V[μ‖S−I‖² + (λ/2)tr(S−I)²], S = (AᵀA)^{1/2} by scipy.linalg.sqrtm.
+
+    Independent of the oracle's SVD route to R.
+    """
+    S = np.real(scipy.linalg.sqrtm(A.T @ A))
+    E = S - np.eye(3)
+    return V * (mu * np.sum(E * E) + 0.5 * lam * np.trace(E) ** 2)
+
+
+def test_elastic_force_is_fd_gradient():
+    """P9: V vec(RΠ(RᵀA)) = ∂E/∂vec(A) for the co-rotated energy (A10); zero at rotations."""
+    rng = np.random.default_rng(3)
+    V, mu, lam = 1e-3, *O.lame(1e8, 0.3)
+    for _ in range(5):
+        R0 = G.random_rotations(rng, 1)[0]
+        A = R0 @ (np.eye(3) + 0.02 * rng.standard_normal((3, 3)))
+        f = O.elastic_force_A(A, V, mu, lam)
+        eps = 1e-7
+        g = np.zeros(9)
+        for i in range(9):
+            vp = O.vec(A).copy()
+            vm = vp.copy()
+            vp[i] += eps
+            vm[i] -= eps
+            g[i] = (_corot_energy(O.unvec(vp), V, mu, lam) - _corot_energy(O.unvec(vm), V, mu, lam)) / (2 * eps)
+        assert np.max(np.abs(f - g)) <= 1e-7 * np.max(np.abs(g))
+        assert np.max(np.abs(O.elastic_force_A(R0, V, mu, lam))) < 1e-12 * V * mu
+
+
+def test_affine_force_is_minus_gradient_of_incremental_potential():
+    """f_A = −∇_q [ (1/2h²)(q−q̂)ᵀM_A(q−q̂) + E_el(q) ] at q = qⁿ, q̂ = qⁿ + hq̇ⁿ + h²[0;g]."""
+    rng = np.random.default_rng(4)
+    sc = G.random_chain(1, seed=4, anchored=False, vel=0.5)
+    q = sc.q0[0].copy()
+    A = O.unvec(q[:9])
+    q[:9] = O.vec(A @ (np.eye(3) + 0.01 * rng.standard_normal((3, 3))))
+    qd = sc.qd0[0]
+    h = 1e-2
+    M = O.mass_A(sc.mbar[0])
+    mu, lam = O.lame(sc.youngs[0], sc.poisson[0])
+    # q̂ from the projected implicit-Euler predictor with M_A⁻¹(JᵀM g-field) = [0;g] computed by solving
+    fext = np.zeros(12)
+    pts, w = _gauss_box_points(*_box_dims(sc.mbar[0]), 1.0)
+    for x, m in zip(pts, w / w.sum() * sc.mbar[0][9]):
+        Ji = np.hstack([np.kron(x[None, :], np.eye(3)), np.eye(3)])
+        fext += m * Ji.T @ sc.gravity
+    qhat = q + h * qd + h * h * np.linalg.solve(M, fext)
+
+    def Etot(x):
+        d = x - qhat
+        return 0.5 / h ** 2 * d @ M @ d + _corot_energy(O.unvec(x[:9]), sc.volume[0], mu, lam)
+
+    eps = 1e-7
+    grad = np.array([(Etot(q + eps * e) - Etot(q - eps * e)) / (2 * eps) for e in np.eye(12)])
+    f = O.affine_force(q, qd, sc.mbar[0], sc.volume[0], sc.youngs[0], sc.poisson[0], sc.gravity, h)
+    assert np.max(np.abs(f + grad)) <= 1e-6 * np.max(np.abs(f))
+
+
+def _box_dims(mbar):
+    m = mbar[9]
+    return tuple(np.sqrt(12.0 * mbar[k] / m) for k in (0, 4, 7))
+
+
+def test_corotation_identities():
+    """P:238-241 diag_N(R)J = J diag₄(R) (point rows: Γ(y)diag₄(R) = RΓ(y)); P:250-254 M_A commutes with diag₄(R)."""
+    rng = np.random.default_rng(5)
+    R = G.random_rotations(rng, 1)[0]
+    D4 = np.kron(np.eye(4), R)
+    y = rng.standard_normal(3)
+    Gy = np.kron(np.append(y, 1.0)[None, :], np.eye(3))
+    assert np.allclose(Gy @ D4, R @ Gy, atol=1e-14)
+    M = O.mass_A(G.box_mbar(0.2, 0.1, 0.05, 900.0))
+    assert np.allclose(D4 @ M @ D4.T, M, atol=1e-14 * np.abs(M).max())
+
+
+# ----------------------------------------------------------------------------- trajectory pins
+
+def test_P1_discrete_free_fall():
+    """P1: tⁿ = t⁰ + nhv⁰ + ½n(n+1)h²g, vⁿ = v⁰ + nhg; A unchanged for A⁰ ∈ SO(3), Ȧ⁰ = 0."""
+    R0 = G.random_rotations(np.random.default_rng(6), 1)[0]
+    v0 = np.array([1.0, -2.0, 3.0])
+    t0 = np.array([0.3, 0.2, 0.1])
+    sc = G.free_body(A0=R0, t0=t0, v0=v0, dims=(0.1, 0.3, 0.2), E=1e8)
+    n = 25
+    q, qd = O.simulate(sc, n)
+    g = sc.gravity
+    h = sc.h
+    t_ref = t0 + n * h * v0 + 0.5 * n * (n + 1) * h * h * g
+    assert np.max(np.abs(q[0, 9:] - t_ref)) <= 1e-14 * np.max(np.abs(t_ref)) * 10
+    assert np.max(np.abs(qd[0, 9:] - (v0 + n * h * g))) <= 1e-13 * np.max(np.abs(v0 + n * h * g))
+    assert np.max(np.abs(q[0, :9] - O.vec(R0))) < 1e-14
+
+
+@pytest.mark.parametrize("maker", [
+    lambda: G.random_chain(9, seed=7, anchored=False, vel=0.3, gravity=False, npts=1, reverse_some=True),
+    lambda: G.random_tree(12, seed=8, anchored=False, vel=0.3, gravity=False, hinge_frac=0.5),
+])
+def test_P2_linear_momentum(maker):
+    """P2: without gravity and anchors, Σ m ṫ is conserved exactly."""
+    sc = maker()
+    m = sc.mbar[:, 9]
+    p0 = (m[:, None] * sc.qd0[:, 9:]).sum(0)
+    q, qd = sc.q0, sc.qd0
+    for _ in range(5):
+        q, qd = O.step(sc, q, qd, sc.h)
+        p = (m[:, None] * qd[:, 9:]).sum(0)
+        assert np.max(np.abs(p - p0)) <= 1e-13 * max(np.max(np.abs(p0)), np.max(m * np.abs(qd[:, 9:]).max(1)))
+
+
+@pytest.mark.parametrize("maker", [
+    lambda: G.cfg1_chain8(),
+    lambda: G.random_chain(10, seed=9, jitter=2e-3, vel=0.2, end_anchor=True),
+    lambda: G.random_tree(14, seed=10, jitter=1e-3, vel=0.2, hinge_frac=0.6),
+    lambda: G.small_net(6, max_off=3),
+])
+def test_P3_constraint_closure(maker):
+    """P3: max‖C(qⁿ⁺¹)‖∞ ≤ 1e-10 m after every step from any start (footnote P:459; A4; BASELINE north star)."""
+    sc = maker()
+    q, qd = sc.q0, sc.qd0
+    for _ in range(4):
+        q, qd = O.step(sc, q, qd, sc.h)
+        assert O.constraint_residual(sc, q) <= 1e-10
+
+
+def _read_golden(name):
+    vals = {}
+    with open(os.path.join(HERE, "golden", name)) as fh:
+        for line in fh:
+            if line.strip() and not line.startswith("#"):
+                k, v = line.split()
+                vals[k] = float(v)
+    return vals
+
+
+@pytest.mark.parametrize("h", [1e-2, 1e-3])
+def test_P4_small_angle_pendulum_period(h):
+    """P4: zero-crossing period of the 2° compound pendulum within 2e-4 s of T₀(1+θ₀²/16) (golden file)."""
+    gold = _read_golden("pendulum_period.txt")
+    sc = G.pendulum(2.0, h=h)
+    q, qd = sc.q0, sc.qd0
+    ys = [q[0, 10]]
+    nsteps = int(round(2.4 * gold["T_s"] / h))
+    for _ in range(nsteps):
+        q, qd = O.step(sc, q, qd, h, route="dense")
+        ys.append(q[0, 10])
+    ys = np.asarray(ys)
+    tt = np.arange(len(ys)) * h
+    idx = np.nonzero(np.sign(ys[:-1]) != np.sign(ys[1:]))[0]
+    zc = tt[idx] - ys[idx] * (tt[idx + 1] - tt[idx]) / (ys[idx + 1] - ys[idx])
+    assert len(zc) >= 4
+    T = 2 * np.mean(np.diff(zc))
+    assert abs(T - gold["T_s"]) <= gold["tolerance_s"], T
+
+
+def test_P5_equilibrium_fixed_point():
+    """P5: zero velocity, zero gravity, satisfied joints, arbitrary rotations → qⁿ⁺¹ = qⁿ."""
+    sc = G.random_tree(15, seed=11, hinge_frac=0.5, gravity=False)
+    q1, qd1 = O.step(sc, sc.q0, sc.qd0, sc.h)
+    assert np.max(np.abs(q1 - sc.q0)) <= 1e-14
+    assert np.max(np.abs(qd1)) <= 1e-12
+
+
+def _rotate_scene(sc, Q, d):
+    s2 = sc.copy()
+    A = O.unvec(sc.q0[:, :9])
+    Ad = O.unvec(sc.qd0[:, :9])
+    s2.q0[:, :9] = O.vec(Q @ A)
+    s2.q0[:, 9:] = sc.q0[:, 9:] @ Q.T + d
+    s2.qd0[:, :9] = O.vec(Q @ Ad)
+    s2.qd0[:, 9:] = sc.qd0[:, 9:] @ Q.T
+    s2.gravity = Q @ sc.gravity
+    wm = np.repeat(sc.body_b, sc.npts) < 0
+    s2.ybar_b[wm] = sc.ybar_b[wm] @ Q.T + d
+    return s2
+
+
+def test_P6_rigid_motion_equivariance():
+    """P6: rotating/translating the whole scene rotates/translates the result (∇C diag₄(R) = R∇C)."""
+    sc = G.random_chain(8, seed=12, vel=0.4, jitter=1e-3, npts=2)
+    Q = G.random_rotations(np.random.default_rng(13), 1)[0]
+    d = np.array([0.5, -1.0, 2.0])
+    q1, _ = O.step(sc, sc.q0, sc.qd0, sc.h)
+    s2 = _rotate_scene(sc, Q, d)
+    q2, _ = O.step(s2, s2.q0, s2.qd0, s2.h)
+    A1 = O.unvec(q1[:, :9])
+    assert np.max(np.abs(O.unvec(q2[:, :9]) - Q @ A1)) < 1e-12
+    assert np.max(np.abs(q2[:, 9:] - (q1[:, 9:] @ Q.T + d))) < 1e-12 * 10
+
+
+# ----------------------------------------------------------------------------- solver pins
+
+@pytest.mark.parametrize("n,anch,end", [(2, False, False), (7, True, False), (16, True, True)])
+def test_P7_block_thomas_vs_dense_kkt(n, anch, end):
+    """P7 / P:568-584: chain dual is block tridiagonal; block Thomas λ = dense-KKT λ (≤ 16 bodies)."""
+    sc = G.random_chain(n, seed=14 + n, anchored=anch, end_anchor=end, vel=0.3, jitter=1e-3)
+    S, r, Jd, Hinv, dqt = O.dual_matrix(sc, sc.q0, sc.qd0, sc.h)
+    K = sc.n_joints
+    # structure (P10): zero outside the block band, symmetric, SPD diagonal blocks
+    for a in range(K):
+        for b in range(K):
+            blk = S[3 * a:3 * a + 3, 3 * b:3 * b + 3]
+            if abs(a - b) > 1:
+                assert np.all(blk == 0)
+        assert np.all(np.linalg.eigvalsh(S[3 * a:3 * a + 3, 3 * a:3 * a + 3]) > 0)
+    assert np.allclose(S, S.T, rtol=0, atol=1e-12 * np.abs(S).max())
+    D = np.array([S[3 * k:3 * k + 3, 3 * k:3 * k + 3] for k in range(K)])
+    B = np.array([S[3 * k:3 * k + 3, 3 * k + 3:3 * k + 6] for k in range(K - 1)])
+    lam_t = O.block_thomas(D, B, r.reshape(K, 3)).reshape(-1)
+    q1, qd1, info = O.step(sc, sc.q0, sc.qd0, sc.h, route="dense", return_info=True)
+    assert O.rel_err(lam_t, info["lam"]) < 1e-10 * max(1.0, np.abs(info["lam"]).max()) or \
+        np.max(np.abs(lam_t - info["lam"])) <= 1e-12 * np.abs(info["lam"]).max()
+    dq = dqt.reshape(-1) - Hinv @ (Jd.T @ lam_t)
+    assert O.rel_err(sc.q0 + dq.reshape(-1, 12), q1) < 1e-12
+
+
+@pytest.mark.parametrize("n,seed", [(3, 20), (9, 21), (16, 22)])
+def test_P7_leaf_to_root_vs_dense_kkt(n, seed):
+    """P7 / A12: exact leaf-to-root elimination of the tree dual = dense KKT; zero fill (chordal dual)."""
+    sc = G.random_tree(n, seed=seed, hinge_frac=0.5, vel=0.3, jitter=1e-3, extra_anchors=1)
+    parent = sc.meta["parent"]
+    depth = np.zeros(n, int)
+    for j in range(1, n):
+        depth[j] = depth[parent[j]] + 1
+    S, r, Jd, Hinv, dqt = O.dual_matrix(sc, sc.q0, sc.qd0, sc.h)
+    rows, child, par = [], [], []
+    off = 0
+    for k in range(sc.n_joints):
+        m = 3 * int(sc.npts[k])
+        rows.append(np.arange(off, off + m))
+        off += m
+        a, b = int(sc.body_a[k]), int(sc.body_b[k])
+        if b < 0:
+            child.append(-1)
+            par.append(a)
+        elif parent[b] == a:
+            child.append(b)
+            par.append(a)
+        else:
+            child.append(a)
+            par.append(b)
+    lam, fill = O.leaf_to_root_solve(S, r, rows, child, par, depth)
+    assert fill == 0.0
+    q1, _, info = O.step(sc, sc.q0, sc.qd0, sc.h, route="dense", return_info=True)
+    assert np.max(np.abs(lam - info["lam"])) <= 1e-10 * np.abs(info["lam"]).max()
+    dq = dqt.reshape(-1) - Hinv @ (Jd.T @ lam)
+    assert O.rel_err(sc.q0 + dq.reshape(-1, 12), q1) < 1e-12
+
+
+@pytest.mark.parametrize("maker", [
+    lambda: G.random_chain(300, seed=30, vel=0.2, jitter=1e-3, end_anchor=True),
+    lambda: G.random_tree(200, seed=31, hinge_frac=0.5, vel=0.2),
+    lambda: G.small_net(12, max_off=4),
+])
+def test_P7_route_agreement(maker):
+    """P7 route agreement: dense LU = SuperLU(full KKT) = block LU (Schur) on the same step."""
+    sc = maker()
+    q_d, _ = O.step(sc, sc.q0, sc.qd0, sc.h, route="dense")
+    q_s, _ = O.step(sc, sc.q0, sc.qd0, sc.h, route="superlu")
+    q_b, _ = O.step(sc, sc.q0, sc.qd0, sc.h, route="blocklu")
+    assert O.rel_err(q_s, q_d) < 1e-12
+    assert O.rel_err(q_b, q_d) < 1e-12
+
+
+def test_P11_decoupling():
+    """P11: chains solved in one scene = each chain solved alone (independence of assemblies)."""
+    sc = G.cfg2_batched_chains(3, 20)
+    q_all, _ = O.step(sc, sc.q0, sc.qd0, sc.h, route="superlu")
+    for c in range(3):
+        sub = G.cfg2_batched_chains(3, 20)
+        keep = slice(20 * c, 20 * c + 20)
+        jk = slice(20 * c, 20 * c + 20)
+        sub.q0, sub.qd0, sub.mbar = sub.q0[keep], sub.qd0[keep], sub.mbar[keep]
+        sub.volume, sub.youngs, sub.poisson = sub.volume[keep], sub.youngs[keep], sub.poisson[keep]
+        ja, jb = sub.body_a[jk] - 20 * c, sub.body_b[jk].copy()
+        jb[jb >= 0] -= 20 * c
+        sub.body_a, sub.body_b, sub.npts = ja, jb, sub.npts[jk]
+        sub.ybar_a, sub.ybar_b = sub.ybar_a[jk], sub.ybar_b[jk]
+        sub.validate()
+        q_c, _ = O.step(sub, sub.q0, sub.qd0, sub.h, route="dense")
+        assert O.rel_err(q_c, q_all[keep]) < 1e-13
+
+
+def test_generators_shapes():
+    """The five BASELINE.json configs have the body/joint/row counts of SURVEY §8 (sizes table)."""
+    s = G.cfg1_chain8()
+    assert (s.n, s.n_joints, s.n_rows) == (8, 8, 24)
+    s = G.cfg3_long_chain(col_len=40, n_cols=4, tail=3)
+    assert s.n == 163 and s.n_joints == 164
+    assert abs(np.linalg.norm(s.ybar_b[-1] - s.ybar_b[0]) - 0.05 * 7) < 1e-12
+    s = G.cfg3_long_chain(col_len=2, n_cols=2, tail=0)   # full size: 194 even columns + 6 → 10.000 m
+    assert s.n == 4
+    s = G.cfg4_binary_tree(5)
+    assert (s.n, s.n_joints, s.n_rows) == (31, 31, 3 + 30 * 6)
+    s = G.cfg5_net(20, max_off=4)
+    assert s.n_joints == 2 * 20 * 19 + int(0.05 * 2 * 20 * 19) + 4
