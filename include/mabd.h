@@ -1,0 +1,142 @@
+/*
+ * mabd.h — C ABI of libmabd.so, the B200 (sm_100a, fp64) hot path of one M-ABD implicit step.
+ *
+ * Method: "M-ABD: Scalable, Efficient, and Robust Multi-Affine-Body Dynamics" (arxiv 2603.08079),
+ * cited as P:<line> of /root/reference/PAPER.md (LaTeX source). One call of mabd_step(h, 1)
+ * performs one Newton iteration of the implicit step (Table 1, "# Iter. 1"):
+ *   (1) per body: polar R of A, f_A = (1/h)M_A q̇ + M_A[0;g] − [V vec(R Π(RᵀA)); 0]
+ *       (P:195-199);
+ *   (2) per body: δq̃ = diag₄(R) H̄⁻¹ diag₄(Rᵀ) f_A with the constant H̄ = M_A/h² + K̄_A
+ *       (Alg. 1 with the exact R);
+ *   (3) the dual (joint-space) solve (∇C̃ H̃⁻¹ ∇C̃ᵀ) λ = C(q̃) (footnote P:459), by topology:
+ *       block-tridiagonal for chains, leaf-to-root elimination for trees (exact
+ *       form, reading A12), sparse for loops/irregular nets;
+ *   (4) q ← q̃ − H̃⁻¹∇C̃ᵀλ, q̇ ← (qⁿ⁺¹ − qⁿ)/h.
+ *
+ * Conventions
+ *   - Everything is IEEE fp64, SI units.
+ *   - q = [vec(A); t] ∈ R¹², vec column-major: q[3c + r] = A[r][c], q[9 + i] = t[i].
+ *   - Arrays of bodies are row-major [n][12] ("AoS" from the caller's view); the library keeps its own
+ *     SoA, topology-ordered copy on the device and undoes the ordering on output.
+ *   - mbar is the packed symmetric 4×4 generalized mass M̄ with M_A = M̄ ⊗ I₃,
+ *     upper triangle row-major (00,01,02,03,11,12,13,22,23,33). This version requires the body frame
+ *     to be central and principal (M̄ diagonal, reading A8); other inputs → MABD_EUNSUPPORTED.
+ *   - Joints are point-coincidence constraints C = x_a(ȳ_a) − x_b(ȳ_b), x(ȳ) = Aȳ + t: a ball joint has
+ *     1 point, the linear ("affine") hinge has 2 points on the axis. body_b = −1
+ *     makes an anchor to the world point stored in ybar_b. Nonlinear joints are not
+ *     supported in this version.
+ *
+ * Ownership
+ *   - Every input pointer is borrowed for the duration of the call only; the library copies what it needs.
+ *   - Device memory: if options.workspace is non-NULL it must hold options.workspace_bytes ≥ the value
+ *     returned by mabd_workspace_size and outlive the handle; the library sub-allocates from it and never
+ *     allocates on the step path. If it is NULL the library allocates (cudaMalloc) inside mabd_create.
+ *   - A handle is bound to the current CUDA device and to options.cuda_stream (NULL = legacy default
+ *     stream) at creation; it is not thread-safe.
+ *
+ * Errors
+ *   - Every call returns mabd_status; nothing is thrown across the ABI. mabd_last_error(handle) returns
+ *     a message for the last failure on that handle (or on the calling thread if handle is NULL).
+ *   - Invalid arguments return MABD_EINVAL and leave the handle unchanged.
+ *   - mabd_step checks a device error word once at the end of the call (one 4-byte D2H copy and a
+ *     stream synchronisation): det A ≤ 1e-9 or a non-finite value → MABD_ENONFINITE, a non-positive
+ *     dual pivot → MABD_ESINGULAR. The message names the first failing step of the call.
+ */
+#ifndef MABD_H
+#define MABD_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef struct mabd_ctx *mabd_handle;
+
+typedef enum {
+  MABD_OK = 0,
+  MABD_EINVAL = 1,       /* bad argument (sizes, indices, h ≤ 0, non-SPD M̄, joint on one body …) */
+  MABD_ESTATE = 2,       /* call out of order (e.g. step before prefactor)                        */
+  MABD_ENOMEM = 3,       /* workspace too small / allocation failed                               */
+  MABD_ECUDA = 4,        /* CUDA runtime error                                                    */
+  MABD_ENCCL = 5,        /* NCCL error (multi-GPU)                                                */
+  MABD_ESINGULAR = 6,    /* dual matrix not SPD (redundant joints)                                */
+  MABD_ENONFINITE = 7,   /* non-finite state or det A ≤ 1e-9                                      */
+  MABD_EUNSUPPORTED = 8  /* input outside this version's scope (non-diagonal M̄, topology …)        */
+} mabd_status;
+
+/* Bodies, in the caller's order. */
+typedef struct {
+  int64_t n;                 /* number of bodies, ≥ 1                                              */
+  const double *q0;          /* [n][12] initial q                                          */
+  const double *qd0;         /* [n][12] initial q̇                                                  */
+  const double *mbar;        /* [n][10] packed M̄ (see above)                                       */
+  const double *volume;      /* [n] V (m³): weight of the elastic force                  */
+  const double *youngs;      /* [n] E (Pa)                                                         */
+  const double *poisson;     /* [n] ν, in (−1, 0.5)                                                 */
+  const int32_t *material;   /* [n] or NULL: ignored hint (the library detects shared materials)   */
+  double gravity[3];         /* m/s²                                                               */
+} mabd_bodies;
+
+/* Joints made of 3-row point-coincidence constraints. */
+typedef struct {
+  int64_t n_joints;          /* K ≥ 0                                                              */
+  const int32_t *body_a;     /* [K] in [0, n)                                                      */
+  const int32_t *body_b;     /* [K] in [−1, n), −1 = world (anchor), ≠ body_a                      */
+  const int32_t *npts;       /* [K] in {1 (ball / anchor), 2 (linear hinge)}                        */
+  const double *ybar_a;      /* [Σnpts][3] material points on body_a (body frame)                  */
+  const double *ybar_b;      /* [Σnpts][3] material points on body_b, or world points for anchors  */
+} mabd_joints;
+
+typedef struct {
+  int32_t newton_iters;      /* must be 1 in this version (Table 1)                                */
+  int32_t residual_rhs;      /* must be 1: include −C(qⁿ) in the dual rhs (footnote P:459)          */
+  int32_t solver;            /* 0 auto | 1 chain | 2 tree | 3 sparse                               */
+  int32_t rank, world;       /* multi-GPU; world = 1 → single GPU                                  */
+  const void *nccl_unique_id;/* 128-byte ncclUniqueId, or NULL when world = 1                      */
+  void *workspace;           /* device memory from the caller (torch), or NULL                     */
+  size_t workspace_bytes;
+  void *cuda_stream;         /* cudaStream_t, or NULL                                              */
+} mabd_options;
+
+/* Topology/solver actually selected (mabd_query). */
+enum { MABD_SOLVER_CHAIN = 1, MABD_SOLVER_TREE = 2, MABD_SOLVER_SPARSE = 3 };
+
+/* Device bytes mabd_create will sub-allocate for these inputs (host analysis only; no GPU work). */
+mabd_status mabd_workspace_size(const mabd_bodies *bodies, const mabd_joints *joints,
+                                const mabd_options *opts, size_t *bytes);
+
+/* Validate, classify the topology, order bodies/joints, copy to the device. */
+mabd_status mabd_create(const mabd_bodies *bodies, const mabd_joints *joints,
+                        const mabd_options *opts, mabd_handle *out);
+
+/* Build the constant per-material H̄⁻¹ data and the solver plan for step size h > 0.
+ * mabd_step with another h re-prefactors transparently. */
+mabd_status mabd_prefactor(mabd_handle h_, double h);
+
+/* Advance nsteps ≥ 0 implicit steps of size h on the handle's stream. Asynchronous apart from the
+ * final error-word check described above. */
+mabd_status mabd_step(mabd_handle h_, double h, int64_t nsteps);
+
+/* Copy the current state out, in the caller's body order ([n][12] each; either pointer may be NULL).
+ * out_on_device != 0 means the pointers are device memory. Synchronises the handle's stream. */
+mabd_status mabd_get_state(mabd_handle h_, double *q_out, double *qd_out, int out_on_device);
+
+/* Overwrite the state (checkpoint restore; stage tests). Same layout as mabd_get_state. */
+mabd_status mabd_set_state(mabd_handle h_, const double *q, const double *qd, int in_on_device);
+
+/* Introspection: selected solver, number of device kernel launches per step, bodies, dual rows. */
+mabd_status mabd_query(mabd_handle h_, int32_t *solver, int32_t *launches_per_step, int64_t *n_bodies,
+                       int64_t *n_dual_rows);
+
+/* Release device memory owned by the library; NULL is a no-op. */
+mabd_status mabd_destroy(mabd_handle h_);
+
+/* Last error message for the handle (or for the calling thread when h_ is NULL). Never NULL. */
+const char *mabd_last_error(mabd_handle h_);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* MABD_H */

@@ -1,0 +1,263 @@
+// Device-side fp64 building blocks of the M-ABD step (sm_100a). No torch types, no host code.
+//
+// Paper references are PAPER.md line numbers (P:n). Conventions: q = [vec(A); t], vec column-major,
+// q[3c+r] = A(r,c). A symmetric 3×3 is packed as (xx, xy, xz, yy, yz, zz).
+#pragma once
+#include <cstdint>
+
+#include "mabd_internal.h"
+
+namespace mabd {
+
+// ------------------------------------------------------------------ small 3×3 helpers
+
+__device__ __forceinline__ void sym_from_full(const double* M, double* S) {
+  S[0] = M[0]; S[1] = M[1]; S[2] = M[2]; S[3] = M[4]; S[4] = M[5]; S[5] = M[8];
+}
+__device__ __forceinline__ void full_from_sym(const double* S, double* M) {
+  M[0] = S[0]; M[1] = S[1]; M[2] = S[2];
+  M[3] = S[1]; M[4] = S[3]; M[5] = S[4];
+  M[6] = S[2]; M[7] = S[4]; M[8] = S[5];
+}
+// row-major 3×3: M[3*r + c]
+__device__ __forceinline__ void mat3_mul(const double* A, const double* B, double* C) {
+#pragma unroll
+  for (int r = 0; r < 3; ++r)
+#pragma unroll
+    for (int c = 0; c < 3; ++c) C[3 * r + c] = A[3 * r] * B[c] + A[3 * r + 1] * B[3 + c] + A[3 * r + 2] * B[6 + c];
+}
+// C = A * Bᵀ
+__device__ __forceinline__ void mat3_mul_bt(const double* A, const double* B, double* C) {
+#pragma unroll
+  for (int r = 0; r < 3; ++r)
+#pragma unroll
+    for (int c = 0; c < 3; ++c)
+      C[3 * r + c] = A[3 * r] * B[3 * c] + A[3 * r + 1] * B[3 * c + 1] + A[3 * r + 2] * B[3 * c + 2];
+}
+// C = Aᵀ * B
+__device__ __forceinline__ void mat3_mul_at(const double* A, const double* B, double* C) {
+#pragma unroll
+  for (int r = 0; r < 3; ++r)
+#pragma unroll
+    for (int c = 0; c < 3; ++c) C[3 * r + c] = A[r] * B[c] + A[3 + r] * B[3 + c] + A[6 + r] * B[6 + c];
+}
+__device__ __forceinline__ void mat3_vec(const double* A, const double* x, double* y) {
+#pragma unroll
+  for (int r = 0; r < 3; ++r) y[r] = A[3 * r] * x[0] + A[3 * r + 1] * x[1] + A[3 * r + 2] * x[2];
+}
+__device__ __forceinline__ void mat3t_vec(const double* A, const double* x, double* y) {
+#pragma unroll
+  for (int r = 0; r < 3; ++r) y[r] = A[r] * x[0] + A[3 + r] * x[1] + A[6 + r] * x[2];
+}
+__device__ __forceinline__ void sym_vec(const double* S, const double* x, double* y) {
+  y[0] = S[0] * x[0] + S[1] * x[1] + S[2] * x[2];
+  y[1] = S[1] * x[0] + S[3] * x[1] + S[4] * x[2];
+  y[2] = S[2] * x[0] + S[4] * x[1] + S[5] * x[2];
+}
+
+// Inverse of an SPD 3×3 (packed sym) by its adjugate; returns false if a leading minor is ≤ 0
+// (the dual matrix must be SPD: a failure means redundant joints, MABD_ESINGULAR).
+__device__ __forceinline__ bool sym_inv_spd(const double* S, double* Si) {
+  const double a = S[0], b = S[1], c = S[2], d = S[3], e = S[4], f = S[5];
+  const double A00 = d * f - e * e, A01 = c * e - b * f, A02 = b * e - c * d;
+  const double det = a * A00 + b * A01 + c * A02;
+  const double m2 = a * d - b * b;
+  const bool ok = (a > 0.0) && (m2 > 0.0) && (det > 0.0) && isfinite(det);
+  const double id = 1.0 / det;
+  Si[0] = A00 * id;
+  Si[1] = A01 * id;
+  Si[2] = A02 * id;
+  Si[3] = (a * f - c * c) * id;
+  Si[4] = (b * c - a * e) * id;
+  Si[5] = m2 * id;
+  return ok;
+}
+
+// ------------------------------------------------------------------ polar decomposition
+// R = A (AᵀA)^{-1/2}. Newton–Schulz X ← X(I − ½(XᵀX − I)) from X₀ = A (quadratic; reading A5),
+// preceded by determinant-scaled Newton X ← ½(ζX + ζ⁻¹X⁻ᵀ) while ‖XᵀX − I‖_max > 0.3.
+// A and R are row-major 3×3. Returns false for det A ≤ 1e-9 or non-finite input.
+__device__ __forceinline__ bool polar_rotation(const double* A, double* R) {
+  const double detA = A[0] * (A[4] * A[8] - A[5] * A[7]) - A[1] * (A[3] * A[8] - A[5] * A[6]) +
+                      A[2] * (A[3] * A[7] - A[4] * A[6]);
+  if (!(detA > 1e-9) || !isfinite(detA)) {
+#pragma unroll
+    for (int i = 0; i < 9; ++i) R[i] = (i % 4 == 0) ? 1.0 : 0.0;
+    return false;
+  }
+  double X[9];
+#pragma unroll
+  for (int i = 0; i < 9; ++i) X[i] = A[i];
+  for (int it = 0; it < 60; ++it) {
+    double E[9];
+    mat3_mul_at(X, X, E);  // XᵀX
+    E[0] -= 1.0; E[4] -= 1.0; E[8] -= 1.0;
+    double emax = 0.0;
+#pragma unroll
+    for (int i = 0; i < 9; ++i) emax = fmax(emax, fabs(E[i]));
+    if (emax > 0.3) {
+      // scaled Newton step (far from orthogonal)
+      const double d = X[0] * (X[4] * X[8] - X[5] * X[7]) - X[1] * (X[3] * X[8] - X[5] * X[6]) +
+                       X[2] * (X[3] * X[7] - X[4] * X[6]);
+      const double z = cbrt(1.0 / d);
+      const double iz = 1.0 / (z * d);  // X⁻ᵀ = cof(X)/det
+      double C[9];
+      C[0] = X[4] * X[8] - X[5] * X[7]; C[1] = X[5] * X[6] - X[3] * X[8]; C[2] = X[3] * X[7] - X[4] * X[6];
+      C[3] = X[2] * X[7] - X[1] * X[8]; C[4] = X[0] * X[8] - X[2] * X[6]; C[5] = X[1] * X[6] - X[0] * X[7];
+      C[6] = X[1] * X[5] - X[2] * X[4]; C[7] = X[2] * X[3] - X[0] * X[5]; C[8] = X[0] * X[4] - X[1] * X[3];
+#pragma unroll
+      for (int i = 0; i < 9; ++i) X[i] = 0.5 * (z * X[i] + iz * C[i]);
+      continue;
+    }
+    double XE[9];
+    mat3_mul(X, E, XE);
+#pragma unroll
+    for (int i = 0; i < 9; ++i) X[i] -= 0.5 * XE[i];
+    if (emax < 1e-8) break;  // next error ≈ ¾·emax² < 1e-16
+  }
+#pragma unroll
+  for (int i = 0; i < 9; ++i) R[i] = X[i];
+  return true;
+}
+
+// ------------------------------------------------------------------ H̄⁻¹ in closed form
+// For a central principal body frame M̄ = diag(a0,a1,a2,m) and K̄_A = V[μ(I₉+T₉) + λ vec(I)vec(I)ᵀ] ⊕ 0,
+// H̄ = M_A/h² + K̄_A splits into: the 3×3 block G on the diagonal entries (A00, A11, A22), three 2×2
+// blocks on the pairs (A_rc, A_cr), r < c, and (m/h²) I₃ on t. H̄⁻¹ keeps that pattern.
+
+__device__ __forceinline__ void hinv_blocks(const Material& M, double mscale, double ih2, HinvBlk& H) {
+  const double Vmu = M.V * M.mu, Vlam = M.V * M.lam;
+  const double a0 = M.a0 * mscale * ih2, a1 = M.a1 * mscale * ih2, a2 = M.a2 * mscale * ih2;
+  double G[6] = {a0 + 2.0 * Vmu + Vlam, Vlam, Vlam, a1 + 2.0 * Vmu + Vlam, Vlam, a2 + 2.0 * Vmu + Vlam};
+  sym_inv_spd(G, H.g);
+  const double ac[3][2] = {{a1, a0}, {a2, a0}, {a2, a1}};  // (mass of column c, mass of column r) per pair
+#pragma unroll
+  for (int k = 0; k < 3; ++k) {
+    const double x = ac[k][0] + Vmu, z = ac[k][1] + Vmu, y = Vmu;
+    const double id = 1.0 / (x * z - y * y);
+    H.pr[k][0] = z * id;
+    H.pr[k][1] = -y * id;
+    H.pr[k][2] = x * id;
+  }
+  H.tinv = 1.0 / (M.m * mscale * ih2);
+}
+
+// out = H̄⁻¹ v (12-vectors in q layout)
+__device__ __forceinline__ void hinv_apply(const HinvBlk& H, const double* v, double* o) {
+  const double d0 = v[0], d1 = v[4], d2 = v[8];
+  o[0] = H.g[0] * d0 + H.g[1] * d1 + H.g[2] * d2;
+  o[4] = H.g[1] * d0 + H.g[3] * d1 + H.g[4] * d2;
+  o[8] = H.g[2] * d0 + H.g[4] * d1 + H.g[5] * d2;
+  // pair (0,1): A01 = q[3], A10 = q[1]
+  o[3] = H.pr[0][0] * v[3] + H.pr[0][1] * v[1];
+  o[1] = H.pr[0][1] * v[3] + H.pr[0][2] * v[1];
+  // pair (0,2): A02 = q[6], A20 = q[2]
+  o[6] = H.pr[1][0] * v[6] + H.pr[1][1] * v[2];
+  o[2] = H.pr[1][1] * v[6] + H.pr[1][2] * v[2];
+  // pair (1,2): A12 = q[7], A21 = q[5]
+  o[7] = H.pr[2][0] * v[7] + H.pr[2][1] * v[5];
+  o[5] = H.pr[2][1] * v[7] + H.pr[2][2] * v[5];
+  o[9] = H.tinv * v[9];
+  o[10] = H.tinv * v[10];
+  o[11] = H.tinv * v[11];
+}
+
+// H̄⁻¹ entry helpers for the 3×3 kernel P(y,y') = Γ(y) H̄⁻¹ Γ(y')ᵀ, Γ(y) = [y_augᵀ ⊗ I₃].
+// self(a,c) = H̄⁻¹[3c+a, 3c+a] for a ≠ c;  cross(a,b) = H̄⁻¹[3b+a, 3a+b] for a ≠ b.
+__device__ __forceinline__ double hinv_self(const HinvBlk& H, int a, int c) {
+  const int lo = a < c ? a : c, hi = a < c ? c : a;
+  const int k = lo + hi - 1;  // (0,1)→0, (0,2)→1, (1,2)→2
+  return a < c ? H.pr[k][0] : H.pr[k][2];
+}
+__device__ __forceinline__ double hinv_cross(const HinvBlk& H, int a, int b) {
+  const int lo = a < b ? a : b, hi = a < b ? b : a;
+  return H.pr[lo + hi - 1][1];
+}
+
+// P_ab = y_a y'_b G⁻¹_ab + [a≠b] y_b y'_a cross(a,b) + [a=b](h²/m + Σ_{c≠a} y_c y'_c self(a,c))   (row-major)
+__device__ __forceinline__ void pblock(const HinvBlk& H, const double* y, const double* yp, double* P) {
+  const double Gf[9] = {H.g[0], H.g[1], H.g[2], H.g[1], H.g[3], H.g[4], H.g[2], H.g[4], H.g[5]};
+#pragma unroll
+  for (int a = 0; a < 3; ++a)
+#pragma unroll
+    for (int b = 0; b < 3; ++b) {
+      double v = y[a] * yp[b] * Gf[3 * a + b];
+      if (a != b) {
+        v += y[b] * yp[a] * hinv_cross(H, a, b);
+      } else {
+        v += H.tinv;
+#pragma unroll
+        for (int c = 0; c < 3; ++c)
+          if (c != a) v += y[c] * yp[c] * hinv_self(H, a, c);
+      }
+      P[3 * a + b] = v;
+    }
+}
+
+// R P Rᵀ (full 3×3 out)
+__device__ __forceinline__ void rot_conj(const double* R, const double* P, double* out) {
+  double T[9];
+  mat3_mul(R, P, T);
+  mat3_mul_bt(T, R, out);
+}
+
+// ------------------------------------------------------------------ per-body predict (stages 1-2)
+// Computes R, q̃ − qⁿ = δq̃ = diag₄(R) H̄⁻¹ diag₄(Rᵀ) f_A with
+// f_A = (1/h) M_A q̇ + M_A[0₉;g] − [V vec(R Π(RᵀA)); 0₃]   (Alg. 1 exact R).
+// Returns false if the polar decomposition failed (det A ≤ 1e-9 / non-finite).
+__device__ __forceinline__ bool predict_body(const double* q, const double* qd, const Material& M, double mscale,
+                                             const HinvBlk& H, double ih, const double* grav, double* R,
+                                             double* dqt) {
+  double A[9];
+#pragma unroll
+  for (int r = 0; r < 3; ++r)
+#pragma unroll
+    for (int c = 0; c < 3; ++c) A[3 * r + c] = q[3 * c + r];
+  const bool ok = polar_rotation(A, R);
+  // F = RᵀA, Π(F) = μ(F+Fᵀ−2I) + λ tr(F−I) I, elastic force V vec(RΠ)
+  double F[9];
+  mat3_mul_at(R, A, F);
+  const double tr = F[0] + F[4] + F[8] - 3.0;
+  double Pi[9];
+#pragma unroll
+  for (int r = 0; r < 3; ++r)
+#pragma unroll
+    for (int c = 0; c < 3; ++c) Pi[3 * r + c] = M.mu * (F[3 * r + c] + F[3 * c + r]) + (r == c ? (M.lam * tr - 2.0 * M.mu) : 0.0);
+  double RPi[9];
+  mat3_mul(R, Pi, RPi);
+  // f_A in q layout, then rotate each 3-block by Rᵀ
+  const double ma[4] = {M.a0 * mscale * ih, M.a1 * mscale * ih, M.a2 * mscale * ih, M.m * mscale};
+  double f[12];
+#pragma unroll
+  for (int c = 0; c < 3; ++c)
+#pragma unroll
+    for (int r = 0; r < 3; ++r) f[3 * c + r] = ma[c] * qd[3 * c + r] - M.V * RPi[3 * r + c];
+#pragma unroll
+  for (int r = 0; r < 3; ++r) f[9 + r] = ma[3] * (qd[9 + r] * ih + grav[r]);
+  double w[12], u[12];
+#pragma unroll
+  for (int k = 0; k < 4; ++k) mat3t_vec(R, f + 3 * k, w + 3 * k);
+  hinv_apply(H, w, u);
+#pragma unroll
+  for (int k = 0; k < 4; ++k) mat3_vec(R, u + 3 * k, dqt + 3 * k);
+  return ok && isfinite(dqt[0] + dqt[4] + dqt[8] + dqt[9] + dqt[10] + dqt[11]);
+}
+
+// x(q; ȳ) = A ȳ + t
+__device__ __forceinline__ void point_pos(const double* q, const double* y, double* x) {
+#pragma unroll
+  for (int r = 0; r < 3; ++r) x[r] = q[r] * y[0] + q[3 + r] * y[1] + q[6 + r] * y[2] + q[9 + r];
+}
+
+// g += s · (ȳ_aug ⊗ w): the body-frame generalized force of a point force w (= Γ(ȳ)ᵀ w)
+__device__ __forceinline__ void add_point_force(double* g, const double* y, const double* w, double s) {
+#pragma unroll
+  for (int r = 0; r < 3; ++r) {
+    g[r] += s * y[0] * w[r];
+    g[3 + r] += s * y[1] * w[r];
+    g[6 + r] += s * y[2] * w[r];
+    g[9 + r] += s * w[r];
+  }
+}
+
+}  // namespace mabd

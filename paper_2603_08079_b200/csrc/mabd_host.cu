@@ -1,0 +1,220 @@
+// libmabd.so host runtime: the C ABI of include/mabd.h.
+//
+// mabd_create: validates the scene, detects shared materials, classifies the joint topology (SURVEY §8(c)
+// A14: forest of paths → chain solver, forest of trees → tree solver, otherwise sparse), orders bodies and
+// joints for the chosen solver, and uploads everything into one device workspace.
+// mabd_prefactor: per-material closed-form H̄⁻¹ and the solver plan.
+// mabd_step: launches the step kernels nsteps times on the handle's stream (no host sync inside the loop).
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <climits>
+#include <cmath>
+#include <cstdarg>
+#include <cstdio>
+#include <cstring>
+#include <string>
+#include <unordered_map>
+#include <vector>
+
+#include "../../include/mabd.h"
+#include "mabd_kernels.h"
+#include "mabd_plan.h"
+
+using namespace mabd;
+
+static thread_local std::string g_thread_err;
+
+struct mabd_ctx {
+  int device = 0;
+  cudaStream_t stream = nullptr;
+  std::string err;
+  bool prefactored = false;
+  double h_pref = 0.0;
+  Plan plan;                 // host-side plan (kept for introspection / sizes)
+  // device memory
+  char* ws = nullptr;
+  size_t ws_bytes = 0;
+  bool own_ws = false;
+  DevPtrs d;
+  int32_t* h_err = nullptr;  // pinned [2]
+  int64_t steps_done = 0;
+};
+
+static mabd_status fail(mabd_ctx* c, mabd_status st, const char* fmt, ...) {
+  char buf[1024];
+  va_list ap;
+  va_start(ap, fmt);
+  vsnprintf(buf, sizeof(buf), fmt, ap);
+  va_end(ap);
+  if (c)
+    c->err = buf;
+  else
+    g_thread_err = buf;
+  return st;
+}
+
+#define CUDA_TRY(c, expr)                                                                          \
+  do {                                                                                             \
+    cudaError_t e_ = (expr);                                                                       \
+    if (e_ != cudaSuccess) return fail((c), MABD_ECUDA, "%s: %s", #expr, cudaGetErrorString(e_)); \
+  } while (0)
+
+extern "C" {
+
+mabd_status mabd_workspace_size(const mabd_bodies* bodies, const mabd_joints* joints, const mabd_options* opts,
+                                size_t* bytes) {
+  if (!bytes) return fail(nullptr, MABD_EINVAL, "bytes is NULL");
+  Plan p;
+  std::string msg;
+  mabd_status st = build_plan(bodies, joints, opts, &p, &msg);
+  if (st != MABD_OK) return fail(nullptr, st, "%s", msg.c_str());
+  *bytes = p.workspace_bytes;
+  return MABD_OK;
+}
+
+mabd_status mabd_create(const mabd_bodies* bodies, const mabd_joints* joints, const mabd_options* opts,
+                        mabd_handle* out) {
+  if (!out) return fail(nullptr, MABD_EINVAL, "out is NULL");
+  *out = nullptr;
+  mabd_ctx* c = new mabd_ctx();
+  std::string msg;
+  mabd_status st = build_plan(bodies, joints, opts, &c->plan, &msg);
+  if (st != MABD_OK) {
+    delete c;
+    return fail(nullptr, st, "%s", msg.c_str());
+  }
+  cudaError_t e = cudaGetDevice(&c->device);
+  if (e != cudaSuccess) {
+    delete c;
+    return fail(nullptr, MABD_ECUDA, "cudaGetDevice: %s", cudaGetErrorString(e));
+  }
+  c->stream = opts ? (cudaStream_t)opts->cuda_stream : nullptr;
+  if (opts && opts->workspace) {
+    if (opts->workspace_bytes < c->plan.workspace_bytes) {
+      size_t need = c->plan.workspace_bytes;
+      delete c;
+      return fail(nullptr, MABD_ENOMEM, "workspace too small: %zu < %zu bytes", opts->workspace_bytes, need);
+    }
+    c->ws = (char*)opts->workspace;
+    c->ws_bytes = opts->workspace_bytes;
+  } else {
+    e = cudaMalloc(&c->ws, c->plan.workspace_bytes);
+    if (e != cudaSuccess) {
+      delete c;
+      return fail(nullptr, MABD_ENOMEM, "cudaMalloc(%zu): %s", c->plan.workspace_bytes, cudaGetErrorString(e));
+    }
+    c->own_ws = true;
+    c->ws_bytes = c->plan.workspace_bytes;
+  }
+  e = cudaMallocHost(&c->h_err, 2 * sizeof(int32_t));
+  if (e == cudaSuccess) e = chain_kernels_init();
+  if (e == cudaSuccess) e = upload_plan(c->plan, c->ws, c->stream, &c->d);
+  if (e == cudaSuccess) e = cudaStreamSynchronize(c->stream);
+  if (e != cudaSuccess) {
+    mabd_destroy(c);
+    return fail(nullptr, MABD_ECUDA, "create: %s", cudaGetErrorString(e));
+  }
+  *out = c;
+  return MABD_OK;
+}
+
+mabd_status mabd_prefactor(mabd_handle c, double h) {
+  if (!c) return fail(nullptr, MABD_EINVAL, "NULL handle");
+  if (!(h > 0.0) || !std::isfinite(h)) return fail(c, MABD_EINVAL, "h must be > 0 (got %g)", h);
+  CUDA_TRY(c, cudaSetDevice(c->device));
+  CUDA_TRY(c, prefactor_device(c->plan, c->d, h, c->stream));
+  c->prefactored = true;
+  c->h_pref = h;
+  return MABD_OK;
+}
+
+mabd_status mabd_step(mabd_handle c, double h, int64_t nsteps) {
+  if (!c) return fail(nullptr, MABD_EINVAL, "NULL handle");
+  if (!c->prefactored) return fail(c, MABD_ESTATE, "mabd_step before mabd_prefactor");
+  if (!(h > 0.0) || !std::isfinite(h)) return fail(c, MABD_EINVAL, "h must be > 0 (got %g)", h);
+  if (nsteps < 0) return fail(c, MABD_EINVAL, "nsteps < 0");
+  if (nsteps == 0) return MABD_OK;
+  CUDA_TRY(c, cudaSetDevice(c->device));
+  if (h != c->h_pref) {
+    mabd_status st = mabd_prefactor(c, h);
+    if (st != MABD_OK) return st;
+  }
+  CUDA_TRY(c, reset_err(c->d, c->stream));
+  for (int64_t s = 0; s < nsteps; ++s) {
+    CUDA_TRY(c, launch_step(c->plan, c->d, h, (int32_t)std::min<int64_t>(s, INT_MAX - 1), c->stream));
+  }
+  CUDA_TRY(c, cudaMemcpyAsync(c->h_err, c->d.err, 2 * sizeof(int32_t), cudaMemcpyDeviceToHost, c->stream));
+  CUDA_TRY(c, cudaStreamSynchronize(c->stream));
+  c->steps_done += nsteps;
+  if (c->h_err[0] & ERR_NONFINITE)
+    return fail(c, MABD_ENONFINITE, "non-finite state or det(A) <= 1e-9 at step %d of this call", c->h_err[1]);
+  if (c->h_err[0] & ERR_SINGULAR)
+    return fail(c, MABD_ESINGULAR, "dual matrix not positive definite (redundant joints?) at step %d of this call",
+                c->h_err[1]);
+  return MABD_OK;
+}
+
+mabd_status mabd_get_state(mabd_handle c, double* q_out, double* qd_out, int out_on_device) {
+  if (!c) return fail(nullptr, MABD_EINVAL, "NULL handle");
+  CUDA_TRY(c, cudaSetDevice(c->device));
+  const int64_t n = c->plan.n;
+  double* dq = out_on_device ? q_out : (q_out ? c->d.io : nullptr);
+  double* dqd = out_on_device ? qd_out : (qd_out ? c->d.io + 12 * n : nullptr);
+  CUDA_TRY(c, launch_gather(c->d.b.q, c->d.b.qd, c->d.b.ld, c->d.perm, n, dq, dqd, c->stream));
+  if (!out_on_device) {
+    if (q_out) CUDA_TRY(c, cudaMemcpyAsync(q_out, dq, 12 * n * sizeof(double), cudaMemcpyDeviceToHost, c->stream));
+    if (qd_out)
+      CUDA_TRY(c, cudaMemcpyAsync(qd_out, dqd, 12 * n * sizeof(double), cudaMemcpyDeviceToHost, c->stream));
+  }
+  CUDA_TRY(c, cudaStreamSynchronize(c->stream));
+  return MABD_OK;
+}
+
+mabd_status mabd_set_state(mabd_handle c, const double* q, const double* qd, int in_on_device) {
+  if (!c) return fail(nullptr, MABD_EINVAL, "NULL handle");
+  CUDA_TRY(c, cudaSetDevice(c->device));
+  const int64_t n = c->plan.n;
+  const double* sq = q;
+  const double* sqd = qd;
+  if (!in_on_device) {
+    if (q) {
+      CUDA_TRY(c, cudaMemcpyAsync(c->d.io, q, 12 * n * sizeof(double), cudaMemcpyHostToDevice, c->stream));
+      sq = c->d.io;
+    }
+    if (qd) {
+      CUDA_TRY(c, cudaMemcpyAsync(c->d.io + 12 * n, qd, 12 * n * sizeof(double), cudaMemcpyHostToDevice, c->stream));
+      sqd = c->d.io + 12 * n;
+    }
+  }
+  CUDA_TRY(c, launch_scatter(c->d.b.q, c->d.b.qd, c->d.b.ld, c->d.perm, n, sq, sqd, c->stream));
+  if (!in_on_device) CUDA_TRY(c, cudaStreamSynchronize(c->stream));
+  return MABD_OK;
+}
+
+mabd_status mabd_query(mabd_handle c, int32_t* solver, int32_t* launches_per_step, int64_t* n_bodies,
+                       int64_t* n_dual_rows) {
+  if (!c) return fail(nullptr, MABD_EINVAL, "NULL handle");
+  if (solver) *solver = c->plan.solver;
+  if (launches_per_step) *launches_per_step = c->plan.launches_per_step;
+  if (n_bodies) *n_bodies = c->plan.n;
+  if (n_dual_rows) *n_dual_rows = c->plan.n_dual_rows;
+  return MABD_OK;
+}
+
+mabd_status mabd_destroy(mabd_handle c) {
+  if (!c) return MABD_OK;
+  cudaSetDevice(c->device);
+  if (c->stream) cudaStreamSynchronize(c->stream);
+  if (c->own_ws && c->ws) cudaFree(c->ws);
+  if (c->h_err) cudaFreeHost(c->h_err);
+  delete c;
+  return MABD_OK;
+}
+
+const char* mabd_last_error(mabd_handle c) {
+  if (c) return c->err.c_str();
+  return g_thread_err.c_str();
+}
+
+}  // extern "C"

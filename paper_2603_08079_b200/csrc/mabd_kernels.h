@@ -1,0 +1,45 @@
+// Kernel launch interface between the host runtime and the CUDA kernels (internal; not part of the ABI).
+#pragma once
+#include <cuda_runtime.h>
+
+#include "mabd_internal.h"
+
+namespace mabd {
+
+struct ChainArgs {
+  BodyArrays b;
+  const uint32_t* slot_info;   // [NS+1] slot encoding (mabd_internal.h)
+  const double* geo;           // [ng][6] (ȳ_L, ȳ_R); world points for anchor sides
+  const int32_t* seg_flags;    // [nseg]
+  const int32_t* seg_red;      // [nseg] ordinal among long segments, −1 otherwise
+  const int32_t* seg_list;     // [nblocks] segment ids of this launch, or null for 0..nblocks−1
+  const HinvBlk* hinv_tab;     // [n_mat] prefactored H̄⁻¹ per material, or null (per-body mass scale)
+  Top* top_out;                // REDUCE output, indexed by seg_red
+  const double* lam_in;        // FINISH input: level-2 λ [n_long][3]
+  StepConsts k;
+};
+
+enum : int32_t { BTD_FUSED = 0, BTD_REDUCE = 1, BTD_FINISH = 2 };
+
+struct BtdArgs {
+  const Top* top_in;           // level L−1 tops, one per unknown
+  const int32_t* left_iface;   // [n_u] or null (then left(u) = u > 0)
+  int64_t n_u;
+  int32_t mode;
+  Top* top_out;                // REDUCE: one per window
+  const double* lam_in;        // FINISH: level L+1 λ, one per window
+  double* lam_out;             // FUSED/FINISH: λ per unknown
+  StepConsts k;
+};
+
+size_t cr_smem_bytes();
+cudaError_t chain_kernels_init();
+cudaError_t launch_chain(const ChainArgs& a, int nblocks, bool finish, cudaStream_t st);
+cudaError_t launch_btd(const BtdArgs& a, int nblocks, cudaStream_t st);
+cudaError_t launch_hinv_table(const Material* mats, int nm, double ih2, HinvBlk* out, cudaStream_t st);
+cudaError_t launch_gather(const double* q, const double* qd, int64_t ld, const int64_t* perm, int64_t n, double* qo,
+                          double* qdo, cudaStream_t st);
+cudaError_t launch_scatter(double* q, double* qd, int64_t ld, const int64_t* perm, int64_t n, const double* qi,
+                           const double* qdi, cudaStream_t st);
+
+}  // namespace mabd

@@ -1,0 +1,506 @@
+// Host-side analysis of a scene: validation, materials, topology classification, chain ordering, the
+// hierarchical reduced-system plan and the device memory layout. Also the per-step launch sequence.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <climits>
+#include <cmath>
+#include <cstring>
+#include <functional>
+#include <string>
+#include <unordered_map>
+#include <vector>
+
+#include "mabd_plan.h"
+
+namespace mabd {
+
+namespace {
+
+struct Key48 {
+  uint64_t w[6];
+  bool operator==(const Key48& o) const { return std::memcmp(w, o.w, sizeof(w)) == 0; }
+};
+struct Key48Hash {
+  size_t operator()(const Key48& k) const {
+    uint64_t h = 1469598103934665603ull;
+    for (int i = 0; i < 6; ++i) {
+      h ^= k.w[i] + 0x9e3779b97f4a7c15ull + (h << 6) + (h >> 2);
+    }
+    return (size_t)h;
+  }
+};
+Key48 key_of(const double* v) {
+  Key48 k;
+  std::memcpy(k.w, v, sizeof(k.w));
+  for (int i = 0; i < 6; ++i)
+    if (v[i] == 0.0) k.w[i] = 0;  // +0 / −0
+  return k;
+}
+
+std::string fmt(const char* f, long long a = 0, long long b = 0) {
+  char buf[512];
+  snprintf(buf, sizeof(buf), f, a, b);
+  return buf;
+}
+
+size_t align_up(size_t x) { return (x + 255) & ~size_t(255); }
+
+}  // namespace
+
+// ------------------------------------------------------------------------------------------ validation
+static mabd_status validate(const mabd_bodies* B, const mabd_joints* J, const mabd_options* o, std::string* msg) {
+  if (!B || !J) return *msg = "bodies/joints NULL", MABD_EINVAL;
+  if (B->n < 1) return *msg = "n must be >= 1", MABD_EINVAL;
+  if (B->n > (int64_t)INT_MAX / 2) return *msg = "too many bodies", MABD_EINVAL;
+  if (!B->q0 || !B->qd0 || !B->mbar || !B->volume || !B->youngs || !B->poisson)
+    return *msg = "a body array is NULL", MABD_EINVAL;
+  if (J->n_joints < 0) return *msg = "n_joints < 0", MABD_EINVAL;
+  if (J->n_joints > 0 && (!J->body_a || !J->body_b || !J->npts || !J->ybar_a || !J->ybar_b))
+    return *msg = "a joint array is NULL", MABD_EINVAL;
+  if (o) {
+    if (o->newton_iters != 0 && o->newton_iters != 1)
+      return *msg = "newton_iters must be 1 in this version", MABD_EUNSUPPORTED;
+    if (o->world > 1) return *msg = "world > 1 is not supported by this build", MABD_EUNSUPPORTED;
+  }
+  for (int64_t i = 0; i < B->n; ++i) {
+    const double* m = B->mbar + 10 * i;
+    const double dmax = std::max(std::max(m[0], m[4]), std::max(m[7], m[9]));
+    if (!(m[0] > 0 && m[4] > 0 && m[7] > 0 && m[9] > 0) || !std::isfinite(dmax))
+      return *msg = fmt("body %lld: mbar diagonal must be positive", (long long)i), MABD_EINVAL;
+    const double off[6] = {m[1], m[2], m[3], m[5], m[6], m[8]};
+    for (double v : off)
+      if (std::fabs(v) > 1e-12 * dmax)
+        return *msg = fmt("body %lld: mbar must be diagonal (central principal body frame, DESIGN.md A8)",
+                          (long long)i),
+               MABD_EUNSUPPORTED;
+    if (!(B->volume[i] > 0) || !(B->youngs[i] > 0) || !(B->poisson[i] > -1.0 && B->poisson[i] < 0.5))
+      return *msg = fmt("body %lld: need V > 0, E > 0, -1 < nu < 0.5", (long long)i), MABD_EINVAL;
+    for (int c = 0; c < 12; ++c)
+      if (!std::isfinite(B->q0[12 * i + c]) || !std::isfinite(B->qd0[12 * i + c]))
+        return *msg = fmt("body %lld: non-finite initial state", (long long)i), MABD_EINVAL;
+  }
+  int64_t P = 0;
+  for (int64_t k = 0; k < J->n_joints; ++k) {
+    const int32_t a = J->body_a[k], b = J->body_b[k], np = J->npts[k];
+    if (a < 0 || a >= B->n) return *msg = fmt("joint %lld: body_a out of range", (long long)k), MABD_EINVAL;
+    if (b < -1 || b >= B->n) return *msg = fmt("joint %lld: body_b out of range", (long long)k), MABD_EINVAL;
+    if (a == b) return *msg = fmt("joint %lld: both ends on body %lld", (long long)k, a), MABD_EINVAL;
+    if (np != 1 && np != 2) return *msg = fmt("joint %lld: npts must be 1 or 2", (long long)k), MABD_EINVAL;
+    P += np;
+  }
+  for (int64_t p = 0; p < 3 * P; ++p)
+    if (!std::isfinite(J->ybar_a[p]) || !std::isfinite(J->ybar_b[p]))
+      return *msg = "non-finite joint point", MABD_EINVAL;
+  return MABD_OK;
+}
+
+// ------------------------------------------------------------------------------------------ materials
+// Bodies that share (V, μ, λ, M̄/m) share a material; their mass ratio is a per-body scale.
+static void detect_materials(const mabd_bodies* B, Plan* p, std::vector<int32_t>* mid_body,
+                             std::vector<double>* msc_body) {
+  std::unordered_map<Key48, int32_t, Key48Hash> map;
+  const int64_t n = B->n;
+  mid_body->resize(n);
+  msc_body->resize(n);
+  p->mats.clear();
+  for (int64_t i = 0; i < n; ++i) {
+    const double* m = B->mbar + 10 * i;
+    const double E = B->youngs[i], nu = B->poisson[i];
+    const double mu = E / (2.0 * (1.0 + nu));
+    const double lam = E * nu / ((1.0 + nu) * (1.0 - 2.0 * nu));
+    const double key[6] = {B->volume[i], mu, lam, m[0] / m[9], m[4] / m[9], m[7] / m[9]};
+    Key48 kk = key_of(key);
+    auto it = map.find(kk);
+    int32_t id;
+    if (it == map.end()) {
+      id = (int32_t)p->mats.size();
+      map.emplace(kk, id);
+      Material M{m[0], m[4], m[7], m[9], B->volume[i], mu, lam, 0.0};
+      p->mats.push_back(M);
+    } else {
+      id = it->second;
+    }
+    (*mid_body)[i] = id;
+    (*msc_body)[i] = m[9] / p->mats[id].m;
+  }
+}
+
+// ------------------------------------------------------------------------------------------ chain topology
+// Forest of paths with ball joints only, each body in ≤ 2 joints, anchors only at path ends (A14).
+static bool chain_build(const mabd_joints* J, int64_t n, Plan* p, std::vector<int64_t>* pos_of_body,
+                        std::string* msg) {
+  const int64_t K = J->n_joints;
+  std::vector<int32_t> deg(n, 0), ideg(n, 0);
+  std::vector<int64_t> pt_off(K + 1, 0);
+  for (int64_t k = 0; k < K; ++k) {
+    if (J->npts[k] != 1) return *msg = "chain solver needs ball joints (npts = 1)", false;
+    pt_off[k + 1] = pt_off[k] + J->npts[k];
+    deg[J->body_a[k]]++;
+    if (J->body_b[k] >= 0) {
+      deg[J->body_b[k]]++;
+      ideg[J->body_a[k]]++;
+      ideg[J->body_b[k]]++;
+    }
+  }
+  for (int64_t i = 0; i < n; ++i)
+    if (deg[i] > 2) return *msg = "a body has more than 2 joints", false;
+  // incidence lists (≤ 2 per body)
+  std::vector<int64_t> inc(2 * n, -1);
+  std::vector<int32_t> cnt(n, 0);
+  for (int64_t k = 0; k < K; ++k) {
+    inc[2 * J->body_a[k] + cnt[J->body_a[k]]++] = k;
+    if (J->body_b[k] >= 0) inc[2 * J->body_b[k] + cnt[J->body_b[k]]++] = k;
+  }
+  auto other = [&](int64_t k, int64_t b) -> int64_t { return J->body_a[k] == b ? J->body_b[k] : J->body_a[k]; };
+  std::vector<char> seen(n, 0);
+  // walk every path from an end (ideg ≤ 1); prefer the end that carries an anchor
+  struct Chain {
+    std::vector<int64_t> bodies;
+    std::vector<int64_t> joints;  // interior joints, joints[i] links bodies[i] and bodies[i+1]
+    int64_t start_anchor = -1, end_anchor = -1;
+  };
+  std::vector<Chain> chains;
+  auto anchor_of = [&](int64_t b, int64_t skip) -> int64_t {
+    for (int s = 0; s < cnt[b]; ++s) {
+      const int64_t k = inc[2 * b + s];
+      if (J->body_b[k] < 0 && k != skip) return k;
+    }
+    return -1;
+  };
+  std::vector<int64_t> starts;
+  for (int64_t i = 0; i < n; ++i)
+    if (ideg[i] <= 1 && anchor_of(i, -1) >= 0) starts.push_back(i);
+  for (int64_t i = 0; i < n; ++i)
+    if (ideg[i] <= 1 && anchor_of(i, -1) < 0) starts.push_back(i);
+  for (int64_t s0 : starts) {
+    if (seen[s0]) continue;
+    Chain ch;
+    int64_t b = s0, prevj = -1;
+    ch.start_anchor = anchor_of(b, -1);
+    while (true) {
+      seen[b] = 1;
+      ch.bodies.push_back(b);
+      int64_t nextj = -1;
+      for (int s = 0; s < cnt[b]; ++s) {
+        const int64_t k = inc[2 * b + s];
+        if (k != prevj && J->body_b[k] >= 0) nextj = k;
+      }
+      if (nextj < 0) break;
+      ch.joints.push_back(nextj);
+      prevj = nextj;
+      b = other(nextj, b);
+      if (seen[b]) return *msg = "cycle in the joint graph", false;
+    }
+    ch.end_anchor = anchor_of(b, ch.start_anchor);
+    if (ch.bodies.size() > 1 || ch.end_anchor != ch.start_anchor) {
+      // anchors at interior bodies are impossible here (deg ≤ 2 and interior bodies have ideg = 2)
+    }
+    if (ch.bodies.size() == 1 && ch.end_anchor == ch.start_anchor) ch.end_anchor = -1;
+    chains.push_back(std::move(ch));
+  }
+  for (int64_t i = 0; i < n; ++i)
+    if (!seen[i]) return *msg = "cycle in the joint graph", false;
+
+  // ---- windows: short chains packed into 256-slot windows, long chains over consecutive windows
+  std::vector<int64_t> chain_base(chains.size());
+  int64_t nwin = 0, used = SEG;  // used = slots used in the current packed window (SEG = none open)
+  std::vector<int32_t> flags;
+  for (size_t c = 0; c < chains.size(); ++c) {
+    const int64_t m = (int64_t)chains[c].bodies.size() + (chains[c].end_anchor >= 0 ? 1 : 0);
+    if (m <= SEG) {
+      if (used + m > SEG) {
+        flags.push_back(0);
+        ++nwin;
+        used = 0;
+      }
+      chain_base[c] = (nwin - 1) * SEG + used;
+      used += m;
+    } else {
+      const int64_t w = (m + SEG - 1) / SEG;
+      chain_base[c] = nwin * SEG;
+      for (int64_t i = 0; i < w; ++i) {
+        int32_t f = SEG_LONG;
+        if (i > 0) f |= SEG_LEFT_IFACE;
+        if (i + 1 < w) f |= SEG_RIGHT_IFACE;
+        flags.push_back(f);
+      }
+      nwin += w;
+      used = SEG;  // do not pack after a long chain's last window
+    }
+  }
+  p->n_windows = nwin;
+  p->ld = nwin * SEG;
+  p->seg_flags = flags;
+  p->slot_info.assign(p->ld + 1, slot_pack(SIDE_NONE, SIDE_NONE, 0));
+  p->geo.assign(6, 0.0);  // geometry 0: zeros (absent slots)
+  std::unordered_map<Key48, uint32_t, Key48Hash> gmap;
+  gmap.emplace(key_of(p->geo.data()), 0u);
+  auto geo_id = [&](const double* yl, const double* yr) -> uint32_t {
+    double v[6] = {yl[0], yl[1], yl[2], yr[0], yr[1], yr[2]};
+    Key48 kk = key_of(v);
+    auto it = gmap.find(kk);
+    if (it != gmap.end()) return it->second;
+    const uint32_t id = (uint32_t)(p->geo.size() / 6);
+    p->geo.insert(p->geo.end(), v, v + 6);
+    gmap.emplace(kk, id);
+    return id;
+  };
+  pos_of_body->assign(n, -1);
+  int64_t rows = 0;
+  for (size_t c = 0; c < chains.size(); ++c) {
+    const Chain& ch = chains[c];
+    const int64_t base = chain_base[c];
+    const int64_t L = (int64_t)ch.bodies.size();
+    for (int64_t i = 0; i < L; ++i) (*pos_of_body)[ch.bodies[i]] = base + i;
+    // slot 0: start anchor (world, body) or absent (none, body)
+    if (ch.start_anchor >= 0) {
+      const int64_t k = ch.start_anchor;  // body_a = body, body_b = world: C = x_a(ȳ_a) − p
+      const uint32_t g = geo_id(J->ybar_b + 3 * k, J->ybar_a + 3 * k);
+      p->slot_info[base] = slot_pack(SIDE_WORLD, SIDE_BODY, g);
+      rows += 3;
+    } else {
+      p->slot_info[base] = slot_pack(SIDE_NONE, SIDE_BODY, 0);
+    }
+    for (int64_t i = 0; i + 1 < L; ++i) {
+      const int64_t k = ch.joints[i];
+      const bool a_left = J->body_a[k] == ch.bodies[i];
+      const double* yl = a_left ? J->ybar_a + 3 * k : J->ybar_b + 3 * k;
+      const double* yr = a_left ? J->ybar_b + 3 * k : J->ybar_a + 3 * k;
+      p->slot_info[base + i + 1] = slot_pack(SIDE_BODY, SIDE_BODY, geo_id(yl, yr));
+      rows += 3;
+    }
+    if (ch.end_anchor >= 0) {
+      const int64_t k = ch.end_anchor;
+      p->slot_info[base + L] = slot_pack(SIDE_BODY, SIDE_WORLD, geo_id(J->ybar_a + 3 * k, J->ybar_b + 3 * k));
+      rows += 3;
+    }
+  }
+  // pt_off unused for ball joints (one point per joint, indexed by joint id)
+  (void)pt_off;
+  p->n_dual_rows = rows;
+  // long windows: ordinal, list, left-interface flags
+  p->seg_red.assign(nwin, -1);
+  p->long_list.clear();
+  p->left_iface.clear();
+  for (int64_t w = 0; w < nwin; ++w)
+    if (p->seg_flags[w] & SEG_LONG) {
+      p->seg_red[w] = (int32_t)p->long_list.size();
+      p->long_list.push_back((int32_t)w);
+      p->left_iface.push_back((p->seg_flags[w] & SEG_LEFT_IFACE) ? 1 : 0);
+    }
+  p->n_long = (int64_t)p->long_list.size();
+  p->levels.clear();
+  if (p->n_long > 0) {
+    int64_t nu = p->n_long;
+    while (true) {
+      BtdLevel L;
+      L.n_u = nu;
+      L.windows = (nu + SEG - 1) / SEG;
+      L.fused = nu <= SEG;
+      p->levels.push_back(L);
+      if (L.fused) break;
+      nu = L.windows;
+    }
+  }
+  const int64_t nl = (int64_t)p->levels.size();
+  p->launches_per_step = 1 + (p->n_long > 0 ? (int32_t)(2 * nl - 1 + 1) : 0);
+  return true;
+}
+
+// ------------------------------------------------------------------------------------------ build_plan
+mabd_status build_plan(const mabd_bodies* B, const mabd_joints* J, const mabd_options* o, Plan* p, std::string* msg) {
+  mabd_status st = validate(B, J, o, msg);
+  if (st != MABD_OK) return st;
+  *p = Plan();
+  p->n = B->n;
+  p->n_joints = J->n_joints;
+  for (int i = 0; i < 3; ++i) p->grav[i] = B->gravity[i];
+  std::vector<int32_t> mid;
+  std::vector<double> msc;
+  detect_materials(B, p, &mid, &msc);
+
+  const int req = o ? o->solver : 0;
+  std::vector<int64_t> pos;
+  std::string why;
+  bool ok = false;
+  if (req == 0 || req == MABD_SOLVER_CHAIN) {
+    ok = chain_build(J, B->n, p, &pos, &why);
+    if (ok) p->solver = MABD_SOLVER_CHAIN;
+    if (!ok && req == MABD_SOLVER_CHAIN) return *msg = "chain solver requested: " + why, MABD_EINVAL;
+  }
+  if (!ok) {
+    *msg = "topology not supported by this build (" + why + ")";
+    return MABD_EUNSUPPORTED;
+  }
+  // per-position arrays
+  const int64_t ld = p->ld;
+  p->perm.assign(B->n, 0);
+  bool multi_mat = p->mats.size() > 1, any_scale = false;
+  for (int64_t i = 0; i < B->n; ++i)
+    if (msc[i] != 1.0) any_scale = true;
+  if (multi_mat) p->mat_id.assign(ld, 0);
+  if (any_scale) p->mscale.assign(ld, 1.0);
+  p->q_soa.assign(12 * ld, 0.0);
+  p->qd_soa.assign(12 * ld, 0.0);
+  for (int64_t i = 0; i < B->n; ++i) {
+    const int64_t s = pos[i];
+    p->perm[i] = s;
+    if (multi_mat) p->mat_id[s] = mid[i];
+    if (any_scale) p->mscale[s] = msc[i];
+    for (int c = 0; c < 12; ++c) {
+      p->q_soa[c * ld + s] = B->q0[12 * i + c];
+      p->qd_soa[c * ld + s] = B->qd0[12 * i + c];
+    }
+  }
+  // ---- device layout
+  size_t cur = 0;
+  auto take = [&](size_t bytes) {
+    const size_t o2 = cur;
+    cur = align_up(cur + std::max<size_t>(bytes, 8));
+    return o2;
+  };
+  Plan::Off& f = p->off;
+  f.q = take(sizeof(double) * 12 * ld);
+  f.qd = take(sizeof(double) * 12 * ld);
+  f.mat_id = multi_mat ? take(sizeof(int32_t) * ld) : 0;
+  f.mscale = any_scale ? take(sizeof(double) * ld) : 0;
+  f.mats = take(sizeof(Material) * p->mats.size());
+  f.hinv = take(sizeof(HinvBlk) * p->mats.size());
+  f.perm = take(sizeof(int64_t) * B->n);
+  f.io = take(sizeof(double) * 24 * B->n);
+  f.err = take(sizeof(int32_t) * 2);
+  if (p->solver == MABD_SOLVER_CHAIN) {
+    f.slot_info = take(sizeof(uint32_t) * (ld + 1));
+    f.geo = take(sizeof(double) * p->geo.size());
+    f.seg_flags = take(sizeof(int32_t) * p->n_windows);
+    f.seg_red = take(sizeof(int32_t) * p->n_windows);
+    f.long_list = take(sizeof(int32_t) * std::max<int64_t>(1, p->n_long));
+    f.left_iface = take(sizeof(int32_t) * std::max<int64_t>(1, p->n_long));
+    f.tops.clear();
+    f.lams.clear();
+    f.tops.push_back(take(sizeof(Top) * std::max<int64_t>(1, p->n_long)));
+    for (const BtdLevel& L : p->levels) {
+      f.lams.push_back(take(sizeof(double) * 3 * L.n_u));
+      if (!L.fused) f.tops.push_back(take(sizeof(Top) * L.windows));
+    }
+  }
+  p->workspace_bytes = cur;
+  return MABD_OK;
+}
+
+// ------------------------------------------------------------------------------------------ device side
+template <class T>
+static cudaError_t put(T* dst, const std::vector<T>& v, cudaStream_t st) {
+  if (v.empty()) return cudaSuccess;
+  return cudaMemcpyAsync(dst, v.data(), sizeof(T) * v.size(), cudaMemcpyHostToDevice, st);
+}
+
+cudaError_t upload_plan(const Plan& p, char* ws, cudaStream_t st, DevPtrs* d) {
+  const Plan::Off& f = p.off;
+  d->b.q = (double*)(ws + f.q);
+  d->b.qd = (double*)(ws + f.qd);
+  d->b.ld = p.ld;
+  d->b.mat_id = p.mat_id.empty() ? nullptr : (const int32_t*)(ws + f.mat_id);
+  d->b.mscale = p.mscale.empty() ? nullptr : (const double*)(ws + f.mscale);
+  d->mats = (Material*)(ws + f.mats);
+  d->b.mats = d->mats;
+  d->hinv = (HinvBlk*)(ws + f.hinv);
+  d->perm = (int64_t*)(ws + f.perm);
+  d->io = (double*)(ws + f.io);
+  d->err = (int32_t*)(ws + f.err);
+  cudaError_t e;
+  if ((e = put(d->b.q, p.q_soa, st))) return e;
+  if ((e = put(d->b.qd, p.qd_soa, st))) return e;
+  if (!p.mat_id.empty() && (e = put((int32_t*)d->b.mat_id, p.mat_id, st))) return e;
+  if (!p.mscale.empty() && (e = put((double*)d->b.mscale, p.mscale, st))) return e;
+  if ((e = put(d->mats, p.mats, st))) return e;
+  if ((e = put(d->perm, p.perm, st))) return e;
+  if (p.solver == MABD_SOLVER_CHAIN) {
+    d->slot_info = (uint32_t*)(ws + f.slot_info);
+    d->geo = (double*)(ws + f.geo);
+    d->seg_flags = (int32_t*)(ws + f.seg_flags);
+    d->seg_red = (int32_t*)(ws + f.seg_red);
+    d->long_list = (int32_t*)(ws + f.long_list);
+    d->left_iface = (int32_t*)(ws + f.left_iface);
+    if ((e = put(d->slot_info, p.slot_info, st))) return e;
+    if ((e = put(d->geo, p.geo, st))) return e;
+    if ((e = put(d->seg_flags, p.seg_flags, st))) return e;
+    if ((e = put(d->seg_red, p.seg_red, st))) return e;
+    if ((e = put(d->long_list, p.long_list, st))) return e;
+    if ((e = put(d->left_iface, p.left_iface, st))) return e;
+    d->tops.clear();
+    d->lams.clear();
+    for (size_t o : f.tops) d->tops.push_back((Top*)(ws + o));
+    for (size_t o : f.lams) d->lams.push_back((double*)(ws + o));
+  }
+  return cudaSuccess;
+}
+
+cudaError_t prefactor_device(const Plan& p, const DevPtrs& d, double h, cudaStream_t st) {
+  return launch_hinv_table(d.mats, (int)p.mats.size(), 1.0 / (h * h), d.hinv, st);
+}
+
+__global__ void err_reset_kernel(int32_t* e) {
+  e[0] = 0;
+  e[1] = INT_MAX;
+}
+
+cudaError_t reset_err(const DevPtrs& d, cudaStream_t st) {
+  err_reset_kernel<<<1, 1, 0, st>>>(d.err);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_step(const Plan& p, const DevPtrs& d, double h, int32_t step, cudaStream_t st) {
+  StepConsts k;
+  k.h = h;
+  k.ih = 1.0 / h;
+  k.ih2 = 1.0 / (h * h);
+  for (int i = 0; i < 3; ++i) k.grav[i] = p.grav[i];
+  k.step_index = step;
+  k.err = d.err;
+  if (p.solver != MABD_SOLVER_CHAIN) return cudaErrorNotSupported;
+  ChainArgs a;
+  a.b = d.b;
+  a.slot_info = d.slot_info;
+  a.geo = d.geo;
+  a.seg_flags = d.seg_flags;
+  a.seg_red = d.seg_red;
+  a.seg_list = nullptr;
+  a.hinv_tab = p.mscale.empty() ? d.hinv : nullptr;
+  a.top_out = d.tops.empty() ? nullptr : d.tops[0];
+  a.lam_in = d.lams.empty() ? nullptr : d.lams[0];
+  a.k = k;
+  cudaError_t e = launch_chain(a, (int)p.n_windows, false, st);
+  if (e != cudaSuccess || p.n_long == 0) return e;
+  const int nl = (int)p.levels.size();
+  // levels i = 0..nl-1 (BTD level i+1): REDUCE for i < nl-1, FUSED at nl-1
+  for (int i = 0; i < nl; ++i) {
+    BtdArgs b;
+    b.top_in = d.tops[i];
+    b.left_iface = (i == 0) ? d.left_iface : nullptr;
+    b.n_u = p.levels[i].n_u;
+    b.mode = p.levels[i].fused ? BTD_FUSED : BTD_REDUCE;
+    b.top_out = p.levels[i].fused ? nullptr : d.tops[i + 1];
+    b.lam_in = nullptr;
+    b.lam_out = d.lams[i];
+    b.k = k;
+    if ((e = launch_btd(b, (int)p.levels[i].windows, st)) != cudaSuccess) return e;
+  }
+  for (int i = nl - 2; i >= 0; --i) {
+    BtdArgs b;
+    b.top_in = d.tops[i];
+    b.left_iface = (i == 0) ? d.left_iface : nullptr;
+    b.n_u = p.levels[i].n_u;
+    b.mode = BTD_FINISH;
+    b.top_out = nullptr;
+    b.lam_in = d.lams[i + 1];
+    b.lam_out = d.lams[i];
+    b.k = k;
+    if ((e = launch_btd(b, (int)p.levels[i].windows, st)) != cudaSuccess) return e;
+  }
+  a.seg_list = d.long_list;
+  return launch_chain(a, (int)p.n_long, true, st);
+}
+
+}  // namespace mabd

@@ -1,0 +1,160 @@
+"""GPU parity of the chain path (configs 1-3 recipes) against the CPU oracle, through the C ABI.
+
+Tolerances (BASELINE.json north star; metric = SURVEY A16): max_{j,i}|q_gpu − q_orc| / max(|q_orc|, 1)
+≤ 1e-9 after one step and ≤ 1e-6 after the multi-step runs.
+"""
+import numpy as np
+import pytest
+
+import oracle as O
+from mabd_scenes import generators as G
+
+pytestmark = pytest.mark.gpu
+
+TOL1 = 1e-9
+TOLN = 1e-6
+
+
+def gpu_run(sc, nsteps, solver=0):
+    from paper_2603_08079_b200 import Simulator
+    sim = Simulator.from_scene(sc, solver=solver)
+    sim.prefactor(sc.h)
+    sim.step(sc.h, nsteps)
+    q, qd = sim.get_state()
+    info = sim.query()
+    sim.close()
+    return q, qd, info
+
+
+def check(sc, nsteps, route="auto", tol=None, solver=0, expect_solver="chain"):
+    q_o, qd_o = O.simulate(sc, nsteps, route=route)
+    q_g, qd_g, info = gpu_run(sc, nsteps, solver)
+    assert info["solver"] == expect_solver
+    err = O.rel_err(q_g, q_o)
+    tol = tol if tol is not None else (TOL1 if nsteps == 1 else TOLN)
+    assert err <= tol, (sc.name, nsteps, err)
+    return err
+
+
+def test_cfg1_one_and_ten_steps(cuda_ok):
+    sc = G.cfg1_chain8()
+    check(sc, 1, route="dense")
+    check(sc, 10, route="dense")
+    q_g, _, _ = gpu_run(sc, 10)
+    assert O.constraint_residual(sc, q_g) <= 1e-10
+
+
+def test_cfg2_recipe_small(cuda_ok):
+    """cfg-2 recipe at 6 chains × 256 (one full segment per chain) plus a ragged 5-chain × 77 batch."""
+    check(G.cfg2_batched_chains(6, 256), 1)
+    check(G.cfg2_batched_chains(6, 256, nsteps=20), 20)
+    check(G.cfg2_batched_chains(5, 77), 3)
+
+
+def test_cfg3_recipe_multi_segment(cuda_ok):
+    """Long chains: 5 segments (one BTD level) and 70k bodies (two BTD levels), both ends pinned."""
+    sc = G.cfg3_long_chain(col_len=300, n_cols=4, tail=5)
+    check(sc, 1)
+    check(sc, 5)
+    sc = G.cfg3_long_chain(col_len=2000, n_cols=35, tail=7)
+    assert sc.n > 256 * 257
+    check(sc, 1)
+    q_g, _, _ = gpu_run(sc, 3)
+    assert O.constraint_residual(sc, q_g) <= 1e-10
+
+
+@pytest.mark.parametrize("seed", range(4))
+def test_random_chains(cuda_ok, seed):
+    """Random geometry, rotations, densities, velocities, joint orientation and anchors (incl. ragged tails)."""
+    rng = np.random.default_rng(seed)
+    parts = []
+    for k in range(6):
+        n = int(rng.integers(1, 600))
+        parts.append(G.random_chain(n, seed=100 * seed + k, anchored=bool(rng.integers(2)),
+                                    end_anchor=bool(rng.integers(2)), vel=0.3, jitter=1e-3,
+                                    reverse_some=True))
+    sc = _concat(parts)
+    check(sc, 1)
+    check(sc, 4)
+
+
+def test_free_bodies_and_double_anchor(cuda_ok):
+    parts = [G.free_body(A0=G.random_rotations(np.random.default_rng(3), 1)[0], v0=(1, 2, 3)),
+             G.random_chain(1, seed=5, anchored=True, end_anchor=True, vel=0.5),
+             G.pendulum(10.0)]
+    sc = _concat(parts)
+    check(sc, 1)
+    check(sc, 50)
+
+
+def test_state_roundtrip_and_errors(cuda_ok):
+    import torch
+    from paper_2603_08079_b200 import MabdError, Simulator
+    sc = G.cfg1_chain8()
+    sim = Simulator.from_scene(sc)
+    with pytest.raises(MabdError) as e:
+        sim.step(sc.h, 1)
+    assert e.value.status == 2   # ESTATE
+    sim.prefactor(sc.h)
+    q, qd = sim.get_state()
+    assert np.array_equal(q, sc.q0) and np.array_equal(qd, sc.qd0)
+    q2 = sc.q0 + 1e-4
+    sim.set_state(q2, sc.qd0)
+    assert np.array_equal(sim.get_state()[0], q2)
+    dq = torch.empty((sc.n, 12), dtype=torch.float64, device="cuda")
+    dqd = torch.empty_like(dq)
+    sim.get_state(dq, dqd)
+    assert np.array_equal(dq.cpu().numpy(), q2)
+    with pytest.raises(MabdError):
+        sim.step(-1.0, 1)
+    bad = sc.q0.copy()
+    bad[3, 0:9] = -bad[3, 0:9]            # det A < 0
+    sim.set_state(bad, sc.qd0)
+    with pytest.raises(MabdError) as e:
+        sim.step(sc.h, 2)
+    assert e.value.status == 7   # ENONFINITE
+    sim.close()
+
+
+def test_h_change_reprefactors(cuda_ok):
+    sc = G.cfg1_chain8()
+    from paper_2603_08079_b200 import Simulator
+    sim = Simulator.from_scene(sc)
+    sim.prefactor(1e-2)
+    sim.step(5e-3, 2)
+    q, _ = sim.get_state()
+    q_o, _ = O.step(sc, sc.q0, sc.qd0, 5e-3)
+    q_o, _ = O.step(sc, q_o, (q_o - sc.q0) / 5e-3, 5e-3)
+    assert O.rel_err(q, q_o) <= TOL1
+    sim.close()
+
+
+def test_determinism(cuda_ok):
+    sc = G.cfg2_batched_chains(8, 256)
+    a, _, _ = gpu_run(sc, 3)
+    b, _, _ = gpu_run(sc, 3)
+    assert np.array_equal(a, b)
+
+
+def _concat(parts):
+    """Concatenate independent scenes into one (bodies and joints renumbered)."""
+    from mabd_scenes.generators import Scene
+    off = 0
+    cat = {k: [] for k in ("q0", "qd0", "mbar", "volume", "youngs", "poisson", "body_a", "body_b", "npts",
+                           "ybar_a", "ybar_b")}
+    for p in parts:
+        for k in ("q0", "qd0", "mbar", "volume", "youngs", "poisson", "npts", "ybar_a", "ybar_b"):
+            cat[k].append(getattr(p, k))
+        cat["body_a"].append(p.body_a + off)
+        bb = p.body_b.copy()
+        bb[bb >= 0] += off
+        cat["body_b"].append(bb)
+        off += p.n
+    arr = {k: np.concatenate(v) for k, v in cat.items()}
+    arr["body_a"] = arr["body_a"].astype(np.int32)
+    arr["body_b"] = arr["body_b"].astype(np.int32)
+    arr["npts"] = arr["npts"].astype(np.int32)
+    sc = Scene(name="concat", gravity=parts[0].gravity.copy(), h=parts[0].h, nsteps=1,
+               meta={"topology": "chain"}, **arr)
+    sc.validate()
+    return sc
