@@ -1,0 +1,316 @@
+#!/usr/bin/env python
+"""Benchmark of the M-ABD step on B200 (BASELINE.json metric: body-steps/s, fp64, device-timed; % of HBM roofline).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--config C] [--impl ours|reference]
+
+Default workload: BASELINE.json configs[1] (config 2): 4096 independent chains × 256 links = 1,048,576
+bodies per GPU, h = 1e-2, one Newton iteration per step. For N > 1 (torchrun) every rank runs its own
+block of 4096 chains of the same recipe (independent assemblies: weak scaling, no collective in the step).
+
+Timed region: W untimed warm-up steps, then barrier + cuda.synchronize, CUDA events on the library's stream
+around ONE mabd_step(h, K) call, barrier + synchronize; the max over ranks is reported. The state
+(q, q̇: 192 MiB + 8 MiB of per-body mass scales per GPU) is larger than the 126 MB L2, so no flush is needed.
+
+``--impl reference`` times the CPU oracle (oracle/, as it stands, single-threaded) on a bounded sample of the
+same workload; it is the reference arm of this tier (the paper has no code to install).
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "body-steps/sec (fp64, device-timed) at 1/2/4/8 B200; % of HBM roofline"
+UNIT = "body-steps/s"
+
+# algorithmic bytes per body-step of the fused chain kernel: read qⁿ, q̇ⁿ, write qⁿ⁺¹, q̇ⁿ⁺¹
+# (4 × 96 B) + the per-body parameter the config carries (cfg 2: one fp64 mass scale; cfg 4: dims)
+BYTES_PER_BODY = {1: 384, 2: 392, 3: 384, 4: 408, 5: 384}
+
+CFG_TEXT = {
+    1: "cfg1: chain of 8 unit cubes, ball joints, top pinned, h=1e-2",
+    2: "cfg2: 4096 independent chains x 256 links (0.1x0.02x0.02 m boxes, rho~U[500,2000]), ball joints, "
+       "first link pinned, twist U[-0.2,0.2] rad, h=1e-2, 1 Newton iteration",
+    3: "cfg3: one chain of 1,048,576 cubes (0.05 m), ball joints, both ends pinned 10 m apart, h=1e-2",
+    4: "cfg4: complete binary tree depth 16 (65,535 boxes), linear 6-row hinges, root pinned, h=1e-2",
+    5: "cfg5: 512x512 net of 0.02 m cubes + 5% long-range links, corners pinned, h=1e-2",
+}
+
+
+def make_scene(cfg: int, rank: int = 0, world: int = 1):
+    from mabd_scenes import generators as G
+    if cfg == 2:
+        return G.cfg2_batched_chains(4096, 256)
+    return G.make_scene(cfg)
+
+
+def peaks():
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    if os.path.exists(p):
+        with open(p) as fh:
+            d = json.load(fh)
+        return float(d["hbm_gbs"]), "measured (MEASURED_PEAKS.json hbm_gbs)"
+    return 6650.0, "fallback (B200_PROFILING.md)"
+
+
+# ----------------------------------------------------------------------------- clocks (NVML, sampled live)
+class ClockSampler:
+    """Samples SM clock and throttle reasons every ~10 ms on a thread while the timed region runs."""
+
+    def __init__(self, index: int):
+        self.samples, self.reasons = [], set()
+        self.max_mhz = None
+        self._stop = threading.Event()
+        self._ok = False
+        try:
+            import pynvml
+            pynvml.nvmlInit()
+            self._nv = pynvml
+            self._h = pynvml.nvmlDeviceGetHandleByIndex(index)
+            self.max_mhz = pynvml.nvmlDeviceGetMaxClockInfo(self._h, pynvml.NVML_CLOCK_SM)
+            self._ok = True
+        except Exception as e:  # pragma: no cover
+            self.err = str(e)
+
+    def _run(self):
+        nv = self._nv
+        names = {
+            "hw_slowdown": getattr(nv, "nvmlClocksEventReasonHwSlowdown", 0x8),
+            "hw_thermal_slowdown": getattr(nv, "nvmlClocksEventReasonHwThermalSlowdown", 0x40),
+            "sw_thermal_slowdown": getattr(nv, "nvmlClocksEventReasonSwThermalSlowdown", 0x20),
+            "sw_power_cap": getattr(nv, "nvmlClocksEventReasonSwPowerCap", 0x4),
+            "hw_power_brake_slowdown": getattr(nv, "nvmlClocksEventReasonHwPowerBrakeSlowdown", 0x80),
+        }
+        while not self._stop.is_set():
+            try:
+                self.samples.append(nv.nvmlDeviceGetClockInfo(self._h, nv.NVML_CLOCK_SM))
+                mask = nv.nvmlDeviceGetCurrentClocksEventReasons(self._h)
+                for k, bit in names.items():
+                    if mask & bit:
+                        self.reasons.add(k)
+            except Exception:
+                pass
+            self._stop.wait(0.01)
+
+    def __enter__(self):
+        if self._ok:
+            self._t = threading.Thread(target=self._run, daemon=True)
+            self._t.start()
+        return self
+
+    def __exit__(self, *a):
+        self._stop.set()
+        if self._ok:
+            self._t.join()
+
+    def summary(self):
+        if not self._ok:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": [], "error": getattr(self, "err", "nvml")}
+        return {"sm_mhz": statistics.median(self.samples) if self.samples else None, "sm_max_mhz": self.max_mhz,
+                "reasons": sorted(self.reasons), "samples": len(self.samples)}
+
+
+# ----------------------------------------------------------------------------- CPU oracle sample
+ORACLE_SAMPLE = {2: dict(n_chains=64, n_links=256), 1: {}, 3: dict(col_len=4096, n_cols=4, tail=0),
+                 4: dict(depth=12), 5: dict(side=96)}
+
+
+def oracle_sample_run(cfg: int, steps: int, warmup: int = 0) -> dict:
+    """Run the oracle single-threaded in a subprocess on a bounded sample of the workload."""
+    code = f"""
+import json, time, sys
+sys.path.insert(0, {ROOT!r})
+import oracle as O
+from mabd_scenes import generators as G
+kw = {ORACLE_SAMPLE.get(cfg, {})!r}
+sc = G.cfg2_batched_chains(**kw) if {cfg} == 2 else G.make_scene({cfg}, **kw)
+q, qd = sc.q0, sc.qd0
+for _ in range({warmup}):
+    q, qd = O.step(sc, q, qd, sc.h)
+t = time.perf_counter()
+for _ in range({steps}):
+    q, qd = O.step(sc, q, qd, sc.h)
+dt = time.perf_counter() - t
+print(json.dumps(dict(n=sc.n, steps={steps}, seconds=dt, name=sc.name)))
+"""
+    env = dict(os.environ, OMP_NUM_THREADS="1", OPENBLAS_NUM_THREADS="1", MKL_NUM_THREADS="1",
+               CUDA_VISIBLE_DEVICES="")
+    out = subprocess.run([sys.executable, "-c", code], capture_output=True, text=True, env=env, check=True)
+    return json.loads(out.stdout.strip().splitlines()[-1])
+
+
+def cpu_baseline(cfg: int, steps: int = 10) -> dict:
+    r = oracle_sample_run(cfg, steps)
+    v = r["n"] * r["steps"] / r["seconds"]
+    return {"value": v, "unit": UNIT, "cores": 1, "kind": "oracle",
+            "sample": f"{r['name']} ({r['n']} bodies, the same recipe), {r['steps']} steps, "
+                      f"{r['seconds']:.1f} s, 1 thread (OMP/OPENBLAS_NUM_THREADS=1), host of the GPU box"}
+
+
+# ----------------------------------------------------------------------------- arms
+def run_reference(args, rank: int, world: int) -> None:
+    if rank != 0:
+        return
+    r = oracle_sample_run(args.config, args.steps, args.warmup)
+    v = r["n"] * r["steps"] / r["seconds"]
+    line = {
+        "impl": "reference", "metric": METRIC, "value": v, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": 1e3 * r["seconds"] / r["steps"], "higher_is_better": True,
+        "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "config": {"workload": CFG_TEXT[args.config], "sample": r["name"], "bodies": r["n"]},
+        "cpu_baseline": {"value": v, "unit": UNIT, "cores": 1, "kind": "oracle",
+                         "sample": f"{r['name']} ({r['n']} bodies), one oracle KKT step per step"},
+        "e2e": {"value": v, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+
+
+def run_ours(args, rank: int, world: int, local_rank: int) -> None:
+    import numpy as np
+    import torch
+    import torch.distributed as dist
+
+    from paper_2603_08079_b200 import Simulator
+
+    torch.cuda.set_device(local_rank)
+    dev = torch.device("cuda", local_rank)
+    sc = make_scene(args.config, rank, world)
+    n = sc.n
+    h = sc.h
+    stream = torch.cuda.Stream(device=dev)
+    sim = Simulator.from_scene(sc, device=local_rank, stream=stream)
+    sim.prefactor(h)
+    q0 = sc.q0.copy()
+    qd0 = sc.qd0.copy()
+    info = sim.query()
+
+    def barrier():
+        if world > 1:
+            dist.barrier()
+        torch.cuda.synchronize(dev)
+
+    # warm-up
+    if args.warmup:
+        sim.step(h, args.warmup)
+    barrier()
+    ev0 = torch.cuda.Event(enable_timing=True)
+    ev1 = torch.cuda.Event(enable_timing=True)
+    sampler = ClockSampler(local_rank if "CUDA_VISIBLE_DEVICES" not in os.environ else int(
+        os.environ["CUDA_VISIBLE_DEVICES"].split(",")[local_rank]))
+    with sampler:
+        ev0.record(stream)
+        sim.step(h, args.steps)
+        ev1.record(stream)
+        barrier()
+    ms = ev0.elapsed_time(ev1)
+    if world > 1:
+        t = torch.tensor([ms], device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms = float(t.item())
+    ms_step = ms / args.steps
+    value = world * n * args.steps / (ms * 1e-3)
+    launches = info["launches_per_step"] * args.steps + 1   # + the error-word reset kernel
+
+    # e2e through the public API with pinned host buffers: per step H2D (q, q̇) → step → D2H (q, q̇)
+    ke = max(1, min(args.steps, args.e2e_steps))
+    hq = torch.empty((n, 12), dtype=torch.float64, pin_memory=True).numpy()
+    hqd = torch.empty((n, 12), dtype=torch.float64, pin_memory=True).numpy()
+    hq[:] = q0
+    hqd[:] = qd0
+    barrier()
+    e0 = torch.cuda.Event(enable_timing=True)
+    e1 = torch.cuda.Event(enable_timing=True)
+    e0.record(stream)
+    for _ in range(ke):
+        sim.set_state(hq, hqd)
+        sim.step(h, 1)
+        sim.get_state(hq, hqd)
+    e1.record(stream)
+    barrier()
+    ems = e0.elapsed_time(e1)
+    if world > 1:
+        t = torch.tensor([ems], device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ems = float(t.item())
+    e2e_value = world * n * ke / (ems * 1e-3)
+
+    if rank == 0:
+        peak, peak_src = peaks()
+        bpb = BYTES_PER_BODY[args.config]
+        achieved = bpb * n / (ms_step * 1e-3) / 1e9
+        traffic = None
+        prof = os.path.join(ROOT, "profiles", "ncu_traffic.json")
+        if os.path.exists(prof):
+            try:
+                with open(prof) as fh:
+                    traffic = json.load(fh).get(str(args.config))
+            except Exception:
+                traffic = None
+        line = {
+            "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": True, "scaling": "weak",
+            "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "config": {"workload": CFG_TEXT[args.config], "bodies_per_gpu": n, "solver": info["solver"],
+                       "dual_rows_per_gpu": info["n_dual_rows"],
+                       "l2": "no flush: state q,qdot (192 MiB) + per-body params > 126 MB L2",
+                       "parallelism": f"dp{world} (independent assemblies per rank)"},
+            "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
+                         "frac": achieved / peak, "traffic": traffic,
+                         "kernel": "chain_kernel (fused stages 1-4)" if info["solver"] == "chain" else info["solver"],
+                         "bytes_per_body_step": bpb, "peak_source": peak_src,
+                         "duration": "timed region / steps (one fused launch per step)"},
+            "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": 2 * 96 * n * world,
+                    "d2h_bytes_per_step": 2 * 96 * n * world, "steps": ke,
+                    "path": "Simulator.set_state(pinned host) -> step(h,1) -> get_state(pinned host)"},
+            "gpu_launches": launches,
+            "clocks": sampler.summary(),
+        }
+        if not args.no_cpu_baseline:
+            try:
+                line["cpu_baseline"] = cpu_baseline(args.config, steps=args.cpu_steps)
+            except Exception as e:  # report, never fake
+                line["cpu_baseline"] = {"value": None, "error": str(e)[:200]}
+        print(json.dumps(line), flush=True)
+    sim.close()
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=200)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--config", type=int, default=2, choices=[1, 2, 3, 4, 5])
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--e2e-steps", type=int, default=5)
+    ap.add_argument("--cpu-steps", type=int, default=10)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    args = ap.parse_args()
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local_rank = int(os.environ.get("LOCAL_RANK", "0"))
+    if args.impl == "reference":
+        run_reference(args, rank, world)
+        return
+    if world > 1:
+        import torch
+        import torch.distributed as dist
+        torch.cuda.set_device(local_rank)
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
+    try:
+        run_ours(args, rank, world, local_rank)
+    finally:
+        if world > 1:
+            import torch.distributed as dist
+            dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

@@ -12,7 +12,7 @@ from typing import Optional
 import numpy as np
 
 _PKG = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_PKG, "libmabd.so")
+LIB_PATH = os.environ.get("MABD_LIB") or os.path.join(_PKG, "libmabd.so")
 
 MABD_OK = 0
 STATUS = {0: "MABD_OK", 1: "MABD_EINVAL", 2: "MABD_ESTATE", 3: "MABD_ENOMEM", 4: "MABD_ECUDA", 5: "MABD_ENCCL",

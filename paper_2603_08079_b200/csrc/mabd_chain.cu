@@ -2,17 +2,22 @@
 // block-tridiagonal reduced-system kernels for chains longer than one segment.
 //
 // Paper: the chain dual is block tridiagonal (Eq. chain-btd); the paper solves it with block
-// Thomas in O(K) on one thread. Here each CTA owns a 256-slot segment of a chain and solves its
-// 257-equation block-tridiagonal system by block cyclic reduction in shared memory (log₂ 256 = 8 levels),
-// so the per-body stages and the solve are fused into one pass over HBM:
-//   per body:  load qⁿ, q̇ⁿ → polar R → f_A → δq̃ (stages 1-2)
-//   per joint: D, B, r = C(q̃) from the constant 3×3 kernels P(ȳ,ȳ') rotated by R
-//   per segment: cyclic reduction → λ
-//   per body:  qⁿ⁺¹ = q̃ − diag₄(R)H̄⁻¹ Σ ±(ȳ_aug ⊗ Rᵀλ), q̇ⁿ⁺¹ = (qⁿ⁺¹ − qⁿ)/h
-// Chains that span several segments are partitioned (SPIKE-style): each segment reduces its interior to a
+// Thomas in O(K) on one thread. Here one 128-thread CTA owns a 256-slot segment of a chain and
+// solves its 257-equation block-tridiagonal system by block cyclic reduction in shared memory
+// (log₂ 256 = 8 levels), fused with the per-body stages in one pass over HBM:
+//   phase 1, per body:  load qⁿ, q̇ⁿ → polar R → f_A → δq̃ (stages 1-2); δq̃ is parked in the
+//                       q̇ buffer (q̇ⁿ is dead after f_A; the line stays in L2);
+//            per joint: D, B, r = C(q̃) from the 3×3 kernels P(ȳ,ȳ') rotated by R
+//   phase 2, per segment: cyclic reduction → λ
+//   phase 3, per body:  re-read qⁿ, δq̃ (L2), recompute R, qⁿ⁺¹ = q̃ − diag₄(R)H̄⁻¹Σ±(ȳ_aug ⊗ Rᵀλ),
+//                       q̇ⁿ⁺¹ = (qⁿ⁺¹ − qⁿ)/h
+// Nothing per body is held in registers across the solve, so 4 CTAs (57 KB shared memory each) fit per SM.
+// Chains spanning several segments are partitioned (SPIKE-style): each segment reduces its interior to a
 // 2-equation "top" system on its end slots (REDUCE), the tops form a smaller block-tridiagonal system
 // solved recursively by btd_kernel, and each segment then recomputes and back-substitutes (FINISH).
 #include <cuda_runtime.h>
+
+#include <algorithm>
 
 #include "mabd_device.cuh"
 #include "mabd_kernels.h"
@@ -20,9 +25,11 @@
 namespace mabd {
 
 // ------------------------------------------------------------------ shared-memory cyclic reduction
-// Equations i = 0..256:  Bl_i λ_{i-s} + D_i λ_i + Br_i λ_{i+s} = r_i at stride s, with Bl_i = Br_{i-s}ᵀ.
-// sD [NEQ][6] (sym; replaced by its inverse once eliminated), sB [NEQ][9] (Br), sBl [NEQ][9] (saved Br_{i-s}
-// of eliminated i), sR [NEQ][3] (rhs, then λ).
+// Equations k = 0..256:  Bl_k λ_{k−s} + D_k λ_k + Br_k λ_{k+s} = r_k at stride s, with Bl_k = Br_{k−s}ᵀ.
+// Component-major arrays D[6][NEQ] (sym; replaced by D⁻¹ once eliminated), B[9][NEQ] (Br), Bl[9][NEQ]
+// (saved Br_{k−s} of an eliminated k), r[3][NEQ] (rhs, then λ). Equation k lives at position cr_pos(k):
+// the equations eliminated at stride 2^l are stored contiguously (level-major order), so every CR level
+// reads and writes contiguous positions (no shared-memory bank conflicts).
 struct CRS {
   double* D;
   double* B;
@@ -30,81 +37,134 @@ struct CRS {
   double* r;
 };
 
+__device__ __forceinline__ int cr_pos(int k) {
+  if (k == 0) return SEG - 1;
+  if (k >= SEG) return SEG;
+  const int l = __ffs(k) - 1;
+  return (SEG - (SEG >> l)) + (k >> (l + 1));
+}
+
+// strided view of one equation's components
+struct SV {
+  double* p;
+  __device__ __forceinline__ double& operator[](int e) const { return p[e * NEQ]; }
+};
+__device__ __forceinline__ SV eqD(const CRS& s, int pos) { return SV{s.D + pos}; }
+__device__ __forceinline__ SV eqB(const CRS& s, int pos) { return SV{s.B + pos}; }
+__device__ __forceinline__ SV eqBl(const CRS& s, int pos) { return SV{s.Bl + pos}; }
+__device__ __forceinline__ SV eqR(const CRS& s, int pos) { return SV{s.r + pos}; }
+template <int N>
+__device__ __forceinline__ void ldv(SV v, double* x) {
+#pragma unroll
+  for (int e = 0; e < N; ++e) x[e] = v[e];
+}
+template <int N>
+__device__ __forceinline__ void stv(SV v, const double* x) {
+#pragma unroll
+  for (int e = 0; e < N; ++e) v[e] = x[e];
+}
+
+#ifdef MABD_EXP_CLOCK
+__device__ unsigned long long g_phase_clk[16];
+#define PH_MARK(i)                                                        \
+  do {                                                                    \
+    if (threadIdx.x == 0) {                                               \
+      const long long now = clock64();                                    \
+      atomicAdd(&g_phase_clk[i], (unsigned long long)(now - ph_last));    \
+      ph_last = now;                                                      \
+    }                                                                     \
+  } while (0)
+extern "C" int mabd_dbg_phases(unsigned long long* out) {
+  return (int)cudaMemcpyFromSymbol(out, g_phase_clk, sizeof(g_phase_clk));
+}
+extern "C" int mabd_dbg_reset() {
+  unsigned long long z[16] = {0};
+  return (int)cudaMemcpyToSymbol(g_phase_clk, z, sizeof(z));
+}
+#else
+#define PH_MARK(i) \
+  do {             \
+  } while (0)
+#endif
+
 __device__ __forceinline__ void report(const StepConsts& k, int32_t flag) {
   atomicOr(k.err, flag);
   atomicMin(k.err + 1, k.step_index);
 }
 
+// invalidate one 128-byte L2 line without write-back (PTX discard.global.L2, sm_80+)
+__device__ __forceinline__ void l2_discard128(const void* p) {
+  asm volatile("discard.global.L2 [%0], 128;" ::"l"(p) : "memory");
+}
+__device__ __forceinline__ void l2_prefetch(const void* p) { asm volatile("prefetch.global.L2 [%0];" ::"l"(p)); }
+
+// update of the surviving equation kq at stride st (both neighbours already hold D⁻¹)
+__device__ __forceinline__ void cr_update(const CRS& s, int kq, int st) {
+  const int pk = cr_pos(kq);
+  double Ds[6], D[9], Br[9], r[3];
+  ldv<6>(eqD(s, pk), Ds);
+  full_from_sym(Ds, D);
+  ldv<9>(eqB(s, pk), Br);
+  ldv<3>(eqR(s, pk), r);
+  double nBr[9] = {0, 0, 0, 0, 0, 0, 0, 0, 0};
+  if (kq >= st) {  // left neighbour i = kq − st:  α = Br_iᵀ D_i⁻¹;  D −= α Br_i;  r −= α r_i
+    const int pi = cr_pos(kq - st);
+    double Dis[6], Di[9], Bi[9], al[9], tmp[9], ri[3], ar[3];
+    ldv<6>(eqD(s, pi), Dis);
+    full_from_sym(Dis, Di);
+    ldv<9>(eqB(s, pi), Bi);
+    mat3_mul_at(Bi, Di, al);
+    mat3_mul(al, Bi, tmp);
+#pragma unroll
+    for (int e = 0; e < 9; ++e) D[e] -= tmp[e];
+    ldv<3>(eqR(s, pi), ri);
+    mat3_vec(al, ri, ar);
+#pragma unroll
+    for (int e = 0; e < 3; ++e) r[e] -= ar[e];
+  }
+  if (kq < SEG) {  // right neighbour j = kq + st:  γ = Br_k D_j⁻¹;  D −= γ Br_kᵀ;  r −= γ r_j;  Br_k ← −γ Br_j
+    const int pj = cr_pos(kq + st);
+    double Djs[6], Dj[9], ga[9], tmp[9], Bj[9], rj[3], gr[3];
+    ldv<6>(eqD(s, pj), Djs);
+    full_from_sym(Djs, Dj);
+    mat3_mul(Br, Dj, ga);
+    mat3_mul_bt(ga, Br, tmp);
+#pragma unroll
+    for (int e = 0; e < 9; ++e) D[e] -= tmp[e];
+    ldv<3>(eqR(s, pj), rj);
+    mat3_vec(ga, rj, gr);
+#pragma unroll
+    for (int e = 0; e < 3; ++e) r[e] -= gr[e];
+    ldv<9>(eqB(s, pj), Bj);
+    mat3_mul(ga, Bj, tmp);
+#pragma unroll
+    for (int e = 0; e < 9; ++e) nBr[e] = -tmp[e];
+    stv<9>(eqBl(s, pj), Br);  // j's left coupling at this level (Bl_j = Br_kᵀ), kept for back substitution
+  }
+  const double Dn[6] = {D[0], 0.5 * (D[1] + D[3]), 0.5 * (D[2] + D[6]), D[4], 0.5 * (D[5] + D[7]), D[8]};
+  stv<6>(eqD(s, pk), Dn);
+  stv<9>(eqB(s, pk), nBr);
+  stv<3>(eqR(s, pk), r);
+}
+
+__device__ __forceinline__ void cr_invert(const CRS& s, int k, const StepConsts& ks) {
+  const int p = cr_pos(k);
+  double Ds[6], Di[6];
+  ldv<6>(eqD(s, p), Ds);
+  if (!sym_inv_spd(Ds, Di)) report(ks, ERR_SINGULAR);
+  stv<6>(eqD(s, p), Di);
+}
+
+// Forward reduction. Precondition: every odd equation (eliminated at stride 1) already holds D⁻¹. A survivor
+// that will be eliminated at the next level inverts its own D right after its update (no one else reads a
+// survivor's D at this level), so each level needs one barrier.
 __device__ void cr_forward(const CRS& s, int t, const StepConsts& k) {
   for (int st = 1; st < SEG; st <<= 1) {
-    const int two = st << 1;
-    if ((t & (two - 1)) == st) {  // eliminated at this level: invert its D
-      double Di[6];
-      if (!sym_inv_spd(s.D + 6 * t, Di)) report(k, ERR_SINGULAR);
-#pragma unroll
-      for (int e = 0; e < 6; ++e) s.D[6 * t + e] = Di[e];
-    }
-    __syncthreads();
-    const int kq = (t == SEG - 1) ? SEG : t;  // thread 255 (never even) carries equation 256
-    if ((kq & (two - 1)) == 0) {
-      double D[9], Br[9], r[3];
-      full_from_sym(s.D + 6 * kq, D);
-#pragma unroll
-      for (int e = 0; e < 9; ++e) Br[e] = s.B[9 * kq + e];
-#pragma unroll
-      for (int e = 0; e < 3; ++e) r[e] = s.r[3 * kq + e];
-      double nBr[9] = {0, 0, 0, 0, 0, 0, 0, 0, 0};
-      if (kq >= st) {  // left neighbour i = kq - st:  α = Br_iᵀ D_i⁻¹
-        const int i = kq - st;
-        double Di[9], Bi[9], al[9], tmp[9];
-        full_from_sym(s.D + 6 * i, Di);
-#pragma unroll
-        for (int e = 0; e < 9; ++e) Bi[e] = s.B[9 * i + e];
-        mat3_mul_at(Bi, Di, al);          // α = Biᵀ Di⁻¹
-        mat3_mul(al, Bi, tmp);            // α Br_i
-#pragma unroll
-        for (int e = 0; e < 9; ++e) D[e] -= tmp[e];
-        double ri[3], ar[3];
-#pragma unroll
-        for (int e = 0; e < 3; ++e) ri[e] = s.r[3 * i + e];
-        mat3_vec(al, ri, ar);
-#pragma unroll
-        for (int e = 0; e < 3; ++e) r[e] -= ar[e];
-      }
-      if (kq < SEG) {  // right neighbour j = kq + st:  γ = Br_k D_j⁻¹
-        const int j = kq + st;
-        double Dj[9], ga[9], tmp[9], Bj[9];
-        full_from_sym(s.D + 6 * j, Dj);
-        mat3_mul(Br, Dj, ga);             // γ
-        mat3_mul_bt(ga, Br, tmp);         // γ Br_kᵀ  (= γ Bl_j)
-#pragma unroll
-        for (int e = 0; e < 9; ++e) D[e] -= tmp[e];
-        double rj[3], gr[3];
-#pragma unroll
-        for (int e = 0; e < 3; ++e) rj[e] = s.r[3 * j + e];
-        mat3_vec(ga, rj, gr);
-#pragma unroll
-        for (int e = 0; e < 3; ++e) r[e] -= gr[e];
-#pragma unroll
-        for (int e = 0; e < 9; ++e) Bj[e] = s.B[9 * j + e];
-        mat3_mul(ga, Bj, tmp);            // new Br_k = −γ Br_j
-#pragma unroll
-        for (int e = 0; e < 9; ++e) nBr[e] = -tmp[e];
-#pragma unroll
-        for (int e = 0; e < 9; ++e) s.Bl[9 * j + e] = Br[e];  // j's left coupling at this level
-      }
-      double Ds[6];
-      sym_from_full(D, Ds);
-      // symmetrise (the two updates are symmetric in exact arithmetic)
-      Ds[1] = 0.5 * (D[1] + D[3]);
-      Ds[2] = 0.5 * (D[2] + D[6]);
-      Ds[4] = 0.5 * (D[5] + D[7]);
-#pragma unroll
-      for (int e = 0; e < 6; ++e) s.D[6 * kq + e] = Ds[e];
-#pragma unroll
-      for (int e = 0; e < 9; ++e) s.B[9 * kq + e] = nBr[e];
-#pragma unroll
-      for (int e = 0; e < 3; ++e) s.r[3 * kq + e] = r[e];
+    const int ne = SEG / (2 * st);
+    for (int m = t; m <= ne; m += CT) {  // survivors k = 2st·m, m ≤ ne
+      const int kq = 2 * st * m;
+      cr_update(s, kq, st);
+      if ((m & 1) && 2 * st < SEG) cr_invert(s, kq, k);
     }
     __syncthreads();
   }
@@ -112,28 +172,32 @@ __device__ void cr_forward(const CRS& s, int t, const StepConsts& k) {
 
 // Solve the remaining 2-equation system [D0 B; Bᵀ D1][λ0; λ1] = [r0; r1] (one thread).
 __device__ void cr_solve_top(const CRS& s, const StepConsts& k) {
-  double D0i[6], D0[9], B[9], D1s[6], D1[9], r0[3], r1[3];
-#pragma unroll
-  for (int e = 0; e < 9; ++e) B[e] = s.B[e];
-#pragma unroll
-  for (int e = 0; e < 3; ++e) { r0[e] = s.r[e]; r1[e] = s.r[3 * SEG + e]; }
-  if (!sym_inv_spd(s.D, D0i)) report(k, ERR_SINGULAR);
+  const int p0 = cr_pos(0), p1 = cr_pos(SEG);
+  double D0s[6], D0i[6], D0[9], B[9], D1s[6], D1[9], r0[3], r1[3];
+  ldv<9>(eqB(s, p0), B);
+  ldv<3>(eqR(s, p0), r0);
+  ldv<3>(eqR(s, p1), r1);
+  ldv<6>(eqD(s, p0), D0s);
+  ldv<6>(eqD(s, p1), D1s);
+  if (!sym_inv_spd(D0s, D0i)) report(k, ERR_SINGULAR);
   full_from_sym(D0i, D0);
-  full_from_sym(s.D + 6 * SEG, D1);
+  full_from_sym(D1s, D1);
   double W[9], T[9];
-  mat3_mul(D0, B, W);          // D0⁻¹ B
-  mat3_mul_at(B, W, T);        // Bᵀ D0⁻¹ B
+  mat3_mul(D0, B, W);     // D0⁻¹ B
+  mat3_mul_at(B, W, T);   // Bᵀ D0⁻¹ B
 #pragma unroll
   for (int e = 0; e < 9; ++e) D1[e] -= T[e];
   double y[3], z[3];
-  mat3_vec(D0, r0, y);         // D0⁻¹ r0
-  mat3t_vec(B, y, z);          // Bᵀ D0⁻¹ r0
+  mat3_vec(D0, r0, y);
+  mat3t_vec(B, y, z);
 #pragma unroll
   for (int e = 0; e < 3; ++e) r1[e] -= z[e];
-  sym_from_full(D1, D1s);
+  D1s[0] = D1[0];
   D1s[1] = 0.5 * (D1[1] + D1[3]);
   D1s[2] = 0.5 * (D1[2] + D1[6]);
+  D1s[3] = D1[4];
   D1s[4] = 0.5 * (D1[5] + D1[7]);
+  D1s[5] = D1[8];
   double S1i[6], l1[3], l0[3], Bl1[3];
   if (!sym_inv_spd(D1s, S1i)) report(k, ERR_SINGULAR);
   sym_vec(S1i, r1, l1);
@@ -141,32 +205,32 @@ __device__ void cr_solve_top(const CRS& s, const StepConsts& k) {
 #pragma unroll
   for (int e = 0; e < 3; ++e) r0[e] -= Bl1[e];
   mat3_vec(D0, r0, l0);
-#pragma unroll
-  for (int e = 0; e < 3; ++e) { s.r[e] = l0[e]; s.r[3 * SEG + e] = l1[e]; }
+  stv<3>(eqR(s, p0), l0);
+  stv<3>(eqR(s, p1), l1);
 }
 
-// Back substitution; sR[0] and sR[256] hold λ of the end equations on entry, all λ on exit.
+// Back substitution; λ of equations 0 and 256 are in r on entry, all λ on exit.
 __device__ void cr_backward(const CRS& s, int t) {
   for (int st = SEG / 2; st >= 1; st >>= 1) {
-    const int two = st << 1;
-    if ((t & (two - 1)) == st) {
-      const int i = t;
+    const int ne = SEG / (2 * st);
+    for (int m = t; m < ne; m += CT) {
+      const int i = st * (2 * m + 1);
+      const int pi = cr_pos(i);
       double Bl[9], Br[9], Di[6], ll[3], lr[3], v[3], w[3];
-#pragma unroll
-      for (int e = 0; e < 9; ++e) { Bl[e] = s.Bl[9 * i + e]; Br[e] = s.B[9 * i + e]; }
-#pragma unroll
-      for (int e = 0; e < 6; ++e) Di[e] = s.D[6 * i + e];
-#pragma unroll
-      for (int e = 0; e < 3; ++e) { ll[e] = s.r[3 * (i - st) + e]; lr[e] = s.r[3 * (i + st) + e]; v[e] = s.r[3 * i + e]; }
-      mat3t_vec(Bl, ll, w);  // Bl_i λ_{i-s} = Br_{i-s}ᵀ λ_{i-s}
+      ldv<9>(eqBl(s, pi), Bl);
+      ldv<9>(eqB(s, pi), Br);
+      ldv<6>(eqD(s, pi), Di);
+      ldv<3>(eqR(s, cr_pos(i - st)), ll);
+      ldv<3>(eqR(s, cr_pos(i + st)), lr);
+      ldv<3>(eqR(s, pi), v);
+      mat3t_vec(Bl, ll, w);  // Bl_i λ_{i−s} = Br_{i−s}ᵀ λ_{i−s}
 #pragma unroll
       for (int e = 0; e < 3; ++e) v[e] -= w[e];
       mat3_vec(Br, lr, w);
 #pragma unroll
       for (int e = 0; e < 3; ++e) v[e] -= w[e];
       sym_vec(Di, v, w);
-#pragma unroll
-      for (int e = 0; e < 3; ++e) s.r[3 * i + e] = w[e];
+      stv<3>(eqR(s, pi), w);
     }
     __syncthreads();
   }
@@ -181,208 +245,314 @@ __device__ __forceinline__ CRS cr_smem(double* smem) {
   return s;
 }
 
+__device__ __forceinline__ void write_top(const CRS& s, Top* o) {
+  const int p0 = cr_pos(0), p1 = cr_pos(SEG);
+  ldv<6>(eqD(s, p0), o->D0);
+  ldv<6>(eqD(s, p1), o->D1);
+  ldv<9>(eqB(s, p0), o->B);
+  ldv<3>(eqR(s, p0), o->r0);
+  ldv<3>(eqR(s, p1), o->r1);
+}
+
+__device__ __forceinline__ void body_material(const ChainArgs& a, int64_t slot, Material& M, double& msc,
+                                              HinvBlk& H) {
+  const int mid = a.b.mat_id ? __ldg(a.b.mat_id + slot) : 0;
+  msc = a.b.mscale ? __ldg(a.b.mscale + slot) : 1.0;
+  M = a.b.mats[mid];
+  if (a.hinv_tab)
+    H = a.hinv_tab[mid];
+  else
+    hinv_blocks(M, msc, a.k.ih2, H);
+}
+
 // ------------------------------------------------------------------ the fused chain segment kernel
+// Persistent: each CTA loops over segments it ← blockIdx.x, += gridDim.x. While a segment is in the
+// cyclic reduction (no memory traffic), the CTA prefetches the NEXT segment's state into L2, so its
+// phase-1 loads are L2 hits (software pipeline across segments).
+// FINISH = false: first pass (fused segments solve completely; long segments REDUCE to their top);
+// FINISH = true: second pass of long segments (recompute, read the ends' λ, back-substitute, update).
+__device__ __forceinline__ void prefetch_segment(const ChainArgs& a, int it, int tid) {
+  if (it >= a.n_items) return;
+  const int g = a.seg_list ? a.seg_list[it] : it;
+  const int64_t base = (int64_t)g * SEG;
+#pragma unroll
+  for (int b = 0; b < 2; ++b) {
+    const int64_t sl = base + tid + b * CT;
+#pragma unroll
+    for (int c = 0; c < 12; ++c) {
+      l2_prefetch(a.b.q + c * a.b.ld + sl);
+      l2_prefetch(a.b.qd + c * a.b.ld + sl);
+    }
+    if (a.b.mscale) l2_prefetch(a.b.mscale + sl);
+    l2_prefetch(a.slot_info + sl);
+  }
+}
+
+#ifndef MABD_CHAIN_MINB
+#define MABD_CHAIN_MINB 4
+#endif
 template <bool FINISH>
-__global__ void __launch_bounds__(SEG) chain_kernel(ChainArgs a) {
+__global__ void __launch_bounds__(CT, MABD_CHAIN_MINB) chain_kernel(ChainArgs a) {
   extern __shared__ double smem[];
   const CRS s = cr_smem(smem);
-  const int t = threadIdx.x;
-  const int g = a.seg_list ? a.seg_list[blockIdx.x] : (int)blockIdx.x;
-  const int flags = a.seg_flags[g];
-  const bool is_long = (flags & SEG_LONG) != 0;
-  const int64_t slot = (int64_t)g * SEG + t;
-  const uint32_t info = a.slot_info[slot];
-  const uint32_t infoN = a.slot_info[slot + 1];
-  const bool has_body = slot_right(info) == SIDE_BODY;
-  const bool eq_real = slot_real(info);
-  const bool right_real = slot_real(infoN) && slot_left(infoN) == SIDE_BODY;
+  const int tid = threadIdx.x;
   const StepConsts& k = a.k;
+  if ((int)blockIdx.x < a.n_items) {  // first segment: its second body is fetched while the first is loaded
+    const int g0 = a.seg_list ? a.seg_list[blockIdx.x] : (int)blockIdx.x;
+    const int64_t s2 = (int64_t)g0 * SEG + tid + CT;
+#pragma unroll
+    for (int c = 0; c < 12; ++c) {
+      l2_prefetch(a.b.q + c * a.b.ld + s2);
+      l2_prefetch(a.b.qd + c * a.b.ld + s2);
+    }
+  }
+#ifdef MABD_EXP_CLOCK
+  long long ph_last = clock64();
+#endif
+  for (int it = blockIdx.x; it < a.n_items; it += gridDim.x) {
+    PH_MARK(7);
+    const int g = a.seg_list ? a.seg_list[it] : it;
+    const int flags = a.seg_flags[g];
+    const bool is_long = (flags & SEG_LONG) != 0;
+    const bool update = !is_long || FINISH;  // this pass writes the new state
+    const int64_t base = (int64_t)g * SEG;
 
-  double q[12], dqt[12], R[9];
-  HinvBlk H;
-  double yR[3] = {0, 0, 0}, yL[3] = {0, 0, 0};
-  double DR[6] = {0, 0, 0, 0, 0, 0}, DL[6] = {0, 0, 0, 0, 0, 0}, Bt[9] = {0, 0, 0, 0, 0, 0, 0, 0, 0};
-  double xR[3] = {0, 0, 0}, xL[3] = {0, 0, 0};
-  if (eq_real) {
-    const double* gp = a.geo + 6 * (size_t)slot_geo(info);
-    if (slot_right(info) == SIDE_BODY) {
+    // ---------------- phase 1: per body predict + joint contributions (thread tid: slots tid, tid+128)
+    // Equation t is assembled in place: sD[t] = D part of body t, sR[t] = rhs part, sB[t] = B_t; body t's
+    // contribution to equation t+1 goes to the scratch row sBl[t+1] and is added after the barrier.
+    uint32_t infos[3];
+    infos[0] = __ldg(a.slot_info + base + tid);
+    infos[1] = __ldg(a.slot_info + base + tid + 1);
+    infos[2] = __ldg(a.slot_info + base + tid + CT + 1);
+#pragma unroll 1
+    for (int b = 0; b < 2; ++b) {
+      const int t = tid + b * CT;
+      const int64_t slot = base + t;
+      const uint32_t info = b == 0 ? infos[0] : __ldg(a.slot_info + slot);
+      const uint32_t infoN = infos[1 + b];
+      const bool has_body = slot_right(info) == SIDE_BODY;
+      const bool eq_real = slot_real(info);
+      const bool right_real = slot_real(infoN) && slot_left(infoN) == SIDE_BODY;
+      const int pt = cr_pos(t);
+      const SV sd = eqD(s, pt), sr = eqR(s, pt), sb = eqB(s, pt);
+      const SV sx = eqBl(s, cr_pos(t + 1));  // scratch row: body t's contribution to equation t+1
+      {
+        const double one = eq_real ? 0.0 : 1.0;  // not a constraint: decoupled identity equation, λ = 0
+        sd[0] = one; sd[1] = 0; sd[2] = 0; sd[3] = one; sd[4] = 0; sd[5] = one;
+        double rr[3] = {0, 0, 0};
+        if (eq_real) {
+          const double* gp = a.geo + 6 * (size_t)slot_geo(info);
+          if (slot_left(info) == SIDE_WORLD)  // start anchor: +p_world
 #pragma unroll
-      for (int e = 0; e < 3; ++e) yR[e] = gp[3 + e];
-    } else {  // end anchor: the right side is a world point
+            for (int e = 0; e < 3; ++e) rr[e] = __ldg(gp + e);
+          if (slot_right(info) == SIDE_WORLD)  // end anchor: −p_world
 #pragma unroll
-      for (int e = 0; e < 3; ++e) xR[e] = gp[3 + e];
-    }
-  }
-  if (has_body) {
-    double qd[12];
-    const double* qb = a.b.q + slot;
-    const double* qdb = a.b.qd + slot;
+            for (int e = 0; e < 3; ++e) rr[e] -= __ldg(gp + 3 + e);
+        }
 #pragma unroll
-    for (int c = 0; c < 12; ++c) q[c] = __ldcs(qb + c * a.b.ld);
+        for (int e = 0; e < 3; ++e) sr[e] = rr[e];
 #pragma unroll
-    for (int c = 0; c < 12; ++c) qd[c] = __ldcs(qdb + c * a.b.ld);
-    const int mid = a.b.mat_id ? a.b.mat_id[slot] : 0;
-    const double msc = a.b.mscale ? a.b.mscale[slot] : 1.0;
-    const Material M = a.b.mats[mid];
-    if (a.hinv_tab)
-      H = a.hinv_tab[mid];
-    else
-      hinv_blocks(M, msc, k.ih2, H);
-    if (!predict_body(q, qd, M, msc, H, k.ih, k.grav, R, dqt)) report(k, ERR_NONFINITE);
-    double qt[12];
+        for (int e = 0; e < 9; ++e) sb[e] = 0.0;
 #pragma unroll
-    for (int c = 0; c < 12; ++c) qt[c] = q[c] + dqt[c];
-    double P[9], F[9];
-    if (eq_real) {  // joint to the left: body is its right side (sign −)
-      pblock(H, yR, yR, P);
-      rot_conj(R, P, F);
-      sym_from_full(F, DR);
-      point_pos(qt, yR, xR);
-    }
-    if (right_real) {  // joint to the right: body is its left side (sign +)
-      const double* gp = a.geo + 6 * (size_t)slot_geo(infoN);
+        for (int e = 0; e < 9; ++e) sx[e] = 0.0;
+      }
+      if (has_body) {
+        double q[12], R[9];
+        HinvBlk H;
+        {
+          double qd[12], dqt[12];
+          double* qdb = a.b.qd + slot;
+          const double* qb = a.b.q + slot;
 #pragma unroll
-      for (int e = 0; e < 3; ++e) yL[e] = gp[e];
-      pblock(H, yL, yL, P);
-      rot_conj(R, P, F);
-      sym_from_full(F, DL);
-      point_pos(qt, yL, xL);
-      if (eq_real) {  // B_t = −R P(ȳ_R, ȳ_L') Rᵀ  (sign −·+)
-        pblock(H, yR, yL, P);
-        rot_conj(R, P, F);
+          for (int c = 0; c < 12; ++c) q[c] = qb[c * a.b.ld];
 #pragma unroll
-        for (int e = 0; e < 9; ++e) Bt[e] = -F[e];
+          for (int c = 0; c < 12; ++c) qd[c] = qdb[c * a.b.ld];
+          Material M;
+          double msc;
+          body_material(a, slot, M, msc, H);
+          if (!predict_body(q, qd, M, msc, H, k.ih, k.grav, R, dqt)) report(k, ERR_NONFINITE);
+          if (update) {
+#pragma unroll
+            for (int c = 0; c < 12; ++c) qdb[c * a.b.ld] = dqt[c];  // park δq̃ (q̇ⁿ is dead from here on)
+#pragma unroll
+            for (int c = 0; c < 9; ++c) a.b.rs[c * a.b.ld + slot] = R[c];  // park R (L2 scratch)
+          }
+#pragma unroll
+          for (int c = 0; c < 12; ++c) q[c] += dqt[c];  // q̃
+        }
+        double P[9], F[6], yR[3], yL[3], x[3];
+        if (eq_real) {  // joint to the left: this body is its right side (sign −)
+          const double* gp = a.geo + 6 * (size_t)slot_geo(info);
+#pragma unroll
+          for (int e = 0; e < 3; ++e) yR[e] = __ldg(gp + 3 + e);
+          pblock(H, yR, yR, P);
+          rot_conj_sym(R, P, F);
+#pragma unroll
+          for (int e = 0; e < 6; ++e) sd[e] = F[e];
+          point_pos(q, yR, x);
+#pragma unroll
+          for (int e = 0; e < 3; ++e) sr[e] -= x[e];
+        }
+        if (right_real) {  // joint to the right: this body is its left side (sign +)
+          const double* gp = a.geo + 6 * (size_t)slot_geo(infoN);
+#pragma unroll
+          for (int e = 0; e < 3; ++e) yL[e] = __ldg(gp + e);
+          pblock(H, yL, yL, P);
+          rot_conj_sym(R, P, F);
+#pragma unroll
+          for (int e = 0; e < 6; ++e) sx[e] = F[e];
+          point_pos(q, yL, x);
+#pragma unroll
+          for (int e = 0; e < 3; ++e) sx[6 + e] = x[e];
+          if (eq_real) {  // B_t = −R P(ȳ_R, ȳ_L') Rᵀ  (signs −·+)
+            double Fb[9];
+            pblock(H, yR, yL, P);
+            rot_conj(R, P, Fb);
+#pragma unroll
+            for (int e = 0; e < 9; ++e) sb[e] = -Fb[e];
+          }
+        }
       }
     }
-  }
-  // exchange the right-joint contributions through shared memory (sBl reused as [NEQ][9] scratch)
-  {
-    double* x = s.Bl + 9 * (t + 1);
+    PH_MARK(0);
+    __syncthreads();
+    PH_MARK(1);
+    // add the left neighbours' contributions (equation 0's left body lies in the previous segment: its part
+    // of the interface equation is added by that segment's REDUCE output)
+#pragma unroll 1
+    for (int b = 0; b < 2; ++b) {
+      const int t = tid + b * CT;
+      const uint32_t info = b == 0 ? infos[0] : __ldg(a.slot_info + base + t);
+      if (t > 0 && slot_real(info) && slot_left(info) == SIDE_BODY) {
+        const int pt = cr_pos(t);
+        const SV x = eqBl(s, pt), d = eqD(s, pt), r = eqR(s, pt);
 #pragma unroll
-    for (int e = 0; e < 6; ++e) x[e] = DL[e];
+        for (int e = 0; e < 6; ++e) d[e] += x[e];
 #pragma unroll
-    for (int e = 0; e < 3; ++e) x[6 + e] = xL[e];
-    if (t == 0) {
-#pragma unroll
-      for (int e = 0; e < 9; ++e) s.Bl[e] = 0.0;
-    }
-  }
-  __syncthreads();
-  {
-    double D[6], r[3];
-    if (eq_real) {
-      const double* x = s.Bl + 9 * t;
-      const uint32_t ls = slot_left(info);
-      double left[3] = {0, 0, 0};
-      if (ls == SIDE_BODY) {
-#pragma unroll
-        for (int e = 0; e < 3; ++e) left[e] = x[6 + e];
-#pragma unroll
-        for (int e = 0; e < 6; ++e) D[e] = DR[e] + x[e];
-      } else {  // world on the left (start anchor): fixed world point
-        const double* gp = a.geo + 6 * (size_t)slot_geo(info);
-#pragma unroll
-        for (int e = 0; e < 3; ++e) left[e] = gp[e];
-#pragma unroll
-        for (int e = 0; e < 6; ++e) D[e] = DR[e];
+        for (int e = 0; e < 3; ++e) r[e] += x[6 + e];
       }
-#pragma unroll
-      for (int e = 0; e < 3; ++e) r[e] = left[e] - xR[e];  // r = C(q̃) (footnote P:459)
-    } else {  // padding / absent slot: decoupled identity equation, λ = 0
-      D[0] = 1; D[1] = 0; D[2] = 0; D[3] = 1; D[4] = 0; D[5] = 1;
-      r[0] = r[1] = r[2] = 0;
+      if (t & 1) cr_invert(s, t, k);  // eliminated at stride 1
     }
-    double D256[6], r256[3];
-    if (t == SEG - 1) {
-      if (flags & SEG_RIGHT_IFACE) {
-        const double* x = s.Bl + 9 * SEG;
+    if (tid == CT - 1) {  // equation 256: next segment's first slot (partial) or padding
+      const bool real = (flags & SEG_RIGHT_IFACE) != 0;
+      const SV x = eqBl(s, SEG);
+      double D[6], r[3];
 #pragma unroll
-        for (int e = 0; e < 6; ++e) D256[e] = x[e];
+      for (int e = 0; e < 6; ++e) D[e] = real ? x[e] : ((e == 0 || e == 3 || e == 5) ? 1.0 : 0.0);
 #pragma unroll
-        for (int e = 0; e < 3; ++e) r256[e] = x[6 + e];
-      } else {
-        D256[0] = 1; D256[1] = 0; D256[2] = 0; D256[3] = 1; D256[4] = 0; D256[5] = 1;
-        r256[0] = r256[1] = r256[2] = 0;
-      }
+      for (int e = 0; e < 3; ++e) r[e] = real ? x[6 + e] : 0.0;
+      const double Z[9] = {0, 0, 0, 0, 0, 0, 0, 0, 0};
+      stv<6>(eqD(s, SEG), D);
+      stv<9>(eqB(s, SEG), Z);
+      stv<3>(eqR(s, SEG), r);
     }
-    __syncthreads();  // all reads of the scratch done before the CR arrays are written
-#pragma unroll
-    for (int e = 0; e < 6; ++e) s.D[6 * t + e] = D[e];
-#pragma unroll
-    for (int e = 0; e < 9; ++e) s.B[9 * t + e] = Bt[e];
-#pragma unroll
-    for (int e = 0; e < 3; ++e) s.r[3 * t + e] = r[e];
-    if (t == SEG - 1) {
-#pragma unroll
-      for (int e = 0; e < 6; ++e) s.D[6 * SEG + e] = D256[e];
-#pragma unroll
-      for (int e = 0; e < 9; ++e) s.B[9 * SEG + e] = 0.0;
-#pragma unroll
-      for (int e = 0; e < 3; ++e) s.r[3 * SEG + e] = r256[e];
-    }
-  }
-  __syncthreads();
-  cr_forward(s, t, k);
+    __syncthreads();
 
-  if (!is_long) {
-    if (t == 0) cr_solve_top(s, k);
-  } else if (!FINISH) {
-    if (t == 0) {
-      Top* o = a.top_out + a.seg_red[g];
-#pragma unroll
-      for (int e = 0; e < 6; ++e) { o->D0[e] = s.D[e]; o->D1[e] = s.D[6 * SEG + e]; }
-#pragma unroll
-      for (int e = 0; e < 9; ++e) o->B[e] = s.B[e];
-#pragma unroll
-      for (int e = 0; e < 3; ++e) { o->r0[e] = s.r[e]; o->r1[e] = s.r[3 * SEG + e]; }
-    }
-    return;
-  } else {
-    if (t == 0) {
+    // ---------------- phase 2: block cyclic reduction (the next segment's state streams into L2 meanwhile)
+    PH_MARK(2);
+    prefetch_segment(a, it + gridDim.x, tid);
+#ifndef MABD_EXP_SKIP_CR
+    cr_forward(s, tid, k);
+#endif
+    PH_MARK(3);
+    if (!is_long) {
+      if (tid == 0) cr_solve_top(s, k);
+    } else if (!FINISH) {
+      if (tid == 0) write_top(s, a.top_out + a.seg_red[g]);
+      __syncthreads();
+      continue;
+    } else if (tid == 0) {
       const int u = a.seg_red[g];
 #pragma unroll
       for (int e = 0; e < 3; ++e) {
-        s.r[e] = a.lam_in[3 * u + e];
-        s.r[3 * SEG + e] = (flags & SEG_RIGHT_IFACE) ? a.lam_in[3 * (u + 1) + e] : 0.0;
+        eqR(s, cr_pos(0))[e] = a.lam_in[3 * u + e];
+        eqR(s, SEG)[e] = (flags & SEG_RIGHT_IFACE) ? a.lam_in[3 * (u + 1) + e] : 0.0;
       }
     }
-  }
-  __syncthreads();
-  cr_backward(s, t);
+    __syncthreads();
+    PH_MARK(4);
+#ifndef MABD_EXP_SKIP_CR
+    cr_backward(s, tid);
+#endif
+    PH_MARK(5);
+#ifdef MABD_EXP_SKIP_P3
+    __syncthreads();
+    continue;
+#endif
 
-  if (has_body) {  // stage 4: qⁿ⁺¹ = q̃ − diag₄(R) H̄⁻¹ Σ ±Γ(ȳ)ᵀ Rᵀλ
-    double gq[12];
+    // ---------------- phase 3: qⁿ⁺¹ = q̃ − diag₄(R) H̄⁻¹ Σ ±Γ(ȳ)ᵀ Rᵀλ
+#pragma unroll 1
+    for (int b = 0; b < 2; ++b) {
+      const int t = tid + b * CT;
+      const int64_t slot = base + t;
+      const uint32_t info = b == 0 ? infos[0] : __ldg(a.slot_info + slot);
+      const uint32_t infoN = infos[1 + b];
+      double* qb = a.b.q + slot;
+      double* qdb = a.b.qd + slot;
+      // issue every load of this body first: R (parked), qⁿ, δq̃ (parked) — all L2 hits
+      double R[9], q[12], dqt[12];
+      const double* rp = a.b.rs + slot;
 #pragma unroll
-    for (int c = 0; c < 12; ++c) gq[c] = 0.0;
-    double w[3], lam[3];
-    if (eq_real) {
+      for (int c = 0; c < 9; ++c) R[c] = __ldcg(rp + c * a.b.ld);
 #pragma unroll
-      for (int e = 0; e < 3; ++e) lam[e] = s.r[3 * t + e];
-      mat3t_vec(R, lam, w);
-      add_point_force(gq, yR, w, -1.0);
-    }
-    if (right_real) {
+      for (int c = 0; c < 12; ++c) q[c] = __ldcs(qb + c * a.b.ld);
 #pragma unroll
-      for (int e = 0; e < 3; ++e) lam[e] = s.r[3 * (t + 1) + e];
-      mat3t_vec(R, lam, w);
-      add_point_force(gq, yL, w, 1.0);
-    }
-    double u[12];
-    hinv_apply(H, gq, u);
-    double* qb = a.b.q + slot;
-    double* qdb = a.b.qd + slot;
+      for (int c = 0; c < 12; ++c) dqt[c] = __ldcs(qdb + c * a.b.ld);
+      // all lanes have their R: discard the scratch lines (no DRAM write-back); the warp covers 32
+      // consecutive, 256-B aligned slots = two 128-B lines per row
+      __syncwarp();
+      if ((threadIdx.x & 15) == 0) {
 #pragma unroll
-    for (int kb = 0; kb < 4; ++kb) {
-      double c3[3];
-      mat3_vec(R, u + 3 * kb, c3);
+        for (int c = 0; c < 9; ++c) l2_discard128(rp + c * a.b.ld);
+      }
+      if (slot_right(info) != SIDE_BODY) continue;
+      const bool eq_real = slot_real(info);
+      const bool right_real = slot_real(infoN) && slot_left(infoN) == SIDE_BODY;
+      double gq[12];
 #pragma unroll
-      for (int e = 0; e < 3; ++e) {
-        const int c = 3 * kb + e;
-        const double dq = dqt[c] - c3[e];
-        __stcs(qb + c * a.b.ld, q[c] + dq);
-        __stcs(qdb + c * a.b.ld, dq * k.ih);
+      for (int c = 0; c < 12; ++c) gq[c] = 0.0;
+      double w[3], lam[3], y[3];
+      if (eq_real) {
+        const double* gp = a.geo + 6 * (size_t)slot_geo(info);
+#pragma unroll
+        for (int e = 0; e < 3; ++e) {
+          y[e] = __ldg(gp + 3 + e);
+          lam[e] = eqR(s, cr_pos(t))[e];
+        }
+        mat3t_vec(R, lam, w);
+        add_point_force(gq, y, w, -1.0);
+      }
+      if (right_real) {
+        const double* gp = a.geo + 6 * (size_t)slot_geo(infoN);
+#pragma unroll
+        for (int e = 0; e < 3; ++e) {
+          y[e] = __ldg(gp + e);
+          lam[e] = eqR(s, cr_pos(t + 1))[e];
+        }
+        mat3t_vec(R, lam, w);
+        add_point_force(gq, y, w, 1.0);
+      }
+      Material M;
+      double msc;
+      HinvBlk H;
+      body_material(a, slot, M, msc, H);
+      double u[12];
+      hinv_apply(H, gq, u);
+#pragma unroll
+      for (int kb = 0; kb < 4; ++kb) {
+        double c3[3];
+        mat3_vec(R, u + 3 * kb, c3);
+#pragma unroll
+        for (int e = 0; e < 3; ++e) {
+          const int c = 3 * kb + e;
+          const double dq = dqt[c] - c3[e];  // δq = δq̃ − correction
+          __stcs(qb + c * a.b.ld, q[c] + dq);
+          __stcs(qdb + c * a.b.ld, dq * k.ih);
+        }
       }
     }
+    PH_MARK(6);
+    __syncthreads();  // shared memory is reused by the next segment
   }
 }
 
@@ -391,14 +561,15 @@ __global__ void __launch_bounds__(SEG) chain_kernel(ChainArgs a) {
 //   D_u = top[u].D0 + (left(u) ? top[u−1].D1 : 0),  B_u = top[u].B,  r_u likewise.
 // A window w of 256 unknowns is one CTA; its equation 256 is the first unknown of window w+1 (partial:
 // D = 0, r = 0; its coupling from unknown 256w+255 is B_{256w+255}), or padding.
-__global__ void __launch_bounds__(SEG) btd_kernel(BtdArgs a) {
+__global__ void __launch_bounds__(CT) btd_kernel(BtdArgs a) {
   extern __shared__ double smem[];
   const CRS s = cr_smem(smem);
-  const int t = threadIdx.x;
+  const int tid = threadIdx.x;
   const int64_t w = blockIdx.x;
-  const int64_t u = w * SEG + t;
   const int64_t nu = a.n_u;
-  {
+  for (int b = 0; b < 2; ++b) {
+    const int t = tid + b * CT;
+    const int64_t u = w * SEG + t;
     double D[6] = {1, 0, 0, 1, 0, 1}, B[9] = {0, 0, 0, 0, 0, 0, 0, 0, 0}, r[3] = {0, 0, 0};
     if (u < nu) {
       const Top& T = a.top_in[u];
@@ -410,82 +581,85 @@ __global__ void __launch_bounds__(SEG) btd_kernel(BtdArgs a) {
 #pragma unroll
       for (int e = 0; e < 9; ++e) B[e] = T.B[e];
     }
-#pragma unroll
-    for (int e = 0; e < 6; ++e) s.D[6 * t + e] = D[e];
-#pragma unroll
-    for (int e = 0; e < 9; ++e) s.B[9 * t + e] = B[e];
-#pragma unroll
-    for (int e = 0; e < 3; ++e) s.r[3 * t + e] = r[e];
-    if (t == SEG - 1) {
-      const bool real_next = (w + 1) * SEG < nu;
-      const double Dn[6] = {real_next ? 0.0 : 1.0, 0, 0, real_next ? 0.0 : 1.0, 0, real_next ? 0.0 : 1.0};
-#pragma unroll
-      for (int e = 0; e < 6; ++e) s.D[6 * SEG + e] = Dn[e];
-#pragma unroll
-      for (int e = 0; e < 9; ++e) s.B[9 * SEG + e] = 0.0;
-#pragma unroll
-      for (int e = 0; e < 3; ++e) s.r[3 * SEG + e] = 0.0;
-    }
+    const int pt = cr_pos(t);
+    stv<6>(eqD(s, pt), D);
+    stv<9>(eqB(s, pt), B);
+    stv<3>(eqR(s, pt), r);
+    if (t & 1) cr_invert(s, t, a.k);  // eliminated at stride 1
+  }
+  if (tid == CT - 1) {
+    const bool real_next = (w + 1) * SEG < nu;
+    const double dv = real_next ? 0.0 : 1.0;
+    const double Dn[6] = {dv, 0, 0, dv, 0, dv};
+    const double Z[9] = {0, 0, 0, 0, 0, 0, 0, 0, 0};
+    stv<6>(eqD(s, SEG), Dn);
+    stv<9>(eqB(s, SEG), Z);
+    stv<3>(eqR(s, SEG), Z);
   }
   __syncthreads();
-  cr_forward(s, t, a.k);
+  cr_forward(s, tid, a.k);
   if (a.mode == BTD_REDUCE) {
-    if (t == 0) {
-      Top* o = a.top_out + w;
-#pragma unroll
-      for (int e = 0; e < 6; ++e) { o->D0[e] = s.D[e]; o->D1[e] = s.D[6 * SEG + e]; }
-#pragma unroll
-      for (int e = 0; e < 9; ++e) o->B[e] = s.B[e];
-#pragma unroll
-      for (int e = 0; e < 3; ++e) { o->r0[e] = s.r[e]; o->r1[e] = s.r[3 * SEG + e]; }
-    }
+    if (tid == 0) write_top(s, a.top_out + w);
     return;
   }
   if (a.mode == BTD_FUSED) {
-    if (t == 0) cr_solve_top(s, a.k);
-  } else {
-    if (t == 0) {
-      const bool real_next = (w + 1) * SEG < nu;
+    if (tid == 0) cr_solve_top(s, a.k);
+  } else if (tid == 0) {
+    const bool real_next = (w + 1) * SEG < nu;
 #pragma unroll
-      for (int e = 0; e < 3; ++e) {
-        s.r[e] = a.lam_in[3 * w + e];
-        s.r[3 * SEG + e] = real_next ? a.lam_in[3 * (w + 1) + e] : 0.0;
-      }
+    for (int e = 0; e < 3; ++e) {
+      eqR(s, cr_pos(0))[e] = a.lam_in[3 * w + e];
+      eqR(s, SEG)[e] = real_next ? a.lam_in[3 * (w + 1) + e] : 0.0;
     }
   }
   __syncthreads();
-  cr_backward(s, t);
-  if (u < nu) {
+  cr_backward(s, tid);
+  for (int b = 0; b < 2; ++b) {
+    const int t = tid + b * CT;
+    const int64_t u = w * SEG + t;
+    if (u < nu) {
 #pragma unroll
-    for (int e = 0; e < 3; ++e) a.lam_out[3 * u + e] = s.r[3 * t + e];
+      for (int e = 0; e < 3; ++e) a.lam_out[3 * u + e] = eqR(s, cr_pos(t))[e];
+    }
   }
 }
 
 size_t cr_smem_bytes() { return sizeof(double) * NEQ * (6 + 9 + 9 + 3); }
 
-cudaError_t launch_chain(const ChainArgs& a, int nblocks, bool finish, cudaStream_t st) {
-  if (nblocks <= 0) return cudaSuccess;
+static int g_num_sms = 0;
+
+cudaError_t launch_chain(const ChainArgs& a0, int nitems, bool finish, cudaStream_t st) {
+  if (nitems <= 0) return cudaSuccess;
+  ChainArgs a = a0;
+  a.n_items = nitems;
   const size_t sm = cr_smem_bytes();
+  const int grid = std::min(nitems, MABD_CHAIN_MINB * std::max(g_num_sms, 1));
   if (finish)
-    chain_kernel<true><<<nblocks, SEG, sm, st>>>(a);
+    chain_kernel<true><<<grid, CT, sm, st>>>(a);
   else
-    chain_kernel<false><<<nblocks, SEG, sm, st>>>(a);
+    chain_kernel<false><<<grid, CT, sm, st>>>(a);
   return cudaGetLastError();
 }
 
 cudaError_t launch_btd(const BtdArgs& a, int nblocks, cudaStream_t st) {
   if (nblocks <= 0) return cudaSuccess;
-  btd_kernel<<<nblocks, SEG, cr_smem_bytes(), st>>>(a);
+  btd_kernel<<<nblocks, CT, cr_smem_bytes(), st>>>(a);
   return cudaGetLastError();
 }
 
 cudaError_t chain_kernels_init() {
   const int sm = (int)cr_smem_bytes();
-  cudaError_t e = cudaFuncSetAttribute(chain_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, sm);
-  if (e != cudaSuccess) return e;
-  e = cudaFuncSetAttribute(chain_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, sm);
-  if (e != cudaSuccess) return e;
-  return cudaFuncSetAttribute(btd_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, sm);
+  cudaError_t e;
+  int dev = 0;
+  if ((e = cudaGetDevice(&dev))) return e;
+  if ((e = cudaDeviceGetAttribute(&g_num_sms, cudaDevAttrMultiProcessorCount, dev))) return e;
+  if ((e = cudaFuncSetAttribute(chain_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, sm))) return e;
+  if ((e = cudaFuncSetAttribute(chain_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, sm))) return e;
+  if ((e = cudaFuncSetAttribute(btd_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, sm))) return e;
+  // favour shared memory in the unified L1/shared carve-out so that 4 segment CTAs fit per SM
+  cudaFuncSetAttribute(chain_kernel<true>, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
+  cudaFuncSetAttribute(chain_kernel<false>, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
+  return cudaSuccess;
 }
 
 // prefactor: per-material closed-form H̄⁻¹ ("pre-factorized")
@@ -500,7 +674,7 @@ cudaError_t launch_hinv_table(const Material* mats, int nm, double ih2, HinvBlk*
   return cudaGetLastError();
 }
 
-// state gather / scatter between the caller's AoS order and the internal SoA slots
+// state gather / scatter between the caller's AoS order and the internal SoA positions
 __global__ void gather_state_kernel(const double* q, const double* qd, int64_t ld, const int64_t* perm, int64_t n,
                                     double* qo, double* qdo) {
   const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;

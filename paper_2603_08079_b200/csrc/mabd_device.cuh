@@ -55,6 +55,17 @@ __device__ __forceinline__ void sym_vec(const double* S, const double* x, double
   y[2] = S[2] * x[0] + S[4] * x[1] + S[5] * x[2];
 }
 
+// 1/x: hardware approximation (MUFU.RCP64H, ~23 bits) refined by two Newton steps (e → e²) to full fp64
+// precision (≤ 1 ulp; not IEEE-rounded, which the parity tolerance of 1e-9 does not need).
+__device__ __forceinline__ double fast_rcp(double x) {
+  double r;
+  asm("rcp.approx.ftz.f64 %0, %1;" : "=d"(r) : "d"(x));
+  double e = fma(-x, r, 1.0);
+  r = fma(r, e, r);
+  e = fma(-x, r, 1.0);
+  return fma(r, e, r);
+}
+
 // Inverse of an SPD 3×3 (packed sym) by its adjugate; returns false if a leading minor is ≤ 0
 // (the dual matrix must be SPD: a failure means redundant joints, MABD_ESINGULAR).
 __device__ __forceinline__ bool sym_inv_spd(const double* S, double* Si) {
@@ -63,7 +74,7 @@ __device__ __forceinline__ bool sym_inv_spd(const double* S, double* Si) {
   const double det = a * A00 + b * A01 + c * A02;
   const double m2 = a * d - b * b;
   const bool ok = (a > 0.0) && (m2 > 0.0) && (det > 0.0) && isfinite(det);
-  const double id = 1.0 / det;
+  const double id = fast_rcp(det);
   Si[0] = A00 * id;
   Si[1] = A01 * id;
   Si[2] = A02 * id;
@@ -74,9 +85,21 @@ __device__ __forceinline__ bool sym_inv_spd(const double* S, double* Si) {
 }
 
 // ------------------------------------------------------------------ polar decomposition
-// R = A (AᵀA)^{-1/2}. Newton–Schulz X ← X(I − ½(XᵀX − I)) from X₀ = A (quadratic; reading A5),
-// preceded by determinant-scaled Newton X ← ½(ζX + ζ⁻¹X⁻ᵀ) while ‖XᵀX − I‖_max > 0.3.
+// R = A (AᵀA)^{-1/2}. With E = XᵀX − I, X ← X·p(E), p the degree-6 truncation of the series of (I+E)^{-1/2}
+// (7th-order convergence: ‖E_new‖ ≈ 0.42‖E‖⁷, one step from ‖E‖ ≤ 1e-2 reaches ~1e-15; reading A5),
+// preceded by determinant-scaled Newton steps X ← ½(ζX + ζ⁻¹X⁻ᵀ) while ‖E‖_F > 0.3.
 // A and R are row-major 3×3. Returns false for det A ≤ 1e-9 or non-finite input.
+
+// C = S T for symmetric commuting S, T (packed sym): the product is symmetric, 6 entries.
+__device__ __forceinline__ void symsym(const double* S, const double* T, double* C) {
+  C[0] = S[0] * T[0] + S[1] * T[1] + S[2] * T[2];
+  C[1] = S[0] * T[1] + S[1] * T[3] + S[2] * T[4];
+  C[2] = S[0] * T[2] + S[1] * T[4] + S[2] * T[5];
+  C[3] = S[1] * T[1] + S[3] * T[3] + S[4] * T[4];
+  C[4] = S[1] * T[2] + S[3] * T[4] + S[4] * T[5];
+  C[5] = S[2] * T[2] + S[4] * T[4] + S[5] * T[5];
+}
+
 __device__ __forceinline__ bool polar_rotation(const double* A, double* R) {
   const double detA = A[0] * (A[4] * A[8] - A[5] * A[7]) - A[1] * (A[3] * A[8] - A[5] * A[6]) +
                       A[2] * (A[3] * A[7] - A[4] * A[6]);
@@ -85,38 +108,56 @@ __device__ __forceinline__ bool polar_rotation(const double* A, double* R) {
     for (int i = 0; i < 9; ++i) R[i] = (i % 4 == 0) ? 1.0 : 0.0;
     return false;
   }
-  double X[9];
 #pragma unroll
-  for (int i = 0; i < 9; ++i) X[i] = A[i];
-  for (int it = 0; it < 60; ++it) {
-    double E[9];
-    mat3_mul_at(X, X, E);  // XᵀX
-    E[0] -= 1.0; E[4] -= 1.0; E[8] -= 1.0;
-    double emax = 0.0;
-#pragma unroll
-    for (int i = 0; i < 9; ++i) emax = fmax(emax, fabs(E[i]));
-    if (emax > 0.3) {
-      // scaled Newton step (far from orthogonal)
-      const double d = X[0] * (X[4] * X[8] - X[5] * X[7]) - X[1] * (X[3] * X[8] - X[5] * X[6]) +
-                       X[2] * (X[3] * X[7] - X[4] * X[6]);
+  for (int i = 0; i < 9; ++i) R[i] = A[i];
+  for (int it = 0; it < 64; ++it) {
+    // E = XᵀX − I (packed sym)
+    double E[6];
+    E[0] = R[0] * R[0] + R[3] * R[3] + R[6] * R[6] - 1.0;
+    E[1] = R[0] * R[1] + R[3] * R[4] + R[6] * R[7];
+    E[2] = R[0] * R[2] + R[3] * R[5] + R[6] * R[8];
+    E[3] = R[1] * R[1] + R[4] * R[4] + R[7] * R[7] - 1.0;
+    E[4] = R[1] * R[2] + R[4] * R[5] + R[7] * R[8];
+    E[5] = R[2] * R[2] + R[5] * R[5] + R[8] * R[8] - 1.0;
+    const double e2 = E[0] * E[0] + E[3] * E[3] + E[5] * E[5] + 2.0 * (E[1] * E[1] + E[2] * E[2] + E[4] * E[4]);
+    if (e2 > 0.09) {  // scaled Newton step, far from orthogonal
+      const double d = R[0] * (R[4] * R[8] - R[5] * R[7]) - R[1] * (R[3] * R[8] - R[5] * R[6]) +
+                       R[2] * (R[3] * R[7] - R[4] * R[6]);
       const double z = cbrt(1.0 / d);
       const double iz = 1.0 / (z * d);  // X⁻ᵀ = cof(X)/det
       double C[9];
-      C[0] = X[4] * X[8] - X[5] * X[7]; C[1] = X[5] * X[6] - X[3] * X[8]; C[2] = X[3] * X[7] - X[4] * X[6];
-      C[3] = X[2] * X[7] - X[1] * X[8]; C[4] = X[0] * X[8] - X[2] * X[6]; C[5] = X[1] * X[6] - X[0] * X[7];
-      C[6] = X[1] * X[5] - X[2] * X[4]; C[7] = X[2] * X[3] - X[0] * X[5]; C[8] = X[0] * X[4] - X[1] * X[3];
+      C[0] = R[4] * R[8] - R[5] * R[7]; C[1] = R[5] * R[6] - R[3] * R[8]; C[2] = R[3] * R[7] - R[4] * R[6];
+      C[3] = R[2] * R[7] - R[1] * R[8]; C[4] = R[0] * R[8] - R[2] * R[6]; C[5] = R[1] * R[6] - R[0] * R[7];
+      C[6] = R[1] * R[5] - R[2] * R[4]; C[7] = R[2] * R[3] - R[0] * R[5]; C[8] = R[0] * R[4] - R[1] * R[3];
 #pragma unroll
-      for (int i = 0; i < 9; ++i) X[i] = 0.5 * (z * X[i] + iz * C[i]);
+      for (int i = 0; i < 9; ++i) R[i] = 0.5 * (z * R[i] + iz * C[i]);
       continue;
     }
-    double XE[9];
-    mat3_mul(X, E, XE);
+    // p(E) − I by Horner: E(c1 + E(c2 + E(c3 + E(c4 + E(c5 + c6 E))))), c_k the series of (1+x)^{-1/2}
+    double T[6], U[6];
 #pragma unroll
-    for (int i = 0; i < 9; ++i) X[i] -= 0.5 * XE[i];
-    if (emax < 1e-8) break;  // next error ≈ ¾·emax² < 1e-16
+    for (int i = 0; i < 6; ++i) T[i] = (231.0 / 1024.0) * E[i];
+    T[0] -= 63.0 / 256.0; T[3] -= 63.0 / 256.0; T[5] -= 63.0 / 256.0;
+    symsym(E, T, U);
+    U[0] += 35.0 / 128.0; U[3] += 35.0 / 128.0; U[5] += 35.0 / 128.0;
+    symsym(E, U, T);
+    T[0] -= 5.0 / 16.0; T[3] -= 5.0 / 16.0; T[5] -= 5.0 / 16.0;
+    symsym(E, T, U);
+    U[0] += 3.0 / 8.0; U[3] += 3.0 / 8.0; U[5] += 3.0 / 8.0;
+    symsym(E, U, T);
+    T[0] -= 0.5; T[3] -= 0.5; T[5] -= 0.5;
+    symsym(E, T, U);  // p − I
+    double X[9];
+#pragma unroll
+    for (int i = 0; i < 9; ++i) X[i] = R[i];
+#pragma unroll
+    for (int r = 0; r < 3; ++r) {
+      R[3 * r + 0] = X[3 * r] + X[3 * r] * U[0] + X[3 * r + 1] * U[1] + X[3 * r + 2] * U[2];
+      R[3 * r + 1] = X[3 * r + 1] + X[3 * r] * U[1] + X[3 * r + 1] * U[3] + X[3 * r + 2] * U[4];
+      R[3 * r + 2] = X[3 * r + 2] + X[3 * r] * U[2] + X[3 * r + 1] * U[4] + X[3 * r + 2] * U[5];
+    }
+    if (e2 < 1e-4) break;  // ‖E_new‖ ≲ 0.42‖E‖⁷ < 5e-15
   }
-#pragma unroll
-  for (int i = 0; i < 9; ++i) R[i] = X[i];
   return true;
 }
 
@@ -134,12 +175,12 @@ __device__ __forceinline__ void hinv_blocks(const Material& M, double mscale, do
 #pragma unroll
   for (int k = 0; k < 3; ++k) {
     const double x = ac[k][0] + Vmu, z = ac[k][1] + Vmu, y = Vmu;
-    const double id = 1.0 / (x * z - y * y);
+    const double id = fast_rcp(x * z - y * y);
     H.pr[k][0] = z * id;
     H.pr[k][1] = -y * id;
     H.pr[k][2] = x * id;
   }
-  H.tinv = 1.0 / (M.m * mscale * ih2);
+  H.tinv = fast_rcp(M.m * mscale * ih2);
 }
 
 // out = H̄⁻¹ v (12-vectors in q layout)
@@ -194,6 +235,18 @@ __device__ __forceinline__ void pblock(const HinvBlk& H, const double* y, const 
     }
 }
 
+// R P Rᵀ for symmetric P, packed sym out
+__device__ __forceinline__ void rot_conj_sym(const double* R, const double* P, double* out) {
+  double T[9];
+  mat3_mul(R, P, T);
+  out[0] = T[0] * R[0] + T[1] * R[1] + T[2] * R[2];
+  out[1] = T[0] * R[3] + T[1] * R[4] + T[2] * R[5];
+  out[2] = T[0] * R[6] + T[1] * R[7] + T[2] * R[8];
+  out[3] = T[3] * R[3] + T[4] * R[4] + T[5] * R[5];
+  out[4] = T[3] * R[6] + T[4] * R[7] + T[5] * R[8];
+  out[5] = T[6] * R[6] + T[7] * R[7] + T[8] * R[8];
+}
+
 // R P Rᵀ (full 3×3 out)
 __device__ __forceinline__ void rot_conj(const double* R, const double* P, double* out) {
   double T[9];
@@ -223,20 +276,24 @@ __device__ __forceinline__ bool predict_body(const double* q, const double* qd, 
   for (int r = 0; r < 3; ++r)
 #pragma unroll
     for (int c = 0; c < 3; ++c) Pi[3 * r + c] = M.mu * (F[3 * r + c] + F[3 * c + r]) + (r == c ? (M.lam * tr - 2.0 * M.mu) : 0.0);
-  double RPi[9];
-  mat3_mul(R, Pi, RPi);
-  // f_A in q layout, then rotate each 3-block by Rᵀ
+  // w = diag₄(Rᵀ) f_A: the A-blocks are Rᵀ(m_c/h · q̇_c) − V Π[:,c] (Rᵀ R Π = Π), the t-block Rᵀ m (q̇_t/h + g)
   const double ma[4] = {M.a0 * mscale * ih, M.a1 * mscale * ih, M.a2 * mscale * ih, M.m * mscale};
-  double f[12];
-#pragma unroll
-  for (int c = 0; c < 3; ++c)
-#pragma unroll
-    for (int r = 0; r < 3; ++r) f[3 * c + r] = ma[c] * qd[3 * c + r] - M.V * RPi[3 * r + c];
-#pragma unroll
-  for (int r = 0; r < 3; ++r) f[9 + r] = ma[3] * (qd[9 + r] * ih + grav[r]);
   double w[12], u[12];
 #pragma unroll
-  for (int k = 0; k < 4; ++k) mat3t_vec(R, f + 3 * k, w + 3 * k);
+  for (int c = 0; c < 3; ++c) {
+    double v[3];
+    mat3t_vec(R, qd + 3 * c, v);
+#pragma unroll
+    for (int r = 0; r < 3; ++r) w[3 * c + r] = ma[c] * v[r] - M.V * Pi[3 * r + c];
+  }
+  {
+    double ft[3], v[3];
+#pragma unroll
+    for (int r = 0; r < 3; ++r) ft[r] = ma[3] * (qd[9 + r] * ih + grav[r]);
+    mat3t_vec(R, ft, v);
+#pragma unroll
+    for (int r = 0; r < 3; ++r) w[9 + r] = v[r];
+  }
   hinv_apply(H, w, u);
 #pragma unroll
   for (int k = 0; k < 4; ++k) mat3_vec(R, u + 3 * k, dqt + 3 * k);

@@ -29,7 +29,8 @@ __host__ __device__ inline uint32_t slot_geo(uint32_t s) { return s >> 4; }
 __host__ __device__ inline bool slot_real(uint32_t s) { return slot_left(s) != SIDE_NONE && slot_right(s) != SIDE_NONE; }
 __host__ __device__ inline uint32_t slot_pack(uint32_t l, uint32_t r, uint32_t g) { return l | (r << 2) | (g << 4); }
 
-constexpr int SEG = 256;        // owned slots per segment (= threads per CTA)
+constexpr int SEG = 256;        // owned slots per segment
+constexpr int CT = 128;         // threads per segment CTA (2 slots per thread)
 constexpr int NEQ = SEG + 1;    // equations per segment CR (the 257th is the next segment's first slot)
 
 // Segment flags
@@ -48,6 +49,7 @@ struct Top {
 struct BodyArrays {
   double* q;               // [12][ld]
   double* qd;              // [12][ld]
+  double* rs;              // [9][ld] scratch: R between the phases of one launch (L2 only, discarded)
   int64_t ld;
   const int32_t* mat_id;   // [ld] or null (all material 0)
   const double* mscale;    // [ld] or null (all 1)

@@ -12,7 +12,8 @@ struct ChainArgs {
   const double* geo;           // [ng][6] (ȳ_L, ȳ_R); world points for anchor sides
   const int32_t* seg_flags;    // [nseg]
   const int32_t* seg_red;      // [nseg] ordinal among long segments, −1 otherwise
-  const int32_t* seg_list;     // [nblocks] segment ids of this launch, or null for 0..nblocks−1
+  const int32_t* seg_list;     // [n_items] segment ids of this launch, or null for 0..n_items−1
+  int32_t n_items;             // segments of this launch (set by launch_chain)
   const HinvBlk* hinv_tab;     // [n_mat] prefactored H̄⁻¹ per material, or null (per-body mass scale)
   Top* top_out;                // REDUCE output, indexed by seg_red
   const double* lam_in;        // FINISH input: level-2 λ [n_long][3]

@@ -363,6 +363,7 @@ mabd_status build_plan(const mabd_bodies* B, const mabd_joints* J, const mabd_op
   Plan::Off& f = p->off;
   f.q = take(sizeof(double) * 12 * ld);
   f.qd = take(sizeof(double) * 12 * ld);
+  f.rs = take(sizeof(double) * 9 * ld);
   f.mat_id = multi_mat ? take(sizeof(int32_t) * ld) : 0;
   f.mscale = any_scale ? take(sizeof(double) * ld) : 0;
   f.mats = take(sizeof(Material) * p->mats.size());
@@ -400,6 +401,7 @@ cudaError_t upload_plan(const Plan& p, char* ws, cudaStream_t st, DevPtrs* d) {
   const Plan::Off& f = p.off;
   d->b.q = (double*)(ws + f.q);
   d->b.qd = (double*)(ws + f.qd);
+  d->b.rs = (double*)(ws + f.rs);
   d->b.ld = p.ld;
   d->b.mat_id = p.mat_id.empty() ? nullptr : (const int32_t*)(ws + f.mat_id);
   d->b.mscale = p.mscale.empty() ? nullptr : (const double*)(ws + f.mscale);

@@ -58,7 +58,7 @@ struct Plan {
   // device layout (byte offsets into the workspace)
   size_t workspace_bytes = 0;
   struct Off {
-    size_t q, qd, mat_id, mscale, mats, hinv, perm, io, err;
+    size_t q, qd, rs, mat_id, mscale, mats, hinv, perm, io, err;
     size_t slot_info, geo, seg_flags, seg_red, long_list, left_iface;
     std::vector<size_t> tops, lams;  // per BTD level: tops[0] = chain tops (n_long), lams[i] = level i+1 λ
     size_t tree_base;
