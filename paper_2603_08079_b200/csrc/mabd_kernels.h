@@ -33,6 +33,31 @@ struct BtdArgs {
   StepConsts k;
 };
 
+struct TreeArgs {
+  BodyArrays b;
+  const HinvBlk* hinv_tab;     // per material, or null (per-body mass scale)
+  const int32_t* up_joint;
+  const int32_t* child_off;
+  const int32_t* child_joint;
+  const int64_t* ws_off;
+  const int32_t* jnpts;
+  const int32_t* jchd;
+  const double* jy;            // [K][12]
+  const int32_t* group_off;
+  const int32_t* glev_ptr;
+  const int32_t* glev_off;
+  double* Shat;                // [K][36] child-side condensed dual block of each joint (6×6, row-major)
+  double* rhat;                // [K][6]
+  double* lam;                 // [K][6]
+  double* bscr;                // [n][21]: R, δq̃ between the passes
+  double* ws;                  // per-body y, W
+  int32_t group0;              // first group of this launch
+  StepConsts k;
+};
+
+enum : int32_t { TREE_UP = 0, TREE_DOWN = 1, TREE_BOTH = 2 };
+cudaError_t launch_tree(const TreeArgs& a, int ngroups, int mode, cudaStream_t st);
+
 size_t cr_smem_bytes();
 cudaError_t chain_kernels_init();
 cudaError_t launch_chain(const ChainArgs& a, int nblocks, bool finish, cudaStream_t st);

@@ -329,6 +329,13 @@ mabd_status build_plan(const mabd_bodies* B, const mabd_joints* J, const mabd_op
     if (ok) p->solver = MABD_SOLVER_CHAIN;
     if (!ok && req == MABD_SOLVER_CHAIN) return *msg = "chain solver requested: " + why, MABD_EINVAL;
   }
+  if (!ok && (req == 0 || req == MABD_SOLVER_TREE)) {
+    std::string why2;
+    ok = tree_build(J, B->n, p, &pos, &why2);
+    if (ok) p->solver = MABD_SOLVER_TREE;
+    if (!ok && req == MABD_SOLVER_TREE) return *msg = "tree solver requested: " + why2, MABD_EINVAL;
+    if (!ok) why += "; " + why2;
+  }
   if (!ok) {
     *msg = "topology not supported by this build (" + why + ")";
     return MABD_EUNSUPPORTED;
@@ -386,6 +393,25 @@ mabd_status build_plan(const mabd_bodies* B, const mabd_joints* J, const mabd_op
       if (!L.fused) f.tops.push_back(take(sizeof(Top) * L.windows));
     }
   }
+  if (p->solver == MABD_SOLVER_TREE) {
+    const TreePlan& t = p->tree;
+    const int64_t K = p->n_joints, n = B->n;
+    f.t_up = take(sizeof(int32_t) * n);
+    f.t_coff = take(sizeof(int32_t) * (n + 1));
+    f.t_cj = take(sizeof(int32_t) * std::max<size_t>(1, t.child_joint.size()));
+    f.t_wsoff = take(sizeof(int64_t) * (n + 1));
+    f.t_jnpts = take(sizeof(int32_t) * std::max<int64_t>(1, K));
+    f.t_jchd = take(sizeof(int32_t) * std::max<int64_t>(1, K));
+    f.t_jy = take(sizeof(double) * 12 * std::max<int64_t>(1, K));
+    f.t_goff = take(sizeof(int32_t) * t.group_off.size());
+    f.t_glp = take(sizeof(int32_t) * t.glev_ptr.size());
+    f.t_glo = take(sizeof(int32_t) * t.glev_off.size());
+    f.t_shat = take(sizeof(double) * 36 * std::max<int64_t>(1, K));
+    f.t_rhat = take(sizeof(double) * 6 * std::max<int64_t>(1, K));
+    f.t_lam = take(sizeof(double) * 6 * std::max<int64_t>(1, K));
+    f.t_bscr = take(sizeof(double) * 21 * n);
+    f.t_ws = take(sizeof(double) * std::max<int64_t>(1, t.ws_total));
+  }
   p->workspace_bytes = cur;
   return MABD_OK;
 }
@@ -436,6 +462,39 @@ cudaError_t upload_plan(const Plan& p, char* ws, cudaStream_t st, DevPtrs* d) {
     for (size_t o : f.tops) d->tops.push_back((Top*)(ws + o));
     for (size_t o : f.lams) d->lams.push_back((double*)(ws + o));
   }
+  if (p.solver == MABD_SOLVER_TREE) {
+    const TreePlan& t = p.tree;
+    TreeArgs& A = d->tree;
+    A.b = d->b;
+    A.hinv_tab = p.mscale.empty() ? d->hinv : nullptr;
+    A.up_joint = (const int32_t*)(ws + f.t_up);
+    A.child_off = (const int32_t*)(ws + f.t_coff);
+    A.child_joint = (const int32_t*)(ws + f.t_cj);
+    A.ws_off = (const int64_t*)(ws + f.t_wsoff);
+    A.jnpts = (const int32_t*)(ws + f.t_jnpts);
+    A.jchd = (const int32_t*)(ws + f.t_jchd);
+    A.jy = (const double*)(ws + f.t_jy);
+    A.group_off = (const int32_t*)(ws + f.t_goff);
+    A.glev_ptr = (const int32_t*)(ws + f.t_glp);
+    A.glev_off = (const int32_t*)(ws + f.t_glo);
+    A.Shat = (double*)(ws + f.t_shat);
+    A.rhat = (double*)(ws + f.t_rhat);
+    A.lam = (double*)(ws + f.t_lam);
+    A.bscr = (double*)(ws + f.t_bscr);
+    A.ws = (double*)(ws + f.t_ws);
+    A.group0 = 0;
+    if ((e = put((int32_t*)A.up_joint, t.up_joint, st))) return e;
+    if ((e = put((int32_t*)A.child_off, t.child_off, st))) return e;
+    if ((e = put((int32_t*)A.child_joint, t.child_joint, st))) return e;
+    if ((e = put((int64_t*)A.ws_off, t.ws_off, st))) return e;
+    if ((e = put((int32_t*)A.jnpts, t.jnpts, st))) return e;
+    if ((e = put((int32_t*)A.jchd, t.jchd, st))) return e;
+    if ((e = put((double*)A.jy, t.jy, st))) return e;
+    if ((e = put((int32_t*)A.group_off, t.group_off, st))) return e;
+    if ((e = put((int32_t*)A.glev_ptr, t.glev_ptr, st))) return e;
+    if ((e = put((int32_t*)A.glev_off, t.glev_off, st))) return e;
+    if ((e = cudaMemsetAsync(A.lam, 0, sizeof(double) * 6 * std::max<int64_t>(1, p.n_joints), st))) return e;
+  }
   return cudaSuccess;
 }
 
@@ -461,6 +520,7 @@ cudaError_t launch_step(const Plan& p, const DevPtrs& d, double h, int32_t step,
   for (int i = 0; i < 3; ++i) k.grav[i] = p.grav[i];
   k.step_index = step;
   k.err = d.err;
+  if (p.solver == MABD_SOLVER_TREE) return tree_step(p, d, k, st);
   if (p.solver != MABD_SOLVER_CHAIN) return cudaErrorNotSupported;
   ChainArgs a;
   a.b = d.b;

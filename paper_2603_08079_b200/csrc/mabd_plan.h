@@ -17,21 +17,25 @@ struct BtdLevel {
   bool fused;      // top level (n_u ≤ 256)
 };
 
-// Tree plan (leaf-to-root elimination, reading A12); see mabd_tree.cu.
+// Tree plan (exact leaf-to-root elimination, reading A12); see mabd_tree.cu.
+// Internal body order: bottom groups (CTA-local subtrees, ≤ TREE_CAP bodies each), then the top group;
+// inside a group bodies are sorted by depth, deepest first, with per-level ranges.
+constexpr int TREE_CAP = 256;
+constexpr int TREE_MAXN = 24;  // max dual rows of the child joints of one body (frontal size ≤ 24 + 6)
 struct TreePlan {
-  int64_t n_levels = 0;
-  std::vector<int64_t> level_off;    // [n_levels+1] body ranges per depth (internal order is by depth)
-  std::vector<int32_t> parent;       // [n] internal parent index (−1 for roots)
-  std::vector<int32_t> up_joint;     // [n] internal joint index of the joint to the parent (−1 if none)
-  std::vector<int32_t> child_off;    // [n+1] CSR of the body's "child joints" (incl. anchors)
-  std::vector<int32_t> child_joint;  // joint ids
-  std::vector<int32_t> jrow_off;     // [K+1] dual row offset per joint (3 or 6 rows)
+  std::vector<int32_t> up_joint;     // [n] joint to the parent (−1 for a root)
+  std::vector<int32_t> child_off;    // [n+1] CSR of each body's child joints (incl. anchors)
+  std::vector<int32_t> child_joint;
+  std::vector<int64_t> ws_off;       // [n+1] per-body doubles of (y, W) kept for the downward pass
   std::vector<int32_t> jnpts;        // [K]
-  std::vector<int32_t> jparent;      // [K] body the joint hangs from (internal index)
-  std::vector<int32_t> jchild;       // [K] child body (internal) or −1 for anchors
-  std::vector<double> jy_par;        // [K][2][3] material points on the parent body
-  std::vector<double> jy_chd;        // [K][2][3] material points on the child body, or world points
-  int32_t max_child_rows = 0;
+  std::vector<int32_t> jchd;         // [K] child body (internal) or −1 for an anchor
+  std::vector<double> jy;            // [K][12]: ȳ on the parent body (2×3), ȳ on the child / world point (2×3)
+  std::vector<int32_t> group_off;    // [G+1] body ranges
+  std::vector<int32_t> glev_ptr;     // [G+1] into glev_off
+  std::vector<int32_t> glev_off;     // level boundaries (absolute body indices), deepest level first
+  int32_t n_bottom = 0;              // bottom groups; the top group (if any) is group n_bottom
+  bool has_top = false;
+  int64_t ws_total = 0;
 };
 
 struct Plan {
@@ -61,8 +65,8 @@ struct Plan {
     size_t q, qd, rs, mat_id, mscale, mats, hinv, perm, io, err;
     size_t slot_info, geo, seg_flags, seg_red, long_list, left_iface;
     std::vector<size_t> tops, lams;  // per BTD level: tops[0] = chain tops (n_long), lams[i] = level i+1 λ
-    size_t tree_base;
-    std::vector<size_t> tree_off;
+    size_t t_up, t_coff, t_cj, t_wsoff, t_jnpts, t_jchd, t_jy, t_goff, t_glp, t_glo, t_shat, t_rhat, t_lam, t_bscr,
+        t_ws;
   } off{};
 };
 
@@ -78,7 +82,7 @@ struct DevPtrs {
   int32_t *seg_flags = nullptr, *seg_red = nullptr, *long_list = nullptr, *left_iface = nullptr;
   std::vector<Top*> tops;
   std::vector<double*> lams;
-  std::vector<void*> tree;           // tree arrays (see mabd_tree.cu)
+  TreeArgs tree{};                   // device pointers of the tree solver
 };
 
 mabd_status build_plan(const mabd_bodies* bodies, const mabd_joints* joints, const mabd_options* opts, Plan* p,
@@ -88,10 +92,8 @@ cudaError_t prefactor_device(const Plan& p, const DevPtrs& d, double h, cudaStre
 cudaError_t reset_err(const DevPtrs& d, cudaStream_t st);
 cudaError_t launch_step(const Plan& p, const DevPtrs& d, double h, int32_t step, cudaStream_t st);
 
-// tree solver hooks (mabd_tree.cu)
-bool tree_build(const mabd_joints* joints, int64_t n, Plan* p, std::string* msg, std::vector<int64_t>* order);
-void tree_layout(Plan* p, size_t* cursor);
-cudaError_t tree_upload(const Plan& p, char* ws, cudaStream_t st, DevPtrs* d);
+// tree solver (mabd_tree.cu)
+bool tree_build(const mabd_joints* joints, int64_t n, Plan* p, std::vector<int64_t>* pos_of_body, std::string* msg);
 cudaError_t tree_step(const Plan& p, const DevPtrs& d, const StepConsts& k, cudaStream_t st);
 
 }  // namespace mabd

@@ -1,0 +1,60 @@
+"""GPU parity of the tree path (config-4 recipe, random trees with ball joints and linear hinges) against the
+CPU oracle, through the C ABI. Tolerances as in test_gpu_chain (BASELINE.json north star)."""
+import numpy as np
+import pytest
+
+import oracle as O
+from mabd_scenes import generators as G
+
+from test_gpu_chain import TOL1, TOLN, _concat, check, gpu_run
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.mark.parametrize("depth", [2, 4, 6])
+def test_cfg4_recipe_small(cuda_ok, depth):
+    """Complete binary trees small enough for one CTA-local group (fused up+down launch)."""
+    sc = G.cfg4_binary_tree(depth)
+    check(sc, 1, route="dense", expect_solver="tree")
+    check(sc, 10, expect_solver="tree")
+
+
+def test_cfg4_recipe_with_top_group(cuda_ok):
+    """Depth 10 (1,023 bodies): four 255-body bottom groups plus a 3-body top group (3 launches/step)."""
+    sc = G.cfg4_binary_tree(10)
+    check(sc, 1, expect_solver="tree")
+    check(sc, 5, expect_solver="tree")
+    q, _, info = gpu_run(sc, 5)
+    assert info["launches_per_step"] == 3
+    assert O.constraint_residual(sc, q) <= 1e-10
+
+
+@pytest.mark.parametrize("seed", range(4))
+def test_random_trees(cuda_ok, seed):
+    rng = np.random.default_rng(seed)
+    parts = []
+    for k in range(4):
+        n = int(rng.integers(2, 400))
+        parts.append(G.random_tree(n, seed=10 * seed + k, anchored=bool(rng.integers(2)),
+                                   hinge_frac=float(rng.uniform(0, 1)), vel=0.3, jitter=1e-3,
+                                   extra_anchors=int(rng.integers(0, 3)), max_children=int(rng.integers(1, 4))))
+    sc = _concat(parts)
+    check(sc, 1, expect_solver="tree")
+    check(sc, 3, expect_solver="tree")
+
+
+def test_hinge_chain_uses_tree_solver(cuda_ok):
+    """A path of linear hinges (6-row joints) is not a ball-joint chain: the tree solver takes it."""
+    sc = G.random_chain(300, seed=3, npts=2, end_anchor=True, vel=0.2)
+    check(sc, 1, expect_solver="tree")
+    check(sc, 3, expect_solver="tree")
+
+
+def test_cfg4_full_size_one_step(cuda_ok):
+    """BASELINE config 4 at full size (65,535 bodies, 393,207 dual rows): one step vs the block-LU oracle."""
+    sc = G.cfg4_binary_tree(16)
+    q_o, _ = O.step(sc, sc.q0, sc.qd0, sc.h, route="blocklu")
+    q_g, _, info = gpu_run(sc, 1)
+    assert info["solver"] == "tree" and info["n_dual_rows"] == 393207
+    assert O.rel_err(q_g, q_o) <= TOL1
+    assert O.constraint_residual(sc, q_g) <= 1e-10
