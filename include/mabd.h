@@ -130,6 +130,10 @@ mabd_status mabd_set_state(mabd_handle h_, const double *q, const double *qd, in
 mabd_status mabd_query(mabd_handle h_, int32_t *solver, int32_t *launches_per_step, int64_t *n_bodies,
                        int64_t *n_dual_rows);
 
+/* Statistics of the last mabd_step call: iterations of the last iterative dual solve (sparse solver: PCG
+ * iterations of the final step; 0 for the direct chain/tree solvers). Synchronises the handle's stream. */
+mabd_status mabd_solver_stats(mabd_handle h_, int64_t *last_iterations);
+
 /* Release device memory owned by the library; NULL is a no-op. */
 mabd_status mabd_destroy(mabd_handle h_);
 

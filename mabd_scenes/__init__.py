@@ -19,6 +19,7 @@ from .generators import (  # noqa: F401
     random_chain,
     random_tree,
     small_net,
+    ring,
     box_mbar,
     CONFIG_NAMES,
 )

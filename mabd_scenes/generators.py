@@ -529,3 +529,22 @@ def random_tree(n: int, seed: int = 0, anchored: bool = True, hinge_frac: float 
 def small_net(side: int = 8, extra_frac: float = 0.05, max_off: int = 4, nsteps: int = 1) -> Scene:
     """cfg-5 recipe at a small side length (corner pins, grid + bounded-range extra links)."""
     return cfg5_net(side=side, extra_frac=extra_frac, max_off=max_off, nsteps=nsteps)
+
+
+def ring(n: int = 4, seed: int = 0, vel: float = 0.3, h: float = 1e-2) -> Scene:
+    """A closed loop of n random boxes ("ring of 4"): a random chain plus one joint closing it."""
+    sc = random_chain(n, seed=seed, anchored=False, vel=vel, h=h, gravity=True)
+    A = np.swapaxes(sc.q0[:, :9].reshape(n, 3, 3), 1, 2)
+    t = sc.q0[:, 9:]
+    p = 0.5 * (t[0] + t[n - 1])
+    ya = A[n - 1].T @ (p - t[n - 1])
+    yb = A[0].T @ (p - t[0])
+    sc.body_a = np.append(sc.body_a, np.int32(n - 1)).astype(np.int32)
+    sc.body_b = np.append(sc.body_b, np.int32(0)).astype(np.int32)
+    sc.npts = np.append(sc.npts, np.int32(1)).astype(np.int32)
+    sc.ybar_a = np.vstack([sc.ybar_a, ya[None]])
+    sc.ybar_b = np.vstack([sc.ybar_b, yb[None]])
+    sc.name = f"ring_{n}"
+    sc.meta = {"topology": "net"}
+    sc.validate()
+    return sc

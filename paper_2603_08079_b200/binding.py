@@ -20,7 +20,7 @@ STATUS = {0: "MABD_OK", 1: "MABD_EINVAL", 2: "MABD_ESTATE", 3: "MABD_ENOMEM", 4:
 SOLVERS = {0: "auto", 1: "chain", 2: "tree", 3: "sparse"}
 
 EXPORTED = ["mabd_workspace_size", "mabd_create", "mabd_prefactor", "mabd_step", "mabd_get_state",
-            "mabd_set_state", "mabd_query", "mabd_destroy", "mabd_last_error"]
+            "mabd_set_state", "mabd_query", "mabd_solver_stats", "mabd_destroy", "mabd_last_error"]
 
 
 class MabdError(RuntimeError):
@@ -73,6 +73,7 @@ def load_library(path: str = LIB_PATH) -> ctypes.CDLL:
     lib.mabd_set_state.argtypes = [H, ctypes.c_void_p, ctypes.c_void_p, ctypes.c_int]
     lib.mabd_query.argtypes = [H, ctypes.POINTER(ctypes.c_int32), ctypes.POINTER(ctypes.c_int32),
                                ctypes.POINTER(ctypes.c_int64), ctypes.POINTER(ctypes.c_int64)]
+    lib.mabd_solver_stats.argtypes = [H, ctypes.POINTER(ctypes.c_int64)]
     lib.mabd_destroy.argtypes = [H]
     lib.mabd_last_error.argtypes = [H]
     lib.mabd_last_error.restype = ctypes.c_char_p
@@ -169,6 +170,11 @@ class Simulator:
                                          ctypes.byref(nr)), self._h)
         return {"solver": SOLVERS.get(s.value, s.value), "launches_per_step": l.value, "n_bodies": nb.value,
                 "n_dual_rows": nr.value}
+
+    def solver_stats(self) -> dict:
+        it = ctypes.c_int64()
+        self._check(self._lib.mabd_solver_stats(self._h, ctypes.byref(it)), self._h)
+        return {"last_iterations": it.value}
 
     def get_state(self, q_out=None, qd_out=None):
         """Copy (q, q̇) out in the caller's body order. Host numpy arrays by default; torch CUDA tensors

@@ -14,7 +14,7 @@ ROOT = os.path.dirname(PKG)
 CSRC = os.path.join(PKG, "csrc")
 LIB = os.path.join(PKG, "libmabd.so")
 
-SOURCES = ["mabd_host.cu", "mabd_plan.cu", "mabd_chain.cu", "mabd_tree.cu"]
+SOURCES = ["mabd_host.cu", "mabd_plan.cu", "mabd_chain.cu", "mabd_tree.cu", "mabd_sparse.cu"]
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 
 

@@ -109,6 +109,7 @@ mabd_status mabd_create(const mabd_bodies* bodies, const mabd_joints* joints, co
   }
   e = cudaMallocHost(&c->h_err, 2 * sizeof(int32_t));
   if (e == cudaSuccess) e = chain_kernels_init();
+  if (e == cudaSuccess && c->plan.solver == MABD_SOLVER_SPARSE) e = sparse_init();
   if (e == cudaSuccess) e = upload_plan(c->plan, c->ws, c->stream, &c->d);
   if (e == cudaSuccess) e = cudaStreamSynchronize(c->stream);
   if (e != cudaSuccess) {
@@ -199,6 +200,20 @@ mabd_status mabd_query(mabd_handle c, int32_t* solver, int32_t* launches_per_ste
   if (launches_per_step) *launches_per_step = c->plan.launches_per_step;
   if (n_bodies) *n_bodies = c->plan.n;
   if (n_dual_rows) *n_dual_rows = c->plan.n_dual_rows;
+  return MABD_OK;
+}
+
+mabd_status mabd_solver_stats(mabd_handle c, int64_t* last_iterations) {
+  if (!c) return fail(nullptr, MABD_EINVAL, "NULL handle");
+  if (!last_iterations) return fail(c, MABD_EINVAL, "last_iterations is NULL");
+  *last_iterations = 0;
+  if (c->plan.solver == MABD_SOLVER_SPARSE) {
+    int32_t it = 0;
+    CUDA_TRY(c, cudaSetDevice(c->device));
+    CUDA_TRY(c, cudaMemcpyAsync(&it, c->d.sparse.iters, sizeof(int32_t), cudaMemcpyDeviceToHost, c->stream));
+    CUDA_TRY(c, cudaStreamSynchronize(c->stream));
+    *last_iterations = it;
+  }
   return MABD_OK;
 }
 

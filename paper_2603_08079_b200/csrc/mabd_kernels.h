@@ -56,6 +56,24 @@ struct TreeArgs {
 };
 
 enum : int32_t { TREE_UP = 0, TREE_DOWN = 1, TREE_BOTH = 2 };
+
+struct SparseArgs {
+  BodyArrays b;
+  const HinvBlk* hinv_tab;     // per material, or null (per-body mass scale)
+  int64_t n, np;               // bodies, constraint points (3 dual rows each)
+  const int32_t* pa;           // [np] body on side a
+  const int32_t* pb;           // [np] body on side b or −1 (world)
+  const double* py;            // [np][6] ȳ_a, ȳ_b (world point when pb < 0)
+  const int32_t* inc_off;      // [n+1] CSR body → incident points (2·point + side)
+  const int32_t* inc;
+  double *rhs, *dinv, *lam, *res, *zz, *pp, *ap;  // component-major [3 or 6][np]
+  double* vv;                  // [12][n]
+  double* part;                // per-block partial sums
+  int32_t* iters;              // iterations of the last solve
+  double tol;
+  int32_t max_iter;
+  StepConsts k;
+};
 cudaError_t launch_tree(const TreeArgs& a, int ngroups, int mode, cudaStream_t st);
 
 size_t cr_smem_bytes();

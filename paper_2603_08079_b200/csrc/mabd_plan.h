@@ -38,6 +38,12 @@ struct TreePlan {
   int64_t ws_total = 0;
 };
 
+struct SparsePlan {
+  int64_t np = 0;
+  std::vector<int32_t> pa, pb, inc_off, inc;
+  std::vector<double> py;
+};
+
 struct Plan {
   int64_t n = 0, n_joints = 0, n_dual_rows = 0;
   int32_t solver = 0;
@@ -59,6 +65,8 @@ struct Plan {
   std::vector<BtdLevel> levels;      // levels[0] is BTD level 1
   // tree solver
   TreePlan tree;
+  // sparse solver
+  SparsePlan sparse;
   // device layout (byte offsets into the workspace)
   size_t workspace_bytes = 0;
   struct Off {
@@ -67,6 +75,7 @@ struct Plan {
     std::vector<size_t> tops, lams;  // per BTD level: tops[0] = chain tops (n_long), lams[i] = level i+1 λ
     size_t t_up, t_coff, t_cj, t_wsoff, t_jnpts, t_jchd, t_jy, t_goff, t_glp, t_glo, t_shat, t_rhat, t_lam, t_bscr,
         t_ws;
+    size_t s_pa, s_pb, s_py, s_incoff, s_inc, s_vec, s_vv, s_part, s_iters;
   } off{};
 };
 
@@ -83,6 +92,7 @@ struct DevPtrs {
   std::vector<Top*> tops;
   std::vector<double*> lams;
   TreeArgs tree{};                   // device pointers of the tree solver
+  SparseArgs sparse{};               // device pointers of the sparse solver
 };
 
 mabd_status build_plan(const mabd_bodies* bodies, const mabd_joints* joints, const mabd_options* opts, Plan* p,
@@ -95,5 +105,11 @@ cudaError_t launch_step(const Plan& p, const DevPtrs& d, double h, int32_t step,
 // tree solver (mabd_tree.cu)
 bool tree_build(const mabd_joints* joints, int64_t n, Plan* p, std::vector<int64_t>* pos_of_body, std::string* msg);
 cudaError_t tree_step(const Plan& p, const DevPtrs& d, const StepConsts& k, cudaStream_t st);
+
+// sparse solver (mabd_sparse.cu)
+bool sparse_build(const mabd_joints* joints, int64_t n, Plan* p, std::vector<int64_t>* pos_of_body, std::string* msg);
+cudaError_t sparse_init();
+cudaError_t sparse_step(const Plan& p, const DevPtrs& d, const StepConsts& k, cudaStream_t st);
+constexpr int SPARSE_MAX_BLOCKS = 148 * 8;
 
 }  // namespace mabd

@@ -22,12 +22,16 @@ except MabdError:
 e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
 torch.cuda.synchronize()
 e0.record(st)
+err = None
 try:
     sim.step(sc.h, steps)
-except MabdError:
-    pass
+except MabdError as ex:
+    err = str(ex)
 e1.record(st)
 torch.cuda.synchronize()
+if err:
+    print("step error:", err)
+print("solver stats:", sim.solver_stats())
 print(f"{os.environ.get('MABD_LIB', 'default')}: cfg{cfg} {e0.elapsed_time(e1) / steps * 1e3:.1f} us/step "
       f"({sim.query()['launches_per_step']} launches/step)")
 
