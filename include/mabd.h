@@ -130,6 +130,20 @@ mabd_status mabd_set_state(mabd_handle h_, const double *q, const double *qd, in
 mabd_status mabd_query(mabd_handle h_, int32_t *solver, int32_t *launches_per_step, int64_t *n_bodies,
                        int64_t *n_dual_rows);
 
+/* Multi-GPU (chain scenes). Every rank passes the full scene with options.world = W, options.rank = r and a
+ * 128-byte ncclUniqueId that rank 0 obtained from mabd_nccl_unique_id and shared (e.g. through
+ * torch.distributed); mabd_create is then collective. Rank r advances a contiguous share of the chain
+ * windows; long chains crossing ranks exchange one 27-double "top" system per rank per step
+ * (ncclAllGather, in-stream). mabd_get_state broadcasts every rank's share first, so all ranks return the
+ * full state. With world > 1 and nccl_unique_id == NULL the W parts are emulated in one process (one GPU,
+ * same arithmetic, the all-gather is a no-op): used to test the partitioned algorithm on one device. */
+mabd_status mabd_nccl_unique_id(void *out, size_t bytes);
+
+/* Host-only analysis for tests: out[0..9] = {parts, windows, long windows, this rank's window range lo/hi,
+ * long-window range lo/hi, left_open, right_open, sequential-top unknowns}. No device work. */
+mabd_status mabd_partition_info(const mabd_bodies *bodies, const mabd_joints *joints,
+                                const mabd_options *opts, int64_t *out, int64_t n_out);
+
 /* Statistics of the last mabd_step call: iterations of the last iterative dual solve (sparse solver: PCG
  * iterations of the final step; 0 for the direct chain/tree solvers). Synchronises the handle's stream. */
 mabd_status mabd_solver_stats(mabd_handle h_, int64_t *last_iterations);

@@ -20,7 +20,8 @@ STATUS = {0: "MABD_OK", 1: "MABD_EINVAL", 2: "MABD_ESTATE", 3: "MABD_ENOMEM", 4:
 SOLVERS = {0: "auto", 1: "chain", 2: "tree", 3: "sparse"}
 
 EXPORTED = ["mabd_workspace_size", "mabd_create", "mabd_prefactor", "mabd_step", "mabd_get_state",
-            "mabd_set_state", "mabd_query", "mabd_solver_stats", "mabd_destroy", "mabd_last_error"]
+            "mabd_set_state", "mabd_query", "mabd_solver_stats", "mabd_nccl_unique_id", "mabd_partition_info",
+            "mabd_destroy", "mabd_last_error"]
 
 
 class MabdError(RuntimeError):
@@ -74,6 +75,9 @@ def load_library(path: str = LIB_PATH) -> ctypes.CDLL:
     lib.mabd_query.argtypes = [H, ctypes.POINTER(ctypes.c_int32), ctypes.POINTER(ctypes.c_int32),
                                ctypes.POINTER(ctypes.c_int64), ctypes.POINTER(ctypes.c_int64)]
     lib.mabd_solver_stats.argtypes = [H, ctypes.POINTER(ctypes.c_int64)]
+    lib.mabd_nccl_unique_id.argtypes = [ctypes.c_void_p, ctypes.c_size_t]
+    lib.mabd_partition_info.argtypes = [ctypes.POINTER(_Bodies), ctypes.POINTER(_Joints), ctypes.POINTER(_Options),
+                                        ctypes.POINTER(ctypes.c_int64), ctypes.c_int64]
     lib.mabd_destroy.argtypes = [H]
     lib.mabd_last_error.argtypes = [H]
     lib.mabd_last_error.restype = ctypes.c_char_p
@@ -98,6 +102,40 @@ def _ptr(a, t=_dp):
     return a.ctypes.data_as(t) if a is not None and a.size else None
 
 
+def nccl_unique_id() -> bytes:
+    """A fresh 128-byte ncclUniqueId (rank 0 calls this and shares it)."""
+    lib = load_library()
+    buf = ctypes.create_string_buffer(128)
+    st = lib.mabd_nccl_unique_id(buf, 128)
+    if st != MABD_OK:
+        raise MabdError(st, lib.mabd_last_error(None).decode())
+    return buf.raw
+
+
+def partition_info(scene, world: int, rank: int) -> dict:
+    """Host-only plan of the multi-part chain decomposition for one rank (no GPU needed)."""
+    lib = load_library()
+    n = int(scene.q0.shape[0])
+    K = int(scene.body_a.shape[0])
+    P = int(np.asarray(scene.npts).sum()) if K else 0
+    k = dict(q0=_f64(scene.q0, (n, 12)), qd0=_f64(scene.qd0, (n, 12)), mbar=_f64(scene.mbar, (n, 10)),
+             volume=_f64(scene.volume, (n,)), youngs=_f64(scene.youngs, (n,)), poisson=_f64(scene.poisson, (n,)),
+             body_a=_i32(scene.body_a, (K,)), body_b=_i32(scene.body_b, (K,)), npts=_i32(scene.npts, (K,)),
+             ybar_a=_f64(scene.ybar_a, (P, 3)), ybar_b=_f64(scene.ybar_b, (P, 3)))
+    b = _Bodies(n, _ptr(k["q0"]), _ptr(k["qd0"]), _ptr(k["mbar"]), _ptr(k["volume"]), _ptr(k["youngs"]),
+                _ptr(k["poisson"]), None, (ctypes.c_double * 3)(*[float(x) for x in np.asarray(scene.gravity)]))
+    j = _Joints(K, _ptr(k["body_a"], _ip), _ptr(k["body_b"], _ip), _ptr(k["npts"], _ip), _ptr(k["ybar_a"]),
+                _ptr(k["ybar_b"]))
+    o = _Options(1, 1, 0, int(rank), int(world), None, None, 0, None)
+    out = (ctypes.c_int64 * 10)()
+    st = lib.mabd_partition_info(ctypes.byref(b), ctypes.byref(j), ctypes.byref(o), out, 10)
+    if st != MABD_OK:
+        raise MabdError(st, lib.mabd_last_error(None).decode())
+    keys = ["parts", "windows", "long_windows", "win_lo", "win_hi", "long_lo", "long_hi", "left_open", "right_open",
+            "seq_unknowns"]
+    return dict(zip(keys, list(out)))
+
+
 class Simulator:
     """One libmabd handle: ``mabd_create`` → ``prefactor(h)`` → ``step(h, n)`` → ``get_state()``.
 
@@ -106,7 +144,8 @@ class Simulator:
     """
 
     def __init__(self, q0, qd0, mbar, volume, youngs, poisson, gravity, body_a, body_b, npts, ybar_a, ybar_b,
-                 solver: int = 0, device: Optional[int] = None, stream=None):
+                 solver: int = 0, device: Optional[int] = None, stream=None, world: int = 1, rank: int = 0,
+                 nccl_id: Optional[bytes] = None):
         import torch
 
         self._lib = load_library()
@@ -129,7 +168,10 @@ class Simulator:
                                _ptr(k["ybar_a"]), _ptr(k["ybar_b"]))
         with torch.cuda.device(self.device):
             self._stream = stream if stream is not None else torch.cuda.current_stream(self.device)
-            opts = _Options(1, 1, int(solver), 0, 1, None, None, 0, ctypes.c_void_p(self._stream.cuda_stream))
+            self._nccl_id = ctypes.create_string_buffer(bytes(nccl_id), 128) if nccl_id is not None else None
+            opts = _Options(1, 1, int(solver), int(rank), int(world),
+                            ctypes.cast(self._nccl_id, ctypes.c_void_p) if self._nccl_id is not None else None,
+                            None, 0, ctypes.c_void_p(self._stream.cuda_stream))
             nbytes = ctypes.c_size_t(0)
             self._check(self._lib.mabd_workspace_size(ctypes.byref(self._bodies), ctypes.byref(self._joints),
                                                       ctypes.byref(opts), ctypes.byref(nbytes)), None)

@@ -14,7 +14,7 @@ ROOT = os.path.dirname(PKG)
 CSRC = os.path.join(PKG, "csrc")
 LIB = os.path.join(PKG, "libmabd.so")
 
-SOURCES = ["mabd_host.cu", "mabd_plan.cu", "mabd_chain.cu", "mabd_tree.cu", "mabd_sparse.cu"]
+SOURCES = ["mabd_host.cu", "mabd_plan.cu", "mabd_chain.cu", "mabd_tree.cu", "mabd_sparse.cu", "mabd_nccl.cu"]
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 
 
@@ -38,7 +38,7 @@ def build(force: bool = False, verbose: bool = False, out: str = LIB, defines=()
         return LIB
     srcs = [os.path.join(CSRC, s) for s in SOURCES if os.path.exists(os.path.join(CSRC, s))]
     cmd = [nvcc(), "-std=c++17", "-O3", "-lineinfo", *ARCH, "-Xcompiler", "-fPIC", "-shared",
-           "-I", os.path.join(ROOT, "include"), *[f"-D{d}" for d in defines], "-o", out + ".tmp", *srcs]
+           "-I", os.path.join(ROOT, "include"), *[f"-D{d}" for d in defines], "-o", out + ".tmp", *srcs, "-ldl"]
     if verbose:
         cmd.insert(1, "-Xptxas=-v")
         print(" ".join(cmd), file=sys.stderr)

@@ -588,13 +588,20 @@ __global__ void __launch_bounds__(CT) btd_kernel(BtdArgs a) {
     if (t & 1) cr_invert(s, t, a.k);  // eliminated at stride 1
   }
   if (tid == CT - 1) {
+    // equation 256: the next window's first unknown (partial, completed by that window), the next part's
+    // first unknown (partial from this part's last unknown: its top D1, r1), or padding
     const bool real_next = (w + 1) * SEG < nu;
-    const double dv = real_next ? 0.0 : 1.0;
-    const double Dn[6] = {dv, 0, 0, dv, 0, dv};
     const double Z[9] = {0, 0, 0, 0, 0, 0, 0, 0, 0};
-    stv<6>(eqD(s, SEG), Dn);
+    if (!real_next && a.right_open) {
+      stv<6>(eqD(s, SEG), a.top_in[nu - 1].D1);
+      stv<3>(eqR(s, SEG), a.top_in[nu - 1].r1);
+    } else {
+      const double dv = real_next ? 0.0 : 1.0;
+      const double Dn[6] = {dv, 0, 0, dv, 0, dv};
+      stv<6>(eqD(s, SEG), Dn);
+      stv<3>(eqR(s, SEG), Z);
+    }
     stv<9>(eqB(s, SEG), Z);
-    stv<3>(eqR(s, SEG), Z);
   }
   __syncthreads();
   cr_forward(s, tid, a.k);
@@ -609,7 +616,7 @@ __global__ void __launch_bounds__(CT) btd_kernel(BtdArgs a) {
 #pragma unroll
     for (int e = 0; e < 3; ++e) {
       eqR(s, cr_pos(0))[e] = a.lam_in[3 * w + e];
-      eqR(s, SEG)[e] = real_next ? a.lam_in[3 * (w + 1) + e] : 0.0;
+      eqR(s, SEG)[e] = real_next ? a.lam_in[3 * (w + 1) + e] : (a.right_open ? a.lam_remote[e] : 0.0);
     }
   }
   __syncthreads();
@@ -622,6 +629,134 @@ __global__ void __launch_bounds__(CT) btd_kernel(BtdArgs a) {
       for (int e = 0; e < 3; ++e) a.lam_out[3 * u + e] = eqR(s, cr_pos(t))[e];
     }
   }
+}
+
+// ------------------------------------------------------------------ multi-part chains: sequential part top
+// A part (one rank's share of a long chain, or an emulated rank) reduces its n level unknowns u = 0..n−1 and
+// the next part's first unknown ρ (partial, from this side) onto {0, ρ}: eliminate u = 1..n−1 in order,
+// carrying the coupling X of equation 0 to the current frontier (block Thomas with a spike).
+// n is small (≤ 256 by construction, typically ≤ 17), so one thread does it.
+__device__ __forceinline__ void seq_eq(const SeqArgs& a, int u, double* D, double* r) {
+  // equation u from the tops of the level below: D_u = top[u].D0 + top[u−1].D1 (u > 0), same for r;
+  // u = n is the remote unknown ρ (partial: top[n−1].D1, r1 if right-open; else padding)
+  const int n = a.n;
+  if (u == n) {
+    if (a.right_open) {
+#pragma unroll
+      for (int e = 0; e < 6; ++e) D[e] = a.top_in[n - 1].D1[e];
+#pragma unroll
+      for (int e = 0; e < 3; ++e) r[e] = a.top_in[n - 1].r1[e];
+    } else {
+      D[0] = 1; D[1] = 0; D[2] = 0; D[3] = 1; D[4] = 0; D[5] = 1;
+      r[0] = r[1] = r[2] = 0;
+    }
+    return;
+  }
+#pragma unroll
+  for (int e = 0; e < 6; ++e) D[e] = a.top_in[u].D0[e] + (u > 0 ? a.top_in[u - 1].D1[e] : 0.0);
+#pragma unroll
+  for (int e = 0; e < 3; ++e) r[e] = a.top_in[u].r0[e] + (u > 0 ? a.top_in[u - 1].r1[e] : 0.0);
+}
+
+__global__ void seq_top_kernel(SeqArgs a) {
+  if (threadIdx.x != 0 || blockIdx.x != 0) return;
+  const int n = a.n;
+  double D0s[6], r0[3], X[9], Dks[6], rk[3];
+  seq_eq(a, 0, D0s, r0);
+#pragma unroll
+  for (int e = 0; e < 9; ++e) X[e] = a.top_in[0].B[e];  // coupling 0 → 1 (or → ρ when n = 1)
+  seq_eq(a, n == 1 ? 1 : 1, Dks, rk);
+  for (int k = 1; k < n; ++k) {
+    double Di[6], Dif[9], Bk[9];
+    if (!sym_inv_spd(Dks, Di)) report(a.k, ERR_SINGULAR);
+    full_from_sym(Di, Dif);
+#pragma unroll
+    for (int e = 0; e < 9; ++e) Bk[e] = a.top_in[k].B[e];  // k → k+1 (ρ when k = n−1)
+    double* sc = a.scratch + 27 * (size_t)k;
+#pragma unroll
+    for (int e = 0; e < 6; ++e) sc[e] = Di[e];
+#pragma unroll
+    for (int e = 0; e < 9; ++e) { sc[6 + e] = X[e]; sc[15 + e] = Bk[e]; }
+#pragma unroll
+    for (int e = 0; e < 3; ++e) sc[24 + e] = rk[e];
+    // eq 0:  D0 −= X D⁻¹ Xᵀ,  r0 −= X D⁻¹ r_k,  X ← −X D⁻¹ B_k
+    double XD[9], T[9], v[3];
+    mat3_mul(X, Dif, XD);
+    mat3_mul_bt(XD, X, T);
+    double D0f[9];
+    full_from_sym(D0s, D0f);
+#pragma unroll
+    for (int e = 0; e < 9; ++e) D0f[e] -= T[e];
+    D0s[0] = D0f[0]; D0s[1] = 0.5 * (D0f[1] + D0f[3]); D0s[2] = 0.5 * (D0f[2] + D0f[6]);
+    D0s[3] = D0f[4]; D0s[4] = 0.5 * (D0f[5] + D0f[7]); D0s[5] = D0f[8];
+    mat3_vec(XD, rk, v);
+#pragma unroll
+    for (int e = 0; e < 3; ++e) r0[e] -= v[e];
+    double nX[9];
+    mat3_mul(XD, Bk, nX);
+#pragma unroll
+    for (int e = 0; e < 9; ++e) X[e] = -nX[e];
+    // eq k+1:  D −= B_kᵀ D⁻¹ B_k,  r −= B_kᵀ D⁻¹ r_k
+    double Dn[6], rn[3], DB[9], BDB[9], Dnf[9], w[3], bw[3];
+    seq_eq(a, k + 1, Dn, rn);
+    mat3_mul(Dif, Bk, DB);
+    mat3_mul_at(Bk, DB, BDB);
+    full_from_sym(Dn, Dnf);
+#pragma unroll
+    for (int e = 0; e < 9; ++e) Dnf[e] -= BDB[e];
+    Dks[0] = Dnf[0]; Dks[1] = 0.5 * (Dnf[1] + Dnf[3]); Dks[2] = 0.5 * (Dnf[2] + Dnf[6]);
+    Dks[3] = Dnf[4]; Dks[4] = 0.5 * (Dnf[5] + Dnf[7]); Dks[5] = Dnf[8];
+    mat3_vec(Dif, rk, w);
+    mat3t_vec(Bk, w, bw);
+#pragma unroll
+    for (int e = 0; e < 3; ++e) rk[e] = rn[e] - bw[e];
+  }
+  Top* o = a.top_out;
+#pragma unroll
+  for (int e = 0; e < 6; ++e) { o->D0[e] = D0s[e]; o->D1[e] = Dks[e]; }
+#pragma unroll
+  for (int e = 0; e < 9; ++e) o->B[e] = X[e];
+#pragma unroll
+  for (int e = 0; e < 3; ++e) { o->r0[e] = r0[e]; o->r1[e] = rk[e]; }
+}
+
+__global__ void seq_finish_kernel(SeqArgs a) {
+  if (threadIdx.x != 0 || blockIdx.x != 0) return;
+  const int n = a.n;
+  double l0[3], lnext[3];
+#pragma unroll
+  for (int e = 0; e < 3; ++e) {
+    l0[e] = a.lam_ends[e];
+    lnext[e] = a.right_open ? a.lam_ends[3 + e] : 0.0;
+    a.lam_out[e] = l0[e];
+  }
+  for (int k = n - 1; k >= 1; --k) {  // λ_k = D'_k⁻¹ (r'_k − X_kᵀ λ_0 − B_k λ_{k+1})
+    const double* sc = a.scratch + 27 * (size_t)k;
+    double v[3], w[3];
+#pragma unroll
+    for (int e = 0; e < 3; ++e) v[e] = sc[24 + e];
+    mat3t_vec(sc + 6, l0, w);
+#pragma unroll
+    for (int e = 0; e < 3; ++e) v[e] -= w[e];
+    mat3_vec(sc + 15, lnext, w);
+#pragma unroll
+    for (int e = 0; e < 3; ++e) v[e] -= w[e];
+    sym_vec(sc, v, w);
+#pragma unroll
+    for (int e = 0; e < 3; ++e) {
+      a.lam_out[3 * k + e] = w[e];
+      lnext[e] = w[e];
+    }
+  }
+}
+
+cudaError_t launch_seq_top(const SeqArgs& a, cudaStream_t st) {
+  seq_top_kernel<<<1, 32, 0, st>>>(a);
+  return cudaGetLastError();
+}
+cudaError_t launch_seq_finish(const SeqArgs& a, cudaStream_t st) {
+  seq_finish_kernel<<<1, 32, 0, st>>>(a);
+  return cudaGetLastError();
 }
 
 size_t cr_smem_bytes() { return sizeof(double) * NEQ * (6 + 9 + 9 + 3); }

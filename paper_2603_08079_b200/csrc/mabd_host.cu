@@ -116,6 +116,18 @@ mabd_status mabd_create(const mabd_bodies* bodies, const mabd_joints* joints, co
     mabd_destroy(c);
     return fail(nullptr, MABD_ECUDA, "create: %s", cudaGetErrorString(e));
   }
+  if (c->plan.use_nccl) {  // collective: every rank of the world calls mabd_create
+    std::string why;
+    if (!nccl_load(&why)) {
+      mabd_destroy(c);
+      return fail(nullptr, MABD_ENCCL, "%s", why.c_str());
+    }
+    const int rc = nccl_comm_init(&c->d.nccl_comm, opts->world, opts->nccl_unique_id, opts->rank);
+    if (rc != 0) {
+      mabd_destroy(c);
+      return fail(nullptr, MABD_ENCCL, "ncclCommInitRank: %s", nccl_err(rc));
+    }
+  }
   *out = c;
   return MABD_OK;
 }
@@ -160,6 +172,13 @@ mabd_status mabd_get_state(mabd_handle c, double* q_out, double* qd_out, int out
   if (!c) return fail(nullptr, MABD_EINVAL, "NULL handle");
   CUDA_TRY(c, cudaSetDevice(c->device));
   const int64_t n = c->plan.n;
+  if (c->plan.use_nccl) {  // every rank advanced only its windows: share them (outside any timed loop)
+    std::vector<std::pair<int64_t, int64_t>> ranges;
+    for (const auto& P : c->plan.parts) ranges.push_back({P.win_lo * SEG, P.win_hi * SEG});
+    int rc = nccl_bcast_ranges(c->d.nccl_comm, c->d.b.q, ranges, c->d.b.ld, 12, c->stream);
+    if (rc == 0) rc = nccl_bcast_ranges(c->d.nccl_comm, c->d.b.qd, ranges, c->d.b.ld, 12, c->stream);
+    if (rc != 0) return fail(c, MABD_ENCCL, "state broadcast: %s", nccl_err(rc));
+  }
   double* dq = out_on_device ? q_out : (q_out ? c->d.io : nullptr);
   double* dqd = out_on_device ? qd_out : (qd_out ? c->d.io + 12 * n : nullptr);
   CUDA_TRY(c, launch_gather(c->d.b.q, c->d.b.qd, c->d.b.ld, c->d.perm, n, dq, dqd, c->stream));
@@ -217,10 +236,41 @@ mabd_status mabd_solver_stats(mabd_handle c, int64_t* last_iterations) {
   return MABD_OK;
 }
 
+mabd_status mabd_nccl_unique_id(void* out, size_t bytes) {
+  if (!out || bytes < 128) return fail(nullptr, MABD_EINVAL, "need a 128-byte buffer");
+  std::string why;
+  if (!nccl_load(&why)) return fail(nullptr, MABD_ENCCL, "%s", why.c_str());
+  const int rc = nccl_unique_id(out);
+  if (rc != 0) return fail(nullptr, MABD_ENCCL, "ncclGetUniqueId: %s", nccl_err(rc));
+  return MABD_OK;
+}
+
+mabd_status mabd_partition_info(const mabd_bodies* bodies, const mabd_joints* joints, const mabd_options* opts,
+                                int64_t* out, int64_t n_out) {
+  if (!out || n_out < 10) return fail(nullptr, MABD_EINVAL, "need 10 output slots");
+  Plan p;
+  std::string msg;
+  mabd_status st = build_plan(bodies, joints, opts, &p, &msg);
+  if (st != MABD_OK) return fail(nullptr, st, "%s", msg.c_str());
+  const int r = opts && opts->world > 1 ? opts->rank : 0;
+  out[0] = p.n_parts;
+  out[1] = p.n_windows;
+  out[2] = p.n_long;
+  if (p.n_parts > 1) {
+    const auto& P = p.parts[r];
+    out[3] = P.win_lo; out[4] = P.win_hi; out[5] = P.long_lo; out[6] = P.long_hi;
+    out[7] = P.left_open; out[8] = P.right_open; out[9] = P.n2;
+  } else {
+    out[3] = 0; out[4] = p.n_windows; out[5] = 0; out[6] = p.n_long; out[7] = 0; out[8] = 0; out[9] = 0;
+  }
+  return MABD_OK;
+}
+
 mabd_status mabd_destroy(mabd_handle c) {
   if (!c) return MABD_OK;
   cudaSetDevice(c->device);
   if (c->stream) cudaStreamSynchronize(c->stream);
+  nccl_comm_destroy(c->d.nccl_comm);
   if (c->own_ws && c->ws) cudaFree(c->ws);
   if (c->h_err) cudaFreeHost(c->h_err);
   delete c;

@@ -30,8 +30,25 @@ struct BtdArgs {
   Top* top_out;                // REDUCE: one per window
   const double* lam_in;        // FINISH: level L+1 λ, one per window
   double* lam_out;             // FUSED/FINISH: λ per unknown
+  int32_t right_open;          // multi-part: the last unknown couples to the next part's first unknown
+  const double* lam_remote;    // FINISH with right_open: λ of that remote unknown
   StepConsts k;
 };
+
+// Sequential reduction of one part's n ≤ 256 unknowns onto {its first unknown, the next part's first unknown}
+// (multi-part chains; see mabd_chain.cu "parts").
+struct SeqArgs {
+  const Top* top_in;           // tops of the level below, one per unknown
+  int32_t n;
+  int32_t right_open;
+  Top* top_out;                // the part's top
+  double* scratch;             // [n][27]: D'⁻¹ (6), X (9), B (9), r' (3) per eliminated unknown
+  const double* lam_ends;      // FINISH: λ of unknown 0 at [0..2], of the remote unknown at [3..5]
+  double* lam_out;             // FINISH: λ per unknown
+  StepConsts k;
+};
+cudaError_t launch_seq_top(const SeqArgs& a, cudaStream_t st);
+cudaError_t launch_seq_finish(const SeqArgs& a, cudaStream_t st);
 
 struct TreeArgs {
   BodyArrays b;

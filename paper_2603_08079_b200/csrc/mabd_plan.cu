@@ -61,7 +61,8 @@ static mabd_status validate(const mabd_bodies* B, const mabd_joints* J, const ma
   if (o) {
     if (o->newton_iters != 0 && o->newton_iters != 1)
       return *msg = "newton_iters must be 1 in this version", MABD_EUNSUPPORTED;
-    if (o->world > 1) return *msg = "world > 1 is not supported by this build", MABD_EUNSUPPORTED;
+    if (o->world > 1 && (o->rank < 0 || o->rank >= o->world)) return *msg = "rank outside [0, world)", MABD_EINVAL;
+    if (o->world > 256) return *msg = "world > 256", MABD_EINVAL;
   }
   for (int64_t i = 0; i < B->n; ++i) {
     const double* m = B->mbar + 10 * i;
@@ -308,6 +309,69 @@ static bool chain_build(const mabd_joints* J, int64_t n, Plan* p, std::vector<in
   return true;
 }
 
+// ------------------------------------------------------------------------------------------ chain parts
+// W parts own contiguous window ranges (≈ nw/W each). A boundary may split a long chain; the part on its left
+// is then "right-open" and must hold ≤ 256 or a multiple of 256 long windows, so that its last BTD window ends
+// exactly on the next part's first slot (the boundary is moved left until that holds). Per step each part
+// reduces its long windows to a 2-equation top (BTD level, then a sequential top); the W tops form a
+// block-tridiagonal system solved redundantly after one all-gather.
+static bool partition_chain(Plan* p, int W, int rank, bool emulate, std::string* msg) {
+  p->n_parts = W;
+  p->parts.clear();
+  p->local_windows.clear();
+  p->local_long.clear();
+  p->part_left_open.assign(W, 0);
+  if (W <= 1) {
+    p->part_lo = 0;
+    p->part_hi = 1;
+    return true;
+  }
+  const int64_t nw = p->n_windows;
+  std::vector<int64_t> long_before(nw + 1, 0);  // long windows in [0, w)
+  for (int64_t w = 0; w < nw; ++w) long_before[w + 1] = long_before[w] + ((p->seg_flags[w] & SEG_LONG) ? 1 : 0);
+  auto splits = [&](int64_t b) { return b > 0 && b < nw && (p->seg_flags[b] & SEG_LEFT_IFACE); };
+  std::vector<int64_t> bnd(W + 1, 0);
+  bnd[W] = nw;
+  for (int q = 1; q < W; ++q) {
+    int64_t b = std::max<int64_t>((int64_t)((double)q * nw / W + 0.5), bnd[q - 1]);
+    b = std::min(b, nw);
+    while (splits(b)) {
+      const int64_t n1 = long_before[b] - long_before[bnd[q - 1]];
+      if (n1 <= SEG || n1 % SEG == 0) break;
+      --b;
+    }
+    bnd[q] = b;
+  }
+  for (int q = 0; q < W; ++q) {
+    Plan::Part P;
+    P.win_lo = bnd[q];
+    P.win_hi = bnd[q + 1];
+    P.long_lo = long_before[P.win_lo];
+    P.long_hi = long_before[P.win_hi];
+    P.left_open = splits(P.win_lo) ? 1 : 0;
+    P.right_open = splits(P.win_hi) ? 1 : 0;
+    P.n1 = P.long_hi - P.long_lo;
+    P.btd1 = P.n1 > SEG;
+    P.n2 = P.btd1 ? (P.n1 + SEG - 1) / SEG : P.n1;
+    if (P.n2 > SEG) return *msg = "a part holds more than 65,536 long-chain segments", false;
+    if (P.right_open && P.btd1 && P.n1 % SEG != 0) return *msg = "internal: unaligned right-open part", false;
+    p->part_left_open[q] = P.left_open;
+    if (P.left_open && P.n1 > 0) p->left_iface[P.long_lo] = 0;  // the left part enters via the rank-level system
+    p->parts.push_back(P);
+  }
+  p->part_lo = emulate ? 0 : rank;
+  p->part_hi = emulate ? W : rank + 1;
+  for (int q = p->part_lo; q < p->part_hi; ++q) {
+    for (int64_t w = p->parts[q].win_lo; w < p->parts[q].win_hi; ++w) p->local_windows.push_back((int32_t)w);
+    for (int64_t u = p->parts[q].long_lo; u < p->parts[q].long_hi; ++u) p->local_long.push_back(p->long_list[u]);
+  }
+  int lps = 1 + 1 + 1;  // chain pass 1, global solve, chain finish
+  for (int q = p->part_lo; q < p->part_hi; ++q)
+    if (p->parts[q].n1 > 0) lps += 2 + (p->parts[q].btd1 ? 2 : 0);
+  p->launches_per_step = lps;
+  return true;
+}
+
 // ------------------------------------------------------------------------------------------ build_plan
 mabd_status build_plan(const mabd_bodies* B, const mabd_joints* J, const mabd_options* o, Plan* p, std::string* msg) {
   mabd_status st = validate(B, J, o, msg);
@@ -326,7 +390,12 @@ mabd_status build_plan(const mabd_bodies* B, const mabd_joints* J, const mabd_op
   bool ok = false;
   if (req == 0 || req == MABD_SOLVER_CHAIN) {
     ok = chain_build(J, B->n, p, &pos, &why);
-    if (ok) p->solver = MABD_SOLVER_CHAIN;
+    if (ok) {
+      p->solver = MABD_SOLVER_CHAIN;
+      const int W = o && o->world > 1 ? o->world : 1;
+      p->use_nccl = W > 1 && o->nccl_unique_id != nullptr;
+      if (!partition_chain(p, W, o ? o->rank : 0, W > 1 && !p->use_nccl, msg)) return MABD_EINVAL;
+    }
     if (!ok && req == MABD_SOLVER_CHAIN) return *msg = "chain solver requested: " + why, MABD_EINVAL;
   }
   if (!ok && (req == 0 || req == MABD_SOLVER_TREE)) {
@@ -346,6 +415,9 @@ mabd_status build_plan(const mabd_bodies* B, const mabd_joints* J, const mabd_op
     *msg = "topology not supported by this build (" + why + ")";
     return MABD_EUNSUPPORTED;
   }
+  if (o && o->world > 1 && p->solver != MABD_SOLVER_CHAIN)
+    return *msg = "world > 1 is implemented for the chain solver only (run tree/sparse scenes as replicas)",
+           MABD_EUNSUPPORTED;
   // per-position arrays
   const int64_t ld = p->ld;
   p->perm.assign(B->n, 0);
@@ -394,9 +466,30 @@ mabd_status build_plan(const mabd_bodies* B, const mabd_joints* J, const mabd_op
     f.tops.clear();
     f.lams.clear();
     f.tops.push_back(take(sizeof(Top) * std::max<int64_t>(1, p->n_long)));
-    for (const BtdLevel& L : p->levels) {
-      f.lams.push_back(take(sizeof(double) * 3 * L.n_u));
-      if (!L.fused) f.tops.push_back(take(sizeof(Top) * L.windows));
+    if (p->n_parts <= 1) {
+      for (const BtdLevel& L : p->levels) {
+        f.lams.push_back(take(sizeof(double) * 3 * L.n_u));
+        if (!L.fused) f.tops.push_back(take(sizeof(Top) * L.windows));
+      }
+    } else {
+      f.lams.push_back(take(sizeof(double) * 3 * (p->n_long + 1)));  // λ of every long window (+ one spare)
+      f.all_tops = take(sizeof(Top) * p->n_parts);
+      f.lam_g = take(sizeof(double) * 3 * (p->n_parts + 1));
+      f.plo = take(sizeof(int32_t) * p->n_parts);
+      f.lwin = take(sizeof(int32_t) * std::max<size_t>(1, p->local_windows.size()));
+      f.llong = take(sizeof(int32_t) * std::max<size_t>(1, p->local_long.size()));
+      f.p_tops1.assign(p->n_parts, 0);
+      f.p_lam2.assign(p->n_parts, 0);
+      f.p_scr.assign(p->n_parts, 0);
+      for (int q = p->part_lo; q < p->part_hi; ++q) {
+        const Plan::Part& P = p->parts[q];
+        if (P.n1 == 0) continue;
+        if (P.btd1) {
+          f.p_tops1[q] = take(sizeof(Top) * P.n2);
+          f.p_lam2[q] = take(sizeof(double) * 3 * P.n2);
+        }
+        f.p_scr[q] = take(sizeof(double) * 27 * (P.n2 + 1));
+      }
     }
   }
   if (p->solver == MABD_SOLVER_TREE) {
@@ -480,6 +573,36 @@ cudaError_t upload_plan(const Plan& p, char* ws, cudaStream_t st, DevPtrs* d) {
     d->lams.clear();
     for (size_t o : f.tops) d->tops.push_back((Top*)(ws + o));
     for (size_t o : f.lams) d->lams.push_back((double*)(ws + o));
+    if (p.n_parts > 1) {
+      d->all_tops = (Top*)(ws + f.all_tops);
+      d->lam_g = (double*)(ws + f.lam_g);
+      d->part_left_open = (int32_t*)(ws + f.plo);
+      d->local_windows = (int32_t*)(ws + f.lwin);
+      d->local_long = (int32_t*)(ws + f.llong);
+      if ((e = put(d->part_left_open, p.part_left_open, st))) return e;
+      if ((e = put(d->local_windows, p.local_windows, st))) return e;
+      if ((e = put(d->local_long, p.local_long, st))) return e;
+      // parts without long windows keep an identity top (their rank-level unknown gets λ = 0)
+      std::vector<Top> ident(p.n_parts);
+      for (Top& T : ident) {
+        std::memset(&T, 0, sizeof(T));
+        T.D0[0] = T.D0[3] = T.D0[5] = 1.0;
+        T.D1[0] = T.D1[3] = T.D1[5] = 1.0;
+      }
+      if ((e = put(d->all_tops, ident, st))) return e;
+      if ((e = cudaMemsetAsync(d->lam_g, 0, sizeof(double) * 3 * (p.n_parts + 1), st))) return e;
+      d->p_tops1.assign(p.n_parts, nullptr);
+      d->p_lam2.assign(p.n_parts, nullptr);
+      d->p_scr.assign(p.n_parts, nullptr);
+      for (int q = p.part_lo; q < p.part_hi; ++q) {
+        if (p.parts[q].n1 == 0) continue;
+        if (p.parts[q].btd1) {
+          d->p_tops1[q] = (Top*)(ws + f.p_tops1[q]);
+          d->p_lam2[q] = (double*)(ws + f.p_lam2[q]);
+        }
+        d->p_scr[q] = (double*)(ws + f.p_scr[q]);
+      }
+    }
   }
   if (p.solver == MABD_SOLVER_TREE) {
     const TreePlan& t = p.tree;
@@ -538,8 +661,8 @@ cudaError_t upload_plan(const Plan& p, char* ws, cudaStream_t st, DevPtrs* d) {
     A.vv = (double*)(ws + f.s_vv);
     A.part = (double*)(ws + f.s_part);
     A.iters = (int32_t*)(ws + f.s_iters);
-    A.tol = 1e-13;
-    A.max_iter = 100000;
+    A.tol = 1e-12;
+    A.max_iter = 50000;
     if ((e = put((int32_t*)A.pa, sp.pa, st))) return e;
     if ((e = put((int32_t*)A.pb, sp.pb, st))) return e;
     if ((e = put((double*)A.py, sp.py, st))) return e;
@@ -561,6 +684,88 @@ __global__ void err_reset_kernel(int32_t* e) {
 cudaError_t reset_err(const DevPtrs& d, cudaStream_t st) {
   err_reset_kernel<<<1, 1, 0, st>>>(d.err);
   return cudaGetLastError();
+}
+
+// one step of a multi-part chain scene for the parts [part_lo, part_hi) of this process
+static cudaError_t launch_step_parts(const Plan& p, const DevPtrs& d, ChainArgs a, cudaStream_t st) {
+  cudaError_t e;
+  const StepConsts& k = a.k;
+  a.seg_list = d.local_windows;
+  if ((e = launch_chain(a, (int)p.local_windows.size(), false, st))) return e;
+  for (int q = p.part_lo; q < p.part_hi; ++q) {
+    const Plan::Part& P = p.parts[q];
+    if (P.n1 == 0) continue;
+    const Top* lvl = d.tops[0] + P.long_lo;
+    if (P.btd1) {
+      BtdArgs b{};
+      b.top_in = lvl;
+      b.left_iface = d.left_iface + P.long_lo;
+      b.n_u = P.n1;
+      b.mode = BTD_REDUCE;
+      b.top_out = d.p_tops1[q];
+      b.right_open = P.right_open;
+      b.k = k;
+      if ((e = launch_btd(b, (int)P.n2, st))) return e;
+      lvl = d.p_tops1[q];
+    }
+    SeqArgs sq{};
+    sq.top_in = lvl;
+    sq.n = (int32_t)P.n2;
+    sq.right_open = P.right_open;
+    sq.top_out = d.all_tops + q;
+    sq.scratch = d.p_scr[q];
+    sq.k = k;
+    if ((e = launch_seq_top(sq, st))) return e;
+  }
+  if (p.use_nccl) {
+    const int rc = nccl_allgather_doubles(d.nccl_comm, (double*)d.all_tops, sizeof(Top) / sizeof(double), p.part_lo, st);
+    if (rc != 0) return cudaErrorUnknown;
+  }
+  {
+    BtdArgs b{};
+    b.top_in = d.all_tops;
+    b.left_iface = d.part_left_open;
+    b.n_u = p.n_parts;
+    b.mode = BTD_FUSED;
+    b.lam_out = d.lam_g;
+    b.k = k;
+    if ((e = launch_btd(b, 1, st))) return e;
+  }
+  double* lam1 = d.lams[0];
+  for (int q = p.part_lo; q < p.part_hi; ++q) {
+    const Plan::Part& P = p.parts[q];
+    if (P.n1 == 0) continue;
+    if (P.right_open) {  // λ of the next part's first long window, for this part's last segment
+      if ((e = cudaMemcpyAsync(lam1 + 3 * P.long_hi, d.lam_g + 3 * (q + 1), 3 * sizeof(double),
+                               cudaMemcpyDeviceToDevice, st)))
+        return e;
+    }
+    SeqArgs sq{};
+    sq.top_in = P.btd1 ? d.p_tops1[q] : d.tops[0] + P.long_lo;
+    sq.n = (int32_t)P.n2;
+    sq.right_open = P.right_open;
+    sq.scratch = d.p_scr[q];
+    sq.lam_ends = d.lam_g + 3 * q;
+    sq.lam_out = P.btd1 ? d.p_lam2[q] : lam1 + 3 * P.long_lo;
+    sq.k = k;
+    if ((e = launch_seq_finish(sq, st))) return e;
+    if (P.btd1) {
+      BtdArgs b{};
+      b.top_in = d.tops[0] + P.long_lo;
+      b.left_iface = d.left_iface + P.long_lo;
+      b.n_u = P.n1;
+      b.mode = BTD_FINISH;
+      b.lam_in = d.p_lam2[q];
+      b.lam_out = lam1 + 3 * P.long_lo;
+      b.right_open = P.right_open;
+      b.lam_remote = d.lam_g + 3 * (q + 1);
+      b.k = k;
+      if ((e = launch_btd(b, (int)P.n2, st))) return e;
+    }
+  }
+  a.seg_list = d.local_long;
+  a.lam_in = lam1;
+  return launch_chain(a, (int)p.local_long.size(), true, st);
 }
 
 cudaError_t launch_step(const Plan& p, const DevPtrs& d, double h, int32_t step, cudaStream_t st) {
@@ -585,12 +790,13 @@ cudaError_t launch_step(const Plan& p, const DevPtrs& d, double h, int32_t step,
   a.top_out = d.tops.empty() ? nullptr : d.tops[0];
   a.lam_in = d.lams.empty() ? nullptr : d.lams[0];
   a.k = k;
+  if (p.n_parts > 1) return launch_step_parts(p, d, a, st);
   cudaError_t e = launch_chain(a, (int)p.n_windows, false, st);
   if (e != cudaSuccess || p.n_long == 0) return e;
   const int nl = (int)p.levels.size();
   // levels i = 0..nl-1 (BTD level i+1): REDUCE for i < nl-1, FUSED at nl-1
   for (int i = 0; i < nl; ++i) {
-    BtdArgs b;
+    BtdArgs b{};
     b.top_in = d.tops[i];
     b.left_iface = (i == 0) ? d.left_iface : nullptr;
     b.n_u = p.levels[i].n_u;
@@ -602,7 +808,7 @@ cudaError_t launch_step(const Plan& p, const DevPtrs& d, double h, int32_t step,
     if ((e = launch_btd(b, (int)p.levels[i].windows, st)) != cudaSuccess) return e;
   }
   for (int i = nl - 2; i >= 0; --i) {
-    BtdArgs b;
+    BtdArgs b{};
     b.top_in = d.tops[i];
     b.left_iface = (i == 0) ? d.left_iface : nullptr;
     b.n_u = p.levels[i].n_u;

@@ -62,7 +62,18 @@ struct Plan {
   std::vector<double> geo;           // [ng][6]
   std::vector<int32_t> seg_flags, seg_red, long_list, left_iface;
   int64_t n_long = 0;
-  std::vector<BtdLevel> levels;      // levels[0] is BTD level 1
+  std::vector<BtdLevel> levels;      // levels[0] is BTD level 1 (single part)
+  // multi-part chains (multi-GPU, or W parts emulated in one process): see partition_chain()
+  struct Part {
+    int64_t win_lo = 0, win_hi = 0, long_lo = 0, long_hi = 0;
+    int32_t left_open = 0, right_open = 0;
+    int64_t n1 = 0, n2 = 0;  // level-1 unknowns (long windows), unknowns of the sequential top
+    bool btd1 = false;       // one BTD level (n1 > 256) before the sequential top
+  };
+  int32_t n_parts = 1, part_lo = 0, part_hi = 1;
+  bool use_nccl = false;
+  std::vector<Part> parts;
+  std::vector<int32_t> local_windows, local_long, part_left_open;
   // tree solver
   TreePlan tree;
   // sparse solver
@@ -73,6 +84,8 @@ struct Plan {
     size_t q, qd, rs, mat_id, mscale, mats, hinv, perm, io, err;
     size_t slot_info, geo, seg_flags, seg_red, long_list, left_iface;
     std::vector<size_t> tops, lams;  // per BTD level: tops[0] = chain tops (n_long), lams[i] = level i+1 λ
+    size_t all_tops, lam_g, plo, lwin, llong;
+    std::vector<size_t> p_tops1, p_lam2, p_scr;
     size_t t_up, t_coff, t_cj, t_wsoff, t_jnpts, t_jchd, t_jy, t_goff, t_glp, t_glo, t_shat, t_rhat, t_lam, t_bscr,
         t_ws;
     size_t s_pa, s_pb, s_py, s_incoff, s_inc, s_vec, s_vv, s_part, s_iters;
@@ -91,9 +104,25 @@ struct DevPtrs {
   int32_t *seg_flags = nullptr, *seg_red = nullptr, *long_list = nullptr, *left_iface = nullptr;
   std::vector<Top*> tops;
   std::vector<double*> lams;
+  Top* all_tops = nullptr;
+  double* lam_g = nullptr;
+  int32_t *part_left_open = nullptr, *local_windows = nullptr, *local_long = nullptr;
+  std::vector<Top*> p_tops1;
+  std::vector<double*> p_lam2, p_scr;
+  void* nccl_comm = nullptr;
   TreeArgs tree{};                   // device pointers of the tree solver
   SparseArgs sparse{};               // device pointers of the sparse solver
 };
+
+// NCCL, loaded on demand (mabd_nccl.cu)
+bool nccl_load(std::string* err);
+int nccl_unique_id(void* out128);
+int nccl_comm_init(void** comm, int world, const void* id128, int rank);
+int nccl_allgather_doubles(void* comm, double* buf, size_t count_per_rank, int rank, cudaStream_t st);
+int nccl_bcast_ranges(void* comm, double* base, const std::vector<std::pair<int64_t, int64_t>>& ranges,
+                      int64_t ld, int ncomp, cudaStream_t st);
+void nccl_comm_destroy(void* comm);
+const char* nccl_err(int code);
 
 mabd_status build_plan(const mabd_bodies* bodies, const mabd_joints* joints, const mabd_options* opts, Plan* p,
                        std::string* msg);

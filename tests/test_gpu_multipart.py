@@ -1,0 +1,66 @@
+"""Multi-part (multi-GPU) chain path, emulated on one GPU: world = W with no NCCL id runs the W parts in one
+process with the same arithmetic (per-part reduction to a top system, rank-level solve, back substitution),
+the all-gather being a no-op. Parity against the oracle and against the single-part path."""
+import ctypes
+
+import numpy as np
+import pytest
+
+import oracle as O
+from mabd_scenes import generators as G
+
+from test_gpu_chain import TOL1, _concat
+
+pytestmark = pytest.mark.gpu
+
+
+def run(sc, nsteps, world=1):
+    import torch
+    from paper_2603_08079_b200 import binding as B
+    sim = B.Simulator.from_scene(sc, world=world)
+    sim.prefactor(sc.h)
+    sim.step(sc.h, nsteps)
+    q, qd = sim.get_state()
+    info = sim.query()
+    sim.close()
+    return q, info
+
+
+@pytest.mark.parametrize("world", [2, 3, 8])
+def test_long_chain_parts_vs_oracle(cuda_ok, world):
+    sc = G.cfg3_long_chain(col_len=2000, n_cols=35, tail=7)   # 70,007 bodies, 274 segments
+    q1, info = run(sc, 2, world)
+    q_o, _ = O.simulate(sc, 2)
+    assert O.rel_err(q1, q_o) <= 1e-9
+    q_single, _ = run(sc, 2, 1)
+    assert O.rel_err(q1, q_single) <= 1e-11
+    assert info["launches_per_step"] > 3
+
+
+@pytest.mark.parametrize("world", [2, 5])
+def test_mixed_chains_parts(cuda_ok, world):
+    parts = [G.random_chain(700, seed=1, vel=0.2, end_anchor=True), G.cfg2_batched_chains(9, 100),
+             G.random_chain(1300, seed=2, vel=0.2), G.random_chain(40, seed=3)]
+    sc = _concat(parts)
+    q1, _ = run(sc, 3, world)
+    q_o, _ = O.simulate(sc, 3)
+    assert O.rel_err(q1, q_o) <= 1e-9
+
+
+@pytest.mark.slow
+@pytest.mark.parametrize("world", [2, 8])
+def test_cfg3_full_size_parts(cuda_ok, world):
+    """The 1,048,576-body chain split into W parts (part sizes are multiples of 256 segments)."""
+    sc = G.cfg3_long_chain()
+    q_w, _ = run(sc, 1, world)
+    q_1, _ = run(sc, 1, 1)
+    assert O.rel_err(q_w, q_1) <= 1e-11
+    assert O.constraint_residual(sc, q_w) <= 1e-10
+
+
+@pytest.mark.slow
+def test_cfg3_full_size_one_step_vs_oracle(cuda_ok):
+    sc = G.cfg3_long_chain()
+    q_g, _ = run(sc, 1, 1)
+    q_o, _ = O.step(sc, sc.q0, sc.qd0, sc.h, route="blocklu")
+    assert O.rel_err(q_g, q_o) <= TOL1
