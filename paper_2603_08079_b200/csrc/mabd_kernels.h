@@ -74,6 +74,31 @@ struct TreeArgs {
 
 enum : int32_t { TREE_UP = 0, TREE_DOWN = 1, TREE_BOTH = 2 };
 
+// Multifrontal Cholesky of the dual S (sparse solver, mabd_sparse.cu). Fronts are dense column-major f×f
+// matrices (f = 3·(own + boundary points)); own columns first, then the boundary rows, both in elimination order.
+struct MfArgs {
+  double* F;                   // all fronts
+  const int64_t* foff;         // [nnode] front offset (doubles)
+  const int32_t* fdim;         // [nnode] f (scalar rows)
+  const int32_t* nown;         // [nnode] own scalar columns (3 · own points)
+  const int32_t* own_first;    // [nnode] first elimination position of the own points
+  const int32_t* ch_off;       // [nnode+1] CSR of the assembly-tree children
+  const int32_t* ch;
+  const int32_t* ea_off;       // [nnode] offset into ea_map
+  const int32_t* ea_map;       // per node: front block position in its parent of each boundary point
+  const int32_t* bnd_off;      // [nnode] offset into bnd
+  const int32_t* bnd;          // boundary points (elimination positions, ascending)
+  const int32_t* ipos;         // elimination position → point
+  const int32_t* ablk;         // [nblk][3] assembly blocks: node, row block, column block
+  const int32_t* acoff;        // [nblk+1] CSR into acon
+  const int32_t* acon;         // [ncon][2] contributions: 2·(row point)+side, 2·(column point)+side
+  int64_t nblk;
+  double* linv;                // inverse of every 64×64 diagonal Cholesky block of the large fronts
+  const int64_t* loff;         // [nnode] offset into linv (chunk c of node at loff + 4096·c)
+  double* wvec;                // [Σf] per-node solve vectors
+  const int64_t* woff;         // [nnode]
+};
+
 struct SparseArgs {
   BodyArrays b;
   const HinvBlk* hinv_tab;     // per material, or null (per-body mass scale)
@@ -83,12 +108,10 @@ struct SparseArgs {
   const double* py;            // [np][6] ȳ_a, ȳ_b (world point when pb < 0)
   const int32_t* inc_off;      // [n+1] CSR body → incident points (2·point + side)
   const int32_t* inc;
-  double *rhs, *dinv, *lam, *res, *zz, *pp, *ap;  // component-major [3 or 6][np]
+  double *rhs, *lam, *res, *dl, *yy;  // component-major [3][np]: r = C(q̃), λ, residual, correction, solve scratch
   double* vv;                  // [12][n]
-  double* part;                // per-block partial sums
-  int32_t* iters;              // iterations of the last solve
-  double tol;
-  int32_t max_iter;
+  int32_t* iters;              // refinement passes of the last solve
+  MfArgs mf;
   StepConsts k;
 };
 cudaError_t launch_tree(const TreeArgs& a, int ngroups, int mode, cudaStream_t st);

@@ -407,7 +407,7 @@ mabd_status build_plan(const mabd_bodies* B, const mabd_joints* J, const mabd_op
   }
   if (!ok && (req == 0 || req == MABD_SOLVER_SPARSE)) {
     std::string why3;
-    ok = sparse_build(J, B->n, p, &pos, &why3);
+    ok = sparse_build(B, J, p, &pos, &why3);
     if (ok) p->solver = MABD_SOLVER_SPARSE;
     if (!ok) why += "; " + why3;
   }
@@ -511,19 +511,7 @@ mabd_status build_plan(const mabd_bodies* B, const mabd_joints* J, const mabd_op
     f.t_bscr = take(sizeof(double) * 21 * n);
     f.t_ws = take(sizeof(double) * std::max<int64_t>(1, t.ws_total));
   }
-  if (p->solver == MABD_SOLVER_SPARSE) {
-    const SparsePlan& sp = p->sparse;
-    const int64_t np = std::max<int64_t>(1, sp.np), n = B->n;
-    f.s_pa = take(sizeof(int32_t) * np);
-    f.s_pb = take(sizeof(int32_t) * np);
-    f.s_py = take(sizeof(double) * 6 * np);
-    f.s_incoff = take(sizeof(int32_t) * (n + 1));
-    f.s_inc = take(sizeof(int32_t) * std::max<size_t>(1, sp.inc.size()));
-    f.s_vec = take(sizeof(double) * 27 * np);  // rhs 3, dinv 6, λ 3, r 3, z 3, p 3, Ap 3 (+3 spare)
-    f.s_vv = take(sizeof(double) * 12 * n);
-    f.s_part = take(sizeof(double) * 4 * SPARSE_MAX_BLOCKS);
-    f.s_iters = take(sizeof(int32_t) * 4);
-  }
+  if (p->solver == MABD_SOLVER_SPARSE) sparse_layout(p, take);
   p->workspace_bytes = cur;
   return MABD_OK;
 }
@@ -637,38 +625,7 @@ cudaError_t upload_plan(const Plan& p, char* ws, cudaStream_t st, DevPtrs* d) {
     if ((e = put((int32_t*)A.glev_off, t.glev_off, st))) return e;
     if ((e = cudaMemsetAsync(A.lam, 0, sizeof(double) * 6 * std::max<int64_t>(1, p.n_joints), st))) return e;
   }
-  if (p.solver == MABD_SOLVER_SPARSE) {
-    const SparsePlan& sp = p.sparse;
-    SparseArgs& A = d->sparse;
-    const int64_t np = std::max<int64_t>(1, sp.np);
-    A.b = d->b;
-    A.hinv_tab = p.mscale.empty() ? d->hinv : nullptr;
-    A.n = p.n;
-    A.np = sp.np;
-    A.pa = (const int32_t*)(ws + f.s_pa);
-    A.pb = (const int32_t*)(ws + f.s_pb);
-    A.py = (const double*)(ws + f.s_py);
-    A.inc_off = (const int32_t*)(ws + f.s_incoff);
-    A.inc = (const int32_t*)(ws + f.s_inc);
-    double* v = (double*)(ws + f.s_vec);
-    A.rhs = v;
-    A.dinv = v + 3 * np;
-    A.lam = v + 9 * np;
-    A.res = v + 12 * np;
-    A.zz = v + 15 * np;
-    A.pp = v + 18 * np;
-    A.ap = v + 21 * np;
-    A.vv = (double*)(ws + f.s_vv);
-    A.part = (double*)(ws + f.s_part);
-    A.iters = (int32_t*)(ws + f.s_iters);
-    A.tol = 1e-12;
-    A.max_iter = 50000;
-    if ((e = put((int32_t*)A.pa, sp.pa, st))) return e;
-    if ((e = put((int32_t*)A.pb, sp.pb, st))) return e;
-    if ((e = put((double*)A.py, sp.py, st))) return e;
-    if ((e = put((int32_t*)A.inc_off, sp.inc_off, st))) return e;
-    if ((e = put((int32_t*)A.inc, sp.inc, st))) return e;
-  }
+  if (p.solver == MABD_SOLVER_SPARSE) return sparse_upload(p, ws, st, d);
   return cudaSuccess;
 }
 

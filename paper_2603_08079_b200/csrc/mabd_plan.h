@@ -2,6 +2,7 @@
 #pragma once
 #include <cuda_runtime.h>
 
+#include <functional>
 #include <string>
 #include <vector>
 
@@ -38,10 +39,43 @@ struct TreePlan {
   int64_t ws_total = 0;
 };
 
+// Sparse plan: constraint points, body → point incidence, and the multifrontal symbolic factorization of the
+// dual (nested dissection on the bodies' initial positions; see mabd_sparse.cu).
 struct SparsePlan {
   int64_t np = 0;
   std::vector<int32_t> pa, pb, inc_off, inc;
   std::vector<double> py;
+  // multifrontal symbolic
+  int32_t nnode = 0;
+  std::vector<int32_t> epos, ipos;                       // point ↔ elimination position
+  std::vector<int32_t> own_first, nown, fdim, height, parent, ch_off, ch;
+  std::vector<int64_t> foff, woff;
+  std::vector<int32_t> bnd_off, bnd, ea_off, ea_map;
+  std::vector<int32_t> ablk, acoff, acon;
+  int64_t front_doubles = 0, w_doubles = 0;
+  double flops = 0.0;                                    // numeric factorization flops per step
+  // launch schedule, by assembly-tree height
+  struct Panel { int64_t potrf, n_potrf, trsm, n_trsm, syrk, n_syrk; };  // offsets into tasks
+  struct Level {
+    int64_t nodes, n_nodes;        // all nodes of the level (solves), into lev_nodes
+    int64_t small, n_small;        // fronts factored in shared memory, into lev_nodes
+    int64_t big = 0, n_big = 0;    // fronts factored by panels, into lev_nodes
+    std::vector<int64_t> fwd, n_fwd, bwd, n_bwd;  // per 64-chunk solve tasks of the big fronts
+    int64_t bwdb = 0, n_bwdb = 0;  // backward boundary-product tasks
+    int32_t max_f = 0, max_f_small = 0, max_children = 0;
+    std::vector<int64_t> ea, n_ea; // per child slot: (parent, column) tasks of big parents
+    std::vector<Panel> panels;
+  };
+  std::vector<Level> levels;
+  std::vector<int32_t> lev_nodes, tasks;
+  std::vector<int64_t> loff;                             // [nnode] inverse diagonal blocks of big fronts
+  int64_t linv_doubles = 0;
+  int32_t refine = 1;                                    // iterative-refinement passes per step
+  int32_t max_f = 0;
+  size_t o_pa = 0, o_pb = 0, o_py = 0, o_incoff = 0, o_inc = 0, o_vec = 0, o_vv = 0, o_iters = 0;
+  size_t o_F = 0, o_foff = 0, o_fdim = 0, o_nown = 0, o_ownf = 0, o_choff = 0, o_ch = 0, o_eaoff = 0, o_eamap = 0,
+         o_bndoff = 0, o_bnd = 0, o_ipos = 0, o_ablk = 0, o_acoff = 0, o_acon = 0, o_linv = 0, o_w = 0, o_woff = 0,
+         o_lev = 0, o_tasks = 0, o_loff = 0;
 };
 
 struct Plan {
@@ -88,7 +122,6 @@ struct Plan {
     std::vector<size_t> p_tops1, p_lam2, p_scr;
     size_t t_up, t_coff, t_cj, t_wsoff, t_jnpts, t_jchd, t_jy, t_goff, t_glp, t_glo, t_shat, t_rhat, t_lam, t_bscr,
         t_ws;
-    size_t s_pa, s_pb, s_py, s_incoff, s_inc, s_vec, s_vv, s_part, s_iters;
   } off{};
 };
 
@@ -112,6 +145,8 @@ struct DevPtrs {
   void* nccl_comm = nullptr;
   TreeArgs tree{};                   // device pointers of the tree solver
   SparseArgs sparse{};               // device pointers of the sparse solver
+  const int32_t* sparse_lev = nullptr;    // level node lists of the sparse schedule
+  const int32_t* sparse_tasks = nullptr;  // extend-add / panel task lists
 };
 
 // NCCL, loaded on demand (mabd_nccl.cu)
@@ -136,9 +171,11 @@ bool tree_build(const mabd_joints* joints, int64_t n, Plan* p, std::vector<int64
 cudaError_t tree_step(const Plan& p, const DevPtrs& d, const StepConsts& k, cudaStream_t st);
 
 // sparse solver (mabd_sparse.cu)
-bool sparse_build(const mabd_joints* joints, int64_t n, Plan* p, std::vector<int64_t>* pos_of_body, std::string* msg);
+bool sparse_build(const mabd_bodies* bodies, const mabd_joints* joints, Plan* p, std::vector<int64_t>* pos_of_body,
+                  std::string* msg);
+void sparse_layout(Plan* p, const std::function<size_t(size_t)>& take);
+cudaError_t sparse_upload(const Plan& p, char* ws, cudaStream_t st, DevPtrs* d);
 cudaError_t sparse_init();
 cudaError_t sparse_step(const Plan& p, const DevPtrs& d, const StepConsts& k, cudaStream_t st);
-constexpr int SPARSE_MAX_BLOCKS = 148 * 8;
 
 }  // namespace mabd

@@ -1,38 +1,48 @@
-// Sparse (loops / irregular networks) solver of the M-ABD step on sm_100a.
+// Sparse (loops / irregular networks) solver of the M-ABD step on sm_100a: a multifrontal Cholesky
+// factorization of the dual, refactored every step, with iterative refinement against the exact dual.
 //
-// The dual S λ = r, S = ∇C̃ H̃⁻¹ ∇C̃ᵀ, r = C(q̃) (P:563-566 with the footnote P:459), is solved by
-// preconditioned conjugate gradients with an EXACT matrix-free product (reading A1: the dual
-// changes every step because H_j⁻¹ = diag₄(R_j) H̄⁻¹ diag₄(R_jᵀ) rotates; the paper says "any linear solver
-// like Cholesky"). Iterations run to ‖r − Sλ‖ ≤ 1e-12‖r‖, so the result agrees with a direct solve
-// to the parity tolerance. Preconditioner: the exact 3×3 diagonal blocks of S (block Jacobi).
-//
-// S·p without forming S (two passes over HBM-resident arrays per product):
-//   bodies:  v_j = H_j⁻¹ Σ_{points p on j} s_p Γ(ȳ_p)ᵀ p_p          (12 doubles per body)
-//   points:  (S p)_p = s_a Γ(ȳ_a) v_a + s_b Γ(ȳ_b) v_b
-// The whole PCG loop is one persistent cooperative kernel (grid.sync between passes); dot products are
-// reduced per block and summed by every block in a fixed order (deterministic, no floating atomics).
-#include <cooperative_groups.h>
+// The dual S λ = r, S = ∇C̃ H̃⁻¹ ∇C̃ᵀ, r = C(q̃) (P:563-566 with the footnote P:459), is solved "by any
+// linear solver like Cholesky". Its sparsity pattern is constant, its values are not: the 3×3 block
+// between constraint points p and q that share body j is s_p s_q R_j P_j(ȳ_p, ȳ_q) R_jᵀ, with the constant
+// kernel P_j = Γ(ȳ_p) H̄_j⁻¹ Γ(ȳ_q)ᵀ and the body rotation R_j of this step (reading A1). So:
+//   create (host, once):  nested-dissection ordering of the points from the bodies' initial positions, the
+//                         assembly tree, front structures, extend-add maps, and the launch schedule;
+//   every step (device):  assemble S into the fronts, factor them level by level (leaves first; small fronts
+//                         in shared memory, large ones by 64-wide panels: POTRF → TRSM → SYRK), then forward
+//                         and backward substitution, then two passes of iterative refinement with the exact
+//                         matrix-free product S·x (bodies: v_j = H_j⁻¹ Σ s Γᵀx; points: Σ s Γ v).
+// Nested dissection (geometric): the bodies of a region are split at the median of their widest coordinate;
+// points joining bodies of both halves form the separator. Two points are coupled in S only if they share a
+// body, so the halves' points are uncoupled and the separator is eliminated after both. Everything is fp64;
+// there are no floating-point atomics (extend-add runs one child slot per launch), so the step is
+// deterministic.
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <cstdlib>
+#include <cmath>
+#include <functional>
+#include <numeric>
 #include <string>
 #include <vector>
 
 #include "mabd_device.cuh"
 #include "mabd_plan.h"
 
-namespace cg = cooperative_groups;
-
 namespace mabd {
 
 constexpr int SP_THREADS = 256;
+constexpr int MF_NB = 64;          // panel width and tile size of the large-front path
+constexpr int MF_SMALL = 96;       // fronts with f ≤ MF_SMALL are factored in shared memory by one CTA
+constexpr int MF_LEAF_PTS = 12;    // nested dissection stops at regions of ≤ this many points
+constexpr int MF_REFINE = 1;       // iterative-refinement passes per step (default)
 
 __device__ __forceinline__ void sreport(const StepConsts& k, int32_t flag) {
   atomicOr(k.err, flag);
   atomicMin(k.err + 1, k.step_index);
 }
 
-// ---------------------------------------------------------------------------- per-step preparation
+// ============================================================================ per-body stages (a1, a2, a5)
 // bodies: predict; R → rs scratch, δq̃ parked in the q̇ buffer
 __global__ void sparse_predict_kernel(SparseArgs a) {
   const int64_t ld = a.b.ld;
@@ -71,11 +81,11 @@ __device__ __forceinline__ void body_R(const SparseArgs& a, int64_t j, double* R
   for (int c = 0; c < 9; ++c) R[c] = a.b.rs[c * a.b.ld + j];
 }
 
-// points: r = C(q̃) and the inverse diagonal block D_p⁻¹ of S (block-Jacobi preconditioner)
+// points: r = C(q̃) (q̃ = qⁿ + δq̃)
 __global__ void sparse_rhs_kernel(SparseArgs a) {
   const int64_t ld = a.b.ld;
   for (int64_t p = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; p < a.np; p += (int64_t)gridDim.x * blockDim.x) {
-    double D[6] = {0, 0, 0, 0, 0, 0}, r[3] = {0, 0, 0};
+    double r[3] = {0, 0, 0};
     for (int side = 0; side < 2; ++side) {
       const int64_t j = side == 0 ? a.pa[p] : a.pb[p];
       const double* y = a.py + 6 * p + 3 * side;
@@ -85,32 +95,20 @@ __global__ void sparse_rhs_kernel(SparseArgs a) {
         for (int e = 0; e < 3; ++e) r[e] += sg * y[e];
         continue;
       }
-      double qt[12], R[9], x[3], P[9], F[6];
+      double qt[12], x[3];
 #pragma unroll
       for (int c = 0; c < 12; ++c) qt[c] = a.b.q[c * ld + j] + a.b.qd[c * ld + j];
-      body_R(a, j, R);
-      HinvBlk H;
-      body_hinv(a, j, H);
       point_pos(qt, y, x);
 #pragma unroll
       for (int e = 0; e < 3; ++e) r[e] += sg * x[e];
-      pblock(H, y, y, P);
-      rot_conj_sym(R, P, F);
-#pragma unroll
-      for (int e = 0; e < 6; ++e) D[e] += F[e];
     }
-    double Di[6];
-    if (!sym_inv_spd(D, Di)) sreport(a.k, ERR_SINGULAR);
-#pragma unroll
-    for (int e = 0; e < 6; ++e) a.dinv[e * a.np + p] = Di[e];
 #pragma unroll
     for (int e = 0; e < 3; ++e) a.rhs[e * a.np + p] = r[e];
   }
 }
 
 // v_j = H_j⁻¹ Σ s Γ(ȳ)ᵀ x_p over the points incident to body j (x: [3][np] component-major)
-__device__ __forceinline__ void body_apply(const SparseArgs& a, int64_t j, const double* x, const double* z,
-                                           double beta, double* out12) {
+__device__ __forceinline__ void body_apply(const SparseArgs& a, int64_t j, const double* x, double* out12) {
   double g[12];
 #pragma unroll
   for (int c = 0; c < 12; ++c) g[c] = 0.0;
@@ -122,7 +120,7 @@ __device__ __forceinline__ void body_apply(const SparseArgs& a, int64_t j, const
     const int side = e & 1;
     double w[3], wl[3];
 #pragma unroll
-    for (int c = 0; c < 3; ++c) w[c] = z ? z[c * a.np + p] + beta * x[c * a.np + p] : x[c * a.np + p];
+    for (int c = 0; c < 3; ++c) w[c] = x[c * a.np + p];
     mat3t_vec(R, w, wl);  // body frame
     add_point_force(g, a.py + 6 * p + 3 * side, wl, side == 0 ? 1.0 : -1.0);
   }
@@ -134,179 +132,44 @@ __device__ __forceinline__ void body_apply(const SparseArgs& a, int64_t j, const
   for (int kb = 0; kb < 4; ++kb) mat3_vec(R, u + 3 * kb, out12 + 3 * kb);
 }
 
-// block reduction of NV values into part[blockIdx.x * NV + v]
-template <int NV>
-__device__ __forceinline__ void block_reduce_store(double (&v)[NV], double* part) {
-  __shared__ double red[NV][SP_THREADS / 32];
+// matrix-free S·x, pass 1 (bodies): V = H⁻¹ Jᵀ x
+__global__ void mv_body_kernel(SparseArgs a, const double* x) {
+  for (int64_t j = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; j < a.n; j += (int64_t)gridDim.x * blockDim.x) {
+    double v[12];
+    body_apply(a, j, x, v);
 #pragma unroll
-  for (int i = 0; i < NV; ++i) {
-    double x = v[i];
-#pragma unroll
-    for (int o = 16; o > 0; o >>= 1) x += __shfl_down_sync(0xffffffffu, x, o);
-    if ((threadIdx.x & 31) == 0) red[i][threadIdx.x >> 5] = x;
+    for (int c = 0; c < 12; ++c) a.vv[c * a.n + j] = v[c];
   }
-  __syncthreads();
-  if (threadIdx.x < NV) {
-    double s = 0.0;
-    for (int w = 0; w < SP_THREADS / 32; ++w) s += red[threadIdx.x][w];
-    part[blockIdx.x * NV + threadIdx.x] = s;
-  }
-  __syncthreads();
 }
-
-// every block sums the partials in the same order (deterministic). A block may start the next pass (and
-// write partials) while others still sum: each reduction kind therefore has its own buffer, and two grid
-// syncs separate consecutive uses of the same buffer.
-template <int NV>
-__device__ __forceinline__ void grid_sum(const double* part, int nblk, double* out) {
-  __shared__ double tot[NV];
-  if (threadIdx.x < NV) {
-    double s = 0.0;
-    for (int b = 0; b < nblk; ++b) s += part[b * NV + threadIdx.x];
-    tot[threadIdx.x] = s;
-  }
-  __syncthreads();
+// pass 2 (points): res = rhs − J V
+__global__ void mv_point_kernel(SparseArgs a) {
+  for (int64_t p = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; p < a.np; p += (int64_t)gridDim.x * blockDim.x) {
+    double s[3] = {0, 0, 0};
+    for (int side = 0; side < 2; ++side) {
+      const int64_t j = side == 0 ? a.pa[p] : a.pb[p];
+      if (j < 0) continue;
+      const double* y = a.py + 6 * p + 3 * side;
+      const double sg = side == 0 ? 1.0 : -1.0;
 #pragma unroll
-  for (int i = 0; i < NV; ++i) out[i] = tot[i];
-  __syncthreads();
-}
-
-__global__ void __launch_bounds__(SP_THREADS) sparse_pcg_kernel(SparseArgs a) {
-  cg::grid_group grid = cg::this_grid();
-  const int64_t tid = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-  const int64_t nth = (int64_t)gridDim.x * blockDim.x;
-  const int nblk = gridDim.x;
-  const int64_t np = a.np;
-  double* X = a.lam;   // λ
-  double* Rr = a.res;  // residual
-  double* Z = a.zz;    // preconditioned residual
-  double* Pp = a.pp;   // search direction
-  double* Ap = a.ap;
-  double* V = a.vv;    // [12][n]
-  // init: λ = 0, r = rhs, z = D⁻¹r, p = z; partials of r·z and r·r
-  {
-    double acc[2] = {0.0, 0.0};
-    for (int64_t p = tid; p < np; p += nth) {
-      double r[3], di[6], z[3];
-#pragma unroll
-      for (int e = 0; e < 3; ++e) {
-        r[e] = a.rhs[e * np + p];
-        X[e * np + p] = 0.0;
-        Rr[e * np + p] = r[e];
-      }
-#pragma unroll
-      for (int e = 0; e < 6; ++e) di[e] = a.dinv[e * np + p];
-      sym_vec(di, r, z);
-#pragma unroll
-      for (int e = 0; e < 3; ++e) {
-        Z[e * np + p] = z[e];
-        Pp[e * np + p] = z[e];
-        acc[0] += r[e] * z[e];
-        acc[1] += r[e] * r[e];
-      }
+      for (int e = 0; e < 3; ++e)
+        s[e] += sg * (a.vv[(0 + e) * a.n + j] * y[0] + a.vv[(3 + e) * a.n + j] * y[1] +
+                      a.vv[(6 + e) * a.n + j] * y[2] + a.vv[(9 + e) * a.n + j]);
     }
-    block_reduce_store<2>(acc, a.part);
-  }
-  grid.sync();
-  double s2[2];
-  grid_sum<2>(a.part, nblk, s2);
-  double rz = s2[0];
-  const double bnorm2 = s2[1];
-  const double tol2 = a.tol * a.tol * bnorm2;
-  double beta = 0.0, last_r2 = bnorm2;
-  bool first = true;
-  int it = 0;
-  if (bnorm2 > 0.0) {
-    for (it = 0; it < a.max_iter; ++it) {
-      // pass 1 (bodies): v = H⁻¹ Jᵀ p with p = z + βp (first iteration: p already set)
-      for (int64_t j = tid; j < a.n; j += nth) {
-        double v[12];
-        body_apply(a, j, Pp, first ? nullptr : Z, beta, v);
 #pragma unroll
-        for (int c = 0; c < 12; ++c) V[c * a.n + j] = v[c];
-      }
-      grid.sync();
-      // pass 2 (points): p ← z + βp (materialised), Ap = J v, partial p·Ap
-      {
-        double acc[1] = {0.0};
-        for (int64_t p = tid; p < np; p += nth) {
-          double pv[3], s[3] = {0, 0, 0};
-#pragma unroll
-          for (int e = 0; e < 3; ++e) {
-            pv[e] = first ? Pp[e * np + p] : Z[e * np + p] + beta * Pp[e * np + p];
-            Pp[e * np + p] = pv[e];
-          }
-          for (int side = 0; side < 2; ++side) {
-            const int64_t j = side == 0 ? a.pa[p] : a.pb[p];
-            if (j < 0) continue;
-            const double* y = a.py + 6 * p + 3 * side;
-            const double sg = side == 0 ? 1.0 : -1.0;
-#pragma unroll
-            for (int e = 0; e < 3; ++e)
-              s[e] += sg * (V[(0 + e) * a.n + j] * y[0] + V[(3 + e) * a.n + j] * y[1] + V[(6 + e) * a.n + j] * y[2] +
-                            V[(9 + e) * a.n + j]);
-          }
-#pragma unroll
-          for (int e = 0; e < 3; ++e) {
-            Ap[e * np + p] = s[e];
-            acc[0] += pv[e] * s[e];
-          }
-        }
-        block_reduce_store<1>(acc, a.part + 2 * SPARSE_MAX_BLOCKS);
-      }
-      grid.sync();
-      double pAp[1];
-      grid_sum<1>(a.part + 2 * SPARSE_MAX_BLOCKS, nblk, pAp);
-      const double alpha = rz / pAp[0];
-      // pass 3 (points): λ += αp, r −= αAp, z = D⁻¹r; partials r·z, r·r
-      {
-        double acc[2] = {0.0, 0.0};
-        for (int64_t p = tid; p < np; p += nth) {
-          double r[3], di[6], z[3];
-#pragma unroll
-          for (int e = 0; e < 3; ++e) {
-            X[e * np + p] += alpha * Pp[e * np + p];
-            r[e] = Rr[e * np + p] - alpha * Ap[e * np + p];
-            Rr[e * np + p] = r[e];
-          }
-#pragma unroll
-          for (int e = 0; e < 6; ++e) di[e] = a.dinv[e * np + p];
-          sym_vec(di, r, z);
-#pragma unroll
-          for (int e = 0; e < 3; ++e) {
-            Z[e * np + p] = z[e];
-            acc[0] += r[e] * z[e];
-            acc[1] += r[e] * r[e];
-          }
-        }
-        block_reduce_store<2>(acc, a.part);
-      }
-      grid.sync();
-      grid_sum<2>(a.part, nblk, s2);
-      beta = s2[0] / rz;
-      rz = s2[0];
-      first = false;
-      last_r2 = s2[1];
-      if (s2[1] <= tol2) {
-        ++it;
-        break;
-      }
-    }
-  }
-  if (tid == 0) {
-    a.iters[0] = it;
-    // the recursive residual stagnates at the fp64 floor (~1e-13 relative for these duals); only a residual
-    // still above 1e-9 of ‖b‖ after max_iter is a failure
-    if (it >= a.max_iter && last_r2 > 1e-18 * bnorm2) sreport(a.k, ERR_SINGULAR);
+    for (int e = 0; e < 3; ++e) a.res[e * a.np + p] = a.rhs[e * a.np + p] - s[e];
   }
 }
+__global__ void axpy_kernel(double* y, const double* x, int64_t n) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+    y[i] += x[i];
+}
 
-// bodies: qⁿ⁺¹ = q̃ − H⁻¹ Jᵀ λ (P:479), q̇ⁿ⁺¹ = δq/h
+// bodies: qⁿ⁺¹ = q̃ − H⁻¹ Jᵀ λ (P:479), q̇ⁿ⁺¹ = δq/h (S:137)
 __global__ void sparse_update_kernel(SparseArgs a) {
   const int64_t ld = a.b.ld;
   for (int64_t j = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; j < a.n; j += (int64_t)gridDim.x * blockDim.x) {
     double v[12];
-    body_apply(a, j, a.lam, nullptr, 0.0, v);
+    body_apply(a, j, a.lam, v);
 #pragma unroll
     for (int c = 0; c < 12; ++c) {
       const double dq = a.b.qd[c * ld + j] - v[c];
@@ -316,43 +179,975 @@ __global__ void sparse_update_kernel(SparseArgs a) {
   }
 }
 
-static int g_sparse_grid = 0;
+// ============================================================================ numeric factorization
+// Assembly of the original entries: one thread per 3×3 block (row point q, column point p, both in the front of
+// the node owning p): S_qp = Σ_{shared bodies j} s_q s_p R_j P_j(ȳ_q, ȳ_p) R_jᵀ.
+__global__ void mf_assemble_kernel(SparseArgs a) {
+  const MfArgs& m = a.mf;
+  for (int64_t b = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; b < m.nblk;
+       b += (int64_t)gridDim.x * blockDim.x) {
+    const int node = m.ablk[3 * b], rb = m.ablk[3 * b + 1], cb = m.ablk[3 * b + 2];
+    double S[9] = {0, 0, 0, 0, 0, 0, 0, 0, 0};
+    for (int c = m.acoff[b]; c < m.acoff[b + 1]; ++c) {
+      const int re = m.acon[2 * c], ce = m.acon[2 * c + 1];
+      const int pr = re >> 1, sr = re & 1, pc = ce >> 1, sc = ce & 1;
+      const int64_t j = sr == 0 ? a.pa[pr] : a.pb[pr];
+      const double sg = (sr == sc) ? 1.0 : -1.0;
+      double R[9], P[9], T[9];
+      body_R(a, j, R);
+      HinvBlk H;
+      body_hinv(a, j, H);
+      pblock(H, a.py + 6 * pr + 3 * sr, a.py + 6 * pc + 3 * sc, P);
+      rot_conj(R, P, T);
+#pragma unroll
+      for (int e = 0; e < 9; ++e) S[e] += sg * T[e];
+    }
+    double* F = m.F + m.foff[node];
+    const int64_t f = m.fdim[node];
+#pragma unroll
+    for (int r = 0; r < 3; ++r)
+#pragma unroll
+      for (int c = 0; c < 3; ++c) F[(3 * cb + c) * f + 3 * rb + r] = S[3 * r + c];
+  }
+}
+
+__device__ __forceinline__ int mapped(const int32_t* map, int i) { return 3 * map[i / 3] + i % 3; }
+
+// Small fronts (f ≤ MF_SMALL): one CTA loads the front into shared memory, extend-adds its children's update
+// matrices, runs the partial (right-looking) Cholesky of its own columns, and writes L and its own update back.
+__global__ void __launch_bounds__(SP_THREADS) mf_small_kernel(SparseArgs a, const int32_t* nodes) {
+  extern __shared__ double sF[];
+  const MfArgs& m = a.mf;
+  const int node = nodes[blockIdx.x];
+  const int f = m.fdim[node], n = m.nown[node];
+  double* F = m.F + m.foff[node];
+  for (int i = threadIdx.x; i < f * f; i += blockDim.x) sF[i] = F[i];
+  __syncthreads();
+  for (int ci = m.ch_off[node]; ci < m.ch_off[node + 1]; ++ci) {
+    const int c = m.ch[ci];
+    const int fc = m.fdim[c], nc = m.nown[c], mc = fc - nc;
+    const double* Fc = m.F + m.foff[c];
+    const int32_t* map = m.ea_map + m.ea_off[c];
+    for (int idx = threadIdx.x; idx < mc * mc; idx += blockDim.x) {
+      const int i = idx % mc, j = idx / mc;
+      if (i < j) continue;
+      sF[mapped(map, j) * f + mapped(map, i)] += Fc[(int64_t)(nc + j) * fc + nc + i];
+    }
+    __syncthreads();
+  }
+  const int tx = threadIdx.x % 16, ty = threadIdx.x / 16;
+  for (int k = 0; k < n; ++k) {
+    double d = sF[k * f + k];
+    if (!(d > 0.0)) {
+      if (threadIdx.x == 0) sreport(a.k, ERR_SINGULAR);
+      d = 1.0;
+    }
+    const double sd = sqrt(d), isd = 1.0 / sd;
+    __syncthreads();
+    for (int i = k + 1 + threadIdx.x; i < f; i += blockDim.x) sF[k * f + i] *= isd;
+    if (threadIdx.x == 0) sF[k * f + k] = sd;
+    __syncthreads();
+    for (int j = k + 1 + ty; j < f; j += 16) {  // column j, rows i ≥ j
+      const double ljk = sF[k * f + j];
+      for (int i = j + tx; i < f; i += 16) sF[j * f + i] -= sF[k * f + i] * ljk;
+    }
+    __syncthreads();
+  }
+  for (int i = threadIdx.x; i < f * f; i += blockDim.x)
+    if (i % f >= i / f) F[i] = sF[i];
+}
+
+// Extend-add into large parents, one child slot per launch: task = (parent, child column j).
+__global__ void __launch_bounds__(128) mf_ea_kernel(SparseArgs a, const int32_t* tasks, int slot) {
+  const MfArgs& m = a.mf;
+  const int node = tasks[2 * blockIdx.x], j = tasks[2 * blockIdx.x + 1];
+  const int c = m.ch[m.ch_off[node] + slot];
+  const int fc = m.fdim[c], nc = m.nown[c], mc = fc - nc;
+  const int64_t f = m.fdim[node];
+  const int32_t* map = m.ea_map + m.ea_off[c];
+  const double* src = m.F + m.foff[c] + (int64_t)(nc + j) * fc + nc;
+  double* dst = m.F + m.foff[node] + mapped(map, j) * f;
+  for (int i = j + threadIdx.x; i < mc; i += blockDim.x) dst[mapped(map, i)] += src[i];
+}
+
+// Panel step 1: Cholesky of the kb×kb diagonal block at k0, and its inverse L⁻¹ (kept per front and chunk: the
+// TRSM of this panel and the triangular solves use it).
+__global__ void __launch_bounds__(SP_THREADS) mf_potrf_kernel(SparseArgs a, const int32_t* tasks, int k0) {
+  extern __shared__ double psm[];
+  double(*L)[MF_NB + 1] = reinterpret_cast<double(*)[MF_NB + 1]>(psm);
+  double(*X)[MF_NB + 1] = reinterpret_cast<double(*)[MF_NB + 1]>(psm + MF_NB * (MF_NB + 1));
+  const MfArgs& m = a.mf;
+  const int node = tasks[blockIdx.x];
+  const int n = m.nown[node];
+  const int64_t f = m.fdim[node];
+  const int kb = min(MF_NB, n - k0);
+  double* F = m.F + m.foff[node];
+  const int tid = threadIdx.x, tx = tid % 16, ty = tid / 16;
+  for (int idx = tid; idx < MF_NB * MF_NB; idx += blockDim.x) {
+    const int r = idx % MF_NB, c = idx / MF_NB;
+    L[r][c] = (r >= c && r < kb) ? F[(k0 + c) * f + k0 + r] : 0.0;
+    X[r][c] = r == c ? 1.0 : 0.0;
+  }
+  __syncthreads();
+  for (int k = 0; k < kb; ++k) {
+    double d = L[k][k];
+    if (!(d > 0.0)) {
+      if (tid == 0) sreport(a.k, ERR_SINGULAR);
+      d = 1.0;
+    }
+    const double sd = sqrt(d), isd = 1.0 / sd;
+    __syncthreads();
+    if (tid > k && tid < kb) L[tid][k] *= isd;
+    if (tid == 0) L[k][k] = sd;
+    __syncthreads();
+    for (int i = k + 1 + ty; i < kb; i += 16) {
+      const double lik = L[i][k];
+      for (int j = k + 1 + tx; j <= i; j += 16) L[i][j] -= lik * L[j][k];
+    }
+    __syncthreads();
+  }
+  for (int idx = tid; idx < kb * kb; idx += blockDim.x) {
+    const int r = idx % kb, c = idx / kb;
+    if (r >= c) F[(k0 + c) * f + k0 + r] = L[r][c];
+  }
+  // X = L⁻¹ by forward elimination on the identity (row k scaled, then eliminated from the rows below)
+  for (int k = 0; k < kb; ++k) {
+    const double ik = 1.0 / L[k][k];
+    if (tid <= k) X[k][tid] *= ik;
+    __syncthreads();
+    for (int i = k + 1 + ty; i < kb; i += 16) {
+      const double lik = L[i][k];
+      for (int j = tx; j <= k; j += 16) X[i][j] -= lik * X[k][j];
+    }
+    __syncthreads();
+  }
+  double* out = m.linv + m.loff[node] + (int64_t)(k0 / MF_NB) * MF_NB * MF_NB;
+  for (int idx = tid; idx < MF_NB * MF_NB; idx += blockDim.x) out[idx] = X[idx / MF_NB][idx % MF_NB];
+}
+
+// Panel step 2: rows r0..r0+63 of the panel: X = B L⁻ᵀ (B = F[r, k0:k0+kb]); task = (node, r0, potrf slot).
+__global__ void __launch_bounds__(SP_THREADS) mf_trsm_kernel(SparseArgs a, const int32_t* tasks, int k0) {
+  extern __shared__ double tsm[];
+  double(*Li)[MF_NB + 1] = reinterpret_cast<double(*)[MF_NB + 1]>(tsm);
+  double(*Bs)[MF_NB + 1] = reinterpret_cast<double(*)[MF_NB + 1]>(tsm + MF_NB * (MF_NB + 1));
+  const MfArgs& m = a.mf;
+  const int node = tasks[3 * blockIdx.x], r0 = tasks[3 * blockIdx.x + 1];
+  const int n = m.nown[node];
+  const int64_t f = m.fdim[node];
+  const int kb = min(MF_NB, n - k0);
+  const int rows = min((int64_t)MF_NB, f - r0);
+  double* F = m.F + m.foff[node];
+  const double* li = m.linv + m.loff[node] + (int64_t)(k0 / MF_NB) * MF_NB * MF_NB;
+  const int tid = threadIdx.x;
+  for (int idx = tid; idx < MF_NB * MF_NB; idx += blockDim.x) {
+    const int r = idx % MF_NB, l = idx / MF_NB;
+    Li[idx / MF_NB][idx % MF_NB] = li[idx];
+    Bs[r][l] = (r < rows && l < kb) ? F[(k0 + l) * f + r0 + r] : 0.0;
+  }
+  __syncthreads();
+  const int tx = tid % 16, ty = tid / 16;
+  double acc[4][4];
+#pragma unroll
+  for (int i = 0; i < 4; ++i)
+#pragma unroll
+    for (int j = 0; j < 4; ++j) acc[i][j] = 0.0;
+  for (int l = 0; l < kb; ++l) {
+    double bv[4], lv[4];
+#pragma unroll
+    for (int i = 0; i < 4; ++i) bv[i] = Bs[ty + 16 * i][l];
+#pragma unroll
+    for (int j = 0; j < 4; ++j) lv[j] = Li[tx + 16 * j][l];  // Linv[c][l], zero above the diagonal
+#pragma unroll
+    for (int i = 0; i < 4; ++i)
+#pragma unroll
+      for (int j = 0; j < 4; ++j) acc[i][j] = fma(bv[i], lv[j], acc[i][j]);
+  }
+#pragma unroll
+  for (int i = 0; i < 4; ++i)
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      const int r = ty + 16 * i, c = tx + 16 * j;
+      if (r < rows && c < kb) F[(k0 + c) * f + r0 + r] = acc[i][j];
+    }
+}
+
+// Panel step 3: trailing update C[r0.., c0..] −= P_r P_cᵀ with the panel P = F[:, k0:k0+kb] (lower tiles only);
+// task = (node, r0, c0). 64 threads, 8×8 outputs each (rows tx + 8i, columns ty + 8j), K staged 16 at a time.
+__global__ void __launch_bounds__(64) mf_syrk_kernel(SparseArgs a, const int32_t* tasks, int k0) {
+  __shared__ double As[16][MF_NB];
+  __shared__ double Bs[16][MF_NB];
+  const MfArgs& m = a.mf;
+  const int node = tasks[3 * blockIdx.x], r0 = tasks[3 * blockIdx.x + 1], c0 = tasks[3 * blockIdx.x + 2];
+  const int n = m.nown[node];
+  const int64_t f = m.fdim[node];
+  const int kb = min(MF_NB, n - k0);
+  double* F = m.F + m.foff[node];
+  const int tid = threadIdx.x, tx = tid % 8, ty = tid / 8;
+  double acc[8][8];
+#pragma unroll
+  for (int i = 0; i < 8; ++i)
+#pragma unroll
+    for (int j = 0; j < 8; ++j) acc[i][j] = 0.0;
+  for (int kk = 0; kk < kb; kk += 16) {
+    const int kc = min(16, kb - kk);
+#pragma unroll
+    for (int t = 0; t < 16; ++t) {
+      const int idx = tid + 64 * t;
+      const int r = idx % MF_NB, k = idx / MF_NB;
+      const double* col = F + (k0 + kk + k) * f;
+      As[k][r] = (k < kc && r0 + r < f) ? col[r0 + r] : 0.0;
+      Bs[k][r] = (k < kc && c0 + r < f) ? col[c0 + r] : 0.0;
+    }
+    __syncthreads();
+#pragma unroll 4
+    for (int k = 0; k < 16; ++k) {
+      double av[8], bv[8];
+#pragma unroll
+      for (int i = 0; i < 8; ++i) av[i] = As[k][tx + 8 * i];
+#pragma unroll
+      for (int j = 0; j < 8; ++j) bv[j] = Bs[k][ty + 8 * j];
+#pragma unroll
+      for (int i = 0; i < 8; ++i)
+#pragma unroll
+        for (int j = 0; j < 8; ++j) acc[i][j] = fma(av[i], bv[j], acc[i][j]);
+    }
+    __syncthreads();
+  }
+#pragma unroll
+  for (int j = 0; j < 8; ++j) {
+    const int c = c0 + ty + 8 * j;
+    if (c >= f) continue;
+    double* col = F + (int64_t)c * f;
+#pragma unroll
+    for (int i = 0; i < 8; ++i) {
+      const int r = r0 + tx + 8 * i;
+      if (r < f && r >= c) col[r] -= acc[i][j];
+    }
+  }
+}
+
+// ============================================================================ triangular solves
+// Forward, one CTA per front of a level: w = [own rhs; 0] + children's boundary vectors; y = L11⁻¹ w_own
+// (blocked by 64; the diagonal block is solved by warp 0 in shared memory); w_bnd −= L21 y. y goes to dst
+// (point order), w_bnd stays in the node's solve vector for the parent.
+__global__ void __launch_bounds__(SP_THREADS) mf_fwd_kernel(SparseArgs a, const int32_t* nodes, const double* src,
+                                                           double* dst) {
+  extern __shared__ double sm[];
+  const MfArgs& m = a.mf;
+  const int node = nodes[blockIdx.x];
+  const int n = m.nown[node];
+  const int64_t f = m.fdim[node];
+  double* w = sm;
+  double* Ld = sm + ((f + 1) & ~1);  // [MF_NB][MF_NB + 1]
+  const double* F = m.F + m.foff[node];
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int first = m.own_first[node];
+  for (int i = tid; i < f; i += blockDim.x)
+    w[i] = i < n ? src[(i % 3) * a.np + m.ipos[first + i / 3]] : 0.0;
+  __syncthreads();
+  for (int ci = m.ch_off[node]; ci < m.ch_off[node + 1]; ++ci) {
+    const int c = m.ch[ci];
+    const int fc = m.fdim[c], nc = m.nown[c];
+    const int32_t* map = m.ea_map + m.ea_off[c];
+    const double* wc = m.wvec + m.woff[c];
+    for (int i = tid; i < fc - nc; i += blockDim.x) w[mapped(map, i)] += wc[nc + i];
+    __syncthreads();
+  }
+  for (int k0 = 0; k0 < n; k0 += MF_NB) {
+    const int kb = min(MF_NB, n - k0);
+    for (int idx = tid; idx < kb * kb; idx += blockDim.x) {
+      const int r = idx % kb, c = idx / kb;
+      Ld[r * (MF_NB + 1) + c] = F[(k0 + c) * f + k0 + r];
+    }
+    __syncthreads();
+    if (warp == 0) {
+      for (int j = 0; j < kb; ++j) {
+        const double xj = w[k0 + j] / Ld[j * (MF_NB + 1) + j];
+        __syncwarp();
+        if (lane == 0) w[k0 + j] = xj;
+        for (int i = j + 1 + lane; i < kb; i += 32) w[k0 + i] -= Ld[i * (MF_NB + 1) + j] * xj;
+        __syncwarp();
+      }
+    }
+    __syncthreads();
+    for (int64_t r = k0 + kb + tid; r < f; r += blockDim.x) {
+      double s = 0.0;
+      for (int j = 0; j < kb; ++j) s += F[(k0 + j) * f + r] * w[k0 + j];
+      w[r] -= s;
+    }
+    __syncthreads();
+  }
+  for (int i = tid; i < n; i += blockDim.x) dst[(i % 3) * a.np + m.ipos[first + i / 3]] = w[i];
+  double* wv = m.wvec + m.woff[node];
+  for (int64_t i = n + tid; i < f; i += blockDim.x) wv[i] = w[i];
+}
+
+// Backward, one CTA per front, top level first: z = y_own − L21ᵀ x_bnd (x_bnd from the ancestors' solution),
+// then L11ᵀ x_own = z by 64-blocks from the last. x goes to sol (point order).
+__global__ void __launch_bounds__(SP_THREADS) mf_bwd_kernel(SparseArgs a, const int32_t* nodes, const double* ysrc,
+                                                           double* sol) {
+  extern __shared__ double sm[];
+  const MfArgs& m = a.mf;
+  const int node = nodes[blockIdx.x];
+  const int n = m.nown[node];
+  const int64_t f = m.fdim[node];
+  double* x = sm;
+  double* Ld = sm + ((f + 1) & ~1);
+  const double* F = m.F + m.foff[node];
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, nw = blockDim.x >> 5;
+  const int first = m.own_first[node];
+  const int32_t* bnd = m.bnd + m.bnd_off[node];
+  for (int64_t i = tid; i < f; i += blockDim.x) {
+    const int p = i < n ? m.ipos[first + i / 3] : m.ipos[bnd[(i - n) / 3]];
+    x[i] = (i < n ? ysrc : sol)[(i % 3) * a.np + p];
+  }
+  __syncthreads();
+  for (int i = warp; i < n; i += nw) {  // z_i = y_i − Σ_r L[r][i] x_r over boundary rows
+    const double* col = F + (int64_t)i * f;
+    double s = 0.0;
+    for (int64_t r = n + lane; r < f; r += 32) s += col[r] * x[r];
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) s += __shfl_down_sync(0xffffffffu, s, o);
+    if (lane == 0) x[i] -= s;
+  }
+  __syncthreads();
+  const int nchunk = (n + MF_NB - 1) / MF_NB;
+  for (int cidx = nchunk - 1; cidx >= 0; --cidx) {
+    const int k0 = cidx * MF_NB, kb = min(MF_NB, n - k0);
+    for (int idx = tid; idx < kb * kb; idx += blockDim.x) {
+      const int r = idx % kb, c = idx / kb;
+      Ld[r * (MF_NB + 1) + c] = F[(k0 + c) * f + k0 + r];
+    }
+    __syncthreads();
+    if (warp == 0) {
+      for (int j = kb - 1; j >= 0; --j) {
+        const double xj = x[k0 + j] / Ld[j * (MF_NB + 1) + j];
+        __syncwarp();
+        if (lane == 0) x[k0 + j] = xj;
+        for (int i = lane; i < j; i += 32) x[k0 + i] -= Ld[j * (MF_NB + 1) + i] * xj;
+        __syncwarp();
+      }
+    }
+    __syncthreads();
+    for (int i = warp; i < k0; i += nw) {  // earlier own entries: x_i −= Σ_{r in chunk} L[r][i] x_r
+      const double* col = F + (int64_t)i * f + k0;
+      double s = 0.0;
+      for (int r = lane; r < kb; r += 32) s += col[r] * x[k0 + r];
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) s += __shfl_down_sync(0xffffffffu, s, o);
+      if (lane == 0) x[i] -= s;
+    }
+    __syncthreads();
+  }
+  for (int i = tid; i < n; i += blockDim.x) sol[(i % 3) * a.np + m.ipos[first + i / 3]] = x[i];
+}
+
+// ---- triangular solves of large fronts, parallel over 64-row / 64-column tiles, one launch per 64-chunk
+// Forward init: w = [own rhs; 0] + the children's boundary vectors (into the node's solve vector).
+__global__ void __launch_bounds__(SP_THREADS) mf_fwd_init_kernel(SparseArgs a, const int32_t* nodes, const double* src) {
+  const MfArgs& m = a.mf;
+  const int node = nodes[blockIdx.x];
+  const int n = m.nown[node];
+  const int64_t f = m.fdim[node];
+  const int first = m.own_first[node];
+  double* w = m.wvec + m.woff[node];
+  for (int64_t i = threadIdx.x; i < f; i += blockDim.x)
+    w[i] = i < n ? src[(i % 3) * a.np + m.ipos[first + i / 3]] : 0.0;
+  __syncthreads();
+  for (int ci = m.ch_off[node]; ci < m.ch_off[node + 1]; ++ci) {
+    const int c = m.ch[ci];
+    const int fc = m.fdim[c], nc = m.nown[c];
+    const int32_t* map = m.ea_map + m.ea_off[c];
+    const double* wc = m.wvec + m.woff[c];
+    for (int i = threadIdx.x; i < fc - nc; i += blockDim.x) w[mapped(map, i)] += wc[nc + i];
+    __syncthreads();
+  }
+}
+
+// Forward chunk c: every CTA forms y_c = L_cc⁻¹ w_c; the writer task stores it, the others update their 64 rows
+// below the chunk: w_r −= L[r, chunk] y_c. task = (node, r0 or −1, writer flag).
+__global__ void __launch_bounds__(SP_THREADS) mf_fwd_chunk_kernel(SparseArgs a, const int32_t* tasks, int c,
+                                                                 double* dst) {
+  __shared__ double yc[MF_NB];
+  __shared__ double part[4][MF_NB];
+  const MfArgs& m = a.mf;
+  const int node = tasks[3 * blockIdx.x], r0 = tasks[3 * blockIdx.x + 1], writer = tasks[3 * blockIdx.x + 2];
+  const int n = m.nown[node];
+  const int64_t f = m.fdim[node];
+  const int k0 = c * MF_NB, kb = min(MF_NB, n - k0);
+  const double* F = m.F + m.foff[node];
+  double* w = m.wvec + m.woff[node];
+  const double* li = m.linv + m.loff[node] + (int64_t)c * MF_NB * MF_NB;
+  const int tid = threadIdx.x;
+  {  // y_c[i] = Σ_j Linv[i][j] w[k0+j]: 4 threads per row
+    const int i = tid % MF_NB, g = tid / MF_NB;
+    double s = 0.0;
+    if (i < kb)
+      for (int j = g * 16; j < min(kb, g * 16 + 16); ++j) s += li[i * MF_NB + j] * w[k0 + j];
+    part[g][i] = s;
+  }
+  __syncthreads();
+  if (tid < MF_NB) yc[tid] = part[0][tid] + part[1][tid] + part[2][tid] + part[3][tid];
+  __syncthreads();
+  if (writer && tid < kb) {
+    const int i = k0 + tid;
+    dst[(i % 3) * a.np + m.ipos[m.own_first[node] + i / 3]] = yc[tid];
+  }
+  if (r0 < 0) return;
+  const int i = tid % MF_NB, g = tid / MF_NB;
+  const int64_t r = r0 + i;
+  double s = 0.0;
+  if (r < f)
+    for (int j = g * 16; j < min(kb, g * 16 + 16); ++j) s += F[(k0 + j) * f + r] * yc[j];
+  part[g][i] = s;
+  __syncthreads();
+  if (tid < MF_NB && r0 + tid < f) w[r0 + tid] -= part[0][tid] + part[1][tid] + part[2][tid] + part[3][tid];
+}
+
+// Backward init: the node's vector ← [y_own; x_bnd] (x_bnd from the ancestors' solution).
+__global__ void __launch_bounds__(SP_THREADS) mf_bwd_init_kernel(SparseArgs a, const int32_t* nodes, const double* ysrc,
+                                                                const double* sol) {
+  const MfArgs& m = a.mf;
+  const int node = nodes[blockIdx.x];
+  const int n = m.nown[node];
+  const int64_t f = m.fdim[node];
+  const int first = m.own_first[node];
+  const int32_t* bnd = m.bnd + m.bnd_off[node];
+  double* x = m.wvec + m.woff[node];
+  for (int64_t i = threadIdx.x; i < f; i += blockDim.x) {
+    const int p = i < n ? m.ipos[first + i / 3] : m.ipos[bnd[(i - n) / 3]];
+    x[i] = (i < n ? ysrc : sol)[(i % 3) * a.np + p];
+  }
+}
+
+// Backward boundary product: z_i = y_i − Σ_{r ≥ n} L[r][i] x_r for the 64 own columns of a tile; task = (node, t0).
+__global__ void __launch_bounds__(SP_THREADS) mf_bwd_bnd_kernel(SparseArgs a, const int32_t* tasks) {
+  const MfArgs& m = a.mf;
+  const int node = tasks[2 * blockIdx.x], t0 = tasks[2 * blockIdx.x + 1];
+  const int n = m.nown[node];
+  const int64_t f = m.fdim[node];
+  const double* F = m.F + m.foff[node];
+  double* x = m.wvec + m.woff[node];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  for (int cc = warp; cc < MF_NB; cc += SP_THREADS / 32) {
+    const int i = t0 + cc;
+    if (i >= n) break;
+    const double* col = F + (int64_t)i * f;
+    double s = 0.0;
+    for (int64_t r = n + lane; r < f; r += 32) s += col[r] * x[r];
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) s += __shfl_down_sync(0xffffffffu, s, o);
+    if (lane == 0) x[i] -= s;
+  }
+}
+
+// Backward chunk c (last chunk first): every CTA forms x_c = L_cc⁻ᵀ z_c; the writer stores it, the others update
+// the 64 earlier own columns of their tile: z_i −= Σ_{r in chunk} L[r][i] x_r. task = (node, t0 or −1, writer).
+__global__ void __launch_bounds__(SP_THREADS) mf_bwd_chunk_kernel(SparseArgs a, const int32_t* tasks, int c,
+                                                                 double* sol) {
+  __shared__ double xc[MF_NB];
+  __shared__ double part[4][MF_NB];
+  const MfArgs& m = a.mf;
+  const int node = tasks[3 * blockIdx.x], t0 = tasks[3 * blockIdx.x + 1], writer = tasks[3 * blockIdx.x + 2];
+  const int n = m.nown[node];
+  const int64_t f = m.fdim[node];
+  const int k0 = c * MF_NB, kb = min(MF_NB, n - k0);
+  const double* F = m.F + m.foff[node];
+  double* x = m.wvec + m.woff[node];
+  const double* li = m.linv + m.loff[node] + (int64_t)c * MF_NB * MF_NB;
+  const int tid = threadIdx.x;
+  {  // x_c[i] = Σ_j Linv[j][i] z[k0+j]
+    const int i = tid % MF_NB, g = tid / MF_NB;
+    double s = 0.0;
+    if (i < kb)
+      for (int j = max(i, g * 16); j < min(kb, g * 16 + 16); ++j) s += li[j * MF_NB + i] * x[k0 + j];
+    part[g][i] = s;
+  }
+  __syncthreads();
+  if (tid < MF_NB) xc[tid] = part[0][tid] + part[1][tid] + part[2][tid] + part[3][tid];
+  __syncthreads();
+  if (writer && tid < kb) {
+    const int i = k0 + tid;
+    sol[(i % 3) * a.np + m.ipos[m.own_first[node] + i / 3]] = xc[tid];
+  }
+  if (t0 < 0) return;
+  // column i = t0 + tid/4 (64 columns, 4 threads each over 16 chunk rows)
+  const int cc = tid / 4, g = tid % 4;
+  const int i = t0 + cc;
+  double s = 0.0;
+  const double* col = F + (int64_t)i * f + k0;
+  for (int r = g * 16; r < min(kb, g * 16 + 16); ++r) s += col[r] * xc[r];
+  s += __shfl_down_sync(0xffffffffu, s, 2, 4);
+  s += __shfl_down_sync(0xffffffffu, s, 1, 4);
+  if (g == 0 && i < k0) x[i] -= s;
+}
+
+// ============================================================================ host side: launches
+constexpr int PANEL_SMEM = 2 * MF_NB * (MF_NB + 1) * (int)sizeof(double);
 
 cudaError_t sparse_init() {
-  int dev = 0, nsm = 0, per = 0;
+  int dev = 0, v = 0;
   cudaError_t e;
   if ((e = cudaGetDevice(&dev))) return e;
-  if ((e = cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev))) return e;
-  if ((e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, sparse_pcg_kernel, SP_THREADS, 0))) return e;
-  g_sparse_grid = std::max(1, std::min(per, 4) * nsm);
+  if ((e = cudaDeviceGetAttribute(&v, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev))) return e;
+  if ((e = cudaFuncSetAttribute(mf_small_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, v))) return e;
+  if ((e = cudaFuncSetAttribute(mf_fwd_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, v))) return e;
+  if ((e = cudaFuncSetAttribute(mf_bwd_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, v))) return e;
+  if ((e = cudaFuncSetAttribute(mf_potrf_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, PANEL_SMEM))) return e;
+  if ((e = cudaFuncSetAttribute(mf_trsm_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, PANEL_SMEM))) return e;
   return cudaSuccess;
 }
 
-int sparse_grid_blocks() { return g_sparse_grid; }
+static size_t solve_smem(int max_f) { return sizeof(double) * (((max_f + 1) & ~1) + MF_NB * (MF_NB + 1)); }
+
+static int grid_for(int64_t n) { return (int)std::max<int64_t>(1, std::min<int64_t>((n + 255) / 256, 148 * 16)); }
+
+static cudaError_t mf_solve(const SparsePlan& sp, const SparseArgs& a, const int32_t* LN, const int32_t* T,
+                            const double* src, double* dst, cudaStream_t st) {
+  const int nl = (int)sp.levels.size();
+  for (int l = 0; l < nl; ++l) {  // forward: leaves first
+    const auto& L = sp.levels[l];
+    if (L.n_small)
+      mf_fwd_kernel<<<(unsigned)L.n_small, SP_THREADS, solve_smem(L.max_f_small), st>>>(a, LN + L.small, src, a.yy);
+    if (L.n_big) {
+      mf_fwd_init_kernel<<<(unsigned)L.n_big, SP_THREADS, 0, st>>>(a, LN + L.big, src);
+      for (size_t c = 0; c < L.fwd.size(); ++c)
+        mf_fwd_chunk_kernel<<<(unsigned)L.n_fwd[c], SP_THREADS, 0, st>>>(a, T + L.fwd[c], (int)c, a.yy);
+    }
+  }
+  for (int l = nl - 1; l >= 0; --l) {  // backward: root first
+    const auto& L = sp.levels[l];
+    if (L.n_small)
+      mf_bwd_kernel<<<(unsigned)L.n_small, SP_THREADS, solve_smem(L.max_f_small), st>>>(a, LN + L.small, a.yy, dst);
+    if (L.n_big) {
+      mf_bwd_init_kernel<<<(unsigned)L.n_big, SP_THREADS, 0, st>>>(a, LN + L.big, a.yy, dst);
+      if (L.n_bwdb) mf_bwd_bnd_kernel<<<(unsigned)L.n_bwdb, SP_THREADS, 0, st>>>(a, T + L.bwdb);
+      for (int c = (int)L.bwd.size() - 1; c >= 0; --c)
+        mf_bwd_chunk_kernel<<<(unsigned)L.n_bwd[c], SP_THREADS, 0, st>>>(a, T + L.bwd[c], c, dst);
+    }
+  }
+  return cudaGetLastError();
+}
 
 cudaError_t sparse_step(const Plan& p, const DevPtrs& d, const StepConsts& k, cudaStream_t st) {
   SparseArgs a = d.sparse;
   a.k = k;
-  const int nb = (int)std::min<int64_t>((a.n + 255) / 256, 148 * 8);
-  const int npb = (int)std::min<int64_t>((a.np + 255) / 256, 148 * 8);
-  sparse_predict_kernel<<<std::max(nb, 1), 256, 0, st>>>(a);
-  sparse_rhs_kernel<<<std::max(npb, 1), 256, 0, st>>>(a);
-  void* args[] = {&a};
-  cudaError_t e = cudaLaunchCooperativeKernel((void*)sparse_pcg_kernel, dim3(g_sparse_grid), dim3(SP_THREADS), args,
-                                              0, st);
-  if (e != cudaSuccess) return e;
-  sparse_update_kernel<<<std::max(nb, 1), 256, 0, st>>>(a);
-  (void)p;
+  const SparsePlan& sp = p.sparse;
+  sparse_predict_kernel<<<grid_for(a.n), 256, 0, st>>>(a);
+  if (sp.np == 0) {
+    sparse_update_kernel<<<grid_for(a.n), 256, 0, st>>>(a);
+    return cudaGetLastError();
+  }
+  sparse_rhs_kernel<<<grid_for(a.np), 256, 0, st>>>(a);
+  cudaError_t e;
+  if ((e = cudaMemsetAsync(a.mf.F, 0, sizeof(double) * sp.front_doubles, st))) return e;
+  mf_assemble_kernel<<<grid_for(a.mf.nblk), 256, 0, st>>>(a);
+  const int32_t* LN = d.sparse_lev;
+  const int32_t* T = d.sparse_tasks;
+  for (const auto& L : sp.levels) {
+    if (L.n_small)
+      mf_small_kernel<<<(unsigned)L.n_small, SP_THREADS, sizeof(double) * L.max_f_small * L.max_f_small, st>>>(
+          a, LN + L.small);
+    for (size_t s = 0; s < L.ea.size(); ++s)
+      if (L.n_ea[s]) mf_ea_kernel<<<(unsigned)L.n_ea[s], 128, 0, st>>>(a, T + L.ea[s], (int)s);
+    for (size_t pi = 0; pi < L.panels.size(); ++pi) {
+      const auto& P = L.panels[pi];
+      const int k0 = (int)pi * MF_NB;
+      if (P.n_potrf) mf_potrf_kernel<<<(unsigned)P.n_potrf, SP_THREADS, PANEL_SMEM, st>>>(a, T + P.potrf, k0);
+      if (P.n_trsm) mf_trsm_kernel<<<(unsigned)P.n_trsm, SP_THREADS, PANEL_SMEM, st>>>(a, T + P.trsm, k0);
+      if (P.n_syrk) mf_syrk_kernel<<<(unsigned)P.n_syrk, 64, 0, st>>>(a, T + P.syrk, k0);
+    }
+  }
+  if ((e = cudaGetLastError())) return e;
+  if ((e = mf_solve(sp, a, LN, T, a.rhs, a.lam, st))) return e;
+  for (int it = 0; it < sp.refine; ++it) {  // iterative refinement against the exact S (matrix-free)
+    mv_body_kernel<<<grid_for(a.n), 256, 0, st>>>(a, a.lam);
+    mv_point_kernel<<<grid_for(a.np), 256, 0, st>>>(a);
+    if ((e = mf_solve(sp, a, LN, T, a.res, a.dl, st))) return e;
+    axpy_kernel<<<grid_for(3 * a.np), 256, 0, st>>>(a.lam, a.dl, 3 * a.np);
+  }
+  sparse_update_kernel<<<grid_for(a.n), 256, 0, st>>>(a);
   return cudaGetLastError();
 }
 
-// ============================================================================ host: point lists and incidence
-bool sparse_build(const mabd_joints* J, int64_t n, Plan* p, std::vector<int64_t>* pos_of_body, std::string* msg) {
-  const int64_t K = J->n_joints;
+// ============================================================================ host side: symbolic analysis
+namespace {
+
+struct NdBuild {
+  const double* q0;
+  const std::vector<int32_t>& pa;
+  const std::vector<int32_t>& pb;
+  std::vector<int8_t> mark;
+  std::vector<std::vector<int32_t>> nodes;  // point sets, in postorder
+
+  NdBuild(const double* q, int64_t n, const std::vector<int32_t>& a, const std::vector<int32_t>& b)
+      : q0(q), pa(a), pb(b), mark(n, 0) {}
+
+  double coord(int32_t b, int ax) const { return q0[12 * (int64_t)b + 9 + ax]; }
+
+  void build(std::vector<int32_t>& bodies, std::vector<int32_t>& pts, int depth) {
+    if (pts.empty()) return;
+    if ((int)pts.size() <= MF_LEAF_PTS || bodies.size() <= 1 || depth > 64) {
+      nodes.push_back(pts);
+      return;
+    }
+    double lo[3] = {1e300, 1e300, 1e300}, hi[3] = {-1e300, -1e300, -1e300};
+    for (int32_t b : bodies)
+      for (int ax = 0; ax < 3; ++ax) {
+        lo[ax] = std::min(lo[ax], coord(b, ax));
+        hi[ax] = std::max(hi[ax], coord(b, ax));
+      }
+    int ax = 0;
+    for (int i = 1; i < 3; ++i)
+      if (hi[i] - lo[i] > hi[ax] - lo[ax]) ax = i;
+    const size_t half = bodies.size() / 2;
+    if (hi[ax] > lo[ax]) {
+      std::nth_element(bodies.begin(), bodies.begin() + half, bodies.end(), [&](int32_t x, int32_t y) {
+        const double cx = coord(x, ax), cy = coord(y, ax);
+        return cx < cy || (cx == cy && x < y);
+      });
+    } else {
+      std::nth_element(bodies.begin(), bodies.begin() + half, bodies.end());
+    }
+    std::vector<int32_t> BL(bodies.begin(), bodies.begin() + half), BR(bodies.begin() + half, bodies.end());
+    for (int32_t b : BL) mark[b] = 0;
+    for (int32_t b : BR) mark[b] = 1;
+    std::vector<int32_t> PL, PR, PS;
+    for (int32_t p : pts) {
+      const int sa = mark[pa[p]];
+      const int sb = pb[p] >= 0 ? mark[pb[p]] : sa;
+      (sa != sb ? PS : sa == 0 ? PL : PR).push_back(p);
+    }
+    if (PL.empty() && PR.empty()) {  // no separation possible: one dense node
+      nodes.push_back(pts);
+      return;
+    }
+    std::vector<int32_t>().swap(pts);
+    build(BL, PL, depth + 1);
+    build(BR, PR, depth + 1);
+    if (!PS.empty()) nodes.push_back(PS);
+  }
+};
+
+}  // namespace
+
+static bool mf_symbolic(const mabd_bodies* B, Plan* plan, std::string* msg) {
+  SparsePlan& s = plan->sparse;
+  const int64_t P = s.np, n = plan->n;
+  if (P == 0) {
+    s.nnode = 0;
+    return true;
+  }
+  // ---- nested dissection on the bodies' initial positions
+  NdBuild nd(B->q0, n, s.pa, s.pb);
+  {
+    std::vector<char> used(n, 0);
+    for (int64_t p = 0; p < P; ++p) {
+      used[s.pa[p]] = 1;
+      if (s.pb[p] >= 0) used[s.pb[p]] = 1;
+    }
+    std::vector<int32_t> bodies, pts(P);
+    for (int64_t b = 0; b < n; ++b)
+      if (used[b]) bodies.push_back((int32_t)b);
+    std::iota(pts.begin(), pts.end(), 0);
+    nd.build(bodies, pts, 0);
+  }
+  const int NN = (int)nd.nodes.size();
+  s.nnode = NN;
+  s.epos.assign(P, -1);
+  s.ipos.assign(P, -1);
+  s.own_first.assign(NN, 0);
+  s.nown.assign(NN, 0);
+  std::vector<int32_t> owner(P), last(NN);
+  {
+    int32_t c = 0;
+    for (int i = 0; i < NN; ++i) {
+      s.own_first[i] = c;
+      for (int32_t p : nd.nodes[i]) {
+        s.epos[p] = c;
+        s.ipos[c] = p;
+        owner[c] = i;
+        ++c;
+      }
+      s.nown[i] = 3 * (int32_t)nd.nodes[i].size();
+      last[i] = c;
+    }
+    if (c != P) return *msg = "sparse symbolic: ordering lost points", false;
+  }
+  // ---- point adjacency (points sharing a body)
+  auto for_neighbors = [&](int32_t p, const std::function<void(int32_t)>& fn) {
+    for (int side = 0; side < 2; ++side) {
+      const int32_t b = side == 0 ? s.pa[p] : s.pb[p];
+      if (b < 0) continue;
+      for (int i = s.inc_off[b]; i < s.inc_off[b + 1]; ++i) fn(s.inc[i] >> 1);
+    }
+  };
+  // ---- boundary sets and the assembly tree (parent = owner of the smallest boundary position)
+  std::vector<std::vector<int32_t>> bnd(NN), kids(NN);
+  s.parent.assign(NN, -1);
+  std::vector<int32_t> tmp;
+  for (int i = 0; i < NN; ++i) {
+    tmp.clear();
+    for (int32_t p : nd.nodes[i])
+      for_neighbors(p, [&](int32_t q) {
+        if (s.epos[q] >= last[i]) tmp.push_back(s.epos[q]);
+      });
+    for (int c : kids[i])
+      for (int32_t e : bnd[c])
+        if (e >= last[i]) tmp.push_back(e);
+    std::sort(tmp.begin(), tmp.end());
+    tmp.erase(std::unique(tmp.begin(), tmp.end()), tmp.end());
+    bnd[i] = tmp;
+    if (!tmp.empty()) {
+      const int par = owner[tmp[0]];
+      s.parent[i] = par;
+      kids[par].push_back(i);
+    }
+  }
+  // ---- fronts, extend-add maps, heights
+  s.fdim.assign(NN, 0);
+  s.foff.assign(NN, 0);
+  s.woff.assign(NN, 0);
+  s.height.assign(NN, 0);
+  s.bnd_off.assign(NN, 0);
+  s.ea_off.assign(NN, 0);
+  s.ch_off.assign(NN + 1, 0);
+  s.bnd.clear();
+  s.ea_map.clear();
+  s.ch.clear();
+  int64_t fo = 0, wo = 0;
+  double flops = 0.0;
+  s.max_f = 0;
+  for (int i = 0; i < NN; ++i) {
+    const int64_t nn = s.nown[i], mm = 3 * (int64_t)bnd[i].size();
+    const int64_t f = nn + mm;
+    if (f > 20000) return *msg = "sparse symbolic: front larger than 20000 rows (dense coupling too wide)", false;
+    s.fdim[i] = (int32_t)f;
+    s.max_f = std::max<int32_t>(s.max_f, (int32_t)f);
+    s.foff[i] = fo;
+    fo += (f * f + 31) & ~int64_t(31);
+    s.woff[i] = wo;
+    wo += (f + 3) & ~int64_t(3);
+    flops += (double)nn * nn * nn / 3.0 + (double)nn * nn * mm + (double)nn * mm * mm;
+    s.bnd_off[i] = (int32_t)s.bnd.size();
+    s.bnd.insert(s.bnd.end(), bnd[i].begin(), bnd[i].end());
+    for (int c : kids[i]) s.height[i] = std::max(s.height[i], s.height[c] + 1);
+    s.ch_off[i + 1] = s.ch_off[i] + (int32_t)kids[i].size();
+    s.ch.insert(s.ch.end(), kids[i].begin(), kids[i].end());
+  }
+  s.front_doubles = fo;
+  s.w_doubles = wo;
+  s.flops = 2.0 * flops;
+  for (int i = 0; i < NN; ++i) {
+    s.ea_off[i] = (int32_t)s.ea_map.size();
+    const int par = s.parent[i];
+    if (par < 0) continue;
+    const int32_t pf = s.own_first[par], pl = last[par];
+    const std::vector<int32_t>& pb = bnd[par];
+    for (int32_t e : bnd[i]) {
+      int32_t pos;
+      if (e >= pf && e < pl) {
+        pos = e - pf;
+      } else {
+        auto it = std::lower_bound(pb.begin(), pb.end(), e);
+        if (it == pb.end() || *it != e) return *msg = "sparse symbolic: boundary not inherited by the parent", false;
+        pos = s.nown[par] / 3 + (int32_t)(it - pb.begin());
+      }
+      s.ea_map.push_back(pos);
+    }
+  }
+  // ---- assembly blocks: (row point q, column point p) with epos(q) ≥ epos(p), in the front of p's node
+  s.ablk.clear();
+  s.acoff.assign(1, 0);
+  s.acon.clear();
+  std::vector<int32_t> nb;
+  for (int i = 0; i < NN; ++i) {
+    const std::vector<int32_t>& bi = bnd[i];
+    for (int32_t p : nd.nodes[i]) {
+      nb.clear();
+      for_neighbors(p, [&](int32_t q) {
+        if (s.epos[q] >= s.epos[p]) nb.push_back(q);
+      });
+      std::sort(nb.begin(), nb.end(), [&](int32_t x, int32_t y) { return s.epos[x] < s.epos[y]; });
+      nb.erase(std::unique(nb.begin(), nb.end()), nb.end());
+      const int32_t cpos = s.epos[p] - s.own_first[i];
+      for (int32_t q : nb) {
+        const int32_t e = s.epos[q];
+        int32_t rpos;
+        if (e < last[i]) {
+          rpos = e - s.own_first[i];
+        } else {
+          auto it = std::lower_bound(bi.begin(), bi.end(), e);
+          if (it == bi.end() || *it != e) return *msg = "sparse symbolic: neighbour missing from the front", false;
+          rpos = s.nown[i] / 3 + (int32_t)(it - bi.begin());
+        }
+        s.ablk.push_back(i);
+        s.ablk.push_back(rpos);
+        s.ablk.push_back(cpos);
+        // shared bodies: (row side, column side)
+        for (int sq = 0; sq < 2; ++sq) {
+          const int32_t bq = sq == 0 ? s.pa[q] : s.pb[q];
+          if (bq < 0) continue;
+          for (int spp = 0; spp < 2; ++spp) {
+            const int32_t bp = spp == 0 ? s.pa[p] : s.pb[p];
+            if (bp != bq) continue;
+            s.acon.push_back(2 * q + sq);
+            s.acon.push_back(2 * p + spp);
+          }
+        }
+        s.acoff.push_back((int32_t)(s.acon.size() / 2));
+      }
+    }
+  }
+  // ---- schedule by height: small fronts in shared memory, large ones by panels
+  int H = 0;
+  for (int i = 0; i < NN; ++i) H = std::max(H, s.height[i] + 1);
+  std::vector<std::vector<int32_t>> byh(H);
+  for (int i = 0; i < NN; ++i) byh[s.height[i]].push_back(i);
+  s.levels.assign(H, SparsePlan::Level());
+  s.lev_nodes.clear();
+  s.tasks.clear();
+  s.loff.assign(NN, 0);
+  s.linv_doubles = 0;
+  const int64_t small_cap = MF_SMALL;
+  for (int h = 0; h < H; ++h) {
+    SparsePlan::Level& L = s.levels[h];
+    const std::vector<int32_t>& nodes = byh[h];
+    L.nodes = (int64_t)s.lev_nodes.size();
+    L.n_nodes = (int64_t)nodes.size();
+    s.lev_nodes.insert(s.lev_nodes.end(), nodes.begin(), nodes.end());
+    std::vector<int32_t> small, big;
+    for (int32_t i : nodes) {
+      L.max_f = std::max(L.max_f, s.fdim[i]);
+      (s.fdim[i] <= small_cap ? small : big).push_back(i);
+    }
+    L.small = (int64_t)s.lev_nodes.size();
+    L.n_small = (int64_t)small.size();
+    s.lev_nodes.insert(s.lev_nodes.end(), small.begin(), small.end());
+    L.big = (int64_t)s.lev_nodes.size();
+    L.n_big = (int64_t)big.size();
+    s.lev_nodes.insert(s.lev_nodes.end(), big.begin(), big.end());
+    for (int32_t i : big) {
+      s.loff[i] = s.linv_doubles;
+      s.linv_doubles += (int64_t)((s.nown[i] + MF_NB - 1) / MF_NB) * MF_NB * MF_NB;
+    }
+    for (int32_t i : small) L.max_f_small = std::max(L.max_f_small, s.fdim[i]);
+    int maxc = 0, maxpan = 0;
+    for (int32_t i : big) {
+      maxc = std::max(maxc, (int)kids[i].size());
+      maxpan = std::max(maxpan, (s.nown[i] + MF_NB - 1) / MF_NB);
+    }
+    L.max_children = maxc;
+    L.ea.assign(maxc, 0);
+    L.n_ea.assign(maxc, 0);
+    for (int sl = 0; sl < maxc; ++sl) {
+      L.ea[sl] = (int64_t)s.tasks.size();
+      for (int32_t i : big) {
+        if ((int)kids[i].size() <= sl) continue;
+        const int c = kids[i][sl];
+        const int mc = s.fdim[c] - s.nown[c];
+        for (int j = 0; j < mc; ++j) {
+          s.tasks.push_back(i);
+          s.tasks.push_back(j);
+        }
+      }
+      L.n_ea[sl] = ((int64_t)s.tasks.size() - L.ea[sl]) / 2;
+    }
+    L.panels.assign(maxpan, SparsePlan::Panel());
+    for (int pi = 0; pi < maxpan; ++pi) {
+      SparsePlan::Panel& Pn = L.panels[pi];
+      const int k0 = pi * MF_NB;
+      std::vector<int32_t> act;
+      for (int32_t i : big)
+        if (s.nown[i] > k0) act.push_back(i);
+      Pn.potrf = (int64_t)s.tasks.size();
+      for (int32_t i : act) s.tasks.push_back(i);
+      Pn.n_potrf = (int64_t)act.size();
+      Pn.trsm = (int64_t)s.tasks.size();
+      for (size_t sl = 0; sl < act.size(); ++sl) {
+        const int i = act[sl];
+        const int t0 = k0 + std::min(MF_NB, s.nown[i] - k0);
+        for (int r0 = t0; r0 < s.fdim[i]; r0 += MF_NB) {
+          s.tasks.push_back(i);
+          s.tasks.push_back(r0);
+          s.tasks.push_back((int32_t)sl);
+        }
+      }
+      Pn.n_trsm = ((int64_t)s.tasks.size() - Pn.trsm) / 3;
+      Pn.syrk = (int64_t)s.tasks.size();
+      for (int32_t i : act) {
+        const int t0 = k0 + std::min(MF_NB, s.nown[i] - k0);
+        for (int r0 = t0; r0 < s.fdim[i]; r0 += MF_NB)
+          for (int c0 = t0; c0 <= r0; c0 += MF_NB) {
+            s.tasks.push_back(i);
+            s.tasks.push_back(r0);
+            s.tasks.push_back(c0);
+          }
+      }
+      Pn.n_syrk = ((int64_t)s.tasks.size() - Pn.syrk) / 3;
+    }
+    // triangular-solve tasks of the big fronts
+    L.fwd.assign(maxpan, 0);
+    L.n_fwd.assign(maxpan, 0);
+    L.bwd.assign(maxpan, 0);
+    L.n_bwd.assign(maxpan, 0);
+    for (int c = 0; c < maxpan; ++c) {
+      const int k0 = c * MF_NB;
+      L.fwd[c] = (int64_t)s.tasks.size();
+      for (int32_t i : big) {
+        if (s.nown[i] <= k0) continue;
+        int wr = 1;
+        for (int r0 = k0 + std::min(MF_NB, s.nown[i] - k0); r0 < s.fdim[i]; r0 += MF_NB, wr = 0) {
+          s.tasks.push_back(i);
+          s.tasks.push_back(r0);
+          s.tasks.push_back(wr);
+        }
+        if (wr) {
+          s.tasks.push_back(i);
+          s.tasks.push_back(-1);
+          s.tasks.push_back(1);
+        }
+      }
+      L.n_fwd[c] = ((int64_t)s.tasks.size() - L.fwd[c]) / 3;
+      L.bwd[c] = (int64_t)s.tasks.size();
+      for (int32_t i : big) {
+        if (s.nown[i] <= k0) continue;
+        int wr = 1;
+        for (int t0 = 0; t0 < k0; t0 += MF_NB, wr = 0) {
+          s.tasks.push_back(i);
+          s.tasks.push_back(t0);
+          s.tasks.push_back(wr);
+        }
+        if (wr) {
+          s.tasks.push_back(i);
+          s.tasks.push_back(-1);
+          s.tasks.push_back(1);
+        }
+      }
+      L.n_bwd[c] = ((int64_t)s.tasks.size() - L.bwd[c]) / 3;
+    }
+    L.bwdb = (int64_t)s.tasks.size();
+    for (int32_t i : big)
+      if (s.fdim[i] > s.nown[i])
+        for (int t0 = 0; t0 < s.nown[i]; t0 += MF_NB) {
+          s.tasks.push_back(i);
+          s.tasks.push_back(t0);
+        }
+    L.n_bwdb = ((int64_t)s.tasks.size() - L.bwdb) / 2;
+  }
+  if (s.tasks.size() > (size_t)INT32_MAX || s.ablk.size() / 3 > (size_t)INT32_MAX)
+    return *msg = "sparse symbolic: too many tasks", false;
+  return true;
+}
+
+bool sparse_build(const mabd_bodies* B, const mabd_joints* J, Plan* p, std::vector<int64_t>* pos_of_body,
+                  std::string* msg) {
+  const int64_t K = J->n_joints, n = B->n;
   SparsePlan& s = p->sparse;
   s = SparsePlan();
   int64_t P = 0;
   for (int64_t k = 0; k < K; ++k) P += J->npts[k];
+  if (2 * P > (int64_t)INT32_MAX) return *msg = "too many joint points", false;
   s.np = P;
   s.pa.resize(P);
   s.pb.resize(P);
@@ -379,13 +1174,167 @@ bool sparse_build(const mabd_joints* J, int64_t n, Plan* p, std::vector<int64_t>
     s.inc[s.inc_off[a] + fill[a]++] = (int32_t)(2 * q);
     if (b >= 0) s.inc[s.inc_off[b] + fill[b]++] = (int32_t)(2 * q + 1);
   }
-  if (2 * P > (int64_t)INT32_MAX) return *msg = "too many joint points", false;
   pos_of_body->resize(n);
-  for (int64_t i = 0; i < n; ++i) (*pos_of_body)[i] = i;  // caller order (grids are already local)
+  for (int64_t i = 0; i < n; ++i) (*pos_of_body)[i] = i;  // caller order
   p->ld = n;
+  p->n = n;
   p->n_dual_rows = 3 * P;
-  p->launches_per_step = 4;
+  if (!mf_symbolic(B, p, msg)) return false;
+  s.refine = MF_REFINE;
+  if (const char* ev = getenv("MABD_SPARSE_REFINE")) s.refine = std::max(0, std::min(8, atoi(ev)));  // developer knob
+  int64_t launches = 4 + (P ? 2 : 0);
+  for (const auto& L : s.levels) {
+    int64_t per = (L.n_small ? 1 : 0);
+    for (int64_t c : L.n_ea) per += c ? 1 : 0;
+    for (const auto& Pn : L.panels) per += (Pn.n_potrf ? 1 : 0) + (Pn.n_trsm ? 1 : 0) + (Pn.n_syrk ? 1 : 0);
+    int64_t sol = 2 * (L.n_small ? 1 : 0);
+    if (L.n_big) sol += 2 + (L.n_bwdb ? 1 : 0) + (int64_t)L.fwd.size() + (int64_t)L.bwd.size();
+    launches += per + sol * (1 + s.refine);
+  }
+  launches += 3 * s.refine;
+  p->launches_per_step = (int32_t)std::min<int64_t>(launches, INT32_MAX);
   return true;
 }
 
+// ============================================================================ host side: layout and upload
+void sparse_layout(Plan* p, const std::function<size_t(size_t)>& take) {
+  SparsePlan& s = p->sparse;
+  const int64_t np = std::max<int64_t>(1, s.np), n = p->n;
+  auto nz = [](size_t x) { return std::max<size_t>(x, 1); };
+  s.o_pa = take(sizeof(int32_t) * np);
+  s.o_pb = take(sizeof(int32_t) * np);
+  s.o_py = take(sizeof(double) * 6 * np);
+  s.o_incoff = take(sizeof(int32_t) * (n + 1));
+  s.o_inc = take(sizeof(int32_t) * nz(s.inc.size()));
+  s.o_vec = take(sizeof(double) * 15 * np);  // rhs, λ, res, δλ, y: [3][np] each
+  s.o_vv = take(sizeof(double) * 12 * n);
+  s.o_iters = take(sizeof(int32_t) * 4);
+  const size_t NN = nz(s.nnode);
+  s.o_F = take(sizeof(double) * nz(s.front_doubles));
+  s.o_foff = take(sizeof(int64_t) * NN);
+  s.o_fdim = take(sizeof(int32_t) * NN);
+  s.o_nown = take(sizeof(int32_t) * NN);
+  s.o_ownf = take(sizeof(int32_t) * NN);
+  s.o_choff = take(sizeof(int32_t) * (NN + 1));
+  s.o_ch = take(sizeof(int32_t) * nz(s.ch.size()));
+  s.o_eaoff = take(sizeof(int32_t) * NN);
+  s.o_eamap = take(sizeof(int32_t) * nz(s.ea_map.size()));
+  s.o_bndoff = take(sizeof(int32_t) * NN);
+  s.o_bnd = take(sizeof(int32_t) * nz(s.bnd.size()));
+  s.o_ipos = take(sizeof(int32_t) * np);
+  s.o_ablk = take(sizeof(int32_t) * nz(s.ablk.size()));
+  s.o_acoff = take(sizeof(int32_t) * nz(s.acoff.size()));
+  s.o_acon = take(sizeof(int32_t) * nz(s.acon.size()));
+  s.o_linv = take(sizeof(double) * nz(s.linv_doubles));
+  s.o_loff = take(sizeof(int64_t) * NN);
+  s.o_w = take(sizeof(double) * nz(s.w_doubles));
+  s.o_woff = take(sizeof(int64_t) * NN);
+  s.o_lev = take(sizeof(int32_t) * nz(s.lev_nodes.size()));
+  s.o_tasks = take(sizeof(int32_t) * nz(s.tasks.size()));
+}
+
+template <class T>
+static cudaError_t upv(char* ws, size_t off, const std::vector<T>& v, cudaStream_t st) {
+  if (v.empty()) return cudaSuccess;
+  return cudaMemcpyAsync(ws + off, v.data(), sizeof(T) * v.size(), cudaMemcpyHostToDevice, st);
+}
+
+cudaError_t sparse_upload(const Plan& p, char* ws, cudaStream_t st, DevPtrs* d) {
+  const SparsePlan& s = p.sparse;
+  SparseArgs& A = d->sparse;
+  const int64_t np = std::max<int64_t>(1, s.np);
+  A.b = d->b;
+  A.hinv_tab = p.mscale.empty() ? d->hinv : nullptr;
+  A.n = p.n;
+  A.np = s.np;
+  A.pa = (const int32_t*)(ws + s.o_pa);
+  A.pb = (const int32_t*)(ws + s.o_pb);
+  A.py = (const double*)(ws + s.o_py);
+  A.inc_off = (const int32_t*)(ws + s.o_incoff);
+  A.inc = (const int32_t*)(ws + s.o_inc);
+  double* v = (double*)(ws + s.o_vec);
+  A.rhs = v;
+  A.lam = v + 3 * np;
+  A.res = v + 6 * np;
+  A.dl = v + 9 * np;
+  A.yy = v + 12 * np;
+  A.vv = (double*)(ws + s.o_vv);
+  A.iters = (int32_t*)(ws + s.o_iters);
+  MfArgs& m = A.mf;
+  m.F = (double*)(ws + s.o_F);
+  m.foff = (const int64_t*)(ws + s.o_foff);
+  m.fdim = (const int32_t*)(ws + s.o_fdim);
+  m.nown = (const int32_t*)(ws + s.o_nown);
+  m.own_first = (const int32_t*)(ws + s.o_ownf);
+  m.ch_off = (const int32_t*)(ws + s.o_choff);
+  m.ch = (const int32_t*)(ws + s.o_ch);
+  m.ea_off = (const int32_t*)(ws + s.o_eaoff);
+  m.ea_map = (const int32_t*)(ws + s.o_eamap);
+  m.bnd_off = (const int32_t*)(ws + s.o_bndoff);
+  m.bnd = (const int32_t*)(ws + s.o_bnd);
+  m.ipos = (const int32_t*)(ws + s.o_ipos);
+  m.ablk = (const int32_t*)(ws + s.o_ablk);
+  m.acoff = (const int32_t*)(ws + s.o_acoff);
+  m.acon = (const int32_t*)(ws + s.o_acon);
+  m.nblk = (int64_t)s.ablk.size() / 3;
+  m.linv = (double*)(ws + s.o_linv);
+  m.loff = (const int64_t*)(ws + s.o_loff);
+  m.wvec = (double*)(ws + s.o_w);
+  m.woff = (const int64_t*)(ws + s.o_woff);
+  d->sparse_lev = (const int32_t*)(ws + s.o_lev);
+  d->sparse_tasks = (const int32_t*)(ws + s.o_tasks);
+  cudaError_t e;
+  if ((e = upv(ws, s.o_pa, s.pa, st))) return e;
+  if ((e = upv(ws, s.o_pb, s.pb, st))) return e;
+  if ((e = upv(ws, s.o_py, s.py, st))) return e;
+  if ((e = upv(ws, s.o_incoff, s.inc_off, st))) return e;
+  if ((e = upv(ws, s.o_inc, s.inc, st))) return e;
+  if ((e = upv(ws, s.o_foff, s.foff, st))) return e;
+  if ((e = upv(ws, s.o_fdim, s.fdim, st))) return e;
+  if ((e = upv(ws, s.o_nown, s.nown, st))) return e;
+  if ((e = upv(ws, s.o_ownf, s.own_first, st))) return e;
+  if ((e = upv(ws, s.o_choff, s.ch_off, st))) return e;
+  if ((e = upv(ws, s.o_ch, s.ch, st))) return e;
+  if ((e = upv(ws, s.o_eaoff, s.ea_off, st))) return e;
+  if ((e = upv(ws, s.o_eamap, s.ea_map, st))) return e;
+  if ((e = upv(ws, s.o_bndoff, s.bnd_off, st))) return e;
+  if ((e = upv(ws, s.o_bnd, s.bnd, st))) return e;
+  if ((e = upv(ws, s.o_ipos, s.ipos, st))) return e;
+  if ((e = upv(ws, s.o_ablk, s.ablk, st))) return e;
+  if ((e = upv(ws, s.o_acoff, s.acoff, st))) return e;
+  if ((e = upv(ws, s.o_acon, s.acon, st))) return e;
+  if ((e = upv(ws, s.o_woff, s.woff, st))) return e;
+  if ((e = upv(ws, s.o_loff, s.loff, st))) return e;
+  if ((e = upv(ws, s.o_lev, s.lev_nodes, st))) return e;
+  if ((e = upv(ws, s.o_tasks, s.tasks, st))) return e;
+  if ((e = cudaMemsetAsync(A.lam, 0, sizeof(double) * 3 * np, st))) return e;
+  int32_t it[4] = {s.refine, 0, 0, 0};
+  if ((e = cudaMemcpyAsync(A.iters, it, sizeof(it), cudaMemcpyHostToDevice, st))) return e;
+  return cudaStreamSynchronize(st);  // the host vectors above are pageable; keep them alive until copied
+}
+
 }  // namespace mabd
+
+// Developer introspection (not part of include/mabd.h): symbolic statistics of the sparse plan of a scene.
+// out[0..7] = nodes, levels, max front, front doubles, factor flops, task ints, launches per step, dual rows.
+extern "C" int mabd_dbg_sparse_stats(const mabd_bodies* B, const mabd_joints* J, double* out) {
+  mabd::Plan p;
+  std::string msg;
+  mabd_options o{};
+  o.newton_iters = 1;
+  o.residual_rhs = 1;
+  o.solver = MABD_SOLVER_SPARSE;
+  o.world = 1;
+  const mabd_status st = mabd::build_plan(B, J, &o, &p, &msg);
+  if (st != MABD_OK) return (int)st;
+  const mabd::SparsePlan& s = p.sparse;
+  out[0] = s.nnode;
+  out[1] = (double)s.levels.size();
+  out[2] = s.max_f;
+  out[3] = (double)s.front_doubles;
+  out[4] = s.flops;
+  out[5] = (double)s.tasks.size();
+  out[6] = p.launches_per_step;
+  out[7] = (double)p.n_dual_rows;
+  return 0;
+}
