@@ -47,7 +47,7 @@ __device__ __forceinline__ int cr_pos(int k) {
 // strided view of one equation's components
 struct SV {
   double* p;
-  __device__ __forceinline__ double& operator[](int e) const { return p[e * NEQ]; }
+  __device__ __forceinline__ double& operator[](int e) const { return p[e * LDS]; }
 };
 __device__ __forceinline__ SV eqD(const CRS& s, int pos) { return SV{s.D + pos}; }
 __device__ __forceinline__ SV eqB(const CRS& s, int pos) { return SV{s.B + pos}; }
@@ -98,8 +98,16 @@ __device__ __forceinline__ void l2_discard128(const void* p) {
 }
 __device__ __forceinline__ void l2_prefetch(const void* p) { asm volatile("prefetch.global.L2 [%0];" ::"l"(p)); }
 
-// update of the surviving equation kq at stride st (both neighbours already hold D⁻¹)
-__device__ __forceinline__ void cr_update(const CRS& s, int kq, int st) {
+// Position of the equation eliminated at level L (stride 2^L) with index e (equation 2^L·(2e+1)).
+template <int L>
+__device__ __forceinline__ int elim_pos(int e) { return (SEG - (SEG >> L)) + e; }
+__device__ __forceinline__ int elim_pos_rt(int L, int e) { return (SEG - (SEG >> L)) + e; }
+
+// update of the surviving equation kq = 2^{L+1}·m at stride ST = 2^L (both neighbours already hold D⁻¹).
+// The level is a runtime argument: one copy of this code serves every level (instruction-cache footprint).
+__device__ __noinline__ void cr_update_rt(const CRS& s, int L, int m) {
+  const int ST = 1 << L;
+  const int kq = 2 * ST * m;
   const int pk = cr_pos(kq);
   double Ds[6], D[9], Br[9], r[3];
   ldv<6>(eqD(s, pk), Ds);
@@ -107,30 +115,40 @@ __device__ __forceinline__ void cr_update(const CRS& s, int kq, int st) {
   ldv<9>(eqB(s, pk), Br);
   ldv<3>(eqR(s, pk), r);
   double nBr[9] = {0, 0, 0, 0, 0, 0, 0, 0, 0};
-  if (kq >= st) {  // left neighbour i = kq − st:  α = Br_iᵀ D_i⁻¹;  D −= α Br_i;  r −= α r_i
-    const int pi = cr_pos(kq - st);
-    double Dis[6], Di[9], Bi[9], al[9], tmp[9], ri[3], ar[3];
+  if (m > 0) {  // left neighbour i = kq − st:  α = Br_iᵀ D_i⁻¹;  D −= α Br_i;  r −= α r_i
+    const int pi = elim_pos_rt(L, m - 1);
+    double Dis[6], Di[9], Bi[9], al[9], ri[3], ar[3];
     ldv<6>(eqD(s, pi), Dis);
     full_from_sym(Dis, Di);
     ldv<9>(eqB(s, pi), Bi);
     mat3_mul_at(Bi, Di, al);
-    mat3_mul(al, Bi, tmp);
 #pragma unroll
-    for (int e = 0; e < 9; ++e) D[e] -= tmp[e];
+    for (int r0 = 0; r0 < 3; ++r0)
+#pragma unroll
+      for (int c = r0; c < 3; ++c) {  // α Br_i is symmetric: lower part only
+        const double v = al[3 * r0] * Bi[c] + al[3 * r0 + 1] * Bi[3 + c] + al[3 * r0 + 2] * Bi[6 + c];
+        D[3 * r0 + c] -= v;
+        if (c != r0) D[3 * c + r0] -= v;
+      }
     ldv<3>(eqR(s, pi), ri);
     mat3_vec(al, ri, ar);
 #pragma unroll
     for (int e = 0; e < 3; ++e) r[e] -= ar[e];
   }
   if (kq < SEG) {  // right neighbour j = kq + st:  γ = Br_k D_j⁻¹;  D −= γ Br_kᵀ;  r −= γ r_j;  Br_k ← −γ Br_j
-    const int pj = cr_pos(kq + st);
+    const int pj = elim_pos_rt(L, m);
     double Djs[6], Dj[9], ga[9], tmp[9], Bj[9], rj[3], gr[3];
     ldv<6>(eqD(s, pj), Djs);
     full_from_sym(Djs, Dj);
     mat3_mul(Br, Dj, ga);
-    mat3_mul_bt(ga, Br, tmp);
 #pragma unroll
-    for (int e = 0; e < 9; ++e) D[e] -= tmp[e];
+    for (int r0 = 0; r0 < 3; ++r0)
+#pragma unroll
+      for (int c = r0; c < 3; ++c) {
+        const double v = ga[3 * r0] * Br[3 * c] + ga[3 * r0 + 1] * Br[3 * c + 1] + ga[3 * r0 + 2] * Br[3 * c + 2];
+        D[3 * r0 + c] -= v;
+        if (c != r0) D[3 * c + r0] -= v;
+      }
     ldv<3>(eqR(s, pj), rj);
     mat3_vec(ga, rj, gr);
 #pragma unroll
@@ -141,33 +159,60 @@ __device__ __forceinline__ void cr_update(const CRS& s, int kq, int st) {
     for (int e = 0; e < 9; ++e) nBr[e] = -tmp[e];
     stv<9>(eqBl(s, pj), Br);  // j's left coupling at this level (Bl_j = Br_kᵀ), kept for back substitution
   }
-  const double Dn[6] = {D[0], 0.5 * (D[1] + D[3]), 0.5 * (D[2] + D[6]), D[4], 0.5 * (D[5] + D[7]), D[8]};
+  const double Dn[6] = {D[0], D[1], D[2], D[4], D[5], D[8]};
   stv<6>(eqD(s, pk), Dn);
   stv<9>(eqB(s, pk), nBr);
   stv<3>(eqR(s, pk), r);
 }
 
-__device__ __forceinline__ void cr_invert(const CRS& s, int k, const StepConsts& ks) {
-  const int p = cr_pos(k);
+template <int L>
+__device__ __forceinline__ void cr_update(const CRS& s, int m) {
+  cr_update_rt(s, L, m);
+}
+
+__device__ __forceinline__ void cr_invert_at(const CRS& s, int p, const StepConsts& ks) {
   double Ds[6], Di[6];
   ldv<6>(eqD(s, p), Ds);
   if (!sym_inv_spd(Ds, Di)) report(ks, ERR_SINGULAR);
   stv<6>(eqD(s, p), Di);
 }
+__device__ __forceinline__ void cr_invert(const CRS& s, int k, const StepConsts& ks) { cr_invert_at(s, cr_pos(k), ks); }
 
-// Forward reduction. Precondition: every odd equation (eliminated at stride 1) already holds D⁻¹. A survivor
-// that will be eliminated at the next level inverts its own D right after its update (no one else reads a
-// survivor's D at this level), so each level needs one barrier.
-__device__ void cr_forward(const CRS& s, int t, const StepConsts& k) {
-  for (int st = 1; st < SEG; st <<= 1) {
-    const int ne = SEG / (2 * st);
-    for (int m = t; m <= ne; m += CT) {  // survivors k = 2st·m, m ≤ ne
-      const int kq = 2 * st * m;
-      cr_update(s, kq, st);
-      if ((m & 1) && 2 * st < SEG) cr_invert(s, kq, k);
-    }
-    __syncthreads();
+// One forward level at stride 2^L over survivors m = first, first+step, …; a survivor that is eliminated at the
+// next level (m odd) inverts its own D right after its update (no one else reads it at this level).
+__device__ __forceinline__ void cr_level_fwd_rt(const CRS& s, int L, int first, int step, const StepConsts& k) {
+  const int NE = SEG >> (L + 1);
+  for (int m = first; m <= NE; m += step) {
+    cr_update_rt(s, L, m);
+    if ((m & 1) && (2 << L) < SEG) cr_invert_at(s, elim_pos_rt(L + 1, m >> 1), k);
   }
+}
+template <int L>
+__device__ __forceinline__ void cr_level_fwd(const CRS& s, int first, int step, const StepConsts& k) {
+  cr_level_fwd_rt(s, L, first, step, k);
+}
+
+// Forward reduction, lower levels (strides 1, 2) by the whole CTA. Precondition: every odd equation already
+// holds D⁻¹. One barrier per level.
+template <int NT>
+__device__ __forceinline__ void cr_forward_lower(const CRS& s, int t, const StepConsts& k) {
+  cr_level_fwd<0>(s, t, NT, k);
+  __syncthreads();
+  cr_level_fwd<1>(s, t, NT, k);
+  __syncthreads();
+}
+// Upper levels (strides 4 … 128, ≤ 33 survivors) by one warp, warp-synchronous.
+__device__ __forceinline__ void cr_forward_upper(const CRS& s, int lane, const StepConsts& k) {
+#pragma unroll 1
+  for (int L = 2; L <= 7; ++L) {
+    cr_level_fwd_rt(s, L, lane, 32, k);
+    __syncwarp();
+  }
+}
+__device__ __forceinline__ void cr_forward(const CRS& s, int t, const StepConsts& k) {
+  cr_forward_lower<CT>(s, t, k);
+  if (t < 32) cr_forward_upper(s, t, k);
+  __syncthreads();
 }
 
 // Solve the remaining 2-equation system [D0 B; Bᵀ D1][λ0; λ1] = [r0; r1] (one thread).
@@ -209,39 +254,62 @@ __device__ void cr_solve_top(const CRS& s, const StepConsts& k) {
   stv<3>(eqR(s, p1), l1);
 }
 
-// Back substitution; λ of equations 0 and 256 are in r on entry, all λ on exit.
-__device__ void cr_backward(const CRS& s, int t) {
-  for (int st = SEG / 2; st >= 1; st >>= 1) {
-    const int ne = SEG / (2 * st);
-    for (int m = t; m < ne; m += CT) {
-      const int i = st * (2 * m + 1);
-      const int pi = cr_pos(i);
-      double Bl[9], Br[9], Di[6], ll[3], lr[3], v[3], w[3];
-      ldv<9>(eqBl(s, pi), Bl);
-      ldv<9>(eqB(s, pi), Br);
-      ldv<6>(eqD(s, pi), Di);
-      ldv<3>(eqR(s, cr_pos(i - st)), ll);
-      ldv<3>(eqR(s, cr_pos(i + st)), lr);
-      ldv<3>(eqR(s, pi), v);
-      mat3t_vec(Bl, ll, w);  // Bl_i λ_{i−s} = Br_{i−s}ᵀ λ_{i−s}
+// Back substitution at stride 2^L: eliminated i = 2^L·(2m+1), m = first, first+step, … < NE.
+__device__ __noinline__ void cr_bwd_one(const CRS& s, int L, int m) {
+  const int ST = 1 << L;
+  const int i = ST * (2 * m + 1);
+  const int pi = elim_pos_rt(L, m);
+  double Bl[9], Br[9], Di[6], ll[3], lr[3], v[3], w[3];
+  ldv<9>(eqBl(s, pi), Bl);
+  ldv<9>(eqB(s, pi), Br);
+  ldv<6>(eqD(s, pi), Di);
+  ldv<3>(eqR(s, cr_pos(i - ST)), ll);
+  ldv<3>(eqR(s, cr_pos(i + ST)), lr);
+  ldv<3>(eqR(s, pi), v);
+  mat3t_vec(Bl, ll, w);  // Bl_i λ_{i−s} = Br_{i−s}ᵀ λ_{i−s}
 #pragma unroll
-      for (int e = 0; e < 3; ++e) v[e] -= w[e];
-      mat3_vec(Br, lr, w);
+  for (int e = 0; e < 3; ++e) v[e] -= w[e];
+  mat3_vec(Br, lr, w);
 #pragma unroll
-      for (int e = 0; e < 3; ++e) v[e] -= w[e];
-      sym_vec(Di, v, w);
-      stv<3>(eqR(s, pi), w);
-    }
-    __syncthreads();
+  for (int e = 0; e < 3; ++e) v[e] -= w[e];
+  sym_vec(Di, v, w);
+  stv<3>(eqR(s, pi), w);
+}
+__device__ __forceinline__ void cr_level_bwd_rt(const CRS& s, int L, int first, int step) {
+  const int NE = SEG >> (L + 1);
+  for (int m = first; m < NE; m += step) cr_bwd_one(s, L, m);
+}
+template <int L>
+__device__ __forceinline__ void cr_level_bwd(const CRS& s, int first, int step) {
+  cr_level_bwd_rt(s, L, first, step);
+}
+// λ of equations 0 and 256 are in r on entry, all λ on exit. Upper levels by one warp, then the CTA.
+__device__ __forceinline__ void cr_backward_upper(const CRS& s, int lane) {
+#pragma unroll 1
+  for (int L = 7; L >= 2; --L) {
+    cr_level_bwd_rt(s, L, lane, 32);
+    __syncwarp();
   }
+}
+template <int NT>
+__device__ __forceinline__ void cr_backward_lower(const CRS& s, int t) {
+  cr_level_bwd<1>(s, t, NT);
+  __syncthreads();
+  cr_level_bwd<0>(s, t, NT);
+  __syncthreads();
+}
+__device__ __forceinline__ void cr_backward(const CRS& s, int t) {
+  if (t < 32) cr_backward_upper(s, t);
+  __syncthreads();
+  cr_backward_lower<CT>(s, t);
 }
 
 __device__ __forceinline__ CRS cr_smem(double* smem) {
   CRS s;
   s.D = smem;
-  s.B = s.D + NEQ * 6;
-  s.Bl = s.B + NEQ * 9;
-  s.r = s.Bl + NEQ * 9;
+  s.B = s.D + LDS * 6;
+  s.Bl = s.B + LDS * 9;
+  s.r = s.Bl + LDS * 9;
   return s;
 }
 
@@ -254,58 +322,198 @@ __device__ __forceinline__ void write_top(const CRS& s, Top* o) {
   ldv<3>(eqR(s, p1), o->r1);
 }
 
-__device__ __forceinline__ void body_material(const ChainArgs& a, int64_t slot, Material& M, double& msc,
-                                              HinvBlk& H) {
-  const int mid = a.b.mat_id ? __ldg(a.b.mat_id + slot) : 0;
-  msc = a.b.mscale ? __ldg(a.b.mscale + slot) : 1.0;
-  M = a.b.mats[mid];
+// ------------------------------------------------------------------ the fused chain segment kernel
+// Persistent: each 128-thread CTA (4 per SM) loops over segments it ← blockIdx.x, += gridDim.x; thread t owns
+// slots t and t+128 (the bodies at those positions and the joints to their left).
+//   staging:  the segment's qⁿ, q̇ⁿ rows (24 × 2 KB) arrive by TMA bulk copies (cp.async.bulk, completion on an
+//             mbarrier) into the CR rows D/B/Bl, its slot-code / mass-scale / material rows into the CR rows r;
+//             all of them are dead while the previous segment finishes phase 3. No L2 round trip of the state
+//             is on the critical path.
+//   phase 1:  each thread moves its two bodies' qⁿ, q̇ⁿ into tensor memory (TMEM, 96 of the CTA's 128 columns,
+//             its own lane), barrier (the CR rows are free), then per body: predict (stages 1-2) with δq̃ kept
+//             in TMEM over q̇ⁿ, and assemble the joint equations (stage 3). TMEM is used purely as per-thread
+//             storage (12-cycle loads): it carries qⁿ and δq̃ across the solve without registers, shared or
+//             global memory, so shared memory holds only the CR arrays and 4 CTAs fit per SM.
+//   phase 2:  block cyclic reduction (stage 3 solve)
+//   phase 3:  read λ, barrier, stage the next segment, then per body: recompute R = polar(Aⁿ) (the same
+//             arithmetic as phase 1, so the same R), qⁿ⁺¹ = q̃ − diag₄(R)H̄⁻¹Σ±Γᵀ Rᵀλ, q̇ⁿ⁺¹ = δq/h → HBM.
+// FINISH = false: first pass (fused segments solve completely; long segments REDUCE to their top);
+// FINISH = true: second pass of long segments (recompute, read the ends' λ, back-substitute, update).
+constexpr int SLOT_ROW = SEG + 4;    // staged slot codes per segment (257 used, padded to 16 B)
+constexpr int TMEM_COLS = 128;       // per CTA: 2 bodies × (24 words qⁿ + 24 words q̇ⁿ/δq̃ + 12 words λ) = 120
+
+__host__ __device__ constexpr size_t chain_smem_size() { return sizeof(double) * LDS * 27 + 16; }
+
+__device__ __forceinline__ uint32_t smem_u32(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
+__device__ __forceinline__ void mbar_init(uint64_t* bar) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(smem_u32(bar)));
+  asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+}
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ bool mbar_try_wait(uint64_t* bar, uint32_t parity) {
+  uint32_t ok;
+  asm volatile(
+      "{\n .reg .pred p;\n mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n selp.u32 %0, 1, 0, p;\n}\n"
+      : "=r"(ok)
+      : "r"(smem_u32(bar)), "r"(parity)
+      : "memory");
+  return ok != 0;
+}
+__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(smem_u32(dst)),
+      "l"(src), "r"(bytes), "r"(smem_u32(bar))
+      : "memory");
+}
+
+// TMEM as per-thread storage: 8 doubles (16 columns) of this thread's lane per call, warp-collective.
+__device__ __forceinline__ void tm_st8(uint32_t taddr, const double* v) {
+  uint32_t w[16];
+#pragma unroll
+  for (int i = 0; i < 8; ++i) {
+    const unsigned long long b = (unsigned long long)__double_as_longlong(v[i]);
+    w[2 * i] = (uint32_t)b;
+    w[2 * i + 1] = (uint32_t)(b >> 32);
+  }
+  asm volatile(
+      "tcgen05.st.sync.aligned.32x32b.x16.b32 [%0], {%1, %2, %3, %4, %5, %6, %7, %8, %9, %10, %11, %12, %13, %14, "
+      "%15, %16};" ::"r"(taddr),
+      "r"(w[0]), "r"(w[1]), "r"(w[2]), "r"(w[3]), "r"(w[4]), "r"(w[5]), "r"(w[6]), "r"(w[7]), "r"(w[8]), "r"(w[9]),
+      "r"(w[10]), "r"(w[11]), "r"(w[12]), "r"(w[13]), "r"(w[14]), "r"(w[15])
+      : "memory");
+}
+__device__ __forceinline__ void tm_ld8(uint32_t taddr, double* v) {
+  uint32_t w[16];
+  asm volatile(
+      "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0, %1, %2, %3, %4, %5, %6, %7, %8, %9, %10, %11, %12, %13, %14, "
+      "%15}, [%16];"
+      : "=r"(w[0]), "=r"(w[1]), "=r"(w[2]), "=r"(w[3]), "=r"(w[4]), "=r"(w[5]), "=r"(w[6]), "=r"(w[7]), "=r"(w[8]),
+        "=r"(w[9]), "=r"(w[10]), "=r"(w[11]), "=r"(w[12]), "=r"(w[13]), "=r"(w[14]), "=r"(w[15])
+      : "r"(taddr)
+      : "memory");
+  asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+#pragma unroll
+  for (int i = 0; i < 8; ++i)
+    v[i] = __longlong_as_double((long long)(((unsigned long long)w[2 * i + 1] << 32) | w[2 * i]));
+}
+// 4 doubles (8 columns) and 2 doubles (4 columns)
+__device__ __forceinline__ void tm_st4(uint32_t taddr, const double* v) {
+  uint32_t w[8];
+#pragma unroll
+  for (int i = 0; i < 4; ++i) {
+    const unsigned long long b = (unsigned long long)__double_as_longlong(v[i]);
+    w[2 * i] = (uint32_t)b;
+    w[2 * i + 1] = (uint32_t)(b >> 32);
+  }
+  asm volatile("tcgen05.st.sync.aligned.32x32b.x8.b32 [%0], {%1, %2, %3, %4, %5, %6, %7, %8};" ::"r"(taddr),
+               "r"(w[0]), "r"(w[1]), "r"(w[2]), "r"(w[3]), "r"(w[4]), "r"(w[5]), "r"(w[6]), "r"(w[7])
+               : "memory");
+}
+__device__ __forceinline__ void tm_ld4(uint32_t taddr, double* v) {
+  uint32_t w[8];
+  asm volatile("tcgen05.ld.sync.aligned.32x32b.x8.b32 {%0, %1, %2, %3, %4, %5, %6, %7}, [%8];"
+               : "=r"(w[0]), "=r"(w[1]), "=r"(w[2]), "=r"(w[3]), "=r"(w[4]), "=r"(w[5]), "=r"(w[6]), "=r"(w[7])
+               : "r"(taddr)
+               : "memory");
+  asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+#pragma unroll
+  for (int i = 0; i < 4; ++i)
+    v[i] = __longlong_as_double((long long)(((unsigned long long)w[2 * i + 1] << 32) | w[2 * i]));
+}
+__device__ __forceinline__ void tm_st2(uint32_t taddr, const double* v) {
+  uint32_t w[4];
+#pragma unroll
+  for (int i = 0; i < 2; ++i) {
+    const unsigned long long b = (unsigned long long)__double_as_longlong(v[i]);
+    w[2 * i] = (uint32_t)b;
+    w[2 * i + 1] = (uint32_t)(b >> 32);
+  }
+  asm volatile("tcgen05.st.sync.aligned.32x32b.x4.b32 [%0], {%1, %2, %3, %4};" ::"r"(taddr), "r"(w[0]), "r"(w[1]),
+               "r"(w[2]), "r"(w[3])
+               : "memory");
+}
+__device__ __forceinline__ void tm_ld2(uint32_t taddr, double* v) {
+  uint32_t w[4];
+  asm volatile("tcgen05.ld.sync.aligned.32x32b.x4.b32 {%0, %1, %2, %3}, [%4];"
+               : "=r"(w[0]), "=r"(w[1]), "=r"(w[2]), "=r"(w[3])
+               : "r"(taddr)
+               : "memory");
+  asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+#pragma unroll
+  for (int i = 0; i < 2; ++i)
+    v[i] = __longlong_as_double((long long)(((unsigned long long)w[2 * i + 1] << 32) | w[2 * i]));
+}
+// 12 doubles = exactly columns c0 … c0+23
+__device__ __forceinline__ void tm_st12(uint32_t taddr, const double* v) {
+  tm_st8(taddr, v);
+  tm_st4(taddr + 16, v + 8);
+}
+__device__ __forceinline__ void tm_ld12(uint32_t taddr, double* v) {
+  tm_ld8(taddr, v);
+  tm_ld4(taddr + 16, v + 8);
+}
+// 6 doubles = columns c0 … c0+11
+__device__ __forceinline__ void tm_st6(uint32_t taddr, const double* v) {
+  tm_st4(taddr, v);
+  tm_st2(taddr + 8, v + 4);
+}
+__device__ __forceinline__ void tm_ld6(uint32_t taddr, double* v) {
+  tm_ld4(taddr, v);
+  tm_ld2(taddr + 8, v + 4);
+}
+__device__ __forceinline__ void tm_wait_st() { asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory"); }
+
+// Thread 0: stage segment `it` and arm the mbarrier; the caller has made every earlier read of the CR rows
+// happen-before (barrier).
+__device__ __forceinline__ void stage_segment(const ChainArgs& a, double* cr, uint64_t* bar, int it) {
+  if (it >= a.n_items) return;
+  const int g = a.seg_list ? a.seg_list[it] : it;
+  const int64_t base = (int64_t)g * SEG;
+  asm volatile("fence.proxy.async.shared::cta;" ::: "memory");  // generic-proxy accesses before async writes
+  uint32_t bytes = 24 * SEG * sizeof(double) + SLOT_ROW * sizeof(uint32_t);
+  if (a.b.mscale) bytes += SEG * sizeof(double);
+  if (a.b.mat_id) bytes += SEG * sizeof(int32_t);
+  mbar_expect_tx(bar, bytes);
+  for (int r = 0; r < 12; ++r) {
+    bulk_g2s(cr + r * LDS, a.b.q + r * a.b.ld + base, SEG * sizeof(double), bar);
+    bulk_g2s(cr + (12 + r) * LDS, a.b.qd + r * a.b.ld + base, SEG * sizeof(double), bar);
+  }
+  bulk_g2s(cr + 24 * LDS, a.slot_info + base, SLOT_ROW * sizeof(uint32_t), bar);
+  if (a.b.mscale) bulk_g2s(cr + 25 * LDS, a.b.mscale + base, SEG * sizeof(double), bar);
+  if (a.b.mat_id) bulk_g2s(cr + 26 * LDS, a.b.mat_id + base, SEG * sizeof(int32_t), bar);
+}
+
+__device__ __forceinline__ void get_hinv(const ChainArgs& a, const Material& M, int mid, double msc, HinvBlk& H) {
   if (a.hinv_tab)
     H = a.hinv_tab[mid];
   else
     hinv_blocks(M, msc, a.k.ih2, H);
 }
 
-// ------------------------------------------------------------------ the fused chain segment kernel
-// Persistent: each CTA loops over segments it ← blockIdx.x, += gridDim.x. While a segment is in the
-// cyclic reduction (no memory traffic), the CTA prefetches the NEXT segment's state into L2, so its
-// phase-1 loads are L2 hits (software pipeline across segments).
-// FINISH = false: first pass (fused segments solve completely; long segments REDUCE to their top);
-// FINISH = true: second pass of long segments (recompute, read the ends' λ, back-substitute, update).
-__device__ __forceinline__ void prefetch_segment(const ChainArgs& a, int it, int tid) {
-  if (it >= a.n_items) return;
-  const int g = a.seg_list ? a.seg_list[it] : it;
-  const int64_t base = (int64_t)g * SEG;
-#pragma unroll
-  for (int b = 0; b < 2; ++b) {
-    const int64_t sl = base + tid + b * CT;
-#pragma unroll
-    for (int c = 0; c < 12; ++c) {
-      l2_prefetch(a.b.q + c * a.b.ld + sl);
-      l2_prefetch(a.b.qd + c * a.b.ld + sl);
-    }
-    if (a.b.mscale) l2_prefetch(a.b.mscale + sl);
-    l2_prefetch(a.slot_info + sl);
-  }
-}
-
-#ifndef MABD_CHAIN_MINB
-#define MABD_CHAIN_MINB 4
-#endif
 template <bool FINISH>
-__global__ void __launch_bounds__(CT, MABD_CHAIN_MINB) chain_kernel(ChainArgs a) {
-  extern __shared__ double smem[];
+__global__ void __launch_bounds__(CT, 4) chain_kernel(ChainArgs a) {
+  extern __shared__ __align__(16) double smem[];
   const CRS s = cr_smem(smem);
-  const int tid = threadIdx.x;
+  uint64_t* bar = reinterpret_cast<uint64_t*>(smem + LDS * 27);
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bar + 1);
+  const int tid = threadIdx.x, warp = tid >> 5;
   const StepConsts& k = a.k;
-  if ((int)blockIdx.x < a.n_items) {  // first segment: its second body is fetched while the first is loaded
-    const int g0 = a.seg_list ? a.seg_list[blockIdx.x] : (int)blockIdx.x;
-    const int64_t s2 = (int64_t)g0 * SEG + tid + CT;
-#pragma unroll
-    for (int c = 0; c < 12; ++c) {
-      l2_prefetch(a.b.q + c * a.b.ld + s2);
-      l2_prefetch(a.b.qd + c * a.b.ld + s2);
-    }
+  if (warp == 0) {  // TMEM: 128 columns for this CTA
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tmem_slot)),
+                 "n"(TMEM_COLS));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
   }
+  if (tid == 0) {
+    mbar_init(bar);
+    stage_segment(a, smem, bar, blockIdx.x);
+  }
+  asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+  __syncthreads();
+  asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+  const uint32_t tbase = *tmem_slot + ((uint32_t)(32 * warp) << 16);  // this warp's lane quarter
+  uint32_t phase = 0;
 #ifdef MABD_EXP_CLOCK
   long long ph_last = clock64();
 #endif
@@ -315,24 +523,55 @@ __global__ void __launch_bounds__(CT, MABD_CHAIN_MINB) chain_kernel(ChainArgs a)
     const int flags = a.seg_flags[g];
     const bool is_long = (flags & SEG_LONG) != 0;
     const bool update = !is_long || FINISH;  // this pass writes the new state
+    const bool reduce_only = is_long && !FINISH;
     const int64_t base = (int64_t)g * SEG;
+    while (!mbar_try_wait(bar, phase)) {
+    }
+    phase ^= 1;
 
-    // ---------------- phase 1: per body predict + joint contributions (thread tid: slots tid, tid+128)
-    // Equation t is assembled in place: sD[t] = D part of body t, sR[t] = rhs part, sB[t] = B_t; body t's
-    // contribution to equation t+1 goes to the scratch row sBl[t+1] and is added after the barrier.
-    uint32_t infos[3];
-    infos[0] = __ldg(a.slot_info + base + tid);
-    infos[1] = __ldg(a.slot_info + base + tid + 1);
-    infos[2] = __ldg(a.slot_info + base + tid + CT + 1);
+    // ---------------- phase 1a: staged rows → registers (slot codes, mass scale, material) and TMEM (qⁿ, q̇ⁿ)
+    // per-slot scalars of the two bodies as separate registers (a runtime-indexed array would go to local memory)
+    uint32_t info0, info1, infoN0, infoN1;
+    double msc0, msc1;
+    int mid0, mid1;
+    {
+      const uint32_t* sinfo = reinterpret_cast<const uint32_t*>(smem + 24 * LDS);
+      const int32_t* smid = reinterpret_cast<const int32_t*>(smem + 26 * LDS);
+      info0 = sinfo[tid];
+      infoN0 = sinfo[tid + 1];
+      info1 = sinfo[tid + CT];
+      infoN1 = sinfo[tid + CT + 1];
+      msc0 = a.b.mscale ? smem[25 * LDS + tid] : 1.0;
+      msc1 = a.b.mscale ? smem[25 * LDS + tid + CT] : 1.0;
+      mid0 = a.b.mat_id ? smid[tid] : 0;
+      mid1 = a.b.mat_id ? smid[tid + CT] : 0;
+#pragma unroll
+      for (int b = 0; b < 2; ++b) {
+        const int t = tid + b * CT;
+        double v[12];
+#pragma unroll
+        for (int r = 0; r < 12; ++r) v[r] = smem[r * LDS + t];
+        tm_st12(tbase + 48 * b, v);
+#pragma unroll
+        for (int r = 0; r < 12; ++r) v[r] = smem[(12 + r) * LDS + t];
+        tm_st12(tbase + 48 * b + 24, v);
+      }
+    }
+    tm_wait_st();
+    __syncthreads();  // the staged rows are consumed: the CR rows take the equations
+
+    // ---------------- phase 1b: per body predict + joint contributions
+    // Equation t is assembled in place: D part of body t, rhs part, B_t; body t's contribution to equation
+    // t+1 goes to the scratch row Bl[t+1] and is added after the barrier.
 #pragma unroll 1
     for (int b = 0; b < 2; ++b) {
       const int t = tid + b * CT;
-      const int64_t slot = base + t;
-      const uint32_t info = b == 0 ? infos[0] : __ldg(a.slot_info + slot);
-      const uint32_t infoN = infos[1 + b];
-      const bool has_body = slot_right(info) == SIDE_BODY;
-      const bool eq_real = slot_real(info);
-      const bool right_real = slot_real(infoN) && slot_left(infoN) == SIDE_BODY;
+      const uint32_t inf = b ? info1 : info0, infN = b ? infoN1 : infoN0;
+      const double msb = b ? msc1 : msc0;
+      const int mdb = b ? mid1 : mid0;
+      const bool has_body = slot_right(inf) == SIDE_BODY;
+      const bool eq_real = slot_real(inf);
+      const bool right_real = slot_real(infN) && slot_left(infN) == SIDE_BODY;
       const int pt = cr_pos(t);
       const SV sd = eqD(s, pt), sr = eqR(s, pt), sb = eqB(s, pt);
       const SV sx = eqBl(s, cr_pos(t + 1));  // scratch row: body t's contribution to equation t+1
@@ -341,11 +580,11 @@ __global__ void __launch_bounds__(CT, MABD_CHAIN_MINB) chain_kernel(ChainArgs a)
         sd[0] = one; sd[1] = 0; sd[2] = 0; sd[3] = one; sd[4] = 0; sd[5] = one;
         double rr[3] = {0, 0, 0};
         if (eq_real) {
-          const double* gp = a.geo + 6 * (size_t)slot_geo(info);
-          if (slot_left(info) == SIDE_WORLD)  // start anchor: +p_world
+          const double* gp = a.geo + 6 * (size_t)slot_geo(inf);
+          if (slot_left(inf) == SIDE_WORLD)  // start anchor: +p_world
 #pragma unroll
             for (int e = 0; e < 3; ++e) rr[e] = __ldg(gp + e);
-          if (slot_right(info) == SIDE_WORLD)  // end anchor: −p_world
+          if (slot_right(inf) == SIDE_WORLD)  // end anchor: −p_world
 #pragma unroll
             for (int e = 0; e < 3; ++e) rr[e] -= __ldg(gp + 3 + e);
         }
@@ -356,54 +595,62 @@ __global__ void __launch_bounds__(CT, MABD_CHAIN_MINB) chain_kernel(ChainArgs a)
 #pragma unroll
         for (int e = 0; e < 9; ++e) sx[e] = 0.0;
       }
-      if (has_body) {
-        double q[12], R[9];
-        HinvBlk H;
-        {
-          double qd[12], dqt[12];
-          double* qdb = a.b.qd + slot;
-          const double* qb = a.b.q + slot;
+      // every lane runs the predict (warp-collective TMEM loads inside); slots without a body use A = I
+      double q[12], dqt[12], R[9];
+      HinvBlk H;
+      {
+        tm_ld12(tbase + 48 * b, q);
+        if (!has_body) {
 #pragma unroll
-          for (int c = 0; c < 12; ++c) q[c] = qb[c * a.b.ld];
-#pragma unroll
-          for (int c = 0; c < 12; ++c) qd[c] = qdb[c * a.b.ld];
-          Material M;
-          double msc;
-          body_material(a, slot, M, msc, H);
-          if (!predict_body(q, qd, M, msc, H, k.ih, k.grav, R, dqt)) report(k, ERR_NONFINITE);
-          if (update) {
-#pragma unroll
-            for (int c = 0; c < 12; ++c) qdb[c * a.b.ld] = dqt[c];  // park δq̃ (q̇ⁿ is dead from here on)
-#pragma unroll
-            for (int c = 0; c < 9; ++c) a.b.rs[c * a.b.ld + slot] = R[c];  // park R (L2 scratch)
-          }
-#pragma unroll
-          for (int c = 0; c < 12; ++c) q[c] += dqt[c];  // q̃
+          for (int r = 0; r < 12; ++r) q[r] = (r == 0 || r == 4 || r == 8) ? 1.0 : 0.0;
         }
-        double P[9], F[6], yR[3], yL[3], x[3];
-        if (eq_real) {  // joint to the left: this body is its right side (sign −)
-          const double* gp = a.geo + 6 * (size_t)slot_geo(info);
+        const Material M = a.b.mats[mdb];
+        const double ms = msb;
+        const int md = mdb;
+        const bool ok = predict_body_lazy(
+            q, [&](double* o) { tm_ld12(tbase + 48 * b + 24, o); }, M, ms,
+            [&](HinvBlk& o) { get_hinv(a, M, md, ms, o); }, H, k.ih, k.grav, R, dqt);
+        if (!ok && has_body) report(k, ERR_NONFINITE);
+      }
+      if (update) tm_st12(tbase + 48 * b + 24, dqt);  // δq̃ over q̇ⁿ (warp-collective: every lane)
+      if (has_body) {
+#pragma unroll
+        for (int r = 0; r < 12; ++r) q[r] += dqt[r];  // q̃
+        double y[3], x[3];
+        if (eq_real) {  // joint to the left: this body is its right side (sign −): r_t −= x(q̃; ȳ_R)
+          const double* gp = a.geo + 6 * (size_t)slot_geo(inf);
+#pragma unroll
+          for (int e = 0; e < 3; ++e) y[e] = __ldg(gp + 3 + e);
+          point_pos(q, y, x);
+#pragma unroll
+          for (int e = 0; e < 3; ++e) sr[e] -= x[e];
+        }
+        if (right_real) {  // joint to the right: this body is its left side (sign +): r_{t+1} += x(q̃; ȳ_L)
+          const double* gp = a.geo + 6 * (size_t)slot_geo(infN);
+#pragma unroll
+          for (int e = 0; e < 3; ++e) y[e] = __ldg(gp + e);
+          point_pos(q, y, x);
+#pragma unroll
+          for (int e = 0; e < 3; ++e) sx[6 + e] = x[e];
+        }
+        double P[9], F[6], yR[3], yL[3];
+        if (eq_real) {  // D_t += R P(ȳ_R, ȳ_R) Rᵀ
+          const double* gp = a.geo + 6 * (size_t)slot_geo(inf);
 #pragma unroll
           for (int e = 0; e < 3; ++e) yR[e] = __ldg(gp + 3 + e);
           pblock(H, yR, yR, P);
           rot_conj_sym(R, P, F);
 #pragma unroll
           for (int e = 0; e < 6; ++e) sd[e] = F[e];
-          point_pos(q, yR, x);
-#pragma unroll
-          for (int e = 0; e < 3; ++e) sr[e] -= x[e];
         }
-        if (right_real) {  // joint to the right: this body is its left side (sign +)
-          const double* gp = a.geo + 6 * (size_t)slot_geo(infoN);
+        if (right_real) {  // D_{t+1} += R P(ȳ_L, ȳ_L) Rᵀ
+          const double* gp = a.geo + 6 * (size_t)slot_geo(infN);
 #pragma unroll
           for (int e = 0; e < 3; ++e) yL[e] = __ldg(gp + e);
           pblock(H, yL, yL, P);
           rot_conj_sym(R, P, F);
 #pragma unroll
           for (int e = 0; e < 6; ++e) sx[e] = F[e];
-          point_pos(q, yL, x);
-#pragma unroll
-          for (int e = 0; e < 3; ++e) sx[6 + e] = x[e];
           if (eq_real) {  // B_t = −R P(ȳ_R, ȳ_L') Rᵀ  (signs −·+)
             double Fb[9];
             pblock(H, yR, yL, P);
@@ -414,16 +661,17 @@ __global__ void __launch_bounds__(CT, MABD_CHAIN_MINB) chain_kernel(ChainArgs a)
         }
       }
     }
+    tm_wait_st();
     PH_MARK(0);
     __syncthreads();
     PH_MARK(1);
-    // add the left neighbours' contributions (equation 0's left body lies in the previous segment: its part
-    // of the interface equation is added by that segment's REDUCE output)
-#pragma unroll 1
+    // add the left neighbour's contribution (equation 0's left body lies in the previous segment: its part of
+    // the interface equation is added by that segment's REDUCE output)
+#pragma unroll
     for (int b = 0; b < 2; ++b) {
       const int t = tid + b * CT;
-      const uint32_t info = b == 0 ? infos[0] : __ldg(a.slot_info + base + t);
-      if (t > 0 && slot_real(info) && slot_left(info) == SIDE_BODY) {
+      const uint32_t inf = b ? info1 : info0;
+      if (t > 0 && slot_real(inf) && slot_left(inf) == SIDE_BODY) {
         const int pt = cr_pos(t);
         const SV x = eqBl(s, pt), d = eqD(s, pt), r = eqR(s, pt);
 #pragma unroll
@@ -448,112 +696,142 @@ __global__ void __launch_bounds__(CT, MABD_CHAIN_MINB) chain_kernel(ChainArgs a)
     }
     __syncthreads();
 
-    // ---------------- phase 2: block cyclic reduction (the next segment's state streams into L2 meanwhile)
+    // ---------------- phase 2: block cyclic reduction
     PH_MARK(2);
-    prefetch_segment(a, it + gridDim.x, tid);
 #ifndef MABD_EXP_SKIP_CR
-    cr_forward(s, tid, k);
-#endif
-    PH_MARK(3);
-    if (!is_long) {
-      if (tid == 0) cr_solve_top(s, k);
-    } else if (!FINISH) {
-      if (tid == 0) write_top(s, a.top_out + a.seg_red[g]);
-      __syncthreads();
-      continue;
-    } else if (tid == 0) {
-      const int u = a.seg_red[g];
+    cr_forward_lower<CT>(s, tid, k);
+    PH_MARK(8);
+    if (tid < 32) {  // upper levels, the 2-equation top and the upper back substitution: warp 0 alone
+      cr_forward_upper(s, tid, k);
+      PH_MARK(9);
+      if (tid == 0) {
+        if (!is_long) {
+          cr_solve_top(s, k);
+        } else if (!FINISH) {
+          write_top(s, a.top_out + a.seg_red[g]);
+        } else {
+          const int u = a.seg_red[g];
 #pragma unroll
-      for (int e = 0; e < 3; ++e) {
-        eqR(s, cr_pos(0))[e] = a.lam_in[3 * u + e];
-        eqR(s, SEG)[e] = (flags & SEG_RIGHT_IFACE) ? a.lam_in[3 * (u + 1) + e] : 0.0;
+          for (int e = 0; e < 3; ++e) {
+            eqR(s, cr_pos(0))[e] = a.lam_in[3 * u + e];
+            eqR(s, SEG)[e] = (flags & SEG_RIGHT_IFACE) ? a.lam_in[3 * (u + 1) + e] : 0.0;
+          }
+        }
       }
+      __syncwarp();
+      PH_MARK(10);
+      if (!reduce_only) cr_backward_upper(s, tid);
+      PH_MARK(11);
     }
     __syncthreads();
+    PH_MARK(3);
+    if (reduce_only) {  // REDUCE pass of a long segment: its top is written, nothing else to do
+      if (tid == 0) stage_segment(a, smem, bar, it + gridDim.x);
+      continue;
+    }
     PH_MARK(4);
-#ifndef MABD_EXP_SKIP_CR
-    cr_backward(s, tid);
+    cr_backward_lower<CT>(s, tid);
+#else
+    __syncthreads();
+    if (reduce_only) {
+      if (tid == 0) stage_segment(a, smem, bar, it + gridDim.x);
+      continue;
+    }
 #endif
     PH_MARK(5);
+    // ---------------- phase 3: qⁿ⁺¹ = q̃ − diag₄(R) H̄⁻¹ Σ ±Γ(ȳ)ᵀ Rᵀλ (P:479, P:598-610)
+#pragma unroll
+    for (int b = 0; b < 2; ++b) {  // λ of the joints left and right of each body → TMEM columns 96 + 12b
+      const int t = tid + b * CT;
+      double l[6];
+#pragma unroll
+      for (int e = 0; e < 3; ++e) {
+        l[e] = eqR(s, cr_pos(t))[e];
+        l[3 + e] = eqR(s, cr_pos(t + 1))[e];
+      }
+      tm_st6(tbase + 96 + 12 * b, l);
+    }
+    tm_wait_st();
+    __syncthreads();  // λ read: every CR row is dead, stage the next segment into them
+    if (tid == 0) stage_segment(a, smem, bar, it + gridDim.x);
 #ifdef MABD_EXP_SKIP_P3
-    __syncthreads();
     continue;
 #endif
-
-    // ---------------- phase 3: qⁿ⁺¹ = q̃ − diag₄(R) H̄⁻¹ Σ ±Γ(ȳ)ᵀ Rᵀλ (P:479, P:598-610)
 #pragma unroll 1
     for (int b = 0; b < 2; ++b) {
       const int t = tid + b * CT;
       const int64_t slot = base + t;
-      const uint32_t info = b == 0 ? infos[0] : __ldg(a.slot_info + slot);
-      const uint32_t infoN = infos[1 + b];
-      double* qb = a.b.q + slot;
-      double* qdb = a.b.qd + slot;
-      // issue every load of this body first: R (parked), qⁿ, δq̃ (parked) — all L2 hits
-      double R[9], q[12], dqt[12];
-      const double* rp = a.b.rs + slot;
+      const uint32_t inf = b ? info1 : info0, infN = b ? infoN1 : infoN0;
+      const double msb = b ? msc1 : msc0;
+      const int mdb = b ? mid1 : mid0;
+      double lam[6];
+      tm_ld6(tbase + 96 + 12 * b, lam);
+      const bool has_body = slot_right(inf) == SIDE_BODY;
+      const bool eq_real = slot_real(inf);
+      const bool right_real = slot_real(infN) && slot_left(infN) == SIDE_BODY;
+      double R[9], u[12];
+      {
+        double q[12];
+        tm_ld12(tbase + 48 * b, q);
+        double A[9];
 #pragma unroll
-      for (int c = 0; c < 9; ++c) R[c] = __ldcg(rp + c * a.b.ld);
+        for (int r = 0; r < 3; ++r)
 #pragma unroll
-      for (int c = 0; c < 12; ++c) q[c] = __ldcs(qb + c * a.b.ld);
-#pragma unroll
-      for (int c = 0; c < 12; ++c) dqt[c] = __ldcs(qdb + c * a.b.ld);
-      // all lanes have their R: discard the scratch lines (no DRAM write-back); the warp covers 32
-      // consecutive, 256-B aligned slots = two 128-B lines per row
-      __syncwarp();
-      if ((threadIdx.x & 15) == 0) {
-#pragma unroll
-        for (int c = 0; c < 9; ++c) l2_discard128(rp + c * a.b.ld);
+          for (int cc = 0; cc < 3; ++cc) A[3 * r + cc] = q[3 * cc + r];
+        polar_rotation(A, R);  // the same R as phase 1 (same input, same arithmetic)
       }
-      if (slot_right(info) != SIDE_BODY) continue;
-      const bool eq_real = slot_real(info);
-      const bool right_real = slot_real(infoN) && slot_left(infoN) == SIDE_BODY;
-      double gq[12];
+      {
+        double gq[12];
 #pragma unroll
-      for (int c = 0; c < 12; ++c) gq[c] = 0.0;
-      double w[3], lam[3], y[3];
-      if (eq_real) {
-        const double* gp = a.geo + 6 * (size_t)slot_geo(info);
+        for (int r = 0; r < 12; ++r) gq[r] = 0.0;
+        double w[3], y[3];
+        if (eq_real) {
+          const double* gp = a.geo + 6 * (size_t)slot_geo(inf);
 #pragma unroll
-        for (int e = 0; e < 3; ++e) {
-          y[e] = __ldg(gp + 3 + e);
-          lam[e] = eqR(s, cr_pos(t))[e];
+          for (int e = 0; e < 3; ++e) y[e] = __ldg(gp + 3 + e);
+          mat3t_vec(R, lam, w);
+          add_point_force(gq, y, w, -1.0);
         }
-        mat3t_vec(R, lam, w);
-        add_point_force(gq, y, w, -1.0);
-      }
-      if (right_real) {
-        const double* gp = a.geo + 6 * (size_t)slot_geo(infoN);
+        if (right_real) {
+          const double* gp = a.geo + 6 * (size_t)slot_geo(infN);
 #pragma unroll
-        for (int e = 0; e < 3; ++e) {
-          y[e] = __ldg(gp + e);
-          lam[e] = eqR(s, cr_pos(t + 1))[e];
+          for (int e = 0; e < 3; ++e) y[e] = __ldg(gp + e);
+          mat3t_vec(R, lam + 3, w);
+          add_point_force(gq, y, w, 1.0);
         }
-        mat3t_vec(R, lam, w);
-        add_point_force(gq, y, w, 1.0);
+        HinvBlk H;
+        if (has_body) {
+          const Material M = a.b.mats[mdb];
+          get_hinv(a, M, mdb, msb, H);
+          hinv_apply(H, gq, u);
+        }
       }
-      Material M;
-      double msc;
-      HinvBlk H;
-      body_material(a, slot, M, msc, H);
-      double u[12];
-      hinv_apply(H, gq, u);
+      double q[12], dqt[12];
+      tm_ld12(tbase + 48 * b, q);
+      tm_ld12(tbase + 48 * b + 24, dqt);
+      if (has_body) {
+        double* qb = a.b.q + slot;
+        double* qdb = a.b.qd + slot;
 #pragma unroll
-      for (int kb = 0; kb < 4; ++kb) {
-        double c3[3];
-        mat3_vec(R, u + 3 * kb, c3);
+        for (int kb = 0; kb < 4; ++kb) {
+          double c3[3];
+          mat3_vec(R, u + 3 * kb, c3);
 #pragma unroll
-        for (int e = 0; e < 3; ++e) {
-          const int c = 3 * kb + e;
-          const double dq = dqt[c] - c3[e];  // δq = δq̃ − correction
-          __stcs(qb + c * a.b.ld, q[c] + dq);
-          __stcs(qdb + c * a.b.ld, dq * k.ih);
+          for (int e = 0; e < 3; ++e) {
+            const int r = 3 * kb + e;
+            const double dq = dqt[r] - c3[e];  // δq = δq̃ − correction
+            __stcs(qb + r * a.b.ld, q[r] + dq);
+            __stcs(qdb + r * a.b.ld, dq * k.ih);
+          }
         }
       }
     }
     PH_MARK(6);
-    __syncthreads();  // shared memory is reused by the next segment
   }
+  asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+  __syncthreads();
+  if (warp == 0)
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(*tmem_slot), "n"(TMEM_COLS));
 }
 
 // ------------------------------------------------------------------ reduced block-tridiagonal levels
@@ -759,7 +1037,8 @@ cudaError_t launch_seq_finish(const SeqArgs& a, cudaStream_t st) {
   return cudaGetLastError();
 }
 
-size_t cr_smem_bytes() { return sizeof(double) * NEQ * (6 + 9 + 9 + 3); }
+size_t cr_smem_bytes() { return sizeof(double) * LDS * (6 + 9 + 9 + 3); }
+static size_t chain_smem_bytes() { return chain_smem_size(); }
 
 static int g_num_sms = 0;
 
@@ -767,8 +1046,8 @@ cudaError_t launch_chain(const ChainArgs& a0, int nitems, bool finish, cudaStrea
   if (nitems <= 0) return cudaSuccess;
   ChainArgs a = a0;
   a.n_items = nitems;
-  const size_t sm = cr_smem_bytes();
-  const int grid = std::min(nitems, MABD_CHAIN_MINB * std::max(g_num_sms, 1));
+  const size_t sm = chain_smem_bytes();
+  const int grid = std::min(nitems, 4 * std::max(g_num_sms, 1));
   if (finish)
     chain_kernel<true><<<grid, CT, sm, st>>>(a);
   else
@@ -788,8 +1067,9 @@ cudaError_t chain_kernels_init() {
   int dev = 0;
   if ((e = cudaGetDevice(&dev))) return e;
   if ((e = cudaDeviceGetAttribute(&g_num_sms, cudaDevAttrMultiProcessorCount, dev))) return e;
-  if ((e = cudaFuncSetAttribute(chain_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, sm))) return e;
-  if ((e = cudaFuncSetAttribute(chain_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, sm))) return e;
+  const int smc = (int)chain_smem_bytes();
+  if ((e = cudaFuncSetAttribute(chain_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, smc))) return e;
+  if ((e = cudaFuncSetAttribute(chain_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, smc))) return e;
   if ((e = cudaFuncSetAttribute(btd_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, sm))) return e;
   // favour shared memory in the unified L1/shared carve-out so that 4 segment CTAs fit per SM
   cudaFuncSetAttribute(chain_kernel<true>, cudaFuncAttributePreferredSharedMemoryCarveout, 100);

@@ -257,10 +257,12 @@ __device__ __forceinline__ void rot_conj(const double* R, const double* P, doubl
 // ------------------------------------------------------------------ per-body predict (stages 1-2)
 // Computes R, q̃ − qⁿ = δq̃ = diag₄(R) H̄⁻¹ diag₄(Rᵀ) f_A with
 // f_A = (1/h) M_A q̇ + M_A[0₉;g] − [V vec(R Π(RᵀA)); 0₃]   (Alg. 1 exact R).
-// Returns false if the polar decomposition failed (det A ≤ 1e-9 / non-finite).
-__device__ __forceinline__ bool predict_body(const double* q, const double* qd, const Material& M, double mscale,
-                                             const HinvBlk& H, double ih, const double* grav, double* R,
-                                             double* dqt) {
+// q̇ is fetched by qd_load(out12) and H̄⁻¹ by get_h(H) only when needed, so that neither is live during the polar
+// decomposition (register pressure). Returns false if the polar decomposition failed.
+template <class QdLoad, class GetH>
+__device__ __forceinline__ bool predict_body_lazy(const double* q, QdLoad qd_load, const Material& M, double mscale,
+                                                  GetH get_h, HinvBlk& H, double ih, const double* grav, double* R,
+                                                  double* dqt) {
   double A[9];
 #pragma unroll
   for (int r = 0; r < 3; ++r)
@@ -278,7 +280,8 @@ __device__ __forceinline__ bool predict_body(const double* q, const double* qd, 
     for (int c = 0; c < 3; ++c) Pi[3 * r + c] = M.mu * (F[3 * r + c] + F[3 * c + r]) + (r == c ? (M.lam * tr - 2.0 * M.mu) : 0.0);
   // w = diag₄(Rᵀ) f_A: the A-blocks are Rᵀ(m_c/h · q̇_c) − V Π[:,c] (Rᵀ R Π = Π), the t-block Rᵀ m (q̇_t/h + g)
   const double ma[4] = {M.a0 * mscale * ih, M.a1 * mscale * ih, M.a2 * mscale * ih, M.m * mscale};
-  double w[12], u[12];
+  double w[12], u[12], qd[12];
+  qd_load(qd);
 #pragma unroll
   for (int c = 0; c < 3; ++c) {
     double v[3];
@@ -294,10 +297,24 @@ __device__ __forceinline__ bool predict_body(const double* q, const double* qd, 
 #pragma unroll
     for (int r = 0; r < 3; ++r) w[9 + r] = v[r];
   }
+  get_h(H);
   hinv_apply(H, w, u);
 #pragma unroll
   for (int k = 0; k < 4; ++k) mat3_vec(R, u + 3 * k, dqt + 3 * k);
   return ok && isfinite(dqt[0] + dqt[4] + dqt[8] + dqt[9] + dqt[10] + dqt[11]);
+}
+
+__device__ __forceinline__ bool predict_body(const double* q, const double* qd, const Material& M, double mscale,
+                                             const HinvBlk& H, double ih, const double* grav, double* R,
+                                             double* dqt) {
+  HinvBlk Hc;
+  return predict_body_lazy(
+      q,
+      [&](double* o) {
+#pragma unroll
+        for (int c = 0; c < 12; ++c) o[c] = qd[c];
+      },
+      M, mscale, [&](HinvBlk& o) { o = H; }, Hc, ih, grav, R, dqt);
 }
 
 // x(q; ȳ) = A ȳ + t

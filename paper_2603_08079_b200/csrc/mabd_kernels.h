@@ -15,6 +15,7 @@ struct ChainArgs {
   const int32_t* seg_list;     // [n_items] segment ids of this launch, or null for 0..n_items−1
   int32_t n_items;             // segments of this launch (set by launch_chain)
   const HinvBlk* hinv_tab;     // [n_mat] prefactored H̄⁻¹ per material, or null (per-body mass scale)
+  int32_t n_mats;              // entries of b.mats
   Top* top_out;                // REDUCE output, indexed by seg_red
   const double* lam_in;        // FINISH input: level-2 λ [n_long][3]
   StepConsts k;

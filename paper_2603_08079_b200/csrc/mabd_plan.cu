@@ -457,7 +457,7 @@ mabd_status build_plan(const mabd_bodies* B, const mabd_joints* J, const mabd_op
   f.io = take(sizeof(double) * 24 * B->n);
   f.err = take(sizeof(int32_t) * 2);
   if (p->solver == MABD_SOLVER_CHAIN) {
-    f.slot_info = take(sizeof(uint32_t) * (ld + 1));
+    f.slot_info = take(sizeof(uint32_t) * (ld + 16));  // + padding: segments stage SEG + 4 slot codes
     f.geo = take(sizeof(double) * p->geo.size());
     f.seg_flags = take(sizeof(int32_t) * p->n_windows);
     f.seg_red = take(sizeof(int32_t) * p->n_windows);
@@ -744,6 +744,7 @@ cudaError_t launch_step(const Plan& p, const DevPtrs& d, double h, int32_t step,
   a.seg_red = d.seg_red;
   a.seg_list = nullptr;
   a.hinv_tab = p.mscale.empty() ? d.hinv : nullptr;
+  a.n_mats = (int32_t)p.mats.size();
   a.top_out = d.tops.empty() ? nullptr : d.tops[0];
   a.lam_in = d.lams.empty() ? nullptr : d.lams[0];
   a.k = k;

@@ -46,8 +46,8 @@ if hasattr(lib, "mabd_dbg_phases"):
         pass
     torch.cuda.synchronize()
     lib.mabd_dbg_phases(buf)
-    names = ["P1 body loop", "barrier", "assemble+inv", "CR fwd", "top+barrier", "CR back", "P3 update",
-             "loop/end barrier"]
+    names = ["P1 body loop", "barrier", "assemble+inv", "CR (2..11)", "top+barrier", "CR back lower", "P3 update",
+             "loop/end barrier", "CR fwd lower", "CR fwd upper (w0)", "top (w0)", "CR bwd upper (w0)"]
     nseg = steps * (sc.n // 256)
     tot = sum(buf[i] for i in range(8))
     for i, nm in enumerate(names):
