@@ -110,6 +110,7 @@ mabd_status mabd_create(const mabd_bodies* bodies, const mabd_joints* joints, co
   e = cudaMallocHost(&c->h_err, 2 * sizeof(int32_t));
   if (e == cudaSuccess) e = chain_kernels_init();
   if (e == cudaSuccess && c->plan.solver == MABD_SOLVER_SPARSE) e = sparse_init();
+  if (e == cudaSuccess && c->plan.solver == MABD_SOLVER_TREE) e = tree_init();
   if (e == cudaSuccess) e = upload_plan(c->plan, c->ws, c->stream, &c->d);
   if (e == cudaSuccess) e = cudaStreamSynchronize(c->stream);
   if (e != cudaSuccess) {

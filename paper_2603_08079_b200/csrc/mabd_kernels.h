@@ -70,10 +70,15 @@ struct TreeArgs {
   double* bscr;                // [n][21]: R, δq̃ between the passes
   double* ws;                  // per-body y, W
   int32_t group0;              // first group of this launch
+  int32_t front_rows;          // largest frontal matrix (rows; shared-memory sizing)
+  const int32_t* pt_off;       // [n+1] per body: its frontal points in pt_code
+  const int32_t* pt_code;      // 4·joint + 2·point + (child side)
+  const int32_t* body_nn;      // [n] N | nu << 8
+  int64_t n;                   // bodies
   StepConsts k;
 };
 
-enum : int32_t { TREE_UP = 0, TREE_DOWN = 1, TREE_BOTH = 2 };
+enum : int32_t { TREE_UP = 0, TREE_DOWN = 1, TREE_BOTH = 2, TREE_UP_LEVEL = 3, TREE_DOWN_LEVEL = 4 };
 
 // Multifrontal Cholesky of the dual S (sparse solver, mabd_sparse.cu). Fronts are dense column-major f×f
 // matrices (f = 3·(own + boundary points)); own columns first, then the boundary rows, both in elimination order.
@@ -115,7 +120,7 @@ struct SparseArgs {
   MfArgs mf;
   StepConsts k;
 };
-cudaError_t launch_tree(const TreeArgs& a, int ngroups, int mode, cudaStream_t st);
+cudaError_t launch_tree(const TreeArgs& a, int ngroups, int mode, int threads, cudaStream_t st);
 
 size_t cr_smem_bytes();
 cudaError_t chain_kernels_init();

@@ -510,6 +510,9 @@ mabd_status build_plan(const mabd_bodies* B, const mabd_joints* J, const mabd_op
     f.t_lam = take(sizeof(double) * 6 * std::max<int64_t>(1, K));
     f.t_bscr = take(sizeof(double) * 21 * n);
     f.t_ws = take(sizeof(double) * std::max<int64_t>(1, t.ws_total));
+    f.t_ptoff = take(sizeof(int32_t) * (n + 1));
+    f.t_ptcode = take(sizeof(int32_t) * std::max<size_t>(1, t.pt_code.size()));
+    f.t_nn = take(sizeof(int32_t) * n);
   }
   if (p->solver == MABD_SOLVER_SPARSE) sparse_layout(p, take);
   p->workspace_bytes = cur;
@@ -613,6 +616,14 @@ cudaError_t upload_plan(const Plan& p, char* ws, cudaStream_t st, DevPtrs* d) {
     A.bscr = (double*)(ws + f.t_bscr);
     A.ws = (double*)(ws + f.t_ws);
     A.group0 = 0;
+    A.front_rows = t.max_m;
+    A.n = p.n;
+    A.pt_off = (const int32_t*)(ws + f.t_ptoff);
+    A.pt_code = (const int32_t*)(ws + f.t_ptcode);
+    A.body_nn = (const int32_t*)(ws + f.t_nn);
+    if ((e = put((int32_t*)A.pt_off, t.pt_off, st))) return e;
+    if ((e = put((int32_t*)A.pt_code, t.pt_code, st))) return e;
+    if ((e = put((int32_t*)A.body_nn, t.body_nn, st))) return e;
     if ((e = put((int32_t*)A.up_joint, t.up_joint, st))) return e;
     if ((e = put((int32_t*)A.child_off, t.child_off, st))) return e;
     if ((e = put((int32_t*)A.child_joint, t.child_joint, st))) return e;

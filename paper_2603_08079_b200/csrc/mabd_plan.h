@@ -37,6 +37,8 @@ struct TreePlan {
   int32_t n_bottom = 0;              // bottom groups; the top group (if any) is group n_bottom
   bool has_top = false;
   int64_t ws_total = 0;
+  int32_t max_m = 3;                 // largest frontal matrix (rows)
+  std::vector<int32_t> pt_off, pt_code, body_nn;  // per body: frontal point codes, N | nu << 8
 };
 
 // Sparse plan: constraint points, body → point incidence, and the multifrontal symbolic factorization of the
@@ -121,7 +123,7 @@ struct Plan {
     size_t all_tops, lam_g, plo, lwin, llong;
     std::vector<size_t> p_tops1, p_lam2, p_scr;
     size_t t_up, t_coff, t_cj, t_wsoff, t_jnpts, t_jchd, t_jy, t_goff, t_glp, t_glo, t_shat, t_rhat, t_lam, t_bscr,
-        t_ws;
+        t_ws, t_ptoff, t_ptcode, t_nn;
   } off{};
 };
 
@@ -169,6 +171,7 @@ cudaError_t launch_step(const Plan& p, const DevPtrs& d, double h, int32_t step,
 // tree solver (mabd_tree.cu)
 bool tree_build(const mabd_joints* joints, int64_t n, Plan* p, std::vector<int64_t>* pos_of_body, std::string* msg);
 cudaError_t tree_step(const Plan& p, const DevPtrs& d, const StepConsts& k, cudaStream_t st);
+cudaError_t tree_init();
 
 // sparse solver (mabd_sparse.cu)
 bool sparse_build(const mabd_bodies* bodies, const mabd_joints* joints, Plan* p, std::vector<int64_t>* pos_of_body,

@@ -26,23 +26,26 @@
 
 namespace mabd {
 
-constexpr int TMAXM = TREE_MAXN + 6;
+// triangular index t → (row, column), column ≤ row, row-major over the lower triangle (lane-divergent indices:
+// computed, not looked up in constant memory, which would serialise the lanes)
+__device__ __forceinline__ void tri_rc(int t, int& r, int& c) {
+  r = (int)((sqrtf(8.0f * (float)t + 1.0f) - 1.0f) * 0.5f);
+  if ((r + 1) * (r + 2) / 2 <= t) ++r;
+  if (r * (r + 1) / 2 > t) --r;
+  c = t - r * (r + 1) / 2;
+}
 
 __device__ __forceinline__ void treport(const StepConsts& k, int32_t flag) {
   atomicOr(k.err, flag);
   atomicMin(k.err + 1, k.step_index);
 }
 
-// Body b's frontal matrix is ordered: the points of its child joints (sign +, b is their parent side), then
-// the points of its up joint (sign −, b is its child side).
-__device__ void tree_up(const TreeArgs& a, int b) {
+// Stages 1-2 for every body at once (no tree dependency): R and δq̃ → bscr.
+__global__ void tree_predict_kernel(TreeArgs a) {
   const StepConsts& k = a.k;
   const int64_t ld = a.b.ld;
-  // ---- stage 1-2: predict
-  double q[12], R[9], dqt[12];
-  HinvBlk H;
-  {
-    double qd[12];
+  for (int64_t b = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; b < a.n; b += (int64_t)gridDim.x * blockDim.x) {
+    double q[12], qd[12], R[9], dqt[12];
 #pragma unroll
     for (int c = 0; c < 12; ++c) {
       q[c] = a.b.q[c * ld + b];
@@ -51,166 +54,233 @@ __device__ void tree_up(const TreeArgs& a, int b) {
     const int mid = a.b.mat_id ? a.b.mat_id[b] : 0;
     const double msc = a.b.mscale ? a.b.mscale[b] : 1.0;
     const Material M = a.b.mats[mid];
+    HinvBlk H;
     if (a.hinv_tab)
       H = a.hinv_tab[mid];
     else
       hinv_blocks(M, msc, k.ih2, H);
     if (!predict_body(q, qd, M, msc, H, k.ih, k.grav, R, dqt)) treport(k, ERR_NONFINITE);
-    double* sc = a.bscr + 21 * (int64_t)b;
+    double* sc = a.bscr + 21 * b;
 #pragma unroll
     for (int c = 0; c < 9; ++c) sc[c] = R[c];
 #pragma unroll
     for (int c = 0; c < 12; ++c) sc[9 + c] = dqt[c];
-#pragma unroll
-    for (int c = 0; c < 12; ++c) q[c] += dqt[c];  // q̃
   }
-  // ---- frontal matrix
+}
+
+// Point i of body b's frontal matrix: the points of its child joints (sign +, b is their parent side), then the
+// points of its up joint (sign −, b is its child side).
+__device__ __forceinline__ void tree_point(const TreeArgs& a, int c0, int N, int u, int i, const double*& y, int& ji,
+                                           int& pi, double& sg) {
+  int row = 3 * i, jj = c0;
+  if (row < N) {
+    while (true) {
+      const int n3 = 3 * a.jnpts[a.child_joint[jj]];
+      if (row < n3) break;
+      row -= n3;
+      ++jj;
+    }
+    ji = a.child_joint[jj];
+    pi = row / 3;
+    sg = 1.0;
+    y = a.jy + 12 * (int64_t)ji + 3 * pi;
+  } else {
+    ji = u;
+    pi = (row - N) / 3;
+    sg = -1.0;
+    y = a.jy + 12 * (int64_t)ji + 6 + 3 * pi;
+  }
+}
+
+// Upward elimination at body b by one warp. The frontal matrix F (M×M, lower part) with the right-hand side as
+// column M lives in shared memory (row stride MS). A partial Cholesky over the N child-joint columns leaves
+//   F[N:,N:] = Ŝ_u = F_uu − F_uX F_XX⁻¹ F_Xu,  F[N:,M] = r̂_u = r_u − F_uX F_XX⁻¹ r_X,
+//   F[:N,:N] = L (F_XX = LLᵀ),  F[N:,:N] = F_uX L⁻ᵀ,  F[:N,M] = L⁻¹ r_X,
+// then Lᵀ back substitutions give y = F_XX⁻¹ r_X and W = F_XX⁻¹ F_Xu for the downward pass.
+__device__ void tree_up_warp(const TreeArgs& a, int b, int lane, double* F, int MS) {
+  const StepConsts& k = a.k;
+  const int64_t ld = a.b.ld;
   const int c0 = a.child_off[b], c1 = a.child_off[b + 1];
   const int u = a.up_joint[b];
-  int N = 0;
-  for (int j = c0; j < c1; ++j) N += 3 * a.jnpts[a.child_joint[j]];
-  const int nu = u >= 0 ? 3 * a.jnpts[u] : 0;
-  const int M = N + nu;
-  double F[TMAXM * TMAXM];
-  double rhs[TMAXM];
-  // point list
-  const int npt = M / 3;
-  for (int i = 0; i < npt; ++i) {
-    int ji, pi;
-    double si;
-    const double* yi;
-    {
-      int row = 3 * i, jj = c0;
-      if (row < N) {
-        while (true) {
-          const int n3 = 3 * a.jnpts[a.child_joint[jj]];
-          if (row < n3) break;
-          row -= n3;
-          ++jj;
-        }
-        ji = a.child_joint[jj];
-        pi = row / 3;
-        si = 1.0;
-        yi = a.jy + 12 * (int64_t)ji + 3 * pi;
-      } else {
-        ji = u;
-        pi = (row - N) / 3;
-        si = -1.0;
-        yi = a.jy + 12 * (int64_t)ji + 6 + 3 * pi;
-      }
-    }
-    // rhs: this body's side of C(q̃) plus the condensed child side
+  const int nn = a.body_nn[b], N = nn & 255, nu = nn >> 8;
+  const int M = N + nu, npt = M / 3;
+  const int32_t* pcode = a.pt_code + a.pt_off[b];
+  double R[9], qt[12];
+  {
+    const double* sc = a.bscr + 21 * (int64_t)b;
+#pragma unroll
+    for (int c = 0; c < 9; ++c) R[c] = sc[c];
+#pragma unroll
+    for (int c = 0; c < 12; ++c) qt[c] = a.b.q[c * ld + b] + sc[9 + c];  // q̃
+  }
+  HinvBlk H;
+  {
+    const int mid = a.b.mat_id ? a.b.mat_id[b] : 0;
+    if (a.hinv_tab)
+      H = a.hinv_tab[mid];
+    else
+      hinv_blocks(a.b.mats[mid], a.b.mscale ? a.b.mscale[b] : 1.0, k.ih2, H);
+  }
+  // right-hand side: this body's side of C(q̃) plus the condensed child side
+  for (int i = lane; i < npt; i += 32) {
+    const int code = pcode[i];
+    const int ji = code >> 2, pi = (code >> 1) & 1;
+    const double si = (code & 1) ? -1.0 : 1.0;
+    const double* yi = a.jy + 12 * (int64_t)ji + 6 * (code & 1) + 3 * pi;
     double x[3];
-    point_pos(q, yi, x);
-    if (si > 0) {
-      if (a.jchd[ji] < 0) {  // anchor: C = x_b(ȳ) − p_world
-        const double* pw = a.jy + 12 * (int64_t)ji + 6 + 3 * pi;
+    point_pos(qt, yi, x);
 #pragma unroll
-        for (int e = 0; e < 3; ++e) rhs[3 * i + e] = x[e] - pw[e];
-      } else {
-#pragma unroll
-        for (int e = 0; e < 3; ++e) rhs[3 * i + e] = x[e] + a.rhat[6 * (int64_t)ji + 3 * pi + e];
-      }
-    } else {
-#pragma unroll
-      for (int e = 0; e < 3; ++e) rhs[3 * i + e] = -x[e];
-    }
-    for (int j = 0; j <= i; ++j) {
-      int jj2, pj;
-      double sj;
-      const double* yj;
-      {
-        int row = 3 * j, jj = c0;
-        if (row < N) {
-          while (true) {
-            const int n3 = 3 * a.jnpts[a.child_joint[jj]];
-            if (row < n3) break;
-            row -= n3;
-            ++jj;
-          }
-          jj2 = a.child_joint[jj];
-          pj = row / 3;
-          sj = 1.0;
-          yj = a.jy + 12 * (int64_t)jj2 + 3 * pj;
-        } else {
-          jj2 = u;
-          pj = (row - N) / 3;
-          sj = -1.0;
-          yj = a.jy + 12 * (int64_t)jj2 + 6 + 3 * pj;
-        }
-      }
-      double P[9], Bk[9];
-      pblock(H, yi, yj, P);
-      rot_conj(R, P, Bk);
-      const double sg = si * sj;
-      for (int r = 0; r < 3; ++r)
-        for (int c = 0; c < 3; ++c) {
-          double v = sg * Bk[3 * r + c];
-          if (si > 0 && sj > 0 && ji == jj2 && a.jchd[ji] >= 0)  // + condensed child side Ŝ_k
-            v += a.Shat[36 * (int64_t)ji + 6 * (3 * pi + r) + 3 * pj + c];
-          F[(3 * i + r) * TMAXM + 3 * j + c] = v;
-          F[(3 * j + c) * TMAXM + 3 * i + r] = v;
-        }
-    }
-  }
-  // ---- Cholesky of F_XX (lower, in place)
-  for (int c = 0; c < N; ++c) {
-    double d = F[c * TMAXM + c];
-    for (int m = 0; m < c; ++m) d -= F[c * TMAXM + m] * F[c * TMAXM + m];
-    if (!(d > 0.0)) {
-      treport(k, ERR_SINGULAR);
-      d = 1.0;
-    }
-    const double l = sqrt(d), il = 1.0 / l;
-    F[c * TMAXM + c] = l;
-    for (int r = c + 1; r < N; ++r) {
-      double v = F[r * TMAXM + c];
-      for (int m = 0; m < c; ++m) v -= F[r * TMAXM + m] * F[c * TMAXM + m];
-      F[r * TMAXM + c] = v * il;
-    }
-  }
-  // solve F_XX Z = [r_X | F_Xu] for Z = [y | W] (columns: 0 = rhs, 1..nu = F_Xu columns)
-  double* ws = a.ws + a.ws_off[b];  // y [N], W [N][nu]
-  for (int col = 0; col <= nu; ++col) {
-    double z[TREE_MAXN];
-    for (int r = 0; r < N; ++r) z[r] = col == 0 ? rhs[r] : F[r * TMAXM + N + col - 1];
-    for (int r = 0; r < N; ++r) {  // L z' = z
-      double v = z[r];
-      for (int m = 0; m < r; ++m) v -= F[r * TMAXM + m] * z[m];
-      z[r] = v / F[r * TMAXM + r];
-    }
-    for (int r = N - 1; r >= 0; --r) {  // Lᵀ z = z'
-      double v = z[r];
-      for (int m = r + 1; m < N; ++m) v -= F[m * TMAXM + r] * z[m];
-      z[r] = v / F[r * TMAXM + r];
-    }
-    for (int r = 0; r < N; ++r) {
-      if (col == 0)
-        ws[r] = z[r];
+    for (int e = 0; e < 3; ++e) {
+      double v;
+      if (si < 0)
+        v = -x[e];
+      else if (a.jchd[ji] < 0)  // anchor: C = x_b(ȳ) − p_world
+        v = x[e] - a.jy[12 * (int64_t)ji + 6 + 3 * pi + e];
       else
-        ws[N + r * nu + col - 1] = z[r];
+        v = x[e] + a.rhat[6 * (int64_t)ji + 3 * pi + e];
+      F[(3 * i + e) * MS + M] = v;
     }
   }
-  if (u >= 0) {  // condensed child side of the up joint
-    for (int r = 0; r < nu; ++r) {
-      double rv = rhs[N + r];
-      for (int m = 0; m < N; ++m) rv -= F[m * TMAXM + N + r] * ws[m];
-      a.rhat[6 * (int64_t)u + r] = rv;
-      for (int c = 0; c < nu; ++c) {
-        double v = F[(N + r) * TMAXM + N + c];
-        for (int m = 0; m < N; ++m) v -= F[m * TMAXM + N + r] * ws[N + m * nu + c];
-        a.Shat[36 * (int64_t)u + 6 * r + c] = v;
+  // blocks (i, j), j ≤ i: s_i s_j R P(ȳ_i, ȳ_j) Rᵀ (+ Ŝ_k on a child joint's own block)
+  const int npair = npt * (npt + 1) / 2;
+  for (int t = lane; t < npair; t += 32) {
+    int i, j;
+    tri_rc(t, i, j);
+    const int ci = pcode[i], cj = pcode[j];
+    const int ji = ci >> 2, pi = (ci >> 1) & 1, jj = cj >> 2, pj = (cj >> 1) & 1;
+    const double si = (ci & 1) ? -1.0 : 1.0, sj = (cj & 1) ? -1.0 : 1.0;
+    const double* yi = a.jy + 12 * (int64_t)ji + 6 * (ci & 1) + 3 * pi;
+    const double* yj = a.jy + 12 * (int64_t)jj + 6 * (cj & 1) + 3 * pj;
+    double P[9], Bk[9];
+    pblock(H, yi, yj, P);
+    rot_conj(R, P, Bk);
+    const double sg = si * sj;
+    const bool add_s = si > 0 && sj > 0 && ji == jj && a.jchd[ji] >= 0;
+#pragma unroll
+    for (int r = 0; r < 3; ++r)
+#pragma unroll
+      for (int c = 0; c < 3; ++c) {
+        double v = sg * Bk[3 * r + c];
+        if (add_s) v += a.Shat[36 * (int64_t)ji + 6 * (3 * pi + r) + 3 * pj + c];
+        if (3 * i + r >= 3 * j + c) F[(3 * i + r) * MS + 3 * j + c] = v;
       }
+  }
+  __syncwarp();
+  // partial Cholesky of the augmented lower matrix over the N child-joint columns, by 3×3 point blocks:
+  // factor the diagonal block (lane 0, closed form, its inverse Li kept in shared memory), scale the block
+  // column and the right-hand side, rank-3 update of the trailing lower part
+  double* Li = F + (size_t)M * MS;  // [N/3][9] inverses of the diagonal blocks (after the front rows)
+  const int NB = N / 3;
+  for (int kb = 0; kb < NB; ++kb) {
+    const int c = 3 * kb;
+    if (lane == 0) {
+      const double d00 = F[c * MS + c], d10 = F[(c + 1) * MS + c], d20 = F[(c + 2) * MS + c];
+      const double d11 = F[(c + 1) * MS + c + 1], d21 = F[(c + 2) * MS + c + 1], d22 = F[(c + 2) * MS + c + 2];
+      double p0 = d00;
+      bool ok = p0 > 0.0;
+      const double l00 = sqrt(ok ? p0 : 1.0), i00 = 1.0 / l00;
+      const double l10 = d10 * i00, l20 = d20 * i00;
+      const double p1 = d11 - l10 * l10;
+      ok = ok && p1 > 0.0;
+      const double l11 = sqrt(p1 > 0.0 ? p1 : 1.0), i11 = 1.0 / l11;
+      const double l21 = (d21 - l20 * l10) * i11;
+      const double p2 = d22 - l20 * l20 - l21 * l21;
+      ok = ok && p2 > 0.0;
+      const double l22 = sqrt(p2 > 0.0 ? p2 : 1.0), i22 = 1.0 / l22;
+      if (!ok) treport(k, ERR_SINGULAR);
+      F[c * MS + c] = l00;
+      F[(c + 1) * MS + c] = l10;
+      F[(c + 2) * MS + c] = l20;
+      F[(c + 1) * MS + c + 1] = l11;
+      F[(c + 2) * MS + c + 1] = l21;
+      F[(c + 2) * MS + c + 2] = l22;
+      // Li = L⁻¹ (lower): row-major 3×3
+      double* li = Li + 9 * kb;
+      li[0] = i00;
+      li[1] = 0.0;
+      li[2] = 0.0;
+      li[3] = -l10 * i00 * i11;
+      li[4] = i11;
+      li[5] = 0.0;
+      li[6] = (l10 * l21 - l20 * l11) * i00 * i11 * i22;
+      li[7] = -l21 * i11 * i22;
+      li[8] = i22;
+      // right-hand side of the block: y_k = Li r_k
+      const double r0 = F[c * MS + M], r1 = F[(c + 1) * MS + M], r2 = F[(c + 2) * MS + M];
+      F[c * MS + M] = li[0] * r0;
+      F[(c + 1) * MS + M] = li[3] * r0 + li[4] * r1;
+      F[(c + 2) * MS + M] = li[6] * r0 + li[7] * r1 + li[8] * r2;
     }
+    __syncwarp();
+    const double* li = Li + 9 * kb;
+    for (int r = c + 3 + lane; r < M; r += 32) {  // block column below: F[r, c:c+3] ← F[r, c:c+3] Liᵀ
+      const double f0 = F[r * MS + c], f1 = F[r * MS + c + 1], f2 = F[r * MS + c + 2];
+      F[r * MS + c] = li[0] * f0;
+      F[r * MS + c + 1] = li[3] * f0 + li[4] * f1;
+      F[r * MS + c + 2] = li[6] * f0 + li[7] * f1 + li[8] * f2;
+    }
+    __syncwarp();
+    // trailing: F[r][cc] −= Σ_e L[r][c+e] L[cc][c+e] (c+3 ≤ cc ≤ r < M); rhs[r] −= Σ_e L[r][c+e] y[c+e]
+    const int T = M - c - 3;
+    for (int t = lane; t < T * T; t += 32) {
+      const int r = c + 3 + t / T, cc = c + 3 + t % T;
+      if (cc > r) continue;
+      F[r * MS + cc] -= F[r * MS + c] * F[cc * MS + c] + F[r * MS + c + 1] * F[cc * MS + c + 1] +
+                        F[r * MS + c + 2] * F[cc * MS + c + 2];
+    }
+    for (int r = c + 3 + lane; r < M; r += 32)
+      F[r * MS + M] -= F[r * MS + c] * F[c * MS + M] + F[r * MS + c + 1] * F[(c + 1) * MS + M] +
+                       F[r * MS + c + 2] * F[(c + 2) * MS + M];
+    __syncwarp();
+  }
+  // back substitutions Lᵀ Z = V by 3×3 blocks (last block first): V column 0 = L⁻¹r_X (F column M), columns
+  // 1..nu = the rows N..M−1 of F_uX L⁻ᵀ (F[N+col−1][0:N]); Z overwrites V: y = F_XX⁻¹ r_X, W = F_XX⁻¹ F_Xu
+  auto vref = [&](int r, int col) -> double& { return col == 0 ? F[r * MS + M] : F[(N + col - 1) * MS + r]; };
+  const int ncol = nu + 1;
+  for (int kb = NB - 1; kb >= 0; --kb) {
+    const int c = 3 * kb;
+    const double* li = Li + 9 * kb;
+    double z = 0.0;
+    const int e = lane / ncol, col = lane % ncol;
+    if (lane < 3 * ncol) {  // z_k = Liᵀ v_k (row e, column col)
+      z = li[e] * vref(c, col) + li[3 + e] * vref(c + 1, col) + li[6 + e] * vref(c + 2, col);
+    }
+    __syncwarp();
+    if (lane < 3 * ncol) vref(c + e, col) = z;
+    __syncwarp();
+    for (int t = lane; t < c * ncol; t += 32) {  // earlier rows: v_j −= L[c:c+3, j]ᵀ z_k
+      const int r = t / ncol, cl = t % ncol;
+      vref(r, cl) -= F[c * MS + r] * vref(c, cl) + F[(c + 1) * MS + r] * vref(c + 1, cl) +
+                     F[(c + 2) * MS + r] * vref(c + 2, cl);
+    }
+    __syncwarp();
+  }
+  double* ws = a.ws + a.ws_off[b];  // y [N], W [N][nu]
+  for (int t = lane; t < N * ncol; t += 32) {
+    const int r = t / ncol, col = t % ncol;
+    if (col == 0)
+      ws[r] = vref(r, 0);
+    else
+      ws[N + r * nu + col - 1] = vref(r, col);
+  }
+  if (u >= 0) {  // condensed child side of the up joint (Ŝ_u symmetric: lower part mirrored)
+    for (int t = lane; t < nu * nu; t += 32) {
+      const int r = t / nu, c = t % nu;
+      const int rr = r > c ? r : c, cc = r > c ? c : r;
+      a.Shat[36 * (int64_t)u + 6 * r + c] = F[(N + rr) * MS + N + cc];
+    }
+    if (lane < nu) a.rhat[6 * (int64_t)u + lane] = F[(N + lane) * MS + M];
   } else {  // root: λ_X = y
+    __syncwarp();
     int off = 0;
     for (int j = c0; j < c1; ++j) {
       const int kj = a.child_joint[j];
       const int n3 = 3 * a.jnpts[kj];
-      for (int r = 0; r < n3; ++r) a.lam[6 * (int64_t)kj + r] = ws[off + r];
+      for (int r = lane; r < n3; r += 32) a.lam[6 * (int64_t)kj + r] = F[(off + r) * MS + M];
       off += n3;
     }
   }
+  __syncwarp();
 }
 
 __device__ void tree_down(const TreeArgs& a, int b) {
@@ -222,8 +292,9 @@ __device__ void tree_down(const TreeArgs& a, int b) {
   for (int j = c0; j < c1; ++j) N += 3 * a.jnpts[a.child_joint[j]];
   const int nu = u >= 0 ? 3 * a.jnpts[u] : 0;
   const double* ws = a.ws + a.ws_off[b];
-  double lu[6] = {0, 0, 0, 0, 0, 0};
-  for (int r = 0; r < nu; ++r) lu[r] = a.lam[6 * (int64_t)u + r];
+  double lu[6];  // fixed-size, fully unrolled accesses only (no local memory)
+#pragma unroll
+  for (int r = 0; r < 6; ++r) lu[r] = r < nu ? a.lam[6 * (int64_t)u + r] : 0.0;
   if (u >= 0) {  // λ_X = y − W λ_u
     int off = 0;
     for (int j = c0; j < c1; ++j) {
@@ -231,7 +302,10 @@ __device__ void tree_down(const TreeArgs& a, int b) {
       const int n3 = 3 * a.jnpts[kj];
       for (int r = 0; r < n3; ++r) {
         double v = ws[off + r];
-        for (int c = 0; c < nu; ++c) v -= ws[N + (off + r) * nu + c] * lu[c];
+        const double* wr = ws + N + (off + r) * nu;
+#pragma unroll
+        for (int c = 0; c < 6; ++c)
+          if (c < nu) v -= wr[c] * lu[c];
         a.lam[6 * (int64_t)kj + r] = v;
       }
       off += n3;
@@ -255,7 +329,9 @@ __device__ void tree_down(const TreeArgs& a, int b) {
       add_point_force(gq, a.jy + 12 * (int64_t)kj + 3 * p, w, 1.0);
     }
   }
-  for (int p = 0; p < nu / 3; ++p) {
+#pragma unroll
+  for (int p = 0; p < 2; ++p) {
+    if (3 * p >= nu) break;
     double w[3];
     mat3t_vec(R, lu + 3 * p, w);
     add_point_force(gq, a.jy + 12 * (int64_t)u + 6 + 3 * p, w, -1.0);
@@ -282,26 +358,43 @@ __device__ void tree_down(const TreeArgs& a, int b) {
   }
 }
 
-__global__ void __launch_bounds__(256) tree_kernel(TreeArgs a, int mode) {
+__global__ void __launch_bounds__(512) tree_kernel(TreeArgs a, int mode, int MS) {
+  extern __shared__ double tsm[];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, nw = blockDim.x >> 5;
+  double* F = tsm + (size_t)warp * (a.front_rows * MS + 9 * (TREE_MAXN / 3));
+  if (mode == TREE_UP_LEVEL || mode == TREE_DOWN_LEVEL) {  // one level of the top group over the whole grid
+    const int l = a.group0;
+    const int b = a.glev_off[l] + (mode == TREE_UP_LEVEL ? blockIdx.x * nw + warp : blockIdx.x * blockDim.x + threadIdx.x);
+    if (b >= a.glev_off[l + 1]) return;
+    if (mode == TREE_UP_LEVEL)
+      tree_up_warp(a, b, lane, F, MS);
+    else
+      tree_down(a, b);
+    return;
+  }
   const int g = a.group0 + blockIdx.x;
   const int l0 = a.glev_ptr[g], l1 = a.glev_ptr[g + 1] - 1;  // levels l ∈ [l0, l1): [glev_off[l], glev_off[l+1])
   if (mode == TREE_UP || mode == TREE_BOTH) {
-    for (int l = l0; l < l1; ++l) {  // deepest first
-      for (int b = a.glev_off[l] + threadIdx.x; b < a.glev_off[l + 1]; b += blockDim.x) tree_up(a, b);
+    for (int l = l0; l < l1; ++l) {  // deepest first; one warp per body
+      for (int b = a.glev_off[l] + warp; b < a.glev_off[l + 1]; b += nw) tree_up_warp(a, b, lane, F, MS);
       __syncthreads();
     }
   }
   if (mode == TREE_DOWN || mode == TREE_BOTH) {
-    for (int l = l1 - 1; l >= l0; --l) {  // shallowest first
+    for (int l = l1 - 1; l >= l0; --l) {  // shallowest first; one thread per body
       for (int b = a.glev_off[l] + threadIdx.x; b < a.glev_off[l + 1]; b += blockDim.x) tree_down(a, b);
       __syncthreads();
     }
   }
 }
 
-cudaError_t launch_tree(const TreeArgs& a, int ngroups, int mode, cudaStream_t st) {
+static int tree_ms(int max_m) { return max_m + 2 + ((max_m & 1) ? 0 : 1); }  // row stride (odd)
+
+cudaError_t launch_tree(const TreeArgs& a, int ngroups, int mode, int threads, cudaStream_t st) {
   if (ngroups <= 0) return cudaSuccess;
-  tree_kernel<<<ngroups, 256, 0, st>>>(a, mode);
+  const int MS = tree_ms(a.front_rows);
+  const size_t sm = sizeof(double) * (size_t)(threads / 32) * (a.front_rows * MS + 9 * (TREE_MAXN / 3));
+  tree_kernel<<<ngroups, threads, sm, st>>>(a, mode, MS);
   return cudaGetLastError();
 }
 
@@ -310,13 +403,36 @@ cudaError_t tree_step(const Plan& p, const DevPtrs& d, const StepConsts& k, cuda
   a.k = k;
   const TreePlan& t = p.tree;
   cudaError_t e;
-  if (!t.has_top) return launch_tree(a, t.n_bottom, TREE_BOTH, st);
+  tree_predict_kernel<<<(unsigned)std::max<int64_t>(1, std::min<int64_t>((a.n + 255) / 256, 148 * 8)), 256, 0, st>>>(a);
+  // warps per CTA of the CTA-local subtrees: up to 8 within the shared memory
+  const size_t per_warp = sizeof(double) * ((size_t)t.max_m * tree_ms(t.max_m) + 9 * (TREE_MAXN / 3));
+  const int bot_threads = 32 * (int)std::max<size_t>(1, std::min<size_t>(8, (200 * 1024) / std::max<size_t>(per_warp, 1)));
+  if (!t.has_top) return launch_tree(a, t.n_bottom, TREE_BOTH, bot_threads, st);
   a.group0 = 0;
-  if ((e = launch_tree(a, t.n_bottom, TREE_UP, st))) return e;
-  a.group0 = t.n_bottom;
-  if ((e = launch_tree(a, 1, TREE_BOTH, st))) return e;
+  if ((e = launch_tree(a, t.n_bottom, TREE_UP, bot_threads, st))) return e;
+  // the top group: one launch per level over the whole GPU (a body per warp up, per thread down), deepest first
+  const int g = t.n_bottom;
+  const int l0 = t.glev_ptr[g], l1 = t.glev_ptr[g + 1] - 1;
+  const int MS = tree_ms(a.front_rows);
+  const int wpc = 4;  // warps per CTA of the level launches
+  const size_t sm = sizeof(double) * (size_t)wpc * (a.front_rows * MS + 9 * (TREE_MAXN / 3));
+  for (int l = l0; l < l1; ++l) {
+    const int nb = t.glev_off[l + 1] - t.glev_off[l];
+    a.group0 = l;
+    tree_kernel<<<(nb + wpc - 1) / wpc, 32 * wpc, sm, st>>>(a, TREE_UP_LEVEL, MS);
+  }
+  for (int l = l1 - 1; l >= l0; --l) {
+    const int nb = t.glev_off[l + 1] - t.glev_off[l];
+    a.group0 = l;
+    tree_kernel<<<(nb + 127) / 128, 128, 0, st>>>(a, TREE_DOWN_LEVEL, MS);
+  }
+  if ((e = cudaGetLastError())) return e;
   a.group0 = 0;
-  return launch_tree(a, t.n_bottom, TREE_DOWN, st);
+  return launch_tree(a, t.n_bottom, TREE_DOWN, bot_threads, st);
+}
+
+cudaError_t tree_init() {
+  return cudaFuncSetAttribute(tree_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 210 * 1024);
 }
 
 // ============================================================================ host: topology and ordering
@@ -483,6 +599,9 @@ bool tree_build(const mabd_joints* J, int64_t n, Plan* p, std::vector<int64_t>* 
   for (int64_t k = 0; k < K; ++k) cj[(*pos_of_body)[jpar[k]]].push_back((int32_t)k);
   t.child_off.assign(n + 1, 0);
   t.ws_off.assign(n + 1, 0);
+  t.pt_off.clear();
+  t.pt_code.clear();
+  t.body_nn.clear();
   for (int64_t i = 0; i < n; ++i) {
     const int64_t v = body_of[i];
     t.up_joint[i] = (int32_t)upj[v];
@@ -493,10 +612,24 @@ bool tree_build(const mabd_joints* J, int64_t n, Plan* p, std::vector<int64_t>* 
     t.child_off[i + 1] = t.child_off[i] + (int32_t)cj[i].size();
     for (int32_t kk : cj[i]) t.child_joint.push_back(kk);
     t.ws_off[i + 1] = t.ws_off[i] + N + (int64_t)N * nu;
+    t.max_m = std::max(t.max_m, N + nu);
+    // frontal point list: child joints' points (parent side, +), then the up joint's (child side, −);
+    // code = 4·joint + 2·point + (1 for the child side)
+    t.pt_off.push_back((int32_t)t.pt_code.size());
+    for (int32_t kk : cj[i])
+      for (int q = 0; q < t.jnpts[kk]; ++q) t.pt_code.push_back(4 * kk + 2 * q);
+    if (upj[v] >= 0)
+      for (int q = 0; q < t.jnpts[upj[v]]; ++q) t.pt_code.push_back(4 * (int32_t)upj[v] + 2 * q + 1);
+    t.body_nn.push_back((int32_t)(N | (nu << 8)));
   }
+  t.pt_off.push_back((int32_t)t.pt_code.size());
   t.ws_total = t.ws_off[n];
   p->ld = n;
-  p->launches_per_step = t.has_top ? (t.n_bottom > 0 ? 3 : 1) : 1;
+  {
+    int top_levels = 0;
+    if (t.has_top) top_levels = t.glev_ptr[t.n_bottom + 1] - 1 - t.glev_ptr[t.n_bottom];
+    p->launches_per_step = 1 + (t.has_top ? 2 + 2 * top_levels : 1);
+  }
   return true;
 }
 

@@ -20,12 +20,12 @@ def test_cfg4_recipe_small(cuda_ok, depth):
 
 
 def test_cfg4_recipe_with_top_group(cuda_ok):
-    """Depth 10 (1,023 bodies): four 255-body bottom groups plus a 3-body top group (3 launches/step)."""
+    """Depth 10 (1,023 bodies): four 255-body bottom groups plus a 3-body top group in 2 levels (7 launches/step)."""
     sc = G.cfg4_binary_tree(10)
     check(sc, 1, expect_solver="tree")
     check(sc, 5, expect_solver="tree")
     q, _, info = gpu_run(sc, 5)
-    assert info["launches_per_step"] == 3
+    assert info["launches_per_step"] == 7   # predict, bottom up, 2 top levels up and down, bottom down
     assert O.constraint_residual(sc, q) <= 1e-10
 
 
