@@ -208,20 +208,41 @@ def run_ours(args, rank: int, world: int, local_rank: int) -> None:
             dist.barrier()
         torch.cuda.synchronize(dev)
 
+    # The configured workload is an episode of sc.nsteps steps (100 for configs 2-4) from the initial state; the
+    # per-step cost depends on the state (the polar decomposition iterates more on strained links), so K timed
+    # steps are run as episodes of ≤ nsteps steps, each from the initial state. The reset (a device copy of
+    # q⁰, q̇⁰) happens between episodes, outside the timed intervals; the reported time is the sum of the
+    # episodes' CUDA-event intervals on the library's stream.
+    episode = max(1, int(getattr(sc, "nsteps", 100) or 100))
+    q0_dev = torch.as_tensor(q0, device=dev)
+    qd0_dev = torch.as_tensor(qd0, device=dev)
+
+    def reset():
+        sim.set_state(q0_dev, qd0_dev)
+
     # warm-up
     if args.warmup:
-        sim.step(h, args.warmup)
+        sim.step(h, min(args.warmup, episode))
+    reset()
     barrier()
-    ev0 = torch.cuda.Event(enable_timing=True)
-    ev1 = torch.cuda.Event(enable_timing=True)
     sampler = ClockSampler(local_rank if "CUDA_VISIBLE_DEVICES" not in os.environ else int(
         os.environ["CUDA_VISIBLE_DEVICES"].split(",")[local_rank]))
+    ms = 0.0
     with sampler:
-        ev0.record(stream)
-        sim.step(h, args.steps)
-        ev1.record(stream)
-        barrier()
-    ms = ev0.elapsed_time(ev1)
+        left = args.steps
+        while left > 0:
+            kk = min(episode, left)
+            ev0 = torch.cuda.Event(enable_timing=True)
+            ev1 = torch.cuda.Event(enable_timing=True)
+            ev0.record(stream)
+            sim.step(h, kk)
+            ev1.record(stream)
+            barrier()
+            ms += ev0.elapsed_time(ev1)
+            left -= kk
+            if left > 0:
+                reset()
+                barrier()
     if world > 1:
         t = torch.tensor([ms], device=dev)
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
@@ -229,7 +250,8 @@ def run_ours(args, rank: int, world: int, local_rank: int) -> None:
     ms_step = ms / args.steps
     bodies_total = n if split else world * n
     value = bodies_total * args.steps / (ms * 1e-3)
-    launches = info["launches_per_step"] * args.steps + 1   # + the error-word reset kernel
+    # + one error-word reset kernel per mabd_step call (one call per episode)
+    launches = info["launches_per_step"] * args.steps + (args.steps + episode - 1) // episode
 
     # e2e through the public API with pinned host buffers: per step H2D (q, q̇) → step → D2H (q, q̇)
     ke = max(1, min(args.steps, args.e2e_steps))
@@ -272,6 +294,9 @@ def run_ours(args, rank: int, world: int, local_rank: int) -> None:
             "scaling": "strong" if split else "weak",
             "vs_baseline": None, "dtype": "f64", "data": "synthetic",
             "config": {"workload": CFG_TEXT[args.config], "bodies_per_gpu": n, "solver": info["solver"],
+                       "episode_steps": episode,
+                       "timing": f"{args.steps} steps as episodes of <= {episode} steps from the initial state "
+                                 "(reset between episodes, outside the CUDA-event intervals)",
                        "dual_rows_per_gpu": info["n_dual_rows"],
                        "l2": "no flush: state q,qdot (192 MiB) + per-body params > 126 MB L2",
                        "parallelism": (f"chain split over {world} ranks (NCCL all-gather of per-rank tops)" if split
@@ -299,7 +324,7 @@ def run_ours(args, rank: int, world: int, local_rank: int) -> None:
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=200)
+    ap.add_argument("--steps", type=int, default=100)
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--config", type=int, default=2, choices=[1, 2, 3, 4, 5])
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
