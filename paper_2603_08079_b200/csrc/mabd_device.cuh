@@ -66,6 +66,16 @@ __device__ __forceinline__ double fast_rcp(double x) {
   return fma(r, e, r);
 }
 
+// 1/√x: hardware approximation (MUFU.RSQ64H) refined by two Newton steps y ← y(3 − xy²)/2 to full fp64
+// precision (≤ 1 ulp; not IEEE-rounded).
+__device__ __forceinline__ double fast_rsqrt(double x) {
+  double y = rsqrt(x);
+  double e = fma(-x * y, y, 1.0);
+  y = fma(0.5 * y, e, y);
+  e = fma(-x * y, y, 1.0);
+  return fma(0.5 * y, e, y);
+}
+
 // Inverse of an SPD 3×3 (packed sym) by its adjugate; returns false if a leading minor is ≤ 0
 // (the dual matrix must be SPD: a failure means redundant joints, MABD_ESINGULAR).
 __device__ __forceinline__ bool sym_inv_spd(const double* S, double* Si) {

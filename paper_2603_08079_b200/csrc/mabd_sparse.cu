@@ -271,38 +271,99 @@ __global__ void __launch_bounds__(128) mf_ea_kernel(SparseArgs a, const int32_t*
 }
 
 // Panel step 1: Cholesky of the kb×kb diagonal block at k0, and its inverse L⁻¹ (kept per front and chunk: the
-// TRSM of this panel and the triangular solves use it).
+// TRSM of this panel and the triangular solves use it). Blocked by 8×8: warp 0 factors a diagonal block (and
+// inverts it), the CTA scales the block column and applies the rank-8 trailing update; the inverse of the
+// whole lower factor is formed block row by block row, X_ij = −X_ii Σ_{j≤k<i} L_ik X_kj.
+constexpr int PB = 8;
 __global__ void __launch_bounds__(SP_THREADS) mf_potrf_kernel(SparseArgs a, const int32_t* tasks, int k0) {
   extern __shared__ double psm[];
   double(*L)[MF_NB + 1] = reinterpret_cast<double(*)[MF_NB + 1]>(psm);
   double(*X)[MF_NB + 1] = reinterpret_cast<double(*)[MF_NB + 1]>(psm + MF_NB * (MF_NB + 1));
+  __shared__ double dinv[MF_NB];  // 1 / L_jj
   const MfArgs& m = a.mf;
   const int node = tasks[blockIdx.x];
   const int n = m.nown[node];
   const int64_t f = m.fdim[node];
   const int kb = min(MF_NB, n - k0);
   double* F = m.F + m.foff[node];
-  const int tid = threadIdx.x, tx = tid % 16, ty = tid / 16;
+  const int tid = threadIdx.x, tx = tid % 16, ty = tid / 16, lane = tid & 31, warp = tid >> 5;
+  // load the lower part; pad to 64 with an identity block (rows/cols ≥ kb) so every block step is 8 wide
   for (int idx = tid; idx < MF_NB * MF_NB; idx += blockDim.x) {
     const int r = idx % MF_NB, c = idx / MF_NB;
-    L[r][c] = (r >= c && r < kb) ? F[(k0 + c) * f + k0 + r] : 0.0;
-    X[r][c] = r == c ? 1.0 : 0.0;
+    double v = 0.0;
+    if (r < kb && c < kb) {
+      if (r >= c) v = F[(k0 + c) * f + k0 + r];
+    } else if (r == c) {
+      v = 1.0;
+    }
+    L[r][c] = v;
+    X[r][c] = 0.0;
   }
   __syncthreads();
-  for (int k = 0; k < kb; ++k) {
-    double d = L[k][k];
-    if (!(d > 0.0)) {
-      if (tid == 0) sreport(a.k, ERR_SINGULAR);
-      d = 1.0;
+  const int nbk = (kb + PB - 1) / PB;
+  for (int bk = 0; bk < nbk; ++bk) {
+    const int c0 = PB * bk;
+    if (warp == 0) {  // 8×8 diagonal block: Cholesky, then its inverse into X's diagonal block
+      for (int j = 0; j < PB; ++j) {
+        double d = L[c0 + j][c0 + j];
+        if (!(d > 0.0)) {
+          if (lane == 0) sreport(a.k, ERR_SINGULAR);
+          d = 1.0;
+        }
+        const double isd = fast_rsqrt(d), sd = d * isd;
+        __syncwarp();
+        if (lane == 0) {
+          L[c0 + j][c0 + j] = sd;
+          dinv[c0 + j] = isd;
+        }
+        if (lane > j && lane < PB) L[c0 + lane][c0 + j] *= isd;
+        __syncwarp();
+        {  // trailing of the block: (i, l), j < l ≤ i < 8; 28 pairs at most
+          const int i = j + 1 + lane / PB, l = j + 1 + lane % PB;
+          if (i < PB && l <= i) L[c0 + i][c0 + l] -= L[c0 + i][c0 + j] * L[c0 + l][c0 + j];
+          const int i2 = i + 4;  // lanes cover rows j+1..j+4 and j+5..j+8
+          if (i2 < PB && l <= i2) L[c0 + i2][c0 + l] -= L[c0 + i2][c0 + j] * L[c0 + l][c0 + j];
+        }
+        __syncwarp();
+      }
+      if (lane < PB) {  // column `lane` of the inverse of the 8×8 lower block by forward substitution
+        const int j = lane;
+        for (int i = 0; i < PB; ++i) {
+          double v = (i == j) ? 1.0 : 0.0;
+          for (int l = j; l < i; ++l) v -= L[c0 + i][c0 + l] * X[c0 + l][c0 + j];
+          X[c0 + i][c0 + j] = i >= j ? v * dinv[c0 + i] : 0.0;
+        }
+      }
     }
-    const double sd = sqrt(d), isd = 1.0 / sd;
     __syncthreads();
-    if (tid > k && tid < kb) L[tid][k] *= isd;
-    if (tid == 0) L[k][k] = sd;
+    // block column below: L[r, c0:c0+8] ← L[r, c0:c0+8] X_bbᵀ (one thread per row)
+    for (int r = c0 + PB + tid; r < MF_NB; r += blockDim.x) {
+      double v[PB], w[PB];
+#pragma unroll
+      for (int e = 0; e < PB; ++e) v[e] = L[r][c0 + e];
+#pragma unroll
+      for (int c = 0; c < PB; ++c) {
+        double acc = 0.0;
+#pragma unroll
+        for (int e = 0; e < PB; ++e)
+          if (e <= c) acc += v[e] * X[c0 + c][c0 + e];
+        w[c] = acc;
+      }
+#pragma unroll
+      for (int e = 0; e < PB; ++e) L[r][c0 + e] = w[e];
+    }
     __syncthreads();
-    for (int i = k + 1 + ty; i < kb; i += 16) {
-      const double lik = L[i][k];
-      for (int j = k + 1 + tx; j <= i; j += 16) L[i][j] -= lik * L[j][k];
+    // rank-8 trailing update of the lower part: rows and columns ≥ c0+8
+    for (int r = c0 + PB + ty; r < MF_NB; r += 16) {
+      double lr[PB];
+#pragma unroll
+      for (int e = 0; e < PB; ++e) lr[e] = L[r][c0 + e];
+      for (int c = c0 + PB + tx; c <= r; c += 16) {
+        double acc = 0.0;
+#pragma unroll
+        for (int e = 0; e < PB; ++e) acc += lr[e] * L[c][c0 + e];
+        L[r][c] -= acc;
+      }
     }
     __syncthreads();
   }
@@ -310,19 +371,51 @@ __global__ void __launch_bounds__(SP_THREADS) mf_potrf_kernel(SparseArgs a, cons
     const int r = idx % kb, c = idx / kb;
     if (r >= c) F[(k0 + c) * f + k0 + r] = L[r][c];
   }
-  // X = L⁻¹ by forward elimination on the identity (row k scaled, then eliminated from the rows below)
-  for (int k = 0; k < kb; ++k) {
-    const double ik = 1.0 / L[k][k];
-    if (tid <= k) X[k][tid] *= ik;
-    __syncthreads();
-    for (int i = k + 1 + ty; i < kb; i += 16) {
-      const double lik = L[i][k];
-      for (int j = tx; j <= k; j += 16) X[i][j] -= lik * X[k][j];
+  // inverse of the whole factor: block rows i = 1 … nbk−1, X_ij = −X_ii Σ_{k=j}^{i−1} L_ik X_kj (j < i)
+  for (int bi = 1; bi < nbk; ++bi) {
+    const int r0 = PB * bi;
+    // T = Σ_k L_ik X_kj for all j < i: thread (r, c) of the block row, columns c < r0
+    double t[2] = {0.0, 0.0};
+    int rr[2], cc[2];
+#pragma unroll
+    for (int q = 0; q < 2; ++q) {
+      const int idx = tid + q * SP_THREADS;  // PB × r0 ≤ 8 × 56 = 448 entries
+      rr[q] = r0 + idx % PB;
+      cc[q] = idx / PB;
+      if (cc[q] < r0) {
+        const int bj = cc[q] / PB;
+        double acc = 0.0;
+        for (int k = PB * bj; k < r0; ++k) acc += L[rr[q]][k] * X[k][cc[q]];
+        t[q] = acc;
+      }
     }
+    __syncthreads();
+#pragma unroll
+    for (int q = 0; q < 2; ++q)  // park T in the (still zero) upper part of X: X[c][r] for c < r0 ≤ r
+      if (cc[q] < r0) X[cc[q]][rr[q]] = t[q];
+    __syncthreads();
+#pragma unroll
+    for (int q = 0; q < 2; ++q) {
+      if (cc[q] < r0) {
+        double acc = 0.0;
+        for (int e = 0; e < PB; ++e) acc += X[rr[q]][r0 + e] * X[cc[q]][r0 + e];  // X_ii row · T column
+        t[q] = -acc;
+      }
+    }
+    __syncthreads();
+#pragma unroll
+    for (int q = 0; q < 2; ++q)
+      if (cc[q] < r0) {
+        X[rr[q]][cc[q]] = t[q];
+        X[cc[q]][rr[q]] = 0.0;
+      }
     __syncthreads();
   }
   double* out = m.linv + m.loff[node] + (int64_t)(k0 / MF_NB) * MF_NB * MF_NB;
-  for (int idx = tid; idx < MF_NB * MF_NB; idx += blockDim.x) out[idx] = X[idx / MF_NB][idx % MF_NB];
+  for (int idx = tid; idx < MF_NB * MF_NB; idx += blockDim.x) {
+    const int r = idx / MF_NB, c = idx % MF_NB;
+    out[idx] = (r < kb && c < kb) ? X[r][c] : 0.0;
+  }
 }
 
 // Panel step 2: rows r0..r0+63 of the panel: X = B L⁻ᵀ (B = F[r, k0:k0+kb]); task = (node, r0, potrf slot).
