@@ -180,32 +180,38 @@ __device__ __forceinline__ void cr_invert(const CRS& s, int k, const StepConsts&
 
 // One forward level at stride 2^L over survivors m = first, first+step, …; a survivor that is eliminated at the
 // next level (m odd) inverts its own D right after its update (no one else reads it at this level).
-__device__ __forceinline__ void cr_level_fwd_rt(const CRS& s, int L, int first, int step, const StepConsts& k) {
+// With end = false the last survivor (equation SEG) is skipped: in a segment without a right interface it is the
+// decoupled padding equation (identity, zero couplings at every level), so its updates are no-ops — and they
+// would be a second, serial update for one lane.
+__device__ __forceinline__ void cr_level_fwd_rt(const CRS& s, int L, int first, int step, const StepConsts& k,
+                                                bool end = true) {
   const int NE = SEG >> (L + 1);
-  for (int m = first; m <= NE; m += step) {
+  const int last = end ? NE : NE - 1;
+  for (int m = first; m <= last; m += step) {
     cr_update_rt(s, L, m);
     if ((m & 1) && (2 << L) < SEG) cr_invert_at(s, elim_pos_rt(L + 1, m >> 1), k);
   }
 }
 template <int L>
-__device__ __forceinline__ void cr_level_fwd(const CRS& s, int first, int step, const StepConsts& k) {
-  cr_level_fwd_rt(s, L, first, step, k);
+__device__ __forceinline__ void cr_level_fwd(const CRS& s, int first, int step, const StepConsts& k,
+                                             bool end = true) {
+  cr_level_fwd_rt(s, L, first, step, k, end);
 }
 
 // Forward reduction, lower levels (strides 1, 2) by the whole CTA. Precondition: every odd equation already
 // holds D⁻¹. One barrier per level.
 template <int NT>
-__device__ __forceinline__ void cr_forward_lower(const CRS& s, int t, const StepConsts& k) {
-  cr_level_fwd<0>(s, t, NT, k);
+__device__ __forceinline__ void cr_forward_lower(const CRS& s, int t, const StepConsts& k, bool end = true) {
+  cr_level_fwd<0>(s, t, NT, k, end);
   __syncthreads();
-  cr_level_fwd<1>(s, t, NT, k);
+  cr_level_fwd<1>(s, t, NT, k, end);
   __syncthreads();
 }
 // Upper levels (strides 4 … 128, ≤ 33 survivors) by one warp, warp-synchronous.
-__device__ __forceinline__ void cr_forward_upper(const CRS& s, int lane, const StepConsts& k) {
+__device__ __forceinline__ void cr_forward_upper(const CRS& s, int lane, const StepConsts& k, bool end = true) {
 #pragma unroll 1
   for (int L = 2; L <= 7; ++L) {
-    cr_level_fwd_rt(s, L, lane, 32, k);
+    cr_level_fwd_rt(s, L, lane, 32, k, end);
     __syncwarp();
   }
 }
@@ -699,10 +705,11 @@ __global__ void __launch_bounds__(CT, 4) chain_kernel(ChainArgs a) {
     // ---------------- phase 2: block cyclic reduction
     PH_MARK(2);
 #ifndef MABD_EXP_SKIP_CR
-    cr_forward_lower<CT>(s, tid, k);
+    const bool right_iface = (flags & SEG_RIGHT_IFACE) != 0;
+    cr_forward_lower<CT>(s, tid, k, right_iface);
     PH_MARK(8);
     if (tid < 32) {  // upper levels, the 2-equation top and the upper back substitution: warp 0 alone
-      cr_forward_upper(s, tid, k);
+      cr_forward_upper(s, tid, k, right_iface);
       PH_MARK(9);
       if (tid == 0) {
         if (!is_long) {
