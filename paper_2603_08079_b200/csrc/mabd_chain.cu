@@ -335,18 +335,18 @@ __device__ __forceinline__ void write_top(const CRS& s, Top* o) {
 //             mbarrier) into the CR rows D/B/Bl, its slot-code / mass-scale / material rows into the CR rows r;
 //             all of them are dead while the previous segment finishes phase 3. No L2 round trip of the state
 //             is on the critical path.
-//   phase 1:  each thread moves its two bodies' qⁿ, q̇ⁿ into tensor memory (TMEM, 96 of the CTA's 128 columns,
+//   phase 1:  each thread moves its two bodies' qⁿ, q̇ⁿ into tensor memory (TMEM, 120 of the CTA's 128 columns,
 //             its own lane), barrier (the CR rows are free), then per body: predict (stages 1-2) with δq̃ kept
-//             in TMEM over q̇ⁿ, and assemble the joint equations (stage 3). TMEM is used purely as per-thread
-//             storage (12-cycle loads): it carries qⁿ and δq̃ across the solve without registers, shared or
+//             in TMEM over q̇ⁿ and R's first two rows beside it, and assemble the joint equations (stage 3). TMEM is used purely as per-thread
+//             storage (12-cycle loads): it carries qⁿ, δq̃ and R across the solve without registers, shared or
 //             global memory, so shared memory holds only the CR arrays and 4 CTAs fit per SM.
 //   phase 2:  block cyclic reduction (stage 3 solve)
-//   phase 3:  read λ, barrier, stage the next segment, then per body: recompute R = polar(Aⁿ) (the same
-//             arithmetic as phase 1, so the same R), qⁿ⁺¹ = q̃ − diag₄(R)H̄⁻¹Σ±Γᵀ Rᵀλ, q̇ⁿ⁺¹ = δq/h → HBM.
+//   phase 3:  per body: R from TMEM (rows 0, 1 stored in phase 1; row 2 = row 0 × row 1), λ from the CR rows,
+//             qⁿ⁺¹ = q̃ − diag₄(R)H̄⁻¹Σ±Γᵀ Rᵀλ, q̇ⁿ⁺¹ = δq/h → HBM; then a barrier and the next segment's staging.
 // FINISH = false: first pass (fused segments solve completely; long segments REDUCE to their top);
 // FINISH = true: second pass of long segments (recompute, read the ends' λ, back-substitute, update).
 constexpr int SLOT_ROW = SEG + 4;    // staged slot codes per segment (257 used, padded to 16 B)
-constexpr int TMEM_COLS = 128;       // per CTA: 2 bodies × (24 words qⁿ + 24 words q̇ⁿ/δq̃ + 12 words λ) = 120
+constexpr int TMEM_COLS = 128;       // per CTA: 2 bodies × (24 words qⁿ + 24 words q̇ⁿ/δq̃ + 12 words R rows 0-1)
 
 __host__ __device__ constexpr size_t chain_smem_size() { return sizeof(double) * LDS * 27 + 16; }
 
@@ -618,7 +618,10 @@ __global__ void __launch_bounds__(CT, 4) chain_kernel(ChainArgs a) {
             [&](HinvBlk& o) { get_hinv(a, M, md, ms, o); }, H, k.ih, k.grav, R, dqt);
         if (!ok && has_body) report(k, ERR_NONFINITE);
       }
-      if (update) tm_st12(tbase + 48 * b + 24, dqt);  // δq̃ over q̇ⁿ (warp-collective: every lane)
+      if (update) {
+        tm_st12(tbase + 48 * b + 24, dqt);  // δq̃ over q̇ⁿ (warp-collective: every lane)
+        tm_st6(tbase + 96 + 12 * b, R);     // rows 0, 1 of R (row 2 = row 0 × row 1 in phase 3)
+      }
       if (has_body) {
 #pragma unroll
         for (int r = 0; r < 12; ++r) q[r] += dqt[r];  // q̃
@@ -747,23 +750,6 @@ __global__ void __launch_bounds__(CT, 4) chain_kernel(ChainArgs a) {
 #endif
     PH_MARK(5);
     // ---------------- phase 3: qⁿ⁺¹ = q̃ − diag₄(R) H̄⁻¹ Σ ±Γ(ȳ)ᵀ Rᵀλ
-#pragma unroll
-    for (int b = 0; b < 2; ++b) {  // λ of the joints left and right of each body → TMEM columns 96 + 12b
-      const int t = tid + b * CT;
-      double l[6];
-#pragma unroll
-      for (int e = 0; e < 3; ++e) {
-        l[e] = eqR(s, cr_pos(t))[e];
-        l[3 + e] = eqR(s, cr_pos(t + 1))[e];
-      }
-      tm_st6(tbase + 96 + 12 * b, l);
-    }
-    tm_wait_st();
-    __syncthreads();  // λ read: every CR row is dead, stage the next segment into them
-    if (tid == 0) stage_segment(a, smem, bar, it + gridDim.x);
-#ifdef MABD_EXP_SKIP_P3
-    continue;
-#endif
 #pragma unroll 1
     for (int b = 0; b < 2; ++b) {
       const int t = tid + b * CT;
@@ -772,21 +758,19 @@ __global__ void __launch_bounds__(CT, 4) chain_kernel(ChainArgs a) {
       const double msb = b ? msc1 : msc0;
       const int mdb = b ? mid1 : mid0;
       double lam[6];
-      tm_ld6(tbase + 96 + 12 * b, lam);
+#pragma unroll
+      for (int e = 0; e < 3; ++e) {
+        lam[e] = eqR(s, cr_pos(t))[e];
+        lam[3 + e] = eqR(s, cr_pos(t + 1))[e];
+      }
       const bool has_body = slot_right(inf) == SIDE_BODY;
       const bool eq_real = slot_real(inf);
       const bool right_real = slot_real(infN) && slot_left(infN) == SIDE_BODY;
       double R[9], u[12];
-      {
-        double q[12];
-        tm_ld12(tbase + 48 * b, q);
-        double A[9];
-#pragma unroll
-        for (int r = 0; r < 3; ++r)
-#pragma unroll
-          for (int cc = 0; cc < 3; ++cc) A[3 * r + cc] = q[3 * cc + r];
-        polar_rotation(A, R);  // the same R as phase 1 (same input, same arithmetic)
-      }
+      tm_ld6(tbase + 96 + 12 * b, R);  // rows 0, 1 of phase 1's R; row 2 = row 0 × row 1 (det R = +1)
+      R[6] = R[1] * R[5] - R[2] * R[4];
+      R[7] = R[2] * R[3] - R[0] * R[5];
+      R[8] = R[0] * R[4] - R[1] * R[3];
       {
         double gq[12];
 #pragma unroll
@@ -834,6 +818,8 @@ __global__ void __launch_bounds__(CT, 4) chain_kernel(ChainArgs a) {
       }
     }
     PH_MARK(6);
+    __syncthreads();  // λ read: every CR row is dead, stage the next segment into them
+    if (tid == 0) stage_segment(a, smem, bar, it + gridDim.x);
   }
   asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
   __syncthreads();
