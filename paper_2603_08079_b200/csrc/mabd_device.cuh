@@ -134,8 +134,10 @@ __device__ __forceinline__ bool polar_rotation(const double* A, double* R) {
     if (e2 > 0.09) {  // scaled Newton step, far from orthogonal
       const double d = R[0] * (R[4] * R[8] - R[5] * R[7]) - R[1] * (R[3] * R[8] - R[5] * R[6]) +
                        R[2] * (R[3] * R[7] - R[4] * R[6]);
-      const double z = cbrt(1.0 / d);
-      const double iz = 1.0 / (z * d);  // X⁻ᵀ = cof(X)/det
+      // ζ = det^{-1/3} only sets the convergence speed (the iteration preserves the polar factor for any ζ > 0,
+      // and a scalar error in 1/det merely rescales X⁻ᵀ), so single precision suffices for both scalars
+      const double z = (double)cbrtf((float)fast_rcp(d));
+      const double iz = fast_rcp(z * d);  // X⁻ᵀ = cof(X)/det
       double C[9];
       C[0] = R[4] * R[8] - R[5] * R[7]; C[1] = R[5] * R[6] - R[3] * R[8]; C[2] = R[3] * R[7] - R[4] * R[6];
       C[3] = R[2] * R[7] - R[1] * R[8]; C[4] = R[0] * R[8] - R[2] * R[6]; C[5] = R[1] * R[6] - R[0] * R[7];
