@@ -16,6 +16,9 @@ H̄_j = M_A/h² + K̄_A                                        (P:279)
 f_A = (1/h) M_A q̇ⁿ + M_A [0₉; g] − [V vec(R Π(RᵀA)); 0₃]
 qⁿ⁺¹ = qⁿ + δq,  q̇ⁿ⁺¹ = δq / h
 
+With K > 1 Newton iterations, each iteration is such a KKT solve linearised at the
+previous iterate (``step(..., iters=K)``); ``nonlinear_residual`` states the nonlinear problem they converge to.
+
 Each function cites the passage it follows. The KKT is solved by a library
 solver (dense LU, SuperLU on the full KKT, or block LU in a fixed bodies-first
 pivot order: SURVEY §8(c) O3). The specialised CPU solvers at the bottom (block
@@ -33,7 +36,7 @@ import scipy.sparse.linalg as spla
 
 __all__ = [
     "lame", "unpack_mbar", "mass_A", "kbar_A", "hbar_A", "polar", "elastic_force_A", "affine_force",
-    "body_hessians", "constraint_system", "constraint_residual", "predict", "step", "simulate",
+    "body_hessians", "constraint_system", "constraint_residual", "predict", "step", "simulate", "nonlinear_residual",
     "block_thomas", "leaf_to_root_solve", "dual_matrix", "rel_err", "T9", "vec", "unvec",
 ]
 
@@ -236,13 +239,23 @@ def _natural_order(scene) -> bool:
     return scene.meta.get("topology") == "chain"
 
 
-def step(scene, q, qd, h, route: str = "auto", return_info: bool = False):
-    """One implicit step = one KKT solve, then qⁿ⁺¹ = qⁿ + δq, q̇ⁿ⁺¹ = δq/h (A6).
+def step(scene, q, qd, h, route: str = "auto", return_info: bool = False, iters: int = 1):
+    """One implicit step: `iters` Newton iterations, each one KKT solve.
+
+    iters = 1 (Table 1): linearised at qⁿ, qⁿ⁺¹ = qⁿ + δq, q̇ⁿ⁺¹ = δq/h (A6).
+    iters = K > 1 ("# Iter."): iteration i is linearised at q⁽ⁱ⁾ with
+    the incremental potential's gradient −∇E(q⁽ⁱ⁾) = M_A(q̂ − q⁽ⁱ⁾)/h² − [V vec(RΠ); 0],
+    q̂ = qⁿ + hq̇ⁿ + h²[0₉; g], the constant pre-factored H̄ rotated by R(q⁽ⁱ⁾), and the constraint
+    residual −C(q⁽ⁱ⁾) of the previous iterate (footnote P:459); q⁽ⁱ⁺¹⁾ = q⁽ⁱ⁾ + δq⁽ⁱ⁾, qⁿ⁺¹ = q⁽ᴷ⁾,
+    q̇ⁿ⁺¹ = Σᵢ δq⁽ⁱ⁾/h. The velocity form is used for i = 0 (identical to iters = 1) and the q̂ form,
+    written as (1/h)M_A v⁽ⁱ⁾ with v⁽ⁱ⁾ = (q̂ − q⁽ⁱ⁾)/h = v⁽ⁱ⁻¹⁾ − δq⁽ⁱ⁻¹⁾/h (+ h g at i = 1), for i ≥ 1.
 
     route: 'dense' (LAPACK dgesv on the full KKT), 'superlu' (SuperLU on the full KKT, COLAMD),
     'blocklu' (bodies first: δq̃ = H⁻¹f, S = ∇C̃H̃⁻¹∇C̃ᵀ, SuperLU on S without pivoting,
     λ = S⁻¹(∇C̃δq̃ + C(qⁿ)), δq = δq̃ − H̃⁻¹∇C̃ᵀλ), or 'auto' (SURVEY §8(c) O3 size rule).
     """
+    if iters > 1:
+        return _step_iterated(scene, q, qd, h, route, return_info, iters)
     q = np.asarray(q, dtype=np.float64)
     qd = np.asarray(qd, dtype=np.float64)
     n = scene.n
@@ -292,11 +305,72 @@ def step(scene, q, qd, h, route: str = "auto", return_info: bool = False):
     return q1, qd1
 
 
-def simulate(scene, nsteps=None, route: str = "auto", q=None, qd=None, callback=None):
+def _step_iterated(scene, q, qd, h, route, return_info, iters):
+    """K Newton iterations of one step (see ``step``): iteration i solves the KKT of the linearisation at q⁽ⁱ⁾."""
+    q = np.asarray(q, dtype=np.float64)
+    qd = np.asarray(qd, dtype=np.float64)
+    g = np.asarray(scene.gravity, dtype=np.float64)
+    qi = q.copy()
+    v = qd.copy()                       # v⁽⁰⁾ = q̇ⁿ with gravity explicit (the iters = 1 formula)
+    zero_g = _SceneGravity(scene, np.zeros(3))
+    info = None
+    for i in range(iters):
+        sc = scene if i == 0 else zero_g
+        qn1, v1, info = step(sc, qi, v, h, route=route, return_info=True, iters=1)
+        dq = qn1 - qi
+        qi = qn1
+        v = v - dq / h                  # v⁽ⁱ⁺¹⁾ = (q̂ − q⁽ⁱ⁺¹⁾)/h
+        if i == 0:
+            v[:, 9:12] += h * g         # q̂ carries h²g: v⁽¹⁾ = q̇ⁿ + h g − δq⁽⁰⁾/h
+    qd1 = (qd + 0.0) - v
+    qd1[:, 9:12] += h * g               # q̇ⁿ⁺¹ = (q̇ⁿ + h[0;g]) − v⁽ᴷ⁾ = Σᵢ δq⁽ⁱ⁾/h
+    if return_info:
+        return qi, qd1, info
+    return qi, qd1
+
+
+class _SceneGravity:
+    """A view of a scene with another gravity vector (iterations i ≥ 1 carry gravity inside q̂)."""
+
+    def __init__(self, scene, g):
+        self._s = scene
+        self.gravity = g
+
+    def __getattr__(self, k):
+        return getattr(self._s, k)
+
+
+def nonlinear_residual(scene, qn, qdn, q, h, lam=None):
+    """Stationarity of the implicit step's nonlinear problem at q (the limit of the Newton iterations):
+    r = M_A(q − q̂)/h² + [V vec(R(q)Π(F)); 0] + ∇Cᵀλ with q̂ = qⁿ + hq̇ⁿ + h²[0₉; g] (P:193-199, P:260-271,
+    P:459-475). λ is taken as the least-squares multiplier when not given. Returns (max |r| / max |M_A(q−q̂)/h²|,
+    max |C(q)|)."""
+    qn = np.asarray(qn, dtype=np.float64)
+    q = np.asarray(q, dtype=np.float64)
+    MA = mass_A(scene.mbar)
+    mu, lam_ = lame(scene.youngs, scene.poisson)
+    qhat = qn + h * np.asarray(qdn)
+    qhat[:, 9:12] += h * h * np.asarray(scene.gravity)
+    inert = np.einsum("nij,nj->ni", MA, q - qhat) / (h * h)
+    gr = inert.copy()
+    gr[:, :9] += elastic_force_A(unvec(q[:, :9]), scene.volume, mu, lam_)
+    J, world = constraint_system(scene)
+    g = gr.reshape(-1)
+    if J.shape[0]:
+        if lam is None:
+            lam = spla.lsqr(J.T, -g, atol=1e-15, btol=1e-15, iter_lim=100000)[0]
+        g = g + J.T @ lam
+        cres = float(np.max(np.abs(J @ q.reshape(-1) - world)))
+    else:
+        cres = 0.0
+    return float(np.max(np.abs(g)) / max(np.max(np.abs(inert)), 1e-300)), cres
+
+
+def simulate(scene, nsteps=None, route: str = "auto", q=None, qd=None, callback=None, iters: int = 1):
     q = scene.q0.copy() if q is None else q
     qd = scene.qd0.copy() if qd is None else qd
     for k in range(scene.nsteps if nsteps is None else nsteps):
-        q, qd = step(scene, q, qd, scene.h, route=route)
+        q, qd = step(scene, q, qd, scene.h, route=route, iters=iters)
         if callback is not None:
             callback(k, q, qd)
     return q, qd

@@ -382,3 +382,61 @@ def test_generators_shapes():
     assert (s.n, s.n_joints, s.n_rows) == (31, 31, 3 + 30 * 6)
     s = G.cfg5_net(20, max_off=4)
     assert s.n_joints == 2 * 20 * 19 + int(0.05 * 2 * 20 * 19) + 4
+
+
+# ----------------------------------------------------------------------------- Newton iterations > 1 (§8(f) NEXT 1)
+
+def test_iterated_step_converges_to_the_implicit_step():
+    """K Newton iterations (each linearised at the previous iterate, P:459 footnote) converge to the
+    stationary point of the implicit step's nonlinear problem: M_A(q − q̂)/h² + ∇VΨ(q) + ∇Cᵀλ = 0, C(q) = 0
+    (P:193-199). The residual is an independent restatement of that problem; the
+    quasi-Newton iteration with the constant rotated H̄ converges linearly."""
+    sc = G.random_chain(6, seed=3, vel=3.0, jitter=1e-3)
+    res = []
+    for K in (1, 2, 4, 8, 40):
+        q1, _ = O.step(sc, sc.q0, sc.qd0, sc.h, iters=K)
+        r, c = O.nonlinear_residual(sc, sc.q0, sc.qd0, q1, sc.h)
+        assert c <= 1e-12
+        res.append(r)
+    assert all(b < a for a, b in zip(res, res[1:])), res
+    assert res[0] > 1.0 and res[-1] <= 1e-10, res
+
+
+def test_iterated_free_fall_is_exact():
+    """P1 with K = 3: the free-fall step is linear, so later iterations change nothing (closed form)."""
+    R0 = G.random_rotations(np.random.default_rng(6), 1)[0]
+    v0 = np.array([1.0, -2.0, 3.0])
+    t0 = np.array([0.3, 0.2, 0.1])
+    sc = G.free_body(A0=R0, t0=t0, v0=v0, dims=(0.1, 0.3, 0.2), E=1e8)
+    n, h, g = 12, sc.h, sc.gravity
+    q, qd = O.simulate(sc, n, iters=3)
+    t_ref = t0 + n * h * v0 + 0.5 * n * (n + 1) * h * h * g
+    assert np.max(np.abs(q[0, 9:] - t_ref)) <= 1e-13 * np.max(np.abs(t_ref))
+    assert np.max(np.abs(qd[0, 9:] - (v0 + n * h * g))) <= 1e-12 * np.max(np.abs(v0 + n * h * g))
+    assert np.max(np.abs(q[0, :9] - O.vec(R0))) < 1e-14
+
+
+def test_iterated_momentum_and_closure():
+    """P2 and P3 with K = 3: every iteration conserves Σ m t (the t-rows of ∇C cancel, H̄'s t-block is (m/h²)I) and
+    closes the linear joints (C(q⁽ⁱ⁺¹⁾) = C(q⁽ⁱ⁾) + ∇Cδq = 0)."""
+    sc = G.random_tree(12, seed=8, anchored=False, vel=0.3, gravity=False, hinge_frac=0.5)
+    m = sc.mbar[:, 9]
+    p0 = (m[:, None] * sc.qd0[:, 9:]).sum(0)
+    q, qd = sc.q0, sc.qd0
+    for _ in range(4):
+        q, qd = O.step(sc, q, qd, sc.h, iters=3)
+        p = (m[:, None] * qd[:, 9:]).sum(0)
+        assert np.max(np.abs(p - p0)) <= 1e-12 * max(np.max(np.abs(p0)), np.max(m * np.abs(qd[:, 9:]).max(1)))
+        assert O.constraint_residual(sc, q) <= 1e-10
+    sc = G.random_chain(10, seed=9, jitter=2e-3, vel=0.2, end_anchor=True)
+    q, qd = sc.q0, sc.qd0
+    for _ in range(3):
+        q, qd = O.step(sc, q, qd, sc.h, iters=2)
+        assert O.constraint_residual(sc, q) <= 1e-10
+
+
+def test_one_iteration_is_the_plain_step():
+    sc = G.random_chain(7, seed=2, vel=0.5, jitter=1e-3)
+    a = O.step(sc, sc.q0, sc.qd0, sc.h)
+    b = O.step(sc, sc.q0, sc.qd0, sc.h, iters=1)
+    assert np.array_equal(a[0], b[0]) and np.array_equal(a[1], b[1])
