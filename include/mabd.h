@@ -90,7 +90,9 @@ typedef struct {
 } mabd_joints;
 
 typedef struct {
-  int32_t newton_iters;      /* must be 1 in this version (Table 1)                                */
+  int32_t newton_iters;      /* Newton iterations per step, 1..16 (0 = 1; Table 1 uses 1). Iteration i is
+                                linearised at the previous iterate (footnote P:459); K > 1 uses 96 more
+                                bytes per body of workspace and K + 2 times the launches              */
   int32_t residual_rhs;      /* must be 1: include −C(qⁿ) in the dual rhs (footnote P:459)          */
   int32_t solver;            /* 0 auto | 1 chain | 2 tree | 3 sparse                               */
   int32_t rank, world;       /* multi-GPU; world = 1 → single GPU                                  */

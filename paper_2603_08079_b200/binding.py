@@ -145,7 +145,7 @@ class Simulator:
 
     def __init__(self, q0, qd0, mbar, volume, youngs, poisson, gravity, body_a, body_b, npts, ybar_a, ybar_b,
                  solver: int = 0, device: Optional[int] = None, stream=None, world: int = 1, rank: int = 0,
-                 nccl_id: Optional[bytes] = None):
+                 nccl_id: Optional[bytes] = None, newton_iters: int = 1):
         import torch
 
         self._lib = load_library()
@@ -169,7 +169,7 @@ class Simulator:
         with torch.cuda.device(self.device):
             self._stream = stream if stream is not None else torch.cuda.current_stream(self.device)
             self._nccl_id = ctypes.create_string_buffer(bytes(nccl_id), 128) if nccl_id is not None else None
-            opts = _Options(1, 1, int(solver), int(rank), int(world),
+            opts = _Options(int(newton_iters), 1, int(solver), int(rank), int(world),
                             ctypes.cast(self._nccl_id, ctypes.c_void_p) if self._nccl_id is not None else None,
                             None, 0, ctypes.c_void_p(self._stream.cuda_stream))
             nbytes = ctypes.c_size_t(0)

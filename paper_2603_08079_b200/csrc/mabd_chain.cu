@@ -812,7 +812,10 @@ __global__ void __launch_bounds__(CT, 4) chain_kernel(ChainArgs a) {
             const int r = 3 * kb + e;
             const double dq = dqt[r] - c3[e];  // δq = δq̃ − correction
             __stcs(qb + r * a.b.ld, q[r] + dq);
-            __stcs(qdb + r * a.b.ld, dq * k.ih);
+            if (k.niter == 1)
+              __stcs(qdb + r * a.b.ld, dq * k.ih);
+            else  // K > 1: v ← v − δq/h + h·grav (launch_step in mabd_plan.cu)
+              qdb[r * a.b.ld] = qdb[r * a.b.ld] - dq * k.ih + (r >= 9 ? k.h * k.grav[r - 9] : 0.0);
           }
         }
       }

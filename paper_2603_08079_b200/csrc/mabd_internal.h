@@ -51,6 +51,7 @@ struct BodyArrays {
   double* q;               // [12][ld]
   double* qd;              // [12][ld]
   double* rs;              // [9][ld] scratch: R between the phases of one launch (L2 only, discarded)
+  double* z;               // [12][ld] K > 1 Newton iterations: q̇ⁿ + h[0;g] of this step
   int64_t ld;
   const int32_t* mat_id;   // [ld] or null (all material 0)
   const double* mscale;    // [ld] or null (all 1)
@@ -59,8 +60,9 @@ struct BodyArrays {
 
 struct StepConsts {
   double h, ih, ih2;
-  double grav[3];
+  double grav[3];          // gravity in the Newton r.h.s. (zero for iterations ≥ 1: q̂ carries it, see below)
   int32_t step_index;
+  int32_t iter, niter;     // Newton iteration of this launch sequence, iterations per step
   int32_t* err;            // [0] flags (1 nonfinite, 2 singular), [1] first failing step
 };
 

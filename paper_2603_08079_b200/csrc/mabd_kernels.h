@@ -116,6 +116,7 @@ struct SparseArgs {
   const int32_t* inc;
   double *rhs, *lam, *res, *dl, *yy;  // component-major [3][np]: r = C(q̃), λ, residual, correction, solve scratch
   double* vv;                  // [12][n]
+  double* dqt;                 // [12][n] δq̃ of the step (predict → rhs, update)
   int32_t* iters;              // refinement passes of the last solve
   MfArgs mf;
   StepConsts k;

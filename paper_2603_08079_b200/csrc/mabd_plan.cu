@@ -59,8 +59,7 @@ static mabd_status validate(const mabd_bodies* B, const mabd_joints* J, const ma
   if (J->n_joints > 0 && (!J->body_a || !J->body_b || !J->npts || !J->ybar_a || !J->ybar_b))
     return *msg = "a joint array is NULL", MABD_EINVAL;
   if (o) {
-    if (o->newton_iters != 0 && o->newton_iters != 1)
-      return *msg = "newton_iters must be 1 in this version", MABD_EUNSUPPORTED;
+    if (o->newton_iters < 0 || o->newton_iters > 16) return *msg = "newton_iters must be in [0, 16]", MABD_EINVAL;
     if (o->world > 1 && (o->rank < 0 || o->rank >= o->world)) return *msg = "rank outside [0, world)", MABD_EINVAL;
     if (o->world > 256) return *msg = "world > 256", MABD_EINVAL;
   }
@@ -379,6 +378,7 @@ mabd_status build_plan(const mabd_bodies* B, const mabd_joints* J, const mabd_op
   *p = Plan();
   p->n = B->n;
   p->n_joints = J->n_joints;
+  p->newton_iters = (o && o->newton_iters > 1) ? o->newton_iters : 1;
   for (int i = 0; i < 3; ++i) p->grav[i] = B->gravity[i];
   std::vector<int32_t> mid;
   std::vector<double> msc;
@@ -415,6 +415,7 @@ mabd_status build_plan(const mabd_bodies* B, const mabd_joints* J, const mabd_op
     *msg = "topology not supported by this build (" + why + ")";
     return MABD_EUNSUPPORTED;
   }
+  if (p->newton_iters > 1) p->launches_per_step = p->newton_iters * p->launches_per_step + 2;  // + prep, final
   if (o && o->world > 1 && p->solver != MABD_SOLVER_CHAIN)
     return *msg = "world > 1 is implemented for the chain solver only (run tree/sparse scenes as replicas)",
            MABD_EUNSUPPORTED;
@@ -449,6 +450,7 @@ mabd_status build_plan(const mabd_bodies* B, const mabd_joints* J, const mabd_op
   f.q = take(sizeof(double) * 12 * ld);
   f.qd = take(sizeof(double) * 12 * ld);
   f.rs = take(sizeof(double) * 9 * ld);
+  f.z = p->newton_iters > 1 ? take(sizeof(double) * 12 * ld) : 0;
   f.mat_id = multi_mat ? take(sizeof(int32_t) * ld) : 0;
   f.mscale = any_scale ? take(sizeof(double) * ld) : 0;
   f.mats = take(sizeof(Material) * p->mats.size());
@@ -531,6 +533,7 @@ cudaError_t upload_plan(const Plan& p, char* ws, cudaStream_t st, DevPtrs* d) {
   d->b.q = (double*)(ws + f.q);
   d->b.qd = (double*)(ws + f.qd);
   d->b.rs = (double*)(ws + f.rs);
+  d->b.z = p.newton_iters > 1 ? (double*)(ws + f.z) : nullptr;
   d->b.ld = p.ld;
   d->b.mat_id = p.mat_id.empty() ? nullptr : (const int32_t*)(ws + f.mat_id);
   d->b.mscale = p.mscale.empty() ? nullptr : (const double*)(ws + f.mscale);
@@ -736,6 +739,24 @@ static cudaError_t launch_step_parts(const Plan& p, const DevPtrs& d, ChainArgs 
   return launch_chain(a, (int)p.local_long.size(), true, st);
 }
 
+// K > 1 Newton iterations: iteration 0 is the plain step's linearisation at qⁿ (velocity
+// form, gravity explicit); iteration i ≥ 1 is linearised at q⁽ⁱ⁾ with the velocity buffer holding
+// v⁽ⁱ⁾ = (q̂ − q⁽ⁱ⁾)/h and zero explicit gravity (q̂ = qⁿ + hq̇ⁿ + h²[0;g] carries it). Each iteration's update
+// writes q⁽ⁱ⁺¹⁾ = q⁽ⁱ⁾ + δq and v⁽ⁱ⁺¹⁾ = v⁽ⁱ⁾ − δq/h + h·grav (t-components); after the last one,
+// q̇ⁿ⁺¹ = z − v⁽ᴷ⁾ with z = q̇ⁿ + h[0;g] saved before the first.
+__global__ void iter_prep_kernel(const double* qd, double* z, int64_t ld, double h, double g0, double g1, double g2) {
+  const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (i >= 12 * ld) return;
+  const int c = (int)(i / ld);
+  z[i] = qd[i] + (c == 9 ? h * g0 : c == 10 ? h * g1 : c == 11 ? h * g2 : 0.0);
+}
+__global__ void iter_final_kernel(double* qd, const double* z, int64_t ld) {
+  const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (i < 12 * ld) qd[i] = z[i] - qd[i];
+}
+
+static cudaError_t launch_iteration(const Plan& p, const DevPtrs& d, const StepConsts& k, cudaStream_t st);
+
 cudaError_t launch_step(const Plan& p, const DevPtrs& d, double h, int32_t step, cudaStream_t st) {
   StepConsts k;
   k.h = h;
@@ -744,6 +765,24 @@ cudaError_t launch_step(const Plan& p, const DevPtrs& d, double h, int32_t step,
   for (int i = 0; i < 3; ++i) k.grav[i] = p.grav[i];
   k.step_index = step;
   k.err = d.err;
+  k.iter = 0;
+  k.niter = std::max(1, p.newton_iters);
+  if (k.niter == 1) return launch_iteration(p, d, k, st);
+  const int64_t tot = 12 * d.b.ld;
+  const unsigned grid = (unsigned)((tot + 255) / 256);
+  iter_prep_kernel<<<grid, 256, 0, st>>>(d.b.qd, d.b.z, d.b.ld, h, p.grav[0], p.grav[1], p.grav[2]);
+  cudaError_t e;
+  for (int i = 0; i < k.niter; ++i) {
+    k.iter = i;
+    if (i == 1)
+      for (int c = 0; c < 3; ++c) k.grav[c] = 0.0;
+    if ((e = launch_iteration(p, d, k, st))) return e;
+  }
+  iter_final_kernel<<<grid, 256, 0, st>>>(d.b.qd, d.b.z, d.b.ld);
+  return cudaGetLastError();
+}
+
+static cudaError_t launch_iteration(const Plan& p, const DevPtrs& d, const StepConsts& k, cudaStream_t st) {
   if (p.solver == MABD_SOLVER_TREE) return tree_step(p, d, k, st);
   if (p.solver == MABD_SOLVER_SPARSE) return sparse_step(p, d, k, st);
   if (p.solver != MABD_SOLVER_CHAIN) return cudaErrorNotSupported;

@@ -74,7 +74,7 @@ struct SparsePlan {
   int64_t linv_doubles = 0;
   int32_t refine = 1;                                    // iterative-refinement passes per step
   int32_t max_f = 0;
-  size_t o_pa = 0, o_pb = 0, o_py = 0, o_incoff = 0, o_inc = 0, o_vec = 0, o_vv = 0, o_iters = 0;
+  size_t o_pa = 0, o_pb = 0, o_py = 0, o_incoff = 0, o_inc = 0, o_vec = 0, o_vv = 0, o_dqt = 0, o_iters = 0;
   size_t o_F = 0, o_foff = 0, o_fdim = 0, o_nown = 0, o_ownf = 0, o_choff = 0, o_ch = 0, o_eaoff = 0, o_eamap = 0,
          o_bndoff = 0, o_bnd = 0, o_ipos = 0, o_ablk = 0, o_acoff = 0, o_acon = 0, o_linv = 0, o_w = 0, o_woff = 0,
          o_lev = 0, o_tasks = 0, o_loff = 0;
@@ -84,6 +84,7 @@ struct Plan {
   int64_t n = 0, n_joints = 0, n_dual_rows = 0;
   int32_t solver = 0;
   int32_t launches_per_step = 0;
+  int32_t newton_iters = 1;      // Newton iterations per step (K)
   double grav[3] = {0, 0, 0};
   // bodies
   std::vector<Material> mats;
@@ -117,7 +118,7 @@ struct Plan {
   // device layout (byte offsets into the workspace)
   size_t workspace_bytes = 0;
   struct Off {
-    size_t q, qd, rs, mat_id, mscale, mats, hinv, perm, io, err;
+    size_t q, qd, rs, z, mat_id, mscale, mats, hinv, perm, io, err;
     size_t slot_info, geo, seg_flags, seg_red, long_list, left_iface;
     std::vector<size_t> tops, lams;  // per BTD level: tops[0] = chain tops (n_long), lams[i] = level i+1 λ
     size_t all_tops, lam_g, plo, lwin, llong;

@@ -43,7 +43,7 @@ __device__ __forceinline__ void sreport(const StepConsts& k, int32_t flag) {
 }
 
 // ============================================================================ per-body stages (a1, a2, a5)
-// bodies: predict; R → rs scratch, δq̃ parked in the q̇ buffer
+// bodies: predict; R → rs scratch, δq̃ → dqt
 __global__ void sparse_predict_kernel(SparseArgs a) {
   const int64_t ld = a.b.ld;
   for (int64_t j = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; j < a.n; j += (int64_t)gridDim.x * blockDim.x) {
@@ -65,7 +65,7 @@ __global__ void sparse_predict_kernel(SparseArgs a) {
 #pragma unroll
     for (int c = 0; c < 9; ++c) a.b.rs[c * ld + j] = R[c];
 #pragma unroll
-    for (int c = 0; c < 12; ++c) a.b.qd[c * ld + j] = dqt[c];
+    for (int c = 0; c < 12; ++c) a.dqt[c * ld + j] = dqt[c];
   }
 }
 
@@ -97,7 +97,7 @@ __global__ void sparse_rhs_kernel(SparseArgs a) {
       }
       double qt[12], x[3];
 #pragma unroll
-      for (int c = 0; c < 12; ++c) qt[c] = a.b.q[c * ld + j] + a.b.qd[c * ld + j];
+      for (int c = 0; c < 12; ++c) qt[c] = a.b.q[c * ld + j] + a.dqt[c * ld + j];
       point_pos(qt, y, x);
 #pragma unroll
       for (int e = 0; e < 3; ++e) r[e] += sg * x[e];
@@ -172,9 +172,12 @@ __global__ void sparse_update_kernel(SparseArgs a) {
     body_apply(a, j, a.lam, v);
 #pragma unroll
     for (int c = 0; c < 12; ++c) {
-      const double dq = a.b.qd[c * ld + j] - v[c];
+      const double dq = a.dqt[c * ld + j] - v[c];
       a.b.q[c * ld + j] += dq;
-      a.b.qd[c * ld + j] = dq * a.k.ih;
+      if (a.k.niter == 1)
+        a.b.qd[c * ld + j] = dq * a.k.ih;
+      else  // K > 1: v ← v − δq/h + h·grav (launch_step in mabd_plan.cu)
+        a.b.qd[c * ld + j] += -dq * a.k.ih + (c >= 9 ? a.k.h * a.k.grav[c - 9] : 0.0);
     }
   }
 }
@@ -1301,6 +1304,7 @@ void sparse_layout(Plan* p, const std::function<size_t(size_t)>& take) {
   s.o_inc = take(sizeof(int32_t) * nz(s.inc.size()));
   s.o_vec = take(sizeof(double) * 15 * np);  // rhs, λ, res, δλ, y: [3][np] each
   s.o_vv = take(sizeof(double) * 12 * n);
+  s.o_dqt = take(sizeof(double) * 12 * n);
   s.o_iters = take(sizeof(int32_t) * 4);
   const size_t NN = nz(s.nnode);
   s.o_F = take(sizeof(double) * nz(s.front_doubles));
@@ -1352,6 +1356,7 @@ cudaError_t sparse_upload(const Plan& p, char* ws, cudaStream_t st, DevPtrs* d) 
   A.dl = v + 9 * np;
   A.yy = v + 12 * np;
   A.vv = (double*)(ws + s.o_vv);
+  A.dqt = (double*)(ws + s.o_dqt);
   A.iters = (int32_t*)(ws + s.o_iters);
   MfArgs& m = A.mf;
   m.F = (double*)(ws + s.o_F);

@@ -353,7 +353,10 @@ __device__ void tree_down(const TreeArgs& a, int b) {
       const int c = 3 * kb + e;
       const double dq = sc[9 + c] - c3[e];
       a.b.q[c * ld + b] += dq;
-      a.b.qd[c * ld + b] = dq * k.ih;
+      if (k.niter == 1)
+        a.b.qd[c * ld + b] = dq * k.ih;
+      else  // K > 1: v ← v − δq/h + h·grav (launch_step in mabd_plan.cu)
+        a.b.qd[c * ld + b] += -dq * k.ih + (c >= 9 ? k.h * k.grav[c - 9] : 0.0);
     }
   }
 }

@@ -15,9 +15,9 @@ TOL1 = 1e-9
 TOLN = 1e-6
 
 
-def gpu_run(sc, nsteps, solver=0):
+def gpu_run(sc, nsteps, solver=0, iters=1):
     from paper_2603_08079_b200 import Simulator
-    sim = Simulator.from_scene(sc, solver=solver)
+    sim = Simulator.from_scene(sc, solver=solver, newton_iters=iters)
     sim.prefactor(sc.h)
     sim.step(sc.h, nsteps)
     q, qd = sim.get_state()
@@ -26,9 +26,9 @@ def gpu_run(sc, nsteps, solver=0):
     return q, qd, info
 
 
-def check(sc, nsteps, route="auto", tol=None, solver=0, expect_solver="chain"):
-    q_o, qd_o = O.simulate(sc, nsteps, route=route)
-    q_g, qd_g, info = gpu_run(sc, nsteps, solver)
+def check(sc, nsteps, route="auto", tol=None, solver=0, expect_solver="chain", iters=1):
+    q_o, qd_o = O.simulate(sc, nsteps, route=route, iters=iters)
+    q_g, qd_g, info = gpu_run(sc, nsteps, solver, iters)
     assert info["solver"] == expect_solver
     err = O.rel_err(q_g, q_o)
     tol = tol if tol is not None else (TOL1 if nsteps == 1 else TOLN)
