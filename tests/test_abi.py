@@ -36,13 +36,13 @@ def test_exports_every_header_symbol(lib):
         assert hasattr(lib, s)
 
 
-def _ws(lib, sc, solver=0):
+def _ws(lib, sc, solver=0, iters=1):
     from paper_2603_08079_b200.binding import _Bodies, _Joints, _Options, _ptr, _ip
     b = _Bodies(sc.n, _ptr(sc.q0), _ptr(sc.qd0), _ptr(sc.mbar), _ptr(sc.volume), _ptr(sc.youngs), _ptr(sc.poisson),
                 None, (ctypes.c_double * 3)(*sc.gravity))
     j = _Joints(sc.n_joints, _ptr(sc.body_a, _ip), _ptr(sc.body_b, _ip), _ptr(sc.npts, _ip), _ptr(sc.ybar_a),
                 _ptr(sc.ybar_b))
-    o = _Options(1, 1, solver, 0, 1, None, None, 0, None)
+    o = _Options(iters, 1, solver, 0, 1, None, None, 0, None)
     n = ctypes.c_size_t()
     st = lib.mabd_workspace_size(ctypes.byref(b), ctypes.byref(j), ctypes.byref(o), ctypes.byref(n))
     return st, n.value, lib.mabd_last_error(None).decode()
@@ -83,3 +83,41 @@ def test_chain_solver_rejects_cycles(lib):
     sc = G.small_net(4, max_off=2)
     st, _, msg = _ws(lib, sc, solver=1)
     assert st == 1 and "chain" in msg
+
+
+def test_newton_iterations_option(lib):
+    """newton_iters: 0 and 1 are one iteration, 2..16 allocate the extra velocity buffer, others are invalid."""
+    sc = G.random_chain(40, seed=1)
+    st1, nb1, _ = _ws(lib, sc, iters=1)
+    st0, nb0, _ = _ws(lib, sc, iters=0)
+    st3, nb3, _ = _ws(lib, sc, iters=3)
+    assert st1 == st0 == st3 == 0
+    assert nb0 == nb1 and nb3 >= nb1 + 12 * 8 * sc.n
+    assert _ws(lib, sc, iters=17)[0] == 1
+    assert _ws(lib, sc, iters=-1)[0] == 1
+
+
+def _sparse_stats(lib, sc):
+    from paper_2603_08079_b200.binding import _Bodies, _Joints, _ptr, _ip
+    b = _Bodies(sc.n, _ptr(sc.q0), _ptr(sc.qd0), _ptr(sc.mbar), _ptr(sc.volume), _ptr(sc.youngs), _ptr(sc.poisson),
+                None, (ctypes.c_double * 3)(*sc.gravity))
+    j = _Joints(sc.n_joints, _ptr(sc.body_a, _ip), _ptr(sc.body_b, _ip), _ptr(sc.npts, _ip), _ptr(sc.ybar_a),
+                _ptr(sc.ybar_b))
+    out = (ctypes.c_double * 8)()
+    assert lib.mabd_dbg_sparse_stats(ctypes.byref(b), ctypes.byref(j), out) == 0
+    return dict(zip(["nodes", "levels", "max_front", "front_doubles", "flops", "tasks", "launches", "rows"], out))
+
+
+def test_sparse_symbolic_nested_dissection(lib):
+    """Host symbolic analysis of the sparse solver (no GPU): the fronts cover every dual row, nested dissection
+    keeps the assembly tree shallow (levels ≈ log₂ of the leaf count) and the largest front well below the
+    dual size, and the factorization work grows like n^1.5 on 2-D nets (a 4× larger net, 8× the flops)."""
+    s32 = _sparse_stats(lib, G.cfg5_net(32))
+    s64 = _sparse_stats(lib, G.cfg5_net(64))
+    for st, sc in ((s32, G.cfg5_net(32)), (s64, G.cfg5_net(64))):
+        assert st["rows"] == 3 * int(sc.npts.sum())
+        assert st["max_front"] < 0.2 * st["rows"]
+        assert st["levels"] <= 2 * np.log2(st["nodes"] + 1) + 2
+        assert st["front_doubles"] >= st["rows"]
+    ratio = s64["flops"] / s32["flops"]
+    assert 4.0 <= ratio <= 16.0, ratio
