@@ -468,10 +468,16 @@ __global__ void __launch_bounds__(SP_THREADS) mf_trsm_kernel(SparseArgs a, const
 }
 
 // Panel step 3: trailing update C[r0.., c0..] −= P_r P_cᵀ with the panel P = F[:, k0:k0+kb] (lower tiles only);
-// task = (node, r0, c0). 64 threads, 8×8 outputs each (rows tx + 8i, columns ty + 8j), K staged 16 at a time.
+// task = (node, r0, c0). 64 threads, 8×8 outputs each (rows tx + 8i, columns ty + 8j); the panel is staged 16
+// columns at a time through a double-buffered cp.async pipeline (loads of chunk c+1 overlap the DFMAs of c).
+__device__ __forceinline__ void cp_async8(double* dst, const double* src, bool valid) {
+  const uint32_t d = (uint32_t)__cvta_generic_to_shared(dst);
+  const int sz = valid ? 8 : 0;  // zero-fill outside the front / panel
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 8, %2;" ::"r"(d), "l"(src), "r"(sz) : "memory");
+}
 __global__ void __launch_bounds__(64) mf_syrk_kernel(SparseArgs a, const int32_t* tasks, int k0) {
-  __shared__ double As[16][MF_NB];
-  __shared__ double Bs[16][MF_NB];
+  __shared__ double As[2][16][MF_NB];
+  __shared__ double Bs[2][16][MF_NB];
   const MfArgs& m = a.mf;
   const int node = tasks[3 * blockIdx.x], r0 = tasks[3 * blockIdx.x + 1], c0 = tasks[3 * blockIdx.x + 2];
   const int n = m.nown[node];
@@ -479,35 +485,47 @@ __global__ void __launch_bounds__(64) mf_syrk_kernel(SparseArgs a, const int32_t
   const int kb = min(MF_NB, n - k0);
   double* F = m.F + m.foff[node];
   const int tid = threadIdx.x, tx = tid % 8, ty = tid / 8;
+  auto stage = [&](int buf, int kk) {
+#pragma unroll
+    for (int t = 0; t < 16; ++t) {
+      const int idx = tid + 64 * t;
+      const int r = idx % MF_NB, kc = idx / MF_NB;
+      const bool kin = kk + kc < kb;
+      const double* col = F + (k0 + kk + (kin ? kc : 0)) * f;
+      cp_async8(&As[buf][kc][r], col + (r0 + r < f ? r0 + r : 0), kin && r0 + r < f);
+      cp_async8(&Bs[buf][kc][r], col + (c0 + r < f ? c0 + r : 0), kin && c0 + r < f);
+    }
+    asm volatile("cp.async.commit_group;" ::: "memory");
+  };
   double acc[8][8];
 #pragma unroll
   for (int i = 0; i < 8; ++i)
 #pragma unroll
     for (int j = 0; j < 8; ++j) acc[i][j] = 0.0;
-  for (int kk = 0; kk < kb; kk += 16) {
-    const int kc = min(16, kb - kk);
-#pragma unroll
-    for (int t = 0; t < 16; ++t) {
-      const int idx = tid + 64 * t;
-      const int r = idx % MF_NB, k = idx / MF_NB;
-      const double* col = F + (k0 + kk + k) * f;
-      As[k][r] = (k < kc && r0 + r < f) ? col[r0 + r] : 0.0;
-      Bs[k][r] = (k < kc && c0 + r < f) ? col[c0 + r] : 0.0;
+  const int nch = (kb + 15) / 16;
+  stage(0, 0);
+  for (int ch = 0; ch < nch; ++ch) {
+    const int buf = ch & 1;
+    if (ch + 1 < nch) {
+      stage(buf ^ 1, (ch + 1) * 16);
+      asm volatile("cp.async.wait_group 1;" ::: "memory");
+    } else {
+      asm volatile("cp.async.wait_group 0;" ::: "memory");
     }
     __syncthreads();
 #pragma unroll 4
     for (int k = 0; k < 16; ++k) {
       double av[8], bv[8];
 #pragma unroll
-      for (int i = 0; i < 8; ++i) av[i] = As[k][tx + 8 * i];
+      for (int i = 0; i < 8; ++i) av[i] = As[buf][k][tx + 8 * i];
 #pragma unroll
-      for (int j = 0; j < 8; ++j) bv[j] = Bs[k][ty + 8 * j];
+      for (int j = 0; j < 8; ++j) bv[j] = Bs[buf][k][ty + 8 * j];
 #pragma unroll
       for (int i = 0; i < 8; ++i)
 #pragma unroll
         for (int j = 0; j < 8; ++j) acc[i][j] = fma(av[i], bv[j], acc[i][j]);
     }
-    __syncthreads();
+    __syncthreads();  // this buffer is refilled two chunks later
   }
 #pragma unroll
   for (int j = 0; j < 8; ++j) {
