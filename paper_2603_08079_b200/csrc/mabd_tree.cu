@@ -176,17 +176,18 @@ __device__ void tree_up_warp(const TreeArgs& a, int b, int lane, double* F, int 
     if (lane == 0) {
       const double d00 = F[c * MS + c], d10 = F[(c + 1) * MS + c], d20 = F[(c + 2) * MS + c];
       const double d11 = F[(c + 1) * MS + c + 1], d21 = F[(c + 2) * MS + c + 1], d22 = F[(c + 2) * MS + c + 2];
+      // pivots by refined hardware reciprocal square roots (fast_rsqrt, ≤ 1 ulp): l = p·p^{-1/2}
       double p0 = d00;
       bool ok = p0 > 0.0;
-      const double l00 = sqrt(ok ? p0 : 1.0), i00 = 1.0 / l00;
+      const double i00 = fast_rsqrt(ok ? p0 : 1.0), l00 = (ok ? p0 : 1.0) * i00;
       const double l10 = d10 * i00, l20 = d20 * i00;
       const double p1 = d11 - l10 * l10;
       ok = ok && p1 > 0.0;
-      const double l11 = sqrt(p1 > 0.0 ? p1 : 1.0), i11 = 1.0 / l11;
+      const double i11 = fast_rsqrt(p1 > 0.0 ? p1 : 1.0), l11 = (p1 > 0.0 ? p1 : 1.0) * i11;
       const double l21 = (d21 - l20 * l10) * i11;
       const double p2 = d22 - l20 * l20 - l21 * l21;
       ok = ok && p2 > 0.0;
-      const double l22 = sqrt(p2 > 0.0 ? p2 : 1.0), i22 = 1.0 / l22;
+      const double i22 = fast_rsqrt(p2 > 0.0 ? p2 : 1.0), l22 = (p2 > 0.0 ? p2 : 1.0) * i22;
       if (!ok) treport(k, ERR_SINGULAR);
       F[c * MS + c] = l00;
       F[(c + 1) * MS + c] = l10;
