@@ -185,9 +185,10 @@ def run_ours(args, rank: int, world: int, local_rank: int) -> None:
     n = sc.n
     h = sc.h
     stream = torch.cuda.Stream(device=dev)
-    # config 3 (one chain) is split across ranks (strong scaling, one all-gather of per-rank top systems per
-    # step); every other config runs one independent assembly per rank (weak scaling, no collective)
-    split = world > 1 and args.config == 3
+    # config 3 (one chain) and config 4 (one tree) are split across ranks (strong scaling, one all-gather per step:
+    # of per-rank top systems for the chain, of the subtree roots' condensed blocks for the tree); configs 1, 2, 5
+    # run one independent assembly per rank (weak scaling, no collective; config 5 as replicas)
+    split = world > 1 and args.config in (3, 4)
     if split:
         from paper_2603_08079_b200.binding import nccl_unique_id
         blob = torch.zeros(128, dtype=torch.uint8, device=dev)
@@ -299,7 +300,10 @@ def run_ours(args, rank: int, world: int, local_rank: int) -> None:
                                  "(reset between episodes, outside the CUDA-event intervals)",
                        "dual_rows_per_gpu": info["n_dual_rows"],
                        "l2": "no flush: state q,qdot (192 MiB) + per-body params > 126 MB L2",
-                       "parallelism": (f"chain split over {world} ranks (NCCL all-gather of per-rank tops)" if split
+                       "parallelism": ((f"chain split over {world} ranks (NCCL all-gather of per-rank tops)"
+                                        if args.config == 3 else
+                                        f"tree split over {world} ranks (subtrees per rank, NCCL all-gather of the "
+                                        "roots' condensed blocks, top levels replicated)") if split
                                        else f"dp{world} (independent assemblies per rank)")},
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                          "frac": achieved / peak, "traffic": traffic,

@@ -142,12 +142,15 @@ mabd_status mabd_query(mabd_handle h_, int32_t *solver, int32_t *launches_per_st
 mabd_status mabd_nccl_unique_id(void *out, size_t bytes);
 
 /* Host-only analysis for tests: out[0..9] = {parts, windows, long windows, this rank's window range lo/hi,
- * long-window range lo/hi, left_open, right_open, sequential-top unknowns}. No device work. */
+ * long-window range lo/hi, left_open, right_open, sequential-top unknowns} of the chain split; with
+ * n_out >= 20 also out[10..19] = {solver, tree parts, bottom groups, groups per part, gather slots per part,
+ * this rank's group range lo/hi and body range lo/hi, joints into bottom groups} of the tree split
+ * (SURVEY §8(e)). No device work. */
 mabd_status mabd_partition_info(const mabd_bodies *bodies, const mabd_joints *joints,
                                 const mabd_options *opts, int64_t *out, int64_t n_out);
 
-/* Statistics of the last mabd_step call: iterations of the last iterative dual solve (sparse solver: PCG
- * iterations of the final step; 0 for the direct chain/tree solvers). Synchronises the handle's stream. */
+/* Statistics of the last mabd_step call: iterative-refinement passes of the sparse solver's direct dual solve
+ * (0 for the chain and tree solvers). Synchronises the handle's stream. */
 mabd_status mabd_solver_stats(mabd_handle h_, int64_t *last_iterations);
 
 /* Release device memory owned by the library; NULL is a no-op. */

@@ -113,7 +113,7 @@ def nccl_unique_id() -> bytes:
 
 
 def partition_info(scene, world: int, rank: int) -> dict:
-    """Host-only plan of the multi-part chain decomposition for one rank (no GPU needed)."""
+    """Host-only plan of the multi-part chain / tree decomposition for one rank (no GPU needed)."""
     lib = load_library()
     n = int(scene.q0.shape[0])
     K = int(scene.body_a.shape[0])
@@ -127,12 +127,13 @@ def partition_info(scene, world: int, rank: int) -> dict:
     j = _Joints(K, _ptr(k["body_a"], _ip), _ptr(k["body_b"], _ip), _ptr(k["npts"], _ip), _ptr(k["ybar_a"]),
                 _ptr(k["ybar_b"]))
     o = _Options(1, 1, 0, int(rank), int(world), None, None, 0, None)
-    out = (ctypes.c_int64 * 10)()
-    st = lib.mabd_partition_info(ctypes.byref(b), ctypes.byref(j), ctypes.byref(o), out, 10)
+    out = (ctypes.c_int64 * 20)()
+    st = lib.mabd_partition_info(ctypes.byref(b), ctypes.byref(j), ctypes.byref(o), out, 20)
     if st != MABD_OK:
         raise MabdError(st, lib.mabd_last_error(None).decode())
     keys = ["parts", "windows", "long_windows", "win_lo", "win_hi", "long_lo", "long_hi", "left_open", "right_open",
-            "seq_unknowns"]
+            "seq_unknowns", "solver", "tree_parts", "groups", "groups_per_part", "slots_per_part", "group_lo",
+            "group_hi", "body_lo", "body_hi", "root_joints"]
     return dict(zip(keys, list(out)))
 
 

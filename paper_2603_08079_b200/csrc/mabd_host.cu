@@ -175,7 +175,15 @@ mabd_status mabd_get_state(mabd_handle c, double* q_out, double* qd_out, int out
   const int64_t n = c->plan.n;
   if (c->plan.use_nccl) {  // every rank advanced only its windows: share them (outside any timed loop)
     std::vector<std::pair<int64_t, int64_t>> ranges;
-    for (const auto& P : c->plan.parts) ranges.push_back({P.win_lo * SEG, P.win_hi * SEG});
+    if (c->plan.solver == MABD_SOLVER_TREE) {  // each rank advanced its bottom groups (the top is replicated)
+      const TreePlan& t = c->plan.tree;
+      for (int r = 0; r < t.parts; ++r) {
+        const int lo = std::min(t.n_bottom, r * t.gpr), hi = std::min(t.n_bottom, (r + 1) * t.gpr);
+        ranges.push_back({t.group_off[lo], t.group_off[hi]});
+      }
+    } else {
+      for (const auto& P : c->plan.parts) ranges.push_back({P.win_lo * SEG, P.win_hi * SEG});
+    }
     int rc = nccl_bcast_ranges(c->d.nccl_comm, c->d.b.q, ranges, c->d.b.ld, 12, c->stream);
     if (rc == 0) rc = nccl_bcast_ranges(c->d.nccl_comm, c->d.b.qd, ranges, c->d.b.ld, 12, c->stream);
     if (rc != 0) return fail(c, MABD_ENCCL, "state broadcast: %s", nccl_err(rc));
@@ -263,6 +271,18 @@ mabd_status mabd_partition_info(const mabd_bodies* bodies, const mabd_joints* jo
     out[7] = P.left_open; out[8] = P.right_open; out[9] = P.n2;
   } else {
     out[3] = 0; out[4] = p.n_windows; out[5] = 0; out[6] = p.n_long; out[7] = 0; out[8] = 0; out[9] = 0;
+  }
+  if (n_out >= 20) {  // tree split: solver, parts, bottom groups, groups per part, gather slots per part, this
+                      // part's group range and body range, first top body, joints into the bottom groups
+    for (int i = 10; i < 20; ++i) out[i] = 0;
+    out[10] = p.solver;
+    if (p.solver == MABD_SOLVER_TREE) {
+      const TreePlan& t = p.tree;
+      const int lo = std::min(t.n_bottom, t.part * t.gpr), hi = std::min(t.n_bottom, (t.part + 1) * t.gpr);
+      out[11] = t.parts; out[12] = t.n_bottom; out[13] = t.gpr; out[14] = t.rpp;
+      out[15] = lo; out[16] = hi; out[17] = t.group_off[lo]; out[18] = t.group_off[hi];
+      out[19] = t.parts > 1 ? (int64_t)t.root_joint.size() : 0;
+    }
   }
   return MABD_OK;
 }

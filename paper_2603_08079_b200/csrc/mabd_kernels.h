@@ -74,6 +74,9 @@ struct TreeArgs {
   const int32_t* pt_off;       // [n+1] per body: its frontal points in pt_code
   const int32_t* pt_code;      // 4·joint + 2·point + (child side)
   const int32_t* body_nn;      // [n] N | nu << 8
+  const int32_t* root_joint;   // multi-part: joints from top bodies into bottom groups, by group
+  const int32_t* root_slot;    // their slot in xbuf
+  double* xbuf;                // multi-part: [parts][rpp][42] condensed root blocks (all-gather buffer)
   int64_t n;                   // bodies
   StepConsts k;
 };

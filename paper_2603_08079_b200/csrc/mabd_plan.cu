@@ -416,8 +416,13 @@ mabd_status build_plan(const mabd_bodies* B, const mabd_joints* J, const mabd_op
     return MABD_EUNSUPPORTED;
   }
   if (p->newton_iters > 1) p->launches_per_step = p->newton_iters * p->launches_per_step + 2;  // + prep, final
-  if (o && o->world > 1 && p->solver != MABD_SOLVER_CHAIN)
-    return *msg = "world > 1 is implemented for the chain solver only (run tree/sparse scenes as replicas)",
+  if (o && o->world > 1 && p->solver == MABD_SOLVER_TREE) {
+    const int W = o->world;
+    p->use_nccl = o->nccl_unique_id != nullptr;
+    if (!tree_partition(p, W, o->rank, !p->use_nccl, msg)) return MABD_EINVAL;
+  }
+  if (o && o->world > 1 && p->solver == MABD_SOLVER_SPARSE)
+    return *msg = "world > 1 is implemented for the chain and tree solvers (run nets as replicas)",
            MABD_EUNSUPPORTED;
   // per-position arrays
   const int64_t ld = p->ld;
@@ -515,6 +520,9 @@ mabd_status build_plan(const mabd_bodies* B, const mabd_joints* J, const mabd_op
     f.t_ptoff = take(sizeof(int32_t) * (n + 1));
     f.t_ptcode = take(sizeof(int32_t) * std::max<size_t>(1, t.pt_code.size()));
     f.t_nn = take(sizeof(int32_t) * n);
+    f.t_rootj = take(sizeof(int32_t) * std::max<size_t>(1, t.root_joint.size()));
+    f.t_rslot = take(sizeof(int32_t) * std::max<size_t>(1, t.root_slot.size()));
+    f.t_xbuf = take(sizeof(double) * 42 * (size_t)std::max(1, t.parts * t.rpp));
   }
   if (p->solver == MABD_SOLVER_SPARSE) sparse_layout(p, take);
   p->workspace_bytes = cur;
@@ -624,6 +632,11 @@ cudaError_t upload_plan(const Plan& p, char* ws, cudaStream_t st, DevPtrs* d) {
     A.pt_off = (const int32_t*)(ws + f.t_ptoff);
     A.pt_code = (const int32_t*)(ws + f.t_ptcode);
     A.body_nn = (const int32_t*)(ws + f.t_nn);
+    A.root_joint = (const int32_t*)(ws + f.t_rootj);
+    A.root_slot = (const int32_t*)(ws + f.t_rslot);
+    A.xbuf = (double*)(ws + f.t_xbuf);
+    if ((e = put((int32_t*)A.root_joint, t.root_joint, st))) return e;
+    if ((e = put((int32_t*)A.root_slot, t.root_slot, st))) return e;
     if ((e = put((int32_t*)A.pt_off, t.pt_off, st))) return e;
     if ((e = put((int32_t*)A.pt_code, t.pt_code, st))) return e;
     if ((e = put((int32_t*)A.body_nn, t.body_nn, st))) return e;

@@ -39,6 +39,14 @@ struct TreePlan {
   int64_t ws_total = 0;
   int32_t max_m = 3;                 // largest frontal matrix (rows)
   std::vector<int32_t> pt_off, pt_code, body_nn;  // per body: frontal point codes, N | nu << 8
+  // multi-GPU split: the bottom groups are divided into W contiguous blocks of gpr groups;
+  // each part eliminates its groups, the condensed blocks (Ŝ_u, r̂_u) of the group roots' up joints are
+  // all-gathered, and every part solves the top levels redundantly
+  int32_t parts = 1, part = 0, gpr = 0, rpp = 0;
+  bool emulate = false;                      // W parts in one process (no NCCL): single-GPU test of the split
+  std::vector<int32_t> root_off;             // [n_bottom+1] CSR: joints from a top body into each bottom group
+  std::vector<int32_t> root_joint;           // those joints, by group
+  std::vector<int32_t> root_slot;            // their slot in the gather buffer: part · rpp + index in part
 };
 
 // Sparse plan: constraint points, body → point incidence, and the multifrontal symbolic factorization of the
@@ -124,7 +132,7 @@ struct Plan {
     size_t all_tops, lam_g, plo, lwin, llong;
     std::vector<size_t> p_tops1, p_lam2, p_scr;
     size_t t_up, t_coff, t_cj, t_wsoff, t_jnpts, t_jchd, t_jy, t_goff, t_glp, t_glo, t_shat, t_rhat, t_lam, t_bscr,
-        t_ws, t_ptoff, t_ptcode, t_nn;
+        t_ws, t_ptoff, t_ptcode, t_nn, t_rootj, t_rslot, t_xbuf;
   } off{};
 };
 
@@ -173,6 +181,7 @@ cudaError_t launch_step(const Plan& p, const DevPtrs& d, double h, int32_t step,
 bool tree_build(const mabd_joints* joints, int64_t n, Plan* p, std::vector<int64_t>* pos_of_body, std::string* msg);
 cudaError_t tree_step(const Plan& p, const DevPtrs& d, const StepConsts& k, cudaStream_t st);
 cudaError_t tree_init();
+bool tree_partition(Plan* p, int W, int rank, bool emulate, std::string* msg);
 
 // sparse solver (mabd_sparse.cu)
 bool sparse_build(const mabd_bodies* bodies, const mabd_joints* joints, Plan* p, std::vector<int64_t>* pos_of_body,

@@ -10,9 +10,12 @@
 // Down (root first): λ_X = F_XX⁻¹(r_X − F_Xu λ_u), then qⁿ⁺¹ = q̃ − diag₄(R)H̄⁻¹Σ±Γᵀ Rᵀλ.
 // The dual graph of a tree is chordal in this order, so the elimination has no fill (PROBE in SURVEY A12).
 //
-// Parallel schedule: bodies are grouped into CTA-local subtrees (≤ 256 bodies; levels separated by
-// __syncthreads) plus one top group (bodies whose subtree is larger) processed by a single CTA.
-// Launches per step: up(bottom) → up+down(top) → down(bottom), or one fused launch when there is no top.
+// Parallel schedule: a predict kernel for all bodies; bodies are grouped into CTA-local subtrees (≤ 256 bodies;
+// levels separated by __syncthreads; upward one warp per body, downward one thread per body) plus a top group
+// (bodies whose subtree is larger), whose levels run as one launch each over the whole GPU.
+// Across ranks: each rank takes a contiguous block of the CTA-local subtrees, eliminates
+// them, and shares the condensed blocks (Ŝ_u, r̂_u) of the joints into the top through one all-gather; every
+// rank then solves the top levels redundantly and finishes its own subtrees.
 #include <cuda_runtime.h>
 
 #include <algorithm>
@@ -41,10 +44,10 @@ __device__ __forceinline__ void treport(const StepConsts& k, int32_t flag) {
 }
 
 // Stages 1-2 for every body at once (no tree dependency): R and δq̃ → bscr.
-__global__ void tree_predict_kernel(TreeArgs a) {
+__global__ void tree_predict_kernel(TreeArgs a, int64_t b0, int64_t b1) {
   const StepConsts& k = a.k;
   const int64_t ld = a.b.ld;
-  for (int64_t b = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; b < a.n; b += (int64_t)gridDim.x * blockDim.x) {
+  for (int64_t b = b0 + blockIdx.x * (int64_t)blockDim.x + threadIdx.x; b < b1; b += (int64_t)gridDim.x * blockDim.x) {
     double q[12], qd[12], R[9], dqt[12];
 #pragma unroll
     for (int c = 0; c < 12; ++c) {
@@ -392,6 +395,28 @@ __global__ void __launch_bounds__(512) tree_kernel(TreeArgs a, int mode, int MS)
   }
 }
 
+// Multi-part split: the condensed child side (Ŝ_u 36, r̂_u 6) of every joint from a top body into a bottom group,
+// packed by the part owning the group into its block of the all-gather buffer, then unpacked by every part into
+// Shat / rhat for the top levels. Root entries [r0, r1) are those of a part's groups.
+__global__ void tree_pack_kernel(TreeArgs a, int r0, int r1) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  const int r = r0 + i / 42, e = i % 42;
+  if (r >= r1) return;
+  const int u = a.root_joint[r];
+  a.xbuf[(size_t)a.root_slot[r] * 42 + e] = e < 36 ? a.Shat[36 * (int64_t)u + e] : a.rhat[6 * (int64_t)u + e - 36];
+}
+__global__ void tree_unpack_kernel(TreeArgs a, int nroot) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  const int r = i / 42, e = i % 42;
+  if (r >= nroot) return;
+  const int u = a.root_joint[r];
+  const double v = a.xbuf[(size_t)a.root_slot[r] * 42 + e];
+  if (e < 36)
+    a.Shat[36 * (int64_t)u + e] = v;
+  else
+    a.rhat[6 * (int64_t)u + e - 36] = v;
+}
+
 static int tree_ms(int max_m) { return max_m + 2 + ((max_m & 1) ? 0 : 1); }  // row stride (odd)
 
 cudaError_t launch_tree(const TreeArgs& a, int ngroups, int mode, int threads, cudaStream_t st) {
@@ -402,18 +427,50 @@ cudaError_t launch_tree(const TreeArgs& a, int ngroups, int mode, int threads, c
   return cudaGetLastError();
 }
 
+static unsigned grid_for_bodies(int64_t nb) {
+  return (unsigned)std::max<int64_t>(1, std::min<int64_t>((nb + 255) / 256, 148 * 8));
+}
+
 cudaError_t tree_step(const Plan& p, const DevPtrs& d, const StepConsts& k, cudaStream_t st) {
   TreeArgs a = d.tree;
   a.k = k;
   const TreePlan& t = p.tree;
   cudaError_t e;
-  tree_predict_kernel<<<(unsigned)std::max<int64_t>(1, std::min<int64_t>((a.n + 255) / 256, 148 * 8)), 256, 0, st>>>(a);
   // warps per CTA of the CTA-local subtrees: up to 8 within the shared memory
   const size_t per_warp = sizeof(double) * ((size_t)t.max_m * tree_ms(t.max_m) + 9 * (TREE_MAXN / 3));
   const int bot_threads = 32 * (int)std::max<size_t>(1, std::min<size_t>(8, (200 * 1024) / std::max<size_t>(per_warp, 1)));
-  if (!t.has_top) return launch_tree(a, t.n_bottom, TREE_BOTH, bot_threads, st);
-  a.group0 = 0;
-  if ((e = launch_tree(a, t.n_bottom, TREE_UP, bot_threads, st))) return e;
+  // bottom groups of this process: all of them, or this rank's block when the tree is split across ranks
+  const bool split = t.parts > 1 && !t.emulate;
+  const int g_lo = split ? std::min(t.n_bottom, t.part * t.gpr) : 0;
+  const int g_hi = split ? std::min(t.n_bottom, (t.part + 1) * t.gpr) : t.n_bottom;
+  const int64_t top0 = t.group_off[t.n_bottom];
+  if (split) {  // stages 1-2 for this rank's bottom bodies and the (replicated) top bodies
+    const int64_t b0 = t.group_off[g_lo], b1 = t.group_off[g_hi];
+    if (b1 > b0) tree_predict_kernel<<<grid_for_bodies(b1 - b0), 256, 0, st>>>(a, b0, b1);
+    if (a.n > top0) tree_predict_kernel<<<grid_for_bodies(a.n - top0), 256, 0, st>>>(a, top0, a.n);
+  } else {
+    tree_predict_kernel<<<grid_for_bodies(a.n), 256, 0, st>>>(a, 0, a.n);
+  }
+  if (!t.has_top) {
+    a.group0 = g_lo;
+    return launch_tree(a, g_hi - g_lo, TREE_BOTH, bot_threads, st);
+  }
+  a.group0 = g_lo;
+  if ((e = launch_tree(a, g_hi - g_lo, TREE_UP, bot_threads, st))) return e;
+  if (t.parts > 1) {  // exchange of the group roots' condensed blocks (one all-gather; emulated: every part local)
+    const int q0 = split ? t.part : 0, q1 = split ? t.part + 1 : t.parts;
+    for (int q = q0; q < q1; ++q) {
+      const int lo = std::min(t.n_bottom, q * t.gpr), hi = std::min(t.n_bottom, (q + 1) * t.gpr);
+      const int r0 = t.root_off[lo], r1 = t.root_off[hi];
+      if (r1 > r0) tree_pack_kernel<<<(unsigned)(((r1 - r0) * 42 + 255) / 256), 256, 0, st>>>(a, r0, r1);
+    }
+    if (split && t.rpp > 0) {
+      const int rc = nccl_allgather_doubles(d.nccl_comm, a.xbuf, (size_t)t.rpp * 42, t.part, st);
+      if (rc != 0) return cudaErrorUnknown;
+    }
+    const int nroot = t.root_off[t.n_bottom];
+    if (nroot > 0) tree_unpack_kernel<<<(unsigned)((nroot * 42 + 255) / 256), 256, 0, st>>>(a, nroot);
+  }
   // the top group: one launch per level over the whole GPU (a body per warp up, per thread down), deepest first
   const int g = t.n_bottom;
   const int l0 = t.glev_ptr[g], l1 = t.glev_ptr[g + 1] - 1;
@@ -431,8 +488,50 @@ cudaError_t tree_step(const Plan& p, const DevPtrs& d, const StepConsts& k, cuda
     tree_kernel<<<(nb + 127) / 128, 128, 0, st>>>(a, TREE_DOWN_LEVEL, MS);
   }
   if ((e = cudaGetLastError())) return e;
-  a.group0 = 0;
-  return launch_tree(a, t.n_bottom, TREE_DOWN, bot_threads, st);
+  a.group0 = g_lo;
+  return launch_tree(a, g_hi - g_lo, TREE_DOWN, bot_threads, st);
+}
+
+// Split across W ranks (or W emulated parts): contiguous blocks of gpr bottom groups; the joints from top bodies
+// into each group, with their gather-buffer slots (rpp per part).
+bool tree_partition(Plan* p, int W, int rank, bool emulate, std::string* msg) {
+  TreePlan& t = p->tree;
+  t.parts = W;
+  t.part = rank;
+  t.emulate = emulate;
+  t.gpr = std::max(1, (t.n_bottom + W - 1) / W);
+  if (!emulate && t.n_bottom < W)
+    return *msg = "tree split: fewer CTA-local subtrees than ranks (run as replicas)", false;
+  const int64_t n = p->n, top0 = t.n_bottom < (int)t.group_off.size() ? t.group_off[t.n_bottom] : n;
+  std::vector<int32_t> group_of(n, -1);
+  for (int g = 0; g < t.n_bottom; ++g)
+    for (int b = t.group_off[g]; b < t.group_off[g + 1]; ++b) group_of[b] = g;
+  std::vector<std::vector<int32_t>> per(std::max(1, t.n_bottom));
+  for (int64_t pb = top0; pb < n; ++pb)  // child joints of top bodies whose child lies in a bottom group
+    for (int j = t.child_off[pb]; j < t.child_off[pb + 1]; ++j) {
+      const int cj = t.child_joint[j];
+      const int cb = t.jchd[cj];
+      if (cb >= 0 && group_of[cb] >= 0) per[group_of[cb]].push_back(cj);
+    }
+  t.root_off.assign(t.n_bottom + 1, 0);
+  t.root_joint.clear();
+  for (int g = 0; g < t.n_bottom; ++g) {
+    std::sort(per[g].begin(), per[g].end());
+    t.root_joint.insert(t.root_joint.end(), per[g].begin(), per[g].end());
+    t.root_off[g + 1] = (int32_t)t.root_joint.size();
+  }
+  t.rpp = 0;
+  t.root_slot.assign(t.root_joint.size(), 0);
+  for (int q = 0; q < W; ++q) {
+    const int lo = std::min(t.n_bottom, q * t.gpr), hi = std::min(t.n_bottom, (q + 1) * t.gpr);
+    t.rpp = std::max(t.rpp, t.root_off[hi] - t.root_off[lo]);
+  }
+  for (int q = 0; q < W; ++q) {
+    const int lo = std::min(t.n_bottom, q * t.gpr), hi = std::min(t.n_bottom, (q + 1) * t.gpr);
+    for (int r = t.root_off[lo]; r < t.root_off[hi]; ++r) t.root_slot[r] = q * t.rpp + (r - t.root_off[lo]);
+  }
+  p->launches_per_step += 3;
+  return true;
 }
 
 cudaError_t tree_init() {

@@ -64,3 +64,34 @@ def test_cfg3_full_size_one_step_vs_oracle(cuda_ok):
     q_g, _ = run(sc, 1, 1)
     q_o, _ = O.step(sc, sc.q0, sc.qd0, sc.h, route="blocklu")
     assert O.rel_err(q_g, q_o) <= TOL1
+
+
+# ----------------------------------------------------------------------------- trees
+
+@pytest.mark.parametrize("world", [2, 4, 8])
+def test_tree_parts_vs_oracle(cuda_ok, world):
+    """Config-4 recipe at depth 11 (2,047 bodies: 8 CTA-local subtrees and a 7-body top), split into W parts:
+    each part eliminates its subtrees, the condensed root blocks go through the gather buffer, the top is solved
+    by every part. Bitwise the same as the unsplit path (the exchange only copies), and parity with the oracle."""
+    sc = G.cfg4_binary_tree(11)
+    q1, info = run(sc, 3, world)
+    assert info["solver"] == "tree"
+    q_single, _ = run(sc, 3, 1)
+    assert np.array_equal(q1, q_single)
+    q_o, _ = O.simulate(sc, 3)
+    assert O.rel_err(q1, q_o) <= 1e-6
+
+
+@pytest.mark.parametrize("world", [2, 3])
+def test_random_forest_parts(cuda_ok, world):
+    """Random trees packed several per CTA-local group (a group has several joints into the top)."""
+    rng = np.random.default_rng(5)
+    parts = [G.random_tree(int(rng.integers(300, 700)), seed=40 + k, hinge_frac=0.5, vel=0.3, jitter=1e-3,
+                           max_children=3) for k in range(3)]
+    sc = _concat(parts)
+    q1, info = run(sc, 2, world)
+    assert info["solver"] == "tree"
+    q_single, _ = run(sc, 2, 1)
+    assert np.array_equal(q1, q_single)
+    q_o, _ = O.simulate(sc, 2)
+    assert O.rel_err(q1, q_o) <= 1e-6

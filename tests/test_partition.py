@@ -99,3 +99,63 @@ def test_gloo_world2_partition_consistency(lib):
     for p in ps:
         p.join(timeout=60)
     assert res == {0: True, 1: True}
+
+
+# ----------------------------------------------------------------------------- tree split
+
+def _check_tree_parts(infos):
+    W = len(infos)
+    assert all(i["solver"] == 2 and i["tree_parts"] == W for i in infos)
+    ng = infos[0]["groups"]
+    assert infos[0]["group_lo"] == 0 and infos[-1]["group_hi"] == ng
+    for a, b in zip(infos[:-1], infos[1:]):
+        assert a["group_hi"] == b["group_lo"] and a["body_hi"] == b["body_lo"]
+    for i in infos:
+        assert i["group_hi"] - i["group_lo"] <= i["groups_per_part"]
+        assert i["slots_per_part"] * W >= i["root_joints"]
+
+
+@pytest.mark.parametrize("world", [2, 4, 8])
+def test_partition_tree_cfg4(lib, world):
+    """Config 4 at full size: 256 CTA-local subtrees of 255 bodies below a 255-body top, split evenly."""
+    sc = G.cfg4_binary_tree(16)
+    infos = [lib.partition_info(sc, world, r) for r in range(world)]
+    _check_tree_parts(infos)
+    assert infos[0]["groups"] == 256 and infos[0]["root_joints"] == 256
+    assert all(i["body_hi"] - i["body_lo"] == 255 * 256 // world for i in infos)
+    assert infos[0]["slots_per_part"] == 256 // world
+
+
+def _gloo_tree_worker(rank, world, port, out):
+    import torch.distributed as dist
+    from paper_2603_08079_b200 import binding
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    sc = G.cfg4_binary_tree(12)
+    got = [None] * world
+    dist.all_gather_object(got, binding.partition_info(sc, world, rank))
+    ok = True
+    try:
+        _check_tree_parts(got)
+    except AssertionError:
+        ok = False
+    out.put((rank, ok))
+    dist.destroy_process_group()
+
+
+def test_gloo_world2_tree_partition_consistency(lib):
+    import multiprocessing as mp
+    import socket
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    port = s.getsockname()[1]
+    s.close()
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    ps = [ctx.Process(target=_gloo_tree_worker, args=(r, 2, port, q)) for r in range(2)]
+    for p in ps:
+        p.start()
+    res = dict(q.get(timeout=300) for _ in ps)
+    for p in ps:
+        p.join(timeout=60)
+    assert res == {0: True, 1: True}
