@@ -287,65 +287,60 @@ __device__ void tree_up_warp(const TreeArgs& a, int b, int lane, double* F, int 
   __syncwarp();
 }
 
+// Downward pass at body b: λ_X = y − W λ_u for its child-joint points, then the update (stage 4). Every input
+// except λ_u (written by the parent's level) is fetched up front from the per-body tables (body_nn, pt_code,
+// bscr, ws), so one thread waits on about three dependent memory round trips instead of walking the child
+// lists.
 __device__ void tree_down(const TreeArgs& a, int b) {
   const StepConsts& k = a.k;
   const int64_t ld = a.b.ld;
-  const int c0 = a.child_off[b], c1 = a.child_off[b + 1];
+  const int nn = a.body_nn[b], N = nn & 255, nu = nn >> 8;
   const int u = a.up_joint[b];
-  int N = 0;
-  for (int j = c0; j < c1; ++j) N += 3 * a.jnpts[a.child_joint[j]];
-  const int nu = u >= 0 ? 3 * a.jnpts[u] : 0;
+  const int32_t* pcode = a.pt_code + a.pt_off[b];
   const double* ws = a.ws + a.ws_off[b];
-  double lu[6];  // fixed-size, fully unrolled accesses only (no local memory)
-#pragma unroll
-  for (int r = 0; r < 6; ++r) lu[r] = r < nu ? a.lam[6 * (int64_t)u + r] : 0.0;
-  if (u >= 0) {  // λ_X = y − W λ_u
-    int off = 0;
-    for (int j = c0; j < c1; ++j) {
-      const int kj = a.child_joint[j];
-      const int n3 = 3 * a.jnpts[kj];
-      for (int r = 0; r < n3; ++r) {
-        double v = ws[off + r];
-        const double* wr = ws + N + (off + r) * nu;
-#pragma unroll
-        for (int c = 0; c < 6; ++c)
-          if (c < nu) v -= wr[c] * lu[c];
-        a.lam[6 * (int64_t)kj + r] = v;
-      }
-      off += n3;
-    }
-  }
-  // stage 4: qⁿ⁺¹ = q̃ − diag₄(R) H̄⁻¹ Σ ±Γ(ȳ)ᵀ Rᵀλ
   const double* sc = a.bscr + 21 * (int64_t)b;
   double R[9];
 #pragma unroll
   for (int c = 0; c < 9; ++c) R[c] = sc[c];
+  HinvBlk H;
+  {
+    const int mid = a.b.mat_id ? a.b.mat_id[b] : 0;
+    if (a.hinv_tab)
+      H = a.hinv_tab[mid];
+    else
+      hinv_blocks(a.b.mats[mid], a.b.mscale ? a.b.mscale[b] : 1.0, k.ih2, H);
+  }
+  double lu[6];  // fixed-size, fully unrolled accesses only (no local memory)
+#pragma unroll
+  for (int r = 0; r < 6; ++r) lu[r] = r < nu ? a.lam[6 * (int64_t)u + r] : 0.0;
   double gq[12];
 #pragma unroll
   for (int c = 0; c < 12; ++c) gq[c] = 0.0;
-  for (int j = c0; j < c1; ++j) {
-    const int kj = a.child_joint[j];
-    for (int p = 0; p < a.jnpts[kj]; ++p) {
-      double lam[3], w[3];
+#pragma unroll 2
+  for (int i = 0; i < N / 3; ++i) {  // child-joint points (this body is their parent side, sign +)
+    const int code = pcode[i];
+    const int kj = code >> 2, pp = (code >> 1) & 1;
+    double lam[3], w[3];
 #pragma unroll
-      for (int e = 0; e < 3; ++e) lam[e] = a.lam[6 * (int64_t)kj + 3 * p + e];
-      mat3t_vec(R, lam, w);
-      add_point_force(gq, a.jy + 12 * (int64_t)kj + 3 * p, w, 1.0);
+    for (int r = 0; r < 3; ++r) {
+      double v = ws[3 * i + r];
+      const double* wr = ws + N + (3 * i + r) * nu;
+#pragma unroll
+      for (int c = 0; c < 6; ++c)
+        if (c < nu) v -= wr[c] * lu[c];
+      lam[r] = v;
+      a.lam[6 * (int64_t)kj + 3 * pp + r] = v;
     }
+    mat3t_vec(R, lam, w);
+    add_point_force(gq, a.jy + 12 * (int64_t)kj + 3 * pp, w, 1.0);
   }
 #pragma unroll
-  for (int p = 0; p < 2; ++p) {
-    if (3 * p >= nu) break;
+  for (int pp = 0; pp < 2; ++pp) {  // up-joint points (this body is their child side, sign −)
+    if (3 * pp >= nu) break;
     double w[3];
-    mat3t_vec(R, lu + 3 * p, w);
-    add_point_force(gq, a.jy + 12 * (int64_t)u + 6 + 3 * p, w, -1.0);
+    mat3t_vec(R, lu + 3 * pp, w);
+    add_point_force(gq, a.jy + 12 * (int64_t)u + 6 + 3 * pp, w, -1.0);
   }
-  HinvBlk H;
-  const int mid = a.b.mat_id ? a.b.mat_id[b] : 0;
-  if (a.hinv_tab)
-    H = a.hinv_tab[mid];
-  else
-    hinv_blocks(a.b.mats[mid], a.b.mscale ? a.b.mscale[b] : 1.0, k.ih2, H);
   double uu[12];
   hinv_apply(H, gq, uu);
 #pragma unroll
