@@ -498,8 +498,11 @@ __device__ __forceinline__ void get_hinv(const ChainArgs& a, const Material& M, 
     hinv_blocks(M, msc, a.k.ih2, H);
 }
 
+#ifndef MABD_CHAIN_CTAS
+#define MABD_CHAIN_CTAS 4  // CTAs per SM (shared memory: 4 × 56.8 KB; TMEM: 4 × 128 columns)
+#endif
 template <bool FINISH>
-__global__ void __launch_bounds__(CT, 4) chain_kernel(ChainArgs a) {
+__global__ void __launch_bounds__(CT, MABD_CHAIN_CTAS) chain_kernel(ChainArgs a) {
   extern __shared__ __align__(16) double smem[];
   const CRS s = cr_smem(smem);
   uint64_t* bar = reinterpret_cast<uint64_t*>(smem + LDS * 27);
@@ -1043,7 +1046,7 @@ cudaError_t launch_chain(const ChainArgs& a0, int nitems, bool finish, cudaStrea
   ChainArgs a = a0;
   a.n_items = nitems;
   const size_t sm = chain_smem_bytes();
-  const int grid = std::min(nitems, 4 * std::max(g_num_sms, 1));
+  const int grid = std::min(nitems, MABD_CHAIN_CTAS * std::max(g_num_sms, 1));
   if (finish)
     chain_kernel<true><<<grid, CT, sm, st>>>(a);
   else

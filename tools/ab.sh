@@ -1,8 +1,7 @@
 mkdir -p gpurun_out
-timeout 900 python -m pytest tests/test_gpu_chain.py tests/test_gpu_multipart.py -x -q > gpurun_out/ch_test.log 2>&1; echo "rc=$?" >> gpurun_out/ch_test.log
 for i in 1 2; do
-for v in prev cur; do
-  if [ $v = cur ]; then L=paper_2603_08079_b200/libmabd.so; else L=build_variants/lib_$v.so; fi
+for v in prev cta3; do
+  L=build_variants/lib_$v.so
   echo "== $v" >> gpurun_out/ab.log
   MABD_LIB=$L timeout 300 python bench.py --no-cpu-baseline --e2e-steps 1 2>&1 | python -c "import json,sys; [print('bench', round(json.loads(l)['ms_per_step']*1e3,1)) for l in sys.stdin if l.startswith('{')]" >> gpurun_out/ab.log
   MABD_LIB=$L timeout 300 python bench.py --no-cpu-baseline --e2e-steps 1 --config 3 --steps 20 2>&1 | python -c "import json,sys; [print('bench3', round(json.loads(l)['ms_per_step']*1e3,1)) for l in sys.stdin if l.startswith('{')]" >> gpurun_out/ab.log
