@@ -68,6 +68,7 @@ class Scene:
     nsteps: int = 1
     material: Optional[np.ndarray] = None   # [n] int32 or None
     meta: dict = field(default_factory=dict)
+    wrench: Optional[np.ndarray] = None     # [n,6] external wrench (τ, f), world frame, constant; None = none
 
     @property
     def n(self) -> int:

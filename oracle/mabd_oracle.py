@@ -37,6 +37,7 @@ import scipy.sparse.linalg as spla
 __all__ = [
     "lame", "unpack_mbar", "mass_A", "kbar_A", "hbar_A", "polar", "elastic_force_A", "affine_force",
     "body_hessians", "constraint_system", "constraint_residual", "predict", "step", "simulate", "nonlinear_residual",
+    "wrench_force", "twist_velocity", "angular_velocity",
     "block_thomas", "leaf_to_root_solve", "dual_matrix", "rel_err", "T9", "vec", "unvec",
 ]
 
@@ -167,6 +168,37 @@ def affine_force(q, qd, mbar, V, E, nu, g, h) -> np.ndarray:
     return f
 
 
+def wrench_force(q, W) -> np.ndarray:
+    """Affine force of an external spatial wrench W = [τ; f] (Eq. module1-wrench-map):
+    f_A,ext = G(A)ᵀ W with the ABD-to-twist map G(A) = [½[q₁]× ½[q₂]× ½[q₃]× 0; 0 0 0 I₃], so
+    the A-column c receives ½[q_c]×ᵀτ = ½ τ × q_c and the t-block receives f."""
+    q = np.asarray(q, dtype=np.float64)
+    W = np.asarray(W, dtype=np.float64)
+    out = np.zeros(q.shape)
+    tau = W[..., 0:3]
+    for c in range(3):
+        out[..., 3 * c:3 * c + 3] = 0.5 * np.cross(tau, q[..., 3 * c:3 * c + 3])
+    out[..., 9:12] = W[..., 3:6]
+    return out
+
+
+def twist_velocity(q, omega, v) -> np.ndarray:
+    """ABD velocity of a rigid twist (ω, v): q̇_c = ω × q_c, ṫ = v (inverse of P:655-667 on rigid motions)."""
+    q = np.asarray(q, dtype=np.float64)
+    qd = np.zeros(q.shape)
+    for c in range(3):
+        qd[..., 3 * c:3 * c + 3] = np.cross(omega, q[..., 3 * c:3 * c + 3])
+    qd[..., 9:12] = v
+    return qd
+
+
+def angular_velocity(q, qd) -> np.ndarray:
+    """ω = ½ Σ_c q_c × q̇_c."""
+    q = np.asarray(q)
+    qd = np.asarray(qd)
+    return 0.5 * sum(np.cross(q[..., 3 * c:3 * c + 3], qd[..., 3 * c:3 * c + 3]) for c in range(3))
+
+
 def body_hessians(R, Hbar) -> np.ndarray:
     """H_A^j = diag₄(R) H̄ diag₄(Rᵀ) (P:256-258 with P:243-254), as dense 12×12 per body."""
     R = np.asarray(R)
@@ -229,6 +261,8 @@ def predict(scene, q, qd, h):
     A = unvec(q[:, :9])
     R = polar(A)
     f = affine_force(q, qd, scene.mbar, scene.volume, scene.youngs, scene.poisson, scene.gravity, h)
+    if getattr(scene, "wrench", None) is not None:  # at the linearisation point
+        f = f + wrench_force(q, scene.wrench)
     Hbar = hbar_A(scene.mbar, scene.volume, scene.youngs, scene.poisson, h)
     H = body_hessians(R, Hbar)
     dq_tilde = np.linalg.solve(H, f[..., None])[..., 0]
@@ -354,6 +388,8 @@ def nonlinear_residual(scene, qn, qdn, q, h, lam=None):
     inert = np.einsum("nij,nj->ni", MA, q - qhat) / (h * h)
     gr = inert.copy()
     gr[:, :9] += elastic_force_A(unvec(q[:, :9]), scene.volume, mu, lam_)
+    if getattr(scene, "wrench", None) is not None:
+        gr -= wrench_force(q, scene.wrench)
     J, world = constraint_system(scene)
     g = gr.reshape(-1)
     if J.shape[0]:

@@ -440,3 +440,58 @@ def test_one_iteration_is_the_plain_step():
     a = O.step(sc, sc.q0, sc.qd0, sc.h)
     b = O.step(sc, sc.q0, sc.qd0, sc.h, iters=1)
     assert np.array_equal(a[0], b[0]) and np.array_equal(a[1], b[1])
+
+
+# ----------------------------------------------------------------------------- external wrenches (§8(f) NEXT 1)
+
+def test_wrench_com_force_free_flight():
+    """A constant force f at the centre of mass acts like an extra uniform field f/m: the free-fall closed form
+    with g + f/m (P:672-676 with G's t-block = I₃)."""
+    R0 = G.random_rotations(np.random.default_rng(7), 1)[0]
+    v0, t0 = np.array([0.5, 0.0, -1.0]), np.array([0.1, 0.2, 0.3])
+    sc = G.free_body(A0=R0, t0=t0, v0=v0, dims=(0.2, 0.1, 0.3), E=1e8)
+    f = np.array([3.0, -1.0, 2.0])
+    sc.wrench = np.array([[0, 0, 0, *f]])
+    n, h = 15, sc.h
+    q, qd = O.simulate(sc, n)
+    a = sc.gravity + f / sc.mbar[0, 9]
+    t_ref = t0 + n * h * v0 + 0.5 * n * (n + 1) * h * h * a
+    assert np.max(np.abs(q[0, 9:] - t_ref)) <= 1e-13 * np.max(np.abs(t_ref))
+    assert np.max(np.abs(q[0, :9] - O.vec(R0))) < 1e-14
+
+
+def test_wrench_torque_is_rigid_body_dynamics():
+    """A torque τ on a stiff body at rest: after one step its angular velocity ω = ½Σ q_c × q̇_c is the
+    rigid-body ω = I_w⁻¹τh (Euler's equations from rest; I_w = R₀ I_body R₀ᵀ), to O(h) and the stiffness-limited
+    non-rigid part. A wrong sign, factor ½ or cross-product order in G(A)ᵀW fails this."""
+    R0 = G.random_rotations(np.random.default_rng(1), 1)[0]
+    sc = G.free_body(A0=R0, dims=(0.3, 0.2, 0.1), E=1e9)
+    sc.gravity = np.zeros(3)
+    tau = np.array([0.3, -0.2, 0.5])
+    sc.wrench = np.array([[*tau, 0, 0, 0]])
+    q1, qd1 = O.step(sc, sc.q0, sc.qd0, sc.h)
+    w = O.angular_velocity(q1, qd1)[0]
+    m = sc.mbar[0]
+    Ib = np.diag([m[4] + m[7], m[0] + m[7], m[0] + m[4]])   # ∫ρ(y²+z²), … from M̄ = diag(∫ρx², ∫ρy², ∫ρz², m)
+    ref = np.linalg.solve(R0 @ Ib @ R0.T, tau) * sc.h
+    assert np.max(np.abs(w - ref)) <= 1e-4 * np.max(np.abs(ref))
+    # the twist helpers invert each other on rigid motions
+    om, v = np.array([0.4, -0.1, 0.2]), np.array([1.0, 2.0, 3.0])
+    qd = O.twist_velocity(sc.q0, om, v)
+    assert np.allclose(O.angular_velocity(sc.q0, qd)[0], om, atol=1e-15) and np.allclose(qd[0, 9:], v)
+
+
+def test_wrench_momentum_balance():
+    """Linear momentum changes by h Σ(f + m g) per step exactly, with joints (the t-rows of ∇C cancel)."""
+    sc = G.random_chain(8, seed=11, anchored=False, vel=0.3, gravity=True, npts=1)
+    rng = np.random.default_rng(3)
+    sc.wrench = rng.normal(size=(sc.n, 6))
+    m = sc.mbar[:, 9]
+    q, qd = sc.q0, sc.qd0
+    p = (m[:, None] * qd[:, 9:]).sum(0)
+    for _ in range(3):
+        q, qd = O.step(sc, q, qd, sc.h)
+        p1 = (m[:, None] * qd[:, 9:]).sum(0)
+        ref = p + sc.h * (sc.wrench[:, 3:].sum(0) + m.sum() * sc.gravity)
+        assert np.max(np.abs(p1 - ref)) <= 1e-12 * max(np.max(np.abs(ref)), 1.0)
+        p = p1
