@@ -128,6 +128,12 @@ mabd_status mabd_get_state(mabd_handle h_, double *q_out, double *qd_out, int ou
 /* Overwrite the state (checkpoint restore; stage tests). Same layout as mabd_get_state. */
 mabd_status mabd_set_state(mabd_handle h_, const double *q, const double *qd, int in_on_device);
 
+/* Constant external wrenches: W is [n][6] = (τ, f) per body in the caller's
+ * order, world frame, applied in every step (and Newton iteration) as f_A,ext = G(A)ᵀW at the linearisation
+ * point: ½ τ × q_c on the column c of A, f on t. Host or device pointer (in_on_device); the values are copied.
+ * W = NULL removes the wrenches. Uses the handle's stream; a host W synchronises it. */
+mabd_status mabd_set_wrench(mabd_handle h_, const double *W, int in_on_device);
+
 /* Introspection: selected solver, number of device kernel launches per step, bodies, dual rows. */
 mabd_status mabd_query(mabd_handle h_, int32_t *solver, int32_t *launches_per_step, int64_t *n_bodies,
                        int64_t *n_dual_rows);

@@ -20,7 +20,7 @@ STATUS = {0: "MABD_OK", 1: "MABD_EINVAL", 2: "MABD_ESTATE", 3: "MABD_ENOMEM", 4:
 SOLVERS = {0: "auto", 1: "chain", 2: "tree", 3: "sparse"}
 
 EXPORTED = ["mabd_workspace_size", "mabd_create", "mabd_prefactor", "mabd_step", "mabd_get_state",
-            "mabd_set_state", "mabd_query", "mabd_solver_stats", "mabd_nccl_unique_id", "mabd_partition_info",
+            "mabd_set_state", "mabd_set_wrench", "mabd_query", "mabd_solver_stats", "mabd_nccl_unique_id", "mabd_partition_info",
             "mabd_destroy", "mabd_last_error"]
 
 
@@ -72,6 +72,7 @@ def load_library(path: str = LIB_PATH) -> ctypes.CDLL:
     lib.mabd_step.argtypes = [H, ctypes.c_double, ctypes.c_int64]
     lib.mabd_get_state.argtypes = [H, ctypes.c_void_p, ctypes.c_void_p, ctypes.c_int]
     lib.mabd_set_state.argtypes = [H, ctypes.c_void_p, ctypes.c_void_p, ctypes.c_int]
+    lib.mabd_set_wrench.argtypes = [H, ctypes.c_void_p, ctypes.c_int]
     lib.mabd_query.argtypes = [H, ctypes.POINTER(ctypes.c_int32), ctypes.POINTER(ctypes.c_int32),
                                ctypes.POINTER(ctypes.c_int64), ctypes.POINTER(ctypes.c_int64)]
     lib.mabd_solver_stats.argtypes = [H, ctypes.POINTER(ctypes.c_int64)]
@@ -242,6 +243,18 @@ class Simulator:
             q = None if q is None else (q if isinstance(q, torch.Tensor) else np.ascontiguousarray(q, dtype=np.float64))
             qd = None if qd is None else (qd if isinstance(qd, torch.Tensor) else np.ascontiguousarray(qd, dtype=np.float64))
         self._check(self._lib.mabd_set_state(self._h, self._addr(q), self._addr(qd), 1 if on_dev else 0), self._h)
+
+    def set_wrench(self, W=None) -> None:
+        """Constant external wrenches [n][6] = (τ, f) per body, world frame (None removes them)."""
+        import torch
+
+        if W is None:
+            self._check(self._lib.mabd_set_wrench(self._h, None, 0), self._h)
+            return
+        on_dev = isinstance(W, torch.Tensor) and W.is_cuda
+        if not on_dev and not isinstance(W, torch.Tensor):
+            W = np.ascontiguousarray(W, dtype=np.float64).reshape(self.n, 6)
+        self._check(self._lib.mabd_set_wrench(self._h, self._addr(W), 1 if on_dev else 0), self._h)
 
     @staticmethod
     def _addr(a):

@@ -616,9 +616,11 @@ __global__ void __launch_bounds__(CT, MABD_CHAIN_CTAS) chain_kernel(ChainArgs a)
         const Material M = a.b.mats[mdb];
         const double ms = msb;
         const int md = mdb;
+        double W[6];
         const bool ok = predict_body_lazy(
             q, [&](double* o) { tm_ld12(tbase + 48 * b + 24, o); }, M, ms,
-            [&](HinvBlk& o) { get_hinv(a, M, md, ms, o); }, H, k.ih, k.grav, R, dqt);
+            [&](HinvBlk& o) { get_hinv(a, M, md, ms, o); }, H, k.ih, k.grav, R, dqt,
+            load_wrench(a.b, base + t, W));
         if (!ok && has_body) report(k, ERR_NONFINITE);
       }
       if (update) {
@@ -1113,6 +1115,18 @@ cudaError_t launch_gather(const double* q, const double* qd, int64_t ld, const i
   if (n <= 0) return cudaSuccess;
   const int64_t tot = n * 12;
   gather_state_kernel<<<(unsigned)((tot + 255) / 256), 256, 0, st>>>(q, qd, ld, perm, n, qo, qdo);
+  return cudaGetLastError();
+}
+__global__ void scatter_rows_kernel(double* dst, int64_t ld, const int64_t* perm, int64_t n, const double* src, int nc) {
+  const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (i >= n * nc) return;
+  const int64_t b = i / nc, c = i % nc;
+  dst[c * ld + perm[b]] = src[i];
+}
+cudaError_t launch_scatter_rows(double* dst, int64_t ld, const int64_t* perm, int64_t n, const double* src, int nc,
+                                cudaStream_t st) {
+  if (n <= 0) return cudaSuccess;
+  scatter_rows_kernel<<<(unsigned)((n * nc + 255) / 256), 256, 0, st>>>(dst, ld, perm, n, src, nc);
   return cudaGetLastError();
 }
 cudaError_t launch_scatter(double* q, double* qd, int64_t ld, const int64_t* perm, int64_t n, const double* qi,

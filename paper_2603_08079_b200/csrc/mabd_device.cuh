@@ -293,10 +293,11 @@ __device__ __forceinline__ void rot_conj(const double* R, const double* P, doubl
 // f_A = (1/h) M_A q̇ + M_A[0₉;g] − [V vec(R Π(RᵀA)); 0₃]   (Alg. 1 exact R).
 // q̇ is fetched by qd_load(out12) and H̄⁻¹ by get_h(H) only when needed, so that neither is live during the polar
 // decomposition (register pressure). Returns false if the polar decomposition failed.
+// W (optional, world frame [τ; f]): external wrench, f_A,ext = G(A)ᵀW: ½ τ × q_c on column c, f on t.
 template <class QdLoad, class GetH>
 __device__ __forceinline__ bool predict_body_lazy(const double* q, QdLoad qd_load, const Material& M, double mscale,
                                                   GetH get_h, HinvBlk& H, double ih, const double* grav, double* R,
-                                                  double* dqt) {
+                                                  double* dqt, const double* W = nullptr) {
   double A[9];
 #pragma unroll
   for (int r = 0; r < 3; ++r)
@@ -318,15 +319,23 @@ __device__ __forceinline__ bool predict_body_lazy(const double* q, QdLoad qd_loa
   qd_load(qd);
 #pragma unroll
   for (int c = 0; c < 3; ++c) {
-    double v[3];
-    mat3t_vec(R, qd + 3 * c, v);
+    double v[3], fc[3];
 #pragma unroll
-    for (int r = 0; r < 3; ++r) w[3 * c + r] = ma[c] * v[r] - M.V * Pi[3 * r + c];
+    for (int r = 0; r < 3; ++r) fc[r] = ma[c] * qd[3 * c + r];
+    if (W) {  // + ½ τ × q_c
+      const double* qc = q + 3 * c;
+      fc[0] += 0.5 * (W[1] * qc[2] - W[2] * qc[1]);
+      fc[1] += 0.5 * (W[2] * qc[0] - W[0] * qc[2]);
+      fc[2] += 0.5 * (W[0] * qc[1] - W[1] * qc[0]);
+    }
+    mat3t_vec(R, fc, v);
+#pragma unroll
+    for (int r = 0; r < 3; ++r) w[3 * c + r] = v[r] - M.V * Pi[3 * r + c];
   }
   {
     double ft[3], v[3];
 #pragma unroll
-    for (int r = 0; r < 3; ++r) ft[r] = ma[3] * (qd[9 + r] * ih + grav[r]);
+    for (int r = 0; r < 3; ++r) ft[r] = ma[3] * (qd[9 + r] * ih + grav[r]) + (W ? W[3 + r] : 0.0);
     mat3t_vec(R, ft, v);
 #pragma unroll
     for (int r = 0; r < 3; ++r) w[9 + r] = v[r];
@@ -340,7 +349,7 @@ __device__ __forceinline__ bool predict_body_lazy(const double* q, QdLoad qd_loa
 
 __device__ __forceinline__ bool predict_body(const double* q, const double* qd, const Material& M, double mscale,
                                              const HinvBlk& H, double ih, const double* grav, double* R,
-                                             double* dqt) {
+                                             double* dqt, const double* W = nullptr) {
   HinvBlk Hc;
   return predict_body_lazy(
       q,
@@ -348,7 +357,15 @@ __device__ __forceinline__ bool predict_body(const double* q, const double* qd, 
 #pragma unroll
         for (int c = 0; c < 12; ++c) o[c] = qd[c];
       },
-      M, mscale, [&](HinvBlk& o) { o = H; }, Hc, ih, grav, R, dqt);
+      M, mscale, [&](HinvBlk& o) { o = H; }, Hc, ih, grav, R, dqt, W);
+}
+
+// the wrench of body (SoA position) j, or null
+__device__ __forceinline__ const double* load_wrench(const BodyArrays& b, int64_t j, double* W) {
+  if (!b.wr) return nullptr;
+#pragma unroll
+  for (int e = 0; e < 6; ++e) W[e] = b.wr[e * b.ld + j];
+  return W;
 }
 
 // x(q; ȳ) = A ȳ + t

@@ -221,6 +221,28 @@ mabd_status mabd_set_state(mabd_handle c, const double* q, const double* qd, int
   return MABD_OK;
 }
 
+mabd_status mabd_set_wrench(mabd_handle c, const double* W, int in_on_device) {
+  if (!c) return fail(nullptr, MABD_EINVAL, "NULL handle");
+  CUDA_TRY(c, cudaSetDevice(c->device));
+  const double* wr = nullptr;
+  if (W) {
+    const int64_t n = c->plan.n;
+    const double* src = W;
+    if (!in_on_device) {
+      CUDA_TRY(c, cudaMemcpyAsync(c->d.io, W, 6 * n * sizeof(double), cudaMemcpyHostToDevice, c->stream));
+      src = c->d.io;
+    }
+    CUDA_TRY(c, cudaMemsetAsync(c->d.wr_buf, 0, 6 * c->d.b.ld * sizeof(double), c->stream));
+    CUDA_TRY(c, launch_scatter_rows(c->d.wr_buf, c->d.b.ld, c->d.perm, n, src, 6, c->stream));
+    if (!in_on_device) CUDA_TRY(c, cudaStreamSynchronize(c->stream));
+    wr = c->d.wr_buf;
+  }
+  c->d.b.wr = wr;  // every solver reads the wrench through its copy of the body arrays
+  c->d.tree.b.wr = wr;
+  c->d.sparse.b.wr = wr;
+  return MABD_OK;
+}
+
 mabd_status mabd_query(mabd_handle c, int32_t* solver, int32_t* launches_per_step, int64_t* n_bodies,
                        int64_t* n_dual_rows) {
   if (!c) return fail(nullptr, MABD_EINVAL, "NULL handle");

@@ -52,6 +52,7 @@ struct BodyArrays {
   double* qd;              // [12][ld]
   double* rs;              // [9][ld] scratch: R between the phases of one launch (L2 only, discarded)
   double* z;               // [12][ld] K > 1 Newton iterations: q̇ⁿ + h[0;g] of this step
+  const double* wr;        // [6][ld] external wrench (τ, f) per body, or null (mabd_set_wrench)
   int64_t ld;
   const int32_t* mat_id;   // [ld] or null (all material 0)
   const double* mscale;    // [ld] or null (all 1)

@@ -133,6 +133,8 @@ cudaError_t launch_btd(const BtdArgs& a, int nblocks, cudaStream_t st);
 cudaError_t launch_hinv_table(const Material* mats, int nm, double ih2, HinvBlk* out, cudaStream_t st);
 cudaError_t launch_gather(const double* q, const double* qd, int64_t ld, const int64_t* perm, int64_t n, double* qo,
                           double* qdo, cudaStream_t st);
+cudaError_t launch_scatter_rows(double* dst, int64_t ld, const int64_t* perm, int64_t n, const double* src, int nc,
+                                cudaStream_t st);
 cudaError_t launch_scatter(double* q, double* qd, int64_t ld, const int64_t* perm, int64_t n, const double* qi,
                            const double* qdi, cudaStream_t st);
 

@@ -456,6 +456,7 @@ mabd_status build_plan(const mabd_bodies* B, const mabd_joints* J, const mabd_op
   f.qd = take(sizeof(double) * 12 * ld);
   f.rs = take(sizeof(double) * 9 * ld);
   f.z = p->newton_iters > 1 ? take(sizeof(double) * 12 * ld) : 0;
+  f.wr = take(sizeof(double) * 6 * ld);
   f.mat_id = multi_mat ? take(sizeof(int32_t) * ld) : 0;
   f.mscale = any_scale ? take(sizeof(double) * ld) : 0;
   f.mats = take(sizeof(Material) * p->mats.size());
@@ -542,6 +543,8 @@ cudaError_t upload_plan(const Plan& p, char* ws, cudaStream_t st, DevPtrs* d) {
   d->b.qd = (double*)(ws + f.qd);
   d->b.rs = (double*)(ws + f.rs);
   d->b.z = p.newton_iters > 1 ? (double*)(ws + f.z) : nullptr;
+  d->wr_buf = (double*)(ws + f.wr);
+  d->b.wr = nullptr;
   d->b.ld = p.ld;
   d->b.mat_id = p.mat_id.empty() ? nullptr : (const int32_t*)(ws + f.mat_id);
   d->b.mscale = p.mscale.empty() ? nullptr : (const double*)(ws + f.mscale);

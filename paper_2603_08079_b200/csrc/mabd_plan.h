@@ -126,7 +126,7 @@ struct Plan {
   // device layout (byte offsets into the workspace)
   size_t workspace_bytes = 0;
   struct Off {
-    size_t q, qd, rs, z, mat_id, mscale, mats, hinv, perm, io, err;
+    size_t q, qd, rs, z, wr, mat_id, mscale, mats, hinv, perm, io, err;
     size_t slot_info, geo, seg_flags, seg_red, long_list, left_iface;
     std::vector<size_t> tops, lams;  // per BTD level: tops[0] = chain tops (n_long), lams[i] = level i+1 λ
     size_t all_tops, lam_g, plo, lwin, llong;
@@ -138,6 +138,7 @@ struct Plan {
 
 struct DevPtrs {
   BodyArrays b{};
+  double* wr_buf = nullptr;        // [6][ld] wrench storage (b.wr points here once a wrench is set)
   HinvBlk* hinv = nullptr;
   Material* mats = nullptr;
   int64_t* perm = nullptr;

@@ -61,7 +61,9 @@ __global__ void sparse_predict_kernel(SparseArgs a) {
       H = a.hinv_tab[mid];
     else
       hinv_blocks(M, msc, a.k.ih2, H);
-    if (!predict_body(q, qd, M, msc, H, a.k.ih, a.k.grav, R, dqt)) sreport(a.k, ERR_NONFINITE);
+    double W[6];
+    if (!predict_body(q, qd, M, msc, H, a.k.ih, a.k.grav, R, dqt, load_wrench(a.b, j, W)))
+      sreport(a.k, ERR_NONFINITE);
 #pragma unroll
     for (int c = 0; c < 9; ++c) a.b.rs[c * ld + j] = R[c];
 #pragma unroll

@@ -62,7 +62,8 @@ __global__ void tree_predict_kernel(TreeArgs a, int64_t b0, int64_t b1) {
       H = a.hinv_tab[mid];
     else
       hinv_blocks(M, msc, k.ih2, H);
-    if (!predict_body(q, qd, M, msc, H, k.ih, k.grav, R, dqt)) treport(k, ERR_NONFINITE);
+    double W[6];
+    if (!predict_body(q, qd, M, msc, H, k.ih, k.grav, R, dqt, load_wrench(a.b, b, W))) treport(k, ERR_NONFINITE);
     double* sc = a.bscr + 21 * b;
 #pragma unroll
     for (int c = 0; c < 9; ++c) sc[c] = R[c];
