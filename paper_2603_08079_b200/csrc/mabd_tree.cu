@@ -226,12 +226,11 @@ __device__ void tree_up_warp(const TreeArgs& a, int b, int lane, double* F, int 
     }
     __syncwarp();
     // trailing: F[r][cc] −= Σ_e L[r][c+e] L[cc][c+e] (c+3 ≤ cc ≤ r < M); rhs[r] −= Σ_e L[r][c+e] y[c+e]
-    const int T = M - c - 3;
-    for (int t = lane; t < T * T; t += 32) {
-      const int r = c + 3 + t / T, cc = c + 3 + t % T;
-      if (cc > r) continue;
-      F[r * MS + cc] -= F[r * MS + c] * F[cc * MS + c] + F[r * MS + c + 1] * F[cc * MS + c + 1] +
-                        F[r * MS + c + 2] * F[cc * MS + c + 2];
+    // lanes as a fixed 4 × 8 tile over (row, column): no runtime index division
+    for (int r = c + 3 + (lane >> 3); r < M; r += 4) {
+      const double l0 = F[r * MS + c], l1 = F[r * MS + c + 1], l2 = F[r * MS + c + 2];
+      for (int cc = c + 3 + (lane & 7); cc <= r; cc += 8)
+        F[r * MS + cc] -= l0 * F[cc * MS + c] + l1 * F[cc * MS + c + 1] + l2 * F[cc * MS + c + 2];
     }
     for (int r = c + 3 + lane; r < M; r += 32)
       F[r * MS + M] -= F[r * MS + c] * F[c * MS + M] + F[r * MS + c + 1] * F[(c + 1) * MS + M] +
@@ -242,6 +241,9 @@ __device__ void tree_up_warp(const TreeArgs& a, int b, int lane, double* F, int 
   // 1..nu = the rows N..M−1 of F_uX L⁻ᵀ (F[N+col−1][0:N]); Z overwrites V: y = F_XX⁻¹ r_X, W = F_XX⁻¹ F_Xu
   auto vref = [&](int r, int col) -> double& { return col == 0 ? F[r * MS + M] : F[(N + col - 1) * MS + r]; };
   const int ncol = nu + 1;
+  // lane → (row offset, column) of the (rows × ncol) updates, computed once (ncol ≤ 7, rstep = ⌊32/ncol⌋ rows)
+  const int rstep = 32 / ncol, lcol = lane % ncol, lrow = lane / ncol;
+  const bool lact = lrow < rstep;
   for (int kb = NB - 1; kb >= 0; --kb) {
     const int c = 3 * kb;
     const double* li = Li + 9 * kb;
@@ -253,21 +255,20 @@ __device__ void tree_up_warp(const TreeArgs& a, int b, int lane, double* F, int 
     __syncwarp();
     if (lane < 3 * ncol) vref(c + e, col) = z;
     __syncwarp();
-    for (int t = lane; t < c * ncol; t += 32) {  // earlier rows: v_j −= L[c:c+3, j]ᵀ z_k
-      const int r = t / ncol, cl = t % ncol;
-      vref(r, cl) -= F[c * MS + r] * vref(c, cl) + F[(c + 1) * MS + r] * vref(c + 1, cl) +
-                     F[(c + 2) * MS + r] * vref(c + 2, cl);
-    }
+    if (lact)
+      for (int r = lrow; r < c; r += rstep)  // earlier rows: v_j −= L[c:c+3, j]ᵀ z_k
+        vref(r, lcol) -= F[c * MS + r] * vref(c, lcol) + F[(c + 1) * MS + r] * vref(c + 1, lcol) +
+                         F[(c + 2) * MS + r] * vref(c + 2, lcol);
     __syncwarp();
   }
   double* ws = a.ws + a.ws_off[b];  // y [N], W [N][nu]
-  for (int t = lane; t < N * ncol; t += 32) {
-    const int r = t / ncol, col = t % ncol;
-    if (col == 0)
-      ws[r] = vref(r, 0);
-    else
-      ws[N + r * nu + col - 1] = vref(r, col);
-  }
+  if (lact)
+    for (int r = lrow; r < N; r += rstep) {
+      if (lcol == 0)
+        ws[r] = vref(r, 0);
+      else
+        ws[N + r * nu + lcol - 1] = vref(r, lcol);
+    }
   if (u >= 0) {  // condensed child side of the up joint (Ŝ_u symmetric: lower part mirrored)
     for (int t = lane; t < nu * nu; t += 32) {
       const int r = t / nu, c = t % nu;
