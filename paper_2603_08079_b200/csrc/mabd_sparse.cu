@@ -233,10 +233,11 @@ __global__ void __launch_bounds__(SP_THREADS) mf_small_kernel(SparseArgs a, cons
     const int fc = m.fdim[c], nc = m.nown[c], mc = fc - nc;
     const double* Fc = m.F + m.foff[c];
     const int32_t* map = m.ea_map + m.ea_off[c];
-    for (int idx = threadIdx.x; idx < mc * mc; idx += blockDim.x) {
-      const int i = idx % mc, j = idx / mc;
-      if (i < j) continue;
-      sF[mapped(map, j) * f + mapped(map, i)] += Fc[(int64_t)(nc + j) * fc + nc + i];
+    const int tx = threadIdx.x % 16, ty = threadIdx.x / 16;  // 16 × 16 tile over (row i, column j): no division
+    for (int j = ty; j < mc; j += 16) {
+      const int pj = mapped(map, j);
+      const double* src = Fc + (int64_t)(nc + j) * fc + nc;
+      for (int i = j + tx; i < mc; i += 16) sF[pj * f + mapped(map, i)] += src[i];
     }
     __syncthreads();
   }
