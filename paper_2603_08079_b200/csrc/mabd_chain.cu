@@ -501,7 +501,8 @@ __device__ __forceinline__ void get_hinv(const ChainArgs& a, const Material& M, 
 #ifndef MABD_CHAIN_CTAS
 #define MABD_CHAIN_CTAS 4  // CTAs per SM (shared memory: 4 × 56.8 KB; TMEM: 4 × 128 columns)
 #endif
-template <bool FINISH>
+// WRENCH: external wrenches are set (a.b.wr != nullptr); the common no-wrench instance carries no wrench code
+template <bool FINISH, bool WRENCH>
 __global__ void __launch_bounds__(CT, MABD_CHAIN_CTAS) chain_kernel(ChainArgs a) {
   extern __shared__ __align__(16) double smem[];
   const CRS s = cr_smem(smem);
@@ -620,7 +621,7 @@ __global__ void __launch_bounds__(CT, MABD_CHAIN_CTAS) chain_kernel(ChainArgs a)
         const bool ok = predict_body_lazy(
             q, [&](double* o) { tm_ld12(tbase + 48 * b + 24, o); }, M, ms,
             [&](HinvBlk& o) { get_hinv(a, M, md, ms, o); }, H, k.ih, k.grav, R, dqt,
-            load_wrench(a.b, base + t, W));
+            WRENCH ? load_wrench(a.b, base + t, W) : nullptr);
         if (!ok && has_body) report(k, ERR_NONFINITE);
       }
       if (update) {
@@ -1049,10 +1050,11 @@ cudaError_t launch_chain(const ChainArgs& a0, int nitems, bool finish, cudaStrea
   a.n_items = nitems;
   const size_t sm = chain_smem_bytes();
   const int grid = std::min(nitems, MABD_CHAIN_CTAS * std::max(g_num_sms, 1));
+  const bool w = a.b.wr != nullptr;
   if (finish)
-    chain_kernel<true><<<grid, CT, sm, st>>>(a);
+    (w ? chain_kernel<true, true> : chain_kernel<true, false>)<<<grid, CT, sm, st>>>(a);
   else
-    chain_kernel<false><<<grid, CT, sm, st>>>(a);
+    (w ? chain_kernel<false, true> : chain_kernel<false, false>)<<<grid, CT, sm, st>>>(a);
   return cudaGetLastError();
 }
 
@@ -1069,12 +1071,14 @@ cudaError_t chain_kernels_init() {
   if ((e = cudaGetDevice(&dev))) return e;
   if ((e = cudaDeviceGetAttribute(&g_num_sms, cudaDevAttrMultiProcessorCount, dev))) return e;
   const int smc = (int)chain_smem_bytes();
-  if ((e = cudaFuncSetAttribute(chain_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, smc))) return e;
-  if ((e = cudaFuncSetAttribute(chain_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, smc))) return e;
+  void (*const kernels[4])(ChainArgs) = {chain_kernel<true, false>, chain_kernel<false, false>,
+                                         chain_kernel<true, true>, chain_kernel<false, true>};
+  for (auto kf : kernels) {
+    if ((e = cudaFuncSetAttribute(kf, cudaFuncAttributeMaxDynamicSharedMemorySize, smc))) return e;
+    // favour shared memory in the unified L1/shared carve-out so that 4 segment CTAs fit per SM
+    cudaFuncSetAttribute(kf, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
+  }
   if ((e = cudaFuncSetAttribute(btd_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, sm))) return e;
-  // favour shared memory in the unified L1/shared carve-out so that 4 segment CTAs fit per SM
-  cudaFuncSetAttribute(chain_kernel<true>, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
-  cudaFuncSetAttribute(chain_kernel<false>, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
   return cudaSuccess;
 }
 
