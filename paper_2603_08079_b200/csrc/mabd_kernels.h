@@ -64,13 +64,17 @@ struct TreeArgs {
   const int32_t* group_off;
   const int32_t* glev_ptr;
   const int32_t* glev_off;
+  const int32_t* glev_nl;      // [levels] end of the bodies with child joints in each level (they come first)
   double* Shat;                // [K][36] child-side condensed dual block of each joint (6×6, row-major)
   double* rhat;                // [K][6]
   double* lam;                 // [K][6]
   double* bscr;                // [n][21]: R, δq̃ between the passes
   double* ws;                  // per-body y, W
+  double* f0;                  // per-body front records (G H_b⁻¹ Gᵀ packed lower, own right-hand side)
+  const int64_t* fo_off;       // [n] record offset in f0 (−1: none)
   int32_t group0;              // first group of this launch
   int32_t front_rows;          // largest frontal matrix (rows; shared-memory sizing)
+  int32_t cap;                 // group capacity (bodies; shared-memory slots of the group kernel)
   const int32_t* pt_off;       // [n+1] per body: its frontal points in pt_code
   const int32_t* pt_code;      // 4·joint + 2·point + (child side)
   const int32_t* body_nn;      // [n] N | nu << 8
@@ -124,7 +128,6 @@ struct SparseArgs {
   MfArgs mf;
   StepConsts k;
 };
-cudaError_t launch_tree(const TreeArgs& a, int ngroups, int mode, int threads, cudaStream_t st);
 
 size_t cr_smem_bytes();
 cudaError_t chain_kernels_init();

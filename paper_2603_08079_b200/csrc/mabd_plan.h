@@ -19,9 +19,12 @@ struct BtdLevel {
 };
 
 // Tree plan (exact leaf-to-root elimination, reading A12); see mabd_tree.cu.
-// Internal body order: bottom groups (CTA-local subtrees, ≤ TREE_CAP bodies each), then the top group;
-// inside a group bodies are sorted by depth, deepest first, with per-level ranges.
+// Internal body order: bottom groups (CTA-local subtrees, ≤ cap bodies each), then the top group; inside a group
+// bodies are sorted by depth, deepest first, with per-level ranges, bodies with child joints first in each level.
+// cap = TREE_CAP, or 2·TREE_CAP for trees large enough to give every SM a group at the larger size.
 constexpr int TREE_CAP = 256;
+constexpr int TREE_TOP_SMALL = 32;  // a top set larger than this gets a middle layer …
+constexpr int TREE_MID_CAP = 31;    // … of subtrees with at most this many bodies
 constexpr int TREE_MAXN = 24;  // max dual rows of the child joints of one body (frontal size ≤ 24 + 6)
 struct TreePlan {
   std::vector<int32_t> up_joint;     // [n] joint to the parent (−1 for a root)
@@ -34,9 +37,15 @@ struct TreePlan {
   std::vector<int32_t> group_off;    // [G+1] body ranges
   std::vector<int32_t> glev_ptr;     // [G+1] into glev_off
   std::vector<int32_t> glev_off;     // level boundaries (absolute body indices), deepest level first
-  int32_t n_bottom = 0;              // bottom groups; the top group (if any) is group n_bottom
+  std::vector<int32_t> glev_nl;      // [levels] end of the level's bodies with child joints
+  int32_t cap = TREE_CAP;            // group capacity (bodies)
+  bool top_fused = false;            // the top group fits one CTA (else one launch per top level)
+  int32_t n_bottom = 0;              // bottom groups (layer 0)
+  int32_t n_mid = 0;                 // middle-layer groups (after the bottom ones); the top group (if any) is last
   bool has_top = false;
   int64_t ws_total = 0;
+  std::vector<int64_t> fo_off;       // [n] front record offsets (bodies with child joints, and the top group)
+  int64_t fo_total = 0;
   int32_t max_m = 3;                 // largest frontal matrix (rows)
   std::vector<int32_t> pt_off, pt_code, body_nn;  // per body: frontal point codes, N | nu << 8
   // multi-GPU split: the bottom groups are divided into W contiguous blocks of gpr groups;
@@ -131,7 +140,7 @@ struct Plan {
     std::vector<size_t> tops, lams;  // per BTD level: tops[0] = chain tops (n_long), lams[i] = level i+1 λ
     size_t all_tops, lam_g, plo, lwin, llong;
     std::vector<size_t> p_tops1, p_lam2, p_scr;
-    size_t t_up, t_coff, t_cj, t_wsoff, t_jnpts, t_jchd, t_jy, t_goff, t_glp, t_glo, t_shat, t_rhat, t_lam, t_bscr,
+    size_t t_up, t_coff, t_cj, t_wsoff, t_jnpts, t_jchd, t_jy, t_goff, t_glp, t_glo, t_glnl, t_fo, t_f0, t_shat, t_rhat, t_lam, t_bscr,
         t_ws, t_ptoff, t_ptcode, t_nn, t_rootj, t_rslot, t_xbuf;
   } off{};
 };

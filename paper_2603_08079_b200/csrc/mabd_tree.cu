@@ -43,263 +43,339 @@ __device__ __forceinline__ void treport(const StepConsts& k, int32_t flag) {
   atomicMin(k.err + 1, k.step_index);
 }
 
-// Stages 1-2 for every body at once (no tree dependency): R and δq̃ → bscr.
-__global__ void tree_predict_kernel(TreeArgs a, int64_t b0, int64_t b1) {
-  const StepConsts& k = a.k;
-  const int64_t ld = a.b.ld;
-  for (int64_t b = b0 + blockIdx.x * (int64_t)blockDim.x + threadIdx.x; b < b1; b += (int64_t)gridDim.x * blockDim.x) {
-    double q[12], qd[12], R[9], dqt[12];
+// body_nn word: N (child-joint rows) | nu (up-joint rows) << 8 | ext << 16 (the parent lies outside the body's group)
+__device__ __forceinline__ int nn_N(int nn) { return nn & 255; }
+__device__ __forceinline__ int nn_nu(int nn) { return (nn >> 8) & 255; }
+__device__ __forceinline__ bool nn_ext(int nn) { return (nn >> 16) & 1; }
+
+// Per-body shared-memory slots of a CTA-local group [g0, g1): upward, the condensed child side of the body's up
+// joint (Ŝ_u lower triangle in tri6 order, then r̂_u); downward, λ_u. A body whose parent lies outside the group
+// (ext) also publishes Ŝ_u, r̂_u to global memory (Shat, rhat) and reads λ_u from global memory (lam).
+// s == nullptr: no slots (the per-level launches of a large top group: everything through global memory).
+constexpr int TSLOT = 28;
+__device__ __forceinline__ int tri6(int r, int c) { return r >= c ? r * (r + 1) / 2 + c : c * (c + 1) / 2 + r; }
+struct TSlots {
+  double* s;
+  int g0, g1;
+  __device__ __forceinline__ double* at(int b) const { return s + (size_t)(b - g0) * TSLOT; }
+  __device__ __forceinline__ double* local(uint32_t i) const { return s + (size_t)i * TSLOT; }
+};
+
+// Where the condensed block / λ of each child-joint point of a body lives (uint32, frontal point order):
+//   CS_LOCAL  the child body is in the same group: payload = (local index << 1) | point, its slot
+//   CS_GLOBAL the child body is in another group: payload = (joint << 1) | point, Shat / rhat / lam
+//   CS_ANCHOR no child body (world anchor): payload = (joint << 1) | point, λ in lam
+enum : uint32_t { CS_LOCAL = 0u, CS_GLOBAL = 1u << 30, CS_ANCHOR = 2u << 30, CS_KIND = 3u << 30 };
+constexpr int TNP = TREE_MAXN / 3;  // child-joint points per body (max)
+struct TMeta {
+  int32_t nn, u;
+  int64_t fo, ws;   // front record in f0 (−1: none), y / W in ws
+  uint32_t cs[TNP];
+};
+
+__device__ TMeta tree_meta(const TreeArgs& a, int b, int g0, int g1) {
+  TMeta m;
+  m.nn = a.body_nn[b];
+  m.u = a.up_joint[b];
+  m.fo = a.fo_off[b];
+  m.ws = a.ws_off[b];
+  const int32_t* pc = a.pt_code + a.pt_off[b];
+  const int N = nn_N(m.nn);
 #pragma unroll
-    for (int c = 0; c < 12; ++c) {
-      q[c] = a.b.q[c * ld + b];
-      qd[c] = a.b.qd[c * ld + b];
+  for (int i = 0; i < TNP; ++i) {
+    uint32_t v = 0;
+    if (3 * i < N) {
+      const int code = pc[i];
+      const uint32_t kp = (uint32_t)(code >> 1);  // (joint << 1) | point
+      const int c = a.jchd[code >> 2];
+      v = c < 0 ? (CS_ANCHOR | kp) : (c >= g0 && c < g1) ? ((uint32_t)(c - g0) << 1 | (kp & 1u)) : (CS_GLOBAL | kp);
     }
-    const int mid = a.b.mat_id ? a.b.mat_id[b] : 0;
-    const double msc = a.b.mscale ? a.b.mscale[b] : 1.0;
-    const Material M = a.b.mats[mid];
-    HinvBlk H;
-    if (a.hinv_tab)
-      H = a.hinv_tab[mid];
-    else
-      hinv_blocks(M, msc, k.ih2, H);
-    double W[6];
-    if (!predict_body(q, qd, M, msc, H, k.ih, k.grav, R, dqt, load_wrench(a.b, b, W))) treport(k, ERR_NONFINITE);
-    double* sc = a.bscr + 21 * b;
-#pragma unroll
-    for (int c = 0; c < 9; ++c) sc[c] = R[c];
-#pragma unroll
-    for (int c = 0; c < 12; ++c) sc[9 + c] = dqt[c];
+    m.cs[i] = v;
   }
+  return m;
 }
 
-// Point i of body b's frontal matrix: the points of its child joints (sign +, b is their parent side), then the
-// points of its up joint (sign −, b is its child side).
-__device__ __forceinline__ void tree_point(const TreeArgs& a, int c0, int N, int u, int i, const double*& y, int& ji,
-                                           int& pi, double& sg) {
-  int row = 3 * i, jj = c0;
-  if (row < N) {
-    while (true) {
-      const int n3 = 3 * a.jnpts[a.child_joint[jj]];
-      if (row < n3) break;
-      row -= n3;
-      ++jj;
-    }
-    ji = a.child_joint[jj];
-    pi = row / 3;
-    sg = 1.0;
-    y = a.jy + 12 * (int64_t)ji + 3 * pi;
-  } else {
-    ji = u;
-    pi = (row - N) / 3;
-    sg = -1.0;
-    y = a.jy + 12 * (int64_t)ji + 6 + 3 * pi;
-  }
-}
-
-// Upward elimination at body b by one warp. The frontal matrix F (M×M, lower part) with the right-hand side as
-// column M lives in shared memory (row stride MS). A partial Cholesky over the N child-joint columns leaves
-//   F[N:,N:] = Ŝ_u = F_uu − F_uX F_XX⁻¹ F_Xu,  F[N:,M] = r̂_u = r_u − F_uX F_XX⁻¹ r_X,
-//   F[:N,:N] = L (F_XX = LLᵀ),  F[N:,:N] = F_uX L⁻ᵀ,  F[:N,M] = L⁻¹ r_X,
-// then Lᵀ back substitutions give y = F_XX⁻¹ r_X and W = F_XX⁻¹ F_Xu for the downward pass.
-__device__ void tree_up_warp(const TreeArgs& a, int b, int lane, double* F, int MS) {
-  const StepConsts& k = a.k;
-  const int64_t ld = a.b.ld;
-  const int c0 = a.child_off[b], c1 = a.child_off[b + 1];
-  const int u = a.up_joint[b];
-  const int nn = a.body_nn[b], N = nn & 255, nu = nn >> 8;
-  const int M = N + nu, npt = M / 3;
-  const int32_t* pcode = a.pt_code + a.pt_off[b];
-  double R[9], qt[12];
-  {
-    const double* sc = a.bscr + 21 * (int64_t)b;
-#pragma unroll
-    for (int c = 0; c < 9; ++c) R[c] = sc[c];
-#pragma unroll
-    for (int c = 0; c < 12; ++c) qt[c] = a.b.q[c * ld + b] + sc[9 + c];  // q̃
-  }
-  HinvBlk H;
-  {
-    const int mid = a.b.mat_id ? a.b.mat_id[b] : 0;
-    if (a.hinv_tab)
-      H = a.hinv_tab[mid];
-    else
-      hinv_blocks(a.b.mats[mid], a.b.mscale ? a.b.mscale[b] : 1.0, k.ih2, H);
-  }
-  // right-hand side: this body's side of C(q̃) plus the condensed child side
-  for (int i = lane; i < npt; i += 32) {
-    const int code = pcode[i];
-    const int ji = code >> 2, pi = (code >> 1) & 1;
-    const double si = (code & 1) ? -1.0 : 1.0;
-    const double* yi = a.jy + 12 * (int64_t)ji + 6 * (code & 1) + 3 * pi;
+// Body b's front record (f0 + fo): the packed lower triangle of F = G H_b⁻¹ Gᵀ (M×M, (i, j) at i(i+1)/2 + j),
+// then its own side of the right-hand side (M): +x_b(ȳ) (child-joint points; − p_world for an anchor),
+// −x_b(ȳ) (up-joint points), at q̃. The children's condensed blocks are added at elimination.
+__device__ void tree_assemble(const TreeArgs& a, int b, const TMeta& m, const double* R, const double* qt,
+                              const HinvBlk& H) {
+  const int M = nn_N(m.nn) + nn_nu(m.nn), npt = M / 3, T = M * (M + 1) / 2;
+  const int32_t* pc = a.pt_code + a.pt_off[b];
+  double* f = a.f0 + m.fo;
+  for (int i = 0; i < npt; ++i) {
+    const int ci = pc[i];
+    const int ji = ci >> 2, si = ci & 1;
+    const double* yi = a.jy + 12 * (int64_t)ji + 6 * si + 3 * ((ci >> 1) & 1);
     double x[3];
     point_pos(qt, yi, x);
+    const bool anchor = !si && a.jchd[ji] < 0;
 #pragma unroll
-    for (int e = 0; e < 3; ++e) {
-      double v;
-      if (si < 0)
-        v = -x[e];
-      else if (a.jchd[ji] < 0)  // anchor: C = x_b(ȳ) − p_world
-        v = x[e] - a.jy[12 * (int64_t)ji + 6 + 3 * pi + e];
-      else
-        v = x[e] + a.rhat[6 * (int64_t)ji + 3 * pi + e];
-      F[(3 * i + e) * MS + M] = v;
+    for (int e = 0; e < 3; ++e) f[T + 3 * i + e] = si ? -x[e] : (anchor ? x[e] - yi[6 + e] : x[e]);
+    for (int j = 0; j <= i; ++j) {
+      const int cj = pc[j];
+      const double* yj = a.jy + 12 * (int64_t)(cj >> 2) + 6 * (cj & 1) + 3 * ((cj >> 1) & 1);
+      double P[9], Bk[9];
+      pblock(H, yi, yj, P);
+      rot_conj(R, P, Bk);
+      const double sg = ((ci ^ cj) & 1) ? -1.0 : 1.0;
+#pragma unroll
+      for (int r = 0; r < 3; ++r)
+#pragma unroll
+        for (int c = 0; c < 3; ++c)
+          if (i > j || r >= c) f[(3 * i + r) * (3 * i + r + 1) / 2 + 3 * j + c] = sg * Bk[3 * r + c];
     }
   }
-  // blocks (i, j), j ≤ i: s_i s_j R P(ȳ_i, ȳ_j) Rᵀ (+ Ŝ_k on a child joint's own block)
-  const int npair = npt * (npt + 1) / 2;
-  for (int t = lane; t < npair; t += 32) {
-    int i, j;
-    tri_rc(t, i, j);
-    const int ci = pcode[i], cj = pcode[j];
-    const int ji = ci >> 2, pi = (ci >> 1) & 1, jj = cj >> 2, pj = (cj >> 1) & 1;
-    const double si = (ci & 1) ? -1.0 : 1.0, sj = (cj & 1) ? -1.0 : 1.0;
-    const double* yi = a.jy + 12 * (int64_t)ji + 6 * (ci & 1) + 3 * pi;
-    const double* yj = a.jy + 12 * (int64_t)jj + 6 * (cj & 1) + 3 * pj;
-    double P[9], Bk[9];
-    pblock(H, yi, yj, P);
-    rot_conj(R, P, Bk);
-    const double sg = si * sj;
-    const bool add_s = si > 0 && sj > 0 && ji == jj && a.jchd[ji] >= 0;
+}
+
+// Stages 1-2 of body b (no tree dependency): R and δq̃ → bscr, then the body's front record. With slots, a leaf (no
+// child joints) instead condenses its up joint right away: N = 0 leaves nothing to eliminate, so
+// Ŝ_u = F_uu = Σ (−1)² R P(ȳ_i, ȳ_j) Rᵀ over the up joint's child-side points and r̂_u = r_u = −x_b(ȳ_i) at q̃.
+__device__ void tree_predict_body(const TreeArgs& a, int b, const TSlots& sl, const TMeta& m) {
+  const StepConsts& k = a.k;
+  const int64_t ld = a.b.ld;
+  double q[12], qd[12], R[9], dqt[12];
 #pragma unroll
-    for (int r = 0; r < 3; ++r)
+  for (int c = 0; c < 12; ++c) {
+    q[c] = a.b.q[c * ld + b];
+    qd[c] = a.b.qd[c * ld + b];
+  }
+  const int mid = a.b.mat_id ? a.b.mat_id[b] : 0;
+  const double msc = a.b.mscale ? a.b.mscale[b] : 1.0;
+  const Material M = a.b.mats[mid];
+  HinvBlk H;
+  if (a.hinv_tab)
+    H = a.hinv_tab[mid];
+  else
+    hinv_blocks(M, msc, k.ih2, H);
+  double W[6];
+  if (!predict_body(q, qd, M, msc, H, k.ih, k.grav, R, dqt, load_wrench(a.b, b, W))) treport(k, ERR_NONFINITE);
+  double* sc = a.bscr + 21 * (int64_t)b;
 #pragma unroll
-      for (int c = 0; c < 3; ++c) {
-        double v = sg * Bk[3 * r + c];
-        if (add_s) v += a.Shat[36 * (int64_t)ji + 6 * (3 * pi + r) + 3 * pj + c];
-        if (3 * i + r >= 3 * j + c) F[(3 * i + r) * MS + 3 * j + c] = v;
+  for (int c = 0; c < 9; ++c) sc[c] = R[c];
+#pragma unroll
+  for (int c = 0; c < 12; ++c) sc[9 + c] = dqt[c];
+  double qt[12];
+#pragma unroll
+  for (int c = 0; c < 12; ++c) qt[c] = q[c] + dqt[c];
+  const int nu = nn_nu(m.nn);
+  if (sl.s == nullptr || nn_N(m.nn) != 0) {
+    if (m.fo >= 0) tree_assemble(a, b, m, R, qt, H);
+    return;
+  }
+  if (nu == 0) return;
+  const double* yc = a.jy + 12 * (int64_t)m.u + 6;
+  double* o = sl.at(b);
+  for (int pi = 0; pi < nu / 3; ++pi) {
+    for (int pj = 0; pj <= pi; ++pj) {
+      double P[9], Bk[9];
+      pblock(H, yc + 3 * pi, yc + 3 * pj, P);
+      rot_conj(R, P, Bk);
+#pragma unroll
+      for (int r = 0; r < 3; ++r)
+#pragma unroll
+        for (int c = 0; c < 3; ++c)
+          if (3 * pi + r >= 3 * pj + c) o[tri6(3 * pi + r, 3 * pj + c)] = Bk[3 * r + c];
+    }
+    double x[3];
+    point_pos(qt, yc + 3 * pi, x);
+#pragma unroll
+    for (int e = 0; e < 3; ++e) o[21 + 3 * pi + e] = -x[e];
+  }
+  if (nn_ext(m.nn)) {
+    for (int r = 0; r < nu; ++r) {
+      for (int c = 0; c < nu; ++c) a.Shat[36 * (int64_t)m.u + 6 * r + c] = o[tri6(r, c)];
+      a.rhat[6 * (int64_t)m.u + r] = o[21 + r];
+    }
+  }
+}
+
+#ifdef MABD_EXP_TCLOCK  // developer probe: global-timer marks of every CTA's phases (read by mabd_dbg_tclk)
+constexpr int TCLK_SLOTS = 64, TCLK_CTAS = 512;
+__device__ unsigned long long g_tclk[3 * TCLK_CTAS * TCLK_SLOTS];
+#define TMARK(slot)                                                                                        \
+  do {                                                                                                     \
+    if (threadIdx.x == 0 && blockIdx.x < TCLK_CTAS && (slot) < TCLK_SLOTS) {                               \
+      unsigned long long t_;                                                                               \
+      asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_));                                               \
+      g_tclk[(MODE * TCLK_CTAS + blockIdx.x) * TCLK_SLOTS + (slot)] = t_;                                  \
+    }                                                                                                      \
+  } while (0)
+#else
+#define TMARK(slot)
+#endif
+#ifdef MABD_EXP_TCLOCK
+__device__ __forceinline__ void tmark_at(int slot) {  // CTA 0, mode slot range 40..59 of mode 0's CTA 0 row
+  unsigned long long t_;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_));
+  g_tclk[slot] = t_;
+}
+#define EMARK(cond, slot) \
+  if (cond) tmark_at(slot)
+#else
+#define EMARK(cond, slot)
+#endif
+
+// Upward elimination at body b by one warp, in registers: lane j holds column j of the augmented front [F | r]
+// (lane M: r), read from the front record, plus the children's condensed blocks (Ŝ_c on their diagonal blocks,
+// r̂_c on their right-hand-side rows). Gauss-Jordan over the N child-joint columns, pivot column broadcast by
+// shuffles; F is symmetric positive definite on X, so no pivoting is needed. Afterwards the columns hold
+//   rows < N:  F_XX⁻¹ F_Xu = W (lanes N..M−1),  F_XX⁻¹ r_X = y (lane M)
+//   rows ≥ N:  Ŝ_u = F_uu − F_uX F_XX⁻¹ F_Xu (lanes N..M−1),  r̂_u = r_u − F_uX F_XX⁻¹ r_X (lane M).
+// MX: the front size rounded up to a multiple of 6, so that every loop is fully unrolled (register indices).
+template <int MX>
+__device__ __forceinline__ void tree_elim(const TreeArgs& a, int b, int lane, const TMeta* mp, const TSlots& sl) {
+  const StepConsts& k = a.k;
+  const int nn = mp->nn, N = nn_N(nn), nu = nn_nu(nn), M = N + nu, u = mp->u;
+  const double* f = a.f0 + mp->fo;
+  const int T = M * (M + 1) / 2, tl = lane * (lane + 1) / 2;
+#ifdef MABD_EXP_TCLOCK
+  const bool probe = blockIdx.x == 0 && lane == 0 && b == sl.g1 - 1 && sl.s != nullptr;
+#endif
+  EMARK(probe, 40);
+  double v[MX];
+#pragma unroll
+  for (int i = 0; i < MX; ++i) {
+    double x = 0.0;
+    if (i < M && lane <= M) x = f[lane == M ? T + i : (i >= lane ? i * (i + 1) / 2 + lane : tl + i)];
+    v[i] = x;
+  }
+  EMARK(probe && v[0] != 1e300, 41);
+  if (lane < N || lane == M) {  // the children's condensed blocks
+    const uint32_t cj = lane < N ? mp->cs[lane / 3] : 0u;
+    const int rj = 3 * (int)(cj & 1u) + lane % 3;
+#pragma unroll
+    for (int i = 0; i < MX; ++i) {
+      if (i < N) {
+        const uint32_t ci = mp->cs[i / 3];
+        const uint32_t kind = ci & CS_KIND;
+        if (kind != CS_ANCHOR) {
+          const int ri = 3 * (int)(ci & 1u) + i % 3;
+          const uint32_t id = (ci & ~CS_KIND) >> 1;  // child local index or joint
+          if (lane == M)
+            v[i] += kind == CS_LOCAL ? sl.local(id)[21 + ri] : a.rhat[6 * (int64_t)id + ri];
+          else if (((ci ^ cj) & ~1u) == 0u)  // same child joint (same kind and id)
+            v[i] += kind == CS_LOCAL ? sl.local(id)[tri6(ri, rj)] : a.Shat[36 * (int64_t)id + 6 * ri + rj];
+        }
       }
-  }
-  __syncwarp();
-  // partial Cholesky of the augmented lower matrix over the N child-joint columns, by 3×3 point blocks:
-  // factor the diagonal block (lane 0, closed form, its inverse Li kept in shared memory), scale the block
-  // column and the right-hand side, rank-3 update of the trailing lower part
-  double* Li = F + (size_t)M * MS;  // [N/3][9] inverses of the diagonal blocks (after the front rows)
-  const int NB = N / 3;
-  for (int kb = 0; kb < NB; ++kb) {
-    const int c = 3 * kb;
-    if (lane == 0) {
-      const double d00 = F[c * MS + c], d10 = F[(c + 1) * MS + c], d20 = F[(c + 2) * MS + c];
-      const double d11 = F[(c + 1) * MS + c + 1], d21 = F[(c + 2) * MS + c + 1], d22 = F[(c + 2) * MS + c + 2];
-      // pivots by refined hardware reciprocal square roots (fast_rsqrt, ≤ 1 ulp): l = p·p^{-1/2}
-      double p0 = d00;
-      bool ok = p0 > 0.0;
-      const double i00 = fast_rsqrt(ok ? p0 : 1.0), l00 = (ok ? p0 : 1.0) * i00;
-      const double l10 = d10 * i00, l20 = d20 * i00;
-      const double p1 = d11 - l10 * l10;
-      ok = ok && p1 > 0.0;
-      const double i11 = fast_rsqrt(p1 > 0.0 ? p1 : 1.0), l11 = (p1 > 0.0 ? p1 : 1.0) * i11;
-      const double l21 = (d21 - l20 * l10) * i11;
-      const double p2 = d22 - l20 * l20 - l21 * l21;
-      ok = ok && p2 > 0.0;
-      const double i22 = fast_rsqrt(p2 > 0.0 ? p2 : 1.0), l22 = (p2 > 0.0 ? p2 : 1.0) * i22;
-      if (!ok) treport(k, ERR_SINGULAR);
-      F[c * MS + c] = l00;
-      F[(c + 1) * MS + c] = l10;
-      F[(c + 2) * MS + c] = l20;
-      F[(c + 1) * MS + c + 1] = l11;
-      F[(c + 2) * MS + c + 1] = l21;
-      F[(c + 2) * MS + c + 2] = l22;
-      // Li = L⁻¹ (lower): row-major 3×3
-      double* li = Li + 9 * kb;
-      li[0] = i00;
-      li[1] = 0.0;
-      li[2] = 0.0;
-      li[3] = -l10 * i00 * i11;
-      li[4] = i11;
-      li[5] = 0.0;
-      li[6] = (l10 * l21 - l20 * l11) * i00 * i11 * i22;
-      li[7] = -l21 * i11 * i22;
-      li[8] = i22;
-      // right-hand side of the block: y_k = Li r_k
-      const double r0 = F[c * MS + M], r1 = F[(c + 1) * MS + M], r2 = F[(c + 2) * MS + M];
-      F[c * MS + M] = li[0] * r0;
-      F[(c + 1) * MS + M] = li[3] * r0 + li[4] * r1;
-      F[(c + 2) * MS + M] = li[6] * r0 + li[7] * r1 + li[8] * r2;
-    }
-    __syncwarp();
-    const double* li = Li + 9 * kb;
-    for (int r = c + 3 + lane; r < M; r += 32) {  // block column below: F[r, c:c+3] ← F[r, c:c+3] Liᵀ
-      const double f0 = F[r * MS + c], f1 = F[r * MS + c + 1], f2 = F[r * MS + c + 2];
-      F[r * MS + c] = li[0] * f0;
-      F[r * MS + c + 1] = li[3] * f0 + li[4] * f1;
-      F[r * MS + c + 2] = li[6] * f0 + li[7] * f1 + li[8] * f2;
-    }
-    __syncwarp();
-    // trailing: F[r][cc] −= Σ_e L[r][c+e] L[cc][c+e] (c+3 ≤ cc ≤ r < M); rhs[r] −= Σ_e L[r][c+e] y[c+e]
-    // lanes as a fixed 4 × 8 tile over (row, column): no runtime index division
-    for (int r = c + 3 + (lane >> 3); r < M; r += 4) {
-      const double l0 = F[r * MS + c], l1 = F[r * MS + c + 1], l2 = F[r * MS + c + 2];
-      for (int cc = c + 3 + (lane & 7); cc <= r; cc += 8)
-        F[r * MS + cc] -= l0 * F[cc * MS + c] + l1 * F[cc * MS + c + 1] + l2 * F[cc * MS + c + 2];
-    }
-    for (int r = c + 3 + lane; r < M; r += 32)
-      F[r * MS + M] -= F[r * MS + c] * F[c * MS + M] + F[r * MS + c + 1] * F[(c + 1) * MS + M] +
-                       F[r * MS + c + 2] * F[(c + 2) * MS + M];
-    __syncwarp();
-  }
-  // back substitutions Lᵀ Z = V by 3×3 blocks (last block first): V column 0 = L⁻¹r_X (F column M), columns
-  // 1..nu = the rows N..M−1 of F_uX L⁻ᵀ (F[N+col−1][0:N]); Z overwrites V: y = F_XX⁻¹ r_X, W = F_XX⁻¹ F_Xu
-  auto vref = [&](int r, int col) -> double& { return col == 0 ? F[r * MS + M] : F[(N + col - 1) * MS + r]; };
-  const int ncol = nu + 1;
-  // lane → (row offset, column) of the (rows × ncol) updates, computed once (ncol ≤ 7, rstep = ⌊32/ncol⌋ rows)
-  const int rstep = 32 / ncol, lcol = lane % ncol, lrow = lane / ncol;
-  const bool lact = lrow < rstep;
-  for (int kb = NB - 1; kb >= 0; --kb) {
-    const int c = 3 * kb;
-    const double* li = Li + 9 * kb;
-    double z = 0.0;
-    const int e = lane / ncol, col = lane % ncol;
-    if (lane < 3 * ncol) {  // z_k = Liᵀ v_k (row e, column col)
-      z = li[e] * vref(c, col) + li[3 + e] * vref(c + 1, col) + li[6 + e] * vref(c + 2, col);
-    }
-    __syncwarp();
-    if (lane < 3 * ncol) vref(c + e, col) = z;
-    __syncwarp();
-    if (lact)
-      for (int r = lrow; r < c; r += rstep)  // earlier rows: v_j −= L[c:c+3, j]ᵀ z_k
-        vref(r, lcol) -= F[c * MS + r] * vref(c, lcol) + F[(c + 1) * MS + r] * vref(c + 1, lcol) +
-                         F[(c + 2) * MS + r] * vref(c + 2, lcol);
-    __syncwarp();
-  }
-  double* ws = a.ws + a.ws_off[b];  // y [N], W [N][nu]
-  if (lact)
-    for (int r = lrow; r < N; r += rstep) {
-      if (lcol == 0)
-        ws[r] = vref(r, 0);
-      else
-        ws[N + r * nu + lcol - 1] = vref(r, lcol);
-    }
-  if (u >= 0) {  // condensed child side of the up joint (Ŝ_u symmetric: lower part mirrored)
-    for (int t = lane; t < nu * nu; t += 32) {
-      const int r = t / nu, c = t % nu;
-      const int rr = r > c ? r : c, cc = r > c ? c : r;
-      a.Shat[36 * (int64_t)u + 6 * r + c] = F[(N + rr) * MS + N + cc];
-    }
-    if (lane < nu) a.rhat[6 * (int64_t)u + lane] = F[(N + lane) * MS + M];
-  } else {  // root: λ_X = y
-    __syncwarp();
-    int off = 0;
-    for (int j = c0; j < c1; ++j) {
-      const int kj = a.child_joint[j];
-      const int n3 = 3 * a.jnpts[kj];
-      for (int r = lane; r < n3; r += 32) a.lam[6 * (int64_t)kj + r] = F[(off + r) * MS + M];
-      off += n3;
     }
   }
+  EMARK(probe && v[0] != 1e300, 42);
+  // Pivot loop kept rolled (code size: every step runs the same instructions): the registers rotate by one row per
+  // step so that the pivot row is always v[0]; after N steps, v[i] holds original row (i + N) mod MX, i.e.
+  // rows N..M−1 (Ŝ_u / r̂_u) at v[0..nu) and rows 0..N−1 (W / y) at v[MX−N..MX).
+  bool ok = true;
+  for (int kk = 0; kk < N; ++kk) {
+    const double p = __shfl_sync(0xffffffffu, v[0], kk);
+    ok = ok && p > 0.0;
+    const double t = v[0] * fast_rcp(p > 0.0 ? p : 1.0);
+#pragma unroll
+    for (int i = 1; i < MX; ++i) {  // rows beyond M are zero in every column and stay zero
+      const double c = __shfl_sync(0xffffffffu, v[i], kk);
+      v[i - 1] = v[i] - c * t;
+    }
+    v[MX - 1] = t;
+  }
+  EMARK(probe && v[MX - 1] != 1e300, 43);
+  if (!ok && lane == 0) treport(k, ERR_SINGULAR);
+  const int cu = lane - N;  // this lane's column of u (0 ≤ cu < nu), or nu for the right-hand side
+  if (cu < 0 || cu > nu) return;
+  double* ws = a.ws + mp->ws;  // y [N], W [N][nu] (row-major)
+#pragma unroll
+  for (int i = 0; i < MX; ++i) {
+    const int r = i - (MX - N);  // row r < N of y / W
+    if (r >= 0) ws[cu == nu ? r : N + r * nu + cu] = v[i];
+  }
+  if (u >= 0) {  // condensed child side of the up joint → this body's slot, and global memory if ext
+    double* o = sl.s != nullptr ? sl.at(b) : nullptr;
+    const bool glob = sl.s == nullptr || nn_ext(nn);
+#pragma unroll
+    for (int r = 0; r < 6; ++r) {
+      if (r >= nu) break;
+      const double x = v[r];
+      if (o != nullptr && (cu == nu || r >= cu)) o[cu == nu ? 21 + r : tri6(r, cu)] = x;
+      if (glob) {
+        if (cu == nu)
+          a.rhat[6 * (int64_t)u + r] = x;
+        else
+          a.Shat[36 * (int64_t)u + 6 * r + cu] = x;  // column cu of the symmetric Ŝ_u
+      }
+    }
+  } else if (sl.s == nullptr && cu == nu) {  // root of the per-level schedule: λ_X = y
+#pragma unroll
+    for (int i = 0; i < MX; ++i) {
+      const int r = i - (MX - N);
+      if (r >= 0) {
+        const uint32_t kp = mp->cs[r / 3] & ~CS_KIND;
+        a.lam[6 * (int64_t)(kp >> 1) + 3 * (kp & 1u) + r % 3] = v[i];
+      }
+    }
+  }
+}
+
+__device__ __forceinline__ void tree_up_warp(const TreeArgs& a, int b, int lane, const TMeta* mp, const TSlots& sl) {
+  const int M = nn_N(mp->nn) + nn_nu(mp->nn);
+  switch ((M + 5) / 6) {  // the front size rounded up to a multiple of 6 rows
+    case 0:
+    case 1: tree_elim<6>(a, b, lane, mp, sl); break;
+    case 2: tree_elim<12>(a, b, lane, mp, sl); break;
+    case 3: tree_elim<18>(a, b, lane, mp, sl); break;
+    case 4: tree_elim<24>(a, b, lane, mp, sl); break;
+    default: tree_elim<30>(a, b, lane, mp, sl); break;
+  }
+  EMARK(blockIdx.x == 0 && lane == 0 && b == sl.g1 - 1 && sl.s != nullptr, 44);
   __syncwarp();
 }
 
-// Downward pass at body b: λ_X = y − W λ_u for its child-joint points, then the update (stage 4). Every input
-// except λ_u (written by the parent's level) is fetched up front from the per-body tables (body_nn, pt_code,
-// bscr, ws), so one thread waits on about three dependent memory round trips instead of walking the child
-// lists.
-__device__ void tree_down(const TreeArgs& a, int b) {
+// λ_u of body b (zero-padded to 6 rows): its slot (the parent is in the group) or global memory.
+__device__ __forceinline__ void tree_lambda_up(const TreeArgs& a, int b, const TMeta& m, const TSlots& sl,
+                                               double* lu) {
+  const int nu = nn_nu(m.nn);
+  const double* src = (sl.s == nullptr || nn_ext(m.nn)) ? a.lam + 6 * (int64_t)m.u : sl.at(b);
+#pragma unroll
+  for (int r = 0; r < 6; ++r) lu[r] = r < nu ? src[r] : 0.0;
+}
+
+// λ of child-joint point i of a body (source code c), 3 rows
+__device__ __forceinline__ double* tree_lam_at(const TreeArgs& a, const TSlots& sl, uint32_t c) {
+  const uint32_t id = (c & ~CS_KIND) >> 1, pp = c & 1u;
+  return (c & CS_KIND) == CS_LOCAL ? sl.local(id) + 3 * pp : a.lam + 6 * (int64_t)id + 3 * pp;
+}
+
+// Downward step at a body with child joints (one thread): λ_X = y − W λ_u → the child bodies' slots (or lam).
+// Every load is issued before the first store.
+__device__ void tree_lambda(const TreeArgs& a, int b, const TMeta& m, const TSlots& sl) {
+  const int N = nn_N(m.nn), nu = nn_nu(m.nn);
+  const double* ws = a.ws + m.ws;
+  double lu[6];
+  tree_lambda_up(a, b, m, sl, lu);
+  double lx[TREE_MAXN];
+#pragma unroll
+  for (int r = 0; r < TREE_MAXN; ++r) {
+    double v = 0.0;
+    if (r < N) {
+      v = ws[r];
+#pragma unroll
+      for (int c = 0; c < 6; ++c)
+        if (c < nu) v -= ws[N + r * nu + c] * lu[c];
+    }
+    lx[r] = v;
+  }
+#pragma unroll
+  for (int i = 0; i < TNP; ++i) {
+    if (3 * i >= N) break;
+    double* d = tree_lam_at(a, sl, m.cs[i]);
+#pragma unroll
+    for (int e = 0; e < 3; ++e) d[e] = lx[3 * i + e];
+  }
+}
+
+// Stage 4 at body b once every λ of its joints is known (one thread): qⁿ⁺¹ = q̃ − diag₄(R)H̄⁻¹ Σ ±Γᵀ Rᵀλ.
+__device__ void tree_update(const TreeArgs& a, int b, const TMeta& m, const TSlots& sl) {
   const StepConsts& k = a.k;
   const int64_t ld = a.b.ld;
-  const int nn = a.body_nn[b], N = nn & 255, nu = nn >> 8;
-  const int u = a.up_joint[b];
+  const int N = nn_N(m.nn), nu = nn_nu(m.nn);
   const int32_t* pcode = a.pt_code + a.pt_off[b];
-  const double* ws = a.ws + a.ws_off[b];
   const double* sc = a.bscr + 21 * (int64_t)b;
   double R[9];
 #pragma unroll
@@ -312,36 +388,27 @@ __device__ void tree_down(const TreeArgs& a, int b) {
     else
       hinv_blocks(a.b.mats[mid], a.b.mscale ? a.b.mscale[b] : 1.0, k.ih2, H);
   }
-  double lu[6];  // fixed-size, fully unrolled accesses only (no local memory)
-#pragma unroll
-  for (int r = 0; r < 6; ++r) lu[r] = r < nu ? a.lam[6 * (int64_t)u + r] : 0.0;
+  double lu[6];
+  tree_lambda_up(a, b, m, sl, lu);
   double gq[12];
 #pragma unroll
   for (int c = 0; c < 12; ++c) gq[c] = 0.0;
-#pragma unroll 2
-  for (int i = 0; i < N / 3; ++i) {  // child-joint points (this body is their parent side, sign +)
+#pragma unroll
+  for (int i = 0; i < TNP; ++i) {  // child-joint points (this body is their parent side, sign +)
+    if (3 * i >= N) break;
     const int code = pcode[i];
-    const int kj = code >> 2, pp = (code >> 1) & 1;
-    double lam[3], w[3];
-#pragma unroll
-    for (int r = 0; r < 3; ++r) {
-      double v = ws[3 * i + r];
-      const double* wr = ws + N + (3 * i + r) * nu;
-#pragma unroll
-      for (int c = 0; c < 6; ++c)
-        if (c < nu) v -= wr[c] * lu[c];
-      lam[r] = v;
-      a.lam[6 * (int64_t)kj + 3 * pp + r] = v;
-    }
-    mat3t_vec(R, lam, w);
-    add_point_force(gq, a.jy + 12 * (int64_t)kj + 3 * pp, w, 1.0);
+    const double* lam = tree_lam_at(a, sl, m.cs[i]);
+    const double l3[3] = {lam[0], lam[1], lam[2]};
+    double w[3];
+    mat3t_vec(R, l3, w);
+    add_point_force(gq, a.jy + 12 * (int64_t)(code >> 2) + 3 * ((code >> 1) & 1), w, 1.0);
   }
 #pragma unroll
   for (int pp = 0; pp < 2; ++pp) {  // up-joint points (this body is their child side, sign −)
     if (3 * pp >= nu) break;
     double w[3];
     mat3t_vec(R, lu + 3 * pp, w);
-    add_point_force(gq, a.jy + 12 * (int64_t)u + 6 + 3 * pp, w, -1.0);
+    add_point_force(gq, a.jy + 12 * (int64_t)m.u + 6 + 3 * pp, w, -1.0);
   }
   double uu[12];
   hinv_apply(H, gq, uu);
@@ -362,33 +429,81 @@ __device__ void tree_down(const TreeArgs& a, int b) {
   }
 }
 
-__global__ void __launch_bounds__(512) tree_kernel(TreeArgs a, int mode, int MS) {
+// One level of a large top group over the whole GPU (no slots: everything through global memory): upward a warp
+// per body, downward a thread per body (λ of its child joints, then stage 4).
+__global__ void __launch_bounds__(512) tree_level_kernel(TreeArgs a, int mode) {
+  __shared__ TMeta sm[16];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, nw = blockDim.x >> 5;
+  const int l = a.group0;
+  const TSlots none{nullptr, 0, 0};
+  if (mode == TREE_UP_LEVEL) {
+    const int b = a.glev_off[l] + blockIdx.x * nw + warp;
+    if (b >= a.glev_off[l + 1]) return;
+    if (lane == 0) sm[warp] = tree_meta(a, b, 0, 0);
+    __syncwarp();
+    tree_up_warp(a, b, lane, &sm[warp], none);
+  } else {
+    const int b = a.glev_off[l] + blockIdx.x * blockDim.x + threadIdx.x;
+    if (b >= a.glev_off[l + 1]) return;
+    const TMeta m = tree_meta(a, b, 0, 0);
+    tree_lambda(a, b, m, none);
+    tree_update(a, b, m, none);
+  }
+}
+
+
+
+// A CTA-local group (one CTA per group; the top group as a single CTA when it fits). Shared memory: the slots and
+// the per-body metadata of the group. Upward: stages 1-2 with the front records (or, for leaves, the condensed
+// blocks) of every body at once, then the levels with child joints, deepest first, a warp per body (those bodies
+// come first in each level: [glev_off[l], glev_nl[l])). Downward: λ level by level, shallowest first, a thread
+// per body, then stage 4 for every body at once.
+// UP launches of the bottom groups carry extra CTAs (blockIdx.x ≥ ngroups) that prepare the top section
+// [top0, n): stages 1-2 and front records, a thread per body, on the SMs the groups leave idle. The groups of the
+// top section (prepared != 0) then only load their metadata in the first phase.
+template <int MODE>
+__global__ void __launch_bounds__(512, 1) tree_group_kernel(TreeArgs a, int ngroups, int top0, int prepared) {
   extern __shared__ double tsm[];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, nw = blockDim.x >> 5;
-  double* F = tsm + (size_t)warp * (a.front_rows * MS + 9 * (TREE_MAXN / 3));
-  if (mode == TREE_UP_LEVEL || mode == TREE_DOWN_LEVEL) {  // one level of the top group over the whole grid
-    const int l = a.group0;
-    const int b = a.glev_off[l] + (mode == TREE_UP_LEVEL ? blockIdx.x * nw + warp : blockIdx.x * blockDim.x + threadIdx.x);
-    if (b >= a.glev_off[l + 1]) return;
-    if (mode == TREE_UP_LEVEL)
-      tree_up_warp(a, b, lane, F, MS);
-    else
-      tree_down(a, b);
+  if ((int)blockIdx.x >= ngroups) {
+    const int b = top0 + ((int)blockIdx.x - ngroups) * blockDim.x + threadIdx.x;
+    if (b < a.n) tree_predict_body(a, b, TSlots{nullptr, 0, 0}, tree_meta(a, b, 0, 0));
     return;
   }
   const int g = a.group0 + blockIdx.x;
-  const int l0 = a.glev_ptr[g], l1 = a.glev_ptr[g + 1] - 1;  // levels l ∈ [l0, l1): [glev_off[l], glev_off[l+1])
-  if (mode == TREE_UP || mode == TREE_BOTH) {
-    for (int l = l0; l < l1; ++l) {  // deepest first; one warp per body
-      for (int b = a.glev_off[l] + warp; b < a.glev_off[l + 1]; b += nw) tree_up_warp(a, b, lane, F, MS);
+  const int g0 = a.group_off[g], g1 = a.group_off[g + 1];
+  const int l0 = a.glev_ptr[g], l1 = a.glev_ptr[g + 1] - 1;  // levels l ∈ [l0, l1), deepest first
+  const TSlots sl{tsm, g0, g1};
+  TMeta* meta = reinterpret_cast<TMeta*>(tsm + (size_t)a.cap * TSLOT);
+  TMARK(0);
+  for (int b = g0 + threadIdx.x; b < g1; b += blockDim.x) {
+    const TMeta m = tree_meta(a, b, g0, g1);
+    meta[b - g0] = m;
+    if (MODE != TREE_DOWN && !prepared) tree_predict_body(a, b, sl, m);
+  }
+  __syncthreads();
+  TMARK(1);
+  if (MODE != TREE_DOWN) {
+    for (int l = l0; l < l1; ++l) {
+      const int e = a.glev_nl[l];
+      if (e == a.glev_off[l]) continue;  // leaves only (uniform across the CTA)
+      for (int b = a.glev_off[l] + warp; b < e; b += nw) tree_up_warp(a, b, lane, meta + (b - g0), sl);
       __syncthreads();
+      TMARK(2 + l - l0);
     }
   }
-  if (mode == TREE_DOWN || mode == TREE_BOTH) {
-    for (int l = l1 - 1; l >= l0; --l) {  // shallowest first; one thread per body
-      for (int b = a.glev_off[l] + threadIdx.x; b < a.glev_off[l + 1]; b += blockDim.x) tree_down(a, b);
+  if (MODE != TREE_UP) {
+    TMARK(32);
+    for (int l = l1 - 1; l >= l0; --l) {
+      const int e = a.glev_nl[l];
+      if (e == a.glev_off[l]) continue;
+      for (int b = a.glev_off[l] + threadIdx.x; b < e; b += blockDim.x) tree_lambda(a, b, meta[b - g0], sl);
       __syncthreads();
+      TMARK(33 + l1 - 1 - l);
     }
+    for (int b = g0 + threadIdx.x; b < g1; b += blockDim.x) tree_update(a, b, meta[b - g0], sl);
+    __syncthreads();
+    TMARK(63);
   }
 }
 
@@ -414,46 +529,38 @@ __global__ void tree_unpack_kernel(TreeArgs a, int nroot) {
     a.rhat[6 * (int64_t)u + e - 36] = v;
 }
 
-static int tree_ms(int max_m) { return max_m + 2 + ((max_m & 1) ? 0 : 1); }  // row stride (odd)
+constexpr size_t TREE_SMEM_MAX = 227 * 1024;  // dynamic shared memory per CTA (sm_100a opt-in maximum)
 
-cudaError_t launch_tree(const TreeArgs& a, int ngroups, int mode, int threads, cudaStream_t st) {
-  if (ngroups <= 0) return cudaSuccess;
-  const int MS = tree_ms(a.front_rows);
-  const size_t sm = sizeof(double) * (size_t)(threads / 32) * (a.front_rows * MS + 9 * (TREE_MAXN / 3));
-  tree_kernel<<<ngroups, threads, sm, st>>>(a, mode, MS);
+// Shared memory of the group kernel: slots and metadata for cap bodies.
+size_t tree_group_smem(int cap) { return (sizeof(double) * TSLOT + sizeof(TMeta)) * (size_t)cap; }
+
+template <int MODE>
+static cudaError_t launch_group(const TreeArgs& a, int g_lo, int g_hi, const TreePlan& t, cudaStream_t st,
+                                bool prepare_top = false) {
+  const int ng = std::max(0, g_hi - g_lo);
+  const int top0 = t.group_off[t.n_bottom];
+  const int nprep = prepare_top ? (int)((a.n - top0 + 511) / 512) : 0;
+  if (ng + nprep == 0) return cudaSuccess;
+  TreeArgs b = a;
+  b.group0 = g_lo;
+  const int prepared = g_lo >= t.n_bottom ? 1 : 0;
+  tree_group_kernel<MODE><<<ng + nprep, 512, tree_group_smem(t.cap), st>>>(b, ng, top0, prepared);
   return cudaGetLastError();
 }
 
-static unsigned grid_for_bodies(int64_t nb) {
-  return (unsigned)std::max<int64_t>(1, std::min<int64_t>((nb + 255) / 256, 148 * 8));
-}
 
 cudaError_t tree_step(const Plan& p, const DevPtrs& d, const StepConsts& k, cudaStream_t st) {
   TreeArgs a = d.tree;
   a.k = k;
   const TreePlan& t = p.tree;
   cudaError_t e;
-  // warps per CTA of the CTA-local subtrees: up to 8 within the shared memory
-  const size_t per_warp = sizeof(double) * ((size_t)t.max_m * tree_ms(t.max_m) + 9 * (TREE_MAXN / 3));
-  const int bot_threads = 32 * (int)std::max<size_t>(1, std::min<size_t>(8, (200 * 1024) / std::max<size_t>(per_warp, 1)));
   // bottom groups of this process: all of them, or this rank's block when the tree is split across ranks
   const bool split = t.parts > 1 && !t.emulate;
   const int g_lo = split ? std::min(t.n_bottom, t.part * t.gpr) : 0;
   const int g_hi = split ? std::min(t.n_bottom, (t.part + 1) * t.gpr) : t.n_bottom;
-  const int64_t top0 = t.group_off[t.n_bottom];
-  if (split) {  // stages 1-2 for this rank's bottom bodies and the (replicated) top bodies
-    const int64_t b0 = t.group_off[g_lo], b1 = t.group_off[g_hi];
-    if (b1 > b0) tree_predict_kernel<<<grid_for_bodies(b1 - b0), 256, 0, st>>>(a, b0, b1);
-    if (a.n > top0) tree_predict_kernel<<<grid_for_bodies(a.n - top0), 256, 0, st>>>(a, top0, a.n);
-  } else {
-    tree_predict_kernel<<<grid_for_bodies(a.n), 256, 0, st>>>(a, 0, a.n);
-  }
-  if (!t.has_top) {
-    a.group0 = g_lo;
-    return launch_tree(a, g_hi - g_lo, TREE_BOTH, bot_threads, st);
-  }
-  a.group0 = g_lo;
-  if ((e = launch_tree(a, g_hi - g_lo, TREE_UP, bot_threads, st))) return e;
+  const bool top_section = t.n_mid > 0 || t.has_top;
+  if (!top_section) return launch_group<TREE_BOTH>(a, g_lo, g_hi, t, st);
+  if ((e = launch_group<TREE_UP>(a, g_lo, g_hi, t, st, true))) return e;
   if (t.parts > 1) {  // exchange of the group roots' condensed blocks (one all-gather; emulated: every part local)
     const int q0 = split ? t.part : 0, q1 = split ? t.part + 1 : t.parts;
     for (int q = q0; q < q1; ++q) {
@@ -468,25 +575,31 @@ cudaError_t tree_step(const Plan& p, const DevPtrs& d, const StepConsts& k, cuda
     const int nroot = t.root_off[t.n_bottom];
     if (nroot > 0) tree_unpack_kernel<<<(unsigned)((nroot * 42 + 255) / 256), 256, 0, st>>>(a, nroot);
   }
-  // the top group: one launch per level over the whole GPU (a body per warp up, per thread down), deepest first
-  const int g = t.n_bottom;
-  const int l0 = t.glev_ptr[g], l1 = t.glev_ptr[g + 1] - 1;
-  const int MS = tree_ms(a.front_rows);
-  const int wpc = 4;  // warps per CTA of the level launches
-  const size_t sm = sizeof(double) * (size_t)wpc * (a.front_rows * MS + 9 * (TREE_MAXN / 3));
-  for (int l = l0; l < l1; ++l) {
-    const int nb = t.glev_off[l + 1] - t.glev_off[l];
-    a.group0 = l;
-    tree_kernel<<<(nb + wpc - 1) / wpc, 32 * wpc, sm, st>>>(a, TREE_UP_LEVEL, MS);
+  const int m0 = t.n_bottom, m1 = t.n_bottom + t.n_mid, gt = m1;  // middle groups [m0, m1), top group gt
+  if (!t.has_top) {  // the middle groups are whole trees of the top section
+    if ((e = launch_group<TREE_BOTH>(a, m0, m1, t, st))) return e;
+  } else {
+    if ((e = launch_group<TREE_UP>(a, m0, m1, t, st))) return e;
+    if (t.top_fused) {  // the top group as one CTA: up, down and stage 4 in one launch
+      if ((e = launch_group<TREE_BOTH>(a, gt, gt + 1, t, st))) return e;
+    } else {  // a large top group: one launch per level over the whole GPU (a body per warp up, per thread down)
+      const int l0 = t.glev_ptr[gt], l1 = t.glev_ptr[gt + 1] - 1;
+      const int wpc = 4;  // warps per CTA of the upward level launches
+      for (int l = l0; l < l1; ++l) {
+        const int nb = t.glev_off[l + 1] - t.glev_off[l];
+        a.group0 = l;
+        tree_level_kernel<<<(nb + wpc - 1) / wpc, 32 * wpc, 0, st>>>(a, TREE_UP_LEVEL);
+      }
+      for (int l = l1 - 1; l >= l0; --l) {
+        const int nb = t.glev_off[l + 1] - t.glev_off[l];
+        a.group0 = l;
+        tree_level_kernel<<<(nb + 127) / 128, 128, 0, st>>>(a, TREE_DOWN_LEVEL);
+      }
+      if ((e = cudaGetLastError())) return e;
+    }
+    if ((e = launch_group<TREE_DOWN>(a, m0, m1, t, st))) return e;
   }
-  for (int l = l1 - 1; l >= l0; --l) {
-    const int nb = t.glev_off[l + 1] - t.glev_off[l];
-    a.group0 = l;
-    tree_kernel<<<(nb + 127) / 128, 128, 0, st>>>(a, TREE_DOWN_LEVEL, MS);
-  }
-  if ((e = cudaGetLastError())) return e;
-  a.group0 = g_lo;
-  return launch_tree(a, g_hi - g_lo, TREE_DOWN, bot_threads, st);
+  return launch_group<TREE_DOWN>(a, g_lo, g_hi, t, st);
 }
 
 // Split across W ranks (or W emulated parts): contiguous blocks of gpr bottom groups; the joints from top bodies
@@ -531,8 +644,21 @@ bool tree_partition(Plan* p, int W, int rank, bool emulate, std::string* msg) {
   return true;
 }
 
+#ifdef MABD_EXP_TCLOCK
+extern "C" int mabd_dbg_tclk(unsigned long long* out, int n) {
+  const int m = std::min<int>(n, 3 * TCLK_CTAS * TCLK_SLOTS);
+  return (int)cudaMemcpyFromSymbol(out, g_tclk, sizeof(unsigned long long) * m);
+}
+#endif
+
 cudaError_t tree_init() {
-  return cudaFuncSetAttribute(tree_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 210 * 1024);
+  cudaError_t e;
+  if ((e = cudaFuncSetAttribute(tree_group_kernel<TREE_UP>, cudaFuncAttributeMaxDynamicSharedMemorySize, TREE_SMEM_MAX)))
+    return e;
+  if ((e = cudaFuncSetAttribute(tree_group_kernel<TREE_DOWN>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                TREE_SMEM_MAX)))
+    return e;
+  return cudaFuncSetAttribute(tree_group_kernel<TREE_BOTH>, cudaFuncAttributeMaxDynamicSharedMemorySize, TREE_SMEM_MAX);
 }
 
 // ============================================================================ host: topology and ordering
@@ -609,9 +735,17 @@ bool tree_build(const mabd_joints* J, int64_t n, Plan* p, std::vector<int64_t>* 
   std::vector<int64_t> size(n, 1);
   for (auto it = bfs.rbegin(); it != bfs.rend(); ++it)
     if (parent[*it] >= 0) size[parent[*it]] += size[*it];
+  // bodies carrying child joints (real children or anchors): the ones with something to eliminate
+  std::vector<char> nonleaf(n, 0);
+  for (int64_t k = 0; k < K; ++k) {
+    const int64_t a = J->body_a[k], b = J->body_b[k];
+    nonleaf[(b < 0 || (parent[b] == a && upj[b] == k)) ? a : b] = 1;
+  }
+  // group capacity: the larger groups once the tree gives every SM (148 on B200) one of them
+  const int cap = n > 148LL * TREE_CAP ? 2 * TREE_CAP : TREE_CAP;
   std::vector<int64_t> local_roots;
   for (int64_t v : bfs)
-    if (size[v] <= TREE_CAP && (parent[v] < 0 || size[parent[v]] > TREE_CAP)) local_roots.push_back(v);
+    if (size[v] <= cap && (parent[v] < 0 || size[parent[v]] > cap)) local_roots.push_back(v);
   // children lists for subtree collection
   std::vector<std::vector<int64_t>> kids(n);
   for (int64_t v : bfs)
@@ -622,7 +756,7 @@ bool tree_build(const mabd_joints* J, int64_t n, Plan* p, std::vector<int64_t>* 
     std::vector<int64_t> sub{r};
     for (size_t h = 0; h < sub.size(); ++h)
       for (int64_t c : kids[sub[h]]) sub.push_back(c);
-    if (cur.size() + sub.size() > (size_t)TREE_CAP) {
+    if (cur.size() + sub.size() > (size_t)cap) {
       groups.push_back(cur);
       cur.clear();
     }
@@ -631,31 +765,80 @@ bool tree_build(const mabd_joints* J, int64_t n, Plan* p, std::vector<int64_t>* 
   if (!cur.empty()) groups.push_back(cur);
   TreePlan& t = p->tree;
   t = TreePlan();
+  t.cap = cap;
   t.n_bottom = (int32_t)groups.size();
   std::vector<int64_t> top;
   for (int64_t v : bfs)
-    if (size[v] > TREE_CAP) top.push_back(v);
+    if (size[v] > cap) top.push_back(v);
+  if (top.size() > (size_t)TREE_TOP_SMALL && top.size() <= (size_t)cap) {
+    // middle layer: subtrees of the top set with ≤ TREE_MID_CAP bodies (one CTA each), below a small top
+    std::vector<char> in_top(n, 0);
+    for (int64_t v : top) in_top[v] = 1;
+    std::vector<int64_t> size_t_(n, 0);
+    for (auto it = bfs.rbegin(); it != bfs.rend(); ++it)
+      if (in_top[*it]) {
+        size_t_[*it] += 1;
+        if (parent[*it] >= 0) size_t_[parent[*it]] += size_t_[*it];
+      }
+    std::vector<char> taken(n, 0);
+    std::vector<int64_t> mcur;
+    for (int64_t v : top) {
+      if (size_t_[v] > TREE_MID_CAP || (parent[v] >= 0 && size_t_[parent[v]] <= TREE_MID_CAP)) continue;
+      std::vector<int64_t> sub{v};
+      for (size_t h = 0; h < sub.size(); ++h)
+        for (int64_t c : kids[sub[h]])
+          if (in_top[c]) sub.push_back(c);
+      if (mcur.size() + sub.size() > (size_t)TREE_MID_CAP) {
+        groups.push_back(mcur);
+        ++t.n_mid;
+        mcur.clear();
+      }
+      for (int64_t c : sub) taken[c] = 1;
+      mcur.insert(mcur.end(), sub.begin(), sub.end());
+    }
+    if (!mcur.empty()) {
+      groups.push_back(mcur);
+      ++t.n_mid;
+    }
+    std::vector<int64_t> rest;
+    for (int64_t v : top)
+      if (!taken[v]) rest.push_back(v);
+    top.swap(rest);
+  }
   if (!top.empty()) {
     groups.push_back(top);
     t.has_top = true;
+    t.top_fused = top.size() <= (size_t)cap;
   }
   // internal order: groups in sequence, each sorted by depth (deepest first). Level ranges: group g owns
   // levels l ∈ [glev_ptr[g], glev_ptr[g+1]−1), level l spans bodies [glev_off[l], glev_off[l+1]).
   pos_of_body->assign(n, -1);
   std::vector<int64_t> body_of(n);
   int64_t pos = 0;
+  std::vector<int32_t> gid(n, -1);
   t.group_off.push_back(0);
-  for (auto& gvec : groups) {
-    std::stable_sort(gvec.begin(), gvec.end(), [&](int64_t x, int64_t y) { return depth[x] > depth[y]; });
+  for (size_t gi = 0; gi < groups.size(); ++gi) {
+    auto& gvec = groups[gi];
+    std::stable_sort(gvec.begin(), gvec.end(), [&](int64_t x, int64_t y) {
+      return depth[x] != depth[y] ? depth[x] > depth[y] : nonleaf[x] > nonleaf[y];
+    });
     t.glev_ptr.push_back((int32_t)t.glev_off.size());
     for (size_t i = 0; i < gvec.size(); ++i) {
-      if (i == 0 || depth[gvec[i]] != depth[gvec[i - 1]]) t.glev_off.push_back((int32_t)(pos + i));
+      if (i == 0 || depth[gvec[i]] != depth[gvec[i - 1]]) {
+        t.glev_off.push_back((int32_t)(pos + i));
+        t.glev_nl.push_back((int32_t)(pos + i));
+      }
+      if (nonleaf[gvec[i]]) t.glev_nl.back() = (int32_t)(pos + i + 1);
       (*pos_of_body)[gvec[i]] = pos + (int64_t)i;
       body_of[pos + i] = gvec[i];
+      gid[gvec[i]] = (int32_t)gi;
     }
     pos += (int64_t)gvec.size();
     t.glev_off.push_back((int32_t)pos);  // terminator of the group's last level
+    t.glev_nl.push_back((int32_t)pos);   // (keeps glev_nl indexable like glev_off)
     t.group_off.push_back((int32_t)pos);
+    if ((int)gi >= t.n_bottom)  // the top section is prepared by UP0: every body has a front record
+      for (size_t l = t.glev_ptr.back(); l + 1 < t.glev_off.size(); ++l) t.glev_nl[l] = t.glev_off[l + 1];
   }
   t.glev_ptr.push_back((int32_t)t.glev_off.size());
   // joints
@@ -699,6 +882,8 @@ bool tree_build(const mabd_joints* J, int64_t n, Plan* p, std::vector<int64_t>* 
   for (int64_t k = 0; k < K; ++k) cj[(*pos_of_body)[jpar[k]]].push_back((int32_t)k);
   t.child_off.assign(n + 1, 0);
   t.ws_off.assign(n + 1, 0);
+  t.fo_off.assign(n, -1);
+  t.fo_total = 0;
   t.pt_off.clear();
   t.pt_code.clear();
   t.body_nn.clear();
@@ -712,6 +897,9 @@ bool tree_build(const mabd_joints* J, int64_t n, Plan* p, std::vector<int64_t>* 
     t.child_off[i + 1] = t.child_off[i] + (int32_t)cj[i].size();
     for (int32_t kk : cj[i]) t.child_joint.push_back(kk);
     t.ws_off[i + 1] = t.ws_off[i] + N + (int64_t)N * nu;
+    const bool rec = N > 0 || i >= t.group_off[t.n_bottom];  // front record needed (incl. the whole top section)
+    t.fo_off[i] = rec ? t.fo_total : -1;
+    if (rec) t.fo_total += (int64_t)(N + nu) * (N + nu + 1) / 2 + N + nu;
     t.max_m = std::max(t.max_m, N + nu);
     // frontal point list: child joints' points (parent side, +), then the up joint's (child side, −);
     // code = 4·joint + 2·point + (1 for the child side)
@@ -720,15 +908,23 @@ bool tree_build(const mabd_joints* J, int64_t n, Plan* p, std::vector<int64_t>* 
       for (int q = 0; q < t.jnpts[kk]; ++q) t.pt_code.push_back(4 * kk + 2 * q);
     if (upj[v] >= 0)
       for (int q = 0; q < t.jnpts[upj[v]]; ++q) t.pt_code.push_back(4 * (int32_t)upj[v] + 2 * q + 1);
-    t.body_nn.push_back((int32_t)(N | (nu << 8)));
+    const bool ext = parent[v] >= 0 && gid[parent[v]] != gid[v];
+    t.body_nn.push_back((int32_t)(N | (nu << 8) | (ext ? 1 << 16 : 0)));
   }
   t.pt_off.push_back((int32_t)t.pt_code.size());
   t.ws_total = t.ws_off[n];
   p->ld = n;
-  {
+  {  // UP0 (+ top-section preparation), [UP1], top, [DOWN1], DOWN0 — or one launch of whole-tree groups
+    const int gt = t.n_bottom + t.n_mid;  // the top group's index
     int top_levels = 0;
-    if (t.has_top) top_levels = t.glev_ptr[t.n_bottom + 1] - 1 - t.glev_ptr[t.n_bottom];
-    p->launches_per_step = 1 + (t.has_top ? 2 + 2 * top_levels : 1);
+    if (t.has_top) top_levels = t.glev_ptr[gt + 1] - 1 - t.glev_ptr[gt];
+    const int top_launches = !t.has_top ? 0 : t.top_fused ? 1 : 2 * top_levels;
+    if (t.n_mid == 0 && !t.has_top)
+      p->launches_per_step = 1;
+    else if (t.n_mid > 0)
+      p->launches_per_step = 2 + (t.has_top ? 2 + top_launches : 1);
+    else
+      p->launches_per_step = 2 + top_launches;
   }
   return true;
 }

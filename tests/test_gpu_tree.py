@@ -20,12 +20,12 @@ def test_cfg4_recipe_small(cuda_ok, depth):
 
 
 def test_cfg4_recipe_with_top_group(cuda_ok):
-    """Depth 10 (1,023 bodies): four 255-body bottom groups plus a 3-body top group in 2 levels (7 launches/step)."""
+    """Depth 10 (1,023 bodies): four 255-body bottom groups plus a 3-body top group (one CTA): 3 launches/step."""
     sc = G.cfg4_binary_tree(10)
     check(sc, 1, expect_solver="tree")
     check(sc, 5, expect_solver="tree")
     q, _, info = gpu_run(sc, 5)
-    assert info["launches_per_step"] == 7   # predict, bottom up, 2 top levels up and down, bottom down
+    assert info["launches_per_step"] == 3   # bottom groups up, top group (up and down), bottom groups down
     assert O.constraint_residual(sc, q) <= 1e-10
 
 
@@ -48,6 +48,16 @@ def test_hinge_chain_uses_tree_solver(cuda_ok):
     sc = G.random_chain(300, seed=3, npts=2, end_anchor=True, vel=0.2)
     check(sc, 1, expect_solver="tree")
     check(sc, 3, expect_solver="tree")
+
+
+def test_large_top_group_per_level_launches(cuda_ok):
+    """A 1,200-link hinge path rooted at its centre: the ~690 bodies whose subtree exceeds a group form a top group
+    too large for one CTA, which runs one launch per level (up and down) between the bottom-group launches."""
+    sc = G.random_chain(1200, seed=5, npts=2, end_anchor=True, vel=0.2)
+    check(sc, 1, expect_solver="tree")
+    q, _, info = gpu_run(sc, 2)
+    assert info["launches_per_step"] > 100
+    assert O.constraint_residual(sc, q) <= 1e-10
 
 
 def test_cfg4_full_size_one_step(cuda_ok):

@@ -117,13 +117,14 @@ def _check_tree_parts(infos):
 
 @pytest.mark.parametrize("world", [2, 4, 8])
 def test_partition_tree_cfg4(lib, world):
-    """Config 4 at full size: 256 CTA-local subtrees of 255 bodies below a 255-body top, split evenly."""
+    """Config 4 at full size: 128 CTA-local subtrees of 511 bodies (the larger group size: 65,535 bodies give every
+    SM a group) below a 127-body top, split evenly."""
     sc = G.cfg4_binary_tree(16)
     infos = [lib.partition_info(sc, world, r) for r in range(world)]
     _check_tree_parts(infos)
-    assert infos[0]["groups"] == 256 and infos[0]["root_joints"] == 256
-    assert all(i["body_hi"] - i["body_lo"] == 255 * 256 // world for i in infos)
-    assert infos[0]["slots_per_part"] == 256 // world
+    assert infos[0]["groups"] == 128 and infos[0]["root_joints"] == 128
+    assert all(i["body_hi"] - i["body_lo"] == 511 * 128 // world for i in infos)
+    assert infos[0]["slots_per_part"] == 128 // world
 
 
 def _gloo_tree_worker(rank, world, port, out):

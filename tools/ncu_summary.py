@@ -46,30 +46,42 @@ def raw(rep):
 
 
 def source(rep):
+    """Per kernel in the report: warp-stall samples and the SASS opcode mix (the source page repeats its header
+    for every kernel)."""
     rows = list(csv.reader(io.StringIO(ncu("-i", rep, "--page", "source", "--csv", "--print-source", "sass"))))
-    i0 = next(i for i, r in enumerate(rows) if r and r[0] == "Address")
-    hdr, data = rows[i0], [r for r in rows[i0 + 1:] if len(r) >= len(rows[i0])]
-    ix = {k: i for i, k in enumerate(hdr)}
-    stalls = [k for k in hdr if k.startswith("stall_") and "Not Issued" not in k]
-    tot = Counter()
-    ops, ost = Counter(), Counter()
-    for r in data:
-        for k in stalls:
-            tot[k] += float(r[ix[k]] or 0)
-        parts = r[1].split()
-        if not parts:
-            continue
-        op = parts[1] if parts[0].startswith("@") else parts[0]
-        op = op.split(".")[0]
-        ops[op] += float(r[ix["Instructions Executed"]] or 0)
-    S = sum(tot.values()) or 1
-    print("== warp stall samples (share of all samples)")
-    for k, v in tot.most_common(10):
-        print(f"  {k:28s} {100 * v / S:5.1f}%")
-    T = sum(ops.values()) or 1
-    print(f"== SASS opcode mix (warp instructions executed, total {T:.4g})")
-    for k, v in ops.most_common(20):
-        print(f"  {k:10s} {v:12.4g} {100 * v / T:5.1f}%")
+    sections, hdr = [], None
+    for r in rows:
+        if r and r[0] == "Address":
+            hdr = r
+            sections.append((hdr, []))
+        elif hdr is not None and len(r) >= len(hdr):
+            sections[-1][1].append(r)
+    for n, (hdr, data) in enumerate(sections):
+        ix = {k: i for i, k in enumerate(hdr)}
+        stalls = [k for k in hdr if k.startswith("stall_") and "Not Issued" not in k]
+        tot, ops = Counter(), Counter()
+        for r in data:
+            for k in stalls:
+                try:
+                    tot[k] += float(r[ix[k]] or 0)
+                except ValueError:
+                    pass
+            parts = r[1].split()
+            if not parts:
+                continue
+            op = (parts[1] if parts[0].startswith("@") and len(parts) > 1 else parts[0]).split(".")[0]
+            try:
+                ops[op] += float(r[ix["Instructions Executed"]] or 0)
+            except ValueError:
+                pass
+        S = sum(tot.values()) or 1
+        print(f"== source section {n}: warp stall samples (share of all samples)")
+        for k, v in tot.most_common(10):
+            print(f"  {k:28s} {100 * v / S:5.1f}%")
+        T = sum(ops.values()) or 1
+        print(f"== source section {n}: SASS opcode mix (warp instructions executed, total {T:.4g})")
+        for k, v in ops.most_common(20):
+            print(f"  {k:10s} {v:12.4g} {100 * v / T:5.1f}%")
 
 
 def launches(path):
