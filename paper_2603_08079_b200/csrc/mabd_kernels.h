@@ -65,13 +65,15 @@ struct TreeArgs {
   const int32_t* glev_ptr;
   const int32_t* glev_off;
   const int32_t* glev_nl;      // [levels] end of the bodies with child joints in each level (they come first)
-  double* Shat;                // [K][36] child-side condensed dual block of each joint (6×6, row-major)
-  double* rhat;                // [K][6]
+  double* Shat;                // [K][28] child-side condensed dual block of each joint: Ŝ lower triangle (21), r̂ (6)
   double* lam;                 // [K][6]
   double* bscr;                // [n][21]: R, δq̃ between the passes
   double* ws;                  // per-body y, W
   double* f0;                  // per-body front records (G H_b⁻¹ Gᵀ packed lower, own right-hand side)
   const int64_t* fo_off;       // [n] record offset in f0 (−1: none)
+  const int32_t* fo_str;       // [n] record stride (element e at fo_off + e·fo_str)
+  const int32_t* parent;       // [n] parent body (−1: root)
+  const int32_t* up_row;       // [n] row of the body's up joint in its parent's front
   int32_t group0;              // first group of this launch
   int32_t front_rows;          // largest frontal matrix (rows; shared-memory sizing)
   int32_t cap;                 // group capacity (bodies; shared-memory slots of the group kernel)

@@ -515,9 +515,11 @@ mabd_status build_plan(const mabd_bodies* B, const mabd_joints* J, const mabd_op
     f.t_glo = take(sizeof(int32_t) * t.glev_off.size());
     f.t_glnl = take(sizeof(int32_t) * std::max<size_t>(1, t.glev_nl.size()));
     f.t_fo = take(sizeof(int64_t) * std::max<int64_t>(1, n));
+    f.t_fstr = take(sizeof(int32_t) * std::max<int64_t>(1, n));
+    f.t_par = take(sizeof(int32_t) * std::max<int64_t>(1, n));
+    f.t_uprow = take(sizeof(int32_t) * std::max<int64_t>(1, n));
     f.t_f0 = take(sizeof(double) * std::max<int64_t>(1, t.fo_total));
-    f.t_shat = take(sizeof(double) * 36 * std::max<int64_t>(1, K));
-    f.t_rhat = take(sizeof(double) * 6 * std::max<int64_t>(1, K));
+    f.t_shat = take(sizeof(double) * 28 * std::max<int64_t>(1, K));
     f.t_lam = take(sizeof(double) * 6 * std::max<int64_t>(1, K));
     f.t_bscr = take(sizeof(double) * 21 * n);
     f.t_ws = take(sizeof(double) * std::max<int64_t>(1, t.ws_total));
@@ -629,10 +631,12 @@ cudaError_t upload_plan(const Plan& p, char* ws, cudaStream_t st, DevPtrs* d) {
     A.glev_off = (const int32_t*)(ws + f.t_glo);
     A.glev_nl = (const int32_t*)(ws + f.t_glnl);
     A.fo_off = (const int64_t*)(ws + f.t_fo);
+    A.fo_str = (const int32_t*)(ws + f.t_fstr);
+    A.parent = (const int32_t*)(ws + f.t_par);
+    A.up_row = (const int32_t*)(ws + f.t_uprow);
     A.f0 = (double*)(ws + f.t_f0);
     A.cap = t.cap;
     A.Shat = (double*)(ws + f.t_shat);
-    A.rhat = (double*)(ws + f.t_rhat);
     A.lam = (double*)(ws + f.t_lam);
     A.bscr = (double*)(ws + f.t_bscr);
     A.ws = (double*)(ws + f.t_ws);
@@ -662,6 +666,9 @@ cudaError_t upload_plan(const Plan& p, char* ws, cudaStream_t st, DevPtrs* d) {
     if ((e = put((int32_t*)A.glev_off, t.glev_off, st))) return e;
     if ((e = put((int32_t*)A.glev_nl, t.glev_nl, st))) return e;
     if ((e = put((int64_t*)A.fo_off, t.fo_off, st))) return e;
+    if ((e = put((int32_t*)A.fo_str, t.fo_str, st))) return e;
+    if ((e = put((int32_t*)A.parent, t.parent, st))) return e;
+    if ((e = put((int32_t*)A.up_row, t.up_row, st))) return e;
     if ((e = cudaMemsetAsync(A.lam, 0, sizeof(double) * 6 * std::max<int64_t>(1, p.n_joints), st))) return e;
   }
   if (p.solver == MABD_SOLVER_SPARSE) return sparse_upload(p, ws, st, d);

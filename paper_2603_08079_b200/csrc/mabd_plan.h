@@ -45,6 +45,8 @@ struct TreePlan {
   bool has_top = false;
   int64_t ws_total = 0;
   std::vector<int64_t> fo_off;       // [n] front record offsets (bodies with child joints, and the top group)
+  std::vector<int32_t> fo_str;       // [n] their stride (records interleaved per group)
+  std::vector<int32_t> parent, up_row;  // [n] parent body (internal order) and the up joint's row in its front
   int64_t fo_total = 0;
   int32_t max_m = 3;                 // largest frontal matrix (rows)
   std::vector<int32_t> pt_off, pt_code, body_nn;  // per body: frontal point codes, N | nu << 8
@@ -140,7 +142,7 @@ struct Plan {
     std::vector<size_t> tops, lams;  // per BTD level: tops[0] = chain tops (n_long), lams[i] = level i+1 λ
     size_t all_tops, lam_g, plo, lwin, llong;
     std::vector<size_t> p_tops1, p_lam2, p_scr;
-    size_t t_up, t_coff, t_cj, t_wsoff, t_jnpts, t_jchd, t_jy, t_goff, t_glp, t_glo, t_glnl, t_fo, t_f0, t_shat, t_rhat, t_lam, t_bscr,
+    size_t t_up, t_coff, t_cj, t_wsoff, t_jnpts, t_jchd, t_jy, t_goff, t_glp, t_glo, t_glnl, t_fo, t_fstr, t_f0, t_par, t_uprow, t_shat, t_lam, t_bscr,
         t_ws, t_ptoff, t_ptcode, t_nn, t_rootj, t_rslot, t_xbuf;
   } off{};
 };

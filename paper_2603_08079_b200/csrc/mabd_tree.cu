@@ -31,6 +31,7 @@ namespace mabd {
 
 // triangular index t → (row, column), column ≤ row, row-major over the lower triangle (lane-divergent indices:
 // computed, not looked up in constant memory, which would serialise the lanes)
+__host__ __device__ constexpr int tri_row(int t) { return t < 1 ? 0 : t < 3 ? 1 : t < 6 ? 2 : t < 10 ? 3 : t < 15 ? 4 : 5; }
 __device__ __forceinline__ void tri_rc(int t, int& r, int& c) {
   r = (int)((sqrtf(8.0f * (float)t + 1.0f) - 1.0f) * 0.5f);
   if ((r + 1) * (r + 2) / 2 <= t) ++r;
@@ -50,7 +51,7 @@ __device__ __forceinline__ bool nn_ext(int nn) { return (nn >> 16) & 1; }
 
 // Per-body shared-memory slots of a CTA-local group [g0, g1): upward, the condensed child side of the body's up
 // joint (Ŝ_u lower triangle in tri6 order, then r̂_u); downward, λ_u. A body whose parent lies outside the group
-// (ext) also publishes Ŝ_u, r̂_u to global memory (Shat, rhat) and reads λ_u from global memory (lam).
+// (ext) also publishes its slot to global memory (Shat: [joint][TSLOT], same layout) and reads λ_u from lam.
 // s == nullptr: no slots (the per-level launches of a large top group: everything through global memory).
 constexpr int TSLOT = 28;
 __device__ __forceinline__ int tri6(int r, int c) { return r >= c ? r * (r + 1) / 2 + c : c * (c + 1) / 2 + r; }
@@ -63,14 +64,18 @@ struct TSlots {
 
 // Where the condensed block / λ of each child-joint point of a body lives (uint32, frontal point order):
 //   CS_LOCAL  the child body is in the same group: payload = (local index << 1) | point, its slot
-//   CS_GLOBAL the child body is in another group: payload = (joint << 1) | point, Shat / rhat / lam
+//   CS_GLOBAL the child body is in another group: payload = (joint << 1) | point, Shat / lam
 //   CS_ANCHOR no child body (world anchor): payload = (joint << 1) | point, λ in lam
 enum : uint32_t { CS_LOCAL = 0u, CS_GLOBAL = 1u << 30, CS_ANCHOR = 2u << 30, CS_KIND = 3u << 30 };
 constexpr int TNP = TREE_MAXN / 3;  // child-joint points per body (max)
 struct TMeta {
   int32_t nn, u;
   int64_t fo, ws;   // front record in f0 (−1: none), y / W in ws
+  int64_t pf;       // the parent's front record when the parent is in the same group (−1: publish to Shat)
+  int32_t pr, pT;   // row of the up joint in the parent's front; start of the parent's right-hand side
   uint32_t cs[TNP];
+  int32_t any_global;  // some child lies in another group (its condensed block is read from Shat)
+  int32_t fs;          // record stride: the group's records are interleaved (element e of a record at fo + e·fs)
 };
 
 __device__ TMeta tree_meta(const TreeArgs& a, int b, int g0, int g1) {
@@ -78,9 +83,20 @@ __device__ TMeta tree_meta(const TreeArgs& a, int b, int g0, int g1) {
   m.nn = a.body_nn[b];
   m.u = a.up_joint[b];
   m.fo = a.fo_off[b];
+  m.fs = a.fo_str[b];
   m.ws = a.ws_off[b];
   const int32_t* pc = a.pt_code + a.pt_off[b];
   const int N = nn_N(m.nn);
+  const int p = a.parent[b];
+  m.pf = -1;
+  m.pr = a.up_row[b];
+  m.pT = 0;
+  if (p >= g0 && p < g1) {
+    const int pn = a.body_nn[p], Mp = nn_N(pn) + nn_nu(pn);
+    m.pf = a.fo_off[p];
+    m.pT = Mp * (Mp + 1) / 2;
+  }
+  m.any_global = 0;
 #pragma unroll
   for (int i = 0; i < TNP; ++i) {
     uint32_t v = 0;
@@ -89,52 +105,92 @@ __device__ TMeta tree_meta(const TreeArgs& a, int b, int g0, int g1) {
       const uint32_t kp = (uint32_t)(code >> 1);  // (joint << 1) | point
       const int c = a.jchd[code >> 2];
       v = c < 0 ? (CS_ANCHOR | kp) : (c >= g0 && c < g1) ? ((uint32_t)(c - g0) << 1 | (kp & 1u)) : (CS_GLOBAL | kp);
+      if ((v & CS_KIND) == CS_GLOBAL) m.any_global = 1;
     }
     m.cs[i] = v;
   }
   return m;
 }
 
-// Body b's front record (f0 + fo): the packed lower triangle of F = G H_b⁻¹ Gᵀ (M×M, (i, j) at i(i+1)/2 + j),
+__device__ const double kZeroSlot[TSLOT] = {};  // the condensed block of an anchor (none)
+
+// Entry t of a condensed block (tri6 index < 21: Ŝ_u row r ≥ column c; 21 + r: r̂_u row r) added into the parent's
+// front record: Ŝ_u lands on the parent's diagonal block of joint u (rows pr.., packed lower), r̂_u on its
+// right-hand side. Each entry has exactly one writer (its child), after the parent's record was written.
+__device__ __forceinline__ void tree_push(const TreeArgs& a, const TMeta& m, int r, int c, bool rhs, double x) {
+  const int row = m.pr + r;
+  a.f0[m.pf + (int64_t)m.fs * (rhs ? m.pT + row : row * (row + 1) / 2 + m.pr + c)] += x;  // same group: same stride
+}
+
+// Body b's front record (element e at f0[fo + e·fs], interleaved with the group's other records so that a thread per
+// body writes them coalesced): the packed lower triangle of F = G H_b⁻¹ Gᵀ (M×M, (i, j) at i(i+1)/2 + j),
 // then its own side of the right-hand side (M): +x_b(ȳ) (child-joint points; − p_world for an anchor),
-// −x_b(ȳ) (up-joint points), at q̃. The children's condensed blocks are added at elimination.
+// −x_b(ȳ) (up-joint points), at q̃. With slots, the condensed blocks of leaf children in the group (already in
+// their slots) are added here; other children's are added later (pushed by the child, or read from Shat).
 __device__ void tree_assemble(const TreeArgs& a, int b, const TMeta& m, const double* R, const double* qt,
-                              const HinvBlk& H) {
-  const int M = nn_N(m.nn) + nn_nu(m.nn), npt = M / 3, T = M * (M + 1) / 2;
+                              const HinvBlk& H, const TSlots& sl, const TMeta* meta) {
+  const int N = nn_N(m.nn), M = N + nn_nu(m.nn), npt = M / 3, T = M * (M + 1) / 2;
   const int32_t* pc = a.pt_code + a.pt_off[b];
   double* f = a.f0 + m.fo;
+  const int64_t fs = m.fs;
+  // every point's code, ȳ and world point first (independent loads, two round trips in all)
+  constexpr int NPT = TNP + 2;
+  int code[NPT];
+  double yy[NPT][6];
+  const double* leaf[NPT];  // a leaf child's slot (child-joint points), or null
   for (int i = 0; i < npt; ++i) {
-    const int ci = pc[i];
-    const int ji = ci >> 2, si = ci & 1;
-    const double* yi = a.jy + 12 * (int64_t)ji + 6 * si + 3 * ((ci >> 1) & 1);
+    code[i] = pc[i];
+    leaf[i] = nullptr;
+    if (sl.s != nullptr && 3 * i < N) {
+      const uint32_t c = m.cs[i];
+      const uint32_t id = (c & ~CS_KIND) >> 1;
+      if ((c & CS_KIND) == CS_LOCAL && nn_N(meta[id].nn) == 0) leaf[i] = sl.local(id);
+    }
+  }
+  for (int i = 0; i < npt; ++i) {
+    const double* yi = a.jy + 12 * (int64_t)(code[i] >> 2) + 6 * (code[i] & 1) + 3 * ((code[i] >> 1) & 1);
+#pragma unroll
+    for (int e = 0; e < 3; ++e) {
+      yy[i][e] = yi[e];
+      yy[i][3 + e] = (code[i] & 1) ? 0.0 : yi[6 + e];  // anchor world point (child side of a parent point)
+    }
+  }
+  for (int i = 0; i < npt; ++i) {
+    const int ci = code[i];
+    const int si = ci & 1, pi = (ci >> 1) & 1;
+    const double* yi = yy[i];
     double x[3];
     point_pos(qt, yi, x);
-    const bool anchor = !si && a.jchd[ji] < 0;
+    const bool anchor = !si && a.jchd[ci >> 2] < 0;
+    const double* li = leaf[i];
 #pragma unroll
-    for (int e = 0; e < 3; ++e) f[T + 3 * i + e] = si ? -x[e] : (anchor ? x[e] - yi[6 + e] : x[e]);
+    for (int e = 0; e < 3; ++e)
+      f[fs * (T + 3 * i + e)] = si ? -x[e] : (anchor ? x[e] - yi[3 + e] : x[e] + (li ? li[21 + 3 * pi + e] : 0.0));
     for (int j = 0; j <= i; ++j) {
-      const int cj = pc[j];
-      const double* yj = a.jy + 12 * (int64_t)(cj >> 2) + 6 * (cj & 1) + 3 * ((cj >> 1) & 1);
+      const int cj = code[j];
+      const double* yj = yy[j];
       double P[9], Bk[9];
       pblock(H, yi, yj, P);
       rot_conj(R, P, Bk);
       const double sg = ((ci ^ cj) & 1) ? -1.0 : 1.0;
+      const bool same = li != nullptr && (ci >> 2) == (cj >> 2);  // both points of the same leaf child's joint
+      const int pj = (cj >> 1) & 1;
 #pragma unroll
       for (int r = 0; r < 3; ++r)
 #pragma unroll
         for (int c = 0; c < 3; ++c)
-          if (i > j || r >= c) f[(3 * i + r) * (3 * i + r + 1) / 2 + 3 * j + c] = sg * Bk[3 * r + c];
+          if (i > j || r >= c)
+            f[fs * ((3 * i + r) * (3 * i + r + 1) / 2 + 3 * j + c)] =
+                sg * Bk[3 * r + c] + (same ? li[tri6(3 * pi + r, 3 * pj + c)] : 0.0);
     }
   }
 }
 
-// Stages 1-2 of body b (no tree dependency): R and δq̃ → bscr, then the body's front record. With slots, a leaf (no
-// child joints) instead condenses its up joint right away: N = 0 leaves nothing to eliminate, so
-// Ŝ_u = F_uu = Σ (−1)² R P(ȳ_i, ȳ_j) Rᵀ over the up joint's child-side points and r̂_u = r_u = −x_b(ȳ_i) at q̃.
-__device__ void tree_predict_body(const TreeArgs& a, int b, const TSlots& sl, const TMeta& m) {
+// Stages 1-2 of body b (no tree dependency): R, q̃ and H_b⁻¹'s blocks out, R and δq̃ → bscr.
+__device__ void tree_predict_core(const TreeArgs& a, int b, double* R, double* qt, HinvBlk& H) {
   const StepConsts& k = a.k;
   const int64_t ld = a.b.ld;
-  double q[12], qd[12], R[9], dqt[12];
+  double q[12], qd[12], dqt[12];
 #pragma unroll
   for (int c = 0; c < 12; ++c) {
     q[c] = a.b.q[c * ld + b];
@@ -143,7 +199,6 @@ __device__ void tree_predict_body(const TreeArgs& a, int b, const TSlots& sl, co
   const int mid = a.b.mat_id ? a.b.mat_id[b] : 0;
   const double msc = a.b.mscale ? a.b.mscale[b] : 1.0;
   const Material M = a.b.mats[mid];
-  HinvBlk H;
   if (a.hinv_tab)
     H = a.hinv_tab[mid];
   else
@@ -155,14 +210,31 @@ __device__ void tree_predict_body(const TreeArgs& a, int b, const TSlots& sl, co
   for (int c = 0; c < 9; ++c) sc[c] = R[c];
 #pragma unroll
   for (int c = 0; c < 12; ++c) sc[9 + c] = dqt[c];
-  double qt[12];
 #pragma unroll
   for (int c = 0; c < 12; ++c) qt[c] = q[c] + dqt[c];
+}
+
+// R, q̃ = qⁿ + δq̃ (bscr) and the blocks of H_b⁻¹ of body b after its stages 1-2.
+__device__ void tree_reload(const TreeArgs& a, int b, double* R, double* qt, HinvBlk& H) {
+  const int64_t ld = a.b.ld;
+  const double* sc = a.bscr + 21 * (int64_t)b;
+#pragma unroll
+  for (int c = 0; c < 9; ++c) R[c] = sc[c];
+#pragma unroll
+  for (int c = 0; c < 12; ++c) qt[c] = a.b.q[c * ld + b] + sc[9 + c];
+  const int mid = a.b.mat_id ? a.b.mat_id[b] : 0;
+  if (a.hinv_tab)
+    H = a.hinv_tab[mid];
+  else
+    hinv_blocks(a.b.mats[mid], a.b.mscale ? a.b.mscale[b] : 1.0, a.k.ih2, H);
+}
+
+// A leaf (no child joints) of a group condenses its up joint right away: N = 0 leaves nothing to eliminate, so
+// Ŝ_u = F_uu = Σ (−1)² R P(ȳ_i, ȳ_j) Rᵀ over the up joint's child-side points and r̂_u = r_u = −x_b(ȳ_i) at q̃
+// → its slot (and Shat when the parent is in another group).
+__device__ void tree_leaf(const TreeArgs& a, int b, const TMeta& m, const TSlots& sl, const double* R,
+                          const double* qt, const HinvBlk& H) {
   const int nu = nn_nu(m.nn);
-  if (sl.s == nullptr || nn_N(m.nn) != 0) {
-    if (m.fo >= 0) tree_assemble(a, b, m, R, qt, H);
-    return;
-  }
   if (nu == 0) return;
   const double* yc = a.jy + 12 * (int64_t)m.u + 6;
   double* o = sl.at(b);
@@ -183,10 +255,8 @@ __device__ void tree_predict_body(const TreeArgs& a, int b, const TSlots& sl, co
     for (int e = 0; e < 3; ++e) o[21 + 3 * pi + e] = -x[e];
   }
   if (nn_ext(m.nn)) {
-    for (int r = 0; r < nu; ++r) {
-      for (int c = 0; c < nu; ++c) a.Shat[36 * (int64_t)m.u + 6 * r + c] = o[tri6(r, c)];
-      a.rhat[6 * (int64_t)m.u + r] = o[21 + r];
-    }
+    double* g = a.Shat + TSLOT * (int64_t)m.u;
+    for (int t = 0; t < TSLOT - 1; ++t) g[t] = o[t];
   }
 }
 
@@ -228,6 +298,7 @@ __device__ __forceinline__ void tree_elim(const TreeArgs& a, int b, int lane, co
   const StepConsts& k = a.k;
   const int nn = mp->nn, N = nn_N(nn), nu = nn_nu(nn), M = N + nu, u = mp->u;
   const double* f = a.f0 + mp->fo;
+  const int64_t fs = mp->fs;
   const int T = M * (M + 1) / 2, tl = lane * (lane + 1) / 2;
 #ifdef MABD_EXP_TCLOCK
   const bool probe = blockIdx.x == 0 && lane == 0 && b == sl.g1 - 1 && sl.s != nullptr;
@@ -237,30 +308,24 @@ __device__ __forceinline__ void tree_elim(const TreeArgs& a, int b, int lane, co
 #pragma unroll
   for (int i = 0; i < MX; ++i) {
     double x = 0.0;
-    if (i < M && lane <= M) x = f[lane == M ? T + i : (i >= lane ? i * (i + 1) / 2 + lane : tl + i)];
+    if (i < M && lane <= M) x = f[fs * (lane == M ? T + i : (i >= lane ? i * (i + 1) / 2 + lane : tl + i))];
     v[i] = x;
   }
   EMARK(probe && v[0] != 1e300, 41);
-  if (lane < N || lane == M) {  // the children's condensed blocks
+  if (mp->any_global && (lane < N || lane == M)) {  // condensed blocks of children in other groups (Shat); the
+                                                    // children in this group pushed theirs into the record
     const uint32_t cj = lane < N ? mp->cs[lane / 3] : 0u;
     const int rj = 3 * (int)(cj & 1u) + lane % 3;
 #pragma unroll
     for (int i = 0; i < MX; ++i) {
-      if (i < N) {
-        const uint32_t ci = mp->cs[i / 3];
-        const uint32_t kind = ci & CS_KIND;
-        if (kind != CS_ANCHOR) {
-          const int ri = 3 * (int)(ci & 1u) + i % 3;
-          const uint32_t id = (ci & ~CS_KIND) >> 1;  // child local index or joint
-          if (lane == M)
-            v[i] += kind == CS_LOCAL ? sl.local(id)[21 + ri] : a.rhat[6 * (int64_t)id + ri];
-          else if (((ci ^ cj) & ~1u) == 0u)  // same child joint (same kind and id)
-            v[i] += kind == CS_LOCAL ? sl.local(id)[tri6(ri, rj)] : a.Shat[36 * (int64_t)id + 6 * ri + rj];
-        }
-      }
+      const uint32_t ci = i < N ? mp->cs[i / 3] : CS_ANCHOR;
+      const uint32_t kind = ci & CS_KIND, id = (ci & ~CS_KIND) >> 1;
+      const double* src = kind == CS_GLOBAL ? a.Shat + TSLOT * (int64_t)id : kZeroSlot;
+      const int ri = 3 * (int)(ci & 1u) + i % 3;
+      const double x = src[lane == M ? 21 + ri : tri6(ri, rj)];
+      v[i] += (lane == M || ((ci ^ cj) & ~1u) == 0u) ? x : 0.0;  // same child joint as this column
     }
   }
-  EMARK(probe && v[0] != 1e300, 42);
   // Pivot loop kept rolled (code size: every step runs the same instructions): the registers rotate by one row per
   // step so that the pivot row is always v[0]; after N steps, v[i] holds original row (i + N) mod MX, i.e.
   // rows N..M−1 (Ŝ_u / r̂_u) at v[0..nu) and rows 0..N−1 (W / y) at v[MX−N..MX).
@@ -286,19 +351,17 @@ __device__ __forceinline__ void tree_elim(const TreeArgs& a, int b, int lane, co
     const int r = i - (MX - N);  // row r < N of y / W
     if (r >= 0) ws[cu == nu ? r : N + r * nu + cu] = v[i];
   }
-  if (u >= 0) {  // condensed child side of the up joint → this body's slot, and global memory if ext
-    double* o = sl.s != nullptr ? sl.at(b) : nullptr;
-    const bool glob = sl.s == nullptr || nn_ext(nn);
+  if (u >= 0) {  // condensed child side of the up joint → the parent's record, or Shat (parent in another group)
+    const TMeta& m = *mp;
 #pragma unroll
     for (int r = 0; r < 6; ++r) {
       if (r >= nu) break;
       const double x = v[r];
-      if (o != nullptr && (cu == nu || r >= cu)) o[cu == nu ? 21 + r : tri6(r, cu)] = x;
-      if (glob) {
-        if (cu == nu)
-          a.rhat[6 * (int64_t)u + r] = x;
+      if (cu == nu || r >= cu) {
+        if (m.pf >= 0)
+          tree_push(a, m, r, cu, cu == nu, x);
         else
-          a.Shat[36 * (int64_t)u + 6 * r + cu] = x;  // column cu of the symmetric Ŝ_u
+          a.Shat[TSLOT * (int64_t)u + (cu == nu ? 21 + r : tri6(r, cu))] = x;
       }
     }
   } else if (sl.s == nullptr && cu == nu) {  // root of the per-level schedule: λ_X = y
@@ -343,30 +406,42 @@ __device__ __forceinline__ double* tree_lam_at(const TreeArgs& a, const TSlots& 
 }
 
 // Downward step at a body with child joints (one thread): λ_X = y − W λ_u → the child bodies' slots (or lam).
-// Every load is issued before the first store.
-__device__ void tree_lambda(const TreeArgs& a, int b, const TMeta& m, const TSlots& sl) {
-  const int N = nn_N(m.nn), nu = nn_nu(m.nn);
-  const double* ws = a.ws + m.ws;
-  double lu[6];
-  tree_lambda_up(a, b, m, sl, lu);
-  double lx[TREE_MAXN];
+// NP child points (exact size: every load unconditional and issued together).
+template <int NP>
+__device__ __forceinline__ void tree_lambda_np(const TreeArgs& a, const TMeta& m, const TSlots& sl, const double* ws,
+                                               const double* lu) {
+  constexpr int N = 3 * NP;
+  const int nu = nn_nu(m.nn);
+  double lx[N];
 #pragma unroll
-  for (int r = 0; r < TREE_MAXN; ++r) {
-    double v = 0.0;
-    if (r < N) {
-      v = ws[r];
+  for (int r = 0; r < N; ++r) {
+    double v = ws[r];
 #pragma unroll
-      for (int c = 0; c < 6; ++c)
-        if (c < nu) v -= ws[N + r * nu + c] * lu[c];
-    }
+    for (int c = 0; c < 6; ++c) v -= ws[N + r * nu + (c < nu ? c : 0)] * lu[c];  // lu[c ≥ nu] = 0
     lx[r] = v;
   }
 #pragma unroll
-  for (int i = 0; i < TNP; ++i) {
-    if (3 * i >= N) break;
+  for (int i = 0; i < NP; ++i) {
     double* d = tree_lam_at(a, sl, m.cs[i]);
 #pragma unroll
     for (int e = 0; e < 3; ++e) d[e] = lx[3 * i + e];
+  }
+}
+
+__device__ void tree_lambda(const TreeArgs& a, int b, const TMeta& m, const TSlots& sl) {
+  const double* ws = a.ws + m.ws;
+  double lu[6];
+  tree_lambda_up(a, b, m, sl, lu);
+  switch (nn_N(m.nn) / 3) {
+    case 1: tree_lambda_np<1>(a, m, sl, ws, lu); break;
+    case 2: tree_lambda_np<2>(a, m, sl, ws, lu); break;
+    case 3: tree_lambda_np<3>(a, m, sl, ws, lu); break;
+    case 4: tree_lambda_np<4>(a, m, sl, ws, lu); break;
+    case 5: tree_lambda_np<5>(a, m, sl, ws, lu); break;
+    case 6: tree_lambda_np<6>(a, m, sl, ws, lu); break;
+    case 7: tree_lambda_np<7>(a, m, sl, ws, lu); break;
+    case 8: tree_lambda_np<8>(a, m, sl, ws, lu); break;
+    default: break;
   }
 }
 
@@ -393,15 +468,18 @@ __device__ void tree_update(const TreeArgs& a, int b, const TMeta& m, const TSlo
   double gq[12];
 #pragma unroll
   for (int c = 0; c < 12; ++c) gq[c] = 0.0;
+  if (N > 0) {
 #pragma unroll
-  for (int i = 0; i < TNP; ++i) {  // child-joint points (this body is their parent side, sign +)
-    if (3 * i >= N) break;
-    const int code = pcode[i];
-    const double* lam = tree_lam_at(a, sl, m.cs[i]);
-    const double l3[3] = {lam[0], lam[1], lam[2]};
-    double w[3];
-    mat3t_vec(R, l3, w);
-    add_point_force(gq, a.jy + 12 * (int64_t)(code >> 2) + 3 * ((code >> 1) & 1), w, 1.0);
+    for (int i = 0; i < TNP; ++i) {  // child-joint points (this body is their parent side, sign +); loads unguarded
+      const int ii = 3 * i < N ? i : 0;
+      const int code = pcode[ii];
+      const double* lam = tree_lam_at(a, sl, m.cs[ii]);
+      const double s = 3 * i < N ? 1.0 : 0.0;
+      const double l3[3] = {s * lam[0], s * lam[1], s * lam[2]};
+      double w[3];
+      mat3t_vec(R, l3, w);
+      add_point_force(gq, a.jy + 12 * (int64_t)(code >> 2) + 3 * ((code >> 1) & 1), w, 1.0);
+    }
   }
 #pragma unroll
   for (int pp = 0; pp < 2; ++pp) {  // up-joint points (this body is their child side, sign −)
@@ -467,7 +545,13 @@ __global__ void __launch_bounds__(512, 1) tree_group_kernel(TreeArgs a, int ngro
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, nw = blockDim.x >> 5;
   if ((int)blockIdx.x >= ngroups) {
     const int b = top0 + ((int)blockIdx.x - ngroups) * blockDim.x + threadIdx.x;
-    if (b < a.n) tree_predict_body(a, b, TSlots{nullptr, 0, 0}, tree_meta(a, b, 0, 0));
+    if (b < a.n) {
+      double R[9], qt[12];
+      HinvBlk H;
+      tree_predict_core(a, b, R, qt, H);
+      const TMeta m = tree_meta(a, b, 0, 0);
+      if (m.fo >= 0) tree_assemble(a, b, m, R, qt, H, TSlots{nullptr, 0, 0}, nullptr);
+    }
     return;
   }
   const int g = a.group0 + blockIdx.x;
@@ -476,12 +560,31 @@ __global__ void __launch_bounds__(512, 1) tree_group_kernel(TreeArgs a, int ngro
   const TSlots sl{tsm, g0, g1};
   TMeta* meta = reinterpret_cast<TMeta*>(tsm + (size_t)a.cap * TSLOT);
   TMARK(0);
-  for (int b = g0 + threadIdx.x; b < g1; b += blockDim.x) {
-    const TMeta m = tree_meta(a, b, g0, g1);
-    meta[b - g0] = m;
-    if (MODE != TREE_DOWN && !prepared) tree_predict_body(a, b, sl, m);
+  // one body per thread (a group has at most cap ≤ blockDim bodies): stages 1-2 and the leaves' condensed blocks,
+  // then (after the leaves' slots are complete) the front records of the bodies with child joints
+  const int bb = g0 + threadIdx.x;
+  const bool mine = bb < g1, prep = MODE != TREE_DOWN && !prepared;
+  if (mine) {
+    const TMeta m = tree_meta(a, bb, g0, g1);
+    meta[bb - g0] = m;
+    if (prep) {
+      double R[9], qt[12];
+      HinvBlk H;
+      tree_predict_core(a, bb, R, qt, H);
+      if (nn_N(m.nn) == 0) tree_leaf(a, bb, m, sl, R, qt, H);
+    }
   }
   __syncthreads();
+  TMARK(31);
+  if (prep) {
+    if (mine && nn_N(meta[bb - g0].nn) > 0) {  // R, q̃, H_b⁻¹ reloaded (not held across the barrier)
+      double R[9], qt[12];
+      HinvBlk H;
+      tree_reload(a, bb, R, qt, H);
+      tree_assemble(a, bb, meta[bb - g0], R, qt, H, sl, meta);
+    }
+    __syncthreads();
+  }
   TMARK(1);
   if (MODE != TREE_DOWN) {
     for (int l = l0; l < l1; ++l) {
@@ -507,26 +610,21 @@ __global__ void __launch_bounds__(512, 1) tree_group_kernel(TreeArgs a, int ngro
   }
 }
 
-// Multi-part split: the condensed child side (Ŝ_u 36, r̂_u 6) of every joint from a top body into a bottom group,
-// packed by the part owning the group into its block of the all-gather buffer, then unpacked by every part into
-// Shat / rhat for the top levels. Root entries [r0, r1) are those of a part's groups.
+// Multi-part split: the condensed child side (slot layout, TSLOT doubles) of every joint from a top body into a
+// bottom group, packed by the part owning the group into its block of the all-gather buffer, then unpacked by every
+// part into Shat for the top section. Root entries [r0, r1) are those of a part's groups.
 __global__ void tree_pack_kernel(TreeArgs a, int r0, int r1) {
   const int i = blockIdx.x * blockDim.x + threadIdx.x;
-  const int r = r0 + i / 42, e = i % 42;
+  const int r = r0 + i / TSLOT, e = i % TSLOT;
   if (r >= r1) return;
   const int u = a.root_joint[r];
-  a.xbuf[(size_t)a.root_slot[r] * 42 + e] = e < 36 ? a.Shat[36 * (int64_t)u + e] : a.rhat[6 * (int64_t)u + e - 36];
+  a.xbuf[(size_t)a.root_slot[r] * TSLOT + e] = a.Shat[TSLOT * (int64_t)u + e];
 }
 __global__ void tree_unpack_kernel(TreeArgs a, int nroot) {
   const int i = blockIdx.x * blockDim.x + threadIdx.x;
-  const int r = i / 42, e = i % 42;
+  const int r = i / TSLOT, e = i % TSLOT;
   if (r >= nroot) return;
-  const int u = a.root_joint[r];
-  const double v = a.xbuf[(size_t)a.root_slot[r] * 42 + e];
-  if (e < 36)
-    a.Shat[36 * (int64_t)u + e] = v;
-  else
-    a.rhat[6 * (int64_t)u + e - 36] = v;
+  a.Shat[TSLOT * (int64_t)a.root_joint[r] + e] = a.xbuf[(size_t)a.root_slot[r] * TSLOT + e];
 }
 
 constexpr size_t TREE_SMEM_MAX = 227 * 1024;  // dynamic shared memory per CTA (sm_100a opt-in maximum)
@@ -566,14 +664,14 @@ cudaError_t tree_step(const Plan& p, const DevPtrs& d, const StepConsts& k, cuda
     for (int q = q0; q < q1; ++q) {
       const int lo = std::min(t.n_bottom, q * t.gpr), hi = std::min(t.n_bottom, (q + 1) * t.gpr);
       const int r0 = t.root_off[lo], r1 = t.root_off[hi];
-      if (r1 > r0) tree_pack_kernel<<<(unsigned)(((r1 - r0) * 42 + 255) / 256), 256, 0, st>>>(a, r0, r1);
+      if (r1 > r0) tree_pack_kernel<<<(unsigned)(((r1 - r0) * TSLOT + 255) / 256), 256, 0, st>>>(a, r0, r1);
     }
     if (split && t.rpp > 0) {
-      const int rc = nccl_allgather_doubles(d.nccl_comm, a.xbuf, (size_t)t.rpp * 42, t.part, st);
+      const int rc = nccl_allgather_doubles(d.nccl_comm, a.xbuf, (size_t)t.rpp * TSLOT, t.part, st);
       if (rc != 0) return cudaErrorUnknown;
     }
     const int nroot = t.root_off[t.n_bottom];
-    if (nroot > 0) tree_unpack_kernel<<<(unsigned)((nroot * 42 + 255) / 256), 256, 0, st>>>(a, nroot);
+    if (nroot > 0) tree_unpack_kernel<<<(unsigned)((nroot * TSLOT + 255) / 256), 256, 0, st>>>(a, nroot);
   }
   const int m0 = t.n_bottom, m1 = t.n_bottom + t.n_mid, gt = m1;  // middle groups [m0, m1), top group gt
   if (!t.has_top) {  // the middle groups are whole trees of the top section
@@ -883,7 +981,9 @@ bool tree_build(const mabd_joints* J, int64_t n, Plan* p, std::vector<int64_t>* 
   t.child_off.assign(n + 1, 0);
   t.ws_off.assign(n + 1, 0);
   t.fo_off.assign(n, -1);
+  t.fo_str.assign(n, 0);
   t.fo_total = 0;
+  std::vector<int64_t> recsz(n, 0);
   t.pt_off.clear();
   t.pt_code.clear();
   t.body_nn.clear();
@@ -898,8 +998,7 @@ bool tree_build(const mabd_joints* J, int64_t n, Plan* p, std::vector<int64_t>* 
     for (int32_t kk : cj[i]) t.child_joint.push_back(kk);
     t.ws_off[i + 1] = t.ws_off[i] + N + (int64_t)N * nu;
     const bool rec = N > 0 || i >= t.group_off[t.n_bottom];  // front record needed (incl. the whole top section)
-    t.fo_off[i] = rec ? t.fo_total : -1;
-    if (rec) t.fo_total += (int64_t)(N + nu) * (N + nu + 1) / 2 + N + nu;
+    recsz[i] = rec ? (int64_t)(N + nu) * (N + nu + 1) / 2 + N + nu : 0;
     t.max_m = std::max(t.max_m, N + nu);
     // frontal point list: child joints' points (parent side, +), then the up joint's (child side, −);
     // code = 4·joint + 2·point + (1 for the child side)
@@ -913,6 +1012,34 @@ bool tree_build(const mabd_joints* J, int64_t n, Plan* p, std::vector<int64_t>* 
   }
   t.pt_off.push_back((int32_t)t.pt_code.size());
   t.ws_total = t.ws_off[n];
+  for (size_t g = 0; g + 1 < t.group_off.size(); ++g) {  // records interleaved per group
+    int32_t cnt = 0;
+    int64_t mx = 0;
+    for (int b = t.group_off[g]; b < t.group_off[g + 1]; ++b)
+      if (recsz[b] > 0) {
+        ++cnt;
+        mx = std::max(mx, recsz[b]);
+      }
+    int32_t rho = 0;
+    for (int b = t.group_off[g]; b < t.group_off[g + 1]; ++b)
+      if (recsz[b] > 0) {
+        t.fo_off[b] = t.fo_total + rho++;
+        t.fo_str[b] = cnt;
+      }
+    t.fo_total += mx * cnt;
+  }
+  t.parent.assign(n, -1);
+  t.up_row.assign(n, 0);
+  for (int64_t i = 0; i < n; ++i) {  // each child's up-joint rows in its parent's front (child joints in order)
+    int row = 0;
+    for (int32_t kk : cj[i]) {
+      if (t.jchd[kk] >= 0) {
+        t.parent[t.jchd[kk]] = (int32_t)i;
+        t.up_row[t.jchd[kk]] = row;
+      }
+      row += 3 * t.jnpts[kk];
+    }
+  }
   p->ld = n;
   {  // UP0 (+ top-section preparation), [UP1], top, [DOWN1], DOWN0 — or one launch of whole-tree groups
     const int gt = t.n_bottom + t.n_mid;  // the top group's index

@@ -30,6 +30,7 @@ for mode, name in ((0, "UP"), (2, "TOP (both)"), (1, "DOWN")):
     ctas = np.where(t.max(axis=1) > 0)[0]
     t = t[ctas]
     slots = [s for s in range(64) if (t[:, s] > 0).all()]
+    slots.sort(key=lambda s: np.median(t[:, s]))  # in time order
     print(f"== {name}: {len(ctas)} CTAs; kernel span (first mark → last mark) {((t[:, slots].max() - t[:, slots][:, 0].min()) / 1e3):.1f} us")
     prev = None
     for s in slots:
@@ -40,3 +41,6 @@ for mode, name in ((0, "UP"), (2, "TOP (both)"), (1, "DOWN")):
 e = T[0, 0, 40:45]
 print("elim probe (last body of CTA 0, last kernel to write):", [round((int(e[i + 1]) - int(e[i])) / 1e3, 2) for i in range(4)],
       "us: column load | children | Gauss-Jordan | outputs")
+e = T[0, 0, 50:53]
+print("lambda probe (root of group 0, DOWN):", [round((int(e[i + 1]) - int(e[i])) / 1e3, 2) for i in range(2)],
+      "us: λ_u load | y − Wλ_u")
