@@ -539,8 +539,12 @@ __global__ void __launch_bounds__(512) tree_level_kernel(TreeArgs a, int mode) {
 // UP launches of the bottom groups carry extra CTAs (blockIdx.x ≥ ngroups) that prepare the top section
 // [top0, n): stages 1-2 and front records, a thread per body, on the SMs the groups leave idle. The groups of the
 // top section (prepared != 0) then only load their metadata in the first phase.
+#ifndef MABD_TREE_THREADS
+#define MABD_TREE_THREADS 512
+#endif
+constexpr int TREE_THREADS = MABD_TREE_THREADS;  // threads per group CTA (≥ cap: one body per thread in phase A)
 template <int MODE>
-__global__ void __launch_bounds__(512, 1) tree_group_kernel(TreeArgs a, int ngroups, int top0, int prepared) {
+__global__ void __launch_bounds__(TREE_THREADS, 1) tree_group_kernel(TreeArgs a, int ngroups, int top0, int prepared) {
   extern __shared__ double tsm[];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, nw = blockDim.x >> 5;
   if ((int)blockIdx.x >= ngroups) {
@@ -637,12 +641,12 @@ static cudaError_t launch_group(const TreeArgs& a, int g_lo, int g_hi, const Tre
                                 bool prepare_top = false) {
   const int ng = std::max(0, g_hi - g_lo);
   const int top0 = t.group_off[t.n_bottom];
-  const int nprep = prepare_top ? (int)((a.n - top0 + 511) / 512) : 0;
+  const int nprep = prepare_top ? (int)((a.n - top0 + TREE_THREADS - 1) / TREE_THREADS) : 0;
   if (ng + nprep == 0) return cudaSuccess;
   TreeArgs b = a;
   b.group0 = g_lo;
   const int prepared = g_lo >= t.n_bottom ? 1 : 0;
-  tree_group_kernel<MODE><<<ng + nprep, 512, tree_group_smem(t.cap), st>>>(b, ng, top0, prepared);
+  tree_group_kernel<MODE><<<ng + nprep, TREE_THREADS, tree_group_smem(t.cap), st>>>(b, ng, top0, prepared);
   return cudaGetLastError();
 }
 

@@ -50,6 +50,16 @@ def test_hinge_chain_uses_tree_solver(cuda_ok):
     check(sc, 3, expect_solver="tree")
 
 
+def test_middle_layer_multi_step(cuda_ok):
+    """Depth 14 (16,383 bodies): 64 bottom groups of 255 bodies; the 63-body top set gets a middle layer (two
+    31-body groups) below a 1-body top, prepared by the bottom UP launch: 5 launches per step."""
+    sc = G.cfg4_binary_tree(14)
+    q, _, info = gpu_run(sc, 1)
+    assert info["launches_per_step"] == 5
+    check(sc, 1, expect_solver="tree")
+    check(sc, 8, expect_solver="tree")
+
+
 def test_large_top_group_per_level_launches(cuda_ok):
     """A 1,200-link hinge path rooted at its centre: the ~690 bodies whose subtree exceeds a group form a top group
     too large for one CTA, which runs one launch per level (up and down) between the bottom-group launches."""
