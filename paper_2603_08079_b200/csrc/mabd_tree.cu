@@ -117,9 +117,9 @@ __device__ const double kZeroSlot[TSLOT] = {};  // the condensed block of an anc
 // Entry t of a condensed block (tri6 index < 21: Ŝ_u row r ≥ column c; 21 + r: r̂_u row r) added into the parent's
 // front record: Ŝ_u lands on the parent's diagonal block of joint u (rows pr.., packed lower), r̂_u on its
 // right-hand side. Each entry has exactly one writer (its child), after the parent's record was written.
-__device__ __forceinline__ void tree_push(const TreeArgs& a, const TMeta& m, int r, int c, bool rhs, double x) {
+__device__ __forceinline__ int64_t tree_push_at(const TMeta& m, int r, int c, bool rhs) {
   const int row = m.pr + r;
-  a.f0[m.pf + (int64_t)m.fs * (rhs ? m.pT + row : row * (row + 1) / 2 + m.pr + c)] += x;  // same group: same stride
+  return m.pf + (int64_t)m.fs * (rhs ? m.pT + row : row * (row + 1) / 2 + m.pr + c);  // same group: same stride
 }
 
 // Body b's front record (element e at f0[fo + e·fs], interleaved with the group's other records so that a thread per
@@ -326,6 +326,14 @@ __device__ __forceinline__ void tree_elim(const TreeArgs& a, int b, int lane, co
       v[i] += (lane == M || ((ci ^ cj) & ~1u) == 0u) ? x : 0.0;  // same child joint as this column
     }
   }
+  // the parent's record entries this lane will add to (static addresses, no other writer): loaded now, so the
+  // push at the end is a plain store instead of a read-modify-write on the critical path
+  const int cu = lane - N;  // this lane's column of u (0 ≤ cu < nu), or nu for the right-hand side
+  const bool pushes = u >= 0 && mp->pf >= 0 && cu >= 0 && cu <= nu;
+  double pre[6];
+#pragma unroll
+  for (int r = 0; r < 6; ++r)
+    pre[r] = (pushes && r < nu && (cu == nu || r >= cu)) ? a.f0[tree_push_at(*mp, r, cu, cu == nu)] : 0.0;
   // Pivot loop kept rolled (code size: every step runs the same instructions): the registers rotate by one row per
   // step so that the pivot row is always v[0]; after N steps, v[i] holds original row (i + N) mod MX, i.e.
   // rows N..M−1 (Ŝ_u / r̂_u) at v[0..nu) and rows 0..N−1 (W / y) at v[MX−N..MX).
@@ -343,7 +351,6 @@ __device__ __forceinline__ void tree_elim(const TreeArgs& a, int b, int lane, co
   }
   EMARK(probe && v[MX - 1] != 1e300, 43);
   if (!ok && lane == 0) treport(k, ERR_SINGULAR);
-  const int cu = lane - N;  // this lane's column of u (0 ≤ cu < nu), or nu for the right-hand side
   if (cu < 0 || cu > nu) return;
   double* ws = a.ws + mp->ws;  // y [N], W [N][nu] (row-major)
 #pragma unroll
@@ -359,7 +366,7 @@ __device__ __forceinline__ void tree_elim(const TreeArgs& a, int b, int lane, co
       const double x = v[r];
       if (cu == nu || r >= cu) {
         if (m.pf >= 0)
-          tree_push(a, m, r, cu, cu == nu, x);
+          a.f0[tree_push_at(m, r, cu, cu == nu)] = pre[r] + x;
         else
           a.Shat[TSLOT * (int64_t)u + (cu == nu ? 21 + r : tri6(r, cu))] = x;
       }
