@@ -67,7 +67,7 @@ struct TreeArgs {
   const int32_t* glev_nl;      // [levels] end of the bodies with child joints in each level (they come first)
   double* Shat;                // [K][28] child-side condensed dual block of each joint: Ŝ lower triangle (21), r̂ (6)
   double* lam;                 // [K][6]
-  double* bscr;                // [n][21]: R, δq̃ between the passes
+  double* bscr;                // [21][ld]: R, δq̃ between the passes (structure of arrays)
   double* ws;                  // per-body y, W
   double* f0;                  // per-body front records (G H_b⁻¹ Gᵀ packed lower, own right-hand side)
   const int64_t* fo_off;       // [n] record offset in f0 (−1: none)

@@ -205,11 +205,11 @@ __device__ void tree_predict_core(const TreeArgs& a, int b, double* R, double* q
     hinv_blocks(M, msc, k.ih2, H);
   double W[6];
   if (!predict_body(q, qd, M, msc, H, k.ih, k.grav, R, dqt, load_wrench(a.b, b, W))) treport(k, ERR_NONFINITE);
-  double* sc = a.bscr + 21 * (int64_t)b;
+  double* sc = a.bscr + b;  // [21][ld]: component c at sc[c·ld]
 #pragma unroll
-  for (int c = 0; c < 9; ++c) sc[c] = R[c];
+  for (int c = 0; c < 9; ++c) sc[c * ld] = R[c];
 #pragma unroll
-  for (int c = 0; c < 12; ++c) sc[9 + c] = dqt[c];
+  for (int c = 0; c < 12; ++c) sc[(9 + c) * ld] = dqt[c];
 #pragma unroll
   for (int c = 0; c < 12; ++c) qt[c] = q[c] + dqt[c];
 }
@@ -217,11 +217,11 @@ __device__ void tree_predict_core(const TreeArgs& a, int b, double* R, double* q
 // R, q̃ = qⁿ + δq̃ (bscr) and the blocks of H_b⁻¹ of body b after its stages 1-2.
 __device__ void tree_reload(const TreeArgs& a, int b, double* R, double* qt, HinvBlk& H) {
   const int64_t ld = a.b.ld;
-  const double* sc = a.bscr + 21 * (int64_t)b;
+  const double* sc = a.bscr + b;  // [21][ld]: component c at sc[c·ld]
 #pragma unroll
-  for (int c = 0; c < 9; ++c) R[c] = sc[c];
+  for (int c = 0; c < 9; ++c) R[c] = sc[c * ld];
 #pragma unroll
-  for (int c = 0; c < 12; ++c) qt[c] = a.b.q[c * ld + b] + sc[9 + c];
+  for (int c = 0; c < 12; ++c) qt[c] = a.b.q[c * ld + b] + sc[(9 + c) * ld];
   const int mid = a.b.mat_id ? a.b.mat_id[b] : 0;
   if (a.hinv_tab)
     H = a.hinv_tab[mid];
@@ -458,10 +458,10 @@ __device__ void tree_update(const TreeArgs& a, int b, const TMeta& m, const TSlo
   const int64_t ld = a.b.ld;
   const int N = nn_N(m.nn), nu = nn_nu(m.nn);
   const int32_t* pcode = a.pt_code + a.pt_off[b];
-  const double* sc = a.bscr + 21 * (int64_t)b;
+  const double* sc = a.bscr + b;  // [21][ld]: component c at sc[c·ld]
   double R[9];
 #pragma unroll
-  for (int c = 0; c < 9; ++c) R[c] = sc[c];
+  for (int c = 0; c < 9; ++c) R[c] = sc[c * ld];
   HinvBlk H;
   {
     const int mid = a.b.mat_id ? a.b.mat_id[b] : 0;
@@ -504,7 +504,7 @@ __device__ void tree_update(const TreeArgs& a, int b, const TMeta& m, const TSlo
 #pragma unroll
     for (int e = 0; e < 3; ++e) {
       const int c = 3 * kb + e;
-      const double dq = sc[9 + c] - c3[e];
+      const double dq = sc[(9 + c) * ld] - c3[e];
       a.b.q[c * ld + b] += dq;
       if (k.niter == 1)
         a.b.qd[c * ld + b] = dq * k.ih;
