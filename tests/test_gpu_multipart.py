@@ -82,6 +82,20 @@ def test_tree_parts_vs_oracle(cuda_ok, world):
     assert O.rel_err(q1, q_o) <= 1e-6
 
 
+@pytest.mark.parametrize("world", [2, 4])
+def test_tree_parts_with_middle_layer(cuda_ok, world):
+    """Depth 14 (16,383 bodies): 64 bottom subtrees split over W parts; the replicated top section has a middle
+    layer (two 31-body groups below a 1-body top) that reads the gathered root blocks. Bitwise the same as the
+    unsplit path, parity with the oracle."""
+    sc = G.cfg4_binary_tree(14)
+    q1, info = run(sc, 3, world)
+    assert info["solver"] == "tree"
+    q_single, _ = run(sc, 3, 1)
+    assert np.array_equal(q1, q_single)
+    q_o, _ = O.simulate(sc, 3)
+    assert O.rel_err(q1, q_o) <= 1e-6
+
+
 @pytest.mark.parametrize("world", [2, 3])
 def test_random_forest_parts(cuda_ok, world):
     """Random trees packed several per CTA-local group (a group has several joints into the top)."""
