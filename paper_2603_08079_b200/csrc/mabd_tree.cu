@@ -294,7 +294,8 @@ __device__ __forceinline__ void tmark_at(int slot) {  // CTA 0, mode slot range 
 //   rows ≥ N:  Ŝ_u = F_uu − F_uX F_XX⁻¹ F_Xu (lanes N..M−1),  r̂_u = r_u − F_uX F_XX⁻¹ r_X (lane M).
 // MX: the front size rounded up to a multiple of 6, so that every loop is fully unrolled (register indices).
 template <int MX>
-__device__ __forceinline__ void tree_elim(const TreeArgs& a, int b, int lane, const TMeta* mp, const TSlots& sl) {
+__device__ __forceinline__ void tree_elim(const TreeArgs& a, int b, int lane, const TMeta* mp, const TSlots& sl,
+                                          double* colbuf) {
   const StepConsts& k = a.k;
   const int nn = mp->nn, N = nn_N(nn), nu = nn_nu(nn), M = N + nu, u = mp->u;
   const double* f = a.f0 + mp->fo;
@@ -339,14 +340,26 @@ __device__ __forceinline__ void tree_elim(const TreeArgs& a, int b, int lane, co
   // rows N..M−1 (Ŝ_u / r̂_u) at v[0..nu) and rows 0..N−1 (W / y) at v[MX−N..MX).
   bool ok = true;
   for (int kk = 0; kk < N; ++kk) {
-    const double p = __shfl_sync(0xffffffffu, v[0], kk);
+    // the pivot column (lane kk) broadcast through this warp's buffer: MX/2 vector stores by one lane and
+    // MX/2 broadcast vector loads instead of 2·MX 32-bit shuffles
+    if (lane == kk) {
+#pragma unroll
+      for (int i = 0; i < MX; i += 2) *reinterpret_cast<double2*>(colbuf + i) = make_double2(v[i], v[i + 1]);
+    }
+    __syncwarp();
+    double c[MX];
+#pragma unroll
+    for (int i = 0; i < MX; i += 2) {
+      const double2 w = *reinterpret_cast<const double2*>(colbuf + i);
+      c[i] = w.x;
+      c[i + 1] = w.y;
+    }
+    __syncwarp();  // every lane has the column before the next step's pivot lane overwrites it
+    const double p = c[0];
     ok = ok && p > 0.0;
     const double t = v[0] * fast_rcp(p > 0.0 ? p : 1.0);
 #pragma unroll
-    for (int i = 1; i < MX; ++i) {  // rows beyond M are zero in every column and stay zero
-      const double c = __shfl_sync(0xffffffffu, v[i], kk);
-      v[i - 1] = v[i] - c * t;
-    }
+    for (int i = 1; i < MX; ++i) v[i - 1] = v[i] - c[i] * t;  // rows beyond M are zero and stay zero
     v[MX - 1] = t;
   }
   EMARK(probe && v[MX - 1] != 1e300, 43);
@@ -383,15 +396,16 @@ __device__ __forceinline__ void tree_elim(const TreeArgs& a, int b, int lane, co
   }
 }
 
-__device__ __forceinline__ void tree_up_warp(const TreeArgs& a, int b, int lane, const TMeta* mp, const TSlots& sl) {
+__device__ __forceinline__ void tree_up_warp(const TreeArgs& a, int b, int lane, const TMeta* mp, const TSlots& sl,
+                                             double* colbuf) {
   const int M = nn_N(mp->nn) + nn_nu(mp->nn);
   switch ((M + 5) / 6) {  // the front size rounded up to a multiple of 6 rows
     case 0:
-    case 1: tree_elim<6>(a, b, lane, mp, sl); break;
-    case 2: tree_elim<12>(a, b, lane, mp, sl); break;
-    case 3: tree_elim<18>(a, b, lane, mp, sl); break;
-    case 4: tree_elim<24>(a, b, lane, mp, sl); break;
-    default: tree_elim<30>(a, b, lane, mp, sl); break;
+    case 1: tree_elim<6>(a, b, lane, mp, sl, colbuf); break;
+    case 2: tree_elim<12>(a, b, lane, mp, sl, colbuf); break;
+    case 3: tree_elim<18>(a, b, lane, mp, sl, colbuf); break;
+    case 4: tree_elim<24>(a, b, lane, mp, sl, colbuf); break;
+    default: tree_elim<30>(a, b, lane, mp, sl, colbuf); break;
   }
   EMARK(blockIdx.x == 0 && lane == 0 && b == sl.g1 - 1 && sl.s != nullptr, 44);
   __syncwarp();
@@ -518,6 +532,7 @@ __device__ void tree_update(const TreeArgs& a, int b, const TMeta& m, const TSlo
 // per body, downward a thread per body (λ of its child joints, then stage 4).
 __global__ void __launch_bounds__(512) tree_level_kernel(TreeArgs a, int mode) {
   __shared__ TMeta sm[16];
+  __shared__ __align__(16) double colbuf[16][TREE_MAXN + 6];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, nw = blockDim.x >> 5;
   const int l = a.group0;
   const TSlots none{nullptr, 0, 0};
@@ -526,7 +541,7 @@ __global__ void __launch_bounds__(512) tree_level_kernel(TreeArgs a, int mode) {
     if (b >= a.glev_off[l + 1]) return;
     if (lane == 0) sm[warp] = tree_meta(a, b, 0, 0);
     __syncwarp();
-    tree_up_warp(a, b, lane, &sm[warp], none);
+    tree_up_warp(a, b, lane, &sm[warp], none, colbuf[warp]);
   } else {
     const int b = a.glev_off[l] + blockIdx.x * blockDim.x + threadIdx.x;
     if (b >= a.glev_off[l + 1]) return;
@@ -570,6 +585,7 @@ __global__ void __launch_bounds__(TREE_THREADS, 1) tree_group_kernel(TreeArgs a,
   const int l0 = a.glev_ptr[g], l1 = a.glev_ptr[g + 1] - 1;  // levels l ∈ [l0, l1), deepest first
   const TSlots sl{tsm, g0, g1};
   TMeta* meta = reinterpret_cast<TMeta*>(tsm + (size_t)a.cap * TSLOT);
+  double* colbuf = reinterpret_cast<double*>(meta + a.cap) + (size_t)warp * (TREE_MAXN + 6);  // pivot column
   TMARK(0);
   // one body per thread (a group has at most cap ≤ blockDim bodies): stages 1-2 and the leaves' condensed blocks,
   // then (after the leaves' slots are complete) the front records of the bodies with child joints
@@ -601,7 +617,7 @@ __global__ void __launch_bounds__(TREE_THREADS, 1) tree_group_kernel(TreeArgs a,
     for (int l = l0; l < l1; ++l) {
       const int e = a.glev_nl[l];
       if (e == a.glev_off[l]) continue;  // leaves only (uniform across the CTA)
-      for (int b = a.glev_off[l] + warp; b < e; b += nw) tree_up_warp(a, b, lane, meta + (b - g0), sl);
+      for (int b = a.glev_off[l] + warp; b < e; b += nw) tree_up_warp(a, b, lane, meta + (b - g0), sl, colbuf);
       __syncthreads();
       TMARK(2 + l - l0);
     }
@@ -641,7 +657,9 @@ __global__ void tree_unpack_kernel(TreeArgs a, int nroot) {
 constexpr size_t TREE_SMEM_MAX = 227 * 1024;  // dynamic shared memory per CTA (sm_100a opt-in maximum)
 
 // Shared memory of the group kernel: slots and metadata for cap bodies.
-size_t tree_group_smem(int cap) { return (sizeof(double) * TSLOT + sizeof(TMeta)) * (size_t)cap; }
+size_t tree_group_smem(int cap) {
+  return (sizeof(double) * TSLOT + sizeof(TMeta)) * (size_t)cap + sizeof(double) * (TREE_MAXN + 6) * (TREE_THREADS / 32);
+}
 
 template <int MODE>
 static cudaError_t launch_group(const TreeArgs& a, int g_lo, int g_hi, const TreePlan& t, cudaStream_t st,
