@@ -10,9 +10,10 @@
 // Down (root first): λ_X = F_XX⁻¹(r_X − F_Xu λ_u), then qⁿ⁺¹ = q̃ − diag₄(R)H̄⁻¹Σ±Γᵀ Rᵀλ.
 // The dual graph of a tree is chordal in this order, so the elimination has no fill (PROBE in SURVEY A12).
 //
-// Parallel schedule: a predict kernel for all bodies; bodies are grouped into CTA-local subtrees (≤ 256 bodies;
-// levels separated by __syncthreads; upward one warp per body, downward one thread per body) plus a top group
-// (bodies whose subtree is larger), whose levels run as one launch each over the whole GPU.
+// Parallel schedule: bodies are grouped into CTA-local subtrees (layer 0, ≤ cap bodies), an
+// optional middle layer of ≤ 31-body subtrees of the rest, and a top group. One CTA per group runs stages 1-2 and
+// the front records a thread per body, the upward levels a warp per body (Gauss-Jordan in registers), the
+// downward levels a thread per body, and stage 4; a top group too large for one CTA runs one launch per level.
 // Across ranks: each rank takes a contiguous block of the CTA-local subtrees, eliminates
 // them, and shares the condensed blocks (Ŝ_u, r̂_u) of the joints into the top through one all-gather; every
 // rank then solves the top levels redundantly and finishes its own subtrees.
@@ -28,16 +29,6 @@
 #include "mabd_plan.h"
 
 namespace mabd {
-
-// triangular index t → (row, column), column ≤ row, row-major over the lower triangle (lane-divergent indices:
-// computed, not looked up in constant memory, which would serialise the lanes)
-__host__ __device__ constexpr int tri_row(int t) { return t < 1 ? 0 : t < 3 ? 1 : t < 6 ? 2 : t < 10 ? 3 : t < 15 ? 4 : 5; }
-__device__ __forceinline__ void tri_rc(int t, int& r, int& c) {
-  r = (int)((sqrtf(8.0f * (float)t + 1.0f) - 1.0f) * 0.5f);
-  if ((r + 1) * (r + 2) / 2 <= t) ++r;
-  if (r * (r + 1) / 2 > t) --r;
-  c = t - r * (r + 1) / 2;
-}
 
 __device__ __forceinline__ void treport(const StepConsts& k, int32_t flag) {
   atomicOr(k.err, flag);
