@@ -105,7 +105,7 @@ __device__ __forceinline__ int elim_pos_rt(int L, int e) { return (SEG - (SEG >>
 
 // update of the surviving equation kq = 2^{L+1}·m at stride ST = 2^L (both neighbours already hold D⁻¹).
 // The level is a runtime argument: one copy of this code serves every level (instruction-cache footprint).
-__device__ __noinline__ void cr_update_rt(const CRS& s, int L, int m) {
+__device__ __forceinline__ void cr_update_rt(const CRS& s, int L, int m) {
   const int ST = 1 << L;
   const int kq = 2 * ST * m;
   const int pk = cr_pos(kq);
@@ -261,7 +261,7 @@ __device__ void cr_solve_top(const CRS& s, const StepConsts& k) {
 }
 
 // Back substitution at stride 2^L: eliminated i = 2^L·(2m+1), m = first, first+step, … < NE.
-__device__ __noinline__ void cr_bwd_one(const CRS& s, int L, int m) {
+__device__ __forceinline__ void cr_bwd_one(const CRS& s, int L, int m) {
   const int ST = 1 << L;
   const int i = ST * (2 * m + 1);
   const int pi = elim_pos_rt(L, m);
