@@ -809,20 +809,23 @@ __global__ void __launch_bounds__(CT, MABD_CHAIN_CTAS) chain_kernel(ChainArgs a)
       if (has_body) {
         double* qb = a.b.q + slot;
         double* qdb = a.b.qd + slot;
+        double dq[12];  // δq = δq̃ − correction
 #pragma unroll
         for (int kb = 0; kb < 4; ++kb) {
           double c3[3];
           mat3_vec(R, u + 3 * kb, c3);
 #pragma unroll
-          for (int e = 0; e < 3; ++e) {
-            const int r = 3 * kb + e;
-            const double dq = dqt[r] - c3[e];  // δq = δq̃ − correction
-            __stcs(qb + r * a.b.ld, q[r] + dq);
-            if (k.niter == 1)
-              __stcs(qdb + r * a.b.ld, dq * k.ih);
-            else  // K > 1: v ← v − δq/h + h·grav (launch_step in mabd_plan.cu)
-              qdb[r * a.b.ld] = qdb[r * a.b.ld] - dq * k.ih + (r >= 9 ? k.h * k.grav[r - 9] : 0.0);
-          }
+          for (int e = 0; e < 3; ++e) dq[3 * kb + e] = dqt[3 * kb + e] - c3[e];
+        }
+#pragma unroll
+        for (int r = 0; r < 12; ++r) __stcs(qb + r * a.b.ld, q[r] + dq[r]);
+        if (k.niter == 1) {  // uniform branch outside the store loops (no if-converted second path)
+#pragma unroll
+          for (int r = 0; r < 12; ++r) __stcs(qdb + r * a.b.ld, dq[r] * k.ih);
+        } else {  // K > 1: v ← v − δq/h + h·grav (launch_step in mabd_plan.cu)
+#pragma unroll
+          for (int r = 0; r < 12; ++r)
+            qdb[r * a.b.ld] = qdb[r * a.b.ld] - dq[r] * k.ih + (r >= 9 ? k.h * k.grav[r - 9] : 0.0);
         }
       }
     }
