@@ -538,6 +538,7 @@ __global__ void __launch_bounds__(CT, MABD_CHAIN_CTAS) chain_kernel(ChainArgs a)
     while (!mbar_try_wait(bar, phase)) {
     }
     phase ^= 1;
+    PH_MARK(12);
 
     // ---------------- phase 1a: staged rows → registers (slot codes, mass scale, material) and TMEM (qⁿ, q̇ⁿ)
     // per-slot scalars of the two bodies as separate registers (a runtime-indexed array would go to local memory)
@@ -569,6 +570,7 @@ __global__ void __launch_bounds__(CT, MABD_CHAIN_CTAS) chain_kernel(ChainArgs a)
     }
     tm_wait_st();
     __syncthreads();  // the staged rows are consumed: the CR rows take the equations
+    PH_MARK(13);
 
     // ---------------- phase 1b: per body predict + joint contributions
     // Equation t is assembled in place: D part of body t, rhs part, B_t; body t's contribution to equation

@@ -46,9 +46,10 @@ if hasattr(lib, "mabd_dbg_phases"):
         pass
     torch.cuda.synchronize()
     lib.mabd_dbg_phases(buf)
-    names = ["P1 body loop", "barrier", "assemble+inv", "CR (2..11)", "top+barrier", "CR back lower", "P3 update",
-             "loop/end barrier", "CR fwd lower", "CR fwd upper (w0)", "top (w0)", "CR bwd upper (w0)"]
+    names = ["P1b predict", "barrier", "assemble+inv", "CR (2..11)", "top+barrier", "CR back lower", "P3 update",
+             "loop/end barrier", "CR fwd lower", "CR fwd upper (w0)", "top (w0)", "CR bwd upper (w0)",
+             "TMA wait", "P1a staged->TMEM"]
     nseg = steps * (sc.n // 256)
-    tot = sum(buf[i] for i in range(8))
+    tot = sum(buf[i] for i in range(14))
     for i, nm in enumerate(names):
         print(f"  {nm:18s} {buf[i] / nseg:10.0f} cycles/segment  {100 * buf[i] / tot:5.1f}%")
