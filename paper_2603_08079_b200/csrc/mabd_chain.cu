@@ -202,10 +202,11 @@ __device__ __forceinline__ void cr_level_fwd(const CRS& s, int first, int step, 
 // holds D⁻¹. One barrier per level.
 template <int NT>
 __device__ __forceinline__ void cr_forward_lower(const CRS& s, int t, const StepConsts& k, bool end = true) {
-  cr_level_fwd<0>(s, t, NT, k, end);
-  __syncthreads();
-  cr_level_fwd<1>(s, t, NT, k, end);
-  __syncthreads();
+#pragma unroll 1
+  for (int L = 0; L < 2; ++L) {  // one copy of the level code (instruction-cache footprint)
+    cr_level_fwd_rt(s, L, t, NT, k, end);
+    __syncthreads();
+  }
 }
 // Upper levels (strides 4 … 128, ≤ 33 survivors) by one warp, warp-synchronous.
 __device__ __forceinline__ void cr_forward_upper(const CRS& s, int lane, const StepConsts& k, bool end = true) {
@@ -299,10 +300,11 @@ __device__ __forceinline__ void cr_backward_upper(const CRS& s, int lane) {
 }
 template <int NT>
 __device__ __forceinline__ void cr_backward_lower(const CRS& s, int t) {
-  cr_level_bwd<1>(s, t, NT);
-  __syncthreads();
-  cr_level_bwd<0>(s, t, NT);
-  __syncthreads();
+#pragma unroll 1
+  for (int L = 1; L >= 0; --L) {
+    cr_level_bwd_rt(s, L, t, NT);
+    __syncthreads();
+  }
 }
 __device__ __forceinline__ void cr_backward(const CRS& s, int t) {
   if (t < 32) cr_backward_upper(s, t);
