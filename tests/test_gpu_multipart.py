@@ -97,6 +97,20 @@ def test_tree_parts_with_middle_layer(cuda_ok, world):
 
 
 @pytest.mark.parametrize("world", [2, 3])
+def test_tree_parts_with_large_top(cuda_ok, world):
+    """A 1,200-link hinge path rooted at its centre: two bottom subtrees split over W parts, the top group too
+    large for one CTA (one launch per level) reads the gathered root blocks. Bitwise the same as the unsplit
+    path, parity with the oracle."""
+    sc = G.random_chain(1200, seed=5, npts=2, end_anchor=True, vel=0.2)
+    q1, info = run(sc, 2, world)
+    assert info["solver"] == "tree"
+    q_single, _ = run(sc, 2, 1)
+    assert np.array_equal(q1, q_single)
+    q_o, _ = O.simulate(sc, 2)
+    assert O.rel_err(q1, q_o) <= 1e-6
+
+
+@pytest.mark.parametrize("world", [2, 3])
 def test_random_forest_parts(cuda_ok, world):
     """Random trees packed several per CTA-local group (a group has several joints into the top)."""
     rng = np.random.default_rng(5)
