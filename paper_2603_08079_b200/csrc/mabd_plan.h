@@ -24,7 +24,7 @@ struct BtdLevel {
 // cap = TREE_CAP, or 2·TREE_CAP for trees large enough to give every SM a group at the larger size.
 constexpr int TREE_CAP = 256;
 constexpr int TREE_TOP_SMALL = 32;  // a top set larger than this gets a middle layer …
-constexpr int TREE_MID_CAP = 31;    // … of subtrees with at most this many bodies
+constexpr int TREE_MID_CAP = 7;     // … of subtrees with at most this many bodies (measured: 7 < 15 < 31 < 63)
 constexpr int TREE_MAXN = 24;  // max dual rows of the child joints of one body (frontal size ≤ 24 + 6)
 struct TreePlan {
   std::vector<int32_t> up_joint;     // [n] joint to the parent (−1 for a root)

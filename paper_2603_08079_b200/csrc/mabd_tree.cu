@@ -11,7 +11,7 @@
 // The dual graph of a tree is chordal in this order, so the elimination has no fill (PROBE in SURVEY A12).
 //
 // Parallel schedule: bodies are grouped into CTA-local subtrees (layer 0, ≤ cap bodies), an
-// optional middle layer of ≤ 31-body subtrees of the rest, and a top group. One CTA per group runs stages 1-2 and
+// optional middle layer of ≤ 7-body subtrees of the rest (TREE_MID_CAP), and a top group. One CTA per group runs stages 1-2 and
 // the front records a thread per body, the upward levels a warp per body (Gauss-Jordan in registers), the
 // downward levels a thread per body, and stage 4; a top group too large for one CTA runs one launch per level.
 // Across ranks: each rank takes a contiguous block of the CTA-local subtrees, eliminates

@@ -85,7 +85,7 @@ def test_tree_parts_vs_oracle(cuda_ok, world):
 @pytest.mark.parametrize("world", [2, 4])
 def test_tree_parts_with_middle_layer(cuda_ok, world):
     """Depth 14 (16,383 bodies): 64 bottom subtrees split over W parts; the replicated top section has a middle
-    layer (two 31-body groups below a 1-body top) that reads the gathered root blocks. Bitwise the same as the
+    layer (eight 7-body groups below a 7-body top) that reads the gathered root blocks. Bitwise the same as the
     unsplit path, parity with the oracle."""
     sc = G.cfg4_binary_tree(14)
     q1, info = run(sc, 3, world)

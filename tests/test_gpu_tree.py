@@ -51,8 +51,8 @@ def test_hinge_chain_uses_tree_solver(cuda_ok):
 
 
 def test_middle_layer_multi_step(cuda_ok):
-    """Depth 14 (16,383 bodies): 64 bottom groups of 255 bodies; the 63-body top set gets a middle layer (two
-    31-body groups) below a 1-body top, prepared by the bottom UP launch: 5 launches per step."""
+    """Depth 14 (16,383 bodies): 64 bottom groups of 255 bodies; the 63-body top set gets a middle layer (eight
+    7-body groups) below a 7-body top, prepared by the bottom UP launch: 5 launches per step."""
     sc = G.cfg4_binary_tree(14)
     q, _, info = gpu_run(sc, 1)
     assert info["launches_per_step"] == 5
