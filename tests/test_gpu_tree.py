@@ -43,6 +43,17 @@ def test_random_trees(cuda_ok, seed):
     check(sc, 3, expect_solver="tree")
 
 
+@pytest.mark.parametrize("max_children,hinge_frac", [(8, 0.0), (4, 1.0)])
+def test_wide_fronts(cuda_ok, max_children, hinge_frac):
+    """Wide trees: up to 7 ball-joint children (fronts of 24 rows) or 4 hinge children under a hinge (30 rows,
+    the largest front the tree solver takes): the widest register-elimination variants."""
+    # seed 2 for hinges: rooted at its centre the tree keeps ≤ 4 hinge children per body (≤ 24 child rows)
+    seed = 7 if hinge_frac == 0.0 else 2
+    sc = G.random_tree(300, seed=seed, max_children=max_children, hinge_frac=hinge_frac, vel=0.3, jitter=1e-3)
+    check(sc, 1, expect_solver="tree")
+    check(sc, 3, expect_solver="tree")
+
+
 def test_hinge_chain_uses_tree_solver(cuda_ok):
     """A path of linear hinges (6-row joints) is not a ball-joint chain: the tree solver takes it."""
     sc = G.random_chain(300, seed=3, npts=2, end_anchor=True, vel=0.2)
