@@ -172,14 +172,28 @@ __global__ void sparse_update_kernel(SparseArgs a) {
   for (int64_t j = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; j < a.n; j += (int64_t)gridDim.x * blockDim.x) {
     double v[12];
     body_apply(a, j, a.lam, v);
+    // every load before the first store (q, q̇ and δq̃ may alias as far as the compiler knows)
+    double q[12], dq[12];
 #pragma unroll
     for (int c = 0; c < 12; ++c) {
-      const double dq = a.dqt[c * ld + j] - v[c];
-      a.b.q[c * ld + j] += dq;
-      if (a.k.niter == 1)
-        a.b.qd[c * ld + j] = dq * a.k.ih;
-      else  // K > 1: v ← v − δq/h + h·grav (launch_step in mabd_plan.cu)
-        a.b.qd[c * ld + j] += -dq * a.k.ih + (c >= 9 ? a.k.h * a.k.grav[c - 9] : 0.0);
+      q[c] = a.b.q[c * ld + j];
+      dq[c] = a.dqt[c * ld + j] - v[c];
+    }
+    if (a.k.niter == 1) {
+#pragma unroll
+      for (int c = 0; c < 12; ++c) {
+        a.b.q[c * ld + j] = q[c] + dq[c];
+        a.b.qd[c * ld + j] = dq[c] * a.k.ih;
+      }
+    } else {  // K > 1: v ← v − δq/h + h·grav (launch_step in mabd_plan.cu)
+      double w[12];
+#pragma unroll
+      for (int c = 0; c < 12; ++c) w[c] = a.b.qd[c * ld + j];
+#pragma unroll
+      for (int c = 0; c < 12; ++c) {
+        a.b.q[c * ld + j] = q[c] + dq[c];
+        a.b.qd[c * ld + j] = w[c] - dq[c] * a.k.ih + (c >= 9 ? a.k.h * a.k.grav[c - 9] : 0.0);
+      }
     }
   }
 }

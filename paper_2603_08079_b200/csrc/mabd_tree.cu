@@ -502,19 +502,35 @@ __device__ void tree_update(const TreeArgs& a, int b, const TMeta& m, const TSlo
   }
   double uu[12];
   hinv_apply(H, gq, uu);
+  // every load before the first store: q, q̇ and bscr may alias as far as the compiler knows, so a load after a
+  // store would wait for it (12 serialized round trips)
+  double q[12], dq[12];
+#pragma unroll
+  for (int c = 0; c < 12; ++c) {
+    q[c] = a.b.q[c * ld + b];
+    dq[c] = sc[(9 + c) * ld];
+  }
 #pragma unroll
   for (int kb = 0; kb < 4; ++kb) {
     double c3[3];
     mat3_vec(R, uu + 3 * kb, c3);
 #pragma unroll
-    for (int e = 0; e < 3; ++e) {
-      const int c = 3 * kb + e;
-      const double dq = sc[(9 + c) * ld] - c3[e];
-      a.b.q[c * ld + b] += dq;
-      if (k.niter == 1)
-        a.b.qd[c * ld + b] = dq * k.ih;
-      else  // K > 1: v ← v − δq/h + h·grav (launch_step in mabd_plan.cu)
-        a.b.qd[c * ld + b] += -dq * k.ih + (c >= 9 ? k.h * k.grav[c - 9] : 0.0);
+    for (int e = 0; e < 3; ++e) dq[3 * kb + e] -= c3[e];  // δq = δq̃ − correction
+  }
+  if (k.niter == 1) {
+#pragma unroll
+    for (int c = 0; c < 12; ++c) {
+      a.b.q[c * ld + b] = q[c] + dq[c];
+      a.b.qd[c * ld + b] = dq[c] * k.ih;
+    }
+  } else {  // K > 1: v ← v − δq/h + h·grav (launch_step in mabd_plan.cu)
+    double v[12];
+#pragma unroll
+    for (int c = 0; c < 12; ++c) v[c] = a.b.qd[c * ld + b];
+#pragma unroll
+    for (int c = 0; c < 12; ++c) {
+      a.b.q[c * ld + b] = q[c] + dq[c];
+      a.b.qd[c * ld + b] = v[c] - dq[c] * k.ih + (c >= 9 ? k.h * k.grav[c - 9] : 0.0);
     }
   }
 }

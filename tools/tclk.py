@@ -44,3 +44,6 @@ print("elim probe (last body of CTA 0, last kernel to write):", [round((int(e[i 
 e = T[0, 0, 50:53]
 print("lambda probe (root of group 0, DOWN):", [round((int(e[i + 1]) - int(e[i])) / 1e3, 2) for i in range(2)],
       "us: λ_u load | y − Wλ_u")
+e = T[0, 0, 55:59]
+print("update probe (thread 0 of CTA 0, DOWN0):", [round((int(e[i + 1]) - int(e[i])) / 1e3, 2) for i in range(3)],
+      "us: R/H/λ_u loads | child points (λ, ȳ) | H⁻¹ apply + stores")
