@@ -287,7 +287,23 @@ __global__ void __launch_bounds__(128) mf_ea_kernel(SparseArgs a, const int32_t*
   const int32_t* map = m.ea_map + m.ea_off[c];
   const double* src = m.F + m.foff[c] + (int64_t)(nc + j) * fc + nc;
   double* dst = m.F + m.foff[node] + mapped(map, j) * f;
-  for (int i = j + threadIdx.x; i < mc; i += blockDim.x) dst[mapped(map, i)] += src[i];
+  // four entries per round, every load before the stores (dst and src may alias as far as the compiler knows)
+  const int st = blockDim.x;
+  int i = j + threadIdx.x;
+  for (; i + 3 * st < mc; i += 4 * st) {
+    int64_t d[4];
+    double x[4], y[4];
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      d[u] = mapped(map, i + u * st);
+      x[u] = src[i + u * st];
+    }
+#pragma unroll
+    for (int u = 0; u < 4; ++u) y[u] = dst[d[u]];
+#pragma unroll
+    for (int u = 0; u < 4; ++u) dst[d[u]] = y[u] + x[u];
+  }
+  for (; i < mc; i += st) dst[mapped(map, i)] += src[i];
 }
 
 // Panel step 1: Cholesky of the kb×kb diagonal block at k0, and its inverse L⁻¹ (kept per front and chunk: the
@@ -514,11 +530,18 @@ __global__ void __launch_bounds__(64) mf_syrk_kernel(SparseArgs a, const int32_t
     }
     asm volatile("cp.async.commit_group;" ::: "memory");
   };
+  // the accumulators start from the trailing block itself (every load before the first store: a final
+  // col[r] −= acc read-modify-write on possibly aliasing columns would serialize its round trips)
   double acc[8][8];
 #pragma unroll
-  for (int i = 0; i < 8; ++i)
+  for (int j = 0; j < 8; ++j) {
+    const int c = c0 + ty + 8 * j;
 #pragma unroll
-    for (int j = 0; j < 8; ++j) acc[i][j] = 0.0;
+    for (int i = 0; i < 8; ++i) {
+      const int r = r0 + tx + 8 * i;
+      acc[i][j] = (c < f && r < f && r >= c) ? F[(int64_t)c * f + r] : 0.0;
+    }
+  }
   const int nch = (kb + 15) / 16;
   stage(0, 0);
   for (int ch = 0; ch < nch; ++ch) {
@@ -540,7 +563,7 @@ __global__ void __launch_bounds__(64) mf_syrk_kernel(SparseArgs a, const int32_t
 #pragma unroll
       for (int i = 0; i < 8; ++i)
 #pragma unroll
-        for (int j = 0; j < 8; ++j) acc[i][j] = fma(av[i], bv[j], acc[i][j]);
+        for (int j = 0; j < 8; ++j) acc[i][j] = fma(-av[i], bv[j], acc[i][j]);
     }
     __syncthreads();  // this buffer is refilled two chunks later
   }
@@ -552,7 +575,7 @@ __global__ void __launch_bounds__(64) mf_syrk_kernel(SparseArgs a, const int32_t
 #pragma unroll
     for (int i = 0; i < 8; ++i) {
       const int r = r0 + tx + 8 * i;
-      if (r < f && r >= c) col[r] -= acc[i][j];
+      if (r < f && r >= c) col[r] = acc[i][j];
     }
   }
 }
