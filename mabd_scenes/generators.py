@@ -549,3 +549,67 @@ def ring(n: int = 4, seed: int = 0, vel: float = 0.3, h: float = 1e-2) -> Scene:
     sc.meta = {"topology": "net"}
     sc.validate()
     return sc
+
+
+def drop_anchors(sc: Scene) -> Scene:
+    """The same scene without its world anchors (joints with body_b = −1): input construction only."""
+    keep = sc.body_b >= 0
+    pk = np.repeat(keep, sc.npts)
+    out = sc.copy()
+    out.body_a, out.body_b, out.npts = sc.body_a[keep], sc.body_b[keep], sc.npts[keep]
+    out.ybar_a, out.ybar_b = sc.ybar_a[pk], sc.ybar_b[pk]
+    out.name = sc.name + "_free"
+    out.validate()
+    return out
+
+
+def _stretch_matrix(rng, stretch):
+    """Q·S with Q a uniform random rotation and S = U diag(exp(τu)) Uᵀ, Σu = 0 (det = 1), ‖S − I‖_F = stretch."""
+    Q = random_rotations(rng, 1)[0]
+    U = random_rotations(rng, 1)[0]
+    u = rng.standard_normal(3)
+    u -= u.mean()
+    u /= np.linalg.norm(u)
+    lo, hi = 0.0, 1.0
+    while np.linalg.norm(np.exp(hi * u) - 1.0) < stretch:
+        hi *= 2
+    for _ in range(200):
+        mid = 0.5 * (lo + hi)
+        if np.linalg.norm(np.exp(mid * u) - 1.0) < stretch:
+            lo = mid
+        else:
+            hi = mid
+    return Q @ U @ np.diag(np.exp(0.5 * (lo + hi) * u)) @ U.T
+
+
+def affine_strained_state(q: np.ndarray, stretch: float, seed: int = 0, rate: float = 0.3):
+    """A seeded strained state that keeps every joint satisfied (input construction only): the whole scene is
+    mapped by one affine map x ↦ G x with G = Q·S (``_stretch_matrix``), so A_j ← G A_j, t_j ← G t_j, and every
+    body's affine strain is ‖AᵀA − I‖ = ‖S² − I‖ (for a rigid A_j). The velocity is that of the affine motion
+    x ↦ Ġ x with Ġ = rate·(random normal 3×3): q̇_j = [Ġ A_j; Ġ t_j], so ∇C q̇ = 0 for every joint between bodies.
+    World anchors are not mapped: use it on scenes without anchors (``drop_anchors``)."""
+    rng = np.random.default_rng([_seed_base(), 9000, seed])
+    G = _stretch_matrix(rng, stretch)
+    Gd = rate * rng.standard_normal((3, 3))
+    q = np.asarray(q, dtype=np.float64)
+    n = q.shape[0]
+    A = np.swapaxes(q[:, :9].reshape(n, 3, 3), 1, 2)
+    t = q[:, 9:12]
+    q1 = pack_q(G @ A, t @ G.T)
+    qd = pack_q(Gd @ A, t @ Gd.T)
+    return q1, qd
+
+
+
+def duplicate_joint(sc: Scene, k: int) -> Scene:
+    """The same scene with joint k appended once more (a redundant joint set): input construction."""
+    off = np.concatenate([[0], np.cumsum(sc.npts)])
+    out = sc.copy()
+    out.body_a = np.append(sc.body_a, sc.body_a[k]).astype(np.int32)
+    out.body_b = np.append(sc.body_b, sc.body_b[k]).astype(np.int32)
+    out.npts = np.append(sc.npts, sc.npts[k]).astype(np.int32)
+    out.ybar_a = np.vstack([sc.ybar_a, sc.ybar_a[off[k]:off[k + 1]]])
+    out.ybar_b = np.vstack([sc.ybar_b, sc.ybar_b[off[k]:off[k + 1]]])
+    out.name = f"{sc.name}_dup{k}"
+    out.validate()
+    return out

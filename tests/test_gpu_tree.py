@@ -89,3 +89,19 @@ def test_cfg4_full_size_one_step(cuda_ok):
     assert info["solver"] == "tree" and info["n_dual_rows"] == 393207
     assert O.rel_err(q_g, q_o) <= TOL1
     assert O.constraint_residual(sc, q_g) <= 1e-10
+
+
+@pytest.mark.slow
+def test_cfg4_full_size_configured_100_steps(cuda_ok):
+    """BASELINE config 4 at full size for its configured 100 steps: 65,535 bodies, the 512-body
+    layer-0 groups, the middle layer and the 5-launch schedule the benchmark times. The trajectory is stable
+    (E = 1e10; two oracle routes stay within 8.5e-11 over 100 steps at depth 8, profiles/r01_cfg4_parity_floor.txt),
+    so the tolerance is the north star's 1e-6 and the error is printed. About 5 min of host CPU for the oracle."""
+    sc = G.cfg4_binary_tree(16)
+    q_g, _, info = gpu_run(sc, 100)
+    assert info["solver"] == "tree" and info["launches_per_step"] == 5
+    q_o, _ = O.simulate(sc, 100, route="blocklu")
+    err = O.rel_err(q_g, q_o)
+    print(f"cfg4 full size, 100 steps: err {err:.2e}, constraint residual {O.constraint_residual(sc, q_g):.2e}")
+    assert err <= TOLN
+    assert O.constraint_residual(sc, q_g) <= 1e-10

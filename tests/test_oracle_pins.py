@@ -116,6 +116,30 @@ def test_elastic_force_is_fd_gradient():
         assert np.max(np.abs(O.elastic_force_A(R0, V, mu, lam))) < 1e-12 * V * mu
 
 
+@pytest.mark.parametrize("E,nu", [(1e8, 0.3), (1e10, 0.3), (2.5e6, 0.45), (7e7, 0.0), (3e9, -0.2)])
+def test_lame_uniaxial_stress_and_pure_shear(E, nu):
+    """Pins ``lame`` against the definitions of E, ν and the shear modulus (P:267-269 names μ, λ).
+
+    Uniaxial stress: A = diag(1+ε, 1−νε, 1−νε) (R = I, F = A) must carry the stress σ = diag(Eε, 0, 0) — Young's
+    modulus is σ_xx/ε_xx under a lateral contraction of ν·ε with free (zero-traction) lateral faces. Pure shear:
+    a symmetric A = I + (γ/2)(e_x e_yᵀ + e_y e_xᵀ) must carry σ_xy = E/(2(1+ν))·γ and nothing else. The force is
+    V vec(σ) (R = I). Swapping μ and λ, or a wrong (1−2ν) or (1+ν) factor, fails one of the two.
+    """
+    mu, lam = O.lame(E, nu)
+    V, eps = 0.37, 1e-3
+    A = np.diag([1 + eps, 1 - nu * eps, 1 - nu * eps])
+    f = O.elastic_force_A(A, V, mu, lam)
+    expect = V * O.vec(np.diag([E * eps, 0.0, 0.0]))
+    assert np.max(np.abs(f - expect)) <= 1e-12 * V * E * eps
+    gam = 2e-3
+    A = np.eye(3)
+    A[0, 1] = A[1, 0] = 0.5 * gam
+    f = O.elastic_force_A(A, V, mu, lam)
+    sig = np.zeros((3, 3))
+    sig[0, 1] = sig[1, 0] = E / (2 * (1 + nu)) * gam
+    assert np.max(np.abs(f - V * O.vec(sig))) <= 1e-12 * V * E * gam
+
+
 def test_affine_force_is_minus_gradient_of_incremental_potential():
     """f_A = −∇_q [ (1/2h²)(q−q̂)ᵀM_A(q−q̂) + E_el(q) ] at q = qⁿ, q̂ = qⁿ + hq̇ⁿ + h²[0;g]."""
     rng = np.random.default_rng(4)
