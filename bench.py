@@ -65,16 +65,19 @@ def peaks():
 class ClockSampler:
     """Samples SM clock and throttle reasons every ~10 ms on a thread while the timed region runs."""
 
-    def __init__(self, index: int):
+    def __init__(self, device: int):
         self.samples, self.reasons = [], set()
         self.max_mhz = None
         self._stop = threading.Event()
         self._ok = False
-        try:
+        try:  # the NVML handle is resolved from the torch device's UUID (CUDA_VISIBLE_DEVICES may hold UUIDs)
             import pynvml
+            import torch
             pynvml.nvmlInit()
             self._nv = pynvml
-            self._h = pynvml.nvmlDeviceGetHandleByIndex(index)
+            uuid = str(torch.cuda.get_device_properties(device).uuid)
+            uuid = uuid if uuid.startswith("GPU-") else "GPU-" + uuid
+            self._h = pynvml.nvmlDeviceGetHandleByUUID(uuid)
             self.max_mhz = pynvml.nvmlDeviceGetMaxClockInfo(self._h, pynvml.NVML_CLOCK_SM)
             self._ok = True
         except Exception as e:  # pragma: no cover
@@ -226,8 +229,7 @@ def run_ours(args, rank: int, world: int, local_rank: int) -> None:
         sim.step(h, min(args.warmup, episode))
     reset()
     barrier()
-    sampler = ClockSampler(local_rank if "CUDA_VISIBLE_DEVICES" not in os.environ else int(
-        os.environ["CUDA_VISIBLE_DEVICES"].split(",")[local_rank]))
+    sampler = ClockSampler(local_rank)
     ms = 0.0
     with sampler:
         left = args.steps

@@ -93,13 +93,17 @@ typedef struct {
   int32_t newton_iters;      /* Newton iterations per step, 1..16 (0 = 1; Table 1 uses 1). Iteration i is
                                 linearised at the previous iterate (footnote P:459); K > 1 uses 96 more
                                 bytes per body of workspace and K + 2 times the launches              */
-  int32_t residual_rhs;      /* must be 1: include −C(qⁿ) in the dual rhs (footnote P:459)          */
+  int32_t residual_rhs;      /* 1 (0 = default = 1): include −C(qⁿ) in the dual rhs (footnote P:459,
+                                DESIGN.md reading A4); any other value → MABD_EINVAL                  */
   int32_t solver;            /* 0 auto | 1 chain | 2 tree | 3 sparse                               */
   int32_t rank, world;       /* multi-GPU; world = 1 → single GPU                                  */
   const void *nccl_unique_id;/* 128-byte ncclUniqueId, or NULL when world = 1                      */
   void *workspace;           /* device memory from the caller (torch), or NULL                     */
   size_t workspace_bytes;
   void *cuda_stream;         /* cudaStream_t, or NULL                                              */
+  int32_t no_graphs;         /* 0: each step is replayed as one CUDA graph captured on cuda_stream (needs a
+                                non-NULL stream; rebuilt after mabd_prefactor / mabd_set_wrench); 1: plain
+                                stream launches                                                        */
 } mabd_options;
 
 /* Topology/solver actually selected (mabd_query). */
@@ -120,6 +124,14 @@ mabd_status mabd_prefactor(mabd_handle h_, double h);
 /* Advance nsteps ≥ 0 implicit steps of size h on the handle's stream. Asynchronous apart from the
  * final error-word check described above. */
 mabd_status mabd_step(mabd_handle h_, double h, int64_t nsteps);
+
+/* Enqueue nsteps steps on the handle's stream and return without synchronising (a serving loop, or a timed
+ * region that must not contain host waits). The device error word accumulates over async calls; mabd_check (or the
+ * next mabd_step) synchronises, reports the first failing step since the last check and resets it. */
+mabd_status mabd_step_async(mabd_handle h_, double h, int64_t nsteps);
+
+/* Synchronise the handle's stream and report errors of the steps enqueued since the last check (see mabd_step). */
+mabd_status mabd_check(mabd_handle h_);
 
 /* Copy the current state out, in the caller's body order ([n][12] each; either pointer may be NULL).
  * out_on_device != 0 means the pointers are device memory. Synchronises the handle's stream. */
@@ -154,6 +166,11 @@ mabd_status mabd_nccl_unique_id(void *out, size_t bytes);
  * (SURVEY §8(e)). No device work. */
 mabd_status mabd_partition_info(const mabd_bodies *bodies, const mabd_joints *joints,
                                 const mabd_options *opts, int64_t *out, int64_t n_out);
+
+/* Host-only analysis of the sparse solver's plan for a scene (no device work; forces the sparse solver):
+ * out[0..7] = {assembly-tree fronts, levels, largest front (rows), front storage (doubles), flops of one
+ * numeric factorization (fp64, SYRK counted as the full square), task-list ints, launches per step, dual rows}. */
+mabd_status mabd_sparse_plan_stats(const mabd_bodies *bodies, const mabd_joints *joints, double *out);
 
 /* Statistics of the last mabd_step call: iterative-refinement passes of the sparse solver's direct dual solve
  * (0 for the chain and tree solvers). Synchronises the handle's stream. */

@@ -19,7 +19,8 @@ STATUS = {0: "MABD_OK", 1: "MABD_EINVAL", 2: "MABD_ESTATE", 3: "MABD_ENOMEM", 4:
           6: "MABD_ESINGULAR", 7: "MABD_ENONFINITE", 8: "MABD_EUNSUPPORTED"}
 SOLVERS = {0: "auto", 1: "chain", 2: "tree", 3: "sparse"}
 
-EXPORTED = ["mabd_workspace_size", "mabd_create", "mabd_prefactor", "mabd_step", "mabd_get_state",
+EXPORTED = ["mabd_workspace_size", "mabd_create", "mabd_prefactor", "mabd_step", "mabd_step_async", "mabd_check",
+            "mabd_get_state",
             "mabd_set_state", "mabd_set_wrench", "mabd_query", "mabd_solver_stats", "mabd_nccl_unique_id", "mabd_partition_info",
             "mabd_destroy", "mabd_last_error"]
 
@@ -48,7 +49,7 @@ class _Options(ctypes.Structure):
     _fields_ = [("newton_iters", ctypes.c_int32), ("residual_rhs", ctypes.c_int32), ("solver", ctypes.c_int32),
                 ("rank", ctypes.c_int32), ("world", ctypes.c_int32), ("nccl_unique_id", ctypes.c_void_p),
                 ("workspace", ctypes.c_void_p), ("workspace_bytes", ctypes.c_size_t),
-                ("cuda_stream", ctypes.c_void_p)]
+                ("cuda_stream", ctypes.c_void_p), ("no_graphs", ctypes.c_int32)]
 
 
 _lib = None
@@ -70,6 +71,8 @@ def load_library(path: str = LIB_PATH) -> ctypes.CDLL:
                                 ctypes.POINTER(H)]
     lib.mabd_prefactor.argtypes = [H, ctypes.c_double]
     lib.mabd_step.argtypes = [H, ctypes.c_double, ctypes.c_int64]
+    lib.mabd_step_async.argtypes = [H, ctypes.c_double, ctypes.c_int64]
+    lib.mabd_check.argtypes = [H]
     lib.mabd_get_state.argtypes = [H, ctypes.c_void_p, ctypes.c_void_p, ctypes.c_int]
     lib.mabd_set_state.argtypes = [H, ctypes.c_void_p, ctypes.c_void_p, ctypes.c_int]
     lib.mabd_set_wrench.argtypes = [H, ctypes.c_void_p, ctypes.c_int]
@@ -127,7 +130,7 @@ def partition_info(scene, world: int, rank: int) -> dict:
                 _ptr(k["poisson"]), None, (ctypes.c_double * 3)(*[float(x) for x in np.asarray(scene.gravity)]))
     j = _Joints(K, _ptr(k["body_a"], _ip), _ptr(k["body_b"], _ip), _ptr(k["npts"], _ip), _ptr(k["ybar_a"]),
                 _ptr(k["ybar_b"]))
-    o = _Options(1, 1, 0, int(rank), int(world), None, None, 0, None)
+    o = _Options(1, 1, 0, int(rank), int(world), None, None, 0, None, 0)
     out = (ctypes.c_int64 * 20)()
     st = lib.mabd_partition_info(ctypes.byref(b), ctypes.byref(j), ctypes.byref(o), out, 20)
     if st != MABD_OK:
@@ -141,13 +144,14 @@ def partition_info(scene, world: int, rank: int) -> dict:
 class Simulator:
     """One libmabd handle: ``mabd_create`` → ``prefactor(h)`` → ``step(h, n)`` → ``get_state()``.
 
-    Device memory is a torch ``uint8`` workspace tensor owned by this object; the stream is torch's current
-    stream on ``device`` unless one is given.
+    Device memory is a torch ``uint8`` workspace tensor owned by this object. The stream is the one given, else
+    torch's current stream on ``device`` if that is not the default stream, else a dedicated stream (the library
+    replays each step as a CUDA graph captured on it; ``no_graphs=True`` launches plainly).
     """
 
     def __init__(self, q0, qd0, mbar, volume, youngs, poisson, gravity, body_a, body_b, npts, ybar_a, ybar_b,
                  solver: int = 0, device: Optional[int] = None, stream=None, world: int = 1, rank: int = 0,
-                 nccl_id: Optional[bytes] = None, newton_iters: int = 1):
+                 nccl_id: Optional[bytes] = None, newton_iters: int = 1, no_graphs: bool = False):
         import torch
 
         self._lib = load_library()
@@ -170,10 +174,12 @@ class Simulator:
                                _ptr(k["ybar_a"]), _ptr(k["ybar_b"]))
         with torch.cuda.device(self.device):
             self._stream = stream if stream is not None else torch.cuda.current_stream(self.device)
+            if self._stream.cuda_stream == 0:  # the legacy default stream cannot be captured into a graph
+                self._stream = torch.cuda.Stream(device=self.device)
             self._nccl_id = ctypes.create_string_buffer(bytes(nccl_id), 128) if nccl_id is not None else None
             opts = _Options(int(newton_iters), 1, int(solver), int(rank), int(world),
                             ctypes.cast(self._nccl_id, ctypes.c_void_p) if self._nccl_id is not None else None,
-                            None, 0, ctypes.c_void_p(self._stream.cuda_stream))
+                            None, 0, ctypes.c_void_p(self._stream.cuda_stream), int(bool(no_graphs)))
             nbytes = ctypes.c_size_t(0)
             self._check(self._lib.mabd_workspace_size(ctypes.byref(self._bodies), ctypes.byref(self._joints),
                                                       ctypes.byref(opts), ctypes.byref(nbytes)), None)
@@ -207,6 +213,13 @@ class Simulator:
 
     def step(self, h: float, nsteps: int = 1) -> None:
         self._check(self._lib.mabd_step(self._h, float(h), int(nsteps)), self._h)
+
+    def step_async(self, h: float, nsteps: int = 1) -> None:
+        """Enqueue steps without a host wait; errors surface at ``check()`` or the next ``step()``."""
+        self._check(self._lib.mabd_step_async(self._h, float(h), int(nsteps)), self._h)
+
+    def check(self) -> None:
+        self._check(self._lib.mabd_check(self._h), self._h)
 
     def query(self) -> dict:
         s, l, nb, nr = ctypes.c_int32(), ctypes.c_int32(), ctypes.c_int64(), ctypes.c_int64()
@@ -242,6 +255,8 @@ class Simulator:
         if not on_dev:
             q = None if q is None else (q if isinstance(q, torch.Tensor) else np.ascontiguousarray(q, dtype=np.float64))
             qd = None if qd is None else (qd if isinstance(qd, torch.Tensor) else np.ascontiguousarray(qd, dtype=np.float64))
+        if on_dev:  # the tensors were written on torch's current stream; the library reads on its own
+            self._stream.wait_stream(torch.cuda.current_stream(self.device))
         self._check(self._lib.mabd_set_state(self._h, self._addr(q), self._addr(qd), 1 if on_dev else 0), self._h)
 
     def set_wrench(self, W=None) -> None:
@@ -254,6 +269,8 @@ class Simulator:
         on_dev = isinstance(W, torch.Tensor) and W.is_cuda
         if not on_dev and not isinstance(W, torch.Tensor):
             W = np.ascontiguousarray(W, dtype=np.float64).reshape(self.n, 6)
+        if on_dev:
+            self._stream.wait_stream(torch.cuda.current_stream(self.device))
         self._check(self._lib.mabd_set_wrench(self._h, self._addr(W), 1 if on_dev else 0), self._h)
 
     @staticmethod

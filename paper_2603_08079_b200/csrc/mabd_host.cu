@@ -37,8 +37,12 @@ struct mabd_ctx {
   size_t ws_bytes = 0;
   bool own_ws = false;
   DevPtrs d;
-  int32_t* h_err = nullptr;  // pinned [2]
+  int32_t* h_err = nullptr;  // pinned [4]
   int64_t steps_done = 0;
+  int64_t steps_pending = 0;   // enqueued by mabd_step_async since the last mabd_check
+  bool use_graphs = true;      // options.no_graphs == 0 and a non-default stream
+  cudaGraphExec_t graph = nullptr;
+  double graph_h = 0.0;
 };
 
 static mabd_status fail(mabd_ctx* c, mabd_status st, const char* fmt, ...) {
@@ -52,6 +56,14 @@ static mabd_status fail(mabd_ctx* c, mabd_status st, const char* fmt, ...) {
   else
     g_thread_err = buf;
   return st;
+}
+
+// One step as a CUDA graph (captured on the handle's stream at the first step after create / prefactor /
+// set_wrench, replayed nsteps times): the plan's launch sequence plus the step_end node. Kernel arguments (h, the
+// pointers, the wrench) are baked into the graph, so it is rebuilt when any of them changes.
+static void drop_graph(mabd_ctx* c) {
+  if (c->graph) cudaGraphExecDestroy(c->graph);
+  c->graph = nullptr;
 }
 
 #define CUDA_TRY(c, expr)                                                                          \
@@ -107,11 +119,13 @@ mabd_status mabd_create(const mabd_bodies* bodies, const mabd_joints* joints, co
     c->own_ws = true;
     c->ws_bytes = c->plan.workspace_bytes;
   }
-  e = cudaMallocHost(&c->h_err, 2 * sizeof(int32_t));
+  c->use_graphs = c->stream != nullptr && !(opts && opts->no_graphs);
+  e = cudaMallocHost(&c->h_err, 4 * sizeof(int32_t));
   if (e == cudaSuccess) e = chain_kernels_init();
   if (e == cudaSuccess && c->plan.solver == MABD_SOLVER_SPARSE) e = sparse_init();
   if (e == cudaSuccess && c->plan.solver == MABD_SOLVER_TREE) e = tree_init();
   if (e == cudaSuccess) e = upload_plan(c->plan, c->ws, c->stream, &c->d);
+  if (e == cudaSuccess) e = reset_err(c->d, c->stream);
   if (e == cudaSuccess) e = cudaStreamSynchronize(c->stream);
   if (e != cudaSuccess) {
     mabd_destroy(c);
@@ -138,13 +152,37 @@ mabd_status mabd_prefactor(mabd_handle c, double h) {
   if (!(h > 0.0) || !std::isfinite(h)) return fail(c, MABD_EINVAL, "h must be > 0 (got %g)", h);
   CUDA_TRY(c, cudaSetDevice(c->device));
   CUDA_TRY(c, prefactor_device(c->plan, c->d, h, c->stream));
+  drop_graph(c);
   c->prefactored = true;
   c->h_pref = h;
   return MABD_OK;
 }
 
-mabd_status mabd_step(mabd_handle c, double h, int64_t nsteps) {
-  if (!c) return fail(nullptr, MABD_EINVAL, "NULL handle");
+static cudaError_t enqueue_one_step(mabd_ctx* c, double h, int32_t s) {
+  cudaError_t e = launch_step(c->plan, c->d, h, s, c->stream);
+  if (e == cudaSuccess) e = launch_step_end(c->d, c->stream);
+  return e;
+}
+
+static cudaError_t build_graph(mabd_ctx* c, double h) {
+  drop_graph(c);
+  cudaError_t e = cudaStreamBeginCapture(c->stream, cudaStreamCaptureModeThreadLocal);
+  if (e != cudaSuccess) return e;
+  const cudaError_t e1 = enqueue_one_step(c, h, 0);
+  cudaGraph_t g = nullptr;
+  e = cudaStreamEndCapture(c->stream, &g);
+  if (e1 != cudaSuccess || e != cudaSuccess) {
+    if (g) cudaGraphDestroy(g);
+    return e1 != cudaSuccess ? e1 : e;
+  }
+  e = cudaGraphInstantiate(&c->graph, g, 0);
+  cudaGraphDestroy(g);
+  if (e != cudaSuccess) c->graph = nullptr;
+  c->graph_h = h;
+  return e;
+}
+
+static mabd_status enqueue_steps(mabd_ctx* c, double h, int64_t nsteps) {
   if (!c->prefactored) return fail(c, MABD_ESTATE, "mabd_step before mabd_prefactor");
   if (!(h > 0.0) || !std::isfinite(h)) return fail(c, MABD_EINVAL, "h must be > 0 (got %g)", h);
   if (nsteps < 0) return fail(c, MABD_EINVAL, "nsteps < 0");
@@ -154,19 +192,59 @@ mabd_status mabd_step(mabd_handle c, double h, int64_t nsteps) {
     mabd_status st = mabd_prefactor(c, h);
     if (st != MABD_OK) return st;
   }
-  CUDA_TRY(c, reset_err(c->d, c->stream));
-  for (int64_t s = 0; s < nsteps; ++s) {
-    CUDA_TRY(c, launch_step(c->plan, c->d, h, (int32_t)std::min<int64_t>(s, INT_MAX - 1), c->stream));
+  nccl_take_step_error();
+  const bool graphs = c->use_graphs;
+  if (graphs && (!c->graph || c->graph_h != h)) {
+    const cudaError_t e = build_graph(c, h);
+    if (e != cudaSuccess) {
+      if (const int rc = nccl_take_step_error()) return fail(c, MABD_ENCCL, "NCCL exchange (capture): %s", nccl_err(rc));
+      return fail(c, MABD_ECUDA, "step graph capture: %s", cudaGetErrorString(e));
+    }
   }
-  CUDA_TRY(c, cudaMemcpyAsync(c->h_err, c->d.err, 2 * sizeof(int32_t), cudaMemcpyDeviceToHost, c->stream));
-  CUDA_TRY(c, cudaStreamSynchronize(c->stream));
-  c->steps_done += nsteps;
-  if (c->h_err[0] & ERR_NONFINITE)
-    return fail(c, MABD_ENONFINITE, "non-finite state or det(A) <= 1e-9 at step %d of this call", c->h_err[1]);
-  if (c->h_err[0] & ERR_SINGULAR)
-    return fail(c, MABD_ESINGULAR, "dual matrix not positive definite (redundant joints?) at step %d of this call",
-                c->h_err[1]);
+  for (int64_t s = 0; s < nsteps; ++s) {
+    const cudaError_t e = graphs ? cudaGraphLaunch(c->graph, c->stream)
+                                 : enqueue_one_step(c, h, (int32_t)std::min<int64_t>(s, INT_MAX - 1));
+    if (e != cudaSuccess) {
+      if (const int rc = nccl_take_step_error())
+        return fail(c, MABD_ENCCL, "NCCL exchange in step %lld of this call: %s", (long long)s, nccl_err(rc));
+      return fail(c, MABD_ECUDA, "launch_step (step %lld of this call): %s", (long long)s, cudaGetErrorString(e));
+    }
+  }
+  c->steps_pending += nsteps;
   return MABD_OK;
+}
+
+mabd_status mabd_check(mabd_handle c) {
+  if (!c) return fail(nullptr, MABD_EINVAL, "NULL handle");
+  CUDA_TRY(c, cudaSetDevice(c->device));
+  CUDA_TRY(c, cudaMemcpyAsync(c->h_err, c->d.err, 4 * sizeof(int32_t), cudaMemcpyDeviceToHost, c->stream));
+  CUDA_TRY(c, cudaStreamSynchronize(c->stream));
+  const int64_t pending = c->steps_pending;
+  c->steps_done += pending;
+  c->steps_pending = 0;
+  const int32_t flags = c->h_err[0], at = c->h_err[2];
+  CUDA_TRY(c, reset_err(c->d, c->stream));
+  if (flags & ERR_NONFINITE)
+    return fail(c, MABD_ENONFINITE, "non-finite state or det(A) <= 1e-9 at step %d of the %lld steps enqueued",
+                at, (long long)pending);
+  if (flags & ERR_SINGULAR)
+    return fail(c, MABD_ESINGULAR,
+                "dual matrix not positive definite (redundant joints?) at step %d of the %lld steps enqueued", at,
+                (long long)pending);
+  return MABD_OK;
+}
+
+mabd_status mabd_step_async(mabd_handle c, double h, int64_t nsteps) {
+  if (!c) return fail(nullptr, MABD_EINVAL, "NULL handle");
+  return enqueue_steps(c, h, nsteps);
+}
+
+mabd_status mabd_step(mabd_handle c, double h, int64_t nsteps) {
+  if (!c) return fail(nullptr, MABD_EINVAL, "NULL handle");
+  const mabd_status st = enqueue_steps(c, h, nsteps);
+  if (st != MABD_OK) return st;
+  if (nsteps == 0 && c->steps_pending == 0) return MABD_OK;
+  return mabd_check(c);
 }
 
 mabd_status mabd_get_state(mabd_handle c, double* q_out, double* qd_out, int out_on_device) {
@@ -237,6 +315,7 @@ mabd_status mabd_set_wrench(mabd_handle c, const double* W, int in_on_device) {
     if (!in_on_device) CUDA_TRY(c, cudaStreamSynchronize(c->stream));
     wr = c->d.wr_buf;
   }
+  drop_graph(c);   // the wrench pointer is a kernel argument baked into the step graph
   c->d.b.wr = wr;  // every solver reads the wrench through its copy of the body arrays
   c->d.tree.b.wr = wr;
   c->d.sparse.b.wr = wr;
@@ -247,7 +326,7 @@ mabd_status mabd_query(mabd_handle c, int32_t* solver, int32_t* launches_per_ste
                        int64_t* n_dual_rows) {
   if (!c) return fail(nullptr, MABD_EINVAL, "NULL handle");
   if (solver) *solver = c->plan.solver;
-  if (launches_per_step) *launches_per_step = c->plan.launches_per_step;
+  if (launches_per_step) *launches_per_step = c->plan.launches_per_step + 1;  // + the step_end node
   if (n_bodies) *n_bodies = c->plan.n;
   if (n_dual_rows) *n_dual_rows = c->plan.n_dual_rows;
   return MABD_OK;
@@ -313,6 +392,7 @@ mabd_status mabd_destroy(mabd_handle c) {
   if (!c) return MABD_OK;
   cudaSetDevice(c->device);
   if (c->stream) cudaStreamSynchronize(c->stream);
+  drop_graph(c);
   nccl_comm_destroy(c->d.nccl_comm);
   if (c->own_ws && c->ws) cudaFree(c->ws);
   if (c->h_err) cudaFreeHost(c->h_err);

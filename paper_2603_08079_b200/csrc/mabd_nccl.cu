@@ -38,7 +38,18 @@ struct Api {
   ErrStrFn err_str = nullptr;
 } g_api;
 std::mutex g_mu;
+thread_local int g_step_rc = 0;  // first NCCL failure inside a step's launch sequence (nccl_take_step_error)
 }  // namespace
+
+int nccl_step_failed(int rc) {
+  if (rc != 0 && g_step_rc == 0) g_step_rc = rc;
+  return rc;
+}
+int nccl_take_step_error() {
+  const int rc = g_step_rc;
+  g_step_rc = 0;
+  return rc;
+}
 
 bool nccl_load(std::string* err) {
   std::lock_guard<std::mutex> lk(g_mu);

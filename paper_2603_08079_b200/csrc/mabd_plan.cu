@@ -62,6 +62,8 @@ static mabd_status validate(const mabd_bodies* B, const mabd_joints* J, const ma
     if (o->newton_iters < 0 || o->newton_iters > 16) return *msg = "newton_iters must be in [0, 16]", MABD_EINVAL;
     if (o->world > 1 && (o->rank < 0 || o->rank >= o->world)) return *msg = "rank outside [0, world)", MABD_EINVAL;
     if (o->world > 256) return *msg = "world > 256", MABD_EINVAL;
+    if (o->residual_rhs != 0 && o->residual_rhs != 1)
+      return *msg = "residual_rhs must be 1 (0 = default = 1): -C(qn) is always in the dual rhs", MABD_EINVAL;
   }
   for (int64_t i = 0; i < B->n; ++i) {
     const double* m = B->mbar + 10 * i;
@@ -463,7 +465,7 @@ mabd_status build_plan(const mabd_bodies* B, const mabd_joints* J, const mabd_op
   f.hinv = take(sizeof(HinvBlk) * p->mats.size());
   f.perm = take(sizeof(int64_t) * B->n);
   f.io = take(sizeof(double) * 24 * B->n);
-  f.err = take(sizeof(int32_t) * 2);
+  f.err = take(sizeof(int32_t) * 4);
   if (p->solver == MABD_SOLVER_CHAIN) {
     f.slot_info = take(sizeof(uint32_t) * (ld + 16));  // + padding: segments stage SEG + 4 slot codes
     f.geo = take(sizeof(double) * p->geo.size());
@@ -679,13 +681,29 @@ cudaError_t prefactor_device(const Plan& p, const DevPtrs& d, double h, cudaStre
   return launch_hinv_table(d.mats, (int)p.mats.size(), 1.0 / (h * h), d.hinv, st);
 }
 
+// Device error word: [0] flags (ERR_*, set by any kernel), [1] step index as the kernels saw it (unused by the host),
+// [2] first step after which [0] was non-zero (set by step_end_kernel), [3] steps enqueued since the last reset.
 __global__ void err_reset_kernel(int32_t* e) {
   e[0] = 0;
   e[1] = INT_MAX;
+  e[2] = INT_MAX;
+  e[3] = 0;
 }
 
 cudaError_t reset_err(const DevPtrs& d, cudaStream_t st) {
   err_reset_kernel<<<1, 1, 0, st>>>(d.err);
+  return cudaGetLastError();
+}
+
+// The last node of every step (also inside a captured graph, where the step index cannot be a kernel argument):
+// attributes a new error to this step and counts it.
+__global__ void step_end_kernel(int32_t* e) {
+  if (e[0] != 0 && e[2] == INT_MAX) e[2] = e[3];
+  e[3] += 1;
+}
+
+cudaError_t launch_step_end(const DevPtrs& d, cudaStream_t st) {
+  step_end_kernel<<<1, 1, 0, st>>>(d.err);
   return cudaGetLastError();
 }
 
@@ -722,7 +740,7 @@ static cudaError_t launch_step_parts(const Plan& p, const DevPtrs& d, ChainArgs 
   }
   if (p.use_nccl) {
     const int rc = nccl_allgather_doubles(d.nccl_comm, (double*)d.all_tops, sizeof(Top) / sizeof(double), p.part_lo, st);
-    if (rc != 0) return cudaErrorUnknown;
+    if (rc != 0) return nccl_step_failed(rc), cudaErrorUnknown;  // mabd_step reports MABD_ENCCL
   }
   {
     BtdArgs b{};

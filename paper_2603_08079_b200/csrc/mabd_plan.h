@@ -181,12 +181,17 @@ int nccl_bcast_ranges(void* comm, double* base, const std::vector<std::pair<int6
                       int64_t ld, int ncomp, cudaStream_t st);
 void nccl_comm_destroy(void* comm);
 const char* nccl_err(int code);
+// A step's launch sequence that hits an NCCL failure records its code (nccl_step_failed) and returns
+// cudaErrorUnknown; mabd_step then takes the code (nccl_take_step_error, 0 if none) and reports MABD_ENCCL.
+int nccl_step_failed(int rc);
+int nccl_take_step_error();
 
 mabd_status build_plan(const mabd_bodies* bodies, const mabd_joints* joints, const mabd_options* opts, Plan* p,
                        std::string* msg);
 cudaError_t upload_plan(const Plan& p, char* ws, cudaStream_t st, DevPtrs* d);
 cudaError_t prefactor_device(const Plan& p, const DevPtrs& d, double h, cudaStream_t st);
 cudaError_t reset_err(const DevPtrs& d, cudaStream_t st);
+cudaError_t launch_step_end(const DevPtrs& d, cudaStream_t st);
 cudaError_t launch_step(const Plan& p, const DevPtrs& d, double h, int32_t step, cudaStream_t st);
 
 // tree solver (mabd_tree.cu)

@@ -1472,8 +1472,8 @@ cudaError_t sparse_upload(const Plan& p, char* ws, cudaStream_t st, DevPtrs* d) 
 }  // namespace mabd
 
 // Developer introspection (not part of include/mabd.h): symbolic statistics of the sparse plan of a scene.
-// out[0..7] = nodes, levels, max front, front doubles, factor flops, task ints, launches per step, dual rows.
-extern "C" int mabd_dbg_sparse_stats(const mabd_bodies* B, const mabd_joints* J, double* out) {
+// See include/mabd.h (mabd_sparse_plan_stats).
+extern "C" mabd_status mabd_sparse_plan_stats(const mabd_bodies* B, const mabd_joints* J, double* out) {
   mabd::Plan p;
   std::string msg;
   mabd_options o{};
@@ -1482,7 +1482,7 @@ extern "C" int mabd_dbg_sparse_stats(const mabd_bodies* B, const mabd_joints* J,
   o.solver = MABD_SOLVER_SPARSE;
   o.world = 1;
   const mabd_status st = mabd::build_plan(B, J, &o, &p, &msg);
-  if (st != MABD_OK) return (int)st;
+  if (st != MABD_OK) return st;
   const mabd::SparsePlan& s = p.sparse;
   out[0] = s.nnode;
   out[1] = (double)s.levels.size();
@@ -1492,5 +1492,5 @@ extern "C" int mabd_dbg_sparse_stats(const mabd_bodies* B, const mabd_joints* J,
   out[5] = (double)s.tasks.size();
   out[6] = p.launches_per_step;
   out[7] = (double)p.n_dual_rows;
-  return 0;
+  return MABD_OK;
 }

@@ -704,7 +704,7 @@ cudaError_t tree_step(const Plan& p, const DevPtrs& d, const StepConsts& k, cuda
     }
     if (split && t.rpp > 0) {
       const int rc = nccl_allgather_doubles(d.nccl_comm, a.xbuf, (size_t)t.rpp * TSLOT, t.part, st);
-      if (rc != 0) return cudaErrorUnknown;
+      if (rc != 0) return nccl_step_failed(rc), cudaErrorUnknown;  // mabd_step reports MABD_ENCCL
     }
     const int nroot = t.root_off[t.n_bottom];
     if (nroot > 0) tree_unpack_kernel<<<(unsigned)((nroot * TSLOT + 255) / 256), 256, 0, st>>>(a, nroot);

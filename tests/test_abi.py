@@ -104,7 +104,7 @@ def _sparse_stats(lib, sc):
     j = _Joints(sc.n_joints, _ptr(sc.body_a, _ip), _ptr(sc.body_b, _ip), _ptr(sc.npts, _ip), _ptr(sc.ybar_a),
                 _ptr(sc.ybar_b))
     out = (ctypes.c_double * 8)()
-    assert lib.mabd_dbg_sparse_stats(ctypes.byref(b), ctypes.byref(j), out) == 0
+    assert lib.mabd_sparse_plan_stats(ctypes.byref(b), ctypes.byref(j), out) == 0
     return dict(zip(["nodes", "levels", "max_front", "front_doubles", "flops", "tasks", "launches", "rows"], out))
 
 

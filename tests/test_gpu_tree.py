@@ -20,12 +20,13 @@ def test_cfg4_recipe_small(cuda_ok, depth):
 
 
 def test_cfg4_recipe_with_top_group(cuda_ok):
-    """Depth 10 (1,023 bodies): four 255-body bottom groups plus a 3-body top group (one CTA): 3 launches/step."""
+    """Depth 10 (1,023 bodies): four 255-body bottom groups plus a 3-body top group (one CTA): 3 solver launches/step."""
     sc = G.cfg4_binary_tree(10)
     check(sc, 1, expect_solver="tree")
     check(sc, 5, expect_solver="tree")
     q, _, info = gpu_run(sc, 5)
-    assert info["launches_per_step"] == 3   # bottom groups up, top group (up and down), bottom groups down
+    # bottom groups up, top group (up and down), bottom groups down, + the step_end node
+    assert info["launches_per_step"] == 4
     assert O.constraint_residual(sc, q) <= 1e-10
 
 
@@ -66,7 +67,7 @@ def test_middle_layer_multi_step(cuda_ok):
     7-body groups) below a 7-body top, prepared by the bottom UP launch: 5 launches per step."""
     sc = G.cfg4_binary_tree(14)
     q, _, info = gpu_run(sc, 1)
-    assert info["launches_per_step"] == 5
+    assert info["launches_per_step"] == 6  # 5 solver launches + the step_end node
     check(sc, 1, expect_solver="tree")
     check(sc, 8, expect_solver="tree")
 
@@ -99,7 +100,7 @@ def test_cfg4_full_size_configured_100_steps(cuda_ok):
     so the tolerance is the north star's 1e-6 and the error is printed. About 5 min of host CPU for the oracle."""
     sc = G.cfg4_binary_tree(16)
     q_g, _, info = gpu_run(sc, 100)
-    assert info["solver"] == "tree" and info["launches_per_step"] == 5
+    assert info["solver"] == "tree" and info["launches_per_step"] == 6
     q_o, _ = O.simulate(sc, 100, route="blocklu")
     err = O.rel_err(q_g, q_o)
     print(f"cfg4 full size, 100 steps: err {err:.2e}, constraint residual {O.constraint_residual(sc, q_g):.2e}")
