@@ -613,3 +613,54 @@ def duplicate_joint(sc: Scene, k: int) -> Scene:
     out.name = f"{sc.name}_dup{k}"
     out.validate()
     return out
+
+
+def reframe_scene(sc: Scene, seed: int = 0, rotate: bool = True, offset: float = 0.3) -> Scene:
+    """The same physical scene with every body expressed in a seeded general material frame (input construction
+    only): x̄_u = P x̄ + d with P a uniform random rotation (if ``rotate``) and d uniform in ±``offset`` × the body's
+    half-extent (from M̄). Then A_u = A Pᵀ, t_u = t − A Pᵀ d (velocities alike), ȳ_u = P ȳ + d, and
+    M̄_u = T̄ M̄ T̄ᵀ with T̄ = [[P, d], [0, 1]], which is a full SPD 4×4 (non-central, non-principal).
+    Returns the new scene; ``frames`` attribute = (P, d) per body for mapping states back."""
+    rng = np.random.default_rng([_seed_base(), 9100, seed])
+    n = sc.n
+    P = random_rotations(rng, n) if rotate else np.broadcast_to(np.eye(3), (n, 3, 3)).copy()
+    Mb = np.zeros((n, 4, 4))
+    iu = [(0, 0), (0, 1), (0, 2), (0, 3), (1, 1), (1, 2), (1, 3), (2, 2), (2, 3), (3, 3)]
+    for k, (i, j) in enumerate(iu):
+        Mb[:, i, j] = Mb[:, j, i] = sc.mbar[:, k]
+    half = np.sqrt(3.0 * np.maximum(np.diagonal(Mb, axis1=1, axis2=2)[:, :3], 0) / Mb[:, 3:4, 3])  # box: a/2
+    d = offset * half * rng.uniform(-1, 1, size=(n, 3))
+    T = np.zeros((n, 4, 4))
+    T[:, :3, :3] = P
+    T[:, :3, 3] = d
+    T[:, 3, 3] = 1.0
+    Mu = T @ Mb @ np.swapaxes(T, 1, 2)
+    out = sc.copy()
+    out.mbar = np.stack([Mu[:, i, j] for (i, j) in iu], axis=1)
+
+    def to_user(q):
+        A = np.swapaxes(q[:, :9].reshape(n, 3, 3), 1, 2)
+        Au = A @ np.swapaxes(P, 1, 2)
+        return pack_q(Au, q[:, 9:12] - np.einsum("nij,nj->ni", Au, d))
+
+    out.q0 = to_user(sc.q0)
+    out.qd0 = to_user(sc.qd0)
+    pa = np.repeat(sc.body_a, sc.npts)
+    pb = np.repeat(sc.body_b, sc.npts)
+    out.ybar_a = np.einsum("pij,pj->pi", P[pa], sc.ybar_a) + d[pa]
+    yb = sc.ybar_b.copy()
+    m = pb >= 0
+    yb[m] = np.einsum("pij,pj->pi", P[pb[m]], sc.ybar_b[m]) + d[pb[m]]
+    out.ybar_b = yb
+    out.name = sc.name + "_reframed"
+    out.frames = (P, d)
+    out.validate()
+    return out
+
+
+def frame_to_canonical(q: np.ndarray, frames) -> np.ndarray:
+    """Map a state of ``reframe_scene``'s bodies back to the original frames: A = A_u P, t = t_u + A_u d."""
+    P, d = frames
+    n = q.shape[0]
+    Au = np.swapaxes(q[:, :9].reshape(n, 3, 3), 1, 2)
+    return pack_q(Au @ P, q[:, 9:12] + np.einsum("nij,nj->ni", Au, d))

@@ -621,7 +621,7 @@ __global__ void __launch_bounds__(CT, MABD_CHAIN_CTAS) chain_kernel(ChainArgs a)
         const Material M = a.b.mats[mdb];
         const double ms = msb;
         const int md = mdb;
-        double W[6];
+        double W[9];
         const bool ok = predict_body_lazy(
             q, [&](double* o) { tm_ld12(tbase + 48 * b + 24, o); }, M, ms,
             [&](HinvBlk& o) { get_hinv(a, M, md, ms, o); }, H, k.ih, k.grav, R, dqt,
@@ -1121,9 +1121,99 @@ __global__ void scatter_state_kernel(double* q, double* qd, int64_t ld, const in
   if (qdi) qd[c * ld + sidx] = qdi[i];
 }
 
-cudaError_t launch_gather(const double* q, const double* qd, int64_t ld, const int64_t* perm, int64_t n, double* qo,
-                          double* qdo, cudaStream_t st) {
+// caller frame ↔ canonical frame (R8): q = (A'Q, t' − A o) out, q' = (A Qᵀ, t + A o) in; velocities alike
+__device__ __forceinline__ void frame_out(const double* F, double* v) {
+  double A[9];
+#pragma unroll
+  for (int e = 0; e < 9; ++e) A[e] = v[e];  // column-major A'
+#pragma unroll
+  for (int c = 0; c < 3; ++c)
+#pragma unroll
+    for (int r = 0; r < 3; ++r) v[3 * c + r] = A[r] * F[c] + A[3 + r] * F[3 + c] + A[6 + r] * F[6 + c];  // (A'Q)[r][c]
+#pragma unroll
+  for (int r = 0; r < 3; ++r) v[9 + r] -= v[r] * F[9] + v[3 + r] * F[10] + v[6 + r] * F[11];
+}
+__device__ __forceinline__ void frame_in(const double* F, double* v) {
+  double A[9];
+#pragma unroll
+  for (int e = 0; e < 9; ++e) A[e] = v[e];
+#pragma unroll
+  for (int r = 0; r < 3; ++r) v[9 + r] += A[r] * F[9] + A[3 + r] * F[10] + A[6 + r] * F[11];
+#pragma unroll
+  for (int c = 0; c < 3; ++c)
+#pragma unroll
+    for (int r = 0; r < 3; ++r)
+      v[3 * c + r] = A[r] * F[3 * c] + A[3 + r] * F[3 * c + 1] + A[6 + r] * F[3 * c + 2];  // (A Qᵀ)[r][c]
+}
+__global__ void gather_frames_kernel(const double* q, const double* qd, int64_t ld, const int64_t* perm, int64_t n,
+                                     const double* frame, double* qo, double* qdo) {
+  const int64_t b = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (b >= n) return;
+  const int64_t s = perm[b];
+  double F[12], v[12];
+#pragma unroll
+  for (int e = 0; e < 12; ++e) F[e] = frame[12 * b + e];
+  if (qo) {
+#pragma unroll
+    for (int e = 0; e < 12; ++e) v[e] = q[e * ld + s];
+    frame_out(F, v);
+#pragma unroll
+    for (int e = 0; e < 12; ++e) qo[12 * b + e] = v[e];
+  }
+  if (qdo) {
+#pragma unroll
+    for (int e = 0; e < 12; ++e) v[e] = qd[e * ld + s];
+    frame_out(F, v);
+#pragma unroll
+    for (int e = 0; e < 12; ++e) qdo[12 * b + e] = v[e];
+  }
+}
+__global__ void scatter_frames_kernel(double* q, double* qd, int64_t ld, const int64_t* perm, int64_t n,
+                                      const double* frame, const double* qi, const double* qdi) {
+  const int64_t b = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (b >= n) return;
+  const int64_t s = perm[b];
+  double F[12], v[12];
+#pragma unroll
+  for (int e = 0; e < 12; ++e) F[e] = frame[12 * b + e];
+  if (qi) {
+#pragma unroll
+    for (int e = 0; e < 12; ++e) v[e] = qi[12 * b + e];
+    frame_in(F, v);
+#pragma unroll
+    for (int e = 0; e < 12; ++e) q[e * ld + s] = v[e];
+  }
+  if (qdi) {
+#pragma unroll
+    for (int e = 0; e < 12; ++e) v[e] = qdi[12 * b + e];
+    frame_in(F, v);
+#pragma unroll
+    for (int e = 0; e < 12; ++e) qd[e * ld + s] = v[e];
+  }
+}
+// the wrench's force point in the canonical frame: ȳ_f = −Q o (the caller's frame origin), rows 6-8 of wr
+__global__ void wrench_point_kernel(double* wr, int64_t ld, const int64_t* perm, int64_t n, const double* frame) {
+  const int64_t b = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (b >= n) return;
+  const double* F = frame + 12 * b;
+#pragma unroll
+  for (int r = 0; r < 3; ++r) wr[(6 + r) * ld + perm[b]] = -(F[3 * r] * F[9] + F[3 * r + 1] * F[10] + F[3 * r + 2] * F[11]);
+}
+
+cudaError_t launch_wrench_point(double* wr, int64_t ld, const int64_t* perm, int64_t n, const double* frame,
+                                cudaStream_t st) {
+  if (n <= 0 || !frame) return cudaSuccess;
+  wrench_point_kernel<<<(unsigned)((n + 127) / 128), 128, 0, st>>>(wr, ld, perm, n, frame);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_gather(const double* q, const double* qd, int64_t ld, const int64_t* perm, int64_t n,
+                          const double* frame, double* qo, double* qdo, cudaStream_t st) {
   if (n <= 0) return cudaSuccess;
+  if (frame) {
+    gather_frames_kernel<<<(unsigned)((n + 127) / 128), 128, 0, st>>>(q, qd, ld, perm, n, frame, qo, qdo);
+    return cudaGetLastError();
+  }
   const int64_t tot = n * 12;
   gather_state_kernel<<<(unsigned)((tot + 255) / 256), 256, 0, st>>>(q, qd, ld, perm, n, qo, qdo);
   return cudaGetLastError();
@@ -1140,9 +1230,13 @@ cudaError_t launch_scatter_rows(double* dst, int64_t ld, const int64_t* perm, in
   scatter_rows_kernel<<<(unsigned)((n * nc + 255) / 256), 256, 0, st>>>(dst, ld, perm, n, src, nc);
   return cudaGetLastError();
 }
-cudaError_t launch_scatter(double* q, double* qd, int64_t ld, const int64_t* perm, int64_t n, const double* qi,
-                           const double* qdi, cudaStream_t st) {
+cudaError_t launch_scatter(double* q, double* qd, int64_t ld, const int64_t* perm, int64_t n, const double* frame,
+                           const double* qi, const double* qdi, cudaStream_t st) {
   if (n <= 0) return cudaSuccess;
+  if (frame) {
+    scatter_frames_kernel<<<(unsigned)((n + 127) / 128), 128, 0, st>>>(q, qd, ld, perm, n, frame, qi, qdi);
+    return cudaGetLastError();
+  }
   const int64_t tot = n * 12;
   scatter_state_kernel<<<(unsigned)((tot + 255) / 256), 256, 0, st>>>(q, qd, ld, perm, n, qi, qdi);
   return cudaGetLastError();

@@ -293,7 +293,9 @@ __device__ __forceinline__ void rot_conj(const double* R, const double* P, doubl
 // f_A = (1/h) M_A q̇ + M_A[0₉;g] − [V vec(R Π(RᵀA)); 0₃]   (Alg. 1 exact R).
 // q̇ is fetched by qd_load(out12) and H̄⁻¹ by get_h(H) only when needed, so that neither is live during the polar
 // decomposition (register pressure). Returns false if the polar decomposition failed.
-// W (optional, world frame [τ; f]): external wrench, f_A,ext = G(A)ᵀW: ½ τ × q_c on column c, f on t.
+// W (optional, world frame [τ; f; ȳ_f]): external wrench, f_A,ext = G(A)ᵀW: ½ τ × q_c on column c, f on t;
+// f acts at the caller's frame origin, the material point ȳ_f of the canonical frame (0 unless the body was
+// re-framed at create, R8), which adds ȳ_f,c f on column c.
 template <class QdLoad, class GetH>
 __device__ __forceinline__ bool predict_body_lazy(const double* q, QdLoad qd_load, const Material& M, double mscale,
                                                   GetH get_h, HinvBlk& H, double ih, const double* grav, double* R,
@@ -322,11 +324,11 @@ __device__ __forceinline__ bool predict_body_lazy(const double* q, QdLoad qd_loa
     double v[3], fc[3];
 #pragma unroll
     for (int r = 0; r < 3; ++r) fc[r] = ma[c] * qd[3 * c + r];
-    if (W) {  // + ½ τ × q_c
+    if (W) {  // + ½ τ × q_c, + ȳ_f,c f (f acts at the material point ȳ_f: Γ(ȳ_f)ᵀ f)
       const double* qc = q + 3 * c;
-      fc[0] += 0.5 * (W[1] * qc[2] - W[2] * qc[1]);
-      fc[1] += 0.5 * (W[2] * qc[0] - W[0] * qc[2]);
-      fc[2] += 0.5 * (W[0] * qc[1] - W[1] * qc[0]);
+      fc[0] += 0.5 * (W[1] * qc[2] - W[2] * qc[1]) + W[6 + c] * W[3];
+      fc[1] += 0.5 * (W[2] * qc[0] - W[0] * qc[2]) + W[6 + c] * W[4];
+      fc[2] += 0.5 * (W[0] * qc[1] - W[1] * qc[0]) + W[6 + c] * W[5];
     }
     mat3t_vec(R, fc, v);
 #pragma unroll
@@ -360,11 +362,11 @@ __device__ __forceinline__ bool predict_body(const double* q, const double* qd, 
       M, mscale, [&](HinvBlk& o) { o = H; }, Hc, ih, grav, R, dqt, W);
 }
 
-// the wrench of body (SoA position) j, or null
+// the wrench of body (SoA position) j (τ, f, ȳ_f: 9 doubles), or null
 __device__ __forceinline__ const double* load_wrench(const BodyArrays& b, int64_t j, double* W) {
   if (!b.wr) return nullptr;
 #pragma unroll
-  for (int e = 0; e < 6; ++e) W[e] = b.wr[e * b.ld + j];
+  for (int e = 0; e < 9; ++e) W[e] = b.wr[e * b.ld + j];
   return W;
 }
 

@@ -268,7 +268,7 @@ mabd_status mabd_get_state(mabd_handle c, double* q_out, double* qd_out, int out
   }
   double* dq = out_on_device ? q_out : (q_out ? c->d.io : nullptr);
   double* dqd = out_on_device ? qd_out : (qd_out ? c->d.io + 12 * n : nullptr);
-  CUDA_TRY(c, launch_gather(c->d.b.q, c->d.b.qd, c->d.b.ld, c->d.perm, n, dq, dqd, c->stream));
+  CUDA_TRY(c, launch_gather(c->d.b.q, c->d.b.qd, c->d.b.ld, c->d.perm, n, c->d.frame, dq, dqd, c->stream));
   if (!out_on_device) {
     if (q_out) CUDA_TRY(c, cudaMemcpyAsync(q_out, dq, 12 * n * sizeof(double), cudaMemcpyDeviceToHost, c->stream));
     if (qd_out)
@@ -294,7 +294,7 @@ mabd_status mabd_set_state(mabd_handle c, const double* q, const double* qd, int
       sqd = c->d.io + 12 * n;
     }
   }
-  CUDA_TRY(c, launch_scatter(c->d.b.q, c->d.b.qd, c->d.b.ld, c->d.perm, n, sq, sqd, c->stream));
+  CUDA_TRY(c, launch_scatter(c->d.b.q, c->d.b.qd, c->d.b.ld, c->d.perm, n, c->d.frame, sq, sqd, c->stream));
   if (!in_on_device) CUDA_TRY(c, cudaStreamSynchronize(c->stream));
   return MABD_OK;
 }
@@ -310,8 +310,9 @@ mabd_status mabd_set_wrench(mabd_handle c, const double* W, int in_on_device) {
       CUDA_TRY(c, cudaMemcpyAsync(c->d.io, W, 6 * n * sizeof(double), cudaMemcpyHostToDevice, c->stream));
       src = c->d.io;
     }
-    CUDA_TRY(c, cudaMemsetAsync(c->d.wr_buf, 0, 6 * c->d.b.ld * sizeof(double), c->stream));
+    CUDA_TRY(c, cudaMemsetAsync(c->d.wr_buf, 0, 9 * c->d.b.ld * sizeof(double), c->stream));
     CUDA_TRY(c, launch_scatter_rows(c->d.wr_buf, c->d.b.ld, c->d.perm, n, src, 6, c->stream));
+    CUDA_TRY(c, launch_wrench_point(c->d.wr_buf, c->d.b.ld, c->d.perm, n, c->d.frame, c->stream));
     if (!in_on_device) CUDA_TRY(c, cudaStreamSynchronize(c->stream));
     wr = c->d.wr_buf;
   }

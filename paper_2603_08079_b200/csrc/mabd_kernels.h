@@ -136,11 +136,13 @@ cudaError_t chain_kernels_init();
 cudaError_t launch_chain(const ChainArgs& a, int nblocks, bool finish, cudaStream_t st);
 cudaError_t launch_btd(const BtdArgs& a, int nblocks, cudaStream_t st);
 cudaError_t launch_hinv_table(const Material* mats, int nm, double ih2, HinvBlk* out, cudaStream_t st);
-cudaError_t launch_gather(const double* q, const double* qd, int64_t ld, const int64_t* perm, int64_t n, double* qo,
-                          double* qdo, cudaStream_t st);
+cudaError_t launch_gather(const double* q, const double* qd, int64_t ld, const int64_t* perm, int64_t n,
+                          const double* frame, double* qo, double* qdo, cudaStream_t st);
 cudaError_t launch_scatter_rows(double* dst, int64_t ld, const int64_t* perm, int64_t n, const double* src, int nc,
                                 cudaStream_t st);
-cudaError_t launch_scatter(double* q, double* qd, int64_t ld, const int64_t* perm, int64_t n, const double* qi,
-                           const double* qdi, cudaStream_t st);
+cudaError_t launch_scatter(double* q, double* qd, int64_t ld, const int64_t* perm, int64_t n, const double* frame,
+                           const double* qi, const double* qdi, cudaStream_t st);
+cudaError_t launch_wrench_point(double* wr, int64_t ld, const int64_t* perm, int64_t n, const double* frame,
+                                cudaStream_t st);
 
 }  // namespace mabd

@@ -48,6 +48,161 @@ size_t align_up(size_t x) { return (x + 255) & ~size_t(255); }
 
 }  // namespace
 
+// ------------------------------------------------------------------------------------------ body frames
+// Packed M̄ (00,01,02,03,11,12,13,22,23,33) → full 4×4.
+static void unpack_mbar(const double* m, double M[4][4]) {
+  static const int I[10] = {0, 0, 0, 0, 1, 1, 1, 2, 2, 3}, J[10] = {0, 1, 2, 3, 1, 2, 3, 2, 3, 3};
+  for (int k = 0; k < 10; ++k) M[I[k]][J[k]] = M[J[k]][I[k]] = m[k];
+}
+
+// Cholesky test: every pivot positive and finite.
+static bool spd4(const double M[4][4]) {
+  double L[4][4] = {};
+  for (int j = 0; j < 4; ++j) {
+    double d = M[j][j];
+    for (int k = 0; k < j; ++k) d -= L[j][k] * L[j][k];
+    if (!(d > 0.0) || !std::isfinite(d)) return false;
+    L[j][j] = std::sqrt(d);
+    for (int i = j + 1; i < 4; ++i) {
+      double v = M[i][j];
+      for (int k = 0; k < j; ++k) v -= L[i][k] * L[j][k];
+      L[i][j] = v / L[j][j];
+    }
+  }
+  return true;
+}
+
+// Symmetric 3×3 eigen-decomposition by cyclic Jacobi rotations: S = Vᵀ diag(w) V with the eigenvectors as the ROWS
+// of V, det V = +1.
+static void sym3_eig(const double S0[3][3], double w[3], double V[3][3]) {
+  double S[3][3], U[3][3] = {{1, 0, 0}, {0, 1, 0}, {0, 0, 1}};  // S = U diag Uᵀ, eigenvectors in U's columns
+  std::memcpy(S, S0, sizeof(S));
+  for (int sweep = 0; sweep < 64; ++sweep) {
+    const double off = S[0][1] * S[0][1] + S[0][2] * S[0][2] + S[1][2] * S[1][2];
+    const double dia = S[0][0] * S[0][0] + S[1][1] * S[1][1] + S[2][2] * S[2][2];
+    if (off <= 1e-40 * dia) break;
+    for (int p = 0; p < 2; ++p)
+      for (int q = p + 1; q < 3; ++q) {
+        if (S[p][q] == 0.0) continue;
+        const double th = (S[q][q] - S[p][p]) / (2.0 * S[p][q]);
+        const double t = (th >= 0 ? 1.0 : -1.0) / (std::fabs(th) + std::sqrt(th * th + 1.0));
+        const double c = 1.0 / std::sqrt(t * t + 1.0), sn = t * c;
+        for (int k = 0; k < 3; ++k) {  // S ← Jᵀ S J with the rotation J in the (p, q) plane
+          const double skp = S[k][p], skq = S[k][q];
+          S[k][p] = c * skp - sn * skq;
+          S[k][q] = sn * skp + c * skq;
+        }
+        for (int k = 0; k < 3; ++k) {
+          const double spk = S[p][k], sqk = S[q][k];
+          S[p][k] = c * spk - sn * sqk;
+          S[q][k] = sn * spk + c * sqk;
+        }
+        for (int k = 0; k < 3; ++k) {
+          const double ukp = U[k][p], ukq = U[k][q];
+          U[k][p] = c * ukp - sn * ukq;
+          U[k][q] = sn * ukp + c * ukq;
+        }
+      }
+  }
+  for (int i = 0; i < 3; ++i) {
+    w[i] = S[i][i];
+    for (int k = 0; k < 3; ++k) V[i][k] = U[k][i];
+  }
+  const double det = V[0][0] * (V[1][1] * V[2][2] - V[1][2] * V[2][1]) - V[0][1] * (V[1][0] * V[2][2] - V[1][2] * V[2][0]) +
+                     V[0][2] * (V[1][0] * V[2][1] - V[1][1] * V[2][0]);
+  if (det < 0)
+    for (int k = 0; k < 3; ++k) V[2][k] = -V[2][k];
+}
+
+// Canonical (central, principal) body frames: DESIGN.md reading R8. A body given with a general SPD M̄ =
+// [[J, s], [sᵀ, m]] is re-expressed in the frame x̄' = Q(x̄ − o), o = s/m, Q the eigenvector rows of J − s sᵀ/m,
+// where M̄' = diag(eig, m). The co-rotated step is covariant under this rigid change of material frame (the
+// coordinates map by q' = (T̄ ⊗ I₃) q, T̄ = [[Q, 0], [oᵀ, 1]], which commutes with diag₄(R); K̄_A is invariant
+// under δA ↦ Q δA Qᵀ; the elastic force depends on AᵀA only through rotation invariants), so the library steps the
+// canonical copy with the closed-form H̄⁻¹ and maps states back on output. Bodies whose M̄ is already diagonal keep
+// their frame (identity map, bitwise the same arithmetic).
+struct Canon {
+  bool any = false;
+  std::vector<double> q0, qd0, mbar, ya, yb;  // canonical copies of the inputs
+  std::vector<double> frame;                  // [n][12]: Q row-major (9), o (3); identity for diagonal bodies
+  mabd_bodies B;
+  mabd_joints J;
+};
+
+static bool canonical_frames(const mabd_bodies* B, const mabd_joints* J, Canon* c) {
+  const int64_t n = B->n;
+  c->any = false;
+  for (int64_t i = 0; i < n && !c->any; ++i) {
+    const double* m = B->mbar + 10 * i;
+    c->any = m[1] != 0.0 || m[2] != 0.0 || m[3] != 0.0 || m[5] != 0.0 || m[6] != 0.0 || m[8] != 0.0;
+  }
+  if (!c->any) return false;
+  c->frame.assign(12 * n, 0.0);
+  c->q0.assign(B->q0, B->q0 + 12 * n);
+  c->qd0.assign(B->qd0, B->qd0 + 12 * n);
+  c->mbar.assign(B->mbar, B->mbar + 10 * n);
+  for (int64_t i = 0; i < n; ++i) {
+    double* F = c->frame.data() + 12 * i;
+    double M[4][4];
+    unpack_mbar(B->mbar + 10 * i, M);
+    const bool diag = M[0][1] == 0.0 && M[0][2] == 0.0 && M[0][3] == 0.0 && M[1][2] == 0.0 && M[1][3] == 0.0 &&
+                      M[2][3] == 0.0;
+    if (diag) {
+      F[0] = F[4] = F[8] = 1.0;
+      continue;
+    }
+    const double m = M[3][3];
+    const double o[3] = {M[0][3] / m, M[1][3] / m, M[2][3] / m};
+    double Jc[3][3], w[3], Q[3][3];
+    for (int r = 0; r < 3; ++r)
+      for (int k = 0; k < 3; ++k) Jc[r][k] = M[r][k] - m * o[r] * o[k];
+    sym3_eig(Jc, w, Q);
+    for (int r = 0; r < 3; ++r)
+      for (int k = 0; k < 3; ++k) F[3 * r + k] = Q[r][k];
+    for (int r = 0; r < 3; ++r) F[9 + r] = o[r];
+    double* mb = c->mbar.data() + 10 * i;
+    for (int k = 0; k < 10; ++k) mb[k] = 0.0;
+    mb[0] = w[0];
+    mb[4] = w[1];
+    mb[7] = w[2];
+    mb[9] = m;
+    // A' = A Qᵀ, t' = t + A o (and the same map of the velocities): column c' of A' is Σ_c Q[c'][c] A[:, c]
+    for (double* q : {c->q0.data() + 12 * i, c->qd0.data() + 12 * i}) {
+      double A[3][3], t[3];
+      for (int r = 0; r < 3; ++r) {
+        for (int k = 0; k < 3; ++k) A[r][k] = q[3 * k + r];
+        t[r] = q[9 + r];
+      }
+      for (int cp = 0; cp < 3; ++cp)
+        for (int r = 0; r < 3; ++r) q[3 * cp + r] = A[r][0] * Q[cp][0] + A[r][1] * Q[cp][1] + A[r][2] * Q[cp][2];
+      for (int r = 0; r < 3; ++r) q[9 + r] = t[r] + A[r][0] * o[0] + A[r][1] * o[1] + A[r][2] * o[2];
+    }
+  }
+  // material points on bodies: ȳ' = Q(ȳ − o)
+  int64_t P = 0;
+  for (int64_t k = 0; k < J->n_joints; ++k) P += J->npts[k];
+  c->ya.assign(J->ybar_a, J->ybar_a + 3 * P);
+  c->yb.assign(J->ybar_b, J->ybar_b + 3 * P);
+  for (int64_t k = 0, pt = 0; k < J->n_joints; ++k)
+    for (int q = 0; q < J->npts[k]; ++q, ++pt)
+      for (int side = 0; side < 2; ++side) {
+        const int64_t b = side ? J->body_b[k] : J->body_a[k];
+        if (b < 0) continue;  // world point of an anchor
+        const double* F = c->frame.data() + 12 * b;
+        double* y = (side ? c->yb.data() : c->ya.data()) + 3 * pt;
+        const double d[3] = {y[0] - F[9], y[1] - F[10], y[2] - F[11]};
+        for (int r = 0; r < 3; ++r) y[r] = F[3 * r] * d[0] + F[3 * r + 1] * d[1] + F[3 * r + 2] * d[2];
+      }
+  c->B = *B;
+  c->B.q0 = c->q0.data();
+  c->B.qd0 = c->qd0.data();
+  c->B.mbar = c->mbar.data();
+  c->J = *J;
+  c->J.ybar_a = c->ya.data();
+  c->J.ybar_b = c->yb.data();
+  return true;
+}
+
 // ------------------------------------------------------------------------------------------ validation
 static mabd_status validate(const mabd_bodies* B, const mabd_joints* J, const mabd_options* o, std::string* msg) {
   if (!B || !J) return *msg = "bodies/joints NULL", MABD_EINVAL;
@@ -67,15 +222,10 @@ static mabd_status validate(const mabd_bodies* B, const mabd_joints* J, const ma
   }
   for (int64_t i = 0; i < B->n; ++i) {
     const double* m = B->mbar + 10 * i;
-    const double dmax = std::max(std::max(m[0], m[4]), std::max(m[7], m[9]));
-    if (!(m[0] > 0 && m[4] > 0 && m[7] > 0 && m[9] > 0) || !std::isfinite(dmax))
-      return *msg = fmt("body %lld: mbar diagonal must be positive", (long long)i), MABD_EINVAL;
-    const double off[6] = {m[1], m[2], m[3], m[5], m[6], m[8]};
-    for (double v : off)
-      if (std::fabs(v) > 1e-12 * dmax)
-        return *msg = fmt("body %lld: mbar must be diagonal (central principal body frame, DESIGN.md A8)",
-                          (long long)i),
-               MABD_EUNSUPPORTED;
+    double M[4][4];
+    unpack_mbar(m, M);
+    if (!spd4(M))
+      return *msg = fmt("body %lld: mbar must be symmetric positive definite", (long long)i), MABD_EINVAL;
     if (!(B->volume[i] > 0) || !(B->youngs[i] > 0) || !(B->poisson[i] > -1.0 && B->poisson[i] < 0.5))
       return *msg = fmt("body %lld: need V > 0, E > 0, -1 < nu < 0.5", (long long)i), MABD_EINVAL;
     for (int c = 0; c < 12; ++c)
@@ -378,6 +528,12 @@ mabd_status build_plan(const mabd_bodies* B, const mabd_joints* J, const mabd_op
   mabd_status st = validate(B, J, o, msg);
   if (st != MABD_OK) return st;
   *p = Plan();
+  Canon canon;
+  if (canonical_frames(B, J, &canon)) {  // from here on the scene is in the canonical body frames
+    B = &canon.B;
+    J = &canon.J;
+    p->frame = std::move(canon.frame);
+  }
   p->n = B->n;
   p->n_joints = J->n_joints;
   p->newton_iters = (o && o->newton_iters > 1) ? o->newton_iters : 1;
@@ -458,7 +614,7 @@ mabd_status build_plan(const mabd_bodies* B, const mabd_joints* J, const mabd_op
   f.qd = take(sizeof(double) * 12 * ld);
   f.rs = take(sizeof(double) * 9 * ld);
   f.z = p->newton_iters > 1 ? take(sizeof(double) * 12 * ld) : 0;
-  f.wr = take(sizeof(double) * 6 * ld);
+  f.wr = take(sizeof(double) * 9 * ld);
   f.mat_id = multi_mat ? take(sizeof(int32_t) * ld) : 0;
   f.mscale = any_scale ? take(sizeof(double) * ld) : 0;
   f.mats = take(sizeof(Material) * p->mats.size());
@@ -466,6 +622,7 @@ mabd_status build_plan(const mabd_bodies* B, const mabd_joints* J, const mabd_op
   f.perm = take(sizeof(int64_t) * B->n);
   f.io = take(sizeof(double) * 24 * B->n);
   f.err = take(sizeof(int32_t) * 4);
+  f.frame = p->frame.empty() ? 0 : take(sizeof(double) * p->frame.size());
   if (p->solver == MABD_SOLVER_CHAIN) {
     f.slot_info = take(sizeof(uint32_t) * (ld + 16));  // + padding: segments stage SEG + 4 slot codes
     f.geo = take(sizeof(double) * p->geo.size());
@@ -561,7 +718,9 @@ cudaError_t upload_plan(const Plan& p, char* ws, cudaStream_t st, DevPtrs* d) {
   d->perm = (int64_t*)(ws + f.perm);
   d->io = (double*)(ws + f.io);
   d->err = (int32_t*)(ws + f.err);
+  d->frame = p.frame.empty() ? nullptr : (double*)(ws + f.frame);
   cudaError_t e;
+  if (d->frame && (e = put(d->frame, p.frame, st))) return e;
   if ((e = put(d->b.q, p.q_soa, st))) return e;
   if ((e = put(d->b.qd, p.qd_soa, st))) return e;
   if (!p.mat_id.empty() && (e = put((int32_t*)d->b.mat_id, p.mat_id, st))) return e;

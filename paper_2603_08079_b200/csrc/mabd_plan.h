@@ -110,6 +110,7 @@ struct Plan {
   std::vector<int32_t> mat_id;   // [ld] (empty if one material)
   std::vector<double> mscale;    // [ld] (empty if all 1)
   std::vector<int64_t> perm;     // caller body → internal position
+  std::vector<double> frame;     // [n][12] canonical body frame (Q, o) per caller body, or empty (all canonical)
   int64_t ld = 0;                // SoA stride (positions)
   std::vector<double> q_soa, qd_soa;  // [12][ld]
   // chain solver
@@ -137,7 +138,7 @@ struct Plan {
   // device layout (byte offsets into the workspace)
   size_t workspace_bytes = 0;
   struct Off {
-    size_t q, qd, rs, z, wr, mat_id, mscale, mats, hinv, perm, io, err;
+    size_t q, qd, rs, z, wr, mat_id, mscale, mats, hinv, perm, io, err, frame;
     size_t slot_info, geo, seg_flags, seg_red, long_list, left_iface;
     std::vector<size_t> tops, lams;  // per BTD level: tops[0] = chain tops (n_long), lams[i] = level i+1 λ
     size_t all_tops, lam_g, plo, lwin, llong;
@@ -149,7 +150,9 @@ struct Plan {
 
 struct DevPtrs {
   BodyArrays b{};
-  double* wr_buf = nullptr;        // [6][ld] wrench storage (b.wr points here once a wrench is set)
+  double* wr_buf = nullptr;        // [9][ld] wrench storage (b.wr points here once a wrench is set): τ, f, and the
+                                   // material point f acts at (the caller's frame origin, in the canonical frame)
+  double* frame = nullptr;         // [n][12] canonical frames per caller body (Plan::frame), or null
   HinvBlk* hinv = nullptr;
   Material* mats = nullptr;
   int64_t* perm = nullptr;

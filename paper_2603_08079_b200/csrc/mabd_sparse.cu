@@ -61,7 +61,7 @@ __global__ void sparse_predict_kernel(SparseArgs a) {
       H = a.hinv_tab[mid];
     else
       hinv_blocks(M, msc, a.k.ih2, H);
-    double W[6];
+    double W[9];
     if (!predict_body(q, qd, M, msc, H, a.k.ih, a.k.grav, R, dqt, load_wrench(a.b, j, W)))
       sreport(a.k, ERR_NONFINITE);
 #pragma unroll

@@ -194,7 +194,7 @@ __device__ void tree_predict_core(const TreeArgs& a, int b, double* R, double* q
     H = a.hinv_tab[mid];
   else
     hinv_blocks(M, msc, k.ih2, H);
-  double W[6];
+  double W[9];
   if (!predict_body(q, qd, M, msc, H, k.ih, k.grav, R, dqt, load_wrench(a.b, b, W))) treport(k, ERR_NONFINITE);
   double* sc = a.bscr + b;  // [21][ld]: component c at sc[c·ld]
 #pragma unroll

@@ -42,7 +42,7 @@ def _ws(lib, sc, solver=0, iters=1):
                 None, (ctypes.c_double * 3)(*sc.gravity))
     j = _Joints(sc.n_joints, _ptr(sc.body_a, _ip), _ptr(sc.body_b, _ip), _ptr(sc.npts, _ip), _ptr(sc.ybar_a),
                 _ptr(sc.ybar_b))
-    o = _Options(iters, 1, solver, 0, 1, None, None, 0, None)
+    o = _Options(iters, 1, solver, 0, 1, None, None, 0, None, 0)
     n = ctypes.c_size_t()
     st = lib.mabd_workspace_size(ctypes.byref(b), ctypes.byref(j), ctypes.byref(o), ctypes.byref(n))
     return st, n.value, lib.mabd_last_error(None).decode()
@@ -70,10 +70,13 @@ def test_validation_errors(lib):
     bad.ybar_a = np.vstack([bad.ybar_a, np.zeros((2, 3))])
     bad.ybar_b = np.vstack([bad.ybar_b, np.zeros((2, 3))])
     assert _ws(lib, bad)[0] == 1
+    ok = sc.copy()
+    ok.mbar[0, 1] = 0.01 * ok.mbar[0, 0]               # a general SPD M̄ is accepted (canonical frame, DESIGN R8)
+    assert _ws(lib, ok)[0] == 0
     bad = sc.copy()
-    bad.mbar[0, 1] = 0.01 * bad.mbar[0, 0]             # non-diagonal M̄ → unsupported in this version
+    bad.mbar[0, 3] = 2.0 * np.sqrt(bad.mbar[0, 0] * bad.mbar[0, 9])   # indefinite M̄
     st, _, msg = _ws(lib, bad)
-    assert st == 8 and "diagonal" in msg
+    assert st == 1 and "positive definite" in msg
     bad = sc.copy()
     bad.poisson[2] = 0.5
     assert _ws(lib, bad)[0] == 1
@@ -121,3 +124,17 @@ def test_sparse_symbolic_nested_dissection(lib):
         assert st["front_doubles"] >= st["rows"]
     ratio = s64["flops"] / s32["flops"]
     assert 4.0 <= ratio <= 16.0, ratio
+
+
+def test_residual_rhs_option(lib):
+    """options.residual_rhs: 0 (zero-initialised default) and 1 include −C(qⁿ) (footnote P:459); others are invalid."""
+    from paper_2603_08079_b200.binding import _Bodies, _Joints, _Options, _ptr, _ip
+    sc = G.random_chain(5, seed=1)
+    b = _Bodies(sc.n, _ptr(sc.q0), _ptr(sc.qd0), _ptr(sc.mbar), _ptr(sc.volume), _ptr(sc.youngs), _ptr(sc.poisson),
+                None, (ctypes.c_double * 3)(*sc.gravity))
+    j = _Joints(sc.n_joints, _ptr(sc.body_a, _ip), _ptr(sc.body_b, _ip), _ptr(sc.npts, _ip), _ptr(sc.ybar_a),
+                _ptr(sc.ybar_b))
+    n = ctypes.c_size_t()
+    for rr, want in ((0, 0), (1, 0), (2, 1), (-1, 1)):
+        o = _Options(1, rr, 0, 0, 1, None, None, 0, None, 0)
+        assert lib.mabd_workspace_size(ctypes.byref(b), ctypes.byref(j), ctypes.byref(o), ctypes.byref(n)) == want
