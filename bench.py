@@ -4,12 +4,15 @@
     python bench.py [--gpus N] [--steps K] [--warmup W] [--config C] [--impl ours|reference]
 
 Default workload: BASELINE.json configs[1] (config 2): 4096 independent chains × 256 links = 1,048,576
-bodies per GPU, h = 1e-2, one Newton iteration per step. For N > 1 (torchrun) every rank runs its own
-block of 4096 chains of the same recipe (independent assemblies: weak scaling, no collective in the step).
+bodies, h = 1e-2, one Newton iteration per step. For N > 1 (torchrun) the 4096 chains are split into N
+contiguous blocks, one per rank (independent assemblies, no collective in the step; strong
+scaling); configs 3 and 4 split one chain / one tree with one NCCL all-gather per step.
 
 Timed region: W untimed warm-up steps, then barrier + cuda.synchronize, CUDA events on the library's stream
-around ONE mabd_step(h, K) call, barrier + synchronize; the max over ranks is reported. The state
-(q, q̇: 192 MiB + 8 MiB of per-body mass scales per GPU) is larger than the 126 MB L2, so no flush is needed.
+around the enqueued steps (mabd_step_async; one CUDA graph per step), barrier + synchronize; the max over
+ranks is reported. A rank whose state is smaller than the 126 MB L2 flushes L2 (256 MiB memset) before every
+timed step, outside the event intervals; at N = 1 the config-2 state (192 MiB + 8 MiB of per-body mass
+scales) is larger than L2 and streams from HBM.
 
 ``--impl reference`` times the CPU oracle (oracle/, as it stands, single-threaded) on a bounded sample of the
 same workload; it is the reference arm of this tier (the paper has no code to install).
@@ -101,7 +104,7 @@ class ClockSampler:
                         self.reasons.add(k)
             except Exception:
                 pass
-            self._stop.wait(0.01)
+            self._stop.wait(0.002)
 
     def __enter__(self):
         if self._ok:
@@ -176,6 +179,21 @@ def run_reference(args, rank: int, world: int) -> None:
     print(json.dumps(line), flush=True)
 
 
+L2_BYTES = 126 * 2 ** 20
+
+
+def state_bytes_per_rank(cfg: int, n: int, world: int, split: bool) -> int:
+    return (BYTES_PER_BODY[cfg] // 2) * (n // world if split else n)   # q, q̇ (+ per-body params) of one rank
+
+
+PARALLELISM = {
+    2: "chains split over {w} ranks: contiguous blocks of 4096/{w} independent chains (no collective in the step)",
+    3: "chain split over {w} ranks (NCCL all-gather of per-rank top systems, solved redundantly)",
+    4: "tree split over {w} ranks (subtrees per rank, NCCL all-gather of the roots' condensed blocks, top levels "
+       "replicated)",
+}
+
+
 def run_ours(args, rank: int, world: int, local_rank: int) -> None:
     import torch
     import torch.distributed as dist
@@ -188,10 +206,11 @@ def run_ours(args, rank: int, world: int, local_rank: int) -> None:
     n = sc.n
     h = sc.h
     stream = torch.cuda.Stream(device=dev)
-    # config 3 (one chain) and config 4 (one tree) are split across ranks (strong scaling, one all-gather per step:
-    # of per-rank top systems for the chain, of the subtree roots' condensed blocks for the tree); configs 1, 2, 5
-    # run one independent assembly per rank (weak scaling, no collective; config 5 as replicas)
-    split = world > 1 and args.config in (3, 4)
+    # configs 2 (4096 independent chains), 3 (one chain) and 4 (one tree) are split across the ranks (strong
+    # scaling): config 2 by blocks of chains with no collective, config 3 with one all-gather of the
+    # per-rank top systems per step, config 4 with one all-gather of the subtree roots' condensed blocks. Configs 1
+    # and 5 run one independent assembly per rank (replicas, weak scaling).
+    split = world > 1 and args.config in (2, 3, 4)
     if split:
         from paper_2603_08079_b200.binding import nccl_unique_id
         blob = torch.zeros(128, dtype=torch.uint8, device=dev)
@@ -215,16 +234,21 @@ def run_ours(args, rank: int, world: int, local_rank: int) -> None:
     # The configured workload is an episode of sc.nsteps steps (100 for configs 2-4) from the initial state; the
     # per-step cost depends on the state (the polar decomposition iterates more on strained links), so K timed
     # steps are run as episodes of ≤ nsteps steps, each from the initial state. The reset (a device copy of
-    # q⁰, q̇⁰) happens between episodes, outside the timed intervals; the reported time is the sum of the
-    # episodes' CUDA-event intervals on the library's stream.
+    # q⁰, q̇⁰) happens between episodes, outside the timed intervals.
     episode = max(1, int(getattr(sc, "nsteps", 100) or 100))
     q0_dev = torch.as_tensor(q0, device=dev)
     qd0_dev = torch.as_tensor(qd0, device=dev)
 
     def reset():
-        sim.set_state(q0_dev, qd0_dev)
+        with torch.cuda.stream(stream):
+            sim.set_state(q0_dev, qd0_dev)
 
-    # warm-up
+    # L2 rule: a rank whose state is smaller than the 126 MB L2 gets an L2 flush (a 256 MiB memset) before every
+    # timed step, outside the CUDA-event interval; a larger state streams from HBM anyway and is timed in one call.
+    state_b = state_bytes_per_rank(args.config, n, world, split)
+    flush = state_b < L2_BYTES
+    l2buf = torch.empty(256 * 2 ** 20, dtype=torch.uint8, device=dev) if flush else None
+
     if args.warmup:
         sim.step(h, min(args.warmup, episode))
     reset()
@@ -235,13 +259,29 @@ def run_ours(args, rank: int, world: int, local_rank: int) -> None:
         left = args.steps
         while left > 0:
             kk = min(episode, left)
-            ev0 = torch.cuda.Event(enable_timing=True)
-            ev1 = torch.cuda.Event(enable_timing=True)
-            ev0.record(stream)
-            sim.step(h, kk)
-            ev1.record(stream)
-            barrier()
-            ms += ev0.elapsed_time(ev1)
+            if flush:   # per-step intervals, each after an L2 flush; the steps are enqueued without host waits
+                evs = []
+                for _ in range(kk):
+                    with torch.cuda.stream(stream):
+                        l2buf.zero_()
+                    e0 = torch.cuda.Event(enable_timing=True)
+                    e1 = torch.cuda.Event(enable_timing=True)
+                    e0.record(stream)
+                    sim.step_async(h, 1)
+                    e1.record(stream)
+                    evs.append((e0, e1))
+                sim.check()
+                barrier()
+                ms += sum(a.elapsed_time(b) for a, b in evs)
+            else:
+                ev0 = torch.cuda.Event(enable_timing=True)
+                ev1 = torch.cuda.Event(enable_timing=True)
+                ev0.record(stream)
+                sim.step_async(h, kk)
+                ev1.record(stream)
+                sim.check()
+                barrier()
+                ms += ev0.elapsed_time(ev1)
             left -= kk
             if left > 0:
                 reset()
@@ -253,8 +293,7 @@ def run_ours(args, rank: int, world: int, local_rank: int) -> None:
     ms_step = ms / args.steps
     bodies_total = n if split else world * n
     value = bodies_total * args.steps / (ms * 1e-3)
-    # + one error-word reset kernel per mabd_step call (one call per episode)
-    launches = info["launches_per_step"] * args.steps + (args.steps + episode - 1) // episode
+    launches = info["launches_per_step"] * args.steps   # solver launches + the step_end node, per step
 
     # e2e through the public API with pinned host buffers: every step is H2D (q, q̇) → step → D2H (q, q̇). Two
     # independent problems are kept in flight (two handles, two streams, one host thread each: the binding's
@@ -316,7 +355,9 @@ def run_ours(args, rank: int, world: int, local_rank: int) -> None:
     if rank == 0:
         peak, peak_src = peaks()
         bpb = BYTES_PER_BODY[args.config]
-        achieved = bpb * n / (ms_step * 1e-3) / 1e9
+        n_rank = n // world if split else n          # bodies this rank advances per step
+        achieved = bpb * n_rank / (ms_step * 1e-3) / 1e9
+        lps = info["launches_per_step"]
         traffic = None
         prof = os.path.join(ROOT, "profiles", "ncu_traffic.json")
         if os.path.exists(prof):
@@ -325,27 +366,38 @@ def run_ours(args, rank: int, world: int, local_rank: int) -> None:
                     traffic = json.load(fh).get(str(args.config))
             except Exception:
                 traffic = None
+        if info["solver"] == "sparse":
+            bound = {"bound": "fp64", "note": "dominated by the numeric factorization of the dual (fp64 ALU); "
+                     "the HBM fraction below is the per-body state only (step level)"}
+        else:
+            bound = {"bound": "hbm"}
         line = {
             "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": True,
             "scaling": "strong" if split else "weak",
             "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-            "config": {"workload": CFG_TEXT[args.config], "bodies_per_gpu": n, "solver": info["solver"],
-                       "episode_steps": episode,
+            "config": {"workload": CFG_TEXT[args.config], "bodies": n, "bodies_per_gpu": n_rank,
+                       "solver": info["solver"], "episode_steps": episode,
                        "timing": f"{args.steps} steps as episodes of <= {episode} steps from the initial state "
-                                 "(reset between episodes, outside the CUDA-event intervals)",
-                       "dual_rows_per_gpu": info["n_dual_rows"],
-                       "l2": "no flush: state q,qdot (192 MiB) + per-body params > 126 MB L2",
-                       "parallelism": ((f"chain split over {world} ranks (NCCL all-gather of per-rank tops)"
-                                        if args.config == 3 else
-                                        f"tree split over {world} ranks (subtrees per rank, NCCL all-gather of the "
-                                        "roots' condensed blocks, top levels replicated)") if split
-                                       else f"dp{world} (independent assemblies per rank)")},
-            "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
-                         "frac": achieved / peak, "traffic": traffic,
-                         "kernel": "chain_kernel (fused stages 1-4)" if info["solver"] == "chain" else info["solver"],
+                                 "(reset between episodes, outside the CUDA-event intervals); each step replays "
+                                 "one CUDA graph",
+                       "dual_rows": info["n_dual_rows"],
+                       "l2": (f"flushed before every timed step (256 MiB memset outside the event interval): "
+                              f"per-rank state {state_b / 2**20:.1f} MiB < 126 MB L2") if flush else
+                             f"no flush: per-rank state {state_b / 2**20:.0f} MiB > 126 MB L2",
+                       "parallelism": PARALLELISM[args.config].format(w=world) if split
+                       else f"dp{world} (independent assemblies per rank)"},
+            "roofline": {**bound, "achieved": achieved, "peak": peak, "unit": "GB/s",
+                         "frac": achieved / peak,
+                         "traffic": traffic,
+                         "traffic_source": "profiles/ncu_traffic.json (ncu --set full DRAM bytes per launch of the "
+                                           "fused kernel, 1 GPU; not measured by this run)",
+                         "kernel": "chain_kernel (fused stages 1-4)" if info["solver"] == "chain" and lps == 2
+                         else f"{info['solver']} solver, step level ({lps} launches per step)",
                          "bytes_per_body_step": bpb, "peak_source": peak_src,
-                         "duration": "timed region / steps (one fused launch per step)"},
+                         "duration": "CUDA-event time per step on the library's stream (" +
+                                     ("the fused chain kernel + the 1-thread step_end node)" if lps == 2 else
+                                      f"{lps} launches: a step-level roofline)")},
             "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": 2 * 96 * n * world,
                     "d2h_bytes_per_step": 2 * 96 * n * world, "steps": ke,
                     "path": "Simulator.set_state(pinned host) -> step(h,1) -> get_state(pinned host), "
@@ -382,6 +434,8 @@ def main():
     if world > 1:
         import torch
         import torch.distributed as dist
+        os.environ.setdefault("NCCL_DEBUG", "INFO")          # communicator lines name the rank count (stderr)
+        os.environ.setdefault("NCCL_DEBUG_SUBSYS", "INIT")
         torch.cuda.set_device(local_rank)
         dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
     try:

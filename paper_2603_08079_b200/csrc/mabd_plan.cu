@@ -516,7 +516,7 @@ static bool partition_chain(Plan* p, int W, int rank, bool emulate, std::string*
     for (int64_t w = p->parts[q].win_lo; w < p->parts[q].win_hi; ++w) p->local_windows.push_back((int32_t)w);
     for (int64_t u = p->parts[q].long_lo; u < p->parts[q].long_hi; ++u) p->local_long.push_back(p->long_list[u]);
   }
-  int lps = 1 + 1 + 1;  // chain pass 1, global solve, chain finish
+  int lps = p->n_long == 0 ? 1 : 1 + 1 + 1;  // chain pass 1 (+ global solve, chain finish if a chain is long)
   for (int q = p->part_lo; q < p->part_hi; ++q)
     if (p->parts[q].n1 > 0) lps += 2 + (p->parts[q].btd1 ? 2 : 0);
   p->launches_per_step = lps;
@@ -872,6 +872,7 @@ static cudaError_t launch_step_parts(const Plan& p, const DevPtrs& d, ChainArgs 
   const StepConsts& k = a.k;
   a.seg_list = d.local_windows;
   if ((e = launch_chain(a, (int)p.local_windows.size(), false, st))) return e;
+  if (p.n_long == 0) return cudaSuccess;  // independent short chains (config 2): no exchange, nothing to finish
   for (int q = p.part_lo; q < p.part_hi; ++q) {
     const Plan::Part& P = p.parts[q];
     if (P.n1 == 0) continue;
