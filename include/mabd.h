@@ -104,7 +104,15 @@ typedef struct {
   int32_t no_graphs;         /* 0: each step is replayed as one CUDA graph captured on cuda_stream (needs a
                                 non-NULL stream; rebuilt after mabd_prefactor / mabd_set_wrench); 1: plain
                                 stream launches                                                        */
+  int32_t rotation;          /* MABD_ROTATION_POLAR (0): exact R = polar(A). 
+                                MABD_ROTATION_LENGTH_PRESERVING (1): the polar-free variant of P:283-310
+                                (Alg. 1; reading R9): the free solve maps each 3-block by the
+                                length-preserving Aᵀ / A of Eq. len_preserving, the elastic force is the StVK
+                                force of E = ½(AᵀA − I), and constraint forces use diag₄(A)H̄⁻¹diag₄(Aᵀ)
+                                ("A ≈ R"). Equal to (0) at rigid states; an approximation otherwise. */
 } mabd_options;
+
+enum { MABD_ROTATION_POLAR = 0, MABD_ROTATION_LENGTH_PRESERVING = 1 };
 
 /* Topology/solver actually selected (mabd_query). */
 enum { MABD_SOLVER_CHAIN = 1, MABD_SOLVER_TREE = 2, MABD_SOLVER_SPARSE = 3 };

@@ -35,7 +35,8 @@ import scipy.sparse as sp
 import scipy.sparse.linalg as spla
 
 __all__ = [
-    "lame", "unpack_mbar", "mass_A", "kbar_A", "hbar_A", "polar", "elastic_force_A", "affine_force",
+    "lame", "unpack_mbar", "mass_A", "kbar_A", "hbar_A", "polar", "elastic_force_A", "stvk_force_A",
+    "length_preserving", "affine_force",
     "body_hessians", "constraint_system", "constraint_residual", "predict", "step", "simulate", "nonlinear_residual",
     "wrench_force", "twist_velocity", "angular_velocity",
     "block_thomas", "leaf_to_root_solve", "dual_matrix", "rel_err", "T9", "vec", "unvec",
@@ -151,7 +152,30 @@ def elastic_force_A(A, V, mu, lam) -> np.ndarray:
     return np.asarray(V)[..., None] * vec(R @ Pi)
 
 
-def affine_force(q, qd, mbar, V, E, nu, g, h) -> np.ndarray:
+def stvk_force_A(A, V, mu, lam) -> np.ndarray:
+    """Polar-free elastic force (reading R9): V vec(A Σ(E)), Σ = 2μE + λ tr(E) I, E = ½(AᵀA − I) — the
+    gradient of V[μ‖E‖² + (λ/2)tr(E)²], a rotation-invariant energy whose Hessian at A = I is K̄_A, so it
+    pairs with the same pre-factored H̄ and equals the co-rotated force of P:260-271 to first order in the strain.
+    Used by the length-preserving variant of P:283-310 (Alg. 1), which has no R to co-rotate with."""
+    A = np.asarray(A, dtype=np.float64)
+    I = np.eye(3)
+    E = 0.5 * (np.swapaxes(A, -1, -2) @ A - I)
+    trE = np.trace(E, axis1=-2, axis2=-1)
+    Sig = 2.0 * np.asarray(mu)[..., None, None] * E + (np.asarray(lam) * trE)[..., None, None] * I
+    return np.asarray(V)[..., None] * vec(A @ Sig)
+
+
+def length_preserving(M, v) -> np.ndarray:
+    """Eq. len_preserving: the rotation of a 3-vector v is approximated by M v rescaled to |v|,
+    (‖v‖/‖Mv‖) M v (zero stays zero). M = Aᵀ stands for Rᵀ and M = A for R (Alg. 1 lines 4-7 and 9-12)."""
+    v = np.asarray(v, dtype=np.float64)
+    w = np.einsum("...ij,...j->...i", M, v)
+    nv = np.linalg.norm(v, axis=-1, keepdims=True)
+    nw = np.linalg.norm(w, axis=-1, keepdims=True)
+    return np.where(nw > 0, w * (nv / np.where(nw > 0, nw, 1.0)), 0.0)
+
+
+def affine_force(q, qd, mbar, V, E, nu, g, h, rotation: str = "polar") -> np.ndarray:
     """Newton r.h.s. f_A = −∇E at qⁿ for one iteration from q⁽⁰⁾ = qⁿ.
 
     E(q) = (1/2h²)(q−q̂)ᵀM_A(q−q̂) + VΨ (P:193-199 projected by P:211-215), q̂ = qⁿ + hq̇ⁿ + h²M_A⁻¹f_ext,
@@ -164,7 +188,8 @@ def affine_force(q, qd, mbar, V, E, nu, g, h) -> np.ndarray:
     grav = np.zeros(q.shape)
     grav[..., 9:12] = g
     f = np.einsum("...ij,...j->...i", MA, np.asarray(qd) / h + grav)
-    f[..., :9] -= elastic_force_A(unvec(q[..., :9]), V, mu, lam)
+    el = elastic_force_A if rotation == "polar" else stvk_force_A
+    f[..., :9] -= el(unvec(q[..., :9]), V, mu, lam)
     return f
 
 
@@ -255,25 +280,49 @@ def constraint_residual(scene, q) -> float:
 # one step
 # --------------------------------------------------------------------------
 
-def predict(scene, q, qd, h):
-    """Per-body stages 1-2: R, f_A, H_j, and δq̃ = H_j⁻¹ f_A (Alg. 1 with exact R)."""
+def predict(scene, q, qd, h, rotation: str = "polar"):
+    """Per-body stages 1-2: R, f_A, H_j, and δq̃ = H_j⁻¹ f_A (Alg. 1 with exact R).
+
+    rotation = "length_preserving" (R9): no polar decomposition. The free solve is
+    Alg. 1 as printed: each 3-block f_k of f_A → (‖f_k‖/‖Aᵀf_k‖)Aᵀf_k, solve H̄δp = f, each δp_k →
+    (‖δp_k‖/‖Aδp_k‖)Aδp_k; the elastic force is ``stvk_force_A``; the operator that carries constraint forces
+    (stages 3-5) is H̃_j⁻¹ = diag₄(A)H̄⁻¹diag₄(Aᵀ) ("A ≈ R"). Returned as (A, H̃_j δq̃, H̃_j, δq̃), so that every
+    KKT route solves [H̃ ∇Cᵀ; ∇C 0][δq; λ] = [H̃δq̃; −C(qⁿ)], i.e. δq = δq̃ − H̃⁻¹∇Cᵀλ with S λ = C(q̃).
+    """
     q = np.asarray(q, dtype=np.float64)
     A = unvec(q[:, :9])
-    R = polar(A)
-    f = affine_force(q, qd, scene.mbar, scene.volume, scene.youngs, scene.poisson, scene.gravity, h)
+    f = affine_force(q, qd, scene.mbar, scene.volume, scene.youngs, scene.poisson, scene.gravity, h, rotation)
     if getattr(scene, "wrench", None) is not None:  # at the linearisation point (P:676)
         f = f + wrench_force(q, scene.wrench)
     Hbar = hbar_A(scene.mbar, scene.volume, scene.youngs, scene.poisson, h)
-    H = body_hessians(R, Hbar)
-    dq_tilde = np.linalg.solve(H, f[..., None])[..., 0]
-    return R, f, H, dq_tilde
+    if rotation == "polar":
+        R = polar(A)
+        H = body_hessians(R, Hbar)
+        dq_tilde = np.linalg.solve(H, f[..., None])[..., 0]
+        return R, f, H, dq_tilde
+    if rotation != "length_preserving":
+        raise ValueError(rotation)
+    if np.any(~(np.linalg.det(A) > 1e-9)):
+        raise FloatingPointError("det(A) <= 1e-9 (degenerate or inverted body)")
+    At = np.swapaxes(A, -1, -2)
+    fb = f.reshape(-1, 4, 3)
+    w = length_preserving(At[:, None], fb).reshape(-1, 12)          # Alg. 1 lines 4-7
+    dp = np.linalg.solve(Hbar, w[..., None])[..., 0]                   # line 8
+    dq_tilde = length_preserving(A[:, None], dp.reshape(-1, 4, 3)).reshape(-1, 12)   # lines 9-12
+    Ai = np.linalg.inv(A)
+    D4i = np.zeros(A.shape[:-2] + (12, 12))
+    for k in range(4):
+        D4i[..., 3 * k:3 * k + 3, 3 * k:3 * k + 3] = Ai
+    H = np.swapaxes(D4i, -1, -2) @ Hbar @ D4i                         # (diag₄(A) H̄⁻¹ diag₄(Aᵀ))⁻¹
+    return A, np.einsum("nij,nj->ni", H, dq_tilde), H, dq_tilde
 
 
 def _natural_order(scene) -> bool:
     return scene.meta.get("topology") == "chain"
 
 
-def step(scene, q, qd, h, route: str = "auto", return_info: bool = False, iters: int = 1):
+def step(scene, q, qd, h, route: str = "auto", return_info: bool = False, iters: int = 1,
+         rotation: str = "polar"):
     """One implicit step: `iters` Newton iterations, each one KKT solve.
 
     iters = 1 (Table 1): linearised at qⁿ, qⁿ⁺¹ = qⁿ + δq, q̇ⁿ⁺¹ = δq/h (A6).
@@ -289,11 +338,11 @@ def step(scene, q, qd, h, route: str = "auto", return_info: bool = False, iters:
     λ = S⁻¹(∇C̃δq̃ + C(qⁿ)), δq = δq̃ − H̃⁻¹∇C̃ᵀλ), or 'auto' (SURVEY §8(c) O3 size rule).
     """
     if iters > 1:
-        return _step_iterated(scene, q, qd, h, route, return_info, iters)
+        return _step_iterated(scene, q, qd, h, route, return_info, iters, rotation)
     q = np.asarray(q, dtype=np.float64)
     qd = np.asarray(qd, dtype=np.float64)
     n = scene.n
-    R, f, H, dq_tilde = predict(scene, q, qd, h)
+    R, f, H, dq_tilde = predict(scene, q, qd, h, rotation)
     J, world = constraint_system(scene)
     m = J.shape[0]
     c = J @ q.reshape(-1) - world                      # C̃(qⁿ), footnote P:459 (SURVEY A4)
@@ -339,7 +388,7 @@ def step(scene, q, qd, h, route: str = "auto", return_info: bool = False, iters:
     return q1, qd1
 
 
-def _step_iterated(scene, q, qd, h, route, return_info, iters):
+def _step_iterated(scene, q, qd, h, route, return_info, iters, rotation="polar"):
     """K Newton iterations of one step (see ``step``): iteration i solves the KKT of the linearisation at q⁽ⁱ⁾."""
     q = np.asarray(q, dtype=np.float64)
     qd = np.asarray(qd, dtype=np.float64)
@@ -350,7 +399,7 @@ def _step_iterated(scene, q, qd, h, route, return_info, iters):
     info = None
     for i in range(iters):
         sc = scene if i == 0 else zero_g
-        qn1, v1, info = step(sc, qi, v, h, route=route, return_info=True, iters=1)
+        qn1, v1, info = step(sc, qi, v, h, route=route, return_info=True, iters=1, rotation=rotation)
         dq = qn1 - qi
         qi = qn1
         v = v - dq / h                  # v⁽ⁱ⁺¹⁾ = (q̂ − q⁽ⁱ⁺¹⁾)/h
@@ -402,11 +451,12 @@ def nonlinear_residual(scene, qn, qdn, q, h, lam=None):
     return float(np.max(np.abs(g)) / max(np.max(np.abs(inert)), 1e-300)), cres
 
 
-def simulate(scene, nsteps=None, route: str = "auto", q=None, qd=None, callback=None, iters: int = 1):
+def simulate(scene, nsteps=None, route: str = "auto", q=None, qd=None, callback=None, iters: int = 1,
+             rotation: str = "polar"):
     q = scene.q0.copy() if q is None else q
     qd = scene.qd0.copy() if qd is None else qd
     for k in range(scene.nsteps if nsteps is None else nsteps):
-        q, qd = step(scene, q, qd, scene.h, route=route, iters=iters)
+        q, qd = step(scene, q, qd, scene.h, route=route, iters=iters, rotation=rotation)
         if callback is not None:
             callback(k, q, qd)
     return q, qd

@@ -49,7 +49,9 @@ class _Options(ctypes.Structure):
     _fields_ = [("newton_iters", ctypes.c_int32), ("residual_rhs", ctypes.c_int32), ("solver", ctypes.c_int32),
                 ("rank", ctypes.c_int32), ("world", ctypes.c_int32), ("nccl_unique_id", ctypes.c_void_p),
                 ("workspace", ctypes.c_void_p), ("workspace_bytes", ctypes.c_size_t),
-                ("cuda_stream", ctypes.c_void_p), ("no_graphs", ctypes.c_int32)]
+                ("cuda_stream", ctypes.c_void_p), ("no_graphs", ctypes.c_int32), ("rotation", ctypes.c_int32)]
+
+ROTATIONS = {"polar": 0, "length_preserving": 1}
 
 
 _lib = None
@@ -130,7 +132,7 @@ def partition_info(scene, world: int, rank: int) -> dict:
                 _ptr(k["poisson"]), None, (ctypes.c_double * 3)(*[float(x) for x in np.asarray(scene.gravity)]))
     j = _Joints(K, _ptr(k["body_a"], _ip), _ptr(k["body_b"], _ip), _ptr(k["npts"], _ip), _ptr(k["ybar_a"]),
                 _ptr(k["ybar_b"]))
-    o = _Options(1, 1, 0, int(rank), int(world), None, None, 0, None, 0)
+    o = _Options(1, 1, 0, int(rank), int(world), None, None, 0, None, 0, 0)
     out = (ctypes.c_int64 * 20)()
     st = lib.mabd_partition_info(ctypes.byref(b), ctypes.byref(j), ctypes.byref(o), out, 20)
     if st != MABD_OK:
@@ -151,7 +153,8 @@ class Simulator:
 
     def __init__(self, q0, qd0, mbar, volume, youngs, poisson, gravity, body_a, body_b, npts, ybar_a, ybar_b,
                  solver: int = 0, device: Optional[int] = None, stream=None, world: int = 1, rank: int = 0,
-                 nccl_id: Optional[bytes] = None, newton_iters: int = 1, no_graphs: bool = False):
+                 nccl_id: Optional[bytes] = None, newton_iters: int = 1, no_graphs: bool = False,
+                 rotation: str = "polar"):
         import torch
 
         self._lib = load_library()
@@ -179,7 +182,8 @@ class Simulator:
             self._nccl_id = ctypes.create_string_buffer(bytes(nccl_id), 128) if nccl_id is not None else None
             opts = _Options(int(newton_iters), 1, int(solver), int(rank), int(world),
                             ctypes.cast(self._nccl_id, ctypes.c_void_p) if self._nccl_id is not None else None,
-                            None, 0, ctypes.c_void_p(self._stream.cuda_stream), int(bool(no_graphs)))
+                            None, 0, ctypes.c_void_p(self._stream.cuda_stream), int(bool(no_graphs)),
+                            ROTATIONS[rotation])
             nbytes = ctypes.c_size_t(0)
             self._check(self._lib.mabd_workspace_size(ctypes.byref(self._bodies), ctypes.byref(self._joints),
                                                       ctypes.byref(opts), ctypes.byref(nbytes)), None)

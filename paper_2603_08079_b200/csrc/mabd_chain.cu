@@ -504,7 +504,8 @@ __device__ __forceinline__ void get_hinv(const ChainArgs& a, const Material& M, 
 #define MABD_CHAIN_CTAS 4  // CTAs per SM (shared memory: 4 × 56.8 KB; TMEM: 4 × 128 columns)
 #endif
 // WRENCH: external wrenches are set (a.b.wr != nullptr); the common no-wrench instance carries no wrench code
-template <bool FINISH, bool WRENCH>
+// LP: polar-free variant (R9): R := A; phase 3 takes A from the qⁿ parked in TMEM
+template <bool FINISH, bool WRENCH, bool LP>
 __global__ void __launch_bounds__(CT, MABD_CHAIN_CTAS) chain_kernel(ChainArgs a) {
   extern __shared__ __align__(16) double smem[];
   const CRS s = cr_smem(smem);
@@ -622,7 +623,7 @@ __global__ void __launch_bounds__(CT, MABD_CHAIN_CTAS) chain_kernel(ChainArgs a)
         const double ms = msb;
         const int md = mdb;
         double W[9];
-        const bool ok = predict_body_lazy(
+        const bool ok = predict_body_lazy<LP>(
             q, [&](double* o) { tm_ld12(tbase + 48 * b + 24, o); }, M, ms,
             [&](HinvBlk& o) { get_hinv(a, M, md, ms, o); }, H, k.ih, k.grav, R, dqt,
             WRENCH ? load_wrench(a.b, base + t, W) : nullptr);
@@ -777,10 +778,19 @@ __global__ void __launch_bounds__(CT, MABD_CHAIN_CTAS) chain_kernel(ChainArgs a)
       const bool eq_real = slot_real(inf);
       const bool right_real = slot_real(infN) && slot_left(infN) == SIDE_BODY;
       double R[9], u[12];
-      tm_ld6(tbase + 96 + 12 * b, R);  // rows 0, 1 of phase 1's R; row 2 = row 0 × row 1 (det R = +1)
-      R[6] = R[1] * R[5] - R[2] * R[4];
-      R[7] = R[2] * R[3] - R[0] * R[5];
-      R[8] = R[0] * R[4] - R[1] * R[3];
+      if (LP) {  // R := A = mat(qⁿ[0:9])
+        double qa[12];
+        tm_ld12(tbase + 48 * b, qa);
+#pragma unroll
+        for (int r = 0; r < 3; ++r)
+#pragma unroll
+          for (int c = 0; c < 3; ++c) R[3 * r + c] = qa[3 * c + r];
+      } else {
+        tm_ld6(tbase + 96 + 12 * b, R);  // rows 0, 1 of phase 1's R; row 2 = row 0 × row 1 (det R = +1)
+        R[6] = R[1] * R[5] - R[2] * R[4];
+        R[7] = R[2] * R[3] - R[0] * R[5];
+        R[8] = R[0] * R[4] - R[1] * R[3];
+      }
       {
         double gq[12];
 #pragma unroll
@@ -1058,10 +1068,17 @@ cudaError_t launch_chain(const ChainArgs& a0, int nitems, bool finish, cudaStrea
   const size_t sm = chain_smem_bytes();
   const int grid = std::min(nitems, MABD_CHAIN_CTAS * std::max(g_num_sms, 1));
   const bool w = a.b.wr != nullptr;
-  if (finish)
-    (w ? chain_kernel<true, true> : chain_kernel<true, false>)<<<grid, CT, sm, st>>>(a);
-  else
-    (w ? chain_kernel<false, true> : chain_kernel<false, false>)<<<grid, CT, sm, st>>>(a);
+  if (a.k.lp) {
+    if (finish)
+      (w ? chain_kernel<true, true, true> : chain_kernel<true, false, true>)<<<grid, CT, sm, st>>>(a);
+    else
+      (w ? chain_kernel<false, true, true> : chain_kernel<false, false, true>)<<<grid, CT, sm, st>>>(a);
+  } else {
+    if (finish)
+      (w ? chain_kernel<true, true, false> : chain_kernel<true, false, false>)<<<grid, CT, sm, st>>>(a);
+    else
+      (w ? chain_kernel<false, true, false> : chain_kernel<false, false, false>)<<<grid, CT, sm, st>>>(a);
+  }
   return cudaGetLastError();
 }
 
@@ -1078,8 +1095,10 @@ cudaError_t chain_kernels_init() {
   if ((e = cudaGetDevice(&dev))) return e;
   if ((e = cudaDeviceGetAttribute(&g_num_sms, cudaDevAttrMultiProcessorCount, dev))) return e;
   const int smc = (int)chain_smem_bytes();
-  void (*const kernels[4])(ChainArgs) = {chain_kernel<true, false>, chain_kernel<false, false>,
-                                         chain_kernel<true, true>, chain_kernel<false, true>};
+  void (*const kernels[8])(ChainArgs) = {
+      chain_kernel<true, false, false>, chain_kernel<false, false, false>, chain_kernel<true, true, false>,
+      chain_kernel<false, true, false>, chain_kernel<true, false, true>,  chain_kernel<false, false, true>,
+      chain_kernel<true, true, true>,   chain_kernel<false, true, true>};
   for (auto kf : kernels) {
     if ((e = cudaFuncSetAttribute(kf, cudaFuncAttributeMaxDynamicSharedMemorySize, smc))) return e;
     // favour shared memory in the unified L1/shared carve-out so that 4 segment CTAs fit per SM

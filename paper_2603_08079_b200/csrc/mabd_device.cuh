@@ -296,7 +296,26 @@ __device__ __forceinline__ void rot_conj(const double* R, const double* P, doubl
 // W (optional, world frame [τ; f; ȳ_f]): external wrench, f_A,ext = G(A)ᵀW: ½ τ × q_c on column c, f on t;
 // f acts at the caller's frame origin, the material point ȳ_f of the canonical frame (0 unless the body was
 // re-framed at create, R8), which adds ȳ_f,c f on column c.
-template <class QdLoad, class GetH>
+// (‖v‖/‖M v‖) M v for row-major M (MT: Mᵀ v instead): Eq. len_preserving; 0 stays 0.
+template <bool MT>
+__device__ __forceinline__ void len_pres(const double* M, const double* v, double* o) {
+  double w[3];
+  if (MT)
+    mat3t_vec(M, v, w);
+  else
+    mat3_vec(M, v, w);
+  const double nv2 = v[0] * v[0] + v[1] * v[1] + v[2] * v[2];
+  const double nw2 = w[0] * w[0] + w[1] * w[1] + w[2] * w[2];
+  const double sc = nw2 > 0.0 ? sqrt(nv2) * fast_rsqrt(nw2) : 0.0;
+#pragma unroll
+  for (int e = 0; e < 3; ++e) o[e] = sc * w[e];
+}
+
+// Polar-free variant (LP = true, R9): no polar decomposition. R := A (returned, for the
+// constraint-force operator diag₄(A)H̄⁻¹diag₄(Aᵀ) of stages 3-5, "A ≈ R"); the elastic force is the StVK force
+// V vec(A Σ(E)), Σ = 2μE + λ tr(E) I, E = ½(AᵀA − I); the free solve is Alg. 1: each 3-block of f_A is
+// mapped by len_pres(Aᵀ), H̄⁻¹ applied, each block of the result mapped by len_pres(A).
+template <bool LP = false, class QdLoad, class GetH>
 __device__ __forceinline__ bool predict_body_lazy(const double* q, QdLoad qd_load, const Material& M, double mscale,
                                                   GetH get_h, HinvBlk& H, double ih, const double* grav, double* R,
                                                   double* dqt, const double* W = nullptr) {
@@ -305,6 +324,49 @@ __device__ __forceinline__ bool predict_body_lazy(const double* q, QdLoad qd_loa
   for (int r = 0; r < 3; ++r)
 #pragma unroll
     for (int c = 0; c < 3; ++c) A[3 * r + c] = q[3 * c + r];
+  if (LP) {
+    const double detA = A[0] * (A[4] * A[8] - A[5] * A[7]) - A[1] * (A[3] * A[8] - A[5] * A[6]) +
+                        A[2] * (A[3] * A[7] - A[4] * A[6]);
+    double E[9];  // ½(AᵀA − I)
+    mat3_mul_at(A, A, E);
+#pragma unroll
+    for (int i = 0; i < 9; ++i) E[i] = 0.5 * (E[i] - (i % 4 == 0 ? 1.0 : 0.0));
+    const double trE = E[0] + E[4] + E[8];
+    double Sg[9];
+#pragma unroll
+    for (int i = 0; i < 9; ++i) Sg[i] = 2.0 * M.mu * E[i] + (i % 4 == 0 ? M.lam * trE : 0.0);
+    double AS[9];  // A Σ: column c is the elastic force on column c of A (over V)
+    mat3_mul(A, Sg, AS);
+    const double ma[4] = {M.a0 * mscale * ih, M.a1 * mscale * ih, M.a2 * mscale * ih, M.m * mscale};
+    double w[12], u[12], qd[12];
+    qd_load(qd);
+#pragma unroll
+    for (int c = 0; c < 3; ++c) {
+      double fc[3];
+#pragma unroll
+      for (int r = 0; r < 3; ++r) fc[r] = ma[c] * qd[3 * c + r] - M.V * AS[3 * r + c];
+      if (W) {
+        const double* qc = q + 3 * c;
+        fc[0] += 0.5 * (W[1] * qc[2] - W[2] * qc[1]) + W[6 + c] * W[3];
+        fc[1] += 0.5 * (W[2] * qc[0] - W[0] * qc[2]) + W[6 + c] * W[4];
+        fc[2] += 0.5 * (W[0] * qc[1] - W[1] * qc[0]) + W[6 + c] * W[5];
+      }
+      len_pres<true>(A, fc, w + 3 * c);
+    }
+    {
+      double ft[3];
+#pragma unroll
+      for (int r = 0; r < 3; ++r) ft[r] = ma[3] * (qd[9 + r] * ih + grav[r]) + (W ? W[3 + r] : 0.0);
+      len_pres<true>(A, ft, w + 9);
+    }
+    get_h(H);
+    hinv_apply(H, w, u);
+#pragma unroll
+    for (int k = 0; k < 4; ++k) len_pres<false>(A, u + 3 * k, dqt + 3 * k);
+#pragma unroll
+    for (int i = 0; i < 9; ++i) R[i] = A[i];
+    return detA > 1e-9 && isfinite(detA) && isfinite(dqt[0] + dqt[4] + dqt[8] + dqt[9] + dqt[10] + dqt[11]);
+  }
   const bool ok = polar_rotation(A, R);
   // F = RᵀA, Π(F) = μ(F+Fᵀ−2I) + λ tr(F−I) I, elastic force V vec(RΠ)
   double F[9];
@@ -349,11 +411,12 @@ __device__ __forceinline__ bool predict_body_lazy(const double* q, QdLoad qd_loa
   return ok && isfinite(dqt[0] + dqt[4] + dqt[8] + dqt[9] + dqt[10] + dqt[11]);
 }
 
+template <bool LP = false>
 __device__ __forceinline__ bool predict_body(const double* q, const double* qd, const Material& M, double mscale,
                                              const HinvBlk& H, double ih, const double* grav, double* R,
                                              double* dqt, const double* W = nullptr) {
   HinvBlk Hc;
-  return predict_body_lazy(
+  return predict_body_lazy<LP>(
       q,
       [&](double* o) {
 #pragma unroll

@@ -64,6 +64,7 @@ struct StepConsts {
   double grav[3];          // gravity in the Newton r.h.s. (zero for iterations ≥ 1: q̂ carries it, see below)
   int32_t step_index;
   int32_t iter, niter;     // Newton iteration of this launch sequence, iterations per step
+  int32_t lp;              // 1: polar-free variant (options.rotation = MABD_ROTATION_LENGTH_PRESERVING, DESIGN R9)
   int32_t* err;            // [0] flags (1 nonfinite, 2 singular), [1] first failing step
 };
 

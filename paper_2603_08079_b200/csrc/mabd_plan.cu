@@ -217,6 +217,8 @@ static mabd_status validate(const mabd_bodies* B, const mabd_joints* J, const ma
     if (o->newton_iters < 0 || o->newton_iters > 16) return *msg = "newton_iters must be in [0, 16]", MABD_EINVAL;
     if (o->world > 1 && (o->rank < 0 || o->rank >= o->world)) return *msg = "rank outside [0, world)", MABD_EINVAL;
     if (o->world > 256) return *msg = "world > 256", MABD_EINVAL;
+    if (o->rotation != MABD_ROTATION_POLAR && o->rotation != MABD_ROTATION_LENGTH_PRESERVING)
+      return *msg = "rotation must be MABD_ROTATION_POLAR (0) or MABD_ROTATION_LENGTH_PRESERVING (1)", MABD_EINVAL;
     if (o->residual_rhs != 0 && o->residual_rhs != 1)
       return *msg = "residual_rhs must be 1 (0 = default = 1): -C(qn) is always in the dual rhs", MABD_EINVAL;
   }
@@ -537,6 +539,7 @@ mabd_status build_plan(const mabd_bodies* B, const mabd_joints* J, const mabd_op
   p->n = B->n;
   p->n_joints = J->n_joints;
   p->newton_iters = (o && o->newton_iters > 1) ? o->newton_iters : 1;
+  p->rotation = o ? o->rotation : MABD_ROTATION_POLAR;
   for (int i = 0; i < 3; ++i) p->grav[i] = B->gravity[i];
   std::vector<int32_t> mid;
   std::vector<double> msc;
@@ -977,6 +980,7 @@ cudaError_t launch_step(const Plan& p, const DevPtrs& d, double h, int32_t step,
   k.err = d.err;
   k.iter = 0;
   k.niter = std::max(1, p.newton_iters);
+  k.lp = p.rotation == MABD_ROTATION_LENGTH_PRESERVING ? 1 : 0;
   if (k.niter == 1) return launch_iteration(p, d, k, st);
   const int64_t tot = 12 * d.b.ld;
   const unsigned grid = (unsigned)((tot + 255) / 256);

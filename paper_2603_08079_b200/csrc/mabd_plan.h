@@ -104,6 +104,7 @@ struct Plan {
   int32_t solver = 0;
   int32_t launches_per_step = 0;
   int32_t newton_iters = 1;      // Newton iterations per step (K)
+  int32_t rotation = 0;          // MABD_ROTATION_* (options.rotation)
   double grav[3] = {0, 0, 0};
   // bodies
   std::vector<Material> mats;

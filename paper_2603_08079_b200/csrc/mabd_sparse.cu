@@ -62,7 +62,9 @@ __global__ void sparse_predict_kernel(SparseArgs a) {
     else
       hinv_blocks(M, msc, a.k.ih2, H);
     double W[9];
-    if (!predict_body(q, qd, M, msc, H, a.k.ih, a.k.grav, R, dqt, load_wrench(a.b, j, W)))
+    const double* Wp = load_wrench(a.b, j, W);
+    if (!(a.k.lp ? predict_body<true>(q, qd, M, msc, H, a.k.ih, a.k.grav, R, dqt, Wp)
+                 : predict_body<false>(q, qd, M, msc, H, a.k.ih, a.k.grav, R, dqt, Wp)))
       sreport(a.k, ERR_NONFINITE);
 #pragma unroll
     for (int c = 0; c < 9; ++c) a.b.rs[c * ld + j] = R[c];

@@ -195,7 +195,10 @@ __device__ void tree_predict_core(const TreeArgs& a, int b, double* R, double* q
   else
     hinv_blocks(M, msc, k.ih2, H);
   double W[9];
-  if (!predict_body(q, qd, M, msc, H, k.ih, k.grav, R, dqt, load_wrench(a.b, b, W))) treport(k, ERR_NONFINITE);
+  const double* Wp = load_wrench(a.b, b, W);
+  if (!(k.lp ? predict_body<true>(q, qd, M, msc, H, k.ih, k.grav, R, dqt, Wp)
+             : predict_body<false>(q, qd, M, msc, H, k.ih, k.grav, R, dqt, Wp)))
+    treport(k, ERR_NONFINITE);
   double* sc = a.bscr + b;  // [21][ld]: component c at sc[c·ld]
 #pragma unroll
   for (int c = 0; c < 9; ++c) sc[c * ld] = R[c];

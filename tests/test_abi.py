@@ -138,3 +138,17 @@ def test_residual_rhs_option(lib):
     for rr, want in ((0, 0), (1, 0), (2, 1), (-1, 1)):
         o = _Options(1, rr, 0, 0, 1, None, None, 0, None, 0)
         assert lib.mabd_workspace_size(ctypes.byref(b), ctypes.byref(j), ctypes.byref(o), ctypes.byref(n)) == want
+
+
+def test_rotation_option(lib):
+    """options.rotation: 0 (exact polar) and 1 (polar-free Alg. 1 variant, DESIGN R9) are valid, others are not."""
+    from paper_2603_08079_b200.binding import _Bodies, _Joints, _Options, _ptr, _ip
+    sc = G.random_chain(5, seed=1)
+    b = _Bodies(sc.n, _ptr(sc.q0), _ptr(sc.qd0), _ptr(sc.mbar), _ptr(sc.volume), _ptr(sc.youngs), _ptr(sc.poisson),
+                None, (ctypes.c_double * 3)(*sc.gravity))
+    j = _Joints(sc.n_joints, _ptr(sc.body_a, _ip), _ptr(sc.body_b, _ip), _ptr(sc.npts, _ip), _ptr(sc.ybar_a),
+                _ptr(sc.ybar_b))
+    n = ctypes.c_size_t()
+    for rot, want in ((0, 0), (1, 0), (2, 1), (-1, 1)):
+        o = _Options(1, 1, 0, 0, 1, None, None, 0, None, 0, rot)
+        assert lib.mabd_workspace_size(ctypes.byref(b), ctypes.byref(j), ctypes.byref(o), ctypes.byref(n)) == want

@@ -540,3 +540,77 @@ def test_P12_material_frame_covariance(maker):
     qu, qdu = O.simulate(u, steps)
     assert O.rel_err(G.frame_to_canonical(qu, u.frames), q) < tol
     assert O.rel_err(G.frame_to_canonical(qdu * sc.h, u.frames), qd * sc.h) < tol
+
+
+# ----------------------------------------------------------------------------- polar-free variant (NEXT 4, R9)
+
+def _stvk_energy(A, V, mu, lam):
+    """V[μ‖E‖² + (λ/2)tr(E)²], E = ½(AᵀA − I): Saint Venant–Kirchhoff, written out independently."""
+    E = 0.5 * (A.T @ A - np.eye(3))
+    return V * (mu * np.sum(E * E) + 0.5 * lam * np.trace(E) ** 2)
+
+
+def test_R9_stvk_force_is_fd_gradient_with_rest_hessian_kbar():
+    """The polar-free elastic force is the gradient of the StVK energy, and its Jacobian at A = I is K̄_A — the same
+    pre-factored H̄ serves both variants."""
+    rng = np.random.default_rng(21)
+    V, mu, lam = 2e-3, *O.lame(1e8, 0.3)
+    for _ in range(4):
+        A = G.random_rotations(rng, 1)[0] @ (np.eye(3) + 0.05 * rng.standard_normal((3, 3)))
+        f = O.stvk_force_A(A, V, mu, lam)
+        eps = 1e-7
+        g = np.array([(_stvk_energy(O.unvec(O.vec(A) + eps * e), V, mu, lam)
+                       - _stvk_energy(O.unvec(O.vec(A) - eps * e), V, mu, lam)) / (2 * eps) for e in np.eye(9)])
+        assert np.max(np.abs(f - g)) <= 1e-7 * np.max(np.abs(g))
+    eps = 1e-6
+    J = np.array([(O.stvk_force_A(O.unvec(O.vec(np.eye(3)) + eps * e), V, mu, lam)
+                   - O.stvk_force_A(O.unvec(O.vec(np.eye(3)) - eps * e), V, mu, lam)) / (2 * eps) for e in np.eye(9)]).T
+    K = O.kbar_A(V, mu, lam)[:9, :9]
+    assert np.max(np.abs(J - K)) <= 1e-6 * np.max(np.abs(K))
+
+
+def test_R9_length_preserving_map():
+    """Eq. len_preserving: the image has the length of v, and a rotation is reproduced exactly."""
+    rng = np.random.default_rng(22)
+    M = np.eye(3) + 0.3 * rng.standard_normal((5, 3, 3))
+    v = rng.standard_normal((5, 3))
+    w = O.length_preserving(M, v)
+    assert np.allclose(np.linalg.norm(w, axis=1), np.linalg.norm(v, axis=1), rtol=1e-14)
+    assert np.allclose(np.cross(w, np.einsum("nij,nj->ni", M, v)), 0, atol=1e-13)   # parallel to M v
+    R = G.random_rotations(rng, 5)
+    assert np.allclose(O.length_preserving(R, v), np.einsum("nij,nj->ni", R, v), atol=1e-15)
+    assert np.all(O.length_preserving(M, np.zeros((5, 3))) == 0)
+
+
+@pytest.mark.parametrize("maker", ["chain", "tree"])
+def test_R9_polar_free_equals_exact_at_rigid_states(maker):
+    """At a rigid state (every A ∈ SO(3)) Alg. 1's maps are the rotations themselves, the StVK and co-rotated forces
+    both vanish and diag₄(A)H̄⁻¹diag₄(Aᵀ) = H_A⁻¹: one polar-free step equals one exact step."""
+    sc = {"chain": lambda: G.random_chain(9, seed=23, vel=0.4, end_anchor=True, jitter=1e-3),
+          "tree": lambda: G.random_tree(12, seed=24, vel=0.4, jitter=1e-3)}[maker]()
+    q1, qd1 = O.step(sc, sc.q0, sc.qd0, sc.h)
+    q2, qd2 = O.step(sc, sc.q0, sc.qd0, sc.h, rotation="length_preserving")
+    assert O.rel_err(q2, q1) < 1e-13 and O.rel_err(qd2 * sc.h, qd1 * sc.h) < 1e-13
+
+
+def test_R9_polar_free_closure_equivariance_and_rest():
+    """The polar-free step on strained states: joints close (P3), a rigid motion of the scene moves the result with
+    it (P6: Alg. 1's maps are rotation-equivariant), and it differs from the exact step (the variant is not exact
+    away from SO(3))."""
+    sc = G.random_chain(10, seed=25, vel=0.3, npts=2, jitter=1e-3)
+    A = O.unvec(sc.q0[:, :9]) @ (np.eye(3) + 0.03 * np.random.default_rng(26).standard_normal((sc.n, 3, 3)))
+    sc.q0[:, :9] = O.vec(A)
+    q1, _ = O.step(sc, sc.q0, sc.qd0, sc.h, rotation="length_preserving")
+    assert O.constraint_residual(sc, q1) < 1e-10
+    qe, _ = O.step(sc, sc.q0, sc.qd0, sc.h)
+    assert O.rel_err(q1, qe) > 1e-6
+    Q = G.random_rotations(np.random.default_rng(27), 1)[0]
+    d = np.array([0.3, 0.2, -0.1])
+    s2 = _rotate_scene(sc, Q, d)
+    q2, _ = O.step(s2, s2.q0, s2.qd0, s2.h, rotation="length_preserving")
+    assert np.max(np.abs(O.unvec(q2[:, :9]) - Q @ O.unvec(q1[:, :9]))) < 1e-12
+    assert np.max(np.abs(q2[:, 9:] - (q1[:, 9:] @ Q.T + d))) < 1e-11
+    # rest: unstrained, at rest, no gravity, joints satisfied → nothing moves
+    r = G.random_chain(6, seed=28, vel=0.0, gravity=False)
+    q3, qd3 = O.step(r, r.q0, r.qd0, r.h, rotation="length_preserving")
+    assert np.max(np.abs(q3 - r.q0)) < 1e-14 and np.max(np.abs(qd3)) < 1e-12
