@@ -218,9 +218,9 @@ def run_ours(args, rank: int, world: int, local_rank: int) -> None:
             blob.copy_(torch.frombuffer(bytearray(nccl_unique_id()), dtype=torch.uint8))
         dist.broadcast(blob, src=0)
         sim = Simulator.from_scene(sc, device=local_rank, stream=stream, world=world, rank=rank,
-                                   nccl_id=bytes(blob.cpu().tolist()))
+                                   nccl_id=bytes(blob.cpu().tolist()), rotation=args.rotation)
     else:
-        sim = Simulator.from_scene(sc, device=local_rank, stream=stream)
+        sim = Simulator.from_scene(sc, device=local_rank, stream=stream, rotation=args.rotation)
     sim.prefactor(h)
     q0 = sc.q0.copy()
     qd0 = sc.qd0.copy()
@@ -306,7 +306,7 @@ def run_ours(args, rank: int, world: int, local_rank: int) -> None:
     streams = [stream]
     for _ in range(n_pipe - 1):
         s2 = torch.cuda.Stream(device=dev)
-        sims.append(Simulator.from_scene(sc, device=local_rank, stream=s2))
+        sims.append(Simulator.from_scene(sc, device=local_rank, stream=s2, rotation=args.rotation))
         sims[-1].prefactor(h)
         streams.append(s2)
     bufs = []
@@ -376,7 +376,9 @@ def run_ours(args, rank: int, world: int, local_rank: int) -> None:
             "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": True,
             "scaling": "strong" if split else "weak",
             "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-            "config": {"workload": CFG_TEXT[args.config], "bodies": n, "bodies_per_gpu": n_rank,
+            "config": {"workload": CFG_TEXT[args.config] + ("" if args.rotation == "polar" else
+                                                              ", polar-free variant (Alg. 1, DESIGN R9)"),
+                       "bodies": n, "bodies_per_gpu": n_rank,
                        "solver": info["solver"], "episode_steps": episode,
                        "timing": f"{args.steps} steps as episodes of <= {episode} steps from the initial state "
                                  "(reset between episodes, outside the CUDA-event intervals); each step replays "
@@ -424,6 +426,8 @@ def main():
     ap.add_argument("--e2e-steps", type=int, default=5)
     ap.add_argument("--cpu-steps", type=int, default=10)
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--rotation", default="polar", choices=["polar", "length_preserving"],
+                    help="length_preserving: the polar-free variant (P:283-310, DESIGN R9); not the default workload")
     args = ap.parse_args()
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))

@@ -188,8 +188,9 @@ def affine_force(q, qd, mbar, V, E, nu, g, h, rotation: str = "polar") -> np.nda
     grav = np.zeros(q.shape)
     grav[..., 9:12] = g
     f = np.einsum("...ij,...j->...i", MA, np.asarray(qd) / h + grav)
-    el = elastic_force_A if rotation == "polar" else stvk_force_A
-    f[..., :9] -= el(unvec(q[..., :9]), V, mu, lam)
+    if rotation != "none":  # "none": inertia and gravity only (the polar-free variant adds its elastic term itself)
+        el = elastic_force_A if rotation == "polar" else stvk_force_A
+        f[..., :9] -= el(unvec(q[..., :9]), V, mu, lam)
     return f
 
 
@@ -284,14 +285,18 @@ def predict(scene, q, qd, h, rotation: str = "polar"):
     """Per-body stages 1-2: R, f_A, H_j, and δq̃ = H_j⁻¹ f_A (Alg. 1 with exact R).
 
     rotation = "length_preserving" (R9): no polar decomposition. The free solve is
-    Alg. 1 as printed: each 3-block f_k of f_A → (‖f_k‖/‖Aᵀf_k‖)Aᵀf_k, solve H̄δp = f, each δp_k →
-    (‖δp_k‖/‖Aδp_k‖)Aδp_k; the elastic force is ``stvk_force_A``; the operator that carries constraint forces
+    Alg. 1 on the world-frame forces of f_A (inertia, gravity, wrench: Alg. 1's J̄ᵀf): each 3-block f_k
+    → (‖f_k‖/‖Aᵀf_k‖)Aᵀf_k; the elastic force enters in the body frame as the StVK stress, −V Σ(E) on the A-blocks
+    (the co-rotated method's −V Π, with Σ = 2μE + λ tr(E) I, E = ½(AᵀA − I): the body-frame image of
+    ``stvk_force_A``); solve H̄δp = w; each δp_k → (‖δp_k‖/‖Aδp_k‖)Aδp_k. The operator that carries constraint forces
     (stages 3-5) is H̃_j⁻¹ = diag₄(A)H̄⁻¹diag₄(Aᵀ) ("A ≈ R"). Returned as (A, H̃_j δq̃, H̃_j, δq̃), so that every
     KKT route solves [H̃ ∇Cᵀ; ∇C 0][δq; λ] = [H̃δq̃; −C(qⁿ)], i.e. δq = δq̃ − H̃⁻¹∇Cᵀλ with S λ = C(q̃).
     """
     q = np.asarray(q, dtype=np.float64)
     A = unvec(q[:, :9])
-    f = affine_force(q, qd, scene.mbar, scene.volume, scene.youngs, scene.poisson, scene.gravity, h, rotation)
+    lp = rotation == "length_preserving"
+    f = affine_force(q, qd, scene.mbar, scene.volume, scene.youngs, scene.poisson, scene.gravity, h,
+                     "none" if lp else rotation)
     if getattr(scene, "wrench", None) is not None:  # at the linearisation point (P:676)
         f = f + wrench_force(q, scene.wrench)
     Hbar = hbar_A(scene.mbar, scene.volume, scene.youngs, scene.poisson, h)
@@ -307,6 +312,10 @@ def predict(scene, q, qd, h, rotation: str = "polar"):
     At = np.swapaxes(A, -1, -2)
     fb = f.reshape(-1, 4, 3)
     w = length_preserving(At[:, None], fb).reshape(-1, 12)          # Alg. 1 lines 4-7
+    mu, lam = lame(scene.youngs, scene.poisson)
+    E = 0.5 * (At @ A - np.eye(3))
+    Sig = 2.0 * mu[:, None, None] * E + (lam * np.trace(E, axis1=1, axis2=2))[:, None, None] * np.eye(3)
+    w[:, :9] -= np.asarray(scene.volume)[:, None] * vec(Sig)       # body-frame elastic stress
     dp = np.linalg.solve(Hbar, w[..., None])[..., 0]                   # line 8
     dq_tilde = length_preserving(A[:, None], dp.reshape(-1, 4, 3)).reshape(-1, 12)   # lines 9-12
     Ai = np.linalg.inv(A)

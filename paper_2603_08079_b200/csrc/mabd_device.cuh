@@ -312,9 +312,10 @@ __device__ __forceinline__ void len_pres(const double* M, const double* v, doubl
 }
 
 // Polar-free variant (LP = true, R9): no polar decomposition. R := A (returned, for the
-// constraint-force operator diag₄(A)H̄⁻¹diag₄(Aᵀ) of stages 3-5, "A ≈ R"); the elastic force is the StVK force
-// V vec(A Σ(E)), Σ = 2μE + λ tr(E) I, E = ½(AᵀA − I); the free solve is Alg. 1: each 3-block of f_A is
-// mapped by len_pres(Aᵀ), H̄⁻¹ applied, each block of the result mapped by len_pres(A).
+// constraint-force operator diag₄(A)H̄⁻¹diag₄(Aᵀ) of stages 3-5, "A ≈ R"); the free solve is Alg. 1
+// on the world-frame forces (inertia, gravity, wrench): each 3-block mapped by len_pres(Aᵀ); the elastic
+// term enters in the body frame as the StVK stress −V Σ(E), Σ = 2μE + λ tr(E) I, E = ½(AᵀA − I) (the co-rotated
+// method's −V Π); then H̄⁻¹, then each block of the result mapped by len_pres(A).
 template <bool LP = false, class QdLoad, class GetH>
 __device__ __forceinline__ bool predict_body_lazy(const double* q, QdLoad qd_load, const Material& M, double mscale,
                                                   GetH get_h, HinvBlk& H, double ih, const double* grav, double* R,
@@ -335,8 +336,6 @@ __device__ __forceinline__ bool predict_body_lazy(const double* q, QdLoad qd_loa
     double Sg[9];
 #pragma unroll
     for (int i = 0; i < 9; ++i) Sg[i] = 2.0 * M.mu * E[i] + (i % 4 == 0 ? M.lam * trE : 0.0);
-    double AS[9];  // A Σ: column c is the elastic force on column c of A (over V)
-    mat3_mul(A, Sg, AS);
     const double ma[4] = {M.a0 * mscale * ih, M.a1 * mscale * ih, M.a2 * mscale * ih, M.m * mscale};
     double w[12], u[12], qd[12];
     qd_load(qd);
@@ -344,7 +343,7 @@ __device__ __forceinline__ bool predict_body_lazy(const double* q, QdLoad qd_loa
     for (int c = 0; c < 3; ++c) {
       double fc[3];
 #pragma unroll
-      for (int r = 0; r < 3; ++r) fc[r] = ma[c] * qd[3 * c + r] - M.V * AS[3 * r + c];
+      for (int r = 0; r < 3; ++r) fc[r] = ma[c] * qd[3 * c + r];
       if (W) {
         const double* qc = q + 3 * c;
         fc[0] += 0.5 * (W[1] * qc[2] - W[2] * qc[1]) + W[6 + c] * W[3];
@@ -352,6 +351,8 @@ __device__ __forceinline__ bool predict_body_lazy(const double* q, QdLoad qd_loa
         fc[2] += 0.5 * (W[0] * qc[1] - W[1] * qc[0]) + W[6 + c] * W[5];
       }
       len_pres<true>(A, fc, w + 3 * c);
+#pragma unroll
+      for (int r = 0; r < 3; ++r) w[3 * c + r] -= M.V * Sg[3 * r + c];
     }
     {
       double ft[3];
