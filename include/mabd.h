@@ -95,7 +95,9 @@ typedef struct {
                                 bytes per body of workspace and K + 2 times the launches              */
   int32_t residual_rhs;      /* 1 (0 = default = 1): include −C(qⁿ) in the dual rhs (footnote P:459,
                                 DESIGN.md reading A4); any other value → MABD_EINVAL                  */
-  int32_t solver;            /* 0 auto | 1 chain | 2 tree | 3 sparse                               */
+  int32_t solver;            /* 0 auto | 1 chain | 2 tree | 3 sparse | 4 line Gauss-Seidel (the paper's
+                                Case IV; R10: an iterative dual solve, never chosen by
+                                auto; converged to gs_tol, warm-started from the previous step's λ)     */
   int32_t rank, world;       /* multi-GPU; world = 1 → single GPU                                  */
   const void *nccl_unique_id;/* 128-byte ncclUniqueId, or NULL when world = 1                      */
   void *workspace;           /* device memory from the caller (torch), or NULL                     */
@@ -110,12 +112,14 @@ typedef struct {
                                 length-preserving Aᵀ / A of Eq. len_preserving, the elastic force is the StVK
                                 force of E = ½(AᵀA − I), and constraint forces use diag₄(A)H̄⁻¹diag₄(Aᵀ)
                                 ("A ≈ R"). Equal to (0) at rigid states; an approximation otherwise. */
+  int32_t gs_sweeps;         /* solver 4: maximum sweeps per step (0 = 200)                           */
+  double gs_tol;             /* solver 4: stop when max|C(q̃) − Sλ| ≤ gs_tol · max|C(q̃)| (0 = 1e-12)   */
 } mabd_options;
 
 enum { MABD_ROTATION_POLAR = 0, MABD_ROTATION_LENGTH_PRESERVING = 1 };
 
 /* Topology/solver actually selected (mabd_query). */
-enum { MABD_SOLVER_CHAIN = 1, MABD_SOLVER_TREE = 2, MABD_SOLVER_SPARSE = 3 };
+enum { MABD_SOLVER_CHAIN = 1, MABD_SOLVER_TREE = 2, MABD_SOLVER_SPARSE = 3, MABD_SOLVER_LINE_GS = 4 };
 
 /* Device bytes mabd_create will sub-allocate for these inputs (host analysis only; no GPU work). */
 mabd_status mabd_workspace_size(const mabd_bodies *bodies, const mabd_joints *joints,
@@ -180,8 +184,16 @@ mabd_status mabd_partition_info(const mabd_bodies *bodies, const mabd_joints *jo
  * numeric factorization (fp64, SYRK counted as the full square), task-list ints, launches per step, dual rows}. */
 mabd_status mabd_sparse_plan_stats(const mabd_bodies *bodies, const mabd_joints *joints, double *out);
 
-/* Statistics of the last mabd_step call: iterative-refinement passes of the sparse solver's direct dual solve
- * (0 for the chain and tree solvers). Synchronises the handle's stream. */
+/* Host-only plan of the line Gauss-Seidel solver (solver 4; R10) for a scene: counts = {points, chains,
+ * colours}; when the arrays are non-NULL they receive the joint points in chain order ([points], point index = the
+ * running index over the joints' points), the chain offsets ([chains + 1]) and the colour offsets into the chains
+ * ([colours + 1]). Call once with NULL arrays for the sizes. No device work. */
+mabd_status mabd_line_gs_plan(const mabd_bodies *bodies, const mabd_joints *joints, int32_t *chain_pts,
+                              int32_t *chain_off, int32_t *color_off, int64_t *counts);
+
+/* Statistics of the last step: the sparse solver's configured iterative-refinement passes of its direct dual
+ * solve; the line Gauss-Seidel solver's sweeps run in the last step; 0 for the chain and tree solvers.
+ * Synchronises the handle's stream. */
 mabd_status mabd_solver_stats(mabd_handle h_, int64_t *last_iterations);
 
 /* Release device memory owned by the library; NULL is a no-op. */

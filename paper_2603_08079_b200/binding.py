@@ -17,7 +17,7 @@ LIB_PATH = os.environ.get("MABD_LIB") or os.path.join(_PKG, "libmabd.so")
 MABD_OK = 0
 STATUS = {0: "MABD_OK", 1: "MABD_EINVAL", 2: "MABD_ESTATE", 3: "MABD_ENOMEM", 4: "MABD_ECUDA", 5: "MABD_ENCCL",
           6: "MABD_ESINGULAR", 7: "MABD_ENONFINITE", 8: "MABD_EUNSUPPORTED"}
-SOLVERS = {0: "auto", 1: "chain", 2: "tree", 3: "sparse"}
+SOLVERS = {0: "auto", 1: "chain", 2: "tree", 3: "sparse", 4: "line_gs"}
 
 EXPORTED = ["mabd_workspace_size", "mabd_create", "mabd_prefactor", "mabd_step", "mabd_step_async", "mabd_check",
             "mabd_get_state",
@@ -49,7 +49,8 @@ class _Options(ctypes.Structure):
     _fields_ = [("newton_iters", ctypes.c_int32), ("residual_rhs", ctypes.c_int32), ("solver", ctypes.c_int32),
                 ("rank", ctypes.c_int32), ("world", ctypes.c_int32), ("nccl_unique_id", ctypes.c_void_p),
                 ("workspace", ctypes.c_void_p), ("workspace_bytes", ctypes.c_size_t),
-                ("cuda_stream", ctypes.c_void_p), ("no_graphs", ctypes.c_int32), ("rotation", ctypes.c_int32)]
+                ("cuda_stream", ctypes.c_void_p), ("no_graphs", ctypes.c_int32), ("rotation", ctypes.c_int32),
+                ("gs_sweeps", ctypes.c_int32), ("gs_tol", ctypes.c_double)]
 
 ROTATIONS = {"polar": 0, "length_preserving": 1}
 
@@ -154,7 +155,7 @@ class Simulator:
     def __init__(self, q0, qd0, mbar, volume, youngs, poisson, gravity, body_a, body_b, npts, ybar_a, ybar_b,
                  solver: int = 0, device: Optional[int] = None, stream=None, world: int = 1, rank: int = 0,
                  nccl_id: Optional[bytes] = None, newton_iters: int = 1, no_graphs: bool = False,
-                 rotation: str = "polar"):
+                 rotation: str = "polar", gs_sweeps: int = 0, gs_tol: float = 0.0):
         import torch
 
         self._lib = load_library()
@@ -183,7 +184,7 @@ class Simulator:
             opts = _Options(int(newton_iters), 1, int(solver), int(rank), int(world),
                             ctypes.cast(self._nccl_id, ctypes.c_void_p) if self._nccl_id is not None else None,
                             None, 0, ctypes.c_void_p(self._stream.cuda_stream), int(bool(no_graphs)),
-                            ROTATIONS[rotation])
+                            ROTATIONS[rotation], int(gs_sweeps), float(gs_tol))
             nbytes = ctypes.c_size_t(0)
             self._check(self._lib.mabd_workspace_size(ctypes.byref(self._bodies), ctypes.byref(self._joints),
                                                       ctypes.byref(opts), ctypes.byref(nbytes)), None)

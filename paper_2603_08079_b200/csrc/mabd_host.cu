@@ -122,7 +122,8 @@ mabd_status mabd_create(const mabd_bodies* bodies, const mabd_joints* joints, co
   c->use_graphs = c->stream != nullptr && !(opts && opts->no_graphs);
   e = cudaMallocHost(&c->h_err, 4 * sizeof(int32_t));
   if (e == cudaSuccess) e = chain_kernels_init();
-  if (e == cudaSuccess && c->plan.solver == MABD_SOLVER_SPARSE) e = sparse_init();
+  if (e == cudaSuccess && (c->plan.solver == MABD_SOLVER_SPARSE || c->plan.solver == MABD_SOLVER_LINE_GS))
+    e = sparse_init();
   if (e == cudaSuccess && c->plan.solver == MABD_SOLVER_TREE) e = tree_init();
   if (e == cudaSuccess) e = upload_plan(c->plan, c->ws, c->stream, &c->d);
   if (e == cudaSuccess) e = reset_err(c->d, c->stream);
@@ -337,7 +338,7 @@ mabd_status mabd_solver_stats(mabd_handle c, int64_t* last_iterations) {
   if (!c) return fail(nullptr, MABD_EINVAL, "NULL handle");
   if (!last_iterations) return fail(c, MABD_EINVAL, "last_iterations is NULL");
   *last_iterations = 0;
-  if (c->plan.solver == MABD_SOLVER_SPARSE) {
+  if (c->plan.solver == MABD_SOLVER_SPARSE || c->plan.solver == MABD_SOLVER_LINE_GS) {
     int32_t it = 0;
     CUDA_TRY(c, cudaSetDevice(c->device));
     CUDA_TRY(c, cudaMemcpyAsync(&it, c->d.sparse.iters, sizeof(int32_t), cudaMemcpyDeviceToHost, c->stream));

@@ -114,6 +114,20 @@ struct MfArgs {
   const int64_t* woff;         // [nnode]
 };
 
+// Line Gauss-Seidel on the dual (the paper's Case IV; R10): the joint
+// points are covered by "chains" (paths in the body graph: consecutive points share a body, no other two do), whose
+// dual blocks are block tridiagonal; chains are coloured so that one colour's chains share no body. A sweep relaxes
+// the colours in turn, every chain of a colour solved exactly (block Thomas) in parallel, one thread per chain.
+struct GsArgs {
+  const int32_t* chain_pts;    // [np] points in chain order (chains contiguous, colours contiguous)
+  const int32_t* chain_off;    // [nchain+1] into chain_pts
+  const int32_t* color_off;    // [ncolor+1] chain ranges per colour
+  double* fac;                 // [24][np] per chain position: D'⁻¹ (6, sym), L (9), B (9, coupling to the next)
+  unsigned long long* resmax;  // [2 + max_sweeps] (doubles ≥ 0 as bits): [0] max|r|, [1 + s] max|residual| of sweep s
+  int32_t ncolor, max_sweeps;
+  double tol;                  // stop when max|residual| ≤ tol · max|r|
+};
+
 struct SparseArgs {
   BodyArrays b;
   const HinvBlk* hinv_tab;     // per material, or null (per-body mass scale)
@@ -128,6 +142,7 @@ struct SparseArgs {
   double* dqt;                 // [12][n] δq̃ of the step (predict → rhs, update)
   int32_t* iters;              // refinement passes of the last solve
   MfArgs mf;
+  GsArgs gs;
   StepConsts k;
 };
 

@@ -217,6 +217,8 @@ static mabd_status validate(const mabd_bodies* B, const mabd_joints* J, const ma
     if (o->newton_iters < 0 || o->newton_iters > 16) return *msg = "newton_iters must be in [0, 16]", MABD_EINVAL;
     if (o->world > 1 && (o->rank < 0 || o->rank >= o->world)) return *msg = "rank outside [0, world)", MABD_EINVAL;
     if (o->world > 256) return *msg = "world > 256", MABD_EINVAL;
+    if (o->solver < 0 || o->solver > MABD_SOLVER_LINE_GS) return *msg = "unknown solver", MABD_EINVAL;
+    if (o->gs_sweeps < 0 || !(o->gs_tol >= 0.0)) return *msg = "gs_sweeps and gs_tol must be >= 0", MABD_EINVAL;
     if (o->rotation != MABD_ROTATION_POLAR && o->rotation != MABD_ROTATION_LENGTH_PRESERVING)
       return *msg = "rotation must be MABD_ROTATION_POLAR (0) or MABD_ROTATION_LENGTH_PRESERVING (1)", MABD_EINVAL;
     if (o->residual_rhs != 0 && o->residual_rhs != 1)
@@ -566,6 +568,11 @@ mabd_status build_plan(const mabd_bodies* B, const mabd_joints* J, const mabd_op
     if (!ok && req == MABD_SOLVER_TREE) return *msg = "tree solver requested: " + why2, MABD_EINVAL;
     if (!ok) why += "; " + why2;
   }
+  if (!ok && req == MABD_SOLVER_LINE_GS) {  // the paper's Case IV, any topology
+    ok = sparse_build(B, J, p, &pos, &why, false) && gs_build(B, p, o->gs_sweeps, o->gs_tol, &why);
+    if (!ok) return *msg = "line Gauss-Seidel: " + why, MABD_EINVAL;
+    p->solver = MABD_SOLVER_LINE_GS;
+  }
   if (!ok && (req == 0 || req == MABD_SOLVER_SPARSE)) {
     std::string why3;
     ok = sparse_build(B, J, p, &pos, &why3);
@@ -582,7 +589,7 @@ mabd_status build_plan(const mabd_bodies* B, const mabd_joints* J, const mabd_op
     p->use_nccl = o->nccl_unique_id != nullptr;
     if (!tree_partition(p, W, o->rank, !p->use_nccl, msg)) return MABD_EINVAL;
   }
-  if (o && o->world > 1 && p->solver == MABD_SOLVER_SPARSE)
+  if (o && o->world > 1 && (p->solver == MABD_SOLVER_SPARSE || p->solver == MABD_SOLVER_LINE_GS))
     return *msg = "world > 1 is implemented for the chain and tree solvers (run nets as replicas)",
            MABD_EUNSUPPORTED;
   // per-position arrays
@@ -692,7 +699,7 @@ mabd_status build_plan(const mabd_bodies* B, const mabd_joints* J, const mabd_op
     f.t_rslot = take(sizeof(int32_t) * std::max<size_t>(1, t.root_slot.size()));
     f.t_xbuf = take(sizeof(double) * 42 * (size_t)std::max(1, t.parts * t.rpp));
   }
-  if (p->solver == MABD_SOLVER_SPARSE) sparse_layout(p, take);
+  if (p->solver == MABD_SOLVER_SPARSE || p->solver == MABD_SOLVER_LINE_GS) sparse_layout(p, take);
   p->workspace_bytes = cur;
   return MABD_OK;
 }
@@ -835,7 +842,7 @@ cudaError_t upload_plan(const Plan& p, char* ws, cudaStream_t st, DevPtrs* d) {
     if ((e = put((int32_t*)A.up_row, t.up_row, st))) return e;
     if ((e = cudaMemsetAsync(A.lam, 0, sizeof(double) * 6 * std::max<int64_t>(1, p.n_joints), st))) return e;
   }
-  if (p.solver == MABD_SOLVER_SPARSE) return sparse_upload(p, ws, st, d);
+  if (p.solver == MABD_SOLVER_SPARSE || p.solver == MABD_SOLVER_LINE_GS) return sparse_upload(p, ws, st, d);
   return cudaSuccess;
 }
 
@@ -999,6 +1006,7 @@ cudaError_t launch_step(const Plan& p, const DevPtrs& d, double h, int32_t step,
 static cudaError_t launch_iteration(const Plan& p, const DevPtrs& d, const StepConsts& k, cudaStream_t st) {
   if (p.solver == MABD_SOLVER_TREE) return tree_step(p, d, k, st);
   if (p.solver == MABD_SOLVER_SPARSE) return sparse_step(p, d, k, st);
+  if (p.solver == MABD_SOLVER_LINE_GS) return gs_step(p, d, k, st);
   if (p.solver != MABD_SOLVER_CHAIN) return cudaErrorNotSupported;
   ChainArgs a;
   a.b = d.b;

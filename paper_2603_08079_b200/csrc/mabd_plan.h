@@ -92,6 +92,11 @@ struct SparsePlan {
   std::vector<int64_t> loff;                             // [nnode] inverse diagonal blocks of big fronts
   int64_t linv_doubles = 0;
   int32_t refine = 1;                                    // iterative-refinement passes per step
+  // line Gauss-Seidel (MABD_SOLVER_LINE_GS; gs_build in mabd_sparse.cu)
+  std::vector<int32_t> gs_chain_pts, gs_chain_off, gs_color_off;
+  int32_t gs_ncolor = 0, gs_sweeps = 0;
+  double gs_tol = 0.0;
+  size_t o_gs_pts = 0, o_gs_off = 0, o_gs_col = 0, o_gs_fac = 0, o_gs_res = 0;
   int32_t max_f = 0;
   size_t o_pa = 0, o_pb = 0, o_py = 0, o_incoff = 0, o_inc = 0, o_vec = 0, o_vv = 0, o_dqt = 0, o_iters = 0;
   size_t o_F = 0, o_foff = 0, o_fdim = 0, o_nown = 0, o_ownf = 0, o_choff = 0, o_ch = 0, o_eaoff = 0, o_eamap = 0,
@@ -205,8 +210,10 @@ cudaError_t tree_init();
 bool tree_partition(Plan* p, int W, int rank, bool emulate, std::string* msg);
 
 // sparse solver (mabd_sparse.cu)
+bool gs_build(const mabd_bodies* bodies, Plan* p, int32_t sweeps, double tol, std::string* msg);
+cudaError_t gs_step(const Plan& p, const DevPtrs& d, const StepConsts& k, cudaStream_t st);
 bool sparse_build(const mabd_bodies* bodies, const mabd_joints* joints, Plan* p, std::vector<int64_t>* pos_of_body,
-                  std::string* msg);
+                  std::string* msg, bool symbolic = true);
 void sparse_layout(Plan* p, const std::function<size_t(size_t)>& take);
 cudaError_t sparse_upload(const Plan& p, char* ws, cudaStream_t st, DevPtrs* d);
 cudaError_t sparse_init();

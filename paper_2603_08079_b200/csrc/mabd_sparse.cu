@@ -926,6 +926,203 @@ cudaError_t sparse_step(const Plan& p, const DevPtrs& d, const StepConsts& k, cu
   return cudaGetLastError();
 }
 
+// ============================================================================ line Gauss-Seidel (Case IV)
+// S_pq for two joint points: Σ over the bodies j they share of s_p s_q R_j P_j(ȳ_p, ȳ_q) R_jᵀ.
+__device__ void gs_block(const SparseArgs& a, int32_t p, int32_t q, double* S) {
+#pragma unroll
+  for (int e = 0; e < 9; ++e) S[e] = 0.0;
+  for (int sp = 0; sp < 2; ++sp) {
+    const int32_t j = sp == 0 ? a.pa[p] : a.pb[p];
+    if (j < 0) continue;
+    for (int sq = 0; sq < 2; ++sq) {
+      const int32_t jq = sq == 0 ? a.pa[q] : a.pb[q];
+      if (jq != j) continue;
+      double R[9], P[9], T[9];
+      body_R(a, j, R);
+      HinvBlk H;
+      body_hinv(a, j, H);
+      pblock(H, a.py + 6 * p + 3 * sp, a.py + 6 * q + 3 * sq, P);
+      rot_conj(R, P, T);
+      const double sg = (sp == sq) ? 1.0 : -1.0;
+#pragma unroll
+      for (int e = 0; e < 9; ++e) S[e] += sg * T[e];
+    }
+  }
+}
+
+__device__ __forceinline__ double* gs_fac(const SparseArgs& a, int64_t pos, int comp) {
+  return a.gs.fac + (int64_t)comp * a.np + pos;
+}
+
+// Per step, one thread per chain: assemble the chain's diagonal and coupling blocks and factor them (block Thomas:
+// D'_0 = D_0, L_k = B_{k−1}ᵀ D'_{k−1}⁻¹, D'_k = D_k − L_k B_{k−1}); keeps D'⁻¹, L, B per position.
+__global__ void gs_factor_kernel(SparseArgs a, int32_t nchain) {
+  const int32_t c = blockIdx.x * blockDim.x + threadIdx.x;
+  if (c >= nchain) return;
+  const int32_t lo = a.gs.chain_off[c], hi = a.gs.chain_off[c + 1];
+  double Lp[9], Bp[9], Dpi[6];
+  for (int32_t k = lo; k < hi; ++k) {
+    const int32_t p = a.gs.chain_pts[k];
+    double D[9];
+    gs_block(a, p, p, D);
+    if (k > lo) {  // L = Bpᵀ Dpi, D −= L Bp
+      double Dif[9];
+      full_from_sym(Dpi, Dif);
+      mat3_mul_at(Bp, Dif, Lp);
+      double T[9];
+      mat3_mul(Lp, Bp, T);
+#pragma unroll
+      for (int e = 0; e < 9; ++e) D[e] -= T[e];
+    } else {
+#pragma unroll
+      for (int e = 0; e < 9; ++e) Lp[e] = 0.0;
+    }
+    double Ds[6];
+    Ds[0] = D[0]; Ds[1] = 0.5 * (D[1] + D[3]); Ds[2] = 0.5 * (D[2] + D[6]);
+    Ds[3] = D[4]; Ds[4] = 0.5 * (D[5] + D[7]); Ds[5] = D[8];
+    if (!sym_inv_spd(Ds, Dpi)) sreport(a.k, ERR_SINGULAR);
+    if (k + 1 < hi)
+      gs_block(a, p, a.gs.chain_pts[k + 1], Bp);
+    else
+#pragma unroll
+      for (int e = 0; e < 9; ++e) Bp[e] = 0.0;
+#pragma unroll
+    for (int e = 0; e < 6; ++e) *gs_fac(a, k, e) = Dpi[e];
+#pragma unroll
+    for (int e = 0; e < 9; ++e) {
+      *gs_fac(a, k, 6 + e) = Lp[e];
+      *gs_fac(a, k, 15 + e) = Bp[e];
+    }
+  }
+}
+
+__device__ __forceinline__ void atomic_max_pos(unsigned long long* slot, double v) {
+  atomicMax(slot, (unsigned long long)__double_as_longlong(v));  // v ≥ 0: the bit patterns order like the values
+}
+
+// max |r| over the points (the residual scale of the stopping test)
+__global__ void gs_rmax_kernel(SparseArgs a) {
+  double m = 0.0;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < 3 * a.np; i += (int64_t)gridDim.x * blockDim.x)
+    m = fmax(m, fabs(a.rhs[i]));
+  for (int o = 16; o > 0; o >>= 1) m = fmax(m, __shfl_xor_sync(0xffffffffu, m, o));
+  if ((threadIdx.x & 31) == 0) atomic_max_pos(a.gs.resmax, m);
+}
+
+__device__ __forceinline__ bool gs_converged(const SparseArgs& a, int sweep) {
+  if (sweep == 0) return false;
+  const double r0 = __longlong_as_double((long long)a.gs.resmax[0]);
+  const double rs = __longlong_as_double((long long)a.gs.resmax[sweep]);  // sweep − 1's residual
+  return rs <= a.gs.tol * r0;
+}
+
+// One colour of sweep `sweep`, one thread per chain of the colour: the chain's residual res = r − (J H̃⁻¹Jᵀλ) from the
+// per-body v = H̃⁻¹Jᵀλ (kept current), the exact chain solve S_cc δ = res (forward / backward Thomas), λ += δ, and
+// v_j += H̃_j⁻¹ Σ s Γᵀδ for the chain's bodies (no other chain of the colour touches them). The residual before the
+// update feeds the stopping test of the next sweep; a converged step skips the remaining sweeps.
+__global__ void gs_color_kernel(SparseArgs a, int32_t color, int32_t sweep) {
+  if (gs_converged(a, sweep)) return;
+  const int32_t c = a.gs.color_off[color] + blockIdx.x * blockDim.x + threadIdx.x;
+  double rmax = 0.0;
+  if (c < a.gs.color_off[color + 1]) {
+    const int32_t lo = a.gs.chain_off[c], hi = a.gs.chain_off[c + 1];
+    double y[3] = {0, 0, 0};
+    for (int32_t k = lo; k < hi; ++k) {  // forward: y_k = res_k − L_k y_{k−1}
+      const int32_t p = a.gs.chain_pts[k];
+      double r[3];
+#pragma unroll
+      for (int e = 0; e < 3; ++e) r[e] = a.rhs[e * a.np + p];
+      for (int side = 0; side < 2; ++side) {
+        const int64_t j = side == 0 ? a.pa[p] : a.pb[p];
+        if (j < 0) continue;
+        const double* yb = a.py + 6 * p + 3 * side;
+        const double sg = side == 0 ? 1.0 : -1.0;
+#pragma unroll
+        for (int e = 0; e < 3; ++e)
+          r[e] -= sg * (a.vv[(0 + e) * a.n + j] * yb[0] + a.vv[(3 + e) * a.n + j] * yb[1] +
+                        a.vv[(6 + e) * a.n + j] * yb[2] + a.vv[(9 + e) * a.n + j]);
+      }
+      rmax = fmax(rmax, fmax(fabs(r[0]), fmax(fabs(r[1]), fabs(r[2]))));
+      double L[9], t[3];
+#pragma unroll
+      for (int e = 0; e < 9; ++e) L[e] = *gs_fac(a, k, 6 + e);
+      mat3_vec(L, y, t);
+#pragma unroll
+      for (int e = 0; e < 3; ++e) {
+        y[e] = r[e] - t[e];
+        a.yy[e * a.np + p] = y[e];
+      }
+    }
+    double x[3] = {0, 0, 0};
+    for (int32_t k = hi - 1; k >= lo; --k) {  // backward: x_k = D'_k⁻¹ (y_k − B_k x_{k+1}); λ += x; v += H̃⁻¹Jᵀx
+      const int32_t p = a.gs.chain_pts[k];
+      double B[9], Di[6], t[3], v[3];
+#pragma unroll
+      for (int e = 0; e < 9; ++e) B[e] = *gs_fac(a, k, 15 + e);
+#pragma unroll
+      for (int e = 0; e < 6; ++e) Di[e] = *gs_fac(a, k, e);
+      mat3_vec(B, x, t);
+#pragma unroll
+      for (int e = 0; e < 3; ++e) v[e] = a.yy[e * a.np + p] - t[e];
+      sym_vec(Di, v, x);
+#pragma unroll
+      for (int e = 0; e < 3; ++e) a.lam[e * a.np + p] += x[e];
+      for (int side = 0; side < 2; ++side) {
+        const int64_t j = side == 0 ? a.pa[p] : a.pb[p];
+        if (j < 0) continue;
+        double R[9], g[12], u[12], wl[3], dv[3];
+        body_R(a, j, R);
+#pragma unroll
+        for (int e = 0; e < 12; ++e) g[e] = 0.0;
+        mat3t_vec(R, x, wl);
+        add_point_force(g, a.py + 6 * p + 3 * side, wl, side == 0 ? 1.0 : -1.0);
+        HinvBlk H;
+        body_hinv(a, j, H);
+        hinv_apply(H, g, u);
+#pragma unroll
+        for (int kb = 0; kb < 4; ++kb) {
+          mat3_vec(R, u + 3 * kb, dv);
+#pragma unroll
+          for (int e = 0; e < 3; ++e) a.vv[(3 * kb + e) * a.n + j] += dv[e];
+        }
+      }
+    }
+  }
+  for (int o = 16; o > 0; o >>= 1) rmax = fmax(rmax, __shfl_xor_sync(0xffffffffu, rmax, o));
+  if ((threadIdx.x & 31) == 0) atomic_max_pos(a.gs.resmax + 1 + sweep, rmax);
+}
+
+// sweeps run (the first whose starting residual met the tolerance, else max_sweeps) → iters[0] (mabd_solver_stats)
+__global__ void gs_count_kernel(SparseArgs a) {
+  int s = 1;
+  while (s <= a.gs.max_sweeps && !gs_converged(a, s)) ++s;
+  a.iters[0] = min(s, a.gs.max_sweeps);
+}
+
+cudaError_t gs_step(const Plan& p, const DevPtrs& d, const StepConsts& k, cudaStream_t st) {
+  SparseArgs a = d.sparse;
+  a.k = k;
+  const SparsePlan& sp = p.sparse;
+  sparse_predict_kernel<<<grid_for(a.n), 256, 0, st>>>(a);
+  if (sp.np > 0) {
+    sparse_rhs_kernel<<<grid_for(a.np), 256, 0, st>>>(a);
+    cudaError_t e;
+    if ((e = cudaMemsetAsync(a.gs.resmax, 0, sizeof(unsigned long long) * (2 + sp.gs_sweeps), st))) return e;
+    gs_rmax_kernel<<<grid_for(3 * a.np), 256, 0, st>>>(a);
+    const int32_t nch = (int32_t)(sp.gs_chain_off.size() - 1);
+    gs_factor_kernel<<<(unsigned)((nch + 127) / 128), 128, 0, st>>>(a, nch);
+    mv_body_kernel<<<grid_for(a.n), 256, 0, st>>>(a, a.lam);  // v = H̃⁻¹Jᵀλ of the warm start (last step's λ)
+    for (int s2 = 0; s2 < sp.gs_sweeps; ++s2)
+      for (int c = 0; c < sp.gs_ncolor; ++c) {
+        const int32_t nc = sp.gs_color_off[c + 1] - sp.gs_color_off[c];
+        gs_color_kernel<<<(unsigned)((nc + 127) / 128), 128, 0, st>>>(a, c, s2);
+      }
+    gs_count_kernel<<<1, 1, 0, st>>>(a);
+  }
+  sparse_update_kernel<<<grid_for(a.n), 256, 0, st>>>(a);
+  return cudaGetLastError();
+}
+
 // ============================================================================ host side: symbolic analysis
 namespace {
 
@@ -1297,7 +1494,7 @@ static bool mf_symbolic(const mabd_bodies* B, Plan* plan, std::string* msg) {
 }
 
 bool sparse_build(const mabd_bodies* B, const mabd_joints* J, Plan* p, std::vector<int64_t>* pos_of_body,
-                  std::string* msg) {
+                  std::string* msg, bool symbolic) {
   const int64_t K = J->n_joints, n = B->n;
   SparsePlan& s = p->sparse;
   s = SparsePlan();
@@ -1335,6 +1532,7 @@ bool sparse_build(const mabd_bodies* B, const mabd_joints* J, Plan* p, std::vect
   p->ld = n;
   p->n = n;
   p->n_dual_rows = 3 * P;
+  if (!symbolic) return true;  // line Gauss-Seidel (gs_build) needs the points and the incidence only
   if (!mf_symbolic(B, p, msg)) return false;
   s.refine = MF_REFINE;
   if (const char* ev = getenv("MABD_SPARSE_REFINE")) s.refine = std::max(0, std::min(8, atoi(ev)));  // developer knob
@@ -1349,6 +1547,139 @@ bool sparse_build(const mabd_bodies* B, const mabd_joints* J, Plan* p, std::vect
   }
   launches += 3 * s.refine;
   p->launches_per_step = (int32_t)std::min<int64_t>(launches, INT32_MAX);
+  return true;
+}
+
+// ============================================================================ host side: line Gauss-Seidel plan
+// Chain cover (R10): greedy paths in the body graph, each point (joint row block) on exactly one chain.
+// A chain grows from its last point through that point's other body to an unused point of that body whose bodies are
+// all new to the chain, taking the straightest continuation within ~26° of the direction of travel (the joint
+// positions at create), so a grid net is covered by its rows and columns, as the paper's "multi-directional"
+// relaxation along pre-defined chains.
+// Chains are capped at GS_MAX_CHAIN points (parallelism); chains sharing a body get different colours (greedy).
+constexpr int GS_MAX_CHAIN = 64;
+constexpr double GS_MIN_COS = 0.9;
+
+bool gs_build(const mabd_bodies* B, Plan* p, int32_t sweeps, double tol, std::string* msg) {
+  SparsePlan& s = p->sparse;
+  const int64_t n = p->n, np = s.np;
+  s.gs_sweeps = sweeps > 0 ? sweeps : 200;
+  s.gs_tol = tol > 0 ? tol : 1e-12;
+  if (s.gs_sweeps > 100000) return *msg = "gs_sweeps > 100000", false;
+  // joint positions at create (side a)
+  std::vector<double> xp(3 * np);
+  for (int64_t q = 0; q < np; ++q) {
+    const double* qa = B->q0 + 12 * (int64_t)s.pa[q];
+    const double* y = s.py.data() + 6 * q;
+    for (int r = 0; r < 3; ++r) xp[3 * q + r] = qa[r] * y[0] + qa[3 + r] * y[1] + qa[6 + r] * y[2] + qa[9 + r];
+  }
+  std::vector<char> used(np, 0);
+  std::vector<int32_t> mark(n, -1);  // chain id that owns a body (body-path property)
+  std::vector<int32_t> pts, off{0};
+  auto other = [&](int32_t q, int32_t b) { return s.pa[q] == b ? s.pb[q] : s.pa[q]; };
+  for (int64_t q0 = 0; q0 < np; ++q0) {
+    if (used[q0]) continue;
+    const int32_t cid = (int32_t)off.size() - 1;
+    std::vector<int32_t> ch{(int32_t)q0};
+    used[q0] = 1;
+    mark[s.pa[q0]] = cid;
+    if (s.pb[q0] >= 0) mark[s.pb[q0]] = cid;
+    for (int dir = 0; dir < 2 && (int)ch.size() < GS_MAX_CHAIN; ++dir) {
+      // grow from the end (dir 0: through body b of the first point, then onwards; dir 1: the other way)
+      int32_t last = dir == 0 ? ch.back() : ch.front();
+      int32_t via = dir == 0 ? s.pb[q0] : s.pa[q0];
+      if (ch.size() > 1 && dir == 0) via = -1;  // (only the seed point chooses the direction)
+      while (via >= 0 && (int)ch.size() < GS_MAX_CHAIN) {
+        int32_t best = -1;
+        double best_score = GS_MIN_COS;  // continue only within ~26° of straight ahead
+        const double* xl = xp.data() + 3 * last;
+        double dprev[3] = {0, 0, 0};
+        {  // direction of travel: previous point → last point (or body → last point at the start)
+          const int32_t prev = ch.size() > 1 ? (dir == 0 ? ch[ch.size() - 2] : ch[1]) : -1;
+          for (int r = 0; r < 3; ++r)
+            dprev[r] = prev >= 0 ? xl[r] - xp[3 * prev + r] : B->q0[12 * (int64_t)via + 9 + r] - xl[r];
+        }
+        for (int i = s.inc_off[via]; i < s.inc_off[via + 1]; ++i) {
+          const int32_t q = s.inc[i] >> 1;
+          if (used[q]) continue;
+          const int32_t o = other(q, via);
+          if (o >= 0 && mark[o] == cid) continue;  // would revisit a body of this chain
+          double dq[3], nd = 0, nq = 0, dot = 0;
+          for (int r = 0; r < 3; ++r) {
+            dq[r] = xp[3 * q + r] - xl[r];
+            nd += dprev[r] * dprev[r];
+            nq += dq[r] * dq[r];
+            dot += dprev[r] * dq[r];
+          }
+          const double score = (nd > 0 && nq > 0) ? dot / std::sqrt(nd * nq) : 0.0;
+          if (score > best_score) {
+            best_score = score;
+            best = q;
+          }
+        }
+        if (best < 0) break;
+        used[best] = 1;
+        const int32_t o = other(best, via);
+        if (o >= 0) mark[o] = cid;
+        if (dir == 0)
+          ch.push_back(best);
+        else
+          ch.insert(ch.begin(), best);
+        last = best;
+        via = o;
+      }
+    }
+    pts.insert(pts.end(), ch.begin(), ch.end());
+    off.push_back((int32_t)pts.size());
+  }
+  const int32_t nch = (int32_t)off.size() - 1;
+  // colouring: chains that share a body conflict
+  std::vector<std::vector<int32_t>> body_chains(n);
+  for (int32_t c = 0; c < nch; ++c)
+    for (int32_t k = off[c]; k < off[c + 1]; ++k) {
+      const int32_t q = pts[k];
+      for (int32_t b : {s.pa[q], s.pb[q]})
+        if (b >= 0 && (body_chains[b].empty() || body_chains[b].back() != c)) body_chains[b].push_back(c);
+    }
+  std::vector<int32_t> color(nch, -1), order(nch);
+  for (int32_t c = 0; c < nch; ++c) order[c] = c;
+  std::stable_sort(order.begin(), order.end(),
+                   [&](int32_t x, int32_t y) { return off[x + 1] - off[x] > off[y + 1] - off[y]; });
+  int32_t ncolor = 0;
+  std::vector<int32_t> seen;
+  for (int32_t c : order) {
+    seen.clear();
+    for (int32_t k = off[c]; k < off[c + 1]; ++k) {
+      const int32_t q = pts[k];
+      for (int32_t b : {s.pa[q], s.pb[q]})
+        if (b >= 0)
+          for (int32_t d : body_chains[b])
+            if (d != c && color[d] >= 0) seen.push_back(color[d]);
+    }
+    std::sort(seen.begin(), seen.end());
+    int32_t col = 0;
+    for (int32_t v : seen) {
+      if (v == col) ++col;
+      else if (v > col) break;
+    }
+    color[c] = col;
+    ncolor = std::max(ncolor, col + 1);
+  }
+  // chains sorted by colour (stable), points in chain order
+  std::vector<int32_t> by_color(nch);
+  for (int32_t c = 0; c < nch; ++c) by_color[c] = c;
+  std::stable_sort(by_color.begin(), by_color.end(), [&](int32_t x, int32_t y) { return color[x] < color[y]; });
+  s.gs_chain_pts.clear();
+  s.gs_chain_off.assign(1, 0);
+  s.gs_color_off.assign(ncolor + 1, 0);
+  for (int32_t c : by_color) {
+    s.gs_chain_pts.insert(s.gs_chain_pts.end(), pts.begin() + off[c], pts.begin() + off[c + 1]);
+    s.gs_chain_off.push_back((int32_t)s.gs_chain_pts.size());
+    s.gs_color_off[color[c] + 1]++;
+  }
+  for (int32_t c = 0; c < ncolor; ++c) s.gs_color_off[c + 1] += s.gs_color_off[c];
+  s.gs_ncolor = ncolor;
+  p->launches_per_step = 5 + (np ? 4 + s.gs_sweeps * ncolor : 0);
   return true;
 }
 
@@ -1388,6 +1719,11 @@ void sparse_layout(Plan* p, const std::function<size_t(size_t)>& take) {
   s.o_woff = take(sizeof(int64_t) * NN);
   s.o_lev = take(sizeof(int32_t) * nz(s.lev_nodes.size()));
   s.o_tasks = take(sizeof(int32_t) * nz(s.tasks.size()));
+  s.o_gs_pts = take(sizeof(int32_t) * nz(s.gs_chain_pts.size()));
+  s.o_gs_off = take(sizeof(int32_t) * nz(s.gs_chain_off.size()));
+  s.o_gs_col = take(sizeof(int32_t) * nz(s.gs_color_off.size()));
+  s.o_gs_fac = s.gs_ncolor ? take(sizeof(double) * 24 * np) : 0;
+  s.o_gs_res = take(sizeof(unsigned long long) * (2 + std::max(0, s.gs_sweeps)));
 }
 
 template <class T>
@@ -1439,6 +1775,14 @@ cudaError_t sparse_upload(const Plan& p, char* ws, cudaStream_t st, DevPtrs* d) 
   m.loff = (const int64_t*)(ws + s.o_loff);
   m.wvec = (double*)(ws + s.o_w);
   m.woff = (const int64_t*)(ws + s.o_woff);
+  A.gs.chain_pts = (const int32_t*)(ws + s.o_gs_pts);
+  A.gs.chain_off = (const int32_t*)(ws + s.o_gs_off);
+  A.gs.color_off = (const int32_t*)(ws + s.o_gs_col);
+  A.gs.fac = s.gs_ncolor ? (double*)(ws + s.o_gs_fac) : nullptr;
+  A.gs.resmax = (unsigned long long*)(ws + s.o_gs_res);
+  A.gs.ncolor = s.gs_ncolor;
+  A.gs.max_sweeps = s.gs_sweeps;
+  A.gs.tol = s.gs_tol;
   d->sparse_lev = (const int32_t*)(ws + s.o_lev);
   d->sparse_tasks = (const int32_t*)(ws + s.o_tasks);
   cudaError_t e;
@@ -1465,6 +1809,9 @@ cudaError_t sparse_upload(const Plan& p, char* ws, cudaStream_t st, DevPtrs* d) 
   if ((e = upv(ws, s.o_loff, s.loff, st))) return e;
   if ((e = upv(ws, s.o_lev, s.lev_nodes, st))) return e;
   if ((e = upv(ws, s.o_tasks, s.tasks, st))) return e;
+  if ((e = upv(ws, s.o_gs_pts, s.gs_chain_pts, st))) return e;
+  if ((e = upv(ws, s.o_gs_off, s.gs_chain_off, st))) return e;
+  if ((e = upv(ws, s.o_gs_col, s.gs_color_off, st))) return e;
   if ((e = cudaMemsetAsync(A.lam, 0, sizeof(double) * 3 * np, st))) return e;
   int32_t it[4] = {s.refine, 0, 0, 0};
   if ((e = cudaMemcpyAsync(A.iters, it, sizeof(it), cudaMemcpyHostToDevice, st))) return e;
@@ -1494,5 +1841,26 @@ extern "C" mabd_status mabd_sparse_plan_stats(const mabd_bodies* B, const mabd_j
   out[5] = (double)s.tasks.size();
   out[6] = p.launches_per_step;
   out[7] = (double)p.n_dual_rows;
+  return MABD_OK;
+}
+
+// See include/mabd.h (mabd_line_gs_plan).
+extern "C" mabd_status mabd_line_gs_plan(const mabd_bodies* B, const mabd_joints* J, int32_t* chain_pts,
+                                         int32_t* chain_off, int32_t* color_off, int64_t* counts) {
+  if (!counts) return MABD_EINVAL;
+  mabd::Plan p;
+  std::string msg;
+  mabd_options o{};
+  o.solver = MABD_SOLVER_LINE_GS;
+  o.world = 1;
+  const mabd_status st = mabd::build_plan(B, J, &o, &p, &msg);
+  if (st != MABD_OK) return st;
+  const mabd::SparsePlan& s = p.sparse;
+  counts[0] = (int64_t)s.gs_chain_pts.size();
+  counts[1] = (int64_t)s.gs_chain_off.size() - 1;
+  counts[2] = s.gs_ncolor;
+  if (chain_pts) std::copy(s.gs_chain_pts.begin(), s.gs_chain_pts.end(), chain_pts);
+  if (chain_off) std::copy(s.gs_chain_off.begin(), s.gs_chain_off.end(), chain_off);
+  if (color_off) std::copy(s.gs_color_off.begin(), s.gs_color_off.end(), color_off);
   return MABD_OK;
 }

@@ -152,3 +152,52 @@ def test_rotation_option(lib):
     for rot, want in ((0, 0), (1, 0), (2, 1), (-1, 1)):
         o = _Options(1, 1, 0, 0, 1, None, None, 0, None, 0, rot)
         assert lib.mabd_workspace_size(ctypes.byref(b), ctypes.byref(j), ctypes.byref(o), ctypes.byref(n)) == want
+
+
+def _gs_plan(lib, sc):
+    from paper_2603_08079_b200.binding import _Bodies, _Joints, _ptr, _ip
+    b = _Bodies(sc.n, _ptr(sc.q0), _ptr(sc.qd0), _ptr(sc.mbar), _ptr(sc.volume), _ptr(sc.youngs), _ptr(sc.poisson),
+                None, (ctypes.c_double * 3)(*sc.gravity))
+    j = _Joints(sc.n_joints, _ptr(sc.body_a, _ip), _ptr(sc.body_b, _ip), _ptr(sc.npts, _ip), _ptr(sc.ybar_a),
+                _ptr(sc.ybar_b))
+    cnt = (ctypes.c_int64 * 3)()
+    assert lib.mabd_line_gs_plan(ctypes.byref(b), ctypes.byref(j), None, None, None, cnt) == 0
+    npt, nch, ncol = list(cnt)
+    pts = np.zeros(npt, np.int32)
+    off = np.zeros(nch + 1, np.int32)
+    col = np.zeros(ncol + 1, np.int32)
+    ip = ctypes.POINTER(ctypes.c_int32)
+    assert lib.mabd_line_gs_plan(ctypes.byref(b), ctypes.byref(j), pts.ctypes.data_as(ip), off.ctypes.data_as(ip),
+                                 col.ctypes.data_as(ip), cnt) == 0
+    return pts, off, col
+
+
+@pytest.mark.parametrize("maker", ["net", "tree", "hinges"])
+def test_line_gs_chain_cover(lib, maker):
+    """Line Gauss-Seidel plan (the paper's Case IV; DESIGN R10): every joint point lies on exactly one chain; a
+    chain's points form a path in the body graph (consecutive points share a body, non-consecutive ones none), so its
+    dual block is block tridiagonal; chains of one colour share no body. A grid net is covered by its rows and
+    columns (two long-chain directions) plus the long-range links."""
+    sc = {"net": lambda: G.small_net(32, max_off=4), "tree": lambda: G.random_tree(300, seed=2, hinge_frac=0.0),
+          "hinges": lambda: G.random_tree(200, seed=3, hinge_frac=1.0)}[maker]()
+    pts, off, col = _gs_plan(lib, sc)
+    pa = np.repeat(sc.body_a, sc.npts)
+    pb = np.repeat(sc.body_b, sc.npts)
+    assert sorted(pts.tolist()) == list(range(len(pa)))
+    bodies = lambda p: {int(pa[p])} | ({int(pb[p])} if pb[p] >= 0 else set())
+    for c in range(len(off) - 1):
+        ch = pts[off[c]:off[c + 1]]
+        for i in range(len(ch)):
+            for k in range(i + 1, len(ch)):
+                shared = bodies(ch[i]) & bodies(ch[k])
+                assert (len(shared) > 0) == (k == i + 1), (c, i, k)
+    for k in range(len(col) - 1):
+        seen = set()
+        for c in range(col[k], col[k + 1]):
+            bs = set().union(*(bodies(p) for p in pts[off[c]:off[c + 1]]))
+            assert not (bs & seen)
+            seen |= bs
+    if maker == "net":
+        lengths = np.diff(off)
+        # rows / columns of 32 bodies are 31-joint chains (33 with the corner pins at both ends of a border row)
+        assert np.sum(lengths >= 31) == 64 and lengths.max() <= 33 and len(col) - 1 <= 6
