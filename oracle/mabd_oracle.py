@@ -39,7 +39,8 @@ __all__ = [
     "length_preserving", "affine_force",
     "body_hessians", "constraint_system", "constraint_residual", "predict", "step", "simulate", "nonlinear_residual",
     "wrench_force", "twist_velocity", "angular_velocity",
-    "block_thomas", "leaf_to_root_solve", "dual_matrix", "rel_err", "T9", "vec", "unvec",
+    "block_thomas", "leaf_to_root_solve", "dual_matrix", "line_gauss_seidel", "step_with_dual", "rel_err", "T9",
+    "vec", "unvec",
 ]
 
 # --------------------------------------------------------------------------
@@ -556,3 +557,28 @@ def leaf_to_root_solve(S, r, joint_rows, joint_child, joint_parent, depth):
     for X, Y, SXX, SXY, rX in reversed(elim):   # root-to-leaf back substitution
         lam[X] = np.linalg.solve(SXX, rX - SXY @ lam[Y])
     return lam, fill
+
+
+def line_gauss_seidel(S, r, blocks, colors, sweeps, lam0=None):
+    """Block Gauss-Seidel on S λ = r (the paper's Case IV, "relax … in the dual space joint by joint,
+    following … pre-defined chains"): ``blocks`` are index arrays of the unknowns of each chain, ``colors`` a list of
+    block-index lists relaxed in turn; each block is solved exactly against the current residual,
+    λ_B += S_BB⁻¹ (r − Sλ)_B. One sweep relaxes every colour once. Plain dense algebra (test oracle of the GPU
+    iteration, not of the method's exact step)."""
+    S = np.asarray(S, dtype=np.float64)
+    lam = np.zeros_like(np.asarray(r, dtype=np.float64)) if lam0 is None else np.array(lam0, dtype=np.float64)
+    for _ in range(sweeps):
+        for col in colors:
+            res = r - S @ lam          # blocks of one colour are uncoupled: one residual serves all of them
+            for b in col:
+                idx = blocks[b]
+                lam[idx] += np.linalg.solve(S[np.ix_(idx, idx)], res[idx])
+    return lam
+
+
+def step_with_dual(scene, q, qd, h, solve):
+    """One step with a caller-supplied dual solve λ = solve(S, r): δq = δq̃ − H̃⁻¹∇C̃ᵀλ."""
+    S, r, Jd, Hinv, dq_tilde = dual_matrix(scene, q, qd, h)
+    lam = solve(S, r)
+    dq = (dq_tilde.reshape(-1) - Hinv @ (Jd.T @ lam)).reshape(scene.n, 12)
+    return np.asarray(q) + dq, dq / h

@@ -348,6 +348,16 @@ mabd_status mabd_solver_stats(mabd_handle c, int64_t* last_iterations) {
   return MABD_OK;
 }
 
+// developer probe (not in the header): the line Gauss-Seidel residual history of the last step
+// (out[0] = max|r|, then per sweep max|r − Sλ|, max|Sλ|); returns the number of doubles written
+int mabd_dbg_gs_trace(mabd_handle c, double* out, int n) {
+  if (!c || c->plan.solver != MABD_SOLVER_LINE_GS) return 0;
+  const int m = std::min(n, 1 + 2 * c->plan.sparse.gs_sweeps);
+  cudaMemcpyAsync(out, c->d.sparse.gs.resmax, sizeof(double) * m, cudaMemcpyDeviceToHost, c->stream);
+  cudaStreamSynchronize(c->stream);
+  return m;
+}
+
 mabd_status mabd_nccl_unique_id(void* out, size_t bytes) {
   if (!out || bytes < 128) return fail(nullptr, MABD_EINVAL, "need a 128-byte buffer");
   std::string why;

@@ -123,7 +123,8 @@ struct GsArgs {
   const int32_t* chain_off;    // [nchain+1] into chain_pts
   const int32_t* color_off;    // [ncolor+1] chain ranges per colour
   double* fac;                 // [24][np] per chain position: D'⁻¹ (6, sym), L (9), B (9, coupling to the next)
-  unsigned long long* resmax;  // [2 + max_sweeps] (doubles ≥ 0 as bits): [0] max|r|, [1 + s] max|residual| of sweep s
+  unsigned long long* resmax;  // [1 + 2·max_sweeps] (doubles ≥ 0 as bits): [0] max|r|; sweep s: [1 + 2s] max|r − Sλ|,
+                               // [2 + 2s] max|Sλ| (the stopping scale of a warm start)
   int32_t ncolor, max_sweeps;
   double tol;                  // stop when max|residual| ≤ tol · max|r|
 };

@@ -1009,11 +1009,14 @@ __global__ void gs_rmax_kernel(SparseArgs a) {
   if ((threadIdx.x & 31) == 0) atomic_max_pos(a.gs.resmax, m);
 }
 
+// Stopping test before sweep `sweep`: sweep − 1's residual max|r − Sλ| ≤ tol · max(max|r|, max|Sλ|) (the second
+// scale matters for a warm start, where the joints are nearly satisfied but λ and Sλ are not small).
 __device__ __forceinline__ bool gs_converged(const SparseArgs& a, int sweep) {
   if (sweep == 0) return false;
   const double r0 = __longlong_as_double((long long)a.gs.resmax[0]);
-  const double rs = __longlong_as_double((long long)a.gs.resmax[sweep]);  // sweep − 1's residual
-  return rs <= a.gs.tol * r0;
+  const double rs = __longlong_as_double((long long)a.gs.resmax[2 * sweep - 1]);
+  const double sv = __longlong_as_double((long long)a.gs.resmax[2 * sweep]);
+  return rs <= a.gs.tol * fmax(r0, sv);
 }
 
 // One colour of sweep `sweep`, one thread per chain of the colour: the chain's residual res = r − (J H̃⁻¹Jᵀλ) from the
@@ -1023,15 +1026,13 @@ __device__ __forceinline__ bool gs_converged(const SparseArgs& a, int sweep) {
 __global__ void gs_color_kernel(SparseArgs a, int32_t color, int32_t sweep) {
   if (gs_converged(a, sweep)) return;
   const int32_t c = a.gs.color_off[color] + blockIdx.x * blockDim.x + threadIdx.x;
-  double rmax = 0.0;
+  double rmax = 0.0, smax = 0.0;
   if (c < a.gs.color_off[color + 1]) {
     const int32_t lo = a.gs.chain_off[c], hi = a.gs.chain_off[c + 1];
     double y[3] = {0, 0, 0};
     for (int32_t k = lo; k < hi; ++k) {  // forward: y_k = res_k − L_k y_{k−1}
       const int32_t p = a.gs.chain_pts[k];
-      double r[3];
-#pragma unroll
-      for (int e = 0; e < 3; ++e) r[e] = a.rhs[e * a.np + p];
+      double r[3], sl[3] = {0, 0, 0};  // sl = (S λ)_p = (J v)_p
       for (int side = 0; side < 2; ++side) {
         const int64_t j = side == 0 ? a.pa[p] : a.pb[p];
         if (j < 0) continue;
@@ -1039,10 +1040,13 @@ __global__ void gs_color_kernel(SparseArgs a, int32_t color, int32_t sweep) {
         const double sg = side == 0 ? 1.0 : -1.0;
 #pragma unroll
         for (int e = 0; e < 3; ++e)
-          r[e] -= sg * (a.vv[(0 + e) * a.n + j] * yb[0] + a.vv[(3 + e) * a.n + j] * yb[1] +
-                        a.vv[(6 + e) * a.n + j] * yb[2] + a.vv[(9 + e) * a.n + j]);
+          sl[e] += sg * (a.vv[(0 + e) * a.n + j] * yb[0] + a.vv[(3 + e) * a.n + j] * yb[1] +
+                         a.vv[(6 + e) * a.n + j] * yb[2] + a.vv[(9 + e) * a.n + j]);
       }
+#pragma unroll
+      for (int e = 0; e < 3; ++e) r[e] = a.rhs[e * a.np + p] - sl[e];
       rmax = fmax(rmax, fmax(fabs(r[0]), fmax(fabs(r[1]), fabs(r[2]))));
+      smax = fmax(smax, fmax(fabs(sl[0]), fmax(fabs(sl[1]), fabs(sl[2]))));
       double L[9], t[3];
 #pragma unroll
       for (int e = 0; e < 9; ++e) L[e] = *gs_fac(a, k, 6 + e);
@@ -1088,8 +1092,14 @@ __global__ void gs_color_kernel(SparseArgs a, int32_t color, int32_t sweep) {
       }
     }
   }
-  for (int o = 16; o > 0; o >>= 1) rmax = fmax(rmax, __shfl_xor_sync(0xffffffffu, rmax, o));
-  if ((threadIdx.x & 31) == 0) atomic_max_pos(a.gs.resmax + 1 + sweep, rmax);
+  for (int o = 16; o > 0; o >>= 1) {
+    rmax = fmax(rmax, __shfl_xor_sync(0xffffffffu, rmax, o));
+    smax = fmax(smax, __shfl_xor_sync(0xffffffffu, smax, o));
+  }
+  if ((threadIdx.x & 31) == 0) {
+    atomic_max_pos(a.gs.resmax + 1 + 2 * sweep, rmax);
+    atomic_max_pos(a.gs.resmax + 2 + 2 * sweep, smax);
+  }
 }
 
 // sweeps run (the first whose starting residual met the tolerance, else max_sweeps) → iters[0] (mabd_solver_stats)
@@ -1107,7 +1117,7 @@ cudaError_t gs_step(const Plan& p, const DevPtrs& d, const StepConsts& k, cudaSt
   if (sp.np > 0) {
     sparse_rhs_kernel<<<grid_for(a.np), 256, 0, st>>>(a);
     cudaError_t e;
-    if ((e = cudaMemsetAsync(a.gs.resmax, 0, sizeof(unsigned long long) * (2 + sp.gs_sweeps), st))) return e;
+    if ((e = cudaMemsetAsync(a.gs.resmax, 0, sizeof(unsigned long long) * (1 + 2 * sp.gs_sweeps), st))) return e;
     gs_rmax_kernel<<<grid_for(3 * a.np), 256, 0, st>>>(a);
     const int32_t nch = (int32_t)(sp.gs_chain_off.size() - 1);
     gs_factor_kernel<<<(unsigned)((nch + 127) / 128), 128, 0, st>>>(a, nch);
@@ -1577,6 +1587,9 @@ bool gs_build(const mabd_bodies* B, Plan* p, int32_t sweeps, double tol, std::st
   std::vector<int32_t> mark(n, -1);  // chain id that owns a body (body-path property)
   std::vector<int32_t> pts, off{0};
   auto other = [&](int32_t q, int32_t b) { return s.pa[q] == b ? s.pb[q] : s.pa[q]; };
+  auto twin = [&](int64_t q, int64_t r) {  // two points of one multi-point joint (the same two bodies)
+    return r >= 0 && r < np && s.pa[q] == s.pa[r] && s.pb[q] == s.pb[r];
+  };
   for (int64_t q0 = 0; q0 < np; ++q0) {
     if (used[q0]) continue;
     const int32_t cid = (int32_t)off.size() - 1;
@@ -1584,7 +1597,15 @@ bool gs_build(const mabd_bodies* B, Plan* p, int32_t sweeps, double tol, std::st
     used[q0] = 1;
     mark[s.pa[q0]] = cid;
     if (s.pb[q0] >= 0) mark[s.pb[q0]] = cid;
-    for (int dir = 0; dir < 2 && (int)ch.size() < GS_MAX_CHAIN; ++dir) {
+    // the points of a linear hinge share both bodies and are strongly coupled: they form a chain of their own
+    // (relaxing them in different colours stalls the iteration); such a chain cannot continue through either body
+    bool hinge = false;
+    for (int64_t r = q0 + 1; r < np && twin(q0, r) && !used[r]; ++r) {
+      ch.push_back((int32_t)r);
+      used[r] = 1;
+      hinge = true;
+    }
+    for (int dir = 0; dir < 2 && !hinge && (int)ch.size() < GS_MAX_CHAIN; ++dir) {
       // grow from the end (dir 0: through body b of the first point, then onwards; dir 1: the other way)
       int32_t last = dir == 0 ? ch.back() : ch.front();
       int32_t via = dir == 0 ? s.pb[q0] : s.pa[q0];
@@ -1601,7 +1622,7 @@ bool gs_build(const mabd_bodies* B, Plan* p, int32_t sweeps, double tol, std::st
         }
         for (int i = s.inc_off[via]; i < s.inc_off[via + 1]; ++i) {
           const int32_t q = s.inc[i] >> 1;
-          if (used[q]) continue;
+          if (used[q] || twin(q, q + 1) || twin(q, q - 1)) continue;
           const int32_t o = other(q, via);
           if (o >= 0 && mark[o] == cid) continue;  // would revisit a body of this chain
           double dq[3], nd = 0, nq = 0, dot = 0;
@@ -1723,7 +1744,7 @@ void sparse_layout(Plan* p, const std::function<size_t(size_t)>& take) {
   s.o_gs_off = take(sizeof(int32_t) * nz(s.gs_chain_off.size()));
   s.o_gs_col = take(sizeof(int32_t) * nz(s.gs_color_off.size()));
   s.o_gs_fac = s.gs_ncolor ? take(sizeof(double) * 24 * np) : 0;
-  s.o_gs_res = take(sizeof(unsigned long long) * (2 + std::max(0, s.gs_sweeps)));
+  s.o_gs_res = take(sizeof(unsigned long long) * (1 + 2 * std::max(0, s.gs_sweeps)));
 }
 
 template <class T>

@@ -614,3 +614,32 @@ def test_R9_polar_free_closure_equivariance_and_rest():
     r = G.random_chain(6, seed=28, vel=0.0, gravity=False)
     q3, qd3 = O.step(r, r.q0, r.qd0, r.h, rotation="length_preserving")
     assert np.max(np.abs(q3 - r.q0)) < 1e-14 and np.max(np.abs(qd3)) < 1e-12
+
+
+# ----------------------------------------------------------------------------- line Gauss-Seidel (NEXT 3, R10)
+
+def test_line_gauss_seidel_pins():
+    """Block Gauss-Seidel on SPD systems: one block covering everything is the exact solve after one sweep; any block
+    partition converges to np.linalg.solve; one sweep of single-row blocks is textbook point Gauss-Seidel."""
+    rng = np.random.default_rng(31)
+    X = rng.standard_normal((30, 30))
+    S = X @ X.T + 30 * np.eye(30)
+    r = rng.standard_normal(30)
+    exact = np.linalg.solve(S, r)
+    one = O.line_gauss_seidel(S, r, [np.arange(30)], [[0]], 1)
+    assert np.max(np.abs(one - exact)) < 1e-12 * np.max(np.abs(exact))
+    blocks = [np.arange(i, min(i + 6, 30)) for i in range(0, 30, 6)]
+    lam = O.line_gauss_seidel(S, r, blocks, [[0, 2, 4], [1, 3]], 300)
+    assert np.max(np.abs(lam - exact)) < 1e-10 * np.max(np.abs(exact))
+    # point GS, one sweep, written out as the textbook forward substitution (D + L) x = r
+    pts = [np.array([i]) for i in range(30)]
+    g1 = O.line_gauss_seidel(S, r, pts, [[i] for i in range(30)], 1)
+    assert np.allclose(g1, np.linalg.solve(np.tril(S), r), rtol=1e-12, atol=1e-14)
+
+
+def test_step_with_dual_is_the_step():
+    """step_with_dual with the exact dual solve reproduces the KKT step."""
+    sc = G.small_net(5, max_off=2)
+    q1, qd1 = O.step(sc, sc.q0, sc.qd0, sc.h)
+    q2, qd2 = O.step_with_dual(sc, sc.q0, sc.qd0, sc.h, np.linalg.solve)
+    assert O.rel_err(q2, q1) < 1e-11 and O.rel_err(qd2 * sc.h, qd1 * sc.h) < 1e-11
