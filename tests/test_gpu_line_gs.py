@@ -44,24 +44,25 @@ def test_line_gs_converges_to_the_direct_solution(cuda_ok, case):
     assert O.constraint_residual(sc, q_g) <= 1e-9
 
 
-def _soft(sc, E=1e6):
-    sc = sc.copy()
-    sc.youngs = np.full_like(sc.youngs, E)
-    return sc
-
-
 def test_line_gs_warm_start_and_sweep_budget(cuda_ok):
-    """Several steps on a net softened to E = 1e6: the block Gauss-Seidel rate is set by the ratio of the joints'
-    rigid-body mobility h²/m to the bodies' stretch compliance (~1/E), so the stiff recipe (E = 1e9) converges in
-    thousands of sweeps once the links carry strain (R10); the softened net converges in tens. Warm-started
-    from the previous step's λ, later steps need fewer sweeps; a tiny budget stops early (an approximate λ: the
-    joints do not close to 1e-9)."""
-    sc = _soft(G.small_net(12, max_off=3))
+    """Several steps where the iteration converges (a tree with hinges and ball joints), each warm-started from the
+    previous step's λ: the steps equal the oracle's direct steps (measured: 3,351 / 3,711 / 4,072 sweeps to 1e-11,
+    error 5e-13 — the warm start does not shorten the slow mode here). A tiny budget stops early: an approximate λ,
+    the joints do not close to 1e-9. (On the stiff loop nets the rate collapses once the links carry strain —
+    κ(S) ~ 1e8 — see DESIGN.md R10.)"""
+    sc = G.random_tree(120, seed=4, hinge_frac=0.5, vel=0.3, jitter=1e-3)
     q_o, _ = O.simulate(sc, 3)
-    q_g, _, sweeps3 = _run(sc, 3)
-    _, _, sweeps1 = _run(sc, 1)
-    print(f"line GS warm start: sweeps step 1 {sweeps1}, step 3 {sweeps3}; 3-step err {O.rel_err(q_g, q_o):.2e}")
-    assert O.rel_err(q_g, q_o) <= 1e-8
+    from paper_2603_08079_b200 import Simulator
+    with Simulator.from_scene(sc, solver=4, gs_sweeps=20000, gs_tol=1e-11) as sim:
+        sim.prefactor(sc.h)
+        sweeps = []
+        for _ in range(3):
+            sim.step(sc.h, 1)
+            sweeps.append(sim.solver_stats()["last_iterations"])
+        q_g, _ = sim.get_state()
+    err = O.rel_err(q_g, q_o)
+    print(f"line GS warm start: sweeps per step {sweeps}; 3-step err {err:.2e}")
+    assert err <= 1e-8 and max(sweeps) < 20000
     q_b, _, sb = _run(sc, 1, sweeps=3)
     assert sb == 3 and O.constraint_residual(sc, q_b) > 1e-9
 
