@@ -4,14 +4,15 @@
 // Paper: the chain dual is block tridiagonal (Eq. chain-btd); the paper solves it with block
 // Thomas in O(K) on one thread. Here one 128-thread CTA owns a 256-slot segment of a chain and
 // solves its 257-equation block-tridiagonal system by block cyclic reduction in shared memory
-// (log₂ 256 = 8 levels), fused with the per-body stages in one pass over HBM:
-//   phase 1, per body:  load qⁿ, q̇ⁿ → polar R → f_A → δq̃ (stages 1-2); δq̃ is parked in the
-//                       q̇ buffer (q̇ⁿ is dead after f_A; the line stays in L2);
-//            per joint: D, B, r = C(q̃) from the 3×3 kernels P(ȳ,ȳ') rotated by R
+// (log₂ 256 = 8 levels), fused with the per-body stages in one pass over HBM (details: chain_kernel below):
+//   staging, by TMA: the segment's qⁿ, q̇ⁿ rows (cp.async.bulk, mbarrier) into the shared-memory CR rows;
+//   phase 1, per body:  qⁿ, q̇ⁿ → tensor memory (TMEM, per-thread storage); polar R → f_A → δq̃ (stages 1-2,
+//                       P:260-281); δq̃ and rows 0-1 of R stay in TMEM; per joint D, B, r = C(q̃) from the 3×3
+//                       kernels P(ȳ,ȳ') rotated by R into the CR rows
 //   phase 2, per segment: cyclic reduction → λ
-//   phase 3, per body:  re-read qⁿ, δq̃ (L2), recompute R, qⁿ⁺¹ = q̃ − diag₄(R)H̄⁻¹Σ±(ȳ_aug ⊗ Rᵀλ),
-//                       q̇ⁿ⁺¹ = (qⁿ⁺¹ − qⁿ)/h
-// Nothing per body is held in registers across the solve, so 4 CTAs (57 KB shared memory each) fit per SM.
+//   phase 3, per body:  qⁿ, δq̃, R from TMEM, qⁿ⁺¹ = q̃ − diag₄(R)H̄⁻¹Σ±(ȳ_aug ⊗ Rᵀλ), q̇ⁿ⁺¹ = (qⁿ⁺¹ − qⁿ)/h
+//                        → HBM
+// Shared memory holds only the CR arrays (4 CTAs × 56.8 KB per SM); TMEM holds the per-body state across the solve.
 // Chains spanning several segments are partitioned (SPIKE-style): each segment reduces its interior to a
 // 2-equation "top" system on its end slots (REDUCE), the tops form a smaller block-tridiagonal system
 // solved recursively by btd_kernel, and each segment then recomputes and back-substitutes (FINISH).

@@ -1,6 +1,7 @@
 """GPU parity of the sparse path (loops / irregular nets: config-5 recipe, rings, random graphs) against the
-CPU oracle through the C ABI. The dual is solved by PCG to ‖r‖ ≤ 1e-13‖b‖ with an exact matrix-free S·x
-(reading A1); the tolerances are those of the north star (1e-9 after one step, 1e-6 after many)."""
+CPU oracle through the C ABI. The dual is factored exactly every step (multifrontal Cholesky over a nested-dissection
+assembly tree, reading R2) and refined once against the exact matrix-free S·x; the tolerances are those of
+the north star (1e-9 after one step) and the live-floor rule of test_gpu_chain.check for multi-step runs."""
 import numpy as np
 import pytest
 
