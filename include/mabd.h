@@ -97,7 +97,11 @@ typedef struct {
                                 DESIGN.md reading A4); any other value → MABD_EINVAL                  */
   int32_t solver;            /* 0 auto | 1 chain | 2 tree | 3 sparse | 4 line Gauss-Seidel (the paper's
                                 Case IV; R10: an iterative dual solve, never chosen by
-                                auto; converged to gs_tol, warm-started from the previous step's λ)     */
+                                auto; converged to gs_tol, warm-started from the previous step's λ)
+                                | 5 loop breakers (the paper's Case III; R12: the joints
+                                that close loops (≤ 8 points, ≤ 1 per body) are removed, the remaining forest
+                                runs on the chain / tree solver 2 + 3·points times per iteration and the
+                                breakers' multipliers solve the small Schur system; exact; no wrenches)   */
   int32_t rank, world;       /* multi-GPU; world = 1 → single GPU                                  */
   const void *nccl_unique_id;/* 128-byte ncclUniqueId, or NULL when world = 1                      */
   void *workspace;           /* device memory from the caller (torch), or NULL                     */
@@ -119,7 +123,8 @@ typedef struct {
 enum { MABD_ROTATION_POLAR = 0, MABD_ROTATION_LENGTH_PRESERVING = 1 };
 
 /* Topology/solver actually selected (mabd_query). */
-enum { MABD_SOLVER_CHAIN = 1, MABD_SOLVER_TREE = 2, MABD_SOLVER_SPARSE = 3, MABD_SOLVER_LINE_GS = 4 };
+enum { MABD_SOLVER_CHAIN = 1, MABD_SOLVER_TREE = 2, MABD_SOLVER_SPARSE = 3, MABD_SOLVER_LINE_GS = 4,
+       MABD_SOLVER_LOOP_BREAKER = 5 };
 
 /* Device bytes mabd_create will sub-allocate for these inputs (host analysis only; no GPU work). */
 mabd_status mabd_workspace_size(const mabd_bodies *bodies, const mabd_joints *joints,

@@ -664,3 +664,22 @@ def frame_to_canonical(q: np.ndarray, frames) -> np.ndarray:
     n = q.shape[0]
     Au = np.swapaxes(q[:, :9].reshape(n, 3, 3), 1, 2)
     return pack_q(Au @ P, q[:, 9:12] + np.einsum("nij,nj->ni", Au, d))
+
+
+def add_ball_joint(sc: Scene, a: int, b: int, name: str = None) -> Scene:
+    """The scene plus one ball joint between bodies a and b at the midpoint of their centres (input construction;
+    with a and b already connected it closes a loop)."""
+    n = sc.n
+    A = np.swapaxes(sc.q0[:, :9].reshape(n, 3, 3), 1, 2)
+    t = sc.q0[:, 9:]
+    p = 0.5 * (t[a] + t[b])
+    out = sc.copy()
+    out.body_a = np.append(sc.body_a, np.int32(a)).astype(np.int32)
+    out.body_b = np.append(sc.body_b, np.int32(b)).astype(np.int32)
+    out.npts = np.append(sc.npts, np.int32(1)).astype(np.int32)
+    out.ybar_a = np.vstack([sc.ybar_a, (A[a].T @ (p - t[a]))[None]])
+    out.ybar_b = np.vstack([sc.ybar_b, (A[b].T @ (p - t[b]))[None]])
+    out.name = name or f"{sc.name}_loop{a}_{b}"
+    out.meta = dict(sc.meta, topology="net")
+    out.validate()
+    return out

@@ -17,7 +17,7 @@ LIB_PATH = os.environ.get("MABD_LIB") or os.path.join(_PKG, "libmabd.so")
 MABD_OK = 0
 STATUS = {0: "MABD_OK", 1: "MABD_EINVAL", 2: "MABD_ESTATE", 3: "MABD_ENOMEM", 4: "MABD_ECUDA", 5: "MABD_ENCCL",
           6: "MABD_ESINGULAR", 7: "MABD_ENONFINITE", 8: "MABD_EUNSUPPORTED"}
-SOLVERS = {0: "auto", 1: "chain", 2: "tree", 3: "sparse", 4: "line_gs"}
+SOLVERS = {0: "auto", 1: "chain", 2: "tree", 3: "sparse", 4: "line_gs", 5: "loop_breaker"}
 
 EXPORTED = ["mabd_workspace_size", "mabd_create", "mabd_prefactor", "mabd_step", "mabd_step_async", "mabd_check",
             "mabd_get_state",

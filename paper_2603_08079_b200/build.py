@@ -14,7 +14,8 @@ ROOT = os.path.dirname(PKG)
 CSRC = os.path.join(PKG, "csrc")
 LIB = os.path.join(PKG, "libmabd.so")
 
-SOURCES = ["mabd_host.cu", "mabd_plan.cu", "mabd_chain.cu", "mabd_tree.cu", "mabd_sparse.cu", "mabd_nccl.cu"]
+SOURCES = ["mabd_host.cu", "mabd_plan.cu", "mabd_chain.cu", "mabd_tree.cu", "mabd_sparse.cu", "mabd_nccl.cu",
+           "mabd_loop.cu"]
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 
 

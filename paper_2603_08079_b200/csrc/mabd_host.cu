@@ -302,6 +302,8 @@ mabd_status mabd_set_state(mabd_handle c, const double* q, const double* qd, int
 
 mabd_status mabd_set_wrench(mabd_handle c, const double* W, int in_on_device) {
   if (!c) return fail(nullptr, MABD_EINVAL, "NULL handle");
+  if (c->plan.loop.active)
+    return fail(c, MABD_EUNSUPPORTED, "external wrenches are not available with the loop-breaker solver");
   CUDA_TRY(c, cudaSetDevice(c->device));
   const double* wr = nullptr;
   if (W) {
@@ -327,7 +329,7 @@ mabd_status mabd_set_wrench(mabd_handle c, const double* W, int in_on_device) {
 mabd_status mabd_query(mabd_handle c, int32_t* solver, int32_t* launches_per_step, int64_t* n_bodies,
                        int64_t* n_dual_rows) {
   if (!c) return fail(nullptr, MABD_EINVAL, "NULL handle");
-  if (solver) *solver = c->plan.solver;
+  if (solver) *solver = c->plan.loop.active ? MABD_SOLVER_LOOP_BREAKER : c->plan.solver;
   if (launches_per_step) *launches_per_step = c->plan.launches_per_step + 1;  // + the step_end node
   if (n_bodies) *n_bodies = c->plan.n;
   if (n_dual_rows) *n_dual_rows = c->plan.n_dual_rows;

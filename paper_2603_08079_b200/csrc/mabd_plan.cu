@@ -217,7 +217,7 @@ static mabd_status validate(const mabd_bodies* B, const mabd_joints* J, const ma
     if (o->newton_iters < 0 || o->newton_iters > 16) return *msg = "newton_iters must be in [0, 16]", MABD_EINVAL;
     if (o->world > 1 && (o->rank < 0 || o->rank >= o->world)) return *msg = "rank outside [0, world)", MABD_EINVAL;
     if (o->world > 256) return *msg = "world > 256", MABD_EINVAL;
-    if (o->solver < 0 || o->solver > MABD_SOLVER_LINE_GS) return *msg = "unknown solver", MABD_EINVAL;
+    if (o->solver < 0 || o->solver > MABD_SOLVER_LOOP_BREAKER) return *msg = "unknown solver", MABD_EINVAL;
     if (o->gs_sweeps < 0 || !(o->gs_tol >= 0.0)) return *msg = "gs_sweeps and gs_tol must be >= 0", MABD_EINVAL;
     if (o->rotation != MABD_ROTATION_POLAR && o->rotation != MABD_ROTATION_LENGTH_PRESERVING)
       return *msg = "rotation must be MABD_ROTATION_POLAR (0) or MABD_ROTATION_LENGTH_PRESERVING (1)", MABD_EINVAL;
@@ -547,10 +547,17 @@ mabd_status build_plan(const mabd_bodies* B, const mabd_joints* J, const mabd_op
   std::vector<double> msc;
   detect_materials(B, p, &mid, &msc);
 
-  const int req = o ? o->solver : 0;
+  int req = o ? o->solver : 0;
   std::vector<int64_t> pos;
   std::string why;
   bool ok = false;
+  if (req == MABD_SOLVER_LOOP_BREAKER) {  // the paper's Case III: the forest by chain / tree, + breakers
+    if (o && o->world > 1) return *msg = "loop breakers run on one GPU", MABD_EUNSUPPORTED;
+    if (!loop_split(J, B->n, &p->loop, &why)) return *msg = "loop breakers: " + why, MABD_EINVAL;
+    p->loop.active = true;
+    J = &p->loop.forest;
+    req = 0;  // chain if the forest is a set of ball-joint paths, else tree
+  }
   if (req == 0 || req == MABD_SOLVER_CHAIN) {
     ok = chain_build(J, B->n, p, &pos, &why);
     if (ok) {
@@ -573,6 +580,7 @@ mabd_status build_plan(const mabd_bodies* B, const mabd_joints* J, const mabd_op
     if (!ok) return *msg = "line Gauss-Seidel: " + why, MABD_EINVAL;
     p->solver = MABD_SOLVER_LINE_GS;
   }
+  if (!ok && p->loop.active) return *msg = "loop breakers: the forest is neither chains nor trees", MABD_EINVAL;
   if (!ok && (req == 0 || req == MABD_SOLVER_SPARSE)) {
     std::string why3;
     ok = sparse_build(B, J, p, &pos, &why3);
@@ -582,6 +590,12 @@ mabd_status build_plan(const mabd_bodies* B, const mabd_joints* J, const mabd_op
   if (!ok) {
     *msg = "topology not supported by this build (" + why + ")";
     return MABD_EUNSUPPORTED;
+  }
+  if (p->loop.active) {  // breaker points → internal positions; 2 + 3b forest runs + 2 kernels each, + solve, force
+    for (auto* v : {&p->loop.pa, &p->loop.pb})
+      for (int32_t& b : *v) b = (int32_t)pos[b];
+    const int runs = 2 + 3 * (int)p->loop.pa.size();
+    p->launches_per_step = runs * (p->launches_per_step + 2) - 1;
   }
   if (p->newton_iters > 1) p->launches_per_step = p->newton_iters * p->launches_per_step + 2;  // + prep, final
   if (o && o->world > 1 && p->solver == MABD_SOLVER_TREE) {
@@ -633,6 +647,17 @@ mabd_status build_plan(const mabd_bodies* B, const mabd_joints* J, const mabd_op
   f.io = take(sizeof(double) * 24 * B->n);
   f.err = take(sizeof(int32_t) * 4);
   f.frame = p->frame.empty() ? 0 : take(sizeof(double) * p->frame.size());
+  if (p->loop.active) {
+    LoopPlan& L = p->loop;
+    const size_t m = 3 * L.pa.size();
+    L.o_save = take(sizeof(double) * 24 * ld);
+    L.o_M = take(sizeof(double) * (1 + m) * m);
+    L.o_lam = take(sizeof(double) * m);
+    L.o_pa = take(sizeof(int32_t) * L.pa.size());
+    L.o_pb = take(sizeof(int32_t) * L.pb.size());
+    L.o_ya = take(sizeof(double) * L.ya.size());
+    L.o_yb = take(sizeof(double) * L.yb.size());
+  }
   if (p->solver == MABD_SOLVER_CHAIN) {
     f.slot_info = take(sizeof(uint32_t) * (ld + 16));  // + padding: segments stage SEG + 4 slot codes
     f.geo = take(sizeof(double) * p->geo.size());
@@ -731,6 +756,21 @@ cudaError_t upload_plan(const Plan& p, char* ws, cudaStream_t st, DevPtrs* d) {
   d->frame = p.frame.empty() ? nullptr : (double*)(ws + f.frame);
   cudaError_t e;
   if (d->frame && (e = put(d->frame, p.frame, st))) return e;
+  if (p.loop.active) {  // the breaker forces ride on the wrench buffer, zero elsewhere
+    const LoopPlan& L = p.loop;
+    d->loop_save = (double*)(ws + L.o_save);
+    d->loop_M = (double*)(ws + L.o_M);
+    d->loop_lam = (double*)(ws + L.o_lam);
+    d->loop_pa = (int32_t*)(ws + L.o_pa);
+    d->loop_pb = (int32_t*)(ws + L.o_pb);
+    d->loop_ya = (double*)(ws + L.o_ya);
+    d->loop_yb = (double*)(ws + L.o_yb);
+    if ((e = put(d->loop_pa, L.pa, st)) || (e = put(d->loop_pb, L.pb, st)) || (e = put(d->loop_ya, L.ya, st)) ||
+        (e = put(d->loop_yb, L.yb, st)))
+      return e;
+    if ((e = cudaMemsetAsync(d->wr_buf, 0, sizeof(double) * 9 * p.ld, st))) return e;
+    d->b.wr = d->wr_buf;
+  }
   if ((e = put(d->b.q, p.q_soa, st))) return e;
   if ((e = put(d->b.qd, p.qd_soa, st))) return e;
   if (!p.mat_id.empty() && (e = put((int32_t*)d->b.mat_id, p.mat_id, st))) return e;
@@ -1003,7 +1043,14 @@ cudaError_t launch_step(const Plan& p, const DevPtrs& d, double h, int32_t step,
   return cudaGetLastError();
 }
 
+static cudaError_t forest_iteration(const Plan& p, const DevPtrs& d, const StepConsts& k, cudaStream_t st);
+
 static cudaError_t launch_iteration(const Plan& p, const DevPtrs& d, const StepConsts& k, cudaStream_t st) {
+  if (p.loop.active) return loop_step(p, d, k, st, forest_iteration);
+  return forest_iteration(p, d, k, st);
+}
+
+static cudaError_t forest_iteration(const Plan& p, const DevPtrs& d, const StepConsts& k, cudaStream_t st) {
   if (p.solver == MABD_SOLVER_TREE) return tree_step(p, d, k, st);
   if (p.solver == MABD_SOLVER_SPARSE) return sparse_step(p, d, k, st);
   if (p.solver == MABD_SOLVER_LINE_GS) return gs_step(p, d, k, st);

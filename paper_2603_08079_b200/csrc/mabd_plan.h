@@ -104,6 +104,21 @@ struct SparsePlan {
          o_lev = 0, o_tasks = 0, o_loff = 0;
 };
 
+// Loop breakers (the paper's Case III, MABD_SOLVER_LOOP_BREAKER; mabd_loop.cu): a forest solved by the chain or tree
+// solver plus ≤ LOOP_MAX_PTS breaker points whose multipliers come from a small Schur system formed by forest runs.
+constexpr int LOOP_MAX_PTS = 8;
+struct LoopPlan {
+  bool active = false;
+  std::vector<int64_t> keep, breakers;           // joint indices (caller order)
+  std::vector<int32_t> pa, pb;                   // breaker points: bodies (caller order, then internal positions)
+  std::vector<double> ya, yb;                    // [np][3]
+  std::vector<int32_t> fa, fb, fn;               // the forest's joints
+  std::vector<double> fya, fyb;
+  mabd_joints forest{};
+  size_t o_save = 0, o_M = 0, o_lam = 0, o_pa = 0, o_pb = 0, o_ya = 0, o_yb = 0;
+};
+bool loop_split(const mabd_joints* J, int64_t n, LoopPlan* L, std::string* msg);
+
 struct Plan {
   int64_t n = 0, n_joints = 0, n_dual_rows = 0;
   int32_t solver = 0;
@@ -137,6 +152,8 @@ struct Plan {
   bool use_nccl = false;
   std::vector<Part> parts;
   std::vector<int32_t> local_windows, local_long, part_left_open;
+  // loop breakers (Case III) around the chain or tree solver
+  LoopPlan loop;
   // tree solver
   TreePlan tree;
   // sparse solver
@@ -159,6 +176,8 @@ struct DevPtrs {
   double* wr_buf = nullptr;        // [9][ld] wrench storage (b.wr points here once a wrench is set): τ, f, and the
                                    // material point f acts at (the caller's frame origin, in the canonical frame)
   double* frame = nullptr;         // [n][12] canonical frames per caller body (Plan::frame), or null
+  double *loop_save = nullptr, *loop_M = nullptr, *loop_lam = nullptr, *loop_ya = nullptr, *loop_yb = nullptr;
+  int32_t *loop_pa = nullptr, *loop_pb = nullptr;
   HinvBlk* hinv = nullptr;
   Material* mats = nullptr;
   int64_t* perm = nullptr;
@@ -201,6 +220,8 @@ cudaError_t upload_plan(const Plan& p, char* ws, cudaStream_t st, DevPtrs* d);
 cudaError_t prefactor_device(const Plan& p, const DevPtrs& d, double h, cudaStream_t st);
 cudaError_t reset_err(const DevPtrs& d, cudaStream_t st);
 cudaError_t launch_step_end(const DevPtrs& d, cudaStream_t st);
+cudaError_t loop_step(const Plan& p, const DevPtrs& d, const StepConsts& k, cudaStream_t st,
+                      cudaError_t (*forest_step)(const Plan&, const DevPtrs&, const StepConsts&, cudaStream_t));
 cudaError_t launch_step(const Plan& p, const DevPtrs& d, double h, int32_t step, cudaStream_t st);
 
 // tree solver (mabd_tree.cu)
