@@ -69,6 +69,7 @@ class Scene:
     material: Optional[np.ndarray] = None   # [n] int32 or None
     meta: dict = field(default_factory=dict)
     wrench: Optional[np.ndarray] = None     # [n,6] external wrench (τ, f), world frame, constant; None = none
+    kind: Optional[np.ndarray] = None       # [K] int32 joint kind: 0 point joint (default), 1 five-row hinge
 
     @property
     def n(self) -> int:
@@ -83,7 +84,8 @@ class Scene:
         return 3 * int(self.npts.sum())
 
     def copy(self) -> "Scene":
-        kw = {k: (v.copy() if isinstance(v, np.ndarray) else v) for k, v in self.__dict__.items()}
+        kw = {k: (v.copy() if isinstance(v, np.ndarray) else v) for k, v in self.__dict__.items()
+              if k in self.__dataclass_fields__}
         kw["meta"] = dict(self.meta)
         return Scene(**kw)
 
@@ -683,3 +685,36 @@ def add_ball_joint(sc: Scene, a: int, b: int, name: str = None) -> Scene:
     out.meta = dict(sc.meta, topology="net")
     out.validate()
     return out
+
+
+def five_row_hinges(sc: Scene) -> Scene:
+    """The same scene with every two-point (linear, 6-row) hinge turned into a five-row hinge (kind 1):
+    same material points — the first on the pivot, the second along the axis — with the axial row of the second
+    point freed. Input construction only."""
+    out = sc.copy()
+    out.kind = (np.asarray(sc.npts) == 2).astype(np.int32)
+    out.name = sc.name + "_hinge5"
+    return out
+
+
+def hinge_pendulum(axis=(1.0, 0.0, 0.0), omega0=(0.0, 0.0, 0.0), length: float = 0.4, h: float = 1e-2,
+                   E: float = 1e8) -> Scene:
+    """A 0.4×0.04×0.04 m rod (ρ = 1000) hanging from a world hinge at its top end (two world points on the axis,
+    0.05 m apart), released with angular velocity omega0 about its centre of mass. Input construction only."""
+    axis = np.asarray(axis, dtype=np.float64)
+    axis = axis / np.linalg.norm(axis)
+    a, b = 0.04, length
+    A0 = np.eye(3)
+    # rod along z, top end at the origin
+    dims = (a, a, b)
+    t0 = np.array([[0.0, 0.0, -b / 2]])
+    om = np.asarray(omega0, dtype=np.float64)
+    qd = np.zeros((1, 12))
+    for c in range(3):
+        qd[0, 3 * c:3 * c + 3] = np.cross(om, A0[:, c])
+    qd[0, 9:12] = np.cross(om, t0[0] - t0[0])  # spin about the centre of mass
+    pts = np.array([[0.0, 0.0, 0.0], 0.05 * axis])
+    sc = _assemble("hinge_pendulum", A0[None], t0, qd, box_mbar(*dims, 1000.0)[None], np.array([np.prod(dims)]), E, NU,
+                   np.array([0], np.int32), np.array([-1], np.int32), np.array([2], np.int32), pts, h, 1,
+                   meta={"topology": "tree"})
+    return sc

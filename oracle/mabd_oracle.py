@@ -37,7 +37,7 @@ import scipy.sparse.linalg as spla
 __all__ = [
     "lame", "unpack_mbar", "mass_A", "kbar_A", "hbar_A", "polar", "elastic_force_A", "stvk_force_A",
     "length_preserving", "affine_force",
-    "body_hessians", "constraint_system", "constraint_residual", "predict", "step", "simulate", "nonlinear_residual",
+    "body_hessians", "hinge_frame", "hinge5_rows", "constraint_system", "constraint_residual", "predict", "step", "simulate", "nonlinear_residual",
     "wrench_force", "twist_velocity", "angular_velocity",
     "block_thomas", "leaf_to_root_solve", "dual_matrix", "line_gauss_seidel", "step_with_dual", "rel_err", "T9",
     "vec", "unvec",
@@ -239,8 +239,42 @@ def body_hessians(R, Hbar) -> np.ndarray:
 # constraints (ball = 1 point, linear hinge = 2 points: P:368)
 # --------------------------------------------------------------------------
 
-def constraint_system(scene):
-    """Constant Jacobian ∇C̃ (sparse, 3 rows per joint point) of the point-coincidence constraints.
+def hinge_frame(axis) -> np.ndarray:
+    """ΔR_H of the five-row hinge: the rotation I + [v]× + [v]×²/(1 + a_y), v = a × e_y, that turns the unit
+    axis a upright onto the local y axis (a = −e_y, where the formula is singular, takes diag(1, −1, −1))."""
+    a = np.asarray(axis, dtype=np.float64)
+    a = a / np.linalg.norm(a)
+    if a[1] <= -1.0 + 1e-12:
+        return np.diag([1.0, -1.0, -1.0])
+    v = np.cross(a, [0.0, 1.0, 0.0])
+    V = np.array([[0, -v[2], v[1]], [v[2], 0, -v[0]], [-v[1], v[0], 0]])
+    return np.eye(3) + V + V @ V / (1.0 + a[1])
+
+
+def hinge5_rows(scene, q):
+    """Row transforms of the five-row hinges (Eq. hinge; R13) at the state q:
+    for joint k of kind 1 (two points on the axis, the second's ȳ_a − first's ȳ_a along the axis in body a's frame)
+    the first point keeps its 3 ball rows and the second keeps W = P R_H (2×3), P = [e_x; e_z], R_H = ΔR_H Rᵀ(A_a):
+    the local x̃, z̃ of the CP difference (Eq. hinge), the axial row freed. Returns {point index: W}."""
+    kind = getattr(scene, "kind", None)
+    out = {}
+    if kind is None:
+        return out
+    off = np.concatenate([[0], np.cumsum(scene.npts)])
+    Pxz = np.array([[1.0, 0, 0], [0, 0, 1.0]])
+    for k in np.nonzero(np.asarray(kind) == 1)[0]:
+        p0 = off[k]
+        a = scene.body_a[k]
+        R = polar(unvec(np.asarray(q)[a, :9]))
+        dR = hinge_frame(scene.ybar_a[p0 + 1] - scene.ybar_a[p0])
+        out[p0 + 1] = Pxz @ dR @ R.T
+    return out
+
+
+def constraint_system(scene, q=None):
+    """Jacobian ∇C̃ (sparse) of the joint constraints and the world offsets, at the state q.
+
+    Point joints (kind 0) are state independent: 3 rows per joint point.
 
     A point ȳ on body j sits at x = Aȳ + t = (ȳ_augᵀ ⊗ I₃) q_j, ȳ_aug = [ȳ; 1] (P:182, P:368 with one control
     point placed at the joint). Row block of point p: +(ȳ_a,augᵀ ⊗ I₃) on body a, −(ȳ_b,augᵀ ⊗ I₃) on body b
@@ -267,12 +301,24 @@ def constraint_system(scene):
     world = np.zeros((P, 3))
     wm = rb < 0
     world[wm] = scene.ybar_b[wm]
-    return J, world.reshape(-1)
+    world = world.reshape(-1)
+    W = hinge5_rows(scene, q) if getattr(scene, "kind", None) is not None else {}
+    if W:  # five-row hinges: the second point's 3 rows → its 2 rows W (2×3), linearised with W frozen at q (R13)
+        if q is None:
+            raise ValueError("five-row hinges: the constraint rows depend on the state q")
+        blocks = []
+        for p in range(P):
+            blocks.append(sp.csr_matrix(W[p]) if p in W else sp.identity(3, format="csr"))
+        T = sp.block_diag(blocks, format="csr")
+        J = (T @ J).tocsr()
+        world = T @ world
+    return J, world
 
 
 def constraint_residual(scene, q) -> float:
-    """max_k ‖C_k(q)‖∞ over all joint points (pin P3, BASELINE north star 'residual below 1e-10')."""
-    J, w = constraint_system(scene)
+    """max_k ‖C_k(q)‖∞ over all joint rows (pin P3, BASELINE north star 'residual below 1e-10'); five-row hinges
+    evaluate their rows with R_H at q itself (the nonlinear constraint)."""
+    J, w = constraint_system(scene, q)
     if J.shape[0] == 0:
         return 0.0
     return float(np.max(np.abs(J @ np.asarray(q).reshape(-1) - w)))
@@ -353,7 +399,7 @@ def step(scene, q, qd, h, route: str = "auto", return_info: bool = False, iters:
     qd = np.asarray(qd, dtype=np.float64)
     n = scene.n
     R, f, H, dq_tilde = predict(scene, q, qd, h, rotation)
-    J, world = constraint_system(scene)
+    J, world = constraint_system(scene, q)
     m = J.shape[0]
     c = J @ q.reshape(-1) - world                      # C̃(qⁿ), footnote P:459
     N = 12 * n + m
@@ -449,7 +495,7 @@ def nonlinear_residual(scene, qn, qdn, q, h, lam=None):
     gr[:, :9] += elastic_force_A(unvec(q[:, :9]), scene.volume, mu, lam_)
     if getattr(scene, "wrench", None) is not None:
         gr -= wrench_force(q, scene.wrench)
-    J, world = constraint_system(scene)
+    J, world = constraint_system(scene, q)
     g = gr.reshape(-1)
     if J.shape[0]:
         if lam is None:
@@ -488,7 +534,7 @@ def rel_err(x, ref) -> float:
 def dual_matrix(scene, q, qd, h):
     """Dense dual S = ∇C̃ H̃⁻¹ ∇C̃ᵀ and r = C(q̃) (P:483 with the footnote P:459 term)."""
     R, f, H, dq_tilde = predict(scene, q, qd, h)
-    J, world = constraint_system(scene)
+    J, world = constraint_system(scene, q)
     Jd = J.toarray()
     Hinv = np.zeros((12 * scene.n, 12 * scene.n))
     for j in range(scene.n):

@@ -643,3 +643,80 @@ def test_step_with_dual_is_the_step():
     q1, qd1 = O.step(sc, sc.q0, sc.qd0, sc.h)
     q2, qd2 = O.step_with_dual(sc, sc.q0, sc.qd0, sc.h, np.linalg.solve)
     assert O.rel_err(q2, q1) < 1e-11 and O.rel_err(qd2 * sc.h, qd1 * sc.h) < 1e-11
+
+
+# ----------------------------------------------------------------------------- five-row hinge (NEXT 2, R13)
+
+def _hinge5_C(sc, q):
+    """The five-row hinge constraint written out independently (Eq. hinge): ball rows of the pivot points,
+    and the local x̃, z̃ of the second points' difference in the frame R_H = ΔR_H Rᵀ(A_a), R by scipy's polar."""
+    off = np.concatenate([[0], np.cumsum(sc.npts)])
+    out = []
+    for k in range(sc.n_joints):
+        a, b = sc.body_a[k], sc.body_b[k]
+        def x(body, y):
+            if body < 0:
+                return y
+            A = O.unvec(q[body, :9])
+            return A @ y + q[body, 9:]
+        for i in range(sc.npts[k]):
+            d = x(a, sc.ybar_a[off[k] + i]) - x(b, sc.ybar_b[off[k] + i])
+            if sc.kind is not None and sc.kind[k] == 1 and i == 1:
+                R, _ = scipy.linalg.polar(O.unvec(q[a, :9]))
+                ax = sc.ybar_a[off[k] + 1] - sc.ybar_a[off[k]]
+                ax = ax / np.linalg.norm(ax)
+                v = np.cross(ax, [0, 1, 0])
+                V = np.array([[0, -v[2], v[1]], [v[2], 0, -v[0]], [-v[1], v[0], 0]])
+                dR = np.eye(3) + V + V @ V / (1 + ax[1])
+                assert np.allclose(dR @ ax, [0, 1, 0])
+                out.append((dR @ R.T @ d)[[0, 2]])
+            else:
+                out.append(d)
+    return np.concatenate(out)
+
+
+def test_hinge5_jacobian_is_the_gradient_where_the_axis_points_coincide():
+    """R13: with R_H frozen at q the five-row hinge's rows are W Γ; the dropped ∂R_H/∂q term multiplies the second
+    points' separation, so at states where those coincide (every satisfied hinge, up to axial stretch) the oracle's
+    Jacobian is the exact gradient of the nonlinear constraint (central differences, rotated bodies); away from them
+    it is not."""
+    sc = G.five_row_hinges(G.random_tree(6, seed=41, hinge_frac=1.0, vel=0.3))
+    J, w = O.constraint_system(sc, sc.q0)
+    assert J.shape[0] == 5 * int(np.sum(sc.kind == 1)) + 3 * int(np.sum(sc.kind == 0))
+    assert np.max(np.abs(J @ sc.q0.reshape(-1) - w - _hinge5_C(sc, sc.q0))) < 1e-12
+    eps = 1e-6
+    q0 = sc.q0.reshape(-1)
+    fd = np.array([(_hinge5_C(sc, (q0 + eps * e).reshape(sc.n, 12)) - _hinge5_C(sc, (q0 - eps * e).reshape(sc.n, 12)))
+                   / (2 * eps) for e in np.eye(q0.size)]).T
+    assert np.max(np.abs(fd - J.toarray())) < 1e-7 * np.max(np.abs(fd))
+    # a state with separated axis points: the frozen-R_H Jacobian is no longer the gradient
+    q1 = sc.q0.copy()
+    q1[:, 9:] += 0.01 * np.random.default_rng(42).standard_normal((sc.n, 3))
+    J1, _ = O.constraint_system(sc, q1)
+    fd1 = np.array([(_hinge5_C(sc, (q1.reshape(-1) + eps * e).reshape(sc.n, 12))
+                     - _hinge5_C(sc, (q1.reshape(-1) - eps * e).reshape(sc.n, 12))) / (2 * eps) for e in np.eye(q0.size)]).T
+    assert np.max(np.abs(fd1 - J1.toarray())) > 1e-4 * np.max(np.abs(fd1))
+
+
+def test_hinge5_is_a_hinge():
+    """A rod on a world hinge, released spinning about its centre (ω off the hinge axis): the five-row hinge and the
+    six-row linear hinge give the same motion up to the second point's axial freedom, i.e. up to material
+    stretch — the difference over 50 steps scales as 1/E (6e-6 at E = 1e8, 6e-8 at 1e10) — both closing their
+    constraints, while a ball joint at the pivot lets the rod tumble away (an O(1) difference)."""
+    errs = []
+    for E in (1e8, 1e10):
+        lin = G.hinge_pendulum(axis=(1, 0, 0), omega0=(3.0, 2.0, 1.0), E=E)
+        h5 = G.five_row_hinges(lin)
+        q_l, _ = O.simulate(lin, 50)
+        q_5, qd_5 = O.simulate(h5, 50)
+        errs.append(O.rel_err(q_5, q_l))
+        assert O.constraint_residual(h5, q_5) < 1e-12
+    assert errs[1] < 1e-6 and 50 < errs[0] / errs[1] < 200
+    ball = lin.copy()
+    ball.npts = np.array([1], np.int32)
+    ball.ybar_a, ball.ybar_b = lin.ybar_a[:1], lin.ybar_b[:1]
+    q_b, _ = O.simulate(ball, 50)
+    assert O.rel_err(q_b, q_l) > 1e-2
+    # the rod turns about the hinge axis only: its angular velocity is along x
+    om = O.angular_velocity(q_5, qd_5)[0]
+    assert np.linalg.norm(om) > 0.1 and np.max(np.abs(om[1:])) < 1e-3 * np.linalg.norm(om)
