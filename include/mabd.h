@@ -186,7 +186,8 @@ mabd_status mabd_partition_info(const mabd_bodies *bodies, const mabd_joints *jo
 
 /* Host-only analysis of the sparse solver's plan for a scene (no device work; forces the sparse solver):
  * out[0..7] = {assembly-tree fronts, levels, largest front (rows), front storage (doubles), flops of one
- * numeric factorization (fp64, SYRK counted as the full square), task-list ints, launches per step, dual rows}. */
+ * numeric factorization (fp64, the algorithmic Cholesky count 2·Σ(nn³/6 + nn²mm/2 + nn·mm²/2) over the fronts,
+ * nn eliminated and mm boundary rows), task-list ints, launches per step, dual rows}. */
 mabd_status mabd_sparse_plan_stats(const mabd_bodies *bodies, const mabd_joints *joints, double *out);
 
 /* Host-only plan of the line Gauss-Seidel solver (solver 4; R10) for a scene: counts = {points, chains,

@@ -144,6 +144,28 @@ def partition_info(scene, world: int, rank: int) -> dict:
     return dict(zip(keys, list(out)))
 
 
+def sparse_plan_stats(scene) -> dict:
+    """Host-only statistics of the sparse solver's plan (mabd_sparse_plan_stats; no GPU needed)."""
+    lib = load_library()
+    n = int(scene.q0.shape[0])
+    K = int(scene.body_a.shape[0])
+    P = int(np.asarray(scene.npts).sum()) if K else 0
+    k = dict(q0=_f64(scene.q0, (n, 12)), qd0=_f64(scene.qd0, (n, 12)), mbar=_f64(scene.mbar, (n, 10)),
+             volume=_f64(scene.volume, (n,)), youngs=_f64(scene.youngs, (n,)), poisson=_f64(scene.poisson, (n,)),
+             body_a=_i32(scene.body_a, (K,)), body_b=_i32(scene.body_b, (K,)), npts=_i32(scene.npts, (K,)),
+             ybar_a=_f64(scene.ybar_a, (P, 3)), ybar_b=_f64(scene.ybar_b, (P, 3)))
+    b = _Bodies(n, _ptr(k["q0"]), _ptr(k["qd0"]), _ptr(k["mbar"]), _ptr(k["volume"]), _ptr(k["youngs"]),
+                _ptr(k["poisson"]), None, (ctypes.c_double * 3)(*[float(x) for x in np.asarray(scene.gravity)]))
+    j = _Joints(K, _ptr(k["body_a"], _ip), _ptr(k["body_b"], _ip), _ptr(k["npts"], _ip), _ptr(k["ybar_a"]),
+                _ptr(k["ybar_b"]))
+    out = (ctypes.c_double * 8)()
+    st = lib.mabd_sparse_plan_stats(ctypes.byref(b), ctypes.byref(j), out)
+    if st != MABD_OK:
+        raise MabdError(st, lib.mabd_last_error(None).decode())
+    keys = ["fronts", "levels", "max_front", "front_doubles", "flops", "tasks", "launches", "dual_rows"]
+    return dict(zip(keys, list(out)))
+
+
 class Simulator:
     """One libmabd handle: ``mabd_create`` → ``prefactor(h)`` → ``step(h, n)`` → ``get_state()``.
 

@@ -74,7 +74,7 @@ struct SparsePlan {
   std::vector<int32_t> bnd_off, bnd, ea_off, ea_map;
   std::vector<int32_t> ablk, acoff, acon;
   int64_t front_doubles = 0, w_doubles = 0;
-  double flops = 0.0;                                    // numeric factorization flops per step
+  double flops = 0.0;  // numeric factorization flops per step: 2 × (Σ nn³/6 + nn²mm/2 + nn·mm²/2), the Cholesky count
   // launch schedule, by assembly-tree height
   struct Panel { int64_t potrf, n_potrf, trsm, n_trsm, syrk, n_syrk; };  // offsets into tasks
   struct Level {

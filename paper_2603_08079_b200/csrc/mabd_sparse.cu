@@ -1291,7 +1291,8 @@ static bool mf_symbolic(const mabd_bodies* B, Plan* plan, std::string* msg) {
     fo += (f * f + 31) & ~int64_t(31);
     s.woff[i] = wo;
     wo += (f + 3) & ~int64_t(3);
-    flops += (double)nn * nn * nn / 3.0 + (double)nn * nn * mm + (double)nn * mm * mm;
+    // algorithmic multiply-adds of the front: POTRF nn³/6, TRSM nn²mm/2, SYRK (lower) nn·mm²/2
+    flops += (double)nn * nn * nn / 6.0 + 0.5 * (double)nn * nn * mm + 0.5 * (double)nn * mm * mm;
     s.bnd_off[i] = (int32_t)s.bnd.size();
     s.bnd.insert(s.bnd.end(), bnd[i].begin(), bnd[i].end());
     for (int c : kids[i]) s.height[i] = std::max(s.height[i], s.height[c] + 1);
