@@ -19,12 +19,12 @@
  *   - Arrays of bodies are row-major [n][12] ("AoS" from the caller's view); the library keeps its own
  *     SoA, topology-ordered copy on the device and undoes the ordering on output.
  *   - mbar is the packed symmetric 4×4 generalized mass M̄ with M_A = M̄ ⊗ I₃,
- *     upper triangle row-major (00,01,02,03,11,12,13,22,23,33). This version requires the body frame
- *     to be central and principal (M̄ diagonal, reading A8); other inputs → MABD_EUNSUPPORTED.
+ *     upper triangle row-major (00,01,02,03,11,12,13,22,23,33); any SPD M̄ (any material frame: bodies
+ *     are mapped to their central principal frame internally and back on output, reading R8).
  *   - Joints are point-coincidence constraints C = x_a(ȳ_a) − x_b(ȳ_b), x(ȳ) = Aȳ + t: a ball joint has
  *     1 point, the linear ("affine") hinge has 2 points on the axis. body_b = −1
- *     makes an anchor to the world point stored in ybar_b. Nonlinear joints are not
- *     supported in this version.
+ *     makes an anchor to the world point stored in ybar_b. The five-row (nonlinear) hinge of P:391-404 is
+ *     joints.kind = 1; the universal and prismatic joints are not supported in this version.
  *
  * Ownership
  *   - Every input pointer is borrowed for the duration of the call only; the library copies what it needs.
@@ -63,7 +63,7 @@ typedef enum {
   MABD_ENCCL = 5,        /* NCCL error (multi-GPU)                                                */
   MABD_ESINGULAR = 6,    /* dual matrix not SPD (redundant joints)                                */
   MABD_ENONFINITE = 7,   /* non-finite state or det A ≤ 1e-9                                      */
-  MABD_EUNSUPPORTED = 8  /* input outside this version's scope (non-diagonal M̄, topology …)        */
+  MABD_EUNSUPPORTED = 8  /* input outside this version's scope (topology / joint kind for a solver …) */
 } mabd_status;
 
 /* Bodies, in the caller's order. */
@@ -87,6 +87,11 @@ typedef struct {
   const int32_t *npts;       /* [K] in {1 (ball / anchor), 2 (linear hinge)}                        */
   const double *ybar_a;      /* [Σnpts][3] material points on body_a (body frame)                  */
   const double *ybar_b;      /* [Σnpts][3] material points on body_b, or world points for anchors  */
+  const int32_t *kind;       /* [K] or NULL (all 0). 0: point joint (ball / linear 6-row hinge / anchor);
+                                1: five-row hinge (Eq. hinge; R13): npts = 2, the points on
+                                the axis (the axis in body_a's frame is ȳ_a[1] − ȳ_a[0]); the first point is a
+                                ball, the second keeps only its two rows normal to the axis in the hinge frame
+                                R_H = ΔR_H Rᵀ(A_a), re-evaluated every Newton iteration. Sparse solver only.   */
 } mabd_joints;
 
 typedef struct {

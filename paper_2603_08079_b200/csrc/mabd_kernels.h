@@ -136,6 +136,14 @@ struct SparseArgs {
   const int32_t* pa;           // [np] body on side a
   const int32_t* pb;           // [np] body on side b or −1 (world)
   const double* py;            // [np][6] ȳ_a, ȳ_b (world point when pb < 0)
+  // five-row hinges (R13): the second axis point of such a joint is "projected": its rows are
+  // [w0; w1; dummy] with w_i = R_a ΔR_H[row i]ᵀ (i = x̃, z̃) re-evaluated every step, the dummy row decoupled
+  // (S = 1, r = 0, λ = 0) so the 3×3 block structure stays
+  const int32_t* pslot;        // [np] slot of a projected point, or −1 (null: no projected points)
+  const double* pdr;           // [nproj][6] ΔR_H rows x and z (body a's canonical frame)
+  double* pw;                  // [nproj][6] w0, w1 of this step
+  const int32_t* pplist;       // [nproj] the projected points
+  int64_t nproj;
   const int32_t* inc_off;      // [n+1] CSR body → incident points (2·point + side)
   const int32_t* inc;
   double *rhs, *lam, *res, *dl, *yy;  // component-major [3][np]: r = C(q̃), λ, residual, correction, solve scratch

@@ -35,6 +35,8 @@ bool loop_split(const mabd_joints* J, int64_t n, LoopPlan* L, std::string* msg) 
     while (par[x] != x) x = par[x] = par[par[x]];
     return x;
   };
+  for (int64_t k = 0; J->kind && k < J->n_joints; ++k)
+    if (J->kind[k] != 0) return *msg = "five-row hinges need the sparse solver", false;
   L->keep.clear();
   L->breakers.clear();
   for (int64_t k = 0; k < J->n_joints; ++k) {

@@ -243,6 +243,9 @@ static mabd_status validate(const mabd_bodies* B, const mabd_joints* J, const ma
     if (b < -1 || b >= B->n) return *msg = fmt("joint %lld: body_b out of range", (long long)k), MABD_EINVAL;
     if (a == b) return *msg = fmt("joint %lld: both ends on body %lld", (long long)k, a), MABD_EINVAL;
     if (np != 1 && np != 2) return *msg = fmt("joint %lld: npts must be 1 or 2", (long long)k), MABD_EINVAL;
+    if (J->kind && J->kind[k] != 0 && (J->kind[k] != 1 || np != 2))
+      return *msg = fmt("joint %lld: kind must be 0, or 1 (five-row hinge) with npts = 2", (long long)k),
+             MABD_EINVAL;
     P += np;
   }
   for (int64_t p = 0; p < 3 * P; ++p)

@@ -92,6 +92,10 @@ struct SparsePlan {
   std::vector<int64_t> loff;                             // [nnode] inverse diagonal blocks of big fronts
   int64_t linv_doubles = 0;
   int32_t refine = 1;                                    // iterative-refinement passes per step
+  // five-row hinges: projected points (R13)
+  std::vector<int32_t> pslot, pplist;
+  std::vector<double> pdr;
+  size_t o_pslot = 0, o_pdr = 0, o_pw = 0, o_pplist = 0;
   // line Gauss-Seidel (MABD_SOLVER_LINE_GS; gs_build in mabd_sparse.cu)
   std::vector<int32_t> gs_chain_pts, gs_chain_off, gs_color_off;
   int32_t gs_ncolor = 0, gs_sweeps = 0;

@@ -21,6 +21,7 @@
 #include <algorithm>
 #include <cstdlib>
 #include <cmath>
+#include <cstring>
 #include <functional>
 #include <numeric>
 #include <string>
@@ -85,6 +86,37 @@ __device__ __forceinline__ void body_R(const SparseArgs& a, int64_t j, double* R
   for (int c = 0; c < 9; ++c) R[c] = a.b.rs[c * a.b.ld + j];
 }
 
+// projected point (five-row hinge): v ← [w0·v, w1·v, 0] (its rows), and the transpose x ← w0 x0 + w1 x1
+__device__ __forceinline__ void project_rows(const SparseArgs& a, int64_t p, double* v) {
+  const double* w = a.pw + 6 * (int64_t)a.pslot[p];
+  const double v0 = w[0] * v[0] + w[1] * v[1] + w[2] * v[2];
+  const double v1 = w[3] * v[0] + w[4] * v[1] + w[5] * v[2];
+  v[0] = v0;
+  v[1] = v1;
+  v[2] = 0.0;
+}
+__device__ __forceinline__ void project_cols(const SparseArgs& a, int64_t p, double* x) {
+  const double* w = a.pw + 6 * (int64_t)a.pslot[p];
+  const double x0 = x[0], x1 = x[1];
+#pragma unroll
+  for (int e = 0; e < 3; ++e) x[e] = w[e] * x0 + w[3 + e] * x1;
+}
+
+// per step: w_i = R_a ΔR_H[i]ᵀ of every projected point (R_a of this step's linearisation point, in rs)
+__global__ void proj_rows_kernel(SparseArgs a) {
+  const int64_t s = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (s >= a.nproj) return;
+  const int64_t p = a.pplist[s];
+  double R[9];
+  body_R(a, a.pa[p], R);
+#pragma unroll
+  for (int i = 0; i < 2; ++i) {
+    const double* d = a.pdr + 6 * s + 3 * i;
+#pragma unroll
+    for (int c = 0; c < 3; ++c) a.pw[6 * s + 3 * i + c] = R[3 * c] * d[0] + R[3 * c + 1] * d[1] + R[3 * c + 2] * d[2];
+  }
+}
+
 // points: r = C(q̃) (q̃ = qⁿ + δq̃)
 __global__ void sparse_rhs_kernel(SparseArgs a) {
   const int64_t ld = a.b.ld;
@@ -106,6 +138,7 @@ __global__ void sparse_rhs_kernel(SparseArgs a) {
 #pragma unroll
       for (int e = 0; e < 3; ++e) r[e] += sg * x[e];
     }
+    if (a.pslot && a.pslot[p] >= 0) project_rows(a, p, r);
 #pragma unroll
     for (int e = 0; e < 3; ++e) a.rhs[e * a.np + p] = r[e];
   }
@@ -125,6 +158,7 @@ __device__ __forceinline__ void body_apply(const SparseArgs& a, int64_t j, const
     double w[3], wl[3];
 #pragma unroll
     for (int c = 0; c < 3; ++c) w[c] = x[c * a.np + p];
+    if (a.pslot && a.pslot[p] >= 0) project_cols(a, p, w);
     mat3t_vec(R, w, wl);  // body frame
     add_point_force(g, a.py + 6 * p + 3 * side, wl, side == 0 ? 1.0 : -1.0);
   }
@@ -158,6 +192,10 @@ __global__ void mv_point_kernel(SparseArgs a) {
       for (int e = 0; e < 3; ++e)
         s[e] += sg * (a.vv[(0 + e) * a.n + j] * y[0] + a.vv[(3 + e) * a.n + j] * y[1] +
                       a.vv[(6 + e) * a.n + j] * y[2] + a.vv[(9 + e) * a.n + j]);
+    }
+    if (a.pslot && a.pslot[p] >= 0) {  // rows w·(J V), the dummy row's S = 1
+      project_rows(a, p, s);
+      s[2] = a.lam[2 * a.np + p];  // (the refinement's x is λ)
     }
 #pragma unroll
     for (int e = 0; e < 3; ++e) a.res[e * a.np + p] = a.rhs[e * a.np + p] - s[e];
@@ -209,9 +247,12 @@ __global__ void mf_assemble_kernel(SparseArgs a) {
        b += (int64_t)gridDim.x * blockDim.x) {
     const int node = m.ablk[3 * b], rb = m.ablk[3 * b + 1], cb = m.ablk[3 * b + 2];
     double S[9] = {0, 0, 0, 0, 0, 0, 0, 0, 0};
+    int prow = -1, pcol = -1;
     for (int c = m.acoff[b]; c < m.acoff[b + 1]; ++c) {
       const int re = m.acon[2 * c], ce = m.acon[2 * c + 1];
       const int pr = re >> 1, sr = re & 1, pc = ce >> 1, sc = ce & 1;
+      prow = pr;
+      pcol = pc;
       const int64_t j = sr == 0 ? a.pa[pr] : a.pb[pr];
       const double sg = (sr == sc) ? 1.0 : -1.0;
       double R[9], P[9], T[9];
@@ -222,6 +263,20 @@ __global__ void mf_assemble_kernel(SparseArgs a) {
       rot_conj(R, P, T);
 #pragma unroll
       for (int e = 0; e < 9; ++e) S[e] += sg * T[e];
+    }
+    if (a.pslot && prow >= 0) {  // projected points: S ← T_r S T_cᵀ (+1 on a projected point's dummy row)
+      const bool pjr = a.pslot[prow] >= 0, pjc = a.pslot[pcol] >= 0;
+      if (pjr)
+#pragma unroll
+        for (int c = 0; c < 3; ++c) {
+          double col[3] = {S[c], S[3 + c], S[6 + c]};
+          project_rows(a, prow, col);
+          S[c] = col[0]; S[3 + c] = col[1]; S[6 + c] = col[2];
+        }
+      if (pjc)
+#pragma unroll
+        for (int r = 0; r < 3; ++r) project_rows(a, pcol, S + 3 * r);
+      if (pjr && prow == pcol) S[8] = 1.0;
     }
     double* F = m.F + m.foff[node];
     const int64_t f = m.fdim[node];
@@ -894,6 +949,7 @@ cudaError_t sparse_step(const Plan& p, const DevPtrs& d, const StepConsts& k, cu
     sparse_update_kernel<<<grid_for(a.n), 256, 0, st>>>(a);
     return cudaGetLastError();
   }
+  if (a.nproj) proj_rows_kernel<<<(unsigned)((a.nproj + 127) / 128), 128, 0, st>>>(a);
   sparse_rhs_kernel<<<grid_for(a.np), 256, 0, st>>>(a);
   cudaError_t e;
   if ((e = cudaMemsetAsync(a.mf.F, 0, sizeof(double) * sp.front_doubles, st))) return e;
@@ -1504,6 +1560,24 @@ static bool mf_symbolic(const mabd_bodies* B, Plan* plan, std::string* msg) {
   return true;
 }
 
+// ΔR_H of the five-row hinge: I + [v]× + [v]×²/(1 + a_y), v = a × e_y, turning the unit axis a onto e_y
+// (a = −e_y, where the formula is singular: diag(1, −1, −1)).
+static void hinge_frame(const double* a, double R[3][3]) {
+  if (a[1] <= -1.0 + 1e-12) {
+    const double D[3][3] = {{1, 0, 0}, {0, -1, 0}, {0, 0, -1}};
+    std::memcpy(R, D, sizeof(D));
+    return;
+  }
+  const double v[3] = {-a[2], 0.0, a[0]};  // a × e_y
+  const double V[3][3] = {{0, -v[2], v[1]}, {v[2], 0, -v[0]}, {-v[1], v[0], 0}};
+  for (int r = 0; r < 3; ++r)
+    for (int c = 0; c < 3; ++c) {
+      double vv = 0;
+      for (int m = 0; m < 3; ++m) vv += V[r][m] * V[m][c];
+      R[r][c] = (r == c ? 1.0 : 0.0) + V[r][c] + vv / (1.0 + a[1]);
+    }
+}
+
 bool sparse_build(const mabd_bodies* B, const mabd_joints* J, Plan* p, std::vector<int64_t>* pos_of_body,
                   std::string* msg, bool symbolic) {
   const int64_t K = J->n_joints, n = B->n;
@@ -1537,6 +1611,31 @@ bool sparse_build(const mabd_bodies* B, const mabd_joints* J, Plan* p, std::vect
     const int64_t a = s.pa[q], b = s.pb[q];
     s.inc[s.inc_off[a] + fill[a]++] = (int32_t)(2 * q);
     if (b >= 0) s.inc[s.inc_off[b] + fill[b]++] = (int32_t)(2 * q + 1);
+  }
+  // five-row hinges: the second point of each is projected (rows w0, w1 from ΔR_H of the axis in body a's frame)
+  s.pslot.clear();
+  s.pdr.clear();
+  s.pplist.clear();
+  if (J->kind) {
+    s.pslot.assign(P, -1);
+    int64_t p0 = 0;
+    for (int64_t k = 0; k < K; ++k) {
+      if (J->kind[k] == 1) {
+        const double* y0 = J->ybar_a + 3 * p0;
+        double ax[3] = {y0[3] - y0[0], y0[4] - y0[1], y0[5] - y0[2]};
+        const double nrm = std::sqrt(ax[0] * ax[0] + ax[1] * ax[1] + ax[2] * ax[2]);
+        if (!(nrm > 0)) return *msg = "five-row hinge with coincident axis points", false;
+        for (double& v : ax) v /= nrm;
+        double dR[3][3];
+        hinge_frame(ax, dR);
+        s.pslot[p0 + 1] = (int32_t)s.pplist.size();
+        s.pplist.push_back((int32_t)(p0 + 1));
+        for (int i : {0, 2})
+          for (int c = 0; c < 3; ++c) s.pdr.push_back(dR[i][c]);
+      }
+      p0 += J->npts[k];
+    }
+    if (s.pplist.empty()) s.pslot.clear();
   }
   pos_of_body->resize(n);
   for (int64_t i = 0; i < n; ++i) (*pos_of_body)[i] = i;  // caller order
@@ -1573,6 +1672,7 @@ constexpr double GS_MIN_COS = 0.9;
 
 bool gs_build(const mabd_bodies* B, Plan* p, int32_t sweeps, double tol, std::string* msg) {
   SparsePlan& s = p->sparse;
+  if (!s.pplist.empty()) return *msg = "five-row hinges need the direct sparse solver", false;
   const int64_t n = p->n, np = s.np;
   s.gs_sweeps = sweeps > 0 ? sweeps : 200;
   s.gs_tol = tol > 0 ? tol : 1e-12;
@@ -1741,6 +1841,10 @@ void sparse_layout(Plan* p, const std::function<size_t(size_t)>& take) {
   s.o_woff = take(sizeof(int64_t) * NN);
   s.o_lev = take(sizeof(int32_t) * nz(s.lev_nodes.size()));
   s.o_tasks = take(sizeof(int32_t) * nz(s.tasks.size()));
+  s.o_pslot = take(sizeof(int32_t) * nz(s.pslot.size()));
+  s.o_pdr = take(sizeof(double) * nz(s.pdr.size()));
+  s.o_pw = take(sizeof(double) * nz(s.pdr.size()));
+  s.o_pplist = take(sizeof(int32_t) * nz(s.pplist.size()));
   s.o_gs_pts = take(sizeof(int32_t) * nz(s.gs_chain_pts.size()));
   s.o_gs_off = take(sizeof(int32_t) * nz(s.gs_chain_off.size()));
   s.o_gs_col = take(sizeof(int32_t) * nz(s.gs_color_off.size()));
@@ -1797,6 +1901,11 @@ cudaError_t sparse_upload(const Plan& p, char* ws, cudaStream_t st, DevPtrs* d) 
   m.loff = (const int64_t*)(ws + s.o_loff);
   m.wvec = (double*)(ws + s.o_w);
   m.woff = (const int64_t*)(ws + s.o_woff);
+  A.nproj = (int64_t)s.pplist.size();
+  A.pslot = A.nproj ? (const int32_t*)(ws + s.o_pslot) : nullptr;
+  A.pdr = (const double*)(ws + s.o_pdr);
+  A.pw = (double*)(ws + s.o_pw);
+  A.pplist = (const int32_t*)(ws + s.o_pplist);
   A.gs.chain_pts = (const int32_t*)(ws + s.o_gs_pts);
   A.gs.chain_off = (const int32_t*)(ws + s.o_gs_off);
   A.gs.color_off = (const int32_t*)(ws + s.o_gs_col);
@@ -1831,6 +1940,9 @@ cudaError_t sparse_upload(const Plan& p, char* ws, cudaStream_t st, DevPtrs* d) 
   if ((e = upv(ws, s.o_loff, s.loff, st))) return e;
   if ((e = upv(ws, s.o_lev, s.lev_nodes, st))) return e;
   if ((e = upv(ws, s.o_tasks, s.tasks, st))) return e;
+  if ((e = upv(ws, s.o_pslot, s.pslot, st))) return e;
+  if ((e = upv(ws, s.o_pdr, s.pdr, st))) return e;
+  if ((e = upv(ws, s.o_pplist, s.pplist, st))) return e;
   if ((e = upv(ws, s.o_gs_pts, s.gs_chain_pts, st))) return e;
   if ((e = upv(ws, s.o_gs_off, s.gs_chain_off, st))) return e;
   if ((e = upv(ws, s.o_gs_col, s.gs_color_off, st))) return e;
