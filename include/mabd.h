@@ -121,6 +121,9 @@ typedef struct {
                                 length-preserving Aᵀ / A of Eq. len_preserving, the elastic force is the StVK
                                 force of E = ½(AᵀA − I), and constraint forces use diag₄(A)H̄⁻¹diag₄(Aᵀ)
                                 ("A ≈ R"). Equal to (0) at rigid states; an approximation otherwise. */
+  int32_t host_exchange;     /* world > 1 without NCCL: this process advances rank `rank`'s share and the
+                                caller moves the per-step exchange (mabd_step_exchange_begin / end); see
+                                there. One Newton iteration only.                                       */
   int32_t gs_sweeps;         /* solver 4: maximum sweeps per step (0 = 200)                           */
   double gs_tol;             /* solver 4: stop when max|C(q̃) − Sλ| ≤ gs_tol · max|C(q̃)| (0 = 1e-12)   */
 } mabd_options;
@@ -154,6 +157,19 @@ mabd_status mabd_step_async(mabd_handle h_, double h, int64_t nsteps);
 
 /* Synchronise the handle's stream and report errors of the steps enqueued since the last check (see mabd_step). */
 mabd_status mabd_check(mabd_handle h_);
+
+/* Caller-driven exchange for split scenes (options.world > 1, options.host_exchange = 1): the step
+ * of a chain or tree split across ranks has one all-gather (per-rank top systems, resp. the subtree roots'
+ * condensed blocks). mabd_step_exchange_begin(h) runs this rank's share up to it and synchronises;
+ * mabd_exchange_info gives the buffer's shape (doubles per rank, ranks, this rank's slot); mabd_exchange_copy
+ * copies this rank's slot out to host_all[slot·per_rank …] (to_device = 0) or the whole host_all in
+ * (to_device = 1, after the caller's all-gather); mabd_step_exchange_end finishes the step and checks errors. Any
+ * transport works (a test uses gloo between processes). mabd_get_state then returns this rank's bodies current
+ * and the others stale (the NCCL path broadcasts them). */
+mabd_status mabd_step_exchange_begin(mabd_handle h_, double h);
+mabd_status mabd_exchange_info(mabd_handle h_, int64_t *doubles_per_rank, int32_t *ranks, int32_t *my_slot);
+mabd_status mabd_exchange_copy(mabd_handle h_, double *host_all, int32_t to_device);
+mabd_status mabd_step_exchange_end(mabd_handle h_);
 
 /* Copy the current state out, in the caller's body order ([n][12] each; either pointer may be NULL).
  * out_on_device != 0 means the pointers are device memory. Synchronises the handle's stream. */

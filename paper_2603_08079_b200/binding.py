@@ -20,6 +20,7 @@ STATUS = {0: "MABD_OK", 1: "MABD_EINVAL", 2: "MABD_ESTATE", 3: "MABD_ENOMEM", 4:
 SOLVERS = {0: "auto", 1: "chain", 2: "tree", 3: "sparse", 4: "line_gs", 5: "loop_breaker"}
 
 EXPORTED = ["mabd_workspace_size", "mabd_create", "mabd_prefactor", "mabd_step", "mabd_step_async", "mabd_check",
+            "mabd_step_exchange_begin", "mabd_exchange_info", "mabd_exchange_copy", "mabd_step_exchange_end",
             "mabd_get_state",
             "mabd_set_state", "mabd_set_wrench", "mabd_query", "mabd_solver_stats", "mabd_nccl_unique_id", "mabd_partition_info",
             "mabd_destroy", "mabd_last_error"]
@@ -50,7 +51,7 @@ class _Options(ctypes.Structure):
                 ("rank", ctypes.c_int32), ("world", ctypes.c_int32), ("nccl_unique_id", ctypes.c_void_p),
                 ("workspace", ctypes.c_void_p), ("workspace_bytes", ctypes.c_size_t),
                 ("cuda_stream", ctypes.c_void_p), ("no_graphs", ctypes.c_int32), ("rotation", ctypes.c_int32),
-                ("gs_sweeps", ctypes.c_int32), ("gs_tol", ctypes.c_double)]
+                ("host_exchange", ctypes.c_int32), ("gs_sweeps", ctypes.c_int32), ("gs_tol", ctypes.c_double)]
 
 ROTATIONS = {"polar": 0, "length_preserving": 1}
 
@@ -76,6 +77,11 @@ def load_library(path: str = LIB_PATH) -> ctypes.CDLL:
     lib.mabd_step.argtypes = [H, ctypes.c_double, ctypes.c_int64]
     lib.mabd_step_async.argtypes = [H, ctypes.c_double, ctypes.c_int64]
     lib.mabd_check.argtypes = [H]
+    lib.mabd_step_exchange_begin.argtypes = [H, ctypes.c_double]
+    lib.mabd_exchange_info.argtypes = [H, ctypes.POINTER(ctypes.c_int64), ctypes.POINTER(ctypes.c_int32),
+                                       ctypes.POINTER(ctypes.c_int32)]
+    lib.mabd_exchange_copy.argtypes = [H, ctypes.c_void_p, ctypes.c_int32]
+    lib.mabd_step_exchange_end.argtypes = [H]
     lib.mabd_get_state.argtypes = [H, ctypes.c_void_p, ctypes.c_void_p, ctypes.c_int]
     lib.mabd_set_state.argtypes = [H, ctypes.c_void_p, ctypes.c_void_p, ctypes.c_int]
     lib.mabd_set_wrench.argtypes = [H, ctypes.c_void_p, ctypes.c_int]
@@ -178,7 +184,7 @@ class Simulator:
                  kind=None,
                  solver: int = 0, device: Optional[int] = None, stream=None, world: int = 1, rank: int = 0,
                  nccl_id: Optional[bytes] = None, newton_iters: int = 1, no_graphs: bool = False,
-                 rotation: str = "polar", gs_sweeps: int = 0, gs_tol: float = 0.0):
+                 rotation: str = "polar", gs_sweeps: int = 0, gs_tol: float = 0.0, host_exchange: bool = False):
         import torch
 
         self._lib = load_library()
@@ -208,7 +214,7 @@ class Simulator:
             opts = _Options(int(newton_iters), 1, int(solver), int(rank), int(world),
                             ctypes.cast(self._nccl_id, ctypes.c_void_p) if self._nccl_id is not None else None,
                             None, 0, ctypes.c_void_p(self._stream.cuda_stream), int(bool(no_graphs)),
-                            ROTATIONS[rotation], int(gs_sweeps), float(gs_tol))
+                            ROTATIONS[rotation], int(bool(host_exchange)), int(gs_sweeps), float(gs_tol))
             nbytes = ctypes.c_size_t(0)
             self._check(self._lib.mabd_workspace_size(ctypes.byref(self._bodies), ctypes.byref(self._joints),
                                                       ctypes.byref(opts), ctypes.byref(nbytes)), None)
@@ -250,6 +256,24 @@ class Simulator:
 
     def check(self) -> None:
         self._check(self._lib.mabd_check(self._h), self._h)
+
+    # caller-driven exchange of a split scene (options.host_exchange)
+    def exchange_begin(self, h: float) -> None:
+        self._check(self._lib.mabd_step_exchange_begin(self._h, float(h)), self._h)
+
+    def exchange_info(self) -> dict:
+        per, ranks, slot = ctypes.c_int64(), ctypes.c_int32(), ctypes.c_int32()
+        self._check(self._lib.mabd_exchange_info(self._h, ctypes.byref(per), ctypes.byref(ranks), ctypes.byref(slot)),
+                    self._h)
+        return {"doubles_per_rank": per.value, "ranks": ranks.value, "slot": slot.value}
+
+    def exchange_copy(self, host_all: np.ndarray, to_device: bool) -> None:
+        assert host_all.dtype == np.float64 and host_all.flags.c_contiguous
+        self._check(self._lib.mabd_exchange_copy(self._h, ctypes.c_void_p(host_all.ctypes.data), int(to_device)),
+                    self._h)
+
+    def exchange_end(self) -> None:
+        self._check(self._lib.mabd_step_exchange_end(self._h), self._h)
 
     def query(self) -> dict:
         s, l, nb, nr = ctypes.c_int32(), ctypes.c_int32(), ctypes.c_int64(), ctypes.c_int64()

@@ -41,6 +41,7 @@ struct mabd_ctx {
   int64_t steps_done = 0;
   int64_t steps_pending = 0;   // enqueued by mabd_step_async since the last mabd_check
   bool use_graphs = true;      // options.no_graphs == 0 and a non-default stream
+  double exchange_h = 0.0;     // a host-exchange step in progress (mabd_step_exchange_begin)
   cudaGraphExec_t graph = nullptr;
   double graph_h = 0.0;
 };
@@ -237,11 +238,85 @@ mabd_status mabd_check(mabd_handle c) {
 
 mabd_status mabd_step_async(mabd_handle c, double h, int64_t nsteps) {
   if (!c) return fail(nullptr, MABD_EINVAL, "NULL handle");
+  if (c->plan.host_exchange && nsteps > 0)
+    return fail(c, MABD_ESTATE, "host_exchange: step with mabd_step_exchange_begin / end");
   return enqueue_steps(c, h, nsteps);
+}
+
+// ---- caller-driven exchange (options.host_exchange; SURVEY §8(e) split scenes without NCCL)
+static mabd_status exchange_view(mabd_ctx* c, double** buf, int64_t* per_rank, int32_t* ranks, int32_t* slot) {
+  const Plan& p = c->plan;
+  if (p.solver == MABD_SOLVER_CHAIN && p.n_parts > 1) {
+    *buf = (double*)c->d.all_tops;
+    *per_rank = sizeof(Top) / sizeof(double);
+    *ranks = p.n_parts;
+    *slot = p.part_lo;
+    return MABD_OK;
+  }
+  if (p.solver == MABD_SOLVER_TREE && p.tree.parts > 1) {
+    *buf = c->d.tree.xbuf;
+    *per_rank = (int64_t)p.tree.rpp * TREE_TSLOT;
+    *ranks = p.tree.parts;
+    *slot = p.tree.part;
+    return MABD_OK;
+  }
+  return fail(c, MABD_ESTATE, "no exchange: the scene is not split across ranks");
+}
+
+mabd_status mabd_exchange_info(mabd_handle c, int64_t* doubles_per_rank, int32_t* ranks, int32_t* my_slot) {
+  if (!c || !doubles_per_rank || !ranks || !my_slot) return fail(c, MABD_EINVAL, "NULL argument");
+  double* buf;
+  return exchange_view(c, &buf, doubles_per_rank, ranks, my_slot);
+}
+
+mabd_status mabd_exchange_copy(mabd_handle c, double* host_all, int32_t to_device) {
+  if (!c || !host_all) return fail(c, MABD_EINVAL, "NULL argument");
+  double* buf;
+  int64_t per;
+  int32_t ranks, slot;
+  mabd_status st = exchange_view(c, &buf, &per, &ranks, &slot);
+  if (st != MABD_OK) return st;
+  CUDA_TRY(c, cudaSetDevice(c->device));
+  if (to_device)
+    CUDA_TRY(c, cudaMemcpyAsync(buf, host_all, sizeof(double) * per * ranks, cudaMemcpyHostToDevice, c->stream));
+  else
+    CUDA_TRY(c, cudaMemcpyAsync(host_all + per * slot, buf + per * slot, sizeof(double) * per,
+                                cudaMemcpyDeviceToHost, c->stream));
+  CUDA_TRY(c, cudaStreamSynchronize(c->stream));
+  return MABD_OK;
+}
+
+mabd_status mabd_step_exchange_begin(mabd_handle c, double h) {
+  if (!c) return fail(nullptr, MABD_EINVAL, "NULL handle");
+  if (!c->plan.host_exchange) return fail(c, MABD_ESTATE, "options.host_exchange is not set");
+  if (!c->prefactored) return fail(c, MABD_ESTATE, "step before mabd_prefactor");
+  if (!(h > 0.0) || !std::isfinite(h)) return fail(c, MABD_EINVAL, "h must be > 0 (got %g)", h);
+  CUDA_TRY(c, cudaSetDevice(c->device));
+  if (h != c->h_pref) {
+    mabd_status st = mabd_prefactor(c, h);
+    if (st != MABD_OK) return st;
+  }
+  c->exchange_h = h;
+  CUDA_TRY(c, launch_step(c->plan, c->d, h, 0, c->stream, 1));
+  CUDA_TRY(c, cudaStreamSynchronize(c->stream));
+  return MABD_OK;
+}
+
+mabd_status mabd_step_exchange_end(mabd_handle c) {
+  if (!c) return fail(nullptr, MABD_EINVAL, "NULL handle");
+  if (!(c->exchange_h > 0.0)) return fail(c, MABD_ESTATE, "mabd_step_exchange_end without begin");
+  CUDA_TRY(c, cudaSetDevice(c->device));
+  CUDA_TRY(c, launch_step(c->plan, c->d, c->exchange_h, 0, c->stream, 2));
+  CUDA_TRY(c, launch_step_end(c->d, c->stream));
+  c->exchange_h = 0.0;
+  c->steps_pending += 1;
+  return mabd_check(c);
 }
 
 mabd_status mabd_step(mabd_handle c, double h, int64_t nsteps) {
   if (!c) return fail(nullptr, MABD_EINVAL, "NULL handle");
+  if (c->plan.host_exchange && nsteps > 0)
+    return fail(c, MABD_ESTATE, "host_exchange: step with mabd_step_exchange_begin / end");
   const mabd_status st = enqueue_steps(c, h, nsteps);
   if (st != MABD_OK) return st;
   if (nsteps == 0 && c->steps_pending == 0) return MABD_OK;

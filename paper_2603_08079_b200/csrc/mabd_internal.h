@@ -65,6 +65,7 @@ struct StepConsts {
   int32_t step_index;
   int32_t iter, niter;     // Newton iteration of this launch sequence, iterations per step
   int32_t lp;              // 1: polar-free variant (options.rotation = MABD_ROTATION_LENGTH_PRESERVING, DESIGN R9)
+  int32_t phase;           // host side only: 0 whole step; host exchange: 1 up to the exchange, 2 after it
   int32_t* err;            // [0] flags (1 nonfinite, 2 singular), [1] first failing step
 };
 

@@ -219,6 +219,8 @@ static mabd_status validate(const mabd_bodies* B, const mabd_joints* J, const ma
     if (o->world > 256) return *msg = "world > 256", MABD_EINVAL;
     if (o->solver < 0 || o->solver > MABD_SOLVER_LOOP_BREAKER) return *msg = "unknown solver", MABD_EINVAL;
     if (o->gs_sweeps < 0 || !(o->gs_tol >= 0.0)) return *msg = "gs_sweeps and gs_tol must be >= 0", MABD_EINVAL;
+    if (o->host_exchange && (o->world < 2 || o->newton_iters > 1))
+      return *msg = "host_exchange needs world >= 2 and one Newton iteration", MABD_EINVAL;
     if (o->rotation != MABD_ROTATION_POLAR && o->rotation != MABD_ROTATION_LENGTH_PRESERVING)
       return *msg = "rotation must be MABD_ROTATION_POLAR (0) or MABD_ROTATION_LENGTH_PRESERVING (1)", MABD_EINVAL;
     if (o->residual_rhs != 0 && o->residual_rhs != 1)
@@ -566,8 +568,10 @@ mabd_status build_plan(const mabd_bodies* B, const mabd_joints* J, const mabd_op
     if (ok) {
       p->solver = MABD_SOLVER_CHAIN;
       const int W = o && o->world > 1 ? o->world : 1;
-      p->use_nccl = W > 1 && o->nccl_unique_id != nullptr;
-      if (!partition_chain(p, W, o ? o->rank : 0, W > 1 && !p->use_nccl, msg)) return MABD_EINVAL;
+      p->use_nccl = W > 1 && o->nccl_unique_id != nullptr && !o->host_exchange;
+      p->host_exchange = W > 1 && o->host_exchange;
+      if (!partition_chain(p, W, o ? o->rank : 0, W > 1 && !p->use_nccl && !p->host_exchange, msg))
+        return MABD_EINVAL;
     }
     if (!ok && req == MABD_SOLVER_CHAIN) return *msg = "chain solver requested: " + why, MABD_EINVAL;
   }
@@ -603,8 +607,9 @@ mabd_status build_plan(const mabd_bodies* B, const mabd_joints* J, const mabd_op
   if (p->newton_iters > 1) p->launches_per_step = p->newton_iters * p->launches_per_step + 2;  // + prep, final
   if (o && o->world > 1 && p->solver == MABD_SOLVER_TREE) {
     const int W = o->world;
-    p->use_nccl = o->nccl_unique_id != nullptr;
-    if (!tree_partition(p, W, o->rank, !p->use_nccl, msg)) return MABD_EINVAL;
+    p->use_nccl = o->nccl_unique_id != nullptr && !o->host_exchange;
+    p->host_exchange = o->host_exchange != 0;
+    if (!tree_partition(p, W, o->rank, !p->use_nccl && !p->host_exchange, msg)) return MABD_EINVAL;
   }
   if (o && o->world > 1 && (p->solver == MABD_SOLVER_SPARSE || p->solver == MABD_SOLVER_LINE_GS))
     return *msg = "world > 1 is implemented for the chain and tree solvers (run nets as replicas)",
@@ -923,6 +928,7 @@ cudaError_t launch_step_end(const DevPtrs& d, cudaStream_t st) {
 static cudaError_t launch_step_parts(const Plan& p, const DevPtrs& d, ChainArgs a, cudaStream_t st) {
   cudaError_t e;
   const StepConsts& k = a.k;
+  if (k.phase == 2) goto after_exchange;  // host exchange: the caller has filled all_tops
   a.seg_list = d.local_windows;
   if ((e = launch_chain(a, (int)p.local_windows.size(), false, st))) return e;
   if (p.n_long == 0) return cudaSuccess;  // independent short chains (config 2): no exchange, nothing to finish
@@ -951,10 +957,12 @@ static cudaError_t launch_step_parts(const Plan& p, const DevPtrs& d, ChainArgs 
     sq.k = k;
     if ((e = launch_seq_top(sq, st))) return e;
   }
+  if (k.phase == 1) return cudaSuccess;  // host exchange: the caller all-gathers all_tops now
   if (p.use_nccl) {
     const int rc = nccl_allgather_doubles(d.nccl_comm, (double*)d.all_tops, sizeof(Top) / sizeof(double), p.part_lo, st);
     if (rc != 0) return nccl_step_failed(rc), cudaErrorUnknown;  // mabd_step reports MABD_ENCCL
   }
+after_exchange:
   {
     BtdArgs b{};
     b.top_in = d.all_tops;
@@ -1020,7 +1028,7 @@ __global__ void iter_final_kernel(double* qd, const double* z, int64_t ld) {
 
 static cudaError_t launch_iteration(const Plan& p, const DevPtrs& d, const StepConsts& k, cudaStream_t st);
 
-cudaError_t launch_step(const Plan& p, const DevPtrs& d, double h, int32_t step, cudaStream_t st) {
+cudaError_t launch_step(const Plan& p, const DevPtrs& d, double h, int32_t step, cudaStream_t st, int phase) {
   StepConsts k;
   k.h = h;
   k.ih = 1.0 / h;
@@ -1031,6 +1039,7 @@ cudaError_t launch_step(const Plan& p, const DevPtrs& d, double h, int32_t step,
   k.iter = 0;
   k.niter = std::max(1, p.newton_iters);
   k.lp = p.rotation == MABD_ROTATION_LENGTH_PRESERVING ? 1 : 0;
+  k.phase = phase;
   if (k.niter == 1) return launch_iteration(p, d, k, st);
   const int64_t tot = 12 * d.b.ld;
   const unsigned grid = (unsigned)((tot + 255) / 256);

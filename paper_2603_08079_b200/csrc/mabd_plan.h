@@ -25,6 +25,7 @@ struct BtdLevel {
 constexpr int TREE_CAP = 256;
 constexpr int TREE_TOP_SMALL = 32;  // a top set larger than this gets a middle layer …
 constexpr int TREE_MID_CAP = 7;     // … of subtrees with at most this many bodies (measured: 7 < 15 < 31 < 63)
+constexpr int TREE_TSLOT = 28;  // doubles per condensed joint block (Ŝ_u packed + r̂_u), the tree exchange unit
 constexpr int TREE_MAXN = 24;  // max dual rows of the child joints of one body (frontal size ≤ 24 + 6)
 struct TreePlan {
   std::vector<int32_t> up_joint;     // [n] joint to the parent (−1 for a root)
@@ -154,6 +155,7 @@ struct Plan {
   };
   int32_t n_parts = 1, part_lo = 0, part_hi = 1;
   bool use_nccl = false;
+  bool host_exchange = false;    // options.host_exchange: the caller all-gathers between mabd_step_exchange_begin/end
   std::vector<Part> parts;
   std::vector<int32_t> local_windows, local_long, part_left_open;
   // loop breakers (Case III) around the chain or tree solver
@@ -226,7 +228,7 @@ cudaError_t reset_err(const DevPtrs& d, cudaStream_t st);
 cudaError_t launch_step_end(const DevPtrs& d, cudaStream_t st);
 cudaError_t loop_step(const Plan& p, const DevPtrs& d, const StepConsts& k, cudaStream_t st,
                       cudaError_t (*forest_step)(const Plan&, const DevPtrs&, const StepConsts&, cudaStream_t));
-cudaError_t launch_step(const Plan& p, const DevPtrs& d, double h, int32_t step, cudaStream_t st);
+cudaError_t launch_step(const Plan& p, const DevPtrs& d, double h, int32_t step, cudaStream_t st, int phase = 0);
 
 // tree solver (mabd_tree.cu)
 bool tree_build(const mabd_joints* joints, int64_t n, Plan* p, std::vector<int64_t>* pos_of_body, std::string* msg);

@@ -44,7 +44,7 @@ __device__ __forceinline__ bool nn_ext(int nn) { return (nn >> 16) & 1; }
 // joint (Ŝ_u lower triangle in tri6 order, then r̂_u); downward, λ_u. A body whose parent lies outside the group
 // (ext) also publishes its slot to global memory (Shat: [joint][TSLOT], same layout) and reads λ_u from lam.
 // s == nullptr: no slots (the per-level launches of a large top group: everything through global memory).
-constexpr int TSLOT = 28;
+constexpr int TSLOT = TREE_TSLOT;
 __device__ __forceinline__ int tri6(int r, int c) { return r >= c ? r * (r + 1) / 2 + c : c * (c + 1) / 2 + r; }
 struct TSlots {
   double* s;
@@ -696,16 +696,17 @@ cudaError_t tree_step(const Plan& p, const DevPtrs& d, const StepConsts& k, cuda
   const int g_lo = split ? std::min(t.n_bottom, t.part * t.gpr) : 0;
   const int g_hi = split ? std::min(t.n_bottom, (t.part + 1) * t.gpr) : t.n_bottom;
   const bool top_section = t.n_mid > 0 || t.has_top;
-  if (!top_section) return launch_group<TREE_BOTH>(a, g_lo, g_hi, t, st);
-  if ((e = launch_group<TREE_UP>(a, g_lo, g_hi, t, st, true))) return e;
+  if (!top_section) return k.phase == 2 ? cudaSuccess : launch_group<TREE_BOTH>(a, g_lo, g_hi, t, st);
+  if (k.phase != 2 && (e = launch_group<TREE_UP>(a, g_lo, g_hi, t, st, true))) return e;
   if (t.parts > 1) {  // exchange of the group roots' condensed blocks (one all-gather; emulated: every part local)
     const int q0 = split ? t.part : 0, q1 = split ? t.part + 1 : t.parts;
-    for (int q = q0; q < q1; ++q) {
+    for (int q = q0; q < q1 && k.phase != 2; ++q) {
       const int lo = std::min(t.n_bottom, q * t.gpr), hi = std::min(t.n_bottom, (q + 1) * t.gpr);
       const int r0 = t.root_off[lo], r1 = t.root_off[hi];
       if (r1 > r0) tree_pack_kernel<<<(unsigned)(((r1 - r0) * TSLOT + 255) / 256), 256, 0, st>>>(a, r0, r1);
     }
-    if (split && t.rpp > 0) {
+    if (k.phase == 1) return cudaGetLastError();  // host exchange: the caller all-gathers xbuf now
+    if (split && t.rpp > 0 && p.use_nccl) {
       const int rc = nccl_allgather_doubles(d.nccl_comm, a.xbuf, (size_t)t.rpp * TSLOT, t.part, st);
       if (rc != 0) return nccl_step_failed(rc), cudaErrorUnknown;  // mabd_step reports MABD_ENCCL
     }
