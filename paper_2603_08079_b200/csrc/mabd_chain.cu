@@ -854,6 +854,188 @@ __global__ void __launch_bounds__(CT, MABD_CHAIN_CTAS) chain_kernel(ChainArgs a)
     asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(*tmem_slot), "n"(TMEM_COLS));
 }
 
+// ------------------------------------------------------------------ a small scene: one warp, block Thomas
+// A scene whose chains fit the first 32 slots of one window (config 1: 8 bodies, 9 joints) is latency-bound in the
+// 256-slot segment kernel (TMA staging, 8 CR levels and their barriers for 9 equations). Here one warp does it:
+// lane t owns slot t (the body there and the joint to its left); the equations are assembled as in chain_kernel's
+// phase 1 and solved by block Thomas over the real equations by lane 0; then phase 3 per lane.
+__global__ void __launch_bounds__(32) small_chain_kernel(ChainArgs a) {
+  __shared__ double sD[SMALL_SLOTS + 1][9], sB[SMALL_SLOTS + 1][9], sr[SMALL_SLOTS + 1][3], sx[SMALL_SLOTS + 1][9];
+  const int t = threadIdx.x;
+  const StepConsts& k = a.k;
+  const uint32_t inf = a.slot_info[t], infN = a.slot_info[t + 1];
+  const bool has_body = slot_right(inf) == SIDE_BODY;
+  const bool eq_real = slot_real(inf);
+  const bool right_real = slot_real(infN) && slot_left(infN) == SIDE_BODY;
+  const int mid = a.b.mat_id ? a.b.mat_id[t] : 0;
+  const double msc = a.b.mscale ? a.b.mscale[t] : 1.0;
+  const Material M = a.b.mats[mid];
+  double q[12], qd[12], R[9], dqt[12];
+#pragma unroll
+  for (int c = 0; c < 12; ++c) {
+    q[c] = has_body ? a.b.q[c * a.b.ld + t] : ((c == 0 || c == 4 || c == 8) ? 1.0 : 0.0);
+    qd[c] = has_body ? a.b.qd[c * a.b.ld + t] : 0.0;
+  }
+  HinvBlk H;
+  if (a.hinv_tab)
+    H = a.hinv_tab[mid];
+  else
+    hinv_blocks(M, msc, k.ih2, H);
+  double W[9];
+  const double* Wp = has_body ? load_wrench(a.b, t, W) : nullptr;
+  const bool ok = k.lp ? predict_body<true>(q, qd, M, msc, H, k.ih, k.grav, R, dqt, Wp)
+                       : predict_body<false>(q, qd, M, msc, H, k.ih, k.grav, R, dqt, Wp);
+  if (!ok && has_body) report(k, ERR_NONFINITE);
+  // equation t (own part) and body t's part of equation t+1 (sx)
+  double D[9] = {0, 0, 0, 0, 0, 0, 0, 0, 0}, rr[3] = {0, 0, 0}, Bq[9] = {0, 0, 0, 0, 0, 0, 0, 0, 0};
+  double X[9] = {0, 0, 0, 0, 0, 0, 0, 0, 0};
+  if (!eq_real) D[0] = D[4] = D[8] = 1.0;
+  if (eq_real) {
+    const double* gp = a.geo + 6 * (size_t)slot_geo(inf);
+    if (slot_left(inf) == SIDE_WORLD)
+#pragma unroll
+      for (int e = 0; e < 3; ++e) rr[e] = gp[e];
+    if (slot_right(inf) == SIDE_WORLD)
+#pragma unroll
+      for (int e = 0; e < 3; ++e) rr[e] -= gp[3 + e];
+  }
+  if (has_body) {
+    double qt[12], x[3], P[9], F[9];
+#pragma unroll
+    for (int c = 0; c < 12; ++c) qt[c] = q[c] + dqt[c];
+    if (eq_real) {
+      const double* yR = a.geo + 6 * (size_t)slot_geo(inf) + 3;
+      point_pos(qt, yR, x);
+#pragma unroll
+      for (int e = 0; e < 3; ++e) rr[e] -= x[e];
+      pblock(H, yR, yR, P);
+      rot_conj(R, P, F);
+#pragma unroll
+      for (int e = 0; e < 9; ++e) D[e] += F[e];
+    }
+    if (right_real) {
+      const double* yL = a.geo + 6 * (size_t)slot_geo(infN);
+      point_pos(qt, yL, x);
+#pragma unroll
+      for (int e = 0; e < 3; ++e) X[6 + e] = x[e];
+      pblock(H, yL, yL, P);
+      rot_conj(R, P, F);
+#pragma unroll
+      for (int e = 0; e < 6; ++e) X[e] = 0.0;
+      double Fs[6];
+      sym_from_full(F, Fs);
+#pragma unroll
+      for (int e = 0; e < 6; ++e) X[e] = Fs[e];
+      if (eq_real) {
+        const double* yR = a.geo + 6 * (size_t)slot_geo(inf) + 3;
+        pblock(H, yR, yL, P);
+        rot_conj(R, P, F);
+#pragma unroll
+        for (int e = 0; e < 9; ++e) Bq[e] = -F[e];
+      }
+    }
+  }
+#pragma unroll
+  for (int e = 0; e < 9; ++e) {
+    sD[t][e] = D[e];
+    sB[t][e] = Bq[e];
+    sx[t + 1][e] = X[e];
+  }
+#pragma unroll
+  for (int e = 0; e < 3; ++e) sr[t][e] = rr[e];
+  const unsigned real = __ballot_sync(0xffffffffu, eq_real);
+  __syncwarp();
+  if (t > 0 && eq_real && slot_left(inf) == SIDE_BODY) {  // the left body's part of this equation
+    double Xs[9];
+    full_from_sym(&sx[t][0], Xs);
+#pragma unroll
+    for (int e = 0; e < 9; ++e) sD[t][e] += Xs[e];
+#pragma unroll
+    for (int e = 0; e < 3; ++e) sr[t][e] += sx[t][6 + e];
+  }
+  __syncwarp();
+  const int ne = real ? 32 - __clz((int)real) : 0;  // equations 0 .. ne−1 (beyond: decoupled padding, λ = 0)
+  if (t == 0) {  // block Thomas: D'_0 = D_0, L_k = B_{k−1}ᵀ D'_{k−1}⁻¹, D'_k = D_k − L_k B_{k−1}, y_k = r_k − L_k y_{k−1}
+    double Dpi[9], y[3];
+    for (int kq = 0; kq < ne; ++kq) {
+      double Dk[9], Ds[6], Di[6];
+#pragma unroll
+      for (int e = 0; e < 9; ++e) Dk[e] = sD[kq][e];
+      double yk[3] = {sr[kq][0], sr[kq][1], sr[kq][2]};
+      if (kq > 0) {
+        double Bp[9], L[9], T[9], v[3];
+#pragma unroll
+        for (int e = 0; e < 9; ++e) Bp[e] = sB[kq - 1][e];
+        mat3_mul_at(Bp, Dpi, L);
+        mat3_mul(L, Bp, T);
+        mat3_vec(L, y, v);
+#pragma unroll
+        for (int e = 0; e < 9; ++e) Dk[e] -= T[e];
+#pragma unroll
+        for (int e = 0; e < 3; ++e) yk[e] -= v[e];
+      }
+      Ds[0] = Dk[0]; Ds[1] = 0.5 * (Dk[1] + Dk[3]); Ds[2] = 0.5 * (Dk[2] + Dk[6]);
+      Ds[3] = Dk[4]; Ds[4] = 0.5 * (Dk[5] + Dk[7]); Ds[5] = Dk[8];
+      if (!sym_inv_spd(Ds, Di)) report(k, ERR_SINGULAR);
+      full_from_sym(Di, Dpi);
+#pragma unroll
+      for (int e = 0; e < 9; ++e) sD[kq][e] = Dpi[e];
+#pragma unroll
+      for (int e = 0; e < 3; ++e) sr[kq][e] = y[e] = yk[e];
+    }
+    double lam[3] = {0, 0, 0};
+    for (int kq = ne - 1; kq >= 0; --kq) {  // λ_k = D'_k⁻¹ (y_k − B_k λ_{k+1})
+      double Bk[9], Dk[9], v[3], w[3];
+#pragma unroll
+      for (int e = 0; e < 9; ++e) {
+        Bk[e] = sB[kq][e];
+        Dk[e] = sD[kq][e];
+      }
+      mat3_vec(Bk, lam, w);
+#pragma unroll
+      for (int e = 0; e < 3; ++e) v[e] = sr[kq][e] - (kq + 1 < ne ? w[e] : 0.0);
+      mat3_vec(Dk, v, lam);
+#pragma unroll
+      for (int e = 0; e < 3; ++e) sr[kq][e] = lam[e];
+    }
+  }
+  __syncwarp();
+  if (!has_body) return;
+  // phase 3: qⁿ⁺¹ = q̃ − diag₄(R) H̄⁻¹ Σ ±Γ(ȳ)ᵀ Rᵀλ
+  double gq[12] = {0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0}, w[3], lam[3], u[12];
+  if (eq_real) {
+#pragma unroll
+    for (int e = 0; e < 3; ++e) lam[e] = t < ne ? sr[t][e] : 0.0;
+    mat3t_vec(R, lam, w);
+    add_point_force(gq, a.geo + 6 * (size_t)slot_geo(inf) + 3, w, -1.0);
+  }
+  if (right_real) {
+#pragma unroll
+    for (int e = 0; e < 3; ++e) lam[e] = t + 1 < ne ? sr[t + 1][e] : 0.0;
+    mat3t_vec(R, lam, w);
+    add_point_force(gq, a.geo + 6 * (size_t)slot_geo(infN), w, 1.0);
+  }
+  hinv_apply(H, gq, u);
+  double dq[12];
+#pragma unroll
+  for (int kb = 0; kb < 4; ++kb) {
+    double c3[3];
+    mat3_vec(R, u + 3 * kb, c3);
+#pragma unroll
+    for (int e = 0; e < 3; ++e) dq[3 * kb + e] = dqt[3 * kb + e] - c3[e];
+  }
+#pragma unroll
+  for (int c = 0; c < 12; ++c) {
+    a.b.q[c * a.b.ld + t] = q[c] + dq[c];
+    a.b.qd[c * a.b.ld + t] = k.niter == 1 ? dq[c] * k.ih : qd[c] - dq[c] * k.ih + (c >= 9 ? k.h * k.grav[c - 9] : 0.0);
+  }
+}
+
+cudaError_t launch_small_chain(const ChainArgs& a, cudaStream_t st) {
+  small_chain_kernel<<<1, 32, 0, st>>>(a);
+  return cudaGetLastError();
+}
+
 // ------------------------------------------------------------------ reduced block-tridiagonal levels
 // Unknown u of level L owns the equation built from the level-(L−1) tops:
 //   D_u = top[u].D0 + (left(u) ? top[u−1].D1 : 0),  B_u = top[u].B,  r_u likewise.

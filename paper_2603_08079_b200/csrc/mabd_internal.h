@@ -33,6 +33,7 @@ constexpr int SEG = 256;        // owned slots per segment
 constexpr int CT = 128;         // threads per segment CTA (2 slots per thread)
 constexpr int NEQ = SEG + 1;    // equations per segment CR (the 257th is the next segment's first slot)
 constexpr int LDS = SEG + 2;    // shared-memory row stride of the CR arrays (even: 16-B aligned rows)
+constexpr int SMALL_SLOTS = 32; // a one-window scene using at most this many slots takes the one-warp kernel
 
 // Segment flags
 enum : int32_t { SEG_LEFT_IFACE = 1, SEG_RIGHT_IFACE = 2, SEG_LONG = 4 };

@@ -158,6 +158,7 @@ struct SparseArgs {
 size_t cr_smem_bytes();
 cudaError_t chain_kernels_init();
 cudaError_t launch_chain(const ChainArgs& a, int nblocks, bool finish, cudaStream_t st);
+cudaError_t launch_small_chain(const ChainArgs& a, cudaStream_t st);
 cudaError_t launch_btd(const BtdArgs& a, int nblocks, cudaStream_t st);
 cudaError_t launch_hinv_table(const Material* mats, int nm, double ih2, HinvBlk* out, cudaStream_t st);
 cudaError_t launch_gather(const double* q, const double* qd, int64_t ld, const int64_t* perm, int64_t n,

@@ -466,6 +466,10 @@ static bool chain_build(const mabd_joints* J, int64_t n, Plan* p, std::vector<in
   }
   const int64_t nl = (int64_t)p->levels.size();
   p->launches_per_step = 1 + (p->n_long > 0 ? (int32_t)(2 * nl - 1 + 1) : 0);
+  // one window using at most SMALL_SLOTS slots: the one-warp kernel (latency-bound scenes such as config 1)
+  p->small_chain = p->n_windows == 1 && p->n_long == 0;
+  for (int64_t t = SMALL_SLOTS; t < (int64_t)p->slot_info.size() && p->small_chain; ++t)
+    if (p->slot_info[t] != slot_pack(SIDE_NONE, SIDE_NONE, 0)) p->small_chain = false;
   return true;
 }
 
@@ -1080,6 +1084,7 @@ static cudaError_t forest_iteration(const Plan& p, const DevPtrs& d, const StepC
   a.lam_in = d.lams.empty() ? nullptr : d.lams[0];
   a.k = k;
   if (p.n_parts > 1) return launch_step_parts(p, d, a, st);
+  if (p.small_chain) return launch_small_chain(a, st);
   cudaError_t e = launch_chain(a, (int)p.n_windows, false, st);
   if (e != cudaSuccess || p.n_long == 0) return e;
   const int nl = (int)p.levels.size();

@@ -145,6 +145,7 @@ struct Plan {
   std::vector<double> geo;           // [ng][6]
   std::vector<int32_t> seg_flags, seg_red, long_list, left_iface;
   int64_t n_long = 0;
+  bool small_chain = false;          // one window within SMALL_SLOTS slots: small_chain_kernel
   std::vector<BtdLevel> levels;      // levels[0] is BTD level 1 (single part)
   // multi-part chains (multi-GPU, or W parts emulated in one process): see partition_chain()
   struct Part {
