@@ -411,10 +411,12 @@ def run_ours(args, rank: int, world: int, local_rank: int) -> None:
                          "traffic_source": "profiles/ncu_traffic.json (ncu --set full DRAM bytes per launch of the "
                                            "fused kernel, 1 GPU; not measured by this run)",
                          "kernel": "chain_kernel (fused stages 1-4)" if info["solver"] == "chain" and lps == 2
+                         else "small_chain_kernel (one warp: stages 1-4 and the step bookkeeping)" if lps == 1
                          else f"{info['solver']} solver, step level ({lps} launches per step)",
                          "bytes_per_body_step": bpb, "peak_source": peak_src,
                          "duration": "CUDA-event time per step on the library's stream (" +
                                      ("the fused chain kernel + the 1-thread step_end node)" if lps == 2 else
+                                      "one kernel)" if lps == 1 else
                                       f"{lps} launches: a step-level roofline)")},
             "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": 2 * 96 * n * world,
                     "d2h_bytes_per_step": 2 * 96 * n * world, "steps": ke,

@@ -162,7 +162,7 @@ mabd_status mabd_prefactor(mabd_handle c, double h) {
 
 static cudaError_t enqueue_one_step(mabd_ctx* c, double h, int32_t s) {
   cudaError_t e = launch_step(c->plan, c->d, h, s, c->stream);
-  if (e == cudaSuccess) e = launch_step_end(c->d, c->stream);
+  if (e == cudaSuccess) e = launch_step_end(c->plan, c->d, c->stream);
   return e;
 }
 
@@ -307,7 +307,7 @@ mabd_status mabd_step_exchange_end(mabd_handle c) {
   if (!(c->exchange_h > 0.0)) return fail(c, MABD_ESTATE, "mabd_step_exchange_end without begin");
   CUDA_TRY(c, cudaSetDevice(c->device));
   CUDA_TRY(c, launch_step(c->plan, c->d, c->exchange_h, 0, c->stream, 2));
-  CUDA_TRY(c, launch_step_end(c->d, c->stream));
+  CUDA_TRY(c, launch_step_end(c->plan, c->d, c->stream));
   c->exchange_h = 0.0;
   c->steps_pending += 1;
   return mabd_check(c);
@@ -405,7 +405,8 @@ mabd_status mabd_query(mabd_handle c, int32_t* solver, int32_t* launches_per_ste
                        int64_t* n_dual_rows) {
   if (!c) return fail(nullptr, MABD_EINVAL, "NULL handle");
   if (solver) *solver = c->plan.loop.active ? MABD_SOLVER_LOOP_BREAKER : c->plan.solver;
-  if (launches_per_step) *launches_per_step = c->plan.launches_per_step + 1;  // + the step_end node
+  if (launches_per_step)  // + the step_end node (folded into the one-warp chain kernel when that runs alone)
+    *launches_per_step = c->plan.launches_per_step + (c->plan.step_end_folded ? 0 : 1);
   if (n_bodies) *n_bodies = c->plan.n;
   if (n_dual_rows) *n_dual_rows = c->plan.n_dual_rows;
   return MABD_OK;

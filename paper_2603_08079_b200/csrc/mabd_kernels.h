@@ -18,6 +18,7 @@ struct ChainArgs {
   int32_t n_mats;              // entries of b.mats
   Top* top_out;                // REDUCE output, indexed by seg_red
   const double* lam_in;        // FINISH input: level-2 λ [n_long][3]
+  int32_t step_end;            // small_chain_kernel: also do the step_end node's bookkeeping (Plan::step_end_folded)
   StepConsts k;
 };
 

@@ -602,6 +602,7 @@ mabd_status build_plan(const mabd_bodies* B, const mabd_joints* J, const mabd_op
     *msg = "topology not supported by this build (" + why + ")";
     return MABD_EUNSUPPORTED;
   }
+  p->step_end_folded = p->small_chain && p->newton_iters == 1 && !p->loop.active && p->n_parts <= 1;
   if (p->loop.active) {  // breaker points → internal positions; 2 + 3b forest runs + 2 kernels each, + solve, force
     for (auto* v : {&p->loop.pa, &p->loop.pb})
       for (int32_t& b : *v) b = (int32_t)pos[b];
@@ -923,7 +924,8 @@ __global__ void step_end_kernel(int32_t* e) {
   e[3] += 1;
 }
 
-cudaError_t launch_step_end(const DevPtrs& d, cudaStream_t st) {
+cudaError_t launch_step_end(const Plan& p, const DevPtrs& d, cudaStream_t st) {
+  if (p.step_end_folded) return cudaSuccess;  // done by the step's only kernel
   step_end_kernel<<<1, 1, 0, st>>>(d.err);
   return cudaGetLastError();
 }
@@ -1072,6 +1074,7 @@ static cudaError_t forest_iteration(const Plan& p, const DevPtrs& d, const StepC
   if (p.solver == MABD_SOLVER_LINE_GS) return gs_step(p, d, k, st);
   if (p.solver != MABD_SOLVER_CHAIN) return cudaErrorNotSupported;
   ChainArgs a;
+  a.step_end = 0;
   a.b = d.b;
   a.slot_info = d.slot_info;
   a.geo = d.geo;
@@ -1084,7 +1087,10 @@ static cudaError_t forest_iteration(const Plan& p, const DevPtrs& d, const StepC
   a.lam_in = d.lams.empty() ? nullptr : d.lams[0];
   a.k = k;
   if (p.n_parts > 1) return launch_step_parts(p, d, a, st);
-  if (p.small_chain) return launch_small_chain(a, st);
+  if (p.small_chain) {
+    a.step_end = p.step_end_folded ? 1 : 0;
+    return launch_small_chain(a, st);
+  }
   cudaError_t e = launch_chain(a, (int)p.n_windows, false, st);
   if (e != cudaSuccess || p.n_long == 0) return e;
   const int nl = (int)p.levels.size();

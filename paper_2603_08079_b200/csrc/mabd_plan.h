@@ -146,6 +146,7 @@ struct Plan {
   std::vector<int32_t> seg_flags, seg_red, long_list, left_iface;
   int64_t n_long = 0;
   bool small_chain = false;          // one window within SMALL_SLOTS slots: small_chain_kernel
+  bool step_end_folded = false;      // small_chain_kernel does the step_end bookkeeping (one kernel per step)
   std::vector<BtdLevel> levels;      // levels[0] is BTD level 1 (single part)
   // multi-part chains (multi-GPU, or W parts emulated in one process): see partition_chain()
   struct Part {
@@ -226,7 +227,7 @@ mabd_status build_plan(const mabd_bodies* bodies, const mabd_joints* joints, con
 cudaError_t upload_plan(const Plan& p, char* ws, cudaStream_t st, DevPtrs* d);
 cudaError_t prefactor_device(const Plan& p, const DevPtrs& d, double h, cudaStream_t st);
 cudaError_t reset_err(const DevPtrs& d, cudaStream_t st);
-cudaError_t launch_step_end(const DevPtrs& d, cudaStream_t st);
+cudaError_t launch_step_end(const Plan& p, const DevPtrs& d, cudaStream_t st);
 cudaError_t loop_step(const Plan& p, const DevPtrs& d, const StepConsts& k, cudaStream_t st,
                       cudaError_t (*forest_step)(const Plan&, const DevPtrs&, const StepConsts&, cudaStream_t));
 cudaError_t launch_step(const Plan& p, const DevPtrs& d, double h, int32_t step, cudaStream_t st, int phase = 0);
