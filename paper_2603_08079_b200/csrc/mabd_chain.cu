@@ -873,10 +873,16 @@ __global__ void __launch_bounds__(32) small_chain_kernel(ChainArgs a) {
   const Material M = a.b.mats[mid];
   double q[12], qd[12], R[9], dqt[12];
 #pragma unroll
-  for (int c = 0; c < 12; ++c) {
-    q[c] = has_body ? a.b.q[c * a.b.ld + t] : ((c == 0 || c == 4 || c == 8) ? 1.0 : 0.0);
-    qd[c] = has_body ? a.b.qd[c * a.b.ld + t] : 0.0;
+  for (int c = 0; c < 12; ++c) {  // unconditional loads (slot t < 32 ≤ ld), issued with the slot codes' loads
+    q[c] = a.b.q[c * a.b.ld + t];
+    qd[c] = a.b.qd[c * a.b.ld + t];
   }
+  if (!has_body)
+#pragma unroll
+    for (int c = 0; c < 12; ++c) {
+      q[c] = (c == 0 || c == 4 || c == 8) ? 1.0 : 0.0;
+      qd[c] = 0.0;
+    }
   HinvBlk H;
   if (a.hinv_tab)
     H = a.hinv_tab[mid];
