@@ -92,6 +92,12 @@ typedef struct {
                                 the axis (the axis in body_a's frame is ȳ_a[1] − ȳ_a[0]); the first point is a
                                 ball, the second keeps only its two rows normal to the axis in the hinge frame
                                 R_H = ΔR_H Rᵀ(A_a), re-evaluated every Newton iteration. Sparse solver only.   */
+  const double *limits;      /* [K][8] or NULL: joint limits of five-row hinges (R14): lo, hi
+                                (rad; ±inf = none), u_a (3, ⟂ the axis, body a's frame), u_b (3, body b's frame,
+                                or world for an anchor) with u_a, u_b equal in the world at creation, so the hinge
+                                angle θ = atan2(a_w·(u_aw × u_bw), u_aw·u_bw) is 0 there. A limit violated at a
+                                Newton iteration's linearisation point holds θ at the bound for that iteration
+                                (one extra row; its residual is the dual-space penalty). Ignored for kind 0.      */
 } mabd_joints;
 
 typedef struct {

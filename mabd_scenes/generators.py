@@ -70,6 +70,7 @@ class Scene:
     meta: dict = field(default_factory=dict)
     wrench: Optional[np.ndarray] = None     # [n,6] external wrench (τ, f), world frame, constant; None = none
     kind: Optional[np.ndarray] = None       # [K] int32 joint kind: 0 point joint (default), 1 five-row hinge
+    limits: Optional[np.ndarray] = None     # [K,8] five-row hinge limits: lo, hi (rad), u_a (3), u_b (3)
 
     @property
     def n(self) -> int:
@@ -718,3 +719,36 @@ def hinge_pendulum(axis=(1.0, 0.0, 0.0), omega0=(0.0, 0.0, 0.0), length: float =
                    np.array([0], np.int32), np.array([-1], np.int32), np.array([2], np.int32), pts, h, 1,
                    meta={"topology": "tree"})
     return sc
+
+
+def hinge_limits(sc: Scene, lo: float, hi: float) -> Scene:
+    """Limits [lo, hi] (rad, from the creation configuration) on every five-row hinge (input construction): the
+    reference directions are a unit vector ⟂ the axis in body a's frame and the same world direction expressed in
+    body b's frame (the world frame for an anchor), so the hinge angle is 0 at creation."""
+    out = sc.copy()
+    K = sc.n_joints
+    L = np.full((K, 8), np.nan)
+    off = np.concatenate([[0], np.cumsum(sc.npts)])
+    for k in range(K):
+        if sc.kind is None or sc.kind[k] != 1:
+            continue
+        p0 = off[k]
+        ax = sc.ybar_a[p0 + 1] - sc.ybar_a[p0]
+        ax = ax / np.linalg.norm(ax)
+        e = np.eye(3)[np.argmin(np.abs(ax))]
+        ua = np.cross(ax, e)
+        ua /= np.linalg.norm(ua)
+        a, b = sc.body_a[k], sc.body_b[k]
+        Aa = np.swapaxes(sc.q0[a, :9].reshape(3, 3), 0, 1)
+        Ua, _, Vta = np.linalg.svd(Aa)
+        uw = (Ua @ Vta) @ ua
+        if b >= 0:
+            Ab = np.swapaxes(sc.q0[b, :9].reshape(3, 3), 0, 1)
+            Ub, _, Vtb = np.linalg.svd(Ab)
+            ub = (Ub @ Vtb).T @ uw
+        else:
+            ub = uw
+        L[k] = [lo, hi, *ua, *ub]
+    out.limits = L
+    out.name = sc.name + f"_lim{lo:g}_{hi:g}"
+    return out

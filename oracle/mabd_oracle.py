@@ -37,7 +37,8 @@ import scipy.sparse.linalg as spla
 __all__ = [
     "lame", "unpack_mbar", "mass_A", "kbar_A", "hbar_A", "polar", "elastic_force_A", "stvk_force_A",
     "length_preserving", "affine_force",
-    "body_hessians", "hinge_frame", "hinge5_rows", "constraint_system", "constraint_residual", "predict", "step", "simulate", "nonlinear_residual",
+    "body_hessians", "hinge_frame", "hinge5_rows", "rotation_about", "hinge_angle", "hinge_limit_rows",
+    "constraint_system", "constraint_residual", "predict", "step", "simulate", "nonlinear_residual",
     "wrench_force", "twist_velocity", "angular_velocity",
     "block_thomas", "leaf_to_root_solve", "dual_matrix", "line_gauss_seidel", "step_with_dual", "rel_err", "T9",
     "vec", "unvec",
@@ -271,6 +272,64 @@ def hinge5_rows(scene, q):
     return out
 
 
+def rotation_about(axis, angle) -> np.ndarray:
+    """Rodrigues rotation by `angle` about the unit `axis`."""
+    a = np.asarray(axis, dtype=np.float64)
+    a = a / np.linalg.norm(a)
+    K = np.array([[0, -a[2], a[1]], [a[2], 0, -a[0]], [-a[1], a[0], 0]])
+    return np.eye(3) + np.sin(angle) * K + (1.0 - np.cos(angle)) * K @ K
+
+
+def hinge_angle(scene, q, k):
+    """The five-row hinge k's angle at q (R14): the rotation of body b's reference
+    direction u_b relative to body a's u_a about the world axis a_w = R_a â (R = polar(A); â = ȳ_a[1] − ȳ_a[0]),
+    atan2(a_w·(u_aw × u_bw), u_aw·u_bw); u_a, u_b are scene.limits[k, 2:5], [5:8] (body frames; world for an
+    anchor), equal in the world at creation, so θ = 0 there."""
+    q = np.asarray(q)
+    off = np.concatenate([[0], np.cumsum(scene.npts)])
+    p0 = off[k]
+    a, b = scene.body_a[k], scene.body_b[k]
+    Ra = polar(unvec(q[a, :9]))
+    ax = scene.ybar_a[p0 + 1] - scene.ybar_a[p0]
+    aw = Ra @ (ax / np.linalg.norm(ax))
+    ua = Ra @ scene.limits[k, 2:5]
+    ub = (polar(unvec(q[b, :9])) @ scene.limits[k, 5:8]) if b >= 0 else scene.limits[k, 5:8]
+    return float(np.arctan2(aw @ np.cross(ua, ub), ua @ ub))
+
+
+def hinge_limit_rows(scene, q):
+    """Joint limits of the five-row hinges (R14). A limit [lo, hi] violated at
+    the linearisation point q (θ > hi or θ < lo) becomes, for this Newton iteration, the equality θ = θ̂ (the violated
+    bound): one row t·(x_a(ȳ₃ₐ) − x_b(ȳ₃ᵦ)) = 0 between body a's point ȳ₃ₐ = ȳ_a[0] + ρ Rot(â, θ̂) u_a and body b's
+    ȳ₃ᵦ = ȳ_b[0] + ρ u_b (ρ = |ȳ_a[1] − ȳ_a[0]|), t = a_w × (R_a Rot(â, θ̂) u_a) the tangent, frozen at q. Its residual
+    at q, ≈ ρ sin(θ − θ̂), enters the dual r.h.s. as the footnote term: the "dual-space penalty k(θ − θ̂)"
+    of P:455 with unit gain. Returns [(a, b, ȳ₃ₐ, ȳ₃ᵦ, t)] for the active limits."""
+    if getattr(scene, "limits", None) is None or getattr(scene, "kind", None) is None:
+        return []
+    q = np.asarray(q)
+    off = np.concatenate([[0], np.cumsum(scene.npts)])
+    out = []
+    for k in np.nonzero(np.asarray(scene.kind) == 1)[0]:
+        lo, hi = scene.limits[k, 0], scene.limits[k, 1]
+        if not (np.isfinite(lo) or np.isfinite(hi)):
+            continue
+        th = hinge_angle(scene, q, k)
+        if lo <= th <= hi:
+            continue
+        thh = hi if th > hi else lo
+        p0 = off[k]
+        a, b = scene.body_a[k], scene.body_b[k]
+        ax = scene.ybar_a[p0 + 1] - scene.ybar_a[p0]
+        rho = np.linalg.norm(ax)
+        ua_hat = rotation_about(ax, thh) @ scene.limits[k, 2:5]
+        ya = scene.ybar_a[p0] + rho * ua_hat
+        yb = scene.ybar_b[p0] + rho * scene.limits[k, 5:8]
+        Ra = polar(unvec(q[a, :9]))
+        t = np.cross(Ra @ (ax / rho), Ra @ ua_hat)
+        out.append((a, b, ya, yb, t / np.linalg.norm(t)))
+    return out
+
+
 def constraint_system(scene, q=None):
     """Jacobian ∇C̃ (sparse) of the joint constraints and the world offsets, at the state q.
 
@@ -312,6 +371,25 @@ def constraint_system(scene, q=None):
         T = sp.block_diag(blocks, format="csr")
         J = (T @ J).tocsr()
         world = T @ world
+    lim = hinge_limit_rows(scene, q) if q is not None else []
+    if lim:  # active joint limits: one row each, appended (R14)
+        rows, cols, vals, wext = [], [], [], []
+        for i, (a, b, ya, yb, t) in enumerate(lim):
+            wv = 0.0
+            for body, y, sgn in ((a, ya, 1.0), (b, yb, -1.0)):
+                if body < 0:
+                    wv = t @ y           # world point of an anchor hinge
+                    continue
+                yaug = np.append(y, 1.0)
+                for c in range(4):
+                    for r in range(3):
+                        rows.append(i)
+                        cols.append(12 * body + 3 * c + r)
+                        vals.append(sgn * yaug[c] * t[r])
+            wext.append(wv)
+        Jl = sp.csr_matrix((vals, (rows, cols)), shape=(len(lim), 12 * n))
+        J = sp.vstack([J, Jl], format="csr")
+        world = np.concatenate([world, wext])
     return J, world
 
 

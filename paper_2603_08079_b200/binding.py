@@ -43,7 +43,7 @@ class _Bodies(ctypes.Structure):
 
 class _Joints(ctypes.Structure):
     _fields_ = [("n_joints", ctypes.c_int64), ("body_a", _ip), ("body_b", _ip), ("npts", _ip),
-                ("ybar_a", _dp), ("ybar_b", _dp), ("kind", _ip)]
+                ("ybar_a", _dp), ("ybar_b", _dp), ("kind", _ip), ("limits", _dp)]
 
 
 class _Options(ctypes.Structure):
@@ -181,7 +181,7 @@ class Simulator:
     """
 
     def __init__(self, q0, qd0, mbar, volume, youngs, poisson, gravity, body_a, body_b, npts, ybar_a, ybar_b,
-                 kind=None,
+                 kind=None, limits=None,
                  solver: int = 0, device: Optional[int] = None, stream=None, world: int = 1, rank: int = 0,
                  nccl_id: Optional[bytes] = None, newton_iters: int = 1, no_graphs: bool = False,
                  rotation: str = "polar", gs_sweeps: int = 0, gs_tol: float = 0.0, host_exchange: bool = False):
@@ -199,13 +199,14 @@ class Simulator:
             q0=_f64(q0, (n, 12)), qd0=_f64(qd0, (n, 12)), mbar=_f64(mbar, (n, 10)), volume=_f64(volume, (n,)),
             youngs=_f64(youngs, (n,)), poisson=_f64(poisson, (n,)), body_a=_i32(body_a, (K,)),
             body_b=_i32(body_b, (K,)), npts=_i32(npts, (K,)), ybar_a=_f64(ybar_a, (P, 3)), ybar_b=_f64(ybar_b, (P, 3)),
-            kind=None if kind is None else _i32(kind, (K,)))
+            kind=None if kind is None else _i32(kind, (K,)),
+            limits=None if limits is None else _f64(limits, (K, 8)))
         k = self._keep
         self._bodies = _Bodies(n, _ptr(k["q0"]), _ptr(k["qd0"]), _ptr(k["mbar"]), _ptr(k["volume"]),
                                _ptr(k["youngs"]), _ptr(k["poisson"]), None,
                                (ctypes.c_double * 3)(*[float(x) for x in np.asarray(gravity).reshape(3)]))
         self._joints = _Joints(K, _ptr(k["body_a"], _ip), _ptr(k["body_b"], _ip), _ptr(k["npts"], _ip),
-                               _ptr(k["ybar_a"]), _ptr(k["ybar_b"]), _ptr(k["kind"], _ip))
+                               _ptr(k["ybar_a"]), _ptr(k["ybar_b"]), _ptr(k["kind"], _ip), _ptr(k["limits"]))
         with torch.cuda.device(self.device):
             self._stream = stream if stream is not None else torch.cuda.current_stream(self.device)
             if self._stream.cuda_stream == 0:  # the legacy default stream cannot be captured into a graph
@@ -232,7 +233,7 @@ class Simulator:
     def from_scene(cls, scene, **kw) -> "Simulator":
         return cls(scene.q0, scene.qd0, scene.mbar, scene.volume, scene.youngs, scene.poisson, scene.gravity,
                    scene.body_a, scene.body_b, scene.npts, scene.ybar_a, scene.ybar_b,
-                   kind=getattr(scene, "kind", None), **kw)
+                   kind=getattr(scene, "kind", None), limits=getattr(scene, "limits", None), **kw)
 
     # ------------------------------------------------------------------ calls
     def _check(self, st: int, h) -> None:

@@ -130,6 +130,9 @@ struct GsArgs {
   double tol;                  // stop when max|residual| ≤ tol · max|r|
 };
 
+// a projected slot's limit record (plim): [0] lo, [1] hi, [2..4] u_a, [5..7] u_b, [8..10] ȳ_a0 (pivot on body a),
+// [11..13] â (unit axis, body a), [14] ρ (> 0 marks a limit slot; 0: the hinge rows of a five-row hinge)
+constexpr int LIM_DOUBLES = 15;
 struct SparseArgs {
   BodyArrays b;
   const HinvBlk* hinv_tab;     // per material, or null (per-body mass scale)
@@ -141,9 +144,12 @@ struct SparseArgs {
   // [w0; w1; dummy] with w_i = R_a ΔR_H[row i]ᵀ (i = x̃, z̃) re-evaluated every step, the dummy row decoupled
   // (S = 1, r = 0, λ = 0) so the 3×3 block structure stays
   const int32_t* pslot;        // [np] slot of a projected point, or −1 (null: no projected points)
-  const double* pdr;           // [nproj][6] ΔR_H rows x and z (body a's canonical frame)
+  const double* pdr;           // [nproj][6] ΔR_H rows x and z (body a's canonical frame); limits: unused
   double* pw;                  // [nproj][6] w0, w1 of this step
+  int32_t* pnr;                // [nproj] rows in use this step (2: hinge rows; limits: 1 active, 0 inactive);
+                               // the rows beyond are decoupled dummies (S = 1, r = 0, λ = 0)
   const int32_t* pplist;       // [nproj] the projected points
+  const double* plim;          // [nproj][LIM_DOUBLES] joint limits (R14), or unused (hinge rows)
   int64_t nproj;
   const int32_t* inc_off;      // [n+1] CSR body → incident points (2·point + side)
   const int32_t* inc;

@@ -95,8 +95,8 @@ struct SparsePlan {
   int32_t refine = 1;                                    // iterative-refinement passes per step
   // five-row hinges: projected points (R13)
   std::vector<int32_t> pslot, pplist;
-  std::vector<double> pdr;
-  size_t o_pslot = 0, o_pdr = 0, o_pw = 0, o_pplist = 0;
+  std::vector<double> pdr, plim;   // plim: LIM_DOUBLES per slot (joint limits, R14)
+  size_t o_pslot = 0, o_pdr = 0, o_pw = 0, o_pplist = 0, o_pnr = 0, o_plim = 0;
   // line Gauss-Seidel (MABD_SOLVER_LINE_GS; gs_build in mabd_sparse.cu)
   std::vector<int32_t> gs_chain_pts, gs_chain_off, gs_color_off;
   int32_t gs_ncolor = 0, gs_sweeps = 0;

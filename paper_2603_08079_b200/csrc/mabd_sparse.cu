@@ -102,19 +102,68 @@ __device__ __forceinline__ void project_cols(const SparseArgs& a, int64_t p, dou
   for (int e = 0; e < 3; ++e) x[e] = w[e] * x0 + w[3 + e] * x1;
 }
 
-// per step: w_i = R_a ΔR_H[i]ᵀ of every projected point (R_a of this step's linearisation point, in rs)
+// per step (Newton iteration), at its linearisation point (R in rs):
+//  hinge rows: w_i = R_a ΔR_H[i]ᵀ of the second axis point (R13);
+//  joint limits (R14): θ = atan2(a_w·(u_aw × u_bw), u_aw·u_bw); inside [lo, hi] the slot is inactive (no rows);
+//  beyond, the violated bound θ̂ gives the row w₀ = t, t = unit(a_w × R_a Rot(â, θ̂) u_a), at body a's point
+//  ȳ₃ₐ = ȳ_a0 + ρ Rot(â, θ̂) u_a (written into py; body b's point ȳ_b0 + ρ u_b is constant).
 __global__ void proj_rows_kernel(SparseArgs a) {
   const int64_t s = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   if (s >= a.nproj) return;
   const int64_t p = a.pplist[s];
   double R[9];
   body_R(a, a.pa[p], R);
+  double* w = a.pw + 6 * s;
+  const double* L = a.plim + (int64_t)LIM_DOUBLES * s;
+  if (!(L[14] > 0.0)) {  // hinge rows (ρ = 0 marks a non-limit slot)
 #pragma unroll
-  for (int i = 0; i < 2; ++i) {
-    const double* d = a.pdr + 6 * s + 3 * i;
+    for (int i = 0; i < 2; ++i) {
+      const double* d = a.pdr + 6 * s + 3 * i;
 #pragma unroll
-    for (int c = 0; c < 3; ++c) a.pw[6 * s + 3 * i + c] = R[3 * c] * d[0] + R[3 * c + 1] * d[1] + R[3 * c + 2] * d[2];
+      for (int c = 0; c < 3; ++c) w[3 * i + c] = R[3 * c] * d[0] + R[3 * c + 1] * d[1] + R[3 * c + 2] * d[2];
+    }
+    a.pnr[s] = 2;
+    return;
   }
+  const double* ax = L + 11;
+  double aw[3], uaw[3], ubw[3];
+  mat3_vec(R, ax, aw);
+  mat3_vec(R, L + 2, uaw);
+  if (a.pb[p] >= 0) {
+    double Rb[9];
+    body_R(a, a.pb[p], Rb);
+    mat3_vec(Rb, L + 5, ubw);
+  } else {
+#pragma unroll
+    for (int e = 0; e < 3; ++e) ubw[e] = L[5 + e];
+  }
+  const double cx = uaw[1] * ubw[2] - uaw[2] * ubw[1], cy = uaw[2] * ubw[0] - uaw[0] * ubw[2],
+               cz = uaw[0] * ubw[1] - uaw[1] * ubw[0];
+  const double th = atan2(aw[0] * cx + aw[1] * cy + aw[2] * cz, uaw[0] * ubw[0] + uaw[1] * ubw[1] + uaw[2] * ubw[2]);
+  const double lo = L[0], hi = L[1];
+#pragma unroll
+  for (int e = 0; e < 6; ++e) w[e] = 0.0;
+  if (th >= lo && th <= hi) {
+    a.pnr[s] = 0;
+    return;
+  }
+  const double thh = th > hi ? hi : lo;
+  // Rot(â, θ̂) u_a = u_a cos θ̂ + (â × u_a) sin θ̂ + â (â·u_a)(1 − cos θ̂), in body a's frame
+  const double* ua = L + 2;
+  const double c = cos(thh), sn = sin(thh), ad = ax[0] * ua[0] + ax[1] * ua[1] + ax[2] * ua[2];
+  const double axu[3] = {ax[1] * ua[2] - ax[2] * ua[1], ax[2] * ua[0] - ax[0] * ua[2], ax[0] * ua[1] - ax[1] * ua[0]};
+  double ur[3], urw[3];
+#pragma unroll
+  for (int e = 0; e < 3; ++e) ur[e] = ua[e] * c + axu[e] * sn + ax[e] * ad * (1.0 - c);
+  double* py = const_cast<double*>(a.py) + 6 * p;  // body a's point of this iteration
+#pragma unroll
+  for (int e = 0; e < 3; ++e) py[e] = L[8 + e] + L[14] * ur[e];
+  mat3_vec(R, ur, urw);
+  double t[3] = {aw[1] * urw[2] - aw[2] * urw[1], aw[2] * urw[0] - aw[0] * urw[2], aw[0] * urw[1] - aw[1] * urw[0]};
+  const double it = rsqrt(t[0] * t[0] + t[1] * t[1] + t[2] * t[2]);
+#pragma unroll
+  for (int e = 0; e < 3; ++e) w[e] = t[e] * it;
+  a.pnr[s] = 1;
 }
 
 // points: r = C(q̃) (q̃ = qⁿ + δq̃)
@@ -193,9 +242,10 @@ __global__ void mv_point_kernel(SparseArgs a) {
         s[e] += sg * (a.vv[(0 + e) * a.n + j] * y[0] + a.vv[(3 + e) * a.n + j] * y[1] +
                       a.vv[(6 + e) * a.n + j] * y[2] + a.vv[(9 + e) * a.n + j]);
     }
-    if (a.pslot && a.pslot[p] >= 0) {  // rows w·(J V), the dummy row's S = 1
+    if (a.pslot && a.pslot[p] >= 0) {  // rows w·(J V); the dummy rows' S = 1 (the refinement's x is λ)
       project_rows(a, p, s);
-      s[2] = a.lam[2 * a.np + p];  // (the refinement's x is λ)
+      const int nr = a.pnr[a.pslot[p]];
+      for (int e = nr; e < 3; ++e) s[e] = a.lam[e * a.np + p];
     }
 #pragma unroll
     for (int e = 0; e < 3; ++e) a.res[e * a.np + p] = a.rhs[e * a.np + p] - s[e];
@@ -276,7 +326,8 @@ __global__ void mf_assemble_kernel(SparseArgs a) {
       if (pjc)
 #pragma unroll
         for (int r = 0; r < 3; ++r) project_rows(a, pcol, S + 3 * r);
-      if (pjr && prow == pcol) S[8] = 1.0;
+      if (pjr && prow == pcol)
+        for (int e = a.pnr[a.pslot[prow]]; e < 3; ++e) S[4 * e] = 1.0;  // dummy rows: S = 1, decoupled
     }
     double* F = m.F + m.foff[node];
     const int64_t f = m.fdim[node];
@@ -1612,13 +1663,16 @@ bool sparse_build(const mabd_bodies* B, const mabd_joints* J, Plan* p, std::vect
     s.inc[s.inc_off[a] + fill[a]++] = (int32_t)(2 * q);
     if (b >= 0) s.inc[s.inc_off[b] + fill[b]++] = (int32_t)(2 * q + 1);
   }
-  // five-row hinges: the second point of each is projected (rows w0, w1 from ΔR_H of the axis in body a's frame)
+  // five-row hinges: the second point of each is projected (rows w0, w1 from ΔR_H of the axis in body a's frame);
+  // a limited one also gets an extra point, the limit row (R14), appended after the joints' points
   s.pslot.clear();
   s.pdr.clear();
   s.pplist.clear();
+  s.plim.clear();
   if (J->kind) {
     s.pslot.assign(P, -1);
     int64_t p0 = 0;
+    std::vector<int64_t> lim_joint;
     for (int64_t k = 0; k < K; ++k) {
       if (J->kind[k] == 1) {
         const double* y0 = J->ybar_a + 3 * p0;
@@ -1632,10 +1686,53 @@ bool sparse_build(const mabd_bodies* B, const mabd_joints* J, Plan* p, std::vect
         s.pplist.push_back((int32_t)(p0 + 1));
         for (int i : {0, 2})
           for (int c = 0; c < 3; ++c) s.pdr.push_back(dR[i][c]);
+        for (int e = 0; e < LIM_DOUBLES; ++e) s.plim.push_back(0.0);
+        const double* L = J->limits ? J->limits + 8 * k : nullptr;
+        if (L && (std::isfinite(L[0]) || std::isfinite(L[1]))) {
+          if (!(L[0] < L[1])) return *msg = "joint limits need lo < hi", false;
+          std::vector<double> rec(LIM_DOUBLES, 0.0);
+          rec[0] = std::isfinite(L[0]) ? L[0] : -1e300;
+          rec[1] = std::isfinite(L[1]) ? L[1] : 1e300;
+          for (int e = 0; e < 6; ++e) rec[2 + e] = L[2 + e];
+          for (int e = 0; e < 3; ++e) {
+            rec[8 + e] = y0[e];
+            rec[11 + e] = ax[e];
+          }
+          rec[14] = nrm;
+          // the limit point: body a's point is written per iteration; body b's is ȳ_b0 + ρ u_b
+          const double* yb0 = J->ybar_b + 3 * p0;
+          s.pa.push_back(J->body_a[k]);
+          s.pb.push_back(J->body_b[k]);
+          for (int e = 0; e < 3; ++e) s.py.push_back(y0[e] + nrm * L[2 + e]);
+          for (int e = 0; e < 3; ++e) s.py.push_back(yb0[e] + nrm * L[5 + e]);
+          s.pslot.push_back((int32_t)s.pplist.size());
+          s.pplist.push_back((int32_t)(s.pa.size() - 1));
+          for (int e = 0; e < 6; ++e) s.pdr.push_back(0.0);
+          s.plim.insert(s.plim.end(), rec.begin(), rec.end());
+          lim_joint.push_back(k);
+        }
       }
       p0 += J->npts[k];
     }
     if (s.pplist.empty()) s.pslot.clear();
+    if (!lim_joint.empty()) {  // the incidence with the limit points
+      const int64_t P2 = (int64_t)s.pa.size();
+      std::vector<int32_t> c2(n + 1, 0);
+      for (int64_t q = 0; q < P2; ++q) {
+        c2[s.pa[q] + 1]++;
+        if (s.pb[q] >= 0) c2[s.pb[q] + 1]++;
+      }
+      s.inc_off.assign(n + 1, 0);
+      for (int64_t i = 0; i < n; ++i) s.inc_off[i + 1] = s.inc_off[i] + c2[i + 1];
+      s.inc.assign(s.inc_off[n], 0);
+      std::vector<int32_t> f2(n, 0);
+      for (int64_t q = 0; q < P2; ++q) {
+        const int64_t a = s.pa[q], b = s.pb[q];
+        s.inc[s.inc_off[a] + f2[a]++] = (int32_t)(2 * q);
+        if (b >= 0) s.inc[s.inc_off[b] + f2[b]++] = (int32_t)(2 * q + 1);
+      }
+      s.np = P2;
+    }
   }
   pos_of_body->resize(n);
   for (int64_t i = 0; i < n; ++i) (*pos_of_body)[i] = i;  // caller order
@@ -1844,6 +1941,8 @@ void sparse_layout(Plan* p, const std::function<size_t(size_t)>& take) {
   s.o_pslot = take(sizeof(int32_t) * nz(s.pslot.size()));
   s.o_pdr = take(sizeof(double) * nz(s.pdr.size()));
   s.o_pw = take(sizeof(double) * nz(s.pdr.size()));
+  s.o_pnr = take(sizeof(int32_t) * nz(s.pplist.size()));
+  s.o_plim = take(sizeof(double) * nz(s.plim.size()));
   s.o_pplist = take(sizeof(int32_t) * nz(s.pplist.size()));
   s.o_gs_pts = take(sizeof(int32_t) * nz(s.gs_chain_pts.size()));
   s.o_gs_off = take(sizeof(int32_t) * nz(s.gs_chain_off.size()));
@@ -1906,6 +2005,8 @@ cudaError_t sparse_upload(const Plan& p, char* ws, cudaStream_t st, DevPtrs* d) 
   A.pdr = (const double*)(ws + s.o_pdr);
   A.pw = (double*)(ws + s.o_pw);
   A.pplist = (const int32_t*)(ws + s.o_pplist);
+  A.pnr = (int32_t*)(ws + s.o_pnr);
+  A.plim = (const double*)(ws + s.o_plim);
   A.gs.chain_pts = (const int32_t*)(ws + s.o_gs_pts);
   A.gs.chain_off = (const int32_t*)(ws + s.o_gs_off);
   A.gs.color_off = (const int32_t*)(ws + s.o_gs_col);
@@ -1943,6 +2044,7 @@ cudaError_t sparse_upload(const Plan& p, char* ws, cudaStream_t st, DevPtrs* d) 
   if ((e = upv(ws, s.o_pslot, s.pslot, st))) return e;
   if ((e = upv(ws, s.o_pdr, s.pdr, st))) return e;
   if ((e = upv(ws, s.o_pplist, s.pplist, st))) return e;
+  if ((e = upv(ws, s.o_plim, s.plim, st))) return e;
   if ((e = upv(ws, s.o_gs_pts, s.gs_chain_pts, st))) return e;
   if ((e = upv(ws, s.o_gs_off, s.gs_chain_off, st))) return e;
   if ((e = upv(ws, s.o_gs_col, s.gs_color_off, st))) return e;

@@ -720,3 +720,48 @@ def test_hinge5_is_a_hinge():
     # the rod turns about the hinge axis only: its angular velocity is along x
     om = O.angular_velocity(q_5, qd_5)[0]
     assert np.linalg.norm(om) > 0.1 and np.max(np.abs(om[1:])) < 1e-3 * np.linalg.norm(om)
+
+
+# ----------------------------------------------------------------------------- joint limits (NEXT 4, R14)
+
+def test_hinge_angle_is_the_rotation_about_the_axis():
+    """hinge_angle (the rotation of body b relative to body a about the axis): a rod on a world hinge (body a = the
+    rod, b = the world) turned by φ about the axis through the pivot reads θ = −φ."""
+    base = G.hinge_limits(G.five_row_hinges(G.hinge_pendulum(axis=(0.3, 1.0, 0.2))), -1.0, 1.0)
+    ax = base.ybar_b[1] - base.ybar_b[0]
+    for phi in (-0.7, 0.0, 0.25, 1.3):
+        Q = O.rotation_about(ax, phi)
+        A = O.unvec(base.q0[0, :9])
+        t = base.q0[0, 9:]
+        q = base.q0.copy()
+        q[0, :9] = O.vec(Q @ A)
+        q[0, 9:] = Q @ (t - base.ybar_b[0]) + base.ybar_b[0]      # rotated about the pivot (a world point)
+        assert abs(O.hinge_angle(base, q, 0) + phi) < 1e-12
+
+
+def test_hinge_limits_hold_the_angle():
+    """A rod swinging on a world hinge through ±0.25 rad: with limits ±∞ the motion is unchanged; with ±0.1 rad every
+    step that starts beyond a bound lands on it (one linearised row: within 1e-3 rad) and the angle never leaves
+    [−0.1, 0.1] by more than one step's travel."""
+    base = G.five_row_hinges(G.hinge_pendulum(axis=(1, 0, 0), omega0=(6.0, 0, 0)))
+    free, _ = O.simulate(base, 150)
+    inf = G.hinge_limits(base, -np.inf, np.inf)
+    q_inf, _ = O.simulate(inf, 150)
+    assert np.array_equal(q_inf, free)
+    sc = G.hinge_limits(base, -0.1, 0.1)
+    q, qd = sc.q0, sc.qd0
+    th_free, th = [], []
+    qf, qdf = base.q0, base.qd0
+    landed = 0
+    for _ in range(150):
+        before = O.hinge_angle(sc, q, 0)
+        q, qd = O.step(sc, q, qd, sc.h)
+        after = O.hinge_angle(sc, q, 0)
+        if abs(before) > 0.1:
+            assert abs(after - np.sign(before) * 0.1) < 1e-3
+            landed += 1
+        th.append(after)
+        qf, qdf = O.step(base, qf, qdf, base.h)
+        th_free.append(O.hinge_angle(sc, qf, 0))
+    assert max(np.abs(th_free)) > 0.24 and landed >= 2
+    assert max(np.abs(th)) < 0.1 + 6.0 * sc.h
