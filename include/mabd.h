@@ -144,7 +144,12 @@ enum { MABD_SOLVER_CHAIN = 1, MABD_SOLVER_TREE = 2, MABD_SOLVER_SPARSE = 3, MABD
 mabd_status mabd_workspace_size(const mabd_bodies *bodies, const mabd_joints *joints,
                                 const mabd_options *opts, size_t *bytes);
 
-/* Validate, classify the topology, order bodies/joints, copy to the device. */
+/* The problem statement of P:459-475 (Eq. kkt): M affine bodies (mass M_A = M̄ ⊗ I₃; elastic
+ * weight V with E, ν) and K joints. Validates (MABD_EINVAL on bad sizes, indices, non-SPD M̄,
+ * a joint on one body, npts ∉ {1, 2}, bad kind / limits / options), maps every body to its canonical frame
+ * (R8), classifies the joint topology (forest of ball-joint paths → chain, forest → tree, cycles → sparse;
+ * SURVEY A14) or takes options.solver, orders bodies and joints for that solver, and copies everything into the
+ * device workspace. Borrows the arrays for the duration of the call. World > 1 with an NCCL id: collective. */
 mabd_status mabd_create(const mabd_bodies *bodies, const mabd_joints *joints,
                         const mabd_options *opts, mabd_handle *out);
 
@@ -152,8 +157,12 @@ mabd_status mabd_create(const mabd_bodies *bodies, const mabd_joints *joints,
  * mabd_step with another h re-prefactors transparently. */
 mabd_status mabd_prefactor(mabd_handle h_, double h);
 
-/* Advance nsteps ≥ 0 implicit steps of size h on the handle's stream. Asynchronous apart from the
- * final error-word check described above. */
+/* Advance nsteps ≥ 0 implicit steps of size h on the handle's stream: per step, options.newton_iters Newton
+ * iterations of the linearised KKT (footnote P:459), each the four stages of the hot path — per-body
+ * co-rotated r.h.s., back-substitution through H̄ (Alg. 1), the dual
+ * solve S λ = C(q̃), S = ∇C̃ H̃⁻¹ ∇C̃ᵀ, the primal update —
+ * then q̇ⁿ⁺¹ = (qⁿ⁺¹ − qⁿ)/h. Asynchronous apart from the final error-word check described above (ESINGULAR,
+ * ENONFINITE name the first failing step; ECUDA / ENCCL for launch or exchange failures). */
 mabd_status mabd_step(mabd_handle h_, double h, int64_t nsteps);
 
 /* Enqueue nsteps steps on the handle's stream and return without synchronising (a serving loop, or a timed
@@ -177,8 +186,10 @@ mabd_status mabd_exchange_info(mabd_handle h_, int64_t *doubles_per_rank, int32_
 mabd_status mabd_exchange_copy(mabd_handle h_, double *host_all, int32_t to_device);
 mabd_status mabd_step_exchange_end(mabd_handle h_);
 
-/* Copy the current state out, in the caller's body order ([n][12] each; either pointer may be NULL).
- * out_on_device != 0 means the pointers are device memory. Synchronises the handle's stream. */
+/* Copy the current state (q, q̇; P:184 layout) out, in the caller's body order and material frames ([n][12] each;
+ * either pointer may be NULL): the internal SoA, topology order and canonical frames (R8) are undone.
+ * out_on_device != 0 means the pointers are device memory. Synchronises the handle's stream. With world > 1 and
+ * NCCL, every rank's share is broadcast first, so all ranks return the full state. */
 mabd_status mabd_get_state(mabd_handle h_, double *q_out, double *qd_out, int out_on_device);
 
 /* Overwrite the state (checkpoint restore; stage tests). Same layout as mabd_get_state. */
