@@ -765,3 +765,21 @@ def test_hinge_limits_hold_the_angle():
         th_free.append(O.hinge_angle(sc, qf, 0))
     assert max(np.abs(th_free)) > 0.24 and landed >= 2
     assert max(np.abs(th)) < 0.1 + 6.0 * sc.h
+
+
+def test_hinge_frame_and_rotation_about():
+    """hinge_frame(a) is a proper rotation taking the unit axis a onto e_y (P:397-399; also at a = ±e_y);
+    rotation_about matches scipy's rotation-vector map."""
+    from scipy.spatial.transform import Rotation
+    rng = np.random.default_rng(51)
+    axes = list(rng.standard_normal((8, 3))) + [np.array([0, 1.0, 0]), np.array([0, -1.0, 0]),
+                                                 np.array([1e-9, -1.0, 0])]
+    for a in axes:
+        R = O.hinge_frame(a)
+        assert np.allclose(R @ (a / np.linalg.norm(a)), [0, 1, 0], atol=1e-8)
+        assert np.allclose(R.T @ R, np.eye(3), atol=1e-12) and abs(np.linalg.det(R) - 1) < 1e-12
+    for _ in range(5):
+        ax = rng.standard_normal(3)
+        ang = rng.uniform(-3, 3)
+        ref = Rotation.from_rotvec(ang * ax / np.linalg.norm(ax)).as_matrix()
+        assert np.allclose(O.rotation_about(ax, ang), ref, atol=1e-13)
