@@ -40,7 +40,8 @@ __all__ = [
     "body_hessians", "hinge_frame", "hinge5_rows", "rotation_about", "hinge_angle", "hinge_limit_rows",
     "constraint_system", "constraint_residual", "predict", "step", "simulate", "nonlinear_residual",
     "wrench_force", "twist_velocity", "angular_velocity",
-    "block_thomas", "leaf_to_root_solve", "dual_matrix", "line_gauss_seidel", "step_with_dual", "rel_err", "T9",
+    "block_thomas", "leaf_to_root_solve", "dual_matrix", "line_gauss_seidel", "step_with_dual", "twist_embedding",
+    "joint_subspace", "aba_literal_step", "rel_err", "T9",
     "vec", "unvec",
 ]
 
@@ -706,3 +707,128 @@ def step_with_dual(scene, q, qd, h, solve):
     lam = solve(S, r)
     dq = (dq_tilde.reshape(-1) - Hinv @ (Jd.T @ lam)).reshape(scene.n, 12)
     return np.asarray(q) + dq, dq / h
+
+
+# --------------------------------------------------------------------------
+# literal Alg. 2 (ABD-ABA) as printed: an approximate tree variant (R15)
+# --------------------------------------------------------------------------
+
+def twist_embedding(A) -> np.ndarray:
+    """E(A) of Eq. module2-E: q̇ = E(A) V for the spatial twist V = (ω, v), E = [−[q_c]×; I₃]."""
+    A = np.asarray(A, dtype=np.float64)
+    E = np.zeros((12, 6))
+    for c in range(3):
+        qc = A[:, c]
+        E[3 * c:3 * c + 3, :3] = -np.array([[0, -qc[2], qc[1]], [qc[2], 0, -qc[0]], [-qc[1], qc[0], 0]])
+    E[9:, 3:] = np.eye(3)
+    return E
+
+
+def joint_subspace(p, t_child, axis=None) -> np.ndarray:
+    """S^j: the relative twists (ω, v of the child's frame origin t) a joint at the world point p admits —
+    rotations about p: v = ω × (t − p). A ball joint: S = [I₃; −[t − p]×] (m = 3); a linear hinge about the unit
+    world axis a: S = [a; a × (t − p)] (m = 1)."""
+    d = np.asarray(t_child, dtype=np.float64) - np.asarray(p, dtype=np.float64)
+    D = np.array([[0, -d[2], d[1]], [d[2], 0, -d[0]], [-d[1], d[0], 0]])
+    if axis is None:
+        return np.vstack([np.eye(3), -D])
+    a = np.asarray(axis, dtype=np.float64)
+    a = a / np.linalg.norm(a)
+    return np.concatenate([a, np.cross(a, d)])[:, None]
+
+
+def aba_literal_step(scene, q, qd, h):
+    """One step of Alg. 2 (ABD-ABA, P:612-643) as printed, on a tree scene (joint = (parent body_a, child body_b);
+    anchors: body_b = −1). DESIGN.md R15 lists the readings: H_A^j = diag₄(R)H̄diag₄(Rᵀ) and f_A^j the exact path's
+    (with the co-rotated elastic force, A3); upward, per link j (deepest first) S_abd = E(A^j)S^j,
+    U = Ĥ S_abd, D = S_abdᵀU, α = D⁻¹S_abdᵀf̂, ΔH = Ĥ − UD⁻¹Uᵀ, Δf = f̂ − Uα, X = diag₄(R_relᵀ) with
+    R_rel = A^pᵀA^j, Ĥ^p += XᵀΔHX, f̂^p += XᵀΔf (Eqs. module2-*); downward (root first) the local KKT of Eq.
+    module3-kkt with r^j = −∇C^j_p δq^p − C^j(qⁿ) (the footnote residual, A4) over the joint to the parent and the
+    body's anchors. Not the exact KKT step (A12): an approximation, compared against it in the tests."""
+    q = np.asarray(q, dtype=np.float64)
+    qd = np.asarray(qd, dtype=np.float64)
+    n = scene.n
+    R, f, H, _ = predict(scene, q, qd, h)
+    A = unvec(q[:, :9])
+    off = np.concatenate([[0], np.cumsum(scene.npts)])
+    parent = np.full(n, -1)
+    pjoint = np.full(n, -1)
+    anchors = [[] for _ in range(n)]
+    for k in range(scene.n_joints):
+        a, b = scene.body_a[k], scene.body_b[k]
+        if b < 0:
+            anchors[a].append(k)
+        else:
+            if parent[b] >= 0:
+                raise ValueError("not a tree: a body with two parents")
+            parent[b], pjoint[b] = a, k
+    depth = np.zeros(n, int)
+    for j in range(n):
+        d, x = 0, j
+        while parent[x] >= 0:
+            x = parent[x]
+            d += 1
+            if d > n:
+                raise ValueError("cycle")
+        depth[j] = d
+
+    def point_rows(k, body):
+        """The joint's 3·npts rows on `body` (+Γ on side a, −Γ on side b) and the world offsets."""
+        rows = []
+        for i in range(scene.npts[k]):
+            p = off[k] + i
+            side = 0 if scene.body_a[k] == body else 1
+            y = (scene.ybar_a if side == 0 else scene.ybar_b)[p]
+            G = np.hstack([np.kron(y[None, :], np.eye(3)), np.eye(3)])
+            rows.append((1.0 if side == 0 else -1.0) * G)
+        return np.vstack(rows)
+
+    def residual(k):
+        out = []
+        for i in range(scene.npts[k]):
+            p = off[k] + i
+            xa = A[scene.body_a[k]] @ scene.ybar_a[p] + q[scene.body_a[k], 9:]
+            b = scene.body_b[k]
+            xb = scene.ybar_b[p] if b < 0 else A[b] @ scene.ybar_b[p] + q[b, 9:]
+            out.append(xa - xb)
+        return np.concatenate(out)
+
+    Hh = H.copy()
+    fh = f.copy()
+    for j in sorted(range(n), key=lambda j: -depth[j]):
+        p = parent[j]
+        if p < 0:
+            continue
+        k = pjoint[j]
+        x0 = A[j] @ scene.ybar_b[off[k]] + q[j, 9:]
+        axis = None
+        if scene.npts[k] == 2:
+            axis = (A[j] @ scene.ybar_b[off[k] + 1] + q[j, 9:]) - x0
+        Sabd = twist_embedding(A[j]) @ joint_subspace(x0, q[j, 9:], axis)
+        U = Hh[j] @ Sabd
+        D = Sabd.T @ U
+        alpha = np.linalg.solve(D, Sabd.T @ fh[j])
+        dH = Hh[j] - U @ np.linalg.solve(D, U.T)
+        df = fh[j] - U @ alpha
+        Rrel = A[p].T @ A[j]
+        X = np.kron(np.eye(4), Rrel.T)
+        Hh[p] += X.T @ dH @ X
+        fh[p] += X.T @ df
+    dq = np.zeros((n, 12))
+    for j in sorted(range(n), key=lambda j: depth[j]):
+        Cs, rs = [], []
+        if parent[j] >= 0:
+            k = pjoint[j]
+            Cs.append(point_rows(k, j))
+            rs.append(-point_rows(k, parent[j]) @ dq[parent[j]] - residual(k))
+        for k in anchors[j]:
+            Cs.append(point_rows(k, j))
+            rs.append(-residual(k))
+        if not Cs:
+            dq[j] = np.linalg.solve(Hh[j], fh[j])
+            continue
+        C = np.vstack(Cs)
+        m = C.shape[0]
+        K = np.block([[Hh[j], C.T], [C, np.zeros((m, m))]])
+        dq[j] = np.linalg.solve(K, np.concatenate([fh[j], np.concatenate(rs)]))[:12]
+    return q + dq, dq / h

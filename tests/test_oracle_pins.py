@@ -783,3 +783,24 @@ def test_hinge_frame_and_rotation_about():
         ang = rng.uniform(-3, 3)
         ref = Rotation.from_rotvec(ang * ax / np.linalg.norm(ax)).as_matrix()
         assert np.allclose(O.rotation_about(ax, ang), ref, atol=1e-13)
+
+
+def test_literal_alg2_is_an_approximation():
+    """Literal Alg. 2 (ABD-ABA as printed; DESIGN R15): exact for a lone body (Ĥ = H), it closes every joint
+    (its local KKTs carry the footnote residual), E(A) inverts the twist map G(A) on rigid motions (G E = I₆,
+    P:757), but on articulated trees its step departs from the exact KKT step by about the step itself — the rigid
+    transport X = diag₄(R_relᵀ) ignores the lever arm between the frames."""
+    one = G.random_chain(1, seed=4, anchored=False, vel=0.5)
+    assert O.rel_err(O.aba_literal_step(one, one.q0, one.qd0, one.h)[0], O.step(one, one.q0, one.qd0, one.h)[0]) < 1e-13
+    A = G.random_rotations(np.random.default_rng(61), 1)[0]
+    Gm = np.zeros((6, 12))
+    for c in range(3):
+        qc = A[:, c]
+        Gm[:3, 3 * c:3 * c + 3] = 0.5 * np.array([[0, -qc[2], qc[1]], [qc[2], 0, -qc[0]], [-qc[1], qc[0], 0]])
+    Gm[3:, 9:] = np.eye(3)
+    assert np.allclose(Gm @ O.twist_embedding(A), np.eye(6), atol=1e-13)
+    sc = G.random_tree(20, seed=1, hinge_frac=0.5, vel=0.3)
+    q_lit, _ = O.aba_literal_step(sc, sc.q0, sc.qd0, sc.h)
+    q_ex, _ = O.step(sc, sc.q0, sc.qd0, sc.h)
+    assert O.constraint_residual(sc, q_lit) < 1e-12
+    assert O.rel_err(q_lit, q_ex) > 0.1 * np.max(np.abs(q_ex - sc.q0))
