@@ -235,8 +235,9 @@ mabd_status mabd_sparse_plan_stats(const mabd_bodies *bodies, const mabd_joints 
 mabd_status mabd_line_gs_plan(const mabd_bodies *bodies, const mabd_joints *joints, int32_t *chain_pts,
                               int32_t *chain_off, int32_t *color_off, int64_t *counts);
 
-/* Statistics of the last step: the sparse solver's configured iterative-refinement passes of its direct dual
- * solve; the line Gauss-Seidel solver's sweeps run in the last step; 0 for the chain and tree solvers.
+/* Statistics of the last step: the sparse solver's iterative-refinement passes run in the last Newton iteration
+ * (0 or 1: a pass runs only when the factorization's residual max|r − Sλ| exceeds 1e-10 · max|r|; R2);
+ * the line Gauss-Seidel solver's sweeps run in the last step; 0 for the chain and tree solvers.
  * Synchronises the handle's stream. */
 mabd_status mabd_solver_stats(mabd_handle h_, int64_t *last_iterations);
 

@@ -436,6 +436,14 @@ int mabd_dbg_gs_trace(mabd_handle c, double* out, int n) {
   return m;
 }
 
+// developer probe (not in the header): the sparse solver's last max|r − Sλ| / max|r| before a refinement pass
+int mabd_dbg_refine_ratio(mabd_handle c, double* out) {
+  if (!c || c->plan.solver != MABD_SOLVER_SPARSE || !c->d.sparse.rmax) return 0;
+  cudaMemcpyAsync(out, c->d.sparse.rmax + 2, sizeof(double), cudaMemcpyDeviceToHost, c->stream);
+  cudaStreamSynchronize(c->stream);
+  return 1;
+}
+
 mabd_status mabd_nccl_unique_id(void* out, size_t bytes) {
   if (!out || bytes < 128) return fail(nullptr, MABD_EINVAL, "need a 128-byte buffer");
   std::string why;

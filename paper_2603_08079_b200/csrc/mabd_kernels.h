@@ -156,7 +156,10 @@ struct SparseArgs {
   double *rhs, *lam, *res, *dl, *yy;  // component-major [3][np]: r = C(q̃), λ, residual, correction, solve scratch
   double* vv;                  // [12][n]
   double* dqt;                 // [12][n] δq̃ of the step (predict → rhs, update)
-  int32_t* iters;              // refinement passes of the last solve
+  int32_t* iters;              // [0] refinement passes run in the last step, [1] gate of the current pass
+  unsigned long long* rmax;    // [2] max|r − Sλ|, max|r| (bit patterns) for the refinement gate
+  const int32_t* gate;         // non-null in a refinement pass's solve kernels: skip when *gate
+  double refine_tol;
   MfArgs mf;
   GsArgs gs;
   StepConsts k;

@@ -92,7 +92,9 @@ struct SparsePlan {
   std::vector<int32_t> lev_nodes, tasks;
   std::vector<int64_t> loff;                             // [nnode] inverse diagonal blocks of big fronts
   int64_t linv_doubles = 0;
-  int32_t refine = 1;                                    // iterative-refinement passes per step
+  int32_t refine = 1;                                    // iterative-refinement passes per step (at most)
+  bool syrk_dfma = false;                                // trailing updates on DFMA instead of DMMA (A/B knob)
+  double refine_tol = 1e-10;                             // gate: a pass runs if max|r − Sλ| > tol · max|r|
   // five-row hinges: projected points (R13)
   std::vector<int32_t> pslot, pplist;
   std::vector<double> pdr, plim;   // plim: LIM_DOUBLES per slot (joint limits, R14)

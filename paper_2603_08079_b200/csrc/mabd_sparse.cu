@@ -36,7 +36,8 @@ constexpr int SP_THREADS = 256;
 constexpr int MF_NB = 64;          // panel width and tile size of the large-front path
 constexpr int MF_SMALL = 96;       // fronts with f ≤ MF_SMALL are factored in shared memory by one CTA
 constexpr int MF_LEAF_PTS = 12;    // nested dissection stops at regions of ≤ this many points
-constexpr int MF_REFINE = 1;       // iterative-refinement passes per step (default)
+constexpr int MF_REFINE = 1;       // iterative-refinement passes per step (default; each gated, see below)
+constexpr double MF_REFINE_TOL = 1e-10;  // a pass runs only if max|r − Sλ| > this · max|r| (refine_gate_kernel)
 
 __device__ __forceinline__ void sreport(const StepConsts& k, int32_t flag) {
   atomicOr(k.err, flag);
@@ -220,6 +221,8 @@ __device__ __forceinline__ void body_apply(const SparseArgs& a, int64_t j, const
 }
 
 // matrix-free S·x, pass 1 (bodies): V = H⁻¹ Jᵀ x
+__device__ __forceinline__ bool refine_gated(const SparseArgs& a) { return a.gate && *a.gate; }
+
 __global__ void mv_body_kernel(SparseArgs a, const double* x) {
   for (int64_t j = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; j < a.n; j += (int64_t)gridDim.x * blockDim.x) {
     double v[12];
@@ -230,6 +233,7 @@ __global__ void mv_body_kernel(SparseArgs a, const double* x) {
 }
 // pass 2 (points): res = rhs − J V
 __global__ void mv_point_kernel(SparseArgs a) {
+  double mres = 0.0, mrhs = 0.0;
   for (int64_t p = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; p < a.np; p += (int64_t)gridDim.x * blockDim.x) {
     double s[3] = {0, 0, 0};
     for (int side = 0; side < 2; ++side) {
@@ -248,10 +252,36 @@ __global__ void mv_point_kernel(SparseArgs a) {
       for (int e = nr; e < 3; ++e) s[e] = a.lam[e * a.np + p];
     }
 #pragma unroll
-    for (int e = 0; e < 3; ++e) a.res[e * a.np + p] = a.rhs[e * a.np + p] - s[e];
+    for (int e = 0; e < 3; ++e) {
+      const double r = a.rhs[e * a.np + p];
+      a.res[e * a.np + p] = r - s[e];
+      mres = fmax(mres, fabs(r - s[e]));
+      mrhs = fmax(mrhs, fabs(r));
+    }
+  }
+  // max |res| and max |rhs| for the refinement gate (non-negative doubles order like their bit patterns)
+  for (int o = 16; o > 0; o >>= 1) {
+    mres = fmax(mres, __shfl_xor_sync(0xffffffffu, mres, o));
+    mrhs = fmax(mrhs, __shfl_xor_sync(0xffffffffu, mrhs, o));
+  }
+  if ((threadIdx.x & 31) == 0) {
+    atomicMax(a.rmax, (unsigned long long)__double_as_longlong(mres));
+    atomicMax(a.rmax + 1, (unsigned long long)__double_as_longlong(mrhs));
   }
 }
-__global__ void axpy_kernel(double* y, const double* x, int64_t n) {
+// Refinement gate (pass `it`): the pass runs only if the residual of the current λ exceeds refine_tol · max|r|
+// (a backward-stable factorization of a well-conditioned S already leaves a residual at rounding level, and the
+// pass would change nothing); a NaN residual runs it (the non-finite check sees the result). iters[0] = passes run.
+__global__ void refine_gate_kernel(SparseArgs a, int it) {
+  const double mres = __longlong_as_double((long long)a.rmax[0]), mrhs = __longlong_as_double((long long)a.rmax[1]);
+  const int skip = (it > 0 && a.iters[1]) || mres <= a.refine_tol * mrhs;
+  a.iters[1] = skip;
+  a.rmax[2] = (unsigned long long)__double_as_longlong(mres / mrhs);  // developer probe (mabd_dbg_refine_ratio)
+  a.iters[0] = (it == 0 ? 0 : a.iters[0]) + (skip ? 0 : 1);
+  a.rmax[0] = a.rmax[1] = 0ull;
+}
+__global__ void axpy_kernel(double* y, const double* x, int64_t n, const int32_t* gate) {
+  if (*gate) return;
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
     y[i] += x[i];
 }
@@ -363,26 +393,30 @@ __global__ void __launch_bounds__(SP_THREADS) mf_small_kernel(SparseArgs a, cons
     }
     __syncthreads();
   }
+  // unscaled (L D Lᵀ) elimination: step k reads column k, which it does not write, and updates the columns
+  // j > k with S_ij −= S_ik S_jk / S_kk — one barrier per column; the columns are scaled by 1/√D_k afterwards
+  __shared__ double isd[MF_SMALL];
   const int tx = threadIdx.x % 16, ty = threadIdx.x / 16;
   for (int k = 0; k < n; ++k) {
     double d = sF[k * f + k];
     if (!(d > 0.0)) {
       if (threadIdx.x == 0) sreport(a.k, ERR_SINGULAR);
       d = 1.0;
+      if (threadIdx.x == 0) sF[k * f + k] = 1.0;
     }
-    const double sd = sqrt(d), isd = 1.0 / sd;
-    __syncthreads();
-    for (int i = k + 1 + threadIdx.x; i < f; i += blockDim.x) sF[k * f + i] *= isd;
-    if (threadIdx.x == 0) sF[k * f + k] = sd;
-    __syncthreads();
+    const double id = 1.0 / d;
     for (int j = k + 1 + ty; j < f; j += 16) {  // column j, rows i ≥ j
-      const double ljk = sF[k * f + j];
+      const double ljk = sF[k * f + j] * id;
       for (int i = j + tx; i < f; i += 16) sF[j * f + i] -= sF[k * f + i] * ljk;
     }
     __syncthreads();
   }
-  for (int i = threadIdx.x; i < f * f; i += blockDim.x)
-    if (i % f >= i / f) F[i] = sF[i];
+  for (int k = threadIdx.x; k < n; k += blockDim.x) isd[k] = 1.0 / sqrt(sF[k * f + k]);
+  __syncthreads();
+  for (int i = threadIdx.x; i < f * f; i += blockDim.x) {
+    const int c = i / f, r = i % f;
+    if (r >= c) F[i] = c < n ? sF[i] * isd[c] : sF[i];  // L_rc = S_rc / √D_c (the diagonal: √D_c); update as is
+  }
 }
 
 // Extend-add into large parents, one child slot per launch: task = (parent, child column j).
@@ -608,22 +642,21 @@ __global__ void __launch_bounds__(SP_THREADS) mf_trsm_kernel(SparseArgs a, const
     }
 }
 
-// Panel step 3: trailing update C[r0.., c0..] −= P_r P_cᵀ with the panel P = F[:, k0:k0+kb] (lower tiles only);
-// task = (node, r0, c0). 64 threads, 8×8 outputs each (rows tx + 8i, columns ty + 8j); the panel is staged 16
+// Panel step 3: trailing update C[r0.., c0..] −= P_r P_cᵀ with the panel P = F[:, kbeg:kbeg+kcnt] (lower tiles
+// only; one or two panels, see the plan); task = (node, r0, c0, kbeg, kcnt). 64 threads, 8×8 outputs each (rows tx + 8i, columns ty + 8j); the panel is staged 16
 // columns at a time through a double-buffered cp.async pipeline (loads of chunk c+1 overlap the DFMAs of c).
 __device__ __forceinline__ void cp_async8(double* dst, const double* src, bool valid) {
   const uint32_t d = (uint32_t)__cvta_generic_to_shared(dst);
   const int sz = valid ? 8 : 0;  // zero-fill outside the front / panel
   asm volatile("cp.async.ca.shared.global [%0], [%1], 8, %2;" ::"r"(d), "l"(src), "r"(sz) : "memory");
 }
-__global__ void __launch_bounds__(64) mf_syrk_kernel(SparseArgs a, const int32_t* tasks, int k0) {
+__global__ void __launch_bounds__(64) mf_syrk_kernel(SparseArgs a, const int32_t* tasks) {
   __shared__ double As[2][16][MF_NB];
   __shared__ double Bs[2][16][MF_NB];
   const MfArgs& m = a.mf;
-  const int node = tasks[3 * blockIdx.x], r0 = tasks[3 * blockIdx.x + 1], c0 = tasks[3 * blockIdx.x + 2];
-  const int n = m.nown[node];
+  const int32_t* tk = tasks + 5 * blockIdx.x;
+  const int node = tk[0], r0 = tk[1], c0 = tk[2], k0 = tk[3], kb = tk[4];
   const int64_t f = m.fdim[node];
-  const int kb = min(MF_NB, n - k0);
   double* F = m.F + m.foff[node];
   const int tid = threadIdx.x, tx = tid % 8, ty = tid / 8;
   auto stage = [&](int buf, int kk) {
@@ -688,12 +721,100 @@ __global__ void __launch_bounds__(64) mf_syrk_kernel(SparseArgs a, const int32_t
   }
 }
 
+// The same update on the fp64 tensor cores (mma.sync m8n8k4 .f64 = DMMA: 256 FMAs per warp instruction, so the
+// issue slots the DFMA version spends on 8×8 outer products go free; measured peak 37.0 TFLOP/s vs 34.1 for DFMA,
+// tools/dmma_peak.cu). 128 threads = 2×2 warps of 32×32 per 64×64 tile; the panel is staged as above (16 columns
+// per stage, row stride 72 doubles: the fragment loads — 8 rows × 4 columns per warp — hit distinct banks).
+// Fragments (PTX ISA, m8n8k4 .f64): a0 = A[g][t], b0 = B[t][g], c_e = C[g][2t + e] (g = lane / 4, t = lane % 4).
+constexpr int SYRK_LD = MF_NB + 8;
+__global__ void __launch_bounds__(128) mf_syrk_mma_kernel(SparseArgs a, const int32_t* tasks) {
+  __shared__ __align__(16) double As[2][16][SYRK_LD];
+  __shared__ __align__(16) double Bs[2][16][SYRK_LD];
+  const MfArgs& m = a.mf;
+  const int32_t* tk = tasks + 5 * blockIdx.x;
+  const int node = tk[0], r0 = tk[1], c0 = tk[2], k0 = tk[3], kb = tk[4];
+  const int64_t f = m.fdim[node];
+  double* F = m.F + m.foff[node];
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int g = lane >> 2, t = lane & 3;
+  const int wr = 32 * (warp >> 1), wc = 32 * (warp & 1);  // the warp's 32×32 sub-tile
+  auto stage = [&](int buf, int kk) {
+#pragma unroll
+    for (int u = 0; u < 8; ++u) {
+      const int idx = tid + 128 * u;
+      const int r = idx % MF_NB, kc = idx / MF_NB;
+      const bool kin = kk + kc < kb;
+      const double* col = F + (k0 + kk + (kin ? kc : 0)) * f;
+      cp_async8(&As[buf][kc][r], col + (r0 + r < f ? r0 + r : 0), kin && r0 + r < f);
+      cp_async8(&Bs[buf][kc][r], col + (c0 + r < f ? c0 + r : 0), kin && c0 + r < f);
+    }
+    asm volatile("cp.async.commit_group;" ::: "memory");
+  };
+  // a diagonal tile's strictly upper sub-tile (warp rows 0-31, columns 32-63) holds nothing of the lower part
+  const bool idle = r0 == c0 && wr < wc;
+  double acc[4][4][2];
+#pragma unroll
+  for (int i = 0; i < 4; ++i)
+#pragma unroll
+    for (int j = 0; j < 4; ++j)
+#pragma unroll
+      for (int e = 0; e < 2; ++e) {
+        const int r = r0 + wr + 8 * i + g, c = c0 + wc + 8 * j + 2 * t + e;
+        acc[i][j][e] = (!idle && c < f && r < f && r >= c) ? F[(int64_t)c * f + r] : 0.0;
+      }
+  const int nch = (kb + 15) / 16;
+  stage(0, 0);
+  for (int ch = 0; ch < nch; ++ch) {
+    const int buf = ch & 1;
+    if (ch + 1 < nch) {
+      stage(buf ^ 1, (ch + 1) * 16);
+      asm volatile("cp.async.wait_group 1;" ::: "memory");
+    } else {
+      asm volatile("cp.async.wait_group 0;" ::: "memory");
+    }
+    __syncthreads();
+    if (!idle) {
+#pragma unroll
+      for (int k = 0; k < 16; k += 4) {
+        double av[4], bv[4];
+#pragma unroll
+        for (int i = 0; i < 4; ++i) av[i] = -As[buf][k + t][wr + 8 * i + g];
+#pragma unroll
+        for (int j = 0; j < 4; ++j) bv[j] = Bs[buf][k + t][wc + 8 * j + g];
+#pragma unroll
+        for (int i = 0; i < 4; ++i)
+#pragma unroll
+          for (int j = 0; j < 4; ++j)
+            asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};"
+                         : "+d"(acc[i][j][0]), "+d"(acc[i][j][1])
+                         : "d"(av[i]), "d"(bv[j]));
+      }
+    }
+    __syncthreads();  // this buffer is refilled two chunks later
+  }
+  if (idle) return;
+#pragma unroll
+  for (int j = 0; j < 4; ++j)
+#pragma unroll
+    for (int e = 0; e < 2; ++e) {
+      const int c = c0 + wc + 8 * j + 2 * t + e;
+      if (c >= f) continue;
+      double* col = F + (int64_t)c * f;
+#pragma unroll
+      for (int i = 0; i < 4; ++i) {
+        const int r = r0 + wr + 8 * i + g;
+        if (r < f && r >= c) col[r] = acc[i][j][e];
+      }
+    }
+}
+
 // ============================================================================ triangular solves
 // Forward, one CTA per front of a level: w = [own rhs; 0] + children's boundary vectors; y = L11⁻¹ w_own
 // (blocked by 64; the diagonal block is solved by warp 0 in shared memory); w_bnd −= L21 y. y goes to dst
 // (point order), w_bnd stays in the node's solve vector for the parent.
 __global__ void __launch_bounds__(SP_THREADS) mf_fwd_kernel(SparseArgs a, const int32_t* nodes, const double* src,
                                                            double* dst) {
+  if (refine_gated(a)) return;
   extern __shared__ double sm[];
   const MfArgs& m = a.mf;
   const int node = nodes[blockIdx.x];
@@ -719,12 +840,13 @@ __global__ void __launch_bounds__(SP_THREADS) mf_fwd_kernel(SparseArgs a, const 
     const int kb = min(MF_NB, n - k0);
     for (int idx = tid; idx < kb * kb; idx += blockDim.x) {
       const int r = idx % kb, c = idx / kb;
-      Ld[r * (MF_NB + 1) + c] = F[(k0 + c) * f + k0 + r];
+      const double v = F[(k0 + c) * f + k0 + r];
+      Ld[r * (MF_NB + 1) + c] = r == c ? 1.0 / v : v;  // the diagonal as its reciprocal (no division in the chain)
     }
     __syncthreads();
     if (warp == 0) {
       for (int j = 0; j < kb; ++j) {
-        const double xj = w[k0 + j] / Ld[j * (MF_NB + 1) + j];
+        const double xj = w[k0 + j] * Ld[j * (MF_NB + 1) + j];
         __syncwarp();
         if (lane == 0) w[k0 + j] = xj;
         for (int i = j + 1 + lane; i < kb; i += 32) w[k0 + i] -= Ld[i * (MF_NB + 1) + j] * xj;
@@ -748,6 +870,7 @@ __global__ void __launch_bounds__(SP_THREADS) mf_fwd_kernel(SparseArgs a, const 
 // then L11ᵀ x_own = z by 64-blocks from the last. x goes to sol (point order).
 __global__ void __launch_bounds__(SP_THREADS) mf_bwd_kernel(SparseArgs a, const int32_t* nodes, const double* ysrc,
                                                            double* sol) {
+  if (refine_gated(a)) return;
   extern __shared__ double sm[];
   const MfArgs& m = a.mf;
   const int node = nodes[blockIdx.x];
@@ -778,12 +901,13 @@ __global__ void __launch_bounds__(SP_THREADS) mf_bwd_kernel(SparseArgs a, const 
     const int k0 = cidx * MF_NB, kb = min(MF_NB, n - k0);
     for (int idx = tid; idx < kb * kb; idx += blockDim.x) {
       const int r = idx % kb, c = idx / kb;
-      Ld[r * (MF_NB + 1) + c] = F[(k0 + c) * f + k0 + r];
+      const double v = F[(k0 + c) * f + k0 + r];
+      Ld[r * (MF_NB + 1) + c] = r == c ? 1.0 / v : v;  // the diagonal as its reciprocal
     }
     __syncthreads();
     if (warp == 0) {
       for (int j = kb - 1; j >= 0; --j) {
-        const double xj = x[k0 + j] / Ld[j * (MF_NB + 1) + j];
+        const double xj = x[k0 + j] * Ld[j * (MF_NB + 1) + j];
         __syncwarp();
         if (lane == 0) x[k0 + j] = xj;
         for (int i = lane; i < j; i += 32) x[k0 + i] -= Ld[j * (MF_NB + 1) + i] * xj;
@@ -807,6 +931,7 @@ __global__ void __launch_bounds__(SP_THREADS) mf_bwd_kernel(SparseArgs a, const 
 // ---- triangular solves of large fronts, parallel over 64-row / 64-column tiles, one launch per 64-chunk
 // Forward init: w = [own rhs; 0] + the children's boundary vectors (into the node's solve vector).
 __global__ void __launch_bounds__(SP_THREADS) mf_fwd_init_kernel(SparseArgs a, const int32_t* nodes, const double* src) {
+  if (refine_gated(a)) return;
   const MfArgs& m = a.mf;
   const int node = nodes[blockIdx.x];
   const int n = m.nown[node];
@@ -830,6 +955,7 @@ __global__ void __launch_bounds__(SP_THREADS) mf_fwd_init_kernel(SparseArgs a, c
 // below the chunk: w_r −= L[r, chunk] y_c. task = (node, r0 or −1, writer flag).
 __global__ void __launch_bounds__(SP_THREADS) mf_fwd_chunk_kernel(SparseArgs a, const int32_t* tasks, int c,
                                                                  double* dst) {
+  if (refine_gated(a)) return;
   __shared__ double yc[MF_NB];
   __shared__ double part[4][MF_NB];
   const MfArgs& m = a.mf;
@@ -869,6 +995,7 @@ __global__ void __launch_bounds__(SP_THREADS) mf_fwd_chunk_kernel(SparseArgs a, 
 // Backward init: the node's vector ← [y_own; x_bnd] (x_bnd from the ancestors' solution).
 __global__ void __launch_bounds__(SP_THREADS) mf_bwd_init_kernel(SparseArgs a, const int32_t* nodes, const double* ysrc,
                                                                 const double* sol) {
+  if (refine_gated(a)) return;
   const MfArgs& m = a.mf;
   const int node = nodes[blockIdx.x];
   const int n = m.nown[node];
@@ -884,6 +1011,7 @@ __global__ void __launch_bounds__(SP_THREADS) mf_bwd_init_kernel(SparseArgs a, c
 
 // Backward boundary product: z_i = y_i − Σ_{r ≥ n} L[r][i] x_r for the 64 own columns of a tile; task = (node, t0).
 __global__ void __launch_bounds__(SP_THREADS) mf_bwd_bnd_kernel(SparseArgs a, const int32_t* tasks) {
+  if (refine_gated(a)) return;
   const MfArgs& m = a.mf;
   const int node = tasks[2 * blockIdx.x], t0 = tasks[2 * blockIdx.x + 1];
   const int n = m.nown[node];
@@ -907,6 +1035,7 @@ __global__ void __launch_bounds__(SP_THREADS) mf_bwd_bnd_kernel(SparseArgs a, co
 // the 64 earlier own columns of their tile: z_i −= Σ_{r in chunk} L[r][i] x_r. task = (node, t0 or −1, writer).
 __global__ void __launch_bounds__(SP_THREADS) mf_bwd_chunk_kernel(SparseArgs a, const int32_t* tasks, int c,
                                                                  double* sol) {
+  if (refine_gated(a)) return;
   __shared__ double xc[MF_NB];
   __shared__ double part[4][MF_NB];
   const MfArgs& m = a.mf;
@@ -952,9 +1081,16 @@ cudaError_t sparse_init() {
   cudaError_t e;
   if ((e = cudaGetDevice(&dev))) return e;
   if ((e = cudaDeviceGetAttribute(&v, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev))) return e;
-  if ((e = cudaFuncSetAttribute(mf_small_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, v))) return e;
-  if ((e = cudaFuncSetAttribute(mf_fwd_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, v))) return e;
-  if ((e = cudaFuncSetAttribute(mf_bwd_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, v))) return e;
+  auto opt_in = [&](const void* fn) {  // all of the opt-in shared memory beyond the kernel's static part
+    cudaFuncAttributes fa;
+    cudaError_t r = cudaFuncGetAttributes(&fa, fn);
+    if (r == cudaSuccess)
+      r = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, v - (int)fa.sharedSizeBytes);
+    return r;
+  };
+  if ((e = opt_in((const void*)mf_small_kernel))) return e;
+  if ((e = opt_in((const void*)mf_fwd_kernel))) return e;
+  if ((e = opt_in((const void*)mf_bwd_kernel))) return e;
   if ((e = cudaFuncSetAttribute(mf_potrf_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, PANEL_SMEM))) return e;
   if ((e = cudaFuncSetAttribute(mf_trsm_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, PANEL_SMEM))) return e;
   return cudaSuccess;
@@ -1018,7 +1154,12 @@ cudaError_t sparse_step(const Plan& p, const DevPtrs& d, const StepConsts& k, cu
       const int k0 = (int)pi * MF_NB;
       if (P.n_potrf) mf_potrf_kernel<<<(unsigned)P.n_potrf, SP_THREADS, PANEL_SMEM, st>>>(a, T + P.potrf, k0);
       if (P.n_trsm) mf_trsm_kernel<<<(unsigned)P.n_trsm, SP_THREADS, PANEL_SMEM, st>>>(a, T + P.trsm, k0);
-      if (P.n_syrk) mf_syrk_kernel<<<(unsigned)P.n_syrk, 64, 0, st>>>(a, T + P.syrk, k0);
+      if (P.n_syrk) {
+        if (sp.syrk_dfma)
+          mf_syrk_kernel<<<(unsigned)P.n_syrk, 64, 0, st>>>(a, T + P.syrk);
+        else
+          mf_syrk_mma_kernel<<<(unsigned)P.n_syrk, 128, 0, st>>>(a, T + P.syrk);
+      }
     }
   }
   if ((e = cudaGetLastError())) return e;
@@ -1026,8 +1167,11 @@ cudaError_t sparse_step(const Plan& p, const DevPtrs& d, const StepConsts& k, cu
   for (int it = 0; it < sp.refine; ++it) {  // iterative refinement against the exact S (matrix-free)
     mv_body_kernel<<<grid_for(a.n), 256, 0, st>>>(a, a.lam);
     mv_point_kernel<<<grid_for(a.np), 256, 0, st>>>(a);
-    if ((e = mf_solve(sp, a, LN, T, a.res, a.dl, st))) return e;
-    axpy_kernel<<<grid_for(3 * a.np), 256, 0, st>>>(a.lam, a.dl, 3 * a.np);
+    refine_gate_kernel<<<1, 1, 0, st>>>(a, it);
+    SparseArgs g = a;
+    g.gate = a.iters + 1;
+    if ((e = mf_solve(sp, g, LN, T, a.res, a.dl, st))) return e;
+    axpy_kernel<<<grid_for(3 * a.np), 256, 0, st>>>(a.lam, a.dl, 3 * a.np, g.gate);
   }
   sparse_update_kernel<<<grid_for(a.n), 256, 0, st>>>(a);
   return cudaGetLastError();
@@ -1545,17 +1689,28 @@ static bool mf_symbolic(const mabd_bodies* B, Plan* plan, std::string* msg) {
         }
       }
       Pn.n_trsm = ((int64_t)s.tasks.size() - Pn.trsm) / 3;
+      // Trailing updates by pairs of panels (look-ahead by one): when panels pi (even) and pi+1 are both full, the
+      // even step updates only the next panel's column block (rank 64) and the odd step the rest of the trailing
+      // matrix with both panels at once (rank 128: each trailing tile is read and written once per pair);
+      // otherwise each panel updates its whole trailing matrix. Task = (node, r0, c0, first column, columns).
       Pn.syrk = (int64_t)s.tasks.size();
-      for (int32_t i : act) {
-        const int t0 = k0 + std::min(MF_NB, s.nown[i] - k0);
+      auto tiles = [&](int32_t i, int t0, int cmax, int kbeg, int kcnt) {
         for (int r0 = t0; r0 < s.fdim[i]; r0 += MF_NB)
-          for (int c0 = t0; c0 <= r0; c0 += MF_NB) {
-            s.tasks.push_back(i);
-            s.tasks.push_back(r0);
-            s.tasks.push_back(c0);
-          }
+          for (int c0 = t0; c0 <= r0 && c0 < cmax; c0 += MF_NB)
+            for (int32_t v : {i, (int32_t)r0, (int32_t)c0, (int32_t)kbeg, (int32_t)kcnt}) s.tasks.push_back(v);
+      };
+      for (int32_t i : act) {
+        const int kb = std::min(MF_NB, s.nown[i] - k0);
+        const bool even = pi % 2 == 0;
+        const bool paired = even ? s.nown[i] >= k0 + 2 * MF_NB : s.nown[i] >= k0 + MF_NB;
+        if (even && paired)
+          tiles(i, k0 + MF_NB, k0 + 2 * MF_NB, k0, MF_NB);           // the next panel's block column
+        else if (!even && paired)
+          tiles(i, k0 + MF_NB, INT32_MAX, k0 - MF_NB, 2 * MF_NB);    // the rest, both panels
+        else
+          tiles(i, k0 + kb, INT32_MAX, k0, kb);
       }
-      Pn.n_syrk = ((int64_t)s.tasks.size() - Pn.syrk) / 3;
+      Pn.n_syrk = ((int64_t)s.tasks.size() - Pn.syrk) / 5;
     }
     // triangular-solve tasks of the big fronts
     L.fwd.assign(maxpan, 0);
@@ -1743,6 +1898,9 @@ bool sparse_build(const mabd_bodies* B, const mabd_joints* J, Plan* p, std::vect
   if (!mf_symbolic(B, p, msg)) return false;
   s.refine = MF_REFINE;
   if (const char* ev = getenv("MABD_SPARSE_REFINE")) s.refine = std::max(0, std::min(8, atoi(ev)));  // developer knob
+  s.refine_tol = MF_REFINE_TOL;
+  s.syrk_dfma = getenv("MABD_SPARSE_SYRK_DFMA") != nullptr;  // developer knob: the DFMA trailing update
+  if (const char* ev = getenv("MABD_SPARSE_REFINE_TOL")) s.refine_tol = atof(ev);                   // developer knob
   int64_t launches = 4 + (P ? 2 : 0);
   for (const auto& L : s.levels) {
     int64_t per = (L.n_small ? 1 : 0);
@@ -1752,7 +1910,7 @@ bool sparse_build(const mabd_bodies* B, const mabd_joints* J, Plan* p, std::vect
     if (L.n_big) sol += 2 + (L.n_bwdb ? 1 : 0) + (int64_t)L.fwd.size() + (int64_t)L.bwd.size();
     launches += per + sol * (1 + s.refine);
   }
-  launches += 3 * s.refine;
+  launches += 4 * s.refine;
   p->launches_per_step = (int32_t)std::min<int64_t>(launches, INT32_MAX);
   return true;
 }
@@ -1915,7 +2073,7 @@ void sparse_layout(Plan* p, const std::function<size_t(size_t)>& take) {
   s.o_vec = take(sizeof(double) * 15 * np);  // rhs, λ, res, δλ, y: [3][np] each
   s.o_vv = take(sizeof(double) * 12 * n);
   s.o_dqt = take(sizeof(double) * 12 * n);
-  s.o_iters = take(sizeof(int32_t) * 4);
+  s.o_iters = take(sizeof(int32_t) * 4 + sizeof(unsigned long long) * 3);  // iters[4], the gate's rmax[3]
   const size_t NN = nz(s.nnode);
   s.o_F = take(sizeof(double) * nz(s.front_doubles));
   s.o_foff = take(sizeof(int64_t) * NN);
@@ -1979,6 +2137,9 @@ cudaError_t sparse_upload(const Plan& p, char* ws, cudaStream_t st, DevPtrs* d) 
   A.vv = (double*)(ws + s.o_vv);
   A.dqt = (double*)(ws + s.o_dqt);
   A.iters = (int32_t*)(ws + s.o_iters);
+  A.rmax = (unsigned long long*)(ws + s.o_iters + sizeof(int32_t) * 4);
+  A.gate = nullptr;
+  A.refine_tol = s.refine_tol;
   MfArgs& m = A.mf;
   m.F = (double*)(ws + s.o_F);
   m.foff = (const int64_t*)(ws + s.o_foff);
@@ -2049,7 +2210,7 @@ cudaError_t sparse_upload(const Plan& p, char* ws, cudaStream_t st, DevPtrs* d) 
   if ((e = upv(ws, s.o_gs_off, s.gs_chain_off, st))) return e;
   if ((e = upv(ws, s.o_gs_col, s.gs_color_off, st))) return e;
   if ((e = cudaMemsetAsync(A.lam, 0, sizeof(double) * 3 * np, st))) return e;
-  int32_t it[4] = {s.refine, 0, 0, 0};
+  int32_t it[10] = {0, 0, 0, 0, 0, 0, 0, 0, 0, 0};  // iters[4] and rmax[3] = 0
   if ((e = cudaMemcpyAsync(A.iters, it, sizeof(it), cudaMemcpyHostToDevice, st))) return e;
   return cudaStreamSynchronize(st);  // the host vectors above are pageable; keep them alive until copied
 }
