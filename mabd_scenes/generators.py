@@ -752,3 +752,104 @@ def hinge_limits(sc: Scene, lo: float, hi: float) -> Scene:
     out.limits = L
     out.name = sc.name + f"_lim{lo:g}_{hi:g}"
     return out
+
+# --------------------------------------------------------------------------
+# §6.1 single-body validations
+# --------------------------------------------------------------------------
+
+def mbar_from_inertia(I_principal, mass) -> np.ndarray:
+    """Packed central principal M̄ = diag(a0, a1, a2, m) with I_x = a1 + a2, I_y = a0 + a2, I_z = a0 + a1."""
+    I1, I2, I3 = (float(x) for x in I_principal)
+    out = np.zeros(10)
+    out[0] = 0.5 * (I2 + I3 - I1)
+    out[4] = 0.5 * (I1 + I3 - I2)
+    out[7] = 0.5 * (I1 + I2 - I3)
+    out[9] = float(mass)
+    assert min(out[0], out[4], out[7]) > 0.0, "inertia violates the triangle inequality"
+    return out
+
+
+def twist_velocity(A: np.ndarray, t: np.ndarray, omega, v_origin) -> np.ndarray:
+    """ABD generalised velocity of a rigid twist (Eq. module1-G-twist): Ȧ = ω× A, ṫ = v of the frame
+    origin (world frame ω and v)."""
+    om = np.asarray(omega, dtype=np.float64)
+    qd = np.zeros(12)
+    for c in range(3):
+        qd[3 * c:3 * c + 3] = np.cross(om, A[:, c])
+    qd[9:12] = v_origin
+    return qd
+
+
+def _single_body(name, A0, t0, qd0, mbar, volume, E, h, gravity, ja=(), jb=(), npts=(), ya=None, yb=None, meta=None):
+    sc = Scene(name=name, q0=pack_q(np.asarray(A0)[None], np.asarray(t0, dtype=np.float64)[None]),
+               qd0=np.asarray(qd0, dtype=np.float64)[None].copy(), mbar=np.asarray(mbar)[None].copy(),
+               volume=np.array([float(volume)]), youngs=np.array([float(E)]), poisson=np.array([NU]),
+               gravity=np.asarray(gravity, dtype=np.float64).copy(),
+               body_a=np.asarray(ja, np.int32), body_b=np.asarray(jb, np.int32), npts=np.asarray(npts, np.int32),
+               ybar_a=np.zeros((0, 3)) if ya is None else np.asarray(ya, dtype=np.float64),
+               ybar_b=np.zeros((0, 3)) if yb is None else np.asarray(yb, dtype=np.float64),
+               h=float(h), nsteps=1, meta=dict(meta or {"topology": "chain"}))
+    sc.validate()
+    return sc
+
+
+def spinning_box(h: float = 1e-3, p0=(100.0, 0.0, 0.0), L0=(0.0, 100.0, 0.0)) -> Scene:
+    """a 0.1 m cube (ρ = 1e3, E = 1e9, ν = 0.3) on a frictionless surface (no gravity acts in the
+    plane: gravity off) with initial momenta p₀ and L₀; the twist (ω = I⁻¹L₀, v = p₀/m) is mapped to q̇."""
+    s, rho = 0.1, 1000.0
+    mbar = box_mbar(s, s, s, rho)
+    m = mbar[9]
+    I = mbar[4] + mbar[7]  # cube: isotropic
+    qd = twist_velocity(np.eye(3), np.zeros(3), np.asarray(L0) / I, np.asarray(p0) / m)
+    return _single_body("spinning_box", np.eye(3), np.zeros(3), qd, mbar, s ** 3, 1e9, h, np.zeros(3))
+
+
+def t_handle(h: float = 1e-3, omega0: float = 3.0, perturb: float = 1e-3, E: float = 1e9) -> Scene:
+    """a T-handle in zero gravity spun at ω₀ = 3 rad/s about its intermediate principal axis
+    with a small perturbation on the other axes (1e-3). The handle: a 0.2 m bar (0.02² section) along x
+    joined at its middle to a 0.1 m stem along z, ρ = 1e3; M̄ is the pair's central principal second moment
+    (computed here, principal axes = body axes by symmetry, the frame origin at the COM)."""
+    rho = 1000.0
+    bar, stem = (0.2, 0.02, 0.02), (0.02, 0.02, 0.1)
+    mb, ms = rho * np.prod(bar), rho * np.prod(stem)
+    cb, cs = np.array([0.0, 0.0, 0.0]), np.array([0.0, 0.0, -0.06])   # stem hangs below the bar
+    c = (mb * cb + ms * cs) / (mb + ms)
+    S = np.zeros((3, 3))
+    for (dims, mm, cc) in ((bar, mb, cb), (stem, ms, cs)):
+        S += np.diag([mm * d * d / 12.0 for d in dims]) + mm * np.outer(cc - c, cc - c)
+    mbar = np.zeros(10)
+    mbar[0], mbar[4], mbar[7], mbar[9] = S[0, 0], S[1, 1], S[2, 2], mb + ms
+    I = np.array([S[1, 1] + S[2, 2], S[0, 0] + S[2, 2], S[0, 0] + S[1, 1]])
+    mid = int(np.argsort(I)[1])   # the intermediate principal axis (body z for this handle)
+    w = np.full(3, perturb)
+    w[mid] = 1.0
+    w = w * omega0
+    qd = twist_velocity(np.eye(3), np.zeros(3), w, np.zeros(3))
+    vol = np.prod(bar) + np.prod(stem)
+    return _single_body("t_handle", np.eye(3), np.zeros(3), qd, mbar, vol, E, h, np.zeros(3),
+                        meta={"topology": "chain", "inertia": I, "mid_axis": mid, "omega0_body": w})
+
+
+def heavy_top(h: float = 1e-3, spin: float = 10.0, tilt_deg: float = 5.0, E: float = 1e9) -> Scene:
+    """a heavy top on a fixed pivot under gravity, spun at 10 rad/s about its symmetry axis, tilted 5°.
+    The top: a 0.2 m wide, 0.02 m thick square plate (ρ = 1e3, symmetric: I₁ = I₂) whose COM sits 0.01 m above the
+    pivot on the symmetry axis (body z), so 10 rad/s makes it a fast top (I₃²ω² > 4 I₁ m g d: it precesses and
+    nutates instead of falling); the pivot is a world anchor (ball joint) at the body point ȳ = (0, 0, −0.01)."""
+    rho, a, c, d = 1000.0, 0.2, 0.02, 0.01
+    mbar = box_mbar(a, a, c, rho)
+    R0 = rot_x(np.deg2rad(tilt_deg))
+    t0 = R0 @ np.array([0.0, 0.0, d])                  # pivot at the world origin
+    qd = twist_velocity(R0, t0, spin * R0[:, 2], np.zeros(3))   # spin about the axis through the pivot: ṫ = 0
+    return _single_body("heavy_top", R0, t0, qd, mbar, a * a * c, E, h, GRAVITY, ja=[0], jb=[-1], npts=[1],
+                        ya=[[0.0, 0.0, -d]], yb=[[0.0, 0.0, 0.0]], meta={"topology": "chain", "pivot_to_com": d})
+
+
+def pendulum_horizontal(h: float = 1e-3, length: float = 0.4, E: float = 1e9) -> Scene:
+    """a physical pendulum (a 0.4×0.04×0.04 m rod, ρ = 1e3) on a fixed pivot at one end, released at rest
+    from the horizontal (rod along +x, pivot = world origin, a ball-joint anchor) under gravity."""
+    a = 0.04
+    mbar = box_mbar(length, a, a, 1000.0)
+    t0 = np.array([length / 2, 0.0, 0.0])
+    return _single_body("pendulum_horizontal", np.eye(3), t0, np.zeros(12), mbar, length * a * a, E, h, GRAVITY,
+                        ja=[0], jb=[-1], npts=[1], ya=[[-length / 2, 0.0, 0.0]], yb=[[0.0, 0.0, 0.0]],
+                        meta={"topology": "chain", "length": length})
