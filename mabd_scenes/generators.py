@@ -698,6 +698,95 @@ def five_row_hinges(sc: Scene) -> Scene:
     return out
 
 
+def nonlinear_joints(sc: Scene, seed: int = 0, universal: float = 0.5, prismatic: float = 0.5,
+                     hinge5: float = 0.0) -> Scene:
+    """The same scene with its two-point (linear) hinges turned, at random, into universal joints (kind 2), prismatic
+    joints (kind 3) or five-row hinges (kind 1) (R13, R17). A universal joint keeps the pivot
+    point and body a's axis point; body b's second point moves to a direction ⟂ the axis in b's frame (a₂ ⟂ a₁). A
+    prismatic joint keeps both axis points and gains a third point ⟂ the axis, at the same world position on both
+    bodies (computed from q0). Fractions are of the two-point joints; the rest stay linear hinges. Input
+    construction only."""
+    rng = np.random.default_rng([_seed_base(), 7000 + seed])
+    npts = np.asarray(sc.npts)
+    off = np.concatenate([[0], np.cumsum(npts)])
+    kind = np.zeros(sc.n_joints, np.int32) if sc.kind is None else np.asarray(sc.kind, np.int32).copy()
+    ya, yb, nn = [], [], []
+    for k in range(sc.n_joints):
+        pa, pb = sc.ybar_a[off[k]:off[k + 1]].copy(), sc.ybar_b[off[k]:off[k + 1]].copy()
+        if npts[k] == 2 and kind[k] == 0:
+            u = rng.random()
+            ax_b = pb[1] - pb[0]
+            rho = np.linalg.norm(pa[1] - pa[0])
+            if u < universal:
+                kind[k] = 2
+                v = rng.standard_normal(3)
+                v -= ax_b * (v @ ax_b) / (ax_b @ ax_b)
+                pb[1] = pb[0] + rho * v / np.linalg.norm(v)
+            elif u < universal + prismatic:
+                kind[k] = 3
+                a, b = sc.body_a[k], sc.body_b[k]
+                ax_a = pa[1] - pa[0]
+                v = rng.standard_normal(3)
+                v -= ax_a * (v @ ax_a) / (ax_a @ ax_a)
+                y2a = pa[0] + rho * v / np.linalg.norm(v)
+                Aa = sc.q0[a, :9].reshape(3, 3).T
+                x = Aa @ y2a + sc.q0[a, 9:]
+                if b >= 0:
+                    Ab = sc.q0[b, :9].reshape(3, 3).T
+                    y2b = np.linalg.solve(Ab, x - sc.q0[b, 9:])
+                else:
+                    y2b = x
+                pa = np.vstack([pa, y2a])
+                pb = np.vstack([pb, y2b])
+            elif u < universal + prismatic + hinge5:
+                kind[k] = 1
+        ya.append(pa)
+        yb.append(pb)
+        nn.append(len(pa))
+    out = sc.copy()
+    out.kind = kind
+    out.npts = np.asarray(nn, np.int32)
+    out.ybar_a = np.vstack(ya) if ya else np.zeros((0, 3))
+    out.ybar_b = np.vstack(yb) if yb else np.zeros((0, 3))
+    out.name = sc.name + "_nonlinear"
+    out.validate()
+    return out
+
+
+def universal_pendulum(omega0=(0.0, 0.0, 0.0), length: float = 0.4, h: float = 1e-2, E: float = 1e8) -> Scene:
+    """A 0.04×0.04×0.4 m rod (ρ = 1000) hanging from the world by a universal joint at its top end:
+    axis a₁ = the rod's body x, axis a₂ = the world y, so the rod swings about x and y and cannot turn about its
+    long axis (a₁ × a₂ = z). Released with angular velocity omega0 about its centre of mass."""
+    a, b = 0.04, length
+    t0 = np.array([[0.0, 0.0, -b / 2]])
+    om = np.asarray(omega0, dtype=np.float64)
+    qd = np.zeros((1, 12))
+    for c in range(3):
+        qd[0, 3 * c:3 * c + 3] = np.cross(om, np.eye(3)[:, c])
+    sc = _assemble("universal_pendulum", np.eye(3)[None], t0, qd, box_mbar(a, a, b, 1000.0)[None],
+                   np.array([a * a * b]), E, NU, np.array([0], np.int32), np.array([-1], np.int32),
+                   np.array([2], np.int32), np.array([[0.0, 0.0, 0.0], [0.05, 0.0, 0.0]]), h, 1,
+                   meta={"topology": "tree"})
+    sc.ybar_b[1] = [0.0, 0.05, 0.0]          # a₂ = world y (the rod's a₁ = x stays at ȳ_a[1] − ȳ_a[0])
+    sc.kind = np.array([2], np.int32)
+    return sc
+
+
+def prismatic_rail(tilt_deg: float = 30.0, h: float = 1e-2, E: float = 1e8) -> Scene:
+    """A 0.1×0.05×0.05 m slider (ρ = 1000) on a frictionless world rail tilted by tilt_deg from the horizontal
+    (P:427-444): a prismatic joint whose axis is the slider's body x, mapped onto the rail direction; under gravity
+    it slides down the rail with acceleration g sin(tilt) and does not turn."""
+    th = np.deg2rad(tilt_deg)
+    c, s_ = np.cos(th), np.sin(th)
+    A0 = np.array([[c, 0.0, -s_], [0.0, 1.0, 0.0], [s_, 0.0, c]])   # body x → (cos, 0, sin)
+    pts = np.array([[0.0, 0.0, 0.0], A0 @ [0.05, 0.0, 0.0], A0 @ [0.0, 0.05, 0.0]])
+    sc = _assemble("prismatic_rail", A0[None], np.zeros((1, 3)), None, box_mbar(0.1, 0.05, 0.05, 1000.0)[None],
+                   np.array([0.1 * 0.05 * 0.05]), E, NU, np.array([0], np.int32), np.array([-1], np.int32),
+                   np.array([3], np.int32), pts, h, 1, meta={"topology": "tree", "rail": A0[:, 0]})
+    sc.kind = np.array([3], np.int32)
+    return sc
+
+
 def hinge_pendulum(axis=(1.0, 0.0, 0.0), omega0=(0.0, 0.0, 0.0), length: float = 0.4, h: float = 1e-2,
                    E: float = 1e8) -> Scene:
     """A 0.4×0.04×0.04 m rod (ρ = 1000) hanging from a world hinge at its top end (two world points on the axis,

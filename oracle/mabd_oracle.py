@@ -37,7 +37,8 @@ import scipy.sparse.linalg as spla
 __all__ = [
     "lame", "unpack_mbar", "mass_A", "kbar_A", "hbar_A", "polar", "elastic_force_A", "stvk_force_A",
     "length_preserving", "affine_force",
-    "body_hessians", "hinge_frame", "hinge5_rows", "rotation_about", "hinge_angle", "hinge_limit_rows",
+    "body_hessians", "hinge_frame", "hinge5_rows", "joint_general_rows", "general_row", "rotation_about", "hinge_angle",
+    "hinge_limit_rows",
     "constraint_system", "constraint_residual", "predict", "step", "simulate", "nonlinear_residual",
     "wrench_force", "twist_velocity", "angular_velocity",
     "block_thomas", "leaf_to_root_solve", "dual_matrix", "line_gauss_seidel", "step_with_dual", "twist_embedding",
@@ -264,13 +265,89 @@ def hinge5_rows(scene, q):
         return out
     off = np.concatenate([[0], np.cumsum(scene.npts)])
     Pxz = np.array([[1.0, 0, 0], [0, 0, 1.0]])
-    for k in np.nonzero(np.asarray(kind) == 1)[0]:
+    kind = np.asarray(kind)
+    for k in np.nonzero(kind == 1)[0]:
         p0 = off[k]
         a = scene.body_a[k]
         R = polar(unvec(np.asarray(q)[a, :9]))
         dR = hinge_frame(scene.ybar_a[p0 + 1] - scene.ybar_a[p0])
         out[p0 + 1] = Pxz @ dR @ R.T
+    for k in np.nonzero(kind == 2)[0]:   # universal (R17): the second point carries no point rows
+        out[off[k] + 1] = np.zeros((0, 3))
+    for k in np.nonzero(kind == 3)[0]:   # prismatic (R17): all its rows are general rows (joint_general_rows)
+        for i in range(3):
+            out[off[k] + i] = np.zeros((0, 3))
     return out
+
+
+def joint_general_rows(scene):
+    """The rows of the universal and prismatic joints (SURVEY §8(f) NEXT 2; P:405-444, Eqs. universal and prismatic;
+    DESIGN.md R17). Each row is a scalar C(q) in the joint frame following body a, with R ≈ A ("C̃ can be
+    well approximated as a quadratic function of q̃ since R^j is relaxed to A^j"), so that its gradient (Eq.
+    constraint_gradient, both terms) is exact. Two row types, (type, a, b, d, y_a, y_b):
+    - 'dir':   (A_a d)·(A_b y_b) = 0, a direction of a against a direction of b (A_b = I for the world);
+    - 'point': (A_a d)·(x_a(y_a) − x_b(y_b)) = 0, a component of a point pair's offset in a's frame (x_b = y_b
+      for the world).
+    - universal (kind 2; points: the centre, then ȳ_a[1] − ȳ_a[0] ∥ a₁ in body a, ȳ_b[1] − ȳ_b[0] ∥ a₂ in body b):
+      the centre is a ball (3 point rows, not here) and one 'dir' row (â₁, e₂) — "the local y coordinates of the
+      first and the second CPs of β identical" (P:419-422);
+    - prismatic (kind 3; points: two on the sliding axis, ȳ_a[1] − ȳ_a[0] ∥ â, and a third with ȳ_a[2] − ȳ_a[0] ⟂ â,
+      all coincident at creation): 'point' rows x̂, ẑ of the first points' offset (x̂, ẑ = ΔR_Pᵀe_x, ΔR_Pᵀe_z: "x̃, z̃
+      of ỹ₂^α − ỹ₁^β"), 'dir' rows (x̂, e), (ẑ, e) keeping the axes parallel (e = ȳ_b[1] − ȳ_b[0]: "x̃, z̃
+      of ỹ₁^β − ỹ₂^β"), and the 'dir' row (n̂, u), n̂ = â × unit(ȳ_a[2] − ȳ_a[0]), u = ȳ_b[2] − ȳ_b[0], which stops
+      the twist about the axis (the paper's "x̃₃^β = 0", with its reference direction from the third
+      point)."""
+    kind = getattr(scene, "kind", None)
+    out = []
+    if kind is None:
+        return out
+    kind = np.asarray(kind)
+    off = np.concatenate([[0], np.cumsum(scene.npts)])
+    for k in np.nonzero((kind == 2) | (kind == 3))[0]:
+        p0, a, b = off[k], int(scene.body_a[k]), int(scene.body_b[k])
+        ax = scene.ybar_a[p0 + 1] - scene.ybar_a[p0]
+        ax = ax / np.linalg.norm(ax)
+        e = scene.ybar_b[p0 + 1] - scene.ybar_b[p0]
+        if kind[k] == 2:
+            out.append(("dir", a, b, ax, None, e))
+            continue
+        dR = hinge_frame(ax)
+        ua = scene.ybar_a[p0 + 2] - scene.ybar_a[p0]
+        n = np.cross(ax, ua / np.linalg.norm(ua))
+        for d in (dR[0], dR[2]):
+            out.append(("point", a, b, d, scene.ybar_a[p0], scene.ybar_b[p0]))
+        out.append(("dir", a, b, dR[0], None, e))
+        out.append(("dir", a, b, dR[2], None, e))
+        out.append(("dir", a, b, n, None, scene.ybar_b[p0 + 2] - scene.ybar_b[p0]))
+    return out
+
+
+def general_row(row, q):
+    """Value C(q) and gradient {body: ∂C/∂q_body (12,)} of one row of joint_general_rows (∂/∂A[r, c] at index
+    3c + r, the vec(A) layout)."""
+    typ, a, b, d, ya, yb = row
+    q = np.asarray(q)
+    Aa = unvec(q[a, :9])
+    w = Aa @ d
+    g = {a: np.zeros(12)}
+    if b >= 0:
+        g[b] = np.zeros(12)
+    if typ == "dir":
+        Ab = unvec(q[b, :9]) if b >= 0 else np.eye(3)
+        xb = Ab @ yb
+        g[a][:9] = np.outer(xb, d).T.reshape(9)          # ∂/∂A_a = (A_b y_b) dᵀ
+        if b >= 0:
+            g[b][:9] = np.outer(w, yb).T.reshape(9)      # ∂/∂A_b = (A_a d) y_bᵀ
+        return float(w @ xb), g
+    xa = Aa @ ya + q[a, 9:]
+    xb = (unvec(q[b, :9]) @ yb + q[b, 9:]) if b >= 0 else yb
+    off = xa - xb
+    g[a][:9] = (np.outer(off, d) + np.outer(w, ya)).T.reshape(9)   # rotation term + point term
+    g[a][9:] = w
+    if b >= 0:
+        g[b][:9] = -np.outer(w, yb).T.reshape(9)
+        g[b][9:] = -w
+    return float(w @ off), g
 
 
 def rotation_about(axis, angle) -> np.ndarray:
@@ -363,15 +440,34 @@ def constraint_system(scene, q=None):
     world[wm] = scene.ybar_b[wm]
     world = world.reshape(-1)
     W = hinge5_rows(scene, q) if getattr(scene, "kind", None) is not None else {}
-    if W:  # five-row hinges: the second point's 3 rows → its 2 rows W (2×3), linearised with W frozen at q (R13)
+    if W:  # five-row hinges: the second point's 3 rows → its 2 rows W (2×3), linearised with W frozen at q (R13);
+        # universal / prismatic points: their rows W (R17), possibly none
         if q is None:
-            raise ValueError("five-row hinges: the constraint rows depend on the state q")
+            raise ValueError("nonlinear joints: the constraint rows depend on the state q")
         blocks = []
         for p in range(P):
-            blocks.append(sp.csr_matrix(W[p]) if p in W else sp.identity(3, format="csr"))
+            blocks.append(sp.csr_matrix(W[p], shape=W[p].shape) if p in W else sp.identity(3, format="csr"))
         T = sp.block_diag(blocks, format="csr")
         J = (T @ J).tocsr()
         world = T @ world
+    gen = joint_general_rows(scene)
+    if gen:  # universal / prismatic rows, linearised at q with their exact gradient (R17)
+        if q is None:
+            raise ValueError("nonlinear joints: the constraint rows depend on the state q")
+        q = np.asarray(q)
+        rows, cols, vals, wext = [], [], [], []
+        for i, row in enumerate(gen):
+            c0, g = general_row(row, q)
+            Jq = 0.0
+            for body, gv in g.items():
+                rows.extend([i] * 12)
+                cols.extend(range(12 * body, 12 * body + 12))
+                vals.extend(gv)
+                Jq += gv @ q[body]
+            wext.append(Jq - c0)                     # J q − w = C(q) at the linearisation point
+        Jb = sp.csr_matrix((vals, (rows, cols)), shape=(len(gen), 12 * n))
+        J = sp.vstack([J, Jb], format="csr")
+        world = np.concatenate([world, wext])
     lim = hinge_limit_rows(scene, q) if q is not None else []
     if lim:  # active joint limits: one row each, appended (R14)
         rows, cols, vals, wext = [], [], [], []
