@@ -23,8 +23,8 @@
  *     are mapped to their central principal frame internally and back on output, reading R8).
  *   - Joints are point-coincidence constraints C = x_a(ȳ_a) − x_b(ȳ_b), x(ȳ) = Aȳ + t: a ball joint has
  *     1 point, the linear ("affine") hinge has 2 points on the axis. body_b = −1
- *     makes an anchor to the world point stored in ybar_b. The five-row (nonlinear) hinge of P:391-404 is
- *     joints.kind = 1; the universal and prismatic joints are not supported in this version.
+ *     makes an anchor to the world point stored in ybar_b. The nonlinear joints of P:391-444 are
+ *     joints.kind = 1 (five-row hinge), 2 (universal), 3 (prismatic); the sparse solver runs them.
  *
  * Ownership
  *   - Every input pointer is borrowed for the duration of the call only; the library copies what it needs.
@@ -84,14 +84,24 @@ typedef struct {
   int64_t n_joints;          /* K ≥ 0                                                              */
   const int32_t *body_a;     /* [K] in [0, n)                                                      */
   const int32_t *body_b;     /* [K] in [−1, n), −1 = world (anchor), ≠ body_a                      */
-  const int32_t *npts;       /* [K] in {1 (ball / anchor), 2 (linear hinge)}                        */
+  const int32_t *npts;       /* [K] in {1 (ball / anchor), 2 (linear hinge, five-row hinge, universal),
+                                3 (prismatic)}                                                       */
   const double *ybar_a;      /* [Σnpts][3] material points on body_a (body frame)                  */
   const double *ybar_b;      /* [Σnpts][3] material points on body_b, or world points for anchors  */
   const int32_t *kind;       /* [K] or NULL (all 0). 0: point joint (ball / linear 6-row hinge / anchor);
                                 1: five-row hinge (Eq. hinge; R13): npts = 2, the points on
                                 the axis (the axis in body_a's frame is ȳ_a[1] − ȳ_a[0]); the first point is a
                                 ball, the second keeps only its two rows normal to the axis in the hinge frame
-                                R_H = ΔR_H Rᵀ(A_a), re-evaluated every Newton iteration. Sparse solver only.   */
+                                R_H = ΔR_H Rᵀ(A_a), re-evaluated every Newton iteration. Sparse solver only.
+                                2: universal joint (Eq. universal; R17): npts = 2; point 0
+                                is the centre (a ball); ȳ_a[1] − ȳ_a[0] is the axis a₁ in body_a's frame and
+                                ȳ_b[1] − ȳ_b[0] the axis a₂ in body_b's (world for an anchor), a₁ ⟂ a₂ at creation;
+                                one more row (A_a â₁)·(A_b e₂) = 0 keeps them orthogonal. Sparse solver only.
+                                3: prismatic joint (Eq. prismatic; R17): npts = 3, all three points
+                                coincident at creation; points 0, 1 on the sliding axis (ȳ_a[1] − ȳ_a[0] in
+                                body_a's frame), point 2 off the axis. Five rows: the offset of point 0 normal to
+                                the axis, the axes parallel, no twist. Sparse solver only. Rows of kinds 2, 3 are
+                                linearised at every Newton iteration with R ≈ A and their exact gradient.       */
   const double *limits;      /* [K][8] or NULL: joint limits of five-row hinges (R14): lo, hi
                                 (rad; ±inf = none), u_a (3, ⟂ the axis, body a's frame), u_b (3, body b's frame,
                                 or world for an anchor) with u_a, u_b equal in the world at creation, so the hinge
@@ -146,7 +156,7 @@ mabd_status mabd_workspace_size(const mabd_bodies *bodies, const mabd_joints *jo
 
 /* The problem statement of P:459-475 (Eq. kkt): M affine bodies (mass M_A = M̄ ⊗ I₃; elastic
  * weight V with E, ν) and K joints. Validates (MABD_EINVAL on bad sizes, indices, non-SPD M̄,
- * a joint on one body, npts ∉ {1, 2}, bad kind / limits / options), maps every body to its canonical frame
+ * a joint on one body, npts ∉ {1, 2} (3 for kind 3), bad kind / limits / options), maps every body to its canonical frame
  * (R8), classifies the joint topology (forest of ball-joint paths → chain, forest → tree, cycles → sparse;
  * SURVEY A14) or takes options.solver, orders bodies and joints for that solver, and copies everything into the
  * device workspace. Borrows the arrays for the duration of the call. World > 1 with an NCCL id: collective. */

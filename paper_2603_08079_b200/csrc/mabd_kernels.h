@@ -133,6 +133,12 @@ struct GsArgs {
 // a projected slot's limit record (plim): [0] lo, [1] hi, [2..4] u_a, [5..7] u_b, [8..10] ȳ_a0 (pivot on body a),
 // [11..13] â (unit axis, body a), [14] ρ (> 0 marks a limit slot; 0: the hinge rows of a five-row hinge)
 constexpr int LIM_DOUBLES = 15;
+// universal / prismatic joints (R17): "general" slots of ≤ 2 rows; constant per row: type (0 unused,
+// 1 'point': (A_a d)·(x_a(ȳ_a) − x_b(ȳ_b)) with the slot point's ȳ, 2 'dir': (A_a d)·(A_b e)), d (3), e (3), pad
+constexpr int PGC_ROW = 8, PGC_DOUBLES = 2 * PGC_ROW;
+// per Newton iteration: for row i, side σ the row's world coefficients w (point part), v, dd (direction part) at
+// 18 i + 9 σ; the value at the linearisation point c0[i] at 36 + i
+constexpr int PG_DOUBLES = 38;
 struct SparseArgs {
   BodyArrays b;
   const HinvBlk* hinv_tab;     // per material, or null (per-body mass scale)
@@ -150,6 +156,8 @@ struct SparseArgs {
                                // the rows beyond are decoupled dummies (S = 1, r = 0, λ = 0)
   const int32_t* pplist;       // [nproj] the projected points
   const double* plim;          // [nproj][LIM_DOUBLES] joint limits (R14), or unused (hinge rows)
+  const double* pgc;           // [nproj][PGC_DOUBLES] general-slot rows (R17), type 0 for other slots; or null
+  double* pg;                  // [nproj][PG_DOUBLES] general-slot rows at the linearisation point
   int64_t nproj;
   const int32_t* inc_off;      // [n+1] CSR body → incident points (2·point + side)
   const int32_t* inc;

@@ -36,7 +36,7 @@ bool loop_split(const mabd_joints* J, int64_t n, LoopPlan* L, std::string* msg) 
     return x;
   };
   for (int64_t k = 0; J->kind && k < J->n_joints; ++k)
-    if (J->kind[k] != 0) return *msg = "five-row hinges need the sparse solver", false;
+    if (J->kind[k] != 0) return *msg = "nonlinear joints (five-row hinges, universal, prismatic) need the sparse solver", false;
   L->keep.clear();
   L->breakers.clear();
   for (int64_t k = 0; k < J->n_joints; ++k) {

@@ -244,9 +244,14 @@ static mabd_status validate(const mabd_bodies* B, const mabd_joints* J, const ma
     if (a < 0 || a >= B->n) return *msg = fmt("joint %lld: body_a out of range", (long long)k), MABD_EINVAL;
     if (b < -1 || b >= B->n) return *msg = fmt("joint %lld: body_b out of range", (long long)k), MABD_EINVAL;
     if (a == b) return *msg = fmt("joint %lld: both ends on body %lld", (long long)k, a), MABD_EINVAL;
-    if (np != 1 && np != 2) return *msg = fmt("joint %lld: npts must be 1 or 2", (long long)k), MABD_EINVAL;
-    if (J->kind && J->kind[k] != 0 && (J->kind[k] != 1 || np != 2))
-      return *msg = fmt("joint %lld: kind must be 0, or 1 (five-row hinge) with npts = 2", (long long)k),
+    const int32_t kd = J->kind ? J->kind[k] : 0;
+    if (kd < 0 || kd > 3)
+      return *msg = fmt("joint %lld: kind must be 0 (point), 1 (five-row hinge), 2 (universal) or 3 (prismatic)",
+                        (long long)k), MABD_EINVAL;
+    if (kd == 3 ? np != 3 : (np != 1 && np != 2))
+      return *msg = fmt("joint %lld: npts must be 1 or 2 (3 for a prismatic joint)", (long long)k), MABD_EINVAL;
+    if ((kd == 1 || kd == 2) && np != 2)
+      return *msg = fmt("joint %lld: five-row hinges and universal joints have npts = 2", (long long)k),
              MABD_EINVAL;
     P += np;
   }

@@ -98,7 +98,8 @@ struct SparsePlan {
   // five-row hinges: projected points (R13)
   std::vector<int32_t> pslot, pplist;
   std::vector<double> pdr, plim;   // plim: LIM_DOUBLES per slot (joint limits, R14)
-  size_t o_pslot = 0, o_pdr = 0, o_pw = 0, o_pplist = 0, o_pnr = 0, o_plim = 0;
+  std::vector<double> pgc;         // PGC_DOUBLES per slot (universal / prismatic rows, R17); empty if none
+  size_t o_pslot = 0, o_pdr = 0, o_pw = 0, o_pplist = 0, o_pnr = 0, o_plim = 0, o_pgc = 0, o_pg = 0;
   // line Gauss-Seidel (MABD_SOLVER_LINE_GS; gs_build in mabd_sparse.cu)
   std::vector<int32_t> gs_chain_pts, gs_chain_off, gs_color_off;
   int32_t gs_ncolor = 0, gs_sweeps = 0;

@@ -19,6 +19,7 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <array>
 #include <cstdlib>
 #include <cmath>
 #include <cstring>
@@ -103,6 +104,126 @@ __device__ __forceinline__ void project_cols(const SparseArgs& a, int64_t p, dou
   for (int e = 0; e < 3; ++e) x[e] = w[e] * x0 + w[3 + e] * x1;
 }
 
+// general slots (universal / prismatic joints, R17): each row is a scalar in body a's joint frame with
+// R ≈ A, linearised at the iterate with its exact gradient; per side its coefficients are, in the world frame,
+// w (a point part, at the slot point's ȳ) and v ⊗ dd (a direction part): J_side = [w ȳ_c + v dd_c (c = 0..2); w].
+__device__ __forceinline__ int gen_slot(const SparseArgs& a, int64_t p) {
+  if (!a.pgc || !a.pslot) return -1;
+  const int s = a.pslot[p];
+  return (s >= 0 && a.pgc[(int64_t)PGC_DOUBLES * s] != 0.0) ? s : -1;
+}
+__device__ __forceinline__ void gen_row_world(const SparseArgs& a, int64_t p, int s, int i, int side, double* o) {
+  const double* g = a.pg + (int64_t)PG_DOUBLES * s + 18 * i + 9 * side;
+  const double* y = a.py + 6 * p + 3 * side;
+#pragma unroll
+  for (int c = 0; c < 3; ++c)
+#pragma unroll
+    for (int r = 0; r < 3; ++r) o[3 * c + r] = g[r] * y[c] + g[3 + r] * g[6 + c];
+#pragma unroll
+  for (int r = 0; r < 3; ++r) o[9 + r] = g[r];
+}
+__device__ __forceinline__ double dot12(const double* x, const double* y) {
+  double s = 0.0;
+#pragma unroll
+  for (int c = 0; c < 12; ++c) s += x[c] * y[c];
+  return s;
+}
+__device__ __forceinline__ void to_body12(const double* R, const double* w, double* b) {
+#pragma unroll
+  for (int kb = 0; kb < 4; ++kb) mat3t_vec(R, w + 3 * kb, b + 3 * kb);
+}
+// row e of point p on `side` as a body-frame 12-vector (any point: plain, hinge / limit rows, general rows), with
+// the side's sign; rows beyond a slot's count are zero
+__device__ void row_body(const SparseArgs& a, int64_t p, int e, int side, const double* R, double* o) {
+#pragma unroll
+  for (int c = 0; c < 12; ++c) o[c] = 0.0;
+  const int gs = gen_slot(a, p);
+  if (gs >= 0) {
+    if (e < a.pnr[gs]) {
+      double w[12];
+      gen_row_world(a, p, gs, e, side, w);
+      to_body12(R, w, o);
+    }
+    return;
+  }
+  double wv[3] = {0.0, 0.0, 0.0};
+  if (a.pslot && a.pslot[p] >= 0) {
+    const int sl = a.pslot[p];
+    if (e >= a.pnr[sl]) return;
+    const double* w = a.pw + 6 * (int64_t)sl + 3 * e;
+    wv[0] = w[0];
+    wv[1] = w[1];
+    wv[2] = w[2];
+  } else {
+    wv[e] = 1.0;
+  }
+  double wl[3];
+  mat3t_vec(R, wv, wl);
+  add_point_force(o, a.py + 6 * p + 3 * side, wl, side == 0 ? 1.0 : -1.0);
+}
+// a general slot's rows at the linearisation point (A, t of the iterate in q): 'dir' (A_a d)·(A_b e): side a
+// v = A_b e, dd = d; side b v = A_a d, dd = e. 'point' (A_a d)·(x_a − x_b): side a w = A_a d, v = x_a − x_b (the
+// frame's rotation term), dd = d; side b w = −A_a d. c0 = the row's value.
+__device__ void gen_rows(const SparseArgs& a, int s, int64_t p) {
+  const int64_t ld = a.b.ld, ja = a.pa[p], jb = a.pb[p];
+  double Aa[9], Ab[9], ta[3], tb[3];
+#pragma unroll
+  for (int r = 0; r < 3; ++r) {
+#pragma unroll
+    for (int c = 0; c < 3; ++c) {
+      Aa[3 * r + c] = a.b.q[(3 * c + r) * ld + ja];
+      Ab[3 * r + c] = jb >= 0 ? a.b.q[(3 * c + r) * ld + jb] : (r == c ? 1.0 : 0.0);
+    }
+    ta[r] = a.b.q[(9 + r) * ld + ja];
+    tb[r] = jb >= 0 ? a.b.q[(9 + r) * ld + jb] : 0.0;
+  }
+  int nr = 0;
+  for (int i = 0; i < 2; ++i) {
+    const double* c = a.pgc + (int64_t)PGC_DOUBLES * s + PGC_ROW * i;
+    const int type = (int)c[0];
+    double* g = a.pg + (int64_t)PG_DOUBLES * s + 18 * i;
+#pragma unroll
+    for (int e = 0; e < 18; ++e) g[e] = 0.0;
+    a.pg[(int64_t)PG_DOUBLES * s + 36 + i] = 0.0;
+    if (type == 0) continue;
+    nr = i + 1;
+    double wa[3], xb[3];
+    mat3_vec(Aa, c + 1, wa);
+    double c0 = 0.0;
+    if (type == 2) {
+      mat3_vec(Ab, c + 4, xb);
+#pragma unroll
+      for (int r = 0; r < 3; ++r) {
+        g[3 + r] = xb[r];
+        g[6 + r] = c[1 + r];
+        g[12 + r] = wa[r];
+        g[15 + r] = c[4 + r];
+        c0 += wa[r] * xb[r];
+      }
+    } else {
+      const double* ya = a.py + 6 * p;
+      const double* yb = ya + 3;
+      double xa[3];
+      mat3_vec(Aa, ya, xa);
+      if (jb >= 0)
+        mat3_vec(Ab, yb, xb);
+#pragma unroll
+      for (int r = 0; r < 3; ++r) {
+        xa[r] += ta[r];
+        xb[r] = jb >= 0 ? xb[r] + tb[r] : yb[r];
+        const double off = xa[r] - xb[r];
+        g[r] = wa[r];
+        g[3 + r] = off;
+        g[6 + r] = c[1 + r];
+        g[9 + r] = -wa[r];
+        c0 += wa[r] * off;
+      }
+    }
+    a.pg[(int64_t)PG_DOUBLES * s + 36 + i] = c0;
+  }
+  a.pnr[s] = nr;
+}
+
 // per step (Newton iteration), at its linearisation point (R in rs):
 //  hinge rows: w_i = R_a ΔR_H[i]ᵀ of the second axis point (R13);
 //  joint limits (R14): θ = atan2(a_w·(u_aw × u_bw), u_aw·u_bw); inside [lo, hi] the slot is inactive (no rows);
@@ -112,6 +233,10 @@ __global__ void proj_rows_kernel(SparseArgs a) {
   const int64_t s = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   if (s >= a.nproj) return;
   const int64_t p = a.pplist[s];
+  if (a.pgc && a.pgc[(int64_t)PGC_DOUBLES * s] != 0.0) {  // universal / prismatic rows (R17)
+    gen_rows(a, (int)s, p);
+    return;
+  }
   double R[9];
   body_R(a, a.pa[p], R);
   double* w = a.pw + 6 * s;
@@ -172,6 +297,24 @@ __global__ void sparse_rhs_kernel(SparseArgs a) {
   const int64_t ld = a.b.ld;
   for (int64_t p = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; p < a.np; p += (int64_t)gridDim.x * blockDim.x) {
     double r[3] = {0, 0, 0};
+    const int gs = gen_slot(a, p);
+    if (gs >= 0) {  // general rows: c0 + J δq̃ (linearised at the iterate)
+      for (int e = 0; e < a.pnr[gs]; ++e) {
+        r[e] = a.pg[(int64_t)PG_DOUBLES * gs + 36 + e];
+        for (int side = 0; side < 2; ++side) {
+          const int64_t j = side == 0 ? a.pa[p] : a.pb[p];
+          if (j < 0) continue;
+          double w[12], d[12];
+          gen_row_world(a, p, gs, e, side, w);
+#pragma unroll
+          for (int c = 0; c < 12; ++c) d[c] = a.dqt[c * ld + j];
+          r[e] += dot12(w, d);
+        }
+      }
+#pragma unroll
+      for (int e = 0; e < 3; ++e) a.rhs[e * a.np + p] = r[e];
+      continue;
+    }
     for (int side = 0; side < 2; ++side) {
       const int64_t j = side == 0 ? a.pa[p] : a.pb[p];
       const double* y = a.py + 6 * p + 3 * side;
@@ -205,6 +348,18 @@ __device__ __forceinline__ void body_apply(const SparseArgs& a, int64_t j, const
     const int32_t e = a.inc[i];
     const int64_t p = e >> 1;
     const int side = e & 1;
+    const int gs = gen_slot(a, p);
+    if (gs >= 0) {  // general rows: g += x_e J_e (body frame)
+      for (int r = 0; r < a.pnr[gs]; ++r) {
+        double wr[12], wb[12];
+        gen_row_world(a, p, gs, r, side, wr);
+        to_body12(R, wr, wb);
+        const double xe = x[r * a.np + p];
+#pragma unroll
+        for (int c = 0; c < 12; ++c) g[c] += xe * wb[c];
+      }
+      continue;
+    }
     double w[3], wl[3];
 #pragma unroll
     for (int c = 0; c < 3; ++c) w[c] = x[c * a.np + p];
@@ -236,6 +391,25 @@ __global__ void mv_point_kernel(SparseArgs a) {
   double mres = 0.0, mrhs = 0.0;
   for (int64_t p = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; p < a.np; p += (int64_t)gridDim.x * blockDim.x) {
     double s[3] = {0, 0, 0};
+    const int gs = gen_slot(a, p);
+    if (gs >= 0) {  // general rows: J V; dummy rows S = 1
+      const int nr = a.pnr[gs];
+      for (int e = 0; e < 3; ++e) {
+        if (e >= nr) {
+          s[e] = a.lam[e * a.np + p];
+          continue;
+        }
+        for (int side = 0; side < 2; ++side) {
+          const int64_t j = side == 0 ? a.pa[p] : a.pb[p];
+          if (j < 0) continue;
+          double w[12], v[12];
+          gen_row_world(a, p, gs, e, side, w);
+#pragma unroll
+          for (int c = 0; c < 12; ++c) v[c] = a.vv[c * a.n + j];
+          s[e] += dot12(w, v);
+        }
+      }
+    } else {
     for (int side = 0; side < 2; ++side) {
       const int64_t j = side == 0 ? a.pa[p] : a.pb[p];
       if (j < 0) continue;
@@ -250,6 +424,7 @@ __global__ void mv_point_kernel(SparseArgs a) {
       project_rows(a, p, s);
       const int nr = a.pnr[a.pslot[p]];
       for (int e = nr; e < 3; ++e) s[e] = a.lam[e * a.np + p];
+    }
     }
 #pragma unroll
     for (int e = 0; e < 3; ++e) {
@@ -328,6 +503,37 @@ __global__ void mf_assemble_kernel(SparseArgs a) {
     const int node = m.ablk[3 * b], rb = m.ablk[3 * b + 1], cb = m.ablk[3 * b + 2];
     double S[9] = {0, 0, 0, 0, 0, 0, 0, 0, 0};
     int prow = -1, pcol = -1;
+    if (m.acoff[b] < m.acoff[b + 1]) {
+      prow = m.acon[2 * m.acoff[b]] >> 1;
+      pcol = m.acon[2 * m.acoff[b] + 1] >> 1;
+    }
+    if (prow >= 0 && (gen_slot(a, prow) >= 0 || gen_slot(a, pcol) >= 0)) {  // general rows: J_r H⁻¹ J_cᵀ by rows
+      for (int c = m.acoff[b]; c < m.acoff[b + 1]; ++c) {
+        const int re = m.acon[2 * c], ce = m.acon[2 * c + 1];
+        const int sr = re & 1, sc = ce & 1;
+        const int64_t j = sr == 0 ? a.pa[prow] : a.pb[prow];
+        double R[9];
+        body_R(a, j, R);
+        HinvBlk H;
+        body_hinv(a, j, H);
+        double u[3][12];
+        for (int f = 0; f < 3; ++f) {
+          double cv[12];
+          row_body(a, pcol, f, sc, R, cv);
+          hinv_apply(H, cv, u[f]);
+        }
+        for (int e = 0; e < 3; ++e) {
+          double rv[12];
+          row_body(a, prow, e, sr, R, rv);
+          for (int f = 0; f < 3; ++f) S[3 * e + f] += dot12(rv, u[f]);
+        }
+      }
+      if (prow == pcol) {
+        const int sl = a.pslot[prow];
+        if (sl >= 0)
+          for (int e = a.pnr[sl]; e < 3; ++e) S[4 * e] = 1.0;  // dummy rows: S = 1, decoupled
+      }
+    } else {
     for (int c = m.acoff[b]; c < m.acoff[b + 1]; ++c) {
       const int re = m.acon[2 * c], ce = m.acon[2 * c + 1];
       const int pr = re >> 1, sr = re & 1, pc = ce >> 1, sc = ce & 1;
@@ -358,6 +564,7 @@ __global__ void mf_assemble_kernel(SparseArgs a) {
         for (int r = 0; r < 3; ++r) project_rows(a, pcol, S + 3 * r);
       if (pjr && prow == pcol)
         for (int e = a.pnr[a.pslot[prow]]; e < 3; ++e) S[4 * e] = 1.0;  // dummy rows: S = 1, decoupled
+    }
     }
     double* F = m.F + m.foff[node];
     const int64_t f = m.fdim[node];
@@ -1824,11 +2031,58 @@ bool sparse_build(const mabd_bodies* B, const mabd_joints* J, Plan* p, std::vect
   s.pdr.clear();
   s.pplist.clear();
   s.plim.clear();
+  s.pgc.clear();
   if (J->kind) {
     s.pslot.assign(P, -1);
     int64_t p0 = 0;
     std::vector<int64_t> lim_joint;
+    bool any_general = false;
+    // a general slot (universal / prismatic rows, R17) at point `pt` with rows {type, d, e}
+    auto general = [&](int64_t pt, std::initializer_list<std::array<double, 7>> rows) {
+      s.pslot[pt] = (int32_t)s.pplist.size();
+      s.pplist.push_back((int32_t)pt);
+      for (int e = 0; e < 6; ++e) s.pdr.push_back(0.0);
+      for (int e = 0; e < LIM_DOUBLES; ++e) s.plim.push_back(0.0);
+      std::vector<double> rec(PGC_DOUBLES, 0.0);
+      int i = 0;
+      for (const auto& r : rows) {
+        for (int e = 0; e < 7; ++e) rec[PGC_ROW * i + e] = r[e];
+        ++i;
+      }
+      s.pgc.insert(s.pgc.end(), rec.begin(), rec.end());
+      any_general = true;
+    };
+    auto sub = [](const double* x, const double* y, double* o) {
+      for (int e = 0; e < 3; ++e) o[e] = x[e] - y[e];
+    };
     for (int64_t k = 0; k < K; ++k) {
+      if (J->kind[k] == 2 || J->kind[k] == 3) {
+        const double *ya = J->ybar_a + 3 * p0, *yb = J->ybar_b + 3 * p0;
+        double ax[3], e1[3];
+        sub(ya + 3, ya, ax);
+        sub(yb + 3, yb, e1);
+        const double nrm = std::sqrt(ax[0] * ax[0] + ax[1] * ax[1] + ax[2] * ax[2]);
+        if (!(nrm > 0) || !(e1[0] * e1[0] + e1[1] * e1[1] + e1[2] * e1[2] > 0))
+          return *msg = "universal / prismatic joint with coincident axis points", false;
+        for (double& v : ax) v /= nrm;
+        if (J->kind[k] == 2) {  // the centre stays a ball; the second point: (A_a â₁)·(A_b e₂)
+          general(p0 + 1, {{2.0, ax[0], ax[1], ax[2], e1[0], e1[1], e1[2]}});
+        } else {                // prismatic: x̂, ẑ point rows; parallel axes; no twist
+          double dR[3][3], ua[3], u[3];
+          hinge_frame(ax, dR);
+          sub(ya + 6, ya, ua);
+          sub(yb + 6, yb, u);
+          const double nu = std::sqrt(ua[0] * ua[0] + ua[1] * ua[1] + ua[2] * ua[2]);
+          if (!(nu > 0)) return *msg = "prismatic joint with a coincident third point", false;
+          for (double& v : ua) v /= nu;
+          const double n[3] = {ax[1] * ua[2] - ax[2] * ua[1], ax[2] * ua[0] - ax[0] * ua[2],
+                               ax[0] * ua[1] - ax[1] * ua[0]};
+          general(p0, {{1.0, dR[0][0], dR[0][1], dR[0][2], 0, 0, 0}, {1.0, dR[2][0], dR[2][1], dR[2][2], 0, 0, 0}});
+          general(p0 + 1, {{2.0, dR[0][0], dR[0][1], dR[0][2], e1[0], e1[1], e1[2]},
+                           {2.0, dR[2][0], dR[2][1], dR[2][2], e1[0], e1[1], e1[2]}});
+          general(p0 + 2, {{2.0, n[0], n[1], n[2], u[0], u[1], u[2]}});
+        }
+      }
       if (J->kind[k] == 1) {
         const double* y0 = J->ybar_a + 3 * p0;
         double ax[3] = {y0[3] - y0[0], y0[4] - y0[1], y0[5] - y0[2]};
@@ -1842,6 +2096,7 @@ bool sparse_build(const mabd_bodies* B, const mabd_joints* J, Plan* p, std::vect
         for (int i : {0, 2})
           for (int c = 0; c < 3; ++c) s.pdr.push_back(dR[i][c]);
         for (int e = 0; e < LIM_DOUBLES; ++e) s.plim.push_back(0.0);
+        s.pgc.insert(s.pgc.end(), PGC_DOUBLES, 0.0);
         const double* L = J->limits ? J->limits + 8 * k : nullptr;
         if (L && (std::isfinite(L[0]) || std::isfinite(L[1]))) {
           if (!(L[0] < L[1])) return *msg = "joint limits need lo < hi", false;
@@ -1864,12 +2119,14 @@ bool sparse_build(const mabd_bodies* B, const mabd_joints* J, Plan* p, std::vect
           s.pplist.push_back((int32_t)(s.pa.size() - 1));
           for (int e = 0; e < 6; ++e) s.pdr.push_back(0.0);
           s.plim.insert(s.plim.end(), rec.begin(), rec.end());
+          s.pgc.insert(s.pgc.end(), PGC_DOUBLES, 0.0);
           lim_joint.push_back(k);
         }
       }
       p0 += J->npts[k];
     }
     if (s.pplist.empty()) s.pslot.clear();
+    if (!any_general) s.pgc.clear();
     if (!lim_joint.empty()) {  // the incidence with the limit points
       const int64_t P2 = (int64_t)s.pa.size();
       std::vector<int32_t> c2(n + 1, 0);
@@ -2102,6 +2359,8 @@ void sparse_layout(Plan* p, const std::function<size_t(size_t)>& take) {
   s.o_pnr = take(sizeof(int32_t) * nz(s.pplist.size()));
   s.o_plim = take(sizeof(double) * nz(s.plim.size()));
   s.o_pplist = take(sizeof(int32_t) * nz(s.pplist.size()));
+  s.o_pgc = take(sizeof(double) * nz(s.pgc.size()));
+  s.o_pg = take(sizeof(double) * nz(s.pgc.empty() ? 0 : PG_DOUBLES * s.pplist.size()));
   s.o_gs_pts = take(sizeof(int32_t) * nz(s.gs_chain_pts.size()));
   s.o_gs_off = take(sizeof(int32_t) * nz(s.gs_chain_off.size()));
   s.o_gs_col = take(sizeof(int32_t) * nz(s.gs_color_off.size()));
@@ -2168,6 +2427,8 @@ cudaError_t sparse_upload(const Plan& p, char* ws, cudaStream_t st, DevPtrs* d) 
   A.pplist = (const int32_t*)(ws + s.o_pplist);
   A.pnr = (int32_t*)(ws + s.o_pnr);
   A.plim = (const double*)(ws + s.o_plim);
+  A.pgc = s.pgc.empty() ? nullptr : (const double*)(ws + s.o_pgc);
+  A.pg = (double*)(ws + s.o_pg);
   A.gs.chain_pts = (const int32_t*)(ws + s.o_gs_pts);
   A.gs.chain_off = (const int32_t*)(ws + s.o_gs_off);
   A.gs.color_off = (const int32_t*)(ws + s.o_gs_col);
@@ -2206,6 +2467,7 @@ cudaError_t sparse_upload(const Plan& p, char* ws, cudaStream_t st, DevPtrs* d) 
   if ((e = upv(ws, s.o_pdr, s.pdr, st))) return e;
   if ((e = upv(ws, s.o_pplist, s.pplist, st))) return e;
   if ((e = upv(ws, s.o_plim, s.plim, st))) return e;
+  if ((e = upv(ws, s.o_pgc, s.pgc, st))) return e;
   if ((e = upv(ws, s.o_gs_pts, s.gs_chain_pts, st))) return e;
   if ((e = upv(ws, s.o_gs_off, s.gs_chain_off, st))) return e;
   if ((e = upv(ws, s.o_gs_col, s.gs_color_off, st))) return e;

@@ -802,7 +802,7 @@ cudaError_t tree_init() {
 // ============================================================================ host: topology and ordering
 bool tree_build(const mabd_joints* J, int64_t n, Plan* p, std::vector<int64_t>* pos_of_body, std::string* msg) {
   for (int64_t k = 0; J->kind && k < J->n_joints; ++k)
-    if (J->kind[k] != 0) return *msg = "five-row hinges need the sparse solver", false;
+    if (J->kind[k] != 0) return *msg = "nonlinear joints (five-row hinges, universal, prismatic) need the sparse solver", false;
   const int64_t K = J->n_joints;
   // union-find over inter-body joints: a repeated connection is a cycle
   std::vector<int64_t> uf(n);

@@ -40,8 +40,9 @@ def _ws(lib, sc, solver=0, iters=1):
     from paper_2603_08079_b200.binding import _Bodies, _Joints, _Options, _ptr, _ip
     b = _Bodies(sc.n, _ptr(sc.q0), _ptr(sc.qd0), _ptr(sc.mbar), _ptr(sc.volume), _ptr(sc.youngs), _ptr(sc.poisson),
                 None, (ctypes.c_double * 3)(*sc.gravity))
+    kind = None if sc.kind is None else np.ascontiguousarray(sc.kind, dtype=np.int32)
     j = _Joints(sc.n_joints, _ptr(sc.body_a, _ip), _ptr(sc.body_b, _ip), _ptr(sc.npts, _ip), _ptr(sc.ybar_a),
-                _ptr(sc.ybar_b))
+                _ptr(sc.ybar_b), None if kind is None else _ptr(kind, _ip))
     o = _Options(iters, 1, solver, 0, 1, None, None, 0, None, 0)
     n = ctypes.c_size_t()
     st = lib.mabd_workspace_size(ctypes.byref(b), ctypes.byref(j), ctypes.byref(o), ctypes.byref(n))
@@ -201,3 +202,21 @@ def test_line_gs_chain_cover(lib, maker):
         lengths = np.diff(off)
         # rows / columns of 32 bodies are 31-joint chains (33 with the corner pins at both ends of a border row)
         assert np.sum(lengths >= 31) == 64 and lengths.max() <= 33 and len(col) - 1 <= 6
+
+
+def test_joint_kinds_validation(lib):
+    """joints.kind (R13, R17): universal (2) needs npts = 2, prismatic (3) npts = 3, other kinds are invalid; only
+    the sparse solver takes kinds 1-3 (auto picks it; the tree and line Gauss-Seidel solvers refuse)."""
+    sc = G.nonlinear_joints(G.random_tree(20, seed=4, hinge_frac=1.0), seed=5)
+    assert set(np.unique(sc.kind)) >= {2, 3}
+    assert _ws(lib, sc)[0] == 0
+    st, _, msg = _ws(lib, sc, solver=2)
+    assert st == 1 and "sparse" in msg
+    assert _ws(lib, sc, solver=4)[0] == 1
+    bad = sc.copy()
+    bad.kind = bad.kind.copy()
+    bad.kind[np.nonzero(sc.kind == 2)[0][0]] = 3      # prismatic with 2 points
+    assert _ws(lib, bad)[0] == 1
+    bad.kind = sc.kind.copy()
+    bad.kind[0] = 4
+    assert _ws(lib, bad)[0] == 1
