@@ -655,30 +655,60 @@ __global__ void __launch_bounds__(CT, MABD_CHAIN_CTAS) chain_kernel(ChainArgs a)
 #pragma unroll
           for (int e = 0; e < 3; ++e) sx[6 + e] = x[e];
         }
-        double P[9], F[6], yR[3], yL[3];
-        if (eq_real) {  // D_t += R P(ȳ_R, ȳ_R) Rᵀ
+        double P[9], F[6], yR[3] = {0, 0, 0}, yL[3] = {0, 0, 0};
+        if (eq_real) {
           const double* gp = a.geo + 6 * (size_t)slot_geo(inf);
 #pragma unroll
           for (int e = 0; e < 3; ++e) yR[e] = __ldg(gp + 3 + e);
-          pblock(H, yR, yR, P);
-          rot_conj_sym(R, P, F);
-#pragma unroll
-          for (int e = 0; e < 6; ++e) sd[e] = F[e];
         }
-        if (right_real) {  // D_{t+1} += R P(ȳ_L, ȳ_L) Rᵀ
+        if (right_real) {
           const double* gp = a.geo + 6 * (size_t)slot_geo(infN);
 #pragma unroll
           for (int e = 0; e < 3; ++e) yL[e] = __ldg(gp + e);
-          pblock(H, yL, yL, P);
-          rot_conj_sym(R, P, F);
+        }
+        const int ax = common_axis(point_axis(yR), point_axis(yL));
+        if (ax >= 0) {  // both points on one principal axis (R18): every block is tinv I + s R Q_k Rᵀ
+          double Mq[6];
+          axis_kernel_rot(H, R, ax, Mq);
+          const double yr = yR[0] + yR[1] + yR[2], yl = yL[0] + yL[1] + yL[2];  // the on-axis components
+          const double ti = H.tinv;
+          if (eq_real) {
+            const double s2 = yr * yr;
+            sd[0] = fma(s2, Mq[0], ti); sd[1] = s2 * Mq[1]; sd[2] = s2 * Mq[2];
+            sd[3] = fma(s2, Mq[3], ti); sd[4] = s2 * Mq[4]; sd[5] = fma(s2, Mq[5], ti);
+          }
+          if (right_real) {
+            const double s2 = yl * yl;
+            sx[0] = fma(s2, Mq[0], ti); sx[1] = s2 * Mq[1]; sx[2] = s2 * Mq[2];
+            sx[3] = fma(s2, Mq[3], ti); sx[4] = s2 * Mq[4]; sx[5] = fma(s2, Mq[5], ti);
+            if (eq_real) {  // B_t = −R P(ȳ_R, ȳ_L') Rᵀ (symmetric here)
+              const double s = -(yr * yl);
+              const double b0 = fma(s, Mq[0], -ti), b1 = s * Mq[1], b2 = s * Mq[2];
+              const double b3 = fma(s, Mq[3], -ti), b4 = s * Mq[4], b5 = fma(s, Mq[5], -ti);
+              sb[0] = b0; sb[1] = b1; sb[2] = b2;
+              sb[3] = b1; sb[4] = b3; sb[5] = b4;
+              sb[6] = b2; sb[7] = b4; sb[8] = b5;
+            }
+          }
+        } else {
+          if (eq_real) {  // D_t += R P(ȳ_R, ȳ_R) Rᵀ
+            pblock(H, yR, yR, P);
+            rot_conj_sym(R, P, F);
 #pragma unroll
-          for (int e = 0; e < 6; ++e) sx[e] = F[e];
-          if (eq_real) {  // B_t = −R P(ȳ_R, ȳ_L') Rᵀ  (signs −·+)
-            double Fb[9];
-            pblock(H, yR, yL, P);
-            rot_conj(R, P, Fb);
+            for (int e = 0; e < 6; ++e) sd[e] = F[e];
+          }
+          if (right_real) {  // D_{t+1} += R P(ȳ_L, ȳ_L) Rᵀ
+            pblock(H, yL, yL, P);
+            rot_conj_sym(R, P, F);
 #pragma unroll
-            for (int e = 0; e < 9; ++e) sb[e] = -Fb[e];
+            for (int e = 0; e < 6; ++e) sx[e] = F[e];
+            if (eq_real) {  // B_t = −R P(ȳ_R, ȳ_L') Rᵀ  (signs −·+)
+              double Fb[9];
+              pblock(H, yR, yL, P);
+              rot_conj(R, P, Fb);
+#pragma unroll
+              for (int e = 0; e < 9; ++e) sb[e] = -Fb[e];
+            }
           }
         }
       }
