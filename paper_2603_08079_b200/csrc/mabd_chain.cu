@@ -46,24 +46,41 @@ __device__ __forceinline__ int cr_pos(int k) {
   return (SEG - (SEG >> l)) + (k >> (l + 1));
 }
 
-// strided view of one equation's components
-struct SV {
-  double* p;
-  __device__ __forceinline__ double& operator[](int e) const { return p[e * LDS]; }
-};
-__device__ __forceinline__ SV eqD(const CRS& s, int pos) { return SV{s.D + pos}; }
-__device__ __forceinline__ SV eqB(const CRS& s, int pos) { return SV{s.B + pos}; }
-__device__ __forceinline__ SV eqBl(const CRS& s, int pos) { return SV{s.Bl + pos}; }
-__device__ __forceinline__ SV eqR(const CRS& s, int pos) { return SV{s.r + pos}; }
+// View of one equation's N components. Components are stored in pairs: components 2j, 2j+1 of the equation at
+// position p form one 16-byte word of row-pair j (a row of 2·LDS doubles), an odd last component sits in a row of
+// its own; so ldv/stv move a 3×3 block with 5 shared-memory accesses (LDS.128) instead of 9, and lanes that read
+// consecutive positions stay conflict-free.
 template <int N>
-__device__ __forceinline__ void ldv(SV v, double* x) {
+struct SV {
+  double* p;  // group base + 2·pos (pairs)
+  double* s;  // group base + (N/2)·2·LDS + pos (odd last component)
+  __device__ __forceinline__ double& operator[](int e) const {
+    return (N % 2 == 1 && e == N - 1) ? *s : p[(e >> 1) * 2 * LDS + (e & 1)];
+  }
+};
+template <int N>
+__device__ __forceinline__ SV<N> sview(double* g, int pos) {
+  return SV<N>{g + 2 * pos, g + (N / 2) * 2 * LDS + pos};
+}
+__device__ __forceinline__ SV<6> eqD(const CRS& s, int pos) { return sview<6>(s.D, pos); }
+__device__ __forceinline__ SV<9> eqB(const CRS& s, int pos) { return sview<9>(s.B, pos); }
+__device__ __forceinline__ SV<9> eqBl(const CRS& s, int pos) { return sview<9>(s.Bl, pos); }
+__device__ __forceinline__ SV<3> eqR(const CRS& s, int pos) { return sview<3>(s.r, pos); }
+template <int N>
+__device__ __forceinline__ void ldv(SV<N> v, double* x) {
 #pragma unroll
-  for (int e = 0; e < N; ++e) x[e] = v[e];
+  for (int j = 0; j < N / 2; ++j) {
+    const double2 t = *reinterpret_cast<const double2*>(v.p + j * 2 * LDS);
+    x[2 * j] = t.x;
+    x[2 * j + 1] = t.y;
+  }
+  if (N % 2 == 1) x[N - 1] = *v.s;
 }
 template <int N>
-__device__ __forceinline__ void stv(SV v, const double* x) {
+__device__ __forceinline__ void stv(SV<N> v, const double* x) {
 #pragma unroll
-  for (int e = 0; e < N; ++e) v[e] = x[e];
+  for (int j = 0; j < N / 2; ++j) *reinterpret_cast<double2*>(v.p + j * 2 * LDS) = make_double2(x[2 * j], x[2 * j + 1]);
+  if (N % 2 == 1) *v.s = x[N - 1];
 }
 
 #ifdef MABD_EXP_CLOCK
@@ -590,8 +607,10 @@ __global__ void __launch_bounds__(CT, MABD_CHAIN_CTAS) chain_kernel(ChainArgs a)
       const bool eq_real = slot_real(inf);
       const bool right_real = slot_real(infN) && slot_left(infN) == SIDE_BODY;
       const int pt = cr_pos(t);
-      const SV sd = eqD(s, pt), sr = eqR(s, pt), sb = eqB(s, pt);
-      const SV sx = eqBl(s, cr_pos(t + 1));  // scratch row: body t's contribution to equation t+1
+      const auto sd = eqD(s, pt);
+      const auto sr = eqR(s, pt);
+      const auto sb = eqB(s, pt);
+      const auto sx = eqBl(s, cr_pos(t + 1));  // scratch row: body t's contribution to equation t+1
       {
         const double one = eq_real ? 0.0 : 1.0;  // not a constraint: decoupled identity equation, λ = 0
         sd[0] = one; sd[1] = 0; sd[2] = 0; sd[3] = one; sd[4] = 0; sd[5] = one;
@@ -666,7 +685,7 @@ __global__ void __launch_bounds__(CT, MABD_CHAIN_CTAS) chain_kernel(ChainArgs a)
 #pragma unroll
           for (int e = 0; e < 3; ++e) yL[e] = __ldg(gp + e);
         }
-        const int ax = common_axis(point_axis(yR), point_axis(yL));
+        const int ax = LP ? -1 : common_axis(point_axis(yR), point_axis(yL));
         if (ax >= 0) {  // both points on one principal axis (R18): every block is tinv I + s R Q_k Rᵀ
           double Mq[6];
           axis_kernel_rot(H, R, ax, Mq);
@@ -725,7 +744,9 @@ __global__ void __launch_bounds__(CT, MABD_CHAIN_CTAS) chain_kernel(ChainArgs a)
       const uint32_t inf = b ? info1 : info0;
       if (t > 0 && slot_real(inf) && slot_left(inf) == SIDE_BODY) {
         const int pt = cr_pos(t);
-        const SV x = eqBl(s, pt), d = eqD(s, pt), r = eqR(s, pt);
+        const auto x = eqBl(s, pt);
+        const auto d = eqD(s, pt);
+        const auto r = eqR(s, pt);
 #pragma unroll
         for (int e = 0; e < 6; ++e) d[e] += x[e];
 #pragma unroll
@@ -735,7 +756,7 @@ __global__ void __launch_bounds__(CT, MABD_CHAIN_CTAS) chain_kernel(ChainArgs a)
     }
     if (tid == CT - 1) {  // equation 256: next segment's first slot (partial) or padding
       const bool real = (flags & SEG_RIGHT_IFACE) != 0;
-      const SV x = eqBl(s, SEG);
+      const auto x = eqBl(s, SEG);
       double D[6], r[3];
 #pragma unroll
       for (int e = 0; e < 6; ++e) D[e] = real ? x[e] : ((e == 0 || e == 3 || e == 5) ? 1.0 : 0.0);
