@@ -124,7 +124,9 @@ __device__ __forceinline__ int elim_pos_rt(int L, int e) { return (SEG - (SEG >>
 
 // update of the surviving equation kq = 2^{L+1}·m at stride ST = 2^L (both neighbours already hold D⁻¹).
 // The level is a runtime argument: one copy of this code serves every level (instruction-cache footprint).
-__device__ __forceinline__ void cr_update_rt(const CRS& s, int L, int m) {
+// inv: kq is eliminated at the next level, so its new D is inverted here (in registers, no reload)
+__device__ __forceinline__ void cr_update_rt(const CRS& s, int L, int m, bool inv = false,
+                                             const StepConsts* ks = nullptr) {
   const int ST = 1 << L;
   const int kq = 2 * ST * m;
   const int pk = cr_pos(kq);
@@ -179,7 +181,13 @@ __device__ __forceinline__ void cr_update_rt(const CRS& s, int L, int m) {
     stv<9>(eqBl(s, pj), Br);  // j's left coupling at this level (Bl_j = Br_kᵀ), kept for back substitution
   }
   const double Dn[6] = {D[0], D[1], D[2], D[4], D[5], D[8]};
-  stv<6>(eqD(s, pk), Dn);
+  if (inv) {
+    double Di[6];
+    if (!sym_inv_spd(Dn, Di)) report(*ks, ERR_SINGULAR);
+    stv<6>(eqD(s, pk), Di);
+  } else {
+    stv<6>(eqD(s, pk), Dn);
+  }
   stv<9>(eqB(s, pk), nBr);
   stv<3>(eqR(s, pk), r);
 }
@@ -207,8 +215,7 @@ __device__ __forceinline__ void cr_level_fwd_rt(const CRS& s, int L, int first, 
   const int NE = SEG >> (L + 1);
   const int last = end ? NE : NE - 1;
   for (int m = first; m <= last; m += step) {
-    cr_update_rt(s, L, m);
-    if ((m & 1) && (2 << L) < SEG) cr_invert_at(s, elim_pos_rt(L + 1, m >> 1), k);
+    cr_update_rt(s, L, m, (m & 1) && (2 << L) < SEG, &k);
   }
 }
 template <int L>
@@ -742,17 +749,27 @@ __global__ void __launch_bounds__(CT, MABD_CHAIN_CTAS) chain_kernel(ChainArgs a)
     for (int b = 0; b < 2; ++b) {
       const int t = tid + b * CT;
       const uint32_t inf = b ? info1 : info0;
-      if (t > 0 && slot_real(inf) && slot_left(inf) == SIDE_BODY) {
-        const int pt = cr_pos(t);
-        const auto x = eqBl(s, pt);
-        const auto d = eqD(s, pt);
-        const auto r = eqR(s, pt);
+      const int pt = cr_pos(t);
+      if (t > 0 && slot_real(inf) && slot_left(inf) == SIDE_BODY) {  // + the left body's part, and invert if odd
+        double x[9], D[6], r[3];
+        ldv<9>(eqBl(s, pt), x);
+        ldv<6>(eqD(s, pt), D);
+        ldv<3>(eqR(s, pt), r);
 #pragma unroll
-        for (int e = 0; e < 6; ++e) d[e] += x[e];
+        for (int e = 0; e < 6; ++e) D[e] += x[e];
 #pragma unroll
         for (int e = 0; e < 3; ++e) r[e] += x[6 + e];
+        stv<3>(eqR(s, pt), r);
+        if (t & 1) {  // eliminated at stride 1
+          double Di[6];
+          if (!sym_inv_spd(D, Di)) report(k, ERR_SINGULAR);
+          stv<6>(eqD(s, pt), Di);
+        } else {
+          stv<6>(eqD(s, pt), D);
+        }
+      } else if (t & 1) {
+        cr_invert_at(s, pt, k);  // eliminated at stride 1
       }
-      if (t & 1) cr_invert(s, t, k);  // eliminated at stride 1
     }
     if (tid == CT - 1) {  // equation 256: next segment's first slot (partial) or padding
       const bool real = (flags & SEG_RIGHT_IFACE) != 0;
