@@ -577,24 +577,36 @@ __global__ void __launch_bounds__(CT, MABD_CHAIN_CTAS) chain_kernel(ChainArgs a)
     {
       const uint32_t* sinfo = reinterpret_cast<const uint32_t*>(smem + 24 * LDS);
       const int32_t* smid = reinterpret_cast<const int32_t*>(smem + 26 * LDS);
-      info0 = sinfo[tid];
-      infoN0 = sinfo[tid + 1];
-      info1 = sinfo[tid + CT];
-      infoN1 = sinfo[tid + CT + 1];
-      msc0 = a.b.mscale ? smem[25 * LDS + tid] : 1.0;
-      msc1 = a.b.mscale ? smem[25 * LDS + tid + CT] : 1.0;
-      mid0 = a.b.mat_id ? smid[tid] : 0;
-      mid1 = a.b.mat_id ? smid[tid + CT] : 0;
+      const int t0 = 2 * tid;  // this thread's slots t0, t0 + 1 (adjacent: one 16-byte word per staged row)
+      info0 = sinfo[t0];
+      infoN0 = sinfo[t0 + 1];
+      info1 = infoN0;
+      infoN1 = sinfo[t0 + 2];
+      if (a.b.mscale) {
+        const double2 m2 = *reinterpret_cast<const double2*>(smem + 25 * LDS + t0);
+        msc0 = m2.x;
+        msc1 = m2.y;
+      } else {
+        msc0 = msc1 = 1.0;
+      }
+      if (a.b.mat_id) {
+        const int2 i2 = *reinterpret_cast<const int2*>(smid + t0);
+        mid0 = i2.x;
+        mid1 = i2.y;
+      } else {
+        mid0 = mid1 = 0;
+      }
 #pragma unroll
-      for (int b = 0; b < 2; ++b) {
-        const int t = tid + b * CT;
-        double v[12];
+      for (int h = 0; h < 2; ++h) {  // qⁿ rows, then q̇ⁿ rows
+        double v0[12], v1[12];
 #pragma unroll
-        for (int r = 0; r < 12; ++r) v[r] = smem[r * LDS + t];
-        tm_st12(tbase + 48 * b, v);
-#pragma unroll
-        for (int r = 0; r < 12; ++r) v[r] = smem[(12 + r) * LDS + t];
-        tm_st12(tbase + 48 * b + 24, v);
+        for (int r = 0; r < 12; ++r) {
+          const double2 w = *reinterpret_cast<const double2*>(smem + (12 * h + r) * LDS + t0);
+          v0[r] = w.x;
+          v1[r] = w.y;
+        }
+        tm_st12(tbase + 24 * h, v0);
+        tm_st12(tbase + 48 + 24 * h, v1);
       }
     }
     tm_wait_st();
@@ -603,10 +615,11 @@ __global__ void __launch_bounds__(CT, MABD_CHAIN_CTAS) chain_kernel(ChainArgs a)
 
     // ---------------- phase 1b: per body predict + joint contributions
     // Equation t is assembled in place: D part of body t, rhs part, B_t; body t's contribution to equation
-    // t+1 goes to the scratch row Bl[t+1] and is added after the barrier.
+    // t+1 goes to the scratch row Bl[t+1]. The odd equation t0 + 1 has both bodies in this thread: it is completed
+    // and inverted here; the even one t0 takes the left neighbour's part after the barrier.
 #pragma unroll 1
     for (int b = 0; b < 2; ++b) {
-      const int t = tid + b * CT;
+      const int t = 2 * tid + b;
       const uint32_t inf = b ? info1 : info0, infN = b ? infoN1 : infoN0;
       const double msb = b ? msc1 : msc0;
       const int mdb = b ? mid1 : mid0;
@@ -739,19 +752,10 @@ __global__ void __launch_bounds__(CT, MABD_CHAIN_CTAS) chain_kernel(ChainArgs a)
         }
       }
     }
-    tm_wait_st();
-    PH_MARK(0);
-    __syncthreads();
-    PH_MARK(1);
-    // add the left neighbour's contribution (equation 0's left body lies in the previous segment: its part of
-    // the interface equation is added by that segment's REDUCE output)
-#pragma unroll
-    for (int b = 0; b < 2; ++b) {
-      const int t = tid + b * CT;
-      const uint32_t inf = b ? info1 : info0;
-      const int pt = cr_pos(t);
-      if (t > 0 && slot_real(inf) && slot_left(inf) == SIDE_BODY) {  // + the left body's part, and invert if odd
-        double x[9], D[6], r[3];
+    {  // equation t0 + 1 (odd: eliminated at stride 1): + body t0's part, then D⁻¹
+      const int pt = cr_pos(2 * tid + 1);
+      if (slot_real(info1) && slot_left(info1) == SIDE_BODY) {
+        double x[9], D[6], r[3], Di[6];
         ldv<9>(eqBl(s, pt), x);
         ldv<6>(eqD(s, pt), D);
         ldv<3>(eqR(s, pt), r);
@@ -760,15 +764,32 @@ __global__ void __launch_bounds__(CT, MABD_CHAIN_CTAS) chain_kernel(ChainArgs a)
 #pragma unroll
         for (int e = 0; e < 3; ++e) r[e] += x[6 + e];
         stv<3>(eqR(s, pt), r);
-        if (t & 1) {  // eliminated at stride 1
-          double Di[6];
-          if (!sym_inv_spd(D, Di)) report(k, ERR_SINGULAR);
-          stv<6>(eqD(s, pt), Di);
-        } else {
-          stv<6>(eqD(s, pt), D);
-        }
-      } else if (t & 1) {
-        cr_invert_at(s, pt, k);  // eliminated at stride 1
+        if (!sym_inv_spd(D, Di)) report(k, ERR_SINGULAR);
+        stv<6>(eqD(s, pt), Di);
+      } else {
+        cr_invert_at(s, pt, k);
+      }
+    }
+    tm_wait_st();
+    PH_MARK(0);
+    __syncthreads();
+    PH_MARK(1);
+    // add the left neighbour's contribution to the even equation t0 (equation 0's left body lies in the previous
+    // segment: its part of the interface equation is added by that segment's REDUCE output)
+    {
+      const int t = 2 * tid;
+      if (t > 0 && slot_real(info0) && slot_left(info0) == SIDE_BODY) {
+        const int pt = cr_pos(t);
+        double x[9], D[6], r[3];
+        ldv<9>(eqBl(s, pt), x);
+        ldv<6>(eqD(s, pt), D);
+        ldv<3>(eqR(s, pt), r);
+#pragma unroll
+        for (int e = 0; e < 6; ++e) D[e] += x[e];
+#pragma unroll
+        for (int e = 0; e < 3; ++e) r[e] += x[6 + e];
+        stv<6>(eqD(s, pt), D);
+        stv<3>(eqR(s, pt), r);
       }
     }
     if (tid == CT - 1) {  // equation 256: next segment's first slot (partial) or padding
@@ -833,7 +854,7 @@ __global__ void __launch_bounds__(CT, MABD_CHAIN_CTAS) chain_kernel(ChainArgs a)
     // ---------------- phase 3: qⁿ⁺¹ = q̃ − diag₄(R) H̄⁻¹ Σ ±Γ(ȳ)ᵀ Rᵀλ
 #pragma unroll 1
     for (int b = 0; b < 2; ++b) {
-      const int t = tid + b * CT;
+      const int t = 2 * tid + b;
       const int64_t slot = base + t;
       const uint32_t inf = b ? info1 : info0, infN = b ? infoN1 : infoN0;
       const double msb = b ? msc1 : msc0;
@@ -901,12 +922,28 @@ __global__ void __launch_bounds__(CT, MABD_CHAIN_CTAS) chain_kernel(ChainArgs a)
 #pragma unroll
           for (int e = 0; e < 3; ++e) dq[3 * kb + e] = dqt[3 * kb + e] - c3[e];
         }
+        const bool pair = slot_right(info0) == SIDE_BODY && slot_right(info1) == SIDE_BODY;
+        if (k.niter == 1 && pair && b == 0) {  // stash slot t0's results (dead CR rows, this thread's column)
 #pragma unroll
-        for (int r = 0; r < 12; ++r) __stcs(qb + r * a.b.ld, q[r] + dq[r]);
-        if (k.niter == 1) {  // uniform branch outside the store loops (no if-converted second path)
+          for (int r = 0; r < 12; ++r) {
+            smem[r * LDS + t] = q[r] + dq[r];
+            smem[(12 + r) * LDS + t] = dq[r] * k.ih;
+          }
+        } else if (k.niter == 1 && pair) {  // slots t0, t0 + 1 as one 16-byte store per row
+#pragma unroll
+          for (int r = 0; r < 12; ++r) {
+            __stcs(reinterpret_cast<double2*>(qb - 1 + r * a.b.ld), make_double2(smem[r * LDS + t - 1], q[r] + dq[r]));
+            __stcs(reinterpret_cast<double2*>(qdb - 1 + r * a.b.ld),
+                   make_double2(smem[(12 + r) * LDS + t - 1], dq[r] * k.ih));
+          }
+        } else if (k.niter == 1) {  // uniform branch outside the store loops (no if-converted second path)
+#pragma unroll
+          for (int r = 0; r < 12; ++r) __stcs(qb + r * a.b.ld, q[r] + dq[r]);
 #pragma unroll
           for (int r = 0; r < 12; ++r) __stcs(qdb + r * a.b.ld, dq[r] * k.ih);
-        } else {  // K > 1: v ← v − δq/h + h·grav (launch_step in mabd_plan.cu)
+        } else {
+#pragma unroll
+          for (int r = 0; r < 12; ++r) __stcs(qb + r * a.b.ld, q[r] + dq[r]);  // K > 1: v ← v − δq/h + h·grav (launch_step in mabd_plan.cu)
 #pragma unroll
           for (int r = 0; r < 12; ++r)
             qdb[r * a.b.ld] = qdb[r * a.b.ld] - dq[r] * k.ih + (r >= 9 ? k.h * k.grav[r - 9] : 0.0);
