@@ -125,16 +125,25 @@ __device__ __forceinline__ int elim_pos_rt(int L, int e) { return (SEG - (SEG >>
 // update of the surviving equation kq = 2^{L+1}·m at stride ST = 2^L (both neighbours already hold D⁻¹).
 // The level is a runtime argument: one copy of this code serves every level (instruction-cache footprint).
 // inv: kq is eliminated at the next level, so its new D is inverted here (in registers, no reload)
+// add: kq's equation still lacks its left body's part, parked in its Bl row (chain phase 1): added first
 __device__ __forceinline__ void cr_update_rt(const CRS& s, int L, int m, bool inv = false,
-                                             const StepConsts* ks = nullptr) {
+                                             const StepConsts* ks = nullptr, bool add = false) {
   const int ST = 1 << L;
   const int kq = 2 * ST * m;
   const int pk = cr_pos(kq);
   double Ds[6], D[9], Br[9], r[3];
   ldv<6>(eqD(s, pk), Ds);
-  full_from_sym(Ds, D);
   ldv<9>(eqB(s, pk), Br);
   ldv<3>(eqR(s, pk), r);
+  if (add) {
+    double x[9];
+    ldv<9>(eqBl(s, pk), x);
+#pragma unroll
+    for (int e = 0; e < 6; ++e) Ds[e] += x[e];
+#pragma unroll
+    for (int e = 0; e < 3; ++e) r[e] += x[6 + e];
+  }
+  full_from_sym(Ds, D);
   double nBr[9] = {0, 0, 0, 0, 0, 0, 0, 0, 0};
   if (m > 0) {  // left neighbour i = kq − st:  α = Br_iᵀ D_i⁻¹;  D −= α Br_i;  r −= α r_i
     const int pi = elim_pos_rt(L, m - 1);
@@ -770,29 +779,7 @@ __global__ void __launch_bounds__(CT, MABD_CHAIN_CTAS) chain_kernel(ChainArgs a)
         cr_invert_at(s, pt, k);
       }
     }
-    tm_wait_st();
-    PH_MARK(0);
-    __syncthreads();
-    PH_MARK(1);
-    // add the left neighbour's contribution to the even equation t0 (equation 0's left body lies in the previous
-    // segment: its part of the interface equation is added by that segment's REDUCE output)
-    {
-      const int t = 2 * tid;
-      if (t > 0 && slot_real(info0) && slot_left(info0) == SIDE_BODY) {
-        const int pt = cr_pos(t);
-        double x[9], D[6], r[3];
-        ldv<9>(eqBl(s, pt), x);
-        ldv<6>(eqD(s, pt), D);
-        ldv<3>(eqR(s, pt), r);
-#pragma unroll
-        for (int e = 0; e < 6; ++e) D[e] += x[e];
-#pragma unroll
-        for (int e = 0; e < 3; ++e) r[e] += x[6 + e];
-        stv<6>(eqD(s, pt), D);
-        stv<3>(eqR(s, pt), r);
-      }
-    }
-    if (tid == CT - 1) {  // equation 256: next segment's first slot (partial) or padding
+    if (tid == CT - 1) {  // equation 256 (this thread's scratch): next segment's first slot (partial) or padding
       const bool real = (flags & SEG_RIGHT_IFACE) != 0;
       const auto x = eqBl(s, SEG);
       double D[6], r[3];
@@ -805,13 +792,23 @@ __global__ void __launch_bounds__(CT, MABD_CHAIN_CTAS) chain_kernel(ChainArgs a)
       stv<9>(eqB(s, SEG), Z);
       stv<3>(eqR(s, SEG), r);
     }
+    tm_wait_st();
+    PH_MARK(0);
     __syncthreads();
+    PH_MARK(1);
 
     // ---------------- phase 2: block cyclic reduction
     PH_MARK(2);
 #ifndef MABD_EXP_SKIP_CR
     const bool right_iface = (flags & SEG_RIGHT_IFACE) != 0;
-    cr_forward_lower<CT>(s, tid, k, right_iface);
+    // stride 1: survivor 2·tid is this thread's even equation t0, completed here with its left neighbour's part
+    // (equation 0's left body lies in the previous segment: its part of the interface equation is added by that
+    // segment's REDUCE output); equation 256 (built above) is updated by thread 0 when it is an interface
+    cr_update_rt(s, 0, tid, (tid & 1) != 0, &k, tid > 0 && slot_real(info0) && slot_left(info0) == SIDE_BODY);
+    if (tid == 0 && right_iface) cr_update_rt(s, 0, SEG >> 1, false, &k);
+    __syncthreads();
+    cr_level_fwd_rt(s, 1, tid, CT, k, right_iface);
+    __syncthreads();
     PH_MARK(8);
     if (tid < 32) {  // upper levels, the 2-equation top and the upper back substitution: warp 0 alone
       cr_forward_upper(s, tid, k, right_iface);
