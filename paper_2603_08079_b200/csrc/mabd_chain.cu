@@ -839,7 +839,11 @@ __global__ void __launch_bounds__(CT, MABD_CHAIN_CTAS) chain_kernel(ChainArgs a)
       continue;
     }
     PH_MARK(4);
-    cr_backward_lower<CT>(s, tid);
+    // strides 2, 1 back; no barrier after stride 1: phase 3 of this thread reads λ of its own equations t0, t0 + 1
+    // (the odd one solved just now by this thread) and of t0 + 2 (solved at a higher level)
+    cr_level_bwd_rt(s, 1, tid, CT);
+    __syncthreads();
+    cr_level_bwd_rt(s, 0, tid, CT);
 #else
     __syncthreads();
     if (reduce_only) {
