@@ -332,29 +332,55 @@ __device__ __forceinline__ void tree_elim(const TreeArgs& a, int b, int lane, co
   // Pivot loop kept rolled (code size: every step runs the same instructions): the registers rotate by one row per
   // step so that the pivot row is always v[0]; after N steps, v[i] holds original row (i + N) mod MX, i.e.
   // rows N..M−1 (Ŝ_u / r̂_u) at v[0..nu) and rows 0..N−1 (W / y) at v[MX−N..MX).
+  // Pivots in 3×3 blocks (a joint point's rows; N is a multiple of 3): block K = rows kb..kb+2 (v[0..2] after the
+  // rotation), columns in lanes kb..kb+2. Per lane (column j): t = F_KK⁻¹ F_Kj, F_ij −= F_iK t for i ∉ K, and the
+  // block's rows become t: three scalar Gauss-Jordan steps at once, one broadcast and one reciprocal instead of three.
+  // The pivot lanes write their columns row-interleaved (row i of the three at colbuf[4i..4i+2]) so that every
+  // lane reads a row's three coefficients with one 16-byte and one 8-byte broadcast load.
   bool ok = true;
-  for (int kk = 0; kk < N; ++kk) {
-    // the pivot column (lane kk) broadcast through this warp's buffer: MX/2 vector stores by one lane and
-    // MX/2 broadcast vector loads instead of 2·MX 32-bit shuffles
-    if (lane == kk) {
+  for (int kb = 0; kb < N; kb += 3) {
+    const int pl = lane - kb;
+    if (pl >= 0 && pl < 3) {
 #pragma unroll
-      for (int i = 0; i < MX; i += 2) *reinterpret_cast<double2*>(colbuf + i) = make_double2(v[i], v[i + 1]);
+      for (int i = 0; i < MX; ++i) colbuf[4 * i + pl] = v[i];
     }
     __syncwarp();
-    double c[MX];
+    double B[9];  // F_KK, row-major: B[3a + b] = F[kb + a][kb + b]
 #pragma unroll
-    for (int i = 0; i < MX; i += 2) {
-      const double2 w = *reinterpret_cast<const double2*>(colbuf + i);
-      c[i] = w.x;
-      c[i + 1] = w.y;
+    for (int a3 = 0; a3 < 3; ++a3) {
+      const double2 w = *reinterpret_cast<const double2*>(colbuf + 4 * a3);
+      B[3 * a3] = w.x;
+      B[3 * a3 + 1] = w.y;
+      B[3 * a3 + 2] = colbuf[4 * a3 + 2];
     }
-    __syncwarp();  // every lane has the column before the next step's pivot lane overwrites it
-    const double p = c[0];
-    ok = ok && p > 0.0;
-    const double t = v[0] * fast_rcp(p > 0.0 ? p : 1.0);
+    const double C00 = B[4] * B[8] - B[5] * B[7], C01 = B[5] * B[6] - B[3] * B[8], C02 = B[3] * B[7] - B[4] * B[6];
+    const double det = B[0] * C00 + B[1] * C01 + B[2] * C02;
+    ok = ok && B[0] > 0.0 && B[0] * B[4] - B[1] * B[3] > 0.0 && det > 0.0;
+    const double id = fast_rcp(det > 0.0 ? det : 1.0);
+    // adj(B) rows: adj[a][b] = cofactor C[b][a]
+    const double C10 = B[2] * B[7] - B[1] * B[8], C11 = B[0] * B[8] - B[2] * B[6], C12 = B[1] * B[6] - B[0] * B[7];
+    const double C20 = B[1] * B[5] - B[2] * B[4], C21 = B[2] * B[3] - B[0] * B[5], C22 = B[0] * B[4] - B[1] * B[3];
+    double t0 = (C00 * v[0] + C10 * v[1] + C20 * v[2]) * id;
+    double t1 = (C01 * v[0] + C11 * v[1] + C21 * v[2]) * id;
+    double t2 = (C02 * v[0] + C12 * v[1] + C22 * v[2]) * id;
+    {  // one refinement step: the adjugate solve alone loses accuracy on stiff hinge blocks
+      const double r0 = v[0] - (B[0] * t0 + B[1] * t1 + B[2] * t2);
+      const double r1 = v[1] - (B[3] * t0 + B[4] * t1 + B[5] * t2);
+      const double r2 = v[2] - (B[6] * t0 + B[7] * t1 + B[8] * t2);
+      t0 += (C00 * r0 + C10 * r1 + C20 * r2) * id;
+      t1 += (C01 * r0 + C11 * r1 + C21 * r2) * id;
+      t2 += (C02 * r0 + C12 * r1 + C22 * r2) * id;
+    }
 #pragma unroll
-    for (int i = 1; i < MX; ++i) v[i - 1] = v[i] - c[i] * t;  // rows beyond M are zero and stay zero
-    v[MX - 1] = t;
+    for (int i = 3; i < MX; ++i) {  // rows beyond M are zero and stay zero
+      const double2 w = *reinterpret_cast<const double2*>(colbuf + 4 * i);
+      const double c2 = colbuf[4 * i + 2];
+      v[i - 3] = v[i] - (w.x * t0 + w.y * t1 + c2 * t2);
+    }
+    v[MX - 3] = t0;
+    v[MX - 2] = t1;
+    v[MX - 1] = t2;
+    __syncwarp();  // every lane has read the block before the next block's pivot lanes overwrite it
   }
   EMARK(probe && v[MX - 1] != 1e300, 43);
   if (!ok && lane == 0) treport(k, ERR_SINGULAR);
@@ -542,7 +568,7 @@ __device__ void tree_update(const TreeArgs& a, int b, const TMeta& m, const TSlo
 // per body, downward a thread per body (λ of its child joints, then stage 4).
 __global__ void __launch_bounds__(512) tree_level_kernel(TreeArgs a, int mode) {
   __shared__ TMeta sm[16];
-  __shared__ __align__(16) double colbuf[16][TREE_MAXN + 6];
+  __shared__ __align__(16) double colbuf[16][4 * (TREE_MAXN + 6)];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, nw = blockDim.x >> 5;
   const int l = a.group0;
   const TSlots none{nullptr, 0, 0};
@@ -595,7 +621,7 @@ __global__ void __launch_bounds__(TREE_THREADS, 1) tree_group_kernel(TreeArgs a,
   const int l0 = a.glev_ptr[g], l1 = a.glev_ptr[g + 1] - 1;  // levels l ∈ [l0, l1), deepest first
   const TSlots sl{tsm, g0, g1};
   TMeta* meta = reinterpret_cast<TMeta*>(tsm + (size_t)a.cap * TSLOT);
-  double* colbuf = reinterpret_cast<double*>(meta + a.cap) + (size_t)warp * (TREE_MAXN + 6);  // pivot column
+  double* colbuf = reinterpret_cast<double*>(meta + a.cap) + (size_t)warp * 4 * (TREE_MAXN + 6);  // pivot block
   TMARK(0);
   // one body per thread (a group has at most cap ≤ blockDim bodies): stages 1-2 and the leaves' condensed blocks,
   // then (after the leaves' slots are complete) the front records of the bodies with child joints
@@ -668,7 +694,7 @@ constexpr size_t TREE_SMEM_MAX = 227 * 1024;  // dynamic shared memory per CTA (
 
 // Shared memory of the group kernel: slots and metadata for cap bodies.
 size_t tree_group_smem(int cap) {
-  return (sizeof(double) * TSLOT + sizeof(TMeta)) * (size_t)cap + sizeof(double) * (TREE_MAXN + 6) * (TREE_THREADS / 32);
+  return (sizeof(double) * TSLOT + sizeof(TMeta)) * (size_t)cap + sizeof(double) * 4 * (TREE_MAXN + 6) * (TREE_THREADS / 32);
 }
 
 template <int MODE>
