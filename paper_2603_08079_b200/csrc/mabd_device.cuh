@@ -98,7 +98,7 @@ __device__ __forceinline__ bool sym_inv_spd(const double* S, double* Si) {
 // R = A (AᵀA)^{-1/2}. With E = XᵀX − I, X ← X·p(E), p the degree-6 truncation of the series of (I+E)^{-1/2}
 // (7th-order convergence: ‖E_new‖ ≈ 0.42‖E‖⁷, one step from ‖E‖ ≤ 1e-2 reaches ~1e-15; reading A5),
 // preceded by determinant-scaled Newton steps X ← ½(ζX + ζ⁻¹X⁻ᵀ) while ‖E‖_F > 0.3, and followed, when
-// 1e-2 ≤ ‖E‖_F < 0.1, by one first-order step X(I − E/2) instead of a second degree-6 step.
+// ‖E‖_F ≥ 1e-2, by one third-order step X(I − E/2 + 3E²/8 − 5E³/16) instead of a second degree-6 step.
 // A and R are row-major 3×3. Returns false for det A ≤ 1e-9 or non-finite input.
 
 // C = S T for symmetric commuting S, T (packed sym): the product is symmetric, 6 entries.
@@ -174,21 +174,29 @@ __device__ __forceinline__ bool polar_rotation(const double* A, double* R) {
     break;
 #endif
     if (e2 < 1e-4) break;  // ‖E_new‖ ≲ 0.42‖E‖⁷ < 5e-15
-    if (e2 < 1e-2) {       // ‖E_new‖ ≲ 0.42‖E‖⁷ < 5e-8: one first-order step X ← X(I − E/2) leaves (3/8)‖E‖² ≲ 1e-15
-      double G[6];
-      G[0] = 1.0 - 0.5 * (R[0] * R[0] + R[3] * R[3] + R[6] * R[6] - 1.0);
-      G[1] = -0.5 * (R[0] * R[1] + R[3] * R[4] + R[6] * R[7]);
-      G[2] = -0.5 * (R[0] * R[2] + R[3] * R[5] + R[6] * R[8]);
-      G[3] = 1.0 - 0.5 * (R[1] * R[1] + R[4] * R[4] + R[7] * R[7] - 1.0);
-      G[4] = -0.5 * (R[1] * R[2] + R[4] * R[5] + R[7] * R[8]);
-      G[5] = 1.0 - 0.5 * (R[2] * R[2] + R[5] * R[5] + R[8] * R[8] - 1.0);
+    {  // ‖E‖ ≤ 0.3: ‖E_new‖ ≲ 0.42‖E‖⁷ < 1e-4; one third-order step X ← X(I − E/2 + 3E²/8 − 5E³/16) leaves
+       // (35/128)‖E_new‖⁴ < 1e-16 (one code path for every lane of a warp, instead of a second degree-6 step for
+       // 1e-2 ≤ ‖E‖² and a first-order step below)
+      double F[6];
+      F[0] = R[0] * R[0] + R[3] * R[3] + R[6] * R[6] - 1.0;
+      F[1] = R[0] * R[1] + R[3] * R[4] + R[6] * R[7];
+      F[2] = R[0] * R[2] + R[3] * R[5] + R[6] * R[8];
+      F[3] = R[1] * R[1] + R[4] * R[4] + R[7] * R[7] - 1.0;
+      F[4] = R[1] * R[2] + R[4] * R[5] + R[7] * R[8];
+      F[5] = R[2] * R[2] + R[5] * R[5] + R[8] * R[8] - 1.0;
+#pragma unroll
+      for (int i = 0; i < 6; ++i) T[i] = (-5.0 / 16.0) * F[i];
+      T[0] += 3.0 / 8.0; T[3] += 3.0 / 8.0; T[5] += 3.0 / 8.0;
+      symsym(F, T, U);
+      U[0] -= 0.5; U[3] -= 0.5; U[5] -= 0.5;
+      symsym(F, U, T);  // −E/2 + 3E²/8 − 5E³/16
 #pragma unroll
       for (int i = 0; i < 9; ++i) X[i] = R[i];
 #pragma unroll
       for (int r = 0; r < 3; ++r) {
-        R[3 * r + 0] = X[3 * r] * G[0] + X[3 * r + 1] * G[1] + X[3 * r + 2] * G[2];
-        R[3 * r + 1] = X[3 * r] * G[1] + X[3 * r + 1] * G[3] + X[3 * r + 2] * G[4];
-        R[3 * r + 2] = X[3 * r] * G[2] + X[3 * r + 1] * G[4] + X[3 * r + 2] * G[5];
+        R[3 * r + 0] = X[3 * r] + X[3 * r] * T[0] + X[3 * r + 1] * T[1] + X[3 * r + 2] * T[2];
+        R[3 * r + 1] = X[3 * r + 1] + X[3 * r] * T[1] + X[3 * r + 1] * T[3] + X[3 * r + 2] * T[4];
+        R[3 * r + 2] = X[3 * r + 2] + X[3 * r] * T[2] + X[3 * r + 1] * T[4] + X[3 * r + 2] * T[5];
       }
       break;
     }
