@@ -268,11 +268,25 @@ def run_ours(args, rank: int, world: int, local_rank: int) -> None:
     # number is the configured workload's average, not its cheapest first K steps (the polar decomposition's cost
     # grows with the strain the episode builds up, DESIGN R4). K ≥ episode: whole episodes.
     spread = args.steps < episode
+    # config 1 (a one-warp chain scene): the library runs all steps of one mabd_step call in one launch, the state
+    # in registers, so a timed interval is one call of a whole episode, with the L2 flush before it
+    whole_calls = args.config == 1 and not spread
     with sampler:
         left = args.steps
         while left > 0:
             kk = min(episode, left)
-            if flush or spread:  # per-step intervals; the steps are enqueued without host waits
+            if flush and whole_calls:  # one mabd_step(h, kk) call per timed interval, L2 flushed before each
+                with torch.cuda.stream(stream):
+                    l2buf.zero_()
+                ev0 = torch.cuda.Event(enable_timing=True)
+                ev1 = torch.cuda.Event(enable_timing=True)
+                ev0.record(stream)
+                sim.step_async(h, kk)
+                ev1.record(stream)
+                sim.check()
+                barrier()
+                ms += ev0.elapsed_time(ev1)
+            elif flush or spread:  # per-step intervals; the steps are enqueued without host waits
                 stride = episode // kk if spread else 1
                 evs = []
                 for i in range(kk):
@@ -311,6 +325,8 @@ def run_ours(args, rank: int, world: int, local_rank: int) -> None:
     bodies_total = n if split else world * n
     value = bodies_total * args.steps / (ms * 1e-3)
     launches = info["launches_per_step"] * args.steps   # solver launches + the step_end node, per step
+    if whole_calls:  # one launch per timed call
+        launches = -(-args.steps // episode)
 
     # e2e through the public API with pinned host buffers: every step is H2D (q, q̇) → step → D2H (q, q̇). Two
     # independent problems are kept in flight (two handles, two streams, one host thread each: the binding's
@@ -409,9 +425,11 @@ def run_ours(args, rank: int, world: int, local_rank: int) -> None:
                                   "untimed)" if spread else
                                   f"{args.steps} steps as episodes of <= {episode} steps from the initial state "
                                   "(reset between episodes, outside the CUDA-event intervals)") +
-                                 "; each step replays one CUDA graph",
+                                 ("; one launch per mabd_step call (all of its steps in one one-warp kernel)"
+                                  if whole_calls else "; each step replays one CUDA graph"),
                        "dual_rows": info["n_dual_rows"],
-                       "l2": (f"flushed before every timed step (256 MiB memset outside the event interval): "
+                       "l2": (f"flushed before every timed {'call (one mabd_step of a whole episode)' if whole_calls else 'step'}"
+                              f" (256 MiB memset outside the event interval): "
                               f"per-rank state {state_b / 2**20:.1f} MiB < 126 MB L2") if flush else
                              f"no flush: per-rank state {state_b / 2**20:.0f} MiB > 126 MB L2",
                        "parallelism": PARALLELISM[args.config].format(w=world) if split

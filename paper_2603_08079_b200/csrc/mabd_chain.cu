@@ -996,6 +996,11 @@ __global__ void __launch_bounds__(32) small_chain_kernel(ChainArgs a) {
     hinv_blocks(M, msc, k.ih2, H);
   double W[9];
   const double* Wp = has_body ? load_wrench(a.b, t, W) : nullptr;
+  // a.nsteps > 1 (step_end folded, one Newton iteration): the steps of one mabd_step call run here back to back, the
+  // state staying in registers (config 1: one launch per call instead of one per step)
+  const int nst = a.nsteps > 1 ? a.nsteps : 1;
+#pragma unroll 1
+  for (int st = 0; st < nst; ++st) {
   const bool ok = k.lp ? predict_body<true>(q, qd, M, msc, H, k.ih, k.grav, R, dqt, Wp)
                        : predict_body<false>(q, qd, M, msc, H, k.ih, k.grav, R, dqt, Wp);
   if (!ok && has_body) report(k, ERR_NONFINITE);
@@ -1119,7 +1124,7 @@ __global__ void __launch_bounds__(32) small_chain_kernel(ChainArgs a) {
     if (e[0] != 0 && e[2] == INT_MAX) e[2] = e[3];
     e[3] += 1;
   }
-  if (!has_body) return;
+  if (has_body) {
   // phase 3: qⁿ⁺¹ = q̃ − diag₄(R) H̄⁻¹ Σ ±Γ(ȳ)ᵀ Rᵀλ
   double gq[12] = {0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0}, w[3], lam[3], u[12];
   if (eq_real) {
@@ -1145,8 +1150,17 @@ __global__ void __launch_bounds__(32) small_chain_kernel(ChainArgs a) {
   }
 #pragma unroll
   for (int c = 0; c < 12; ++c) {
-    a.b.q[c * a.b.ld + t] = q[c] + dq[c];
-    a.b.qd[c * a.b.ld + t] = k.niter == 1 ? dq[c] * k.ih : qd[c] - dq[c] * k.ih + (c >= 9 ? k.h * k.grav[c - 9] : 0.0);
+    q[c] += dq[c];
+    qd[c] = k.niter == 1 ? dq[c] * k.ih : qd[c] - dq[c] * k.ih + (c >= 9 ? k.h * k.grav[c - 9] : 0.0);
+  }
+  }
+  __syncwarp();  // every lane has read this step's λ before the next step's equations overwrite them
+  }
+  if (!has_body) return;
+#pragma unroll
+  for (int c = 0; c < 12; ++c) {
+    a.b.q[c * a.b.ld + t] = q[c];
+    a.b.qd[c * a.b.ld + t] = qd[c];
   }
 }
 

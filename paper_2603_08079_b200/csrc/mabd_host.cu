@@ -195,6 +195,15 @@ static mabd_status enqueue_steps(mabd_ctx* c, double h, int64_t nsteps) {
     if (st != MABD_OK) return st;
   }
   nccl_take_step_error();
+  if (c->plan.step_end_folded && nsteps > 1) {  // one-warp chain scene: all the call's steps in one launch
+    for (int64_t s0 = 0; s0 < nsteps; s0 += INT_MAX) {
+      const cudaError_t e = launch_steps_small(c->plan, c->d, h, (int32_t)std::min<int64_t>(nsteps - s0, INT_MAX),
+                                               c->stream);
+      if (e != cudaSuccess) return fail(c, MABD_ECUDA, "launch_steps_small: %s", cudaGetErrorString(e));
+    }
+    c->steps_pending += nsteps;
+    return MABD_OK;
+  }
   const bool graphs = c->use_graphs;
   if (graphs && (!c->graph || c->graph_h != h)) {
     const cudaError_t e = build_graph(c, h);

@@ -19,6 +19,7 @@ struct ChainArgs {
   Top* top_out;                // REDUCE output, indexed by seg_red
   const double* lam_in;        // FINISH input: level-2 λ [n_long][3]
   int32_t step_end;            // small_chain_kernel: also do the step_end node's bookkeeping (Plan::step_end_folded)
+  int32_t nsteps;              // small_chain_kernel with step_end: steps to run in this launch (≤ 1: one)
   StepConsts k;
 };
 

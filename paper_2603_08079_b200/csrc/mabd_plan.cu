@@ -1039,7 +1039,25 @@ __global__ void iter_final_kernel(double* qd, const double* z, int64_t ld) {
 
 static cudaError_t launch_iteration(const Plan& p, const DevPtrs& d, const StepConsts& k, cudaStream_t st);
 
-cudaError_t launch_step(const Plan& p, const DevPtrs& d, double h, int32_t step, cudaStream_t st, int phase) {
+static ChainArgs chain_args(const Plan& p, const DevPtrs& d, const StepConsts& k) {
+  ChainArgs a;
+  a.step_end = 0;
+  a.nsteps = 1;
+  a.b = d.b;
+  a.slot_info = d.slot_info;
+  a.geo = d.geo;
+  a.seg_flags = d.seg_flags;
+  a.seg_red = d.seg_red;
+  a.seg_list = nullptr;
+  a.hinv_tab = p.mscale.empty() ? d.hinv : nullptr;
+  a.n_mats = (int32_t)p.mats.size();
+  a.top_out = d.tops.empty() ? nullptr : d.tops[0];
+  a.lam_in = d.lams.empty() ? nullptr : d.lams[0];
+  a.k = k;
+  return a;
+}
+
+static StepConsts step_consts(const Plan& p, const DevPtrs& d, double h, int32_t step, int phase) {
   StepConsts k;
   k.h = h;
   k.ih = 1.0 / h;
@@ -1051,6 +1069,21 @@ cudaError_t launch_step(const Plan& p, const DevPtrs& d, double h, int32_t step,
   k.niter = std::max(1, p.newton_iters);
   k.lp = p.rotation == MABD_ROTATION_LENGTH_PRESERVING ? 1 : 0;
   k.phase = phase;
+  return k;
+}
+
+// nsteps steps of a one-warp chain scene (Plan::step_end_folded) in one launch: the state stays in the warp's
+// registers between the steps and each step does its own step_end bookkeeping.
+cudaError_t launch_steps_small(const Plan& p, const DevPtrs& d, double h, int32_t nsteps, cudaStream_t st) {
+  if (!p.step_end_folded) return cudaErrorNotSupported;
+  ChainArgs a = chain_args(p, d, step_consts(p, d, h, 0, 0));
+  a.step_end = 1;
+  a.nsteps = nsteps;
+  return launch_small_chain(a, st);
+}
+
+cudaError_t launch_step(const Plan& p, const DevPtrs& d, double h, int32_t step, cudaStream_t st, int phase) {
+  StepConsts k = step_consts(p, d, h, step, phase);
   if (k.niter == 1) return launch_iteration(p, d, k, st);
   const int64_t tot = 12 * d.b.ld;
   const unsigned grid = (unsigned)((tot + 255) / 256);
@@ -1078,19 +1111,7 @@ static cudaError_t forest_iteration(const Plan& p, const DevPtrs& d, const StepC
   if (p.solver == MABD_SOLVER_SPARSE) return sparse_step(p, d, k, st);
   if (p.solver == MABD_SOLVER_LINE_GS) return gs_step(p, d, k, st);
   if (p.solver != MABD_SOLVER_CHAIN) return cudaErrorNotSupported;
-  ChainArgs a;
-  a.step_end = 0;
-  a.b = d.b;
-  a.slot_info = d.slot_info;
-  a.geo = d.geo;
-  a.seg_flags = d.seg_flags;
-  a.seg_red = d.seg_red;
-  a.seg_list = nullptr;
-  a.hinv_tab = p.mscale.empty() ? d.hinv : nullptr;
-  a.n_mats = (int32_t)p.mats.size();
-  a.top_out = d.tops.empty() ? nullptr : d.tops[0];
-  a.lam_in = d.lams.empty() ? nullptr : d.lams[0];
-  a.k = k;
+  ChainArgs a = chain_args(p, d, k);
   if (p.n_parts > 1) return launch_step_parts(p, d, a, st);
   if (p.small_chain) {
     a.step_end = p.step_end_folded ? 1 : 0;

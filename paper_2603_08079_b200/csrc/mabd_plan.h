@@ -231,6 +231,8 @@ cudaError_t upload_plan(const Plan& p, char* ws, cudaStream_t st, DevPtrs* d);
 cudaError_t prefactor_device(const Plan& p, const DevPtrs& d, double h, cudaStream_t st);
 cudaError_t reset_err(const DevPtrs& d, cudaStream_t st);
 cudaError_t launch_step_end(const Plan& p, const DevPtrs& d, cudaStream_t st);
+// nsteps steps of a one-warp chain scene in one launch (Plan::step_end_folded only)
+cudaError_t launch_steps_small(const Plan& p, const DevPtrs& d, double h, int32_t nsteps, cudaStream_t st);
 cudaError_t loop_step(const Plan& p, const DevPtrs& d, const StepConsts& k, cudaStream_t st,
                       cudaError_t (*forest_step)(const Plan&, const DevPtrs&, const StepConsts&, cudaStream_t));
 cudaError_t launch_step(const Plan& p, const DevPtrs& d, double h, int32_t step, cudaStream_t st, int phase = 0);

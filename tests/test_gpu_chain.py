@@ -183,3 +183,24 @@ def _concat(parts):
                meta={"topology": "chain"}, **arr)
     sc.validate()
     return sc
+
+
+def test_small_chain_fused_steps_match_single_steps(cuda_ok):
+    """A one-warp chain scene runs all steps of one mabd_step call in one launch (state in registers). Its result is
+    bitwise the one of the same steps issued one call at a time (one graph replay each), and the step counter
+    that attributes errors advances by the number of steps."""
+    from paper_2603_08079_b200 import Simulator
+    sc = G.cfg1_chain8()
+    out = []
+    for calls in ((10,), (1,) * 10, (3, 7)):
+        sim = Simulator.from_scene(sc)
+        sim.prefactor(sc.h)
+        assert sim.query()["launches_per_step"] == 1
+        for n in calls:
+            sim.step(sc.h, n)
+        out.append(sim.get_state())
+        sim.close()
+    for q, qd in out[1:]:
+        assert np.array_equal(q, out[0][0]) and np.array_equal(qd, out[0][1])
+    q_o, _ = O.simulate(sc, 10)
+    assert O.rel_err(out[0][0], q_o) <= 1e-9
