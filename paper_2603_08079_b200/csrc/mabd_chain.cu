@@ -944,7 +944,8 @@ __global__ void __launch_bounds__(CT, MABD_CHAIN_CTAS) chain_kernel(ChainArgs a)
           for (int r = 0; r < 12; ++r) __stcs(qdb + r * a.b.ld, dq[r] * k.ih);
         } else {
 #pragma unroll
-          for (int r = 0; r < 12; ++r) __stcs(qb + r * a.b.ld, q[r] + dq[r]);  // K > 1: v ← v − δq/h + h·grav (launch_step in mabd_plan.cu)
+          for (int r = 0; r < 12; ++r) __stcs(qb + r * a.b.ld, q[r] + dq[r]);
+          // K > 1: v ← v − δq/h + h·grav (launch_step in mabd_plan.cu)
 #pragma unroll
           for (int r = 0; r < 12; ++r)
             qdb[r * a.b.ld] = qdb[r * a.b.ld] - dq[r] * k.ih + (r >= 9 ? k.h * k.grav[r - 9] : 0.0);
