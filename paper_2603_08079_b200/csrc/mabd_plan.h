@@ -82,7 +82,7 @@ struct SparsePlan {
     int64_t nodes, n_nodes;        // all nodes of the level (solves), into lev_nodes
     int64_t small, n_small;        // fronts factored in shared memory, into lev_nodes
     int64_t big = 0, n_big = 0;    // fronts factored by panels, into lev_nodes
-    std::vector<int64_t> fwd, n_fwd, bwd, n_bwd;  // per 64-chunk solve tasks of the big fronts
+    std::vector<int64_t> fwd, n_fwd, bwd, n_bwd;  // per MF_SG-chunk group: solve tasks of the big fronts
     int64_t bwdb = 0, n_bwdb = 0;  // backward boundary-product tasks
     int32_t max_f = 0, max_f_small = 0, max_children = 0;
     std::vector<int64_t> ea, n_ea; // per child slot: (parent, column) tasks of big parents
@@ -90,6 +90,7 @@ struct SparsePlan {
   };
   std::vector<Level> levels;
   std::vector<int32_t> lev_nodes, tasks;
+  int64_t zero = 0, n_zero = 0;                          // (node, column) tasks of the per-step front zeroing
   std::vector<int64_t> loff;                             // [nnode] inverse diagonal blocks of big fronts
   int64_t linv_doubles = 0;
   int32_t refine = 1;                                    // iterative-refinement passes per step (at most)

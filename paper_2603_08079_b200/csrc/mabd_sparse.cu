@@ -35,6 +35,10 @@ namespace mabd {
 
 constexpr int SP_THREADS = 256;
 constexpr int MF_NB = 64;          // panel width and tile size of the large-front path
+#ifndef MF_SG
+#define MF_SG 2               // 64-chunks per triangular-solve launch of the large fronts
+#endif
+constexpr int MF_ZC = 16;          // columns per CTA of the per-step lower-triangle zeroing of large fronts
 constexpr int MF_SMALL = 96;       // fronts with f ≤ MF_SMALL are factored in shared memory by one CTA
 constexpr int MF_LEAF_PTS = 12;    // nested dissection stops at regions of ≤ this many points
 constexpr int MF_REFINE = 1;       // iterative-refinement passes per step (default; each gated, see below)
@@ -496,6 +500,23 @@ __global__ void sparse_update_kernel(SparseArgs a) {
 // ============================================================================ numeric factorization
 // Assembly of the original entries: one thread per 3×3 block (row point q, column point p, both in the front of
 // the node owning p): S_qp = Σ_{shared bodies j} s_q s_p R_j P_j(ȳ_q, ȳ_p) R_jᵀ.
+// Fronts are column-major and every factorization and solve kernel reads and writes only their lower triangle
+// (rows r ≥ column c), so a step zeroes only that part: f(f+1)/2 instead of f² doubles per front (the upper part
+// is zeroed once at upload and never touched). task = (node, first column of a run of MF_ZC columns; a small front
+// is one task).
+__global__ void __launch_bounds__(SP_THREADS) mf_zero_kernel(SparseArgs a, const int32_t* tasks) {
+  const MfArgs& m = a.mf;
+  const int node = tasks[2 * blockIdx.x], c0 = tasks[2 * blockIdx.x + 1];
+  const int64_t f = m.fdim[node];
+  double* F = m.F + m.foff[node];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int64_t c1 = f <= MF_SMALL ? f : (f < c0 + MF_ZC ? f : (int64_t)(c0 + MF_ZC));  // a small front: one task
+  for (int64_t c = c0 + warp; c < c1; c += SP_THREADS / 32) {
+    double* col = F + c * f;
+    for (int64_t r = c + lane; r < f; r += 32) col[r] = 0.0;
+  }
+}
+
 __global__ void mf_assemble_kernel(SparseArgs a) {
   const MfArgs& m = a.mf;
   for (int64_t b = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; b < m.nblk;
@@ -656,9 +677,10 @@ __global__ void __launch_bounds__(128) mf_ea_kernel(SparseArgs a, const int32_t*
 }
 
 // Panel step 1: Cholesky of the kb×kb diagonal block at k0, and its inverse L⁻¹ (kept per front and chunk: the
-// TRSM of this panel and the triangular solves use it). Blocked by 8×8: warp 0 factors a diagonal block (and
-// inverts it), the CTA scales the block column and applies the rank-8 trailing update; the inverse of the
-// whole lower factor is formed block row by block row, X_ij = −X_ii Σ_{j≤k<i} L_ik X_kj.
+// TRSM of this panel and the triangular solves use it). Blocked by 8×8: warp 0 factors a diagonal block, the CTA
+// solves the block column below against it (forward substitution per row) and applies the rank-8 trailing update.
+// The inverse is formed afterwards by recursive doubling: the eight 8×8 diagonal inverses at once, then blocks of
+// 16, 32, 64 with X21 = −X22 (L21 X11) (two CTA-wide products per level instead of a serial sweep over block rows).
 constexpr int PB = 8;
 __global__ void __launch_bounds__(SP_THREADS) mf_potrf_kernel(SparseArgs a, const int32_t* tasks, int k0) {
   extern __shared__ double psm[];
@@ -688,7 +710,7 @@ __global__ void __launch_bounds__(SP_THREADS) mf_potrf_kernel(SparseArgs a, cons
   const int nbk = (kb + PB - 1) / PB;
   for (int bk = 0; bk < nbk; ++bk) {
     const int c0 = PB * bk;
-    if (warp == 0) {  // 8×8 diagonal block: Cholesky, then its inverse into X's diagonal block
+    if (warp == 0) {  // 8×8 diagonal block: Cholesky (1 / L_jj kept)
       for (int j = 0; j < PB; ++j) {
         double d = L[c0 + j][c0 + j];
         if (!(d > 0.0)) {
@@ -711,31 +733,22 @@ __global__ void __launch_bounds__(SP_THREADS) mf_potrf_kernel(SparseArgs a, cons
         }
         __syncwarp();
       }
-      if (lane < PB) {  // column `lane` of the inverse of the 8×8 lower block by forward substitution
-        const int j = lane;
-        for (int i = 0; i < PB; ++i) {
-          double v = (i == j) ? 1.0 : 0.0;
-          for (int l = j; l < i; ++l) v -= L[c0 + i][c0 + l] * X[c0 + l][c0 + j];
-          X[c0 + i][c0 + j] = i >= j ? v * dinv[c0 + i] : 0.0;
-        }
-      }
     }
     __syncthreads();
-    // block column below: L[r, c0:c0+8] ← L[r, c0:c0+8] X_bbᵀ (one thread per row)
+    // block column below: L[r, c0:c0+8] ← L[r, c0:c0+8] L_bb⁻ᵀ, forward substitution (one thread per row)
     for (int r = c0 + PB + tid; r < MF_NB; r += blockDim.x) {
-      double v[PB], w[PB];
+      double v[PB];
 #pragma unroll
       for (int e = 0; e < PB; ++e) v[e] = L[r][c0 + e];
 #pragma unroll
       for (int c = 0; c < PB; ++c) {
-        double acc = 0.0;
+        double acc = v[c];
 #pragma unroll
-        for (int e = 0; e < PB; ++e)
-          if (e <= c) acc += v[e] * X[c0 + c][c0 + e];
-        w[c] = acc;
+        for (int e = 0; e < c; ++e) acc -= v[e] * L[c0 + c][c0 + e];
+        v[c] = acc * dinv[c0 + c];
       }
 #pragma unroll
-      for (int e = 0; e < PB; ++e) L[r][c0 + e] = w[e];
+      for (int e = 0; e < PB; ++e) L[r][c0 + e] = v[e];
     }
     __syncthreads();
     // rank-8 trailing update of the lower part: rows and columns ≥ c0+8
@@ -756,50 +769,39 @@ __global__ void __launch_bounds__(SP_THREADS) mf_potrf_kernel(SparseArgs a, cons
     const int r = idx % kb, c = idx / kb;
     if (r >= c) F[(k0 + c) * f + k0 + r] = L[r][c];
   }
-  // inverse of the whole factor: block rows i = 1 … nbk−1, X_ij = −X_ii Σ_{k=j}^{i−1} L_ik X_kj (j < i)
-  for (int bi = 1; bi < nbk; ++bi) {
-    const int r0 = PB * bi;
-    // T = Σ_k L_ik X_kj for all j < i: thread (r, c) of the block row, columns c < r0
-    double t[2] = {0.0, 0.0};
-    int rr[2], cc[2];
-#pragma unroll
-    for (int q = 0; q < 2; ++q) {
-      const int idx = tid + q * SP_THREADS;  // PB × r0 ≤ 8 × 56 = 448 entries
-      rr[q] = r0 + idx % PB;
-      cc[q] = idx / PB;
-      if (cc[q] < r0) {
-        const int bj = cc[q] / PB;
-        double acc = 0.0;
-        for (int k = PB * bj; k < r0; ++k) acc += L[rr[q]][k] * X[k][cc[q]];
-        t[q] = acc;
-      }
+  // the eight 8×8 diagonal inverses (padding blocks are identities): thread (b, j) forms column j of block b
+  if (tid < MF_NB) {
+    const int c0 = PB * (tid / PB), j = tid % PB;
+    for (int i = 0; i < PB; ++i) {
+      double v = (i == j) ? 1.0 : 0.0;
+      for (int l = j; l < i; ++l) v -= L[c0 + i][c0 + l] * X[c0 + l][c0 + j];
+      X[c0 + i][c0 + j] = i >= j ? v / L[c0 + i][c0 + i] : 0.0;
+    }
+  }
+  __syncthreads();
+  // recursive doubling: pairs of s×s diagonal blocks at p, p + s: X21 = −X22 T with T = L21 X11; T is parked
+  // transposed in X's upper part (X[p + j][p + s + i], never read as part of the inverse; masked on output)
+  for (int s = PB; s < MF_NB; s *= 2) {
+    const int ne = (MF_NB / (2 * s)) * s * s;
+    for (int e = tid; e < ne; e += blockDim.x) {
+      const int p = (e / (s * s)) * 2 * s, i = (e % (s * s)) / s, j = e % s;
+      double acc = 0.0;
+      for (int l = j; l < s; ++l) acc += L[p + s + i][p + l] * X[p + l][p + j];  // X11 lower: l ≥ j
+      X[p + j][p + s + i] = acc;
     }
     __syncthreads();
-#pragma unroll
-    for (int q = 0; q < 2; ++q)  // park T in the (still zero) upper part of X: X[c][r] for c < r0 ≤ r
-      if (cc[q] < r0) X[cc[q]][rr[q]] = t[q];
-    __syncthreads();
-#pragma unroll
-    for (int q = 0; q < 2; ++q) {
-      if (cc[q] < r0) {
-        double acc = 0.0;
-        for (int e = 0; e < PB; ++e) acc += X[rr[q]][r0 + e] * X[cc[q]][r0 + e];  // X_ii row · T column
-        t[q] = -acc;
-      }
+    for (int e = tid; e < ne; e += blockDim.x) {
+      const int p = (e / (s * s)) * 2 * s, i = (e % (s * s)) / s, j = e % s;
+      double acc = 0.0;
+      for (int l = 0; l <= i; ++l) acc += X[p + s + i][p + s + l] * X[p + j][p + s + l];  // X22 lower: l ≤ i
+      X[p + s + i][p + j] = -acc;
     }
-    __syncthreads();
-#pragma unroll
-    for (int q = 0; q < 2; ++q)
-      if (cc[q] < r0) {
-        X[rr[q]][cc[q]] = t[q];
-        X[cc[q]][rr[q]] = 0.0;
-      }
     __syncthreads();
   }
   double* out = m.linv + m.loff[node] + (int64_t)(k0 / MF_NB) * MF_NB * MF_NB;
   for (int idx = tid; idx < MF_NB * MF_NB; idx += blockDim.x) {
     const int r = idx / MF_NB, c = idx % MF_NB;
-    out[idx] = (r < kb && c < kb) ? X[r][c] : 0.0;
+    out[idx] = (r < kb && c < kb && c <= r) ? X[r][c] : 0.0;
   }
 }
 
@@ -1135,7 +1137,7 @@ __global__ void __launch_bounds__(SP_THREADS) mf_bwd_kernel(SparseArgs a, const 
   for (int i = tid; i < n; i += blockDim.x) sol[(i % 3) * a.np + m.ipos[first + i / 3]] = x[i];
 }
 
-// ---- triangular solves of large fronts, parallel over 64-row / 64-column tiles, one launch per 64-chunk
+// ---- triangular solves of large fronts, parallel over 64-row / 64-column tiles, one launch per group of MF_SG 64-chunks
 // Forward init: w = [own rhs; 0] + the children's boundary vectors (into the node's solve vector).
 __global__ void __launch_bounds__(SP_THREADS) mf_fwd_init_kernel(SparseArgs a, const int32_t* nodes, const double* src) {
   if (refine_gated(a)) return;
@@ -1158,43 +1160,57 @@ __global__ void __launch_bounds__(SP_THREADS) mf_fwd_init_kernel(SparseArgs a, c
   }
 }
 
-// Forward chunk c: every CTA forms y_c = L_cc⁻¹ w_c; the writer task stores it, the others update their 64 rows
-// below the chunk: w_r −= L[r, chunk] y_c. task = (node, r0 or −1, writer flag).
-__global__ void __launch_bounds__(SP_THREADS) mf_fwd_chunk_kernel(SparseArgs a, const int32_t* tasks, int c,
+// Forward group of MF_SG chunks from c0 (chunks of 64 own columns; one launch per group instead of per chunk):
+// every CTA forms the group's y redundantly, chunk by chunk, y_s = L_ss⁻¹ (w_s − Σ_{t<s} L_st y_t) with the
+// L_st blocks read from the front (L2-resident, 32 KB per pair); the writer task stores y, the others update
+// their 64 rows below the group: w_r −= Σ_{j in group} L[r][j] y_j. task = (node, r0 or −1, writer flag).
+__global__ void __launch_bounds__(SP_THREADS) mf_fwd_chunk_kernel(SparseArgs a, const int32_t* tasks, int c0,
                                                                  double* dst) {
   if (refine_gated(a)) return;
-  __shared__ double yc[MF_NB];
+  __shared__ double yc[MF_SG * MF_NB];
+  __shared__ double wl[MF_NB];
   __shared__ double part[4][MF_NB];
   const MfArgs& m = a.mf;
   const int node = tasks[3 * blockIdx.x], r0 = tasks[3 * blockIdx.x + 1], writer = tasks[3 * blockIdx.x + 2];
   const int n = m.nown[node];
   const int64_t f = m.fdim[node];
-  const int k0 = c * MF_NB, kb = min(MF_NB, n - k0);
+  const int k00 = c0 * MF_NB, cols = min(MF_SG * MF_NB, n - k00);
   const double* F = m.F + m.foff[node];
   double* w = m.wvec + m.woff[node];
-  const double* li = m.linv + m.loff[node] + (int64_t)c * MF_NB * MF_NB;
-  const int tid = threadIdx.x;
-  {  // y_c[i] = Σ_j Linv[i][j] w[k0+j]: 4 threads per row
-    const int i = tid % MF_NB, g = tid / MF_NB;
-    double s = 0.0;
-    if (i < kb)
-      for (int j = g * 16; j < min(kb, g * 16 + 16); ++j) s += li[i * MF_NB + j] * w[k0 + j];
-    part[g][i] = s;
+  const int tid = threadIdx.x, i = tid % MF_NB, g = tid / MF_NB;
+  for (int s = 0; s * MF_NB < cols; ++s) {
+    const int k0 = k00 + s * MF_NB, kb = min(MF_NB, n - k0);
+    {  // w_s − Σ_{t<s} L_st y_t: row k0+i, 4 threads per row over the group's earlier columns
+      double acc = 0.0;
+      if (i < kb)
+        for (int j = g; j < s * MF_NB; j += 4) acc += F[(int64_t)(k00 + j) * f + k0 + i] * yc[j];
+      part[g][i] = acc;
+    }
+    __syncthreads();
+    if (tid < MF_NB) wl[tid] = tid < kb ? w[k0 + tid] - (part[0][tid] + part[1][tid] + part[2][tid] + part[3][tid]) : 0.0;
+    __syncthreads();
+    {  // y_s[i] = Σ_j Linv[i][j] wl[j]: 4 threads per row
+      const double* li = m.linv + m.loff[node] + (int64_t)(c0 + s) * MF_NB * MF_NB;
+      double acc = 0.0;
+      if (i < kb)
+        for (int j = g * 16; j < min(kb, g * 16 + 16); ++j) acc += li[i * MF_NB + j] * wl[j];
+      part[g][i] = acc;
+    }
+    __syncthreads();
+    if (tid < MF_NB) yc[s * MF_NB + tid] = part[0][tid] + part[1][tid] + part[2][tid] + part[3][tid];
+    __syncthreads();
   }
-  __syncthreads();
-  if (tid < MF_NB) yc[tid] = part[0][tid] + part[1][tid] + part[2][tid] + part[3][tid];
-  __syncthreads();
-  if (writer && tid < kb) {
-    const int i = k0 + tid;
-    dst[(i % 3) * a.np + m.ipos[m.own_first[node] + i / 3]] = yc[tid];
-  }
+  if (writer)
+    for (int j = tid; j < cols; j += blockDim.x) {
+      const int e = k00 + j;
+      dst[(e % 3) * a.np + m.ipos[m.own_first[node] + e / 3]] = yc[j];
+    }
   if (r0 < 0) return;
-  const int i = tid % MF_NB, g = tid / MF_NB;
   const int64_t r = r0 + i;
-  double s = 0.0;
+  double acc = 0.0;
   if (r < f)
-    for (int j = g * 16; j < min(kb, g * 16 + 16); ++j) s += F[(k0 + j) * f + r] * yc[j];
-  part[g][i] = s;
+    for (int j = g; j < cols; j += 4) acc += F[(int64_t)(k00 + j) * f + r] * yc[j];
+  part[g][i] = acc;
   __syncthreads();
   if (tid < MF_NB && r0 + tid < f) w[r0 + tid] -= part[0][tid] + part[1][tid] + part[2][tid] + part[3][tid];
 }
@@ -1238,46 +1254,62 @@ __global__ void __launch_bounds__(SP_THREADS) mf_bwd_bnd_kernel(SparseArgs a, co
   }
 }
 
-// Backward chunk c (last chunk first): every CTA forms x_c = L_cc⁻ᵀ z_c; the writer stores it, the others update
-// the 64 earlier own columns of their tile: z_i −= Σ_{r in chunk} L[r][i] x_r. task = (node, t0 or −1, writer).
-__global__ void __launch_bounds__(SP_THREADS) mf_bwd_chunk_kernel(SparseArgs a, const int32_t* tasks, int c,
+// Backward group of MF_SG chunks from c0 (the last group first; inside it the last chunk first): every CTA forms
+// x_s = L_ss⁻ᵀ (z_s − Σ_{t>s} L_tsᵀ x_t) redundantly; the writer stores x, the others update the 64 earlier own
+// columns of their tile: z_i −= Σ_{r in group} L[r][i] x_r. task = (node, t0 or −1, writer).
+__global__ void __launch_bounds__(SP_THREADS) mf_bwd_chunk_kernel(SparseArgs a, const int32_t* tasks, int c0,
                                                                  double* sol) {
   if (refine_gated(a)) return;
-  __shared__ double xc[MF_NB];
+  __shared__ double xc[MF_SG * MF_NB];
+  __shared__ double zl[MF_NB];
   __shared__ double part[4][MF_NB];
   const MfArgs& m = a.mf;
   const int node = tasks[3 * blockIdx.x], t0 = tasks[3 * blockIdx.x + 1], writer = tasks[3 * blockIdx.x + 2];
   const int n = m.nown[node];
   const int64_t f = m.fdim[node];
-  const int k0 = c * MF_NB, kb = min(MF_NB, n - k0);
+  const int k00 = c0 * MF_NB, cols = min(MF_SG * MF_NB, n - k00);
   const double* F = m.F + m.foff[node];
   double* x = m.wvec + m.woff[node];
-  const double* li = m.linv + m.loff[node] + (int64_t)c * MF_NB * MF_NB;
   const int tid = threadIdx.x;
-  {  // x_c[i] = Σ_j Linv[j][i] z[k0+j]
-    const int i = tid % MF_NB, g = tid / MF_NB;
-    double s = 0.0;
-    if (i < kb)
-      for (int j = max(i, g * 16); j < min(kb, g * 16 + 16); ++j) s += li[j * MF_NB + i] * x[k0 + j];
-    part[g][i] = s;
+  const int cc = tid / 4, g4 = tid % 4;  // column cc of a 64-column block, 4 threads per column
+  for (int s = (cols - 1) / MF_NB; s >= 0; --s) {
+    const int k0 = k00 + s * MF_NB, kb = min(MF_NB, n - k0);
+    {  // z_s − Σ_{t>s} L_tsᵀ x_t: column k0+cc over the group's later rows
+      double acc = 0.0;
+      if (cc < kb) {
+        const double* col = F + (int64_t)(k0 + cc) * f + k00;
+        for (int r = (s + 1) * MF_NB + g4; r < cols; r += 4) acc += col[r] * xc[r];
+      }
+      acc += __shfl_down_sync(0xffffffffu, acc, 2, 4);
+      acc += __shfl_down_sync(0xffffffffu, acc, 1, 4);
+      if (g4 == 0) zl[cc] = cc < kb ? x[k0 + cc] - acc : 0.0;
+    }
+    __syncthreads();
+    {  // x_s[i] = Σ_{j ≥ i} Linv[j][i] zl[j]
+      const double* li = m.linv + m.loff[node] + (int64_t)(c0 + s) * MF_NB * MF_NB;
+      const int i = tid % MF_NB, g = tid / MF_NB;
+      double acc = 0.0;
+      if (i < kb)
+        for (int j = max(i, g * 16); j < min(kb, g * 16 + 16); ++j) acc += li[j * MF_NB + i] * zl[j];
+      part[g][i] = acc;
+    }
+    __syncthreads();
+    if (tid < MF_NB) xc[s * MF_NB + tid] = part[0][tid] + part[1][tid] + part[2][tid] + part[3][tid];
+    __syncthreads();
   }
-  __syncthreads();
-  if (tid < MF_NB) xc[tid] = part[0][tid] + part[1][tid] + part[2][tid] + part[3][tid];
-  __syncthreads();
-  if (writer && tid < kb) {
-    const int i = k0 + tid;
-    sol[(i % 3) * a.np + m.ipos[m.own_first[node] + i / 3]] = xc[tid];
-  }
+  if (writer)
+    for (int j = tid; j < cols; j += blockDim.x) {
+      const int e = k00 + j;
+      sol[(e % 3) * a.np + m.ipos[m.own_first[node] + e / 3]] = xc[j];
+    }
   if (t0 < 0) return;
-  // column i = t0 + tid/4 (64 columns, 4 threads each over 16 chunk rows)
-  const int cc = tid / 4, g = tid % 4;
   const int i = t0 + cc;
-  double s = 0.0;
-  const double* col = F + (int64_t)i * f + k0;
-  for (int r = g * 16; r < min(kb, g * 16 + 16); ++r) s += col[r] * xc[r];
-  s += __shfl_down_sync(0xffffffffu, s, 2, 4);
-  s += __shfl_down_sync(0xffffffffu, s, 1, 4);
-  if (g == 0 && i < k0) x[i] -= s;
+  double acc = 0.0;
+  const double* col = F + (int64_t)i * f + k00;
+  for (int r = g4; r < cols; r += 4) acc += col[r] * xc[r];
+  acc += __shfl_down_sync(0xffffffffu, acc, 2, 4);
+  acc += __shfl_down_sync(0xffffffffu, acc, 1, 4);
+  if (g4 == 0 && i < k00) x[i] -= acc;
 }
 
 // ============================================================================ host side: launches
@@ -1317,7 +1349,7 @@ static cudaError_t mf_solve(const SparsePlan& sp, const SparseArgs& a, const int
     if (L.n_big) {
       mf_fwd_init_kernel<<<(unsigned)L.n_big, SP_THREADS, 0, st>>>(a, LN + L.big, src);
       for (size_t c = 0; c < L.fwd.size(); ++c)
-        mf_fwd_chunk_kernel<<<(unsigned)L.n_fwd[c], SP_THREADS, 0, st>>>(a, T + L.fwd[c], (int)c, a.yy);
+        mf_fwd_chunk_kernel<<<(unsigned)L.n_fwd[c], SP_THREADS, 0, st>>>(a, T + L.fwd[c], (int)c * MF_SG, a.yy);
     }
   }
   for (int l = nl - 1; l >= 0; --l) {  // backward: root first
@@ -1328,7 +1360,7 @@ static cudaError_t mf_solve(const SparsePlan& sp, const SparseArgs& a, const int
       mf_bwd_init_kernel<<<(unsigned)L.n_big, SP_THREADS, 0, st>>>(a, LN + L.big, a.yy, dst);
       if (L.n_bwdb) mf_bwd_bnd_kernel<<<(unsigned)L.n_bwdb, SP_THREADS, 0, st>>>(a, T + L.bwdb);
       for (int c = (int)L.bwd.size() - 1; c >= 0; --c)
-        mf_bwd_chunk_kernel<<<(unsigned)L.n_bwd[c], SP_THREADS, 0, st>>>(a, T + L.bwd[c], c, dst);
+        mf_bwd_chunk_kernel<<<(unsigned)L.n_bwd[c], SP_THREADS, 0, st>>>(a, T + L.bwd[c], c * MF_SG, dst);
     }
   }
   return cudaGetLastError();
@@ -1346,7 +1378,11 @@ cudaError_t sparse_step(const Plan& p, const DevPtrs& d, const StepConsts& k, cu
   if (a.nproj) proj_rows_kernel<<<(unsigned)((a.nproj + 127) / 128), 128, 0, st>>>(a);
   sparse_rhs_kernel<<<grid_for(a.np), 256, 0, st>>>(a);
   cudaError_t e;
+#ifdef MF_ZERO_FULL
   if ((e = cudaMemsetAsync(a.mf.F, 0, sizeof(double) * sp.front_doubles, st))) return e;
+#else
+  if (sp.n_zero) mf_zero_kernel<<<(unsigned)sp.n_zero, SP_THREADS, 0, st>>>(a, d.sparse_tasks + sp.zero);
+#endif
   mf_assemble_kernel<<<grid_for(a.mf.nblk), 256, 0, st>>>(a);
   const int32_t* LN = d.sparse_lev;
   const int32_t* T = d.sparse_tasks;
@@ -1919,18 +1955,19 @@ static bool mf_symbolic(const mabd_bodies* B, Plan* plan, std::string* msg) {
       }
       Pn.n_syrk = ((int64_t)s.tasks.size() - Pn.syrk) / 5;
     }
-    // triangular-solve tasks of the big fronts
-    L.fwd.assign(maxpan, 0);
-    L.n_fwd.assign(maxpan, 0);
-    L.bwd.assign(maxpan, 0);
-    L.n_bwd.assign(maxpan, 0);
-    for (int c = 0; c < maxpan; ++c) {
-      const int k0 = c * MF_NB;
+    // triangular-solve tasks of the big fronts, per group of MF_SG chunks
+    const int ngrp = (maxpan + MF_SG - 1) / MF_SG;
+    L.fwd.assign(ngrp, 0);
+    L.n_fwd.assign(ngrp, 0);
+    L.bwd.assign(ngrp, 0);
+    L.n_bwd.assign(ngrp, 0);
+    for (int c = 0; c < ngrp; ++c) {
+      const int k0 = c * MF_SG * MF_NB;
       L.fwd[c] = (int64_t)s.tasks.size();
       for (int32_t i : big) {
         if (s.nown[i] <= k0) continue;
         int wr = 1;
-        for (int r0 = k0 + std::min(MF_NB, s.nown[i] - k0); r0 < s.fdim[i]; r0 += MF_NB, wr = 0) {
+        for (int r0 = k0 + std::min(MF_SG * MF_NB, s.nown[i] - k0); r0 < s.fdim[i]; r0 += MF_NB, wr = 0) {
           s.tasks.push_back(i);
           s.tasks.push_back(r0);
           s.tasks.push_back(wr);
@@ -1968,6 +2005,15 @@ static bool mf_symbolic(const mabd_bodies* B, Plan* plan, std::string* msg) {
         }
     L.n_bwdb = ((int64_t)s.tasks.size() - L.bwdb) / 2;
   }
+#ifndef MF_ZERO_FULL
+  s.zero = (int64_t)s.tasks.size();  // lower-triangle zeroing: MF_ZC columns per task
+  for (int i = 0; i < s.nnode; ++i)
+    for (int c0 = 0; c0 < s.fdim[i]; c0 += s.fdim[i] <= MF_SMALL ? s.fdim[i] : MF_ZC) {
+      s.tasks.push_back(i);
+      s.tasks.push_back(c0);
+    }
+  s.n_zero = ((int64_t)s.tasks.size() - s.zero) / 2;
+#endif
   if (s.tasks.size() > (size_t)INT32_MAX || s.ablk.size() / 3 > (size_t)INT32_MAX)
     return *msg = "sparse symbolic: too many tasks", false;
   return true;
@@ -2158,7 +2204,7 @@ bool sparse_build(const mabd_bodies* B, const mabd_joints* J, Plan* p, std::vect
   s.refine_tol = MF_REFINE_TOL;
   s.syrk_dfma = getenv("MABD_SPARSE_SYRK_DFMA") != nullptr;  // developer knob: the DFMA trailing update
   if (const char* ev = getenv("MABD_SPARSE_REFINE_TOL")) s.refine_tol = atof(ev);                   // developer knob
-  int64_t launches = 4 + (P ? 2 : 0);
+  int64_t launches = 4 + (P ? 2 : 0) + (s.n_zero ? 1 : 0);
   for (const auto& L : s.levels) {
     int64_t per = (L.n_small ? 1 : 0);
     for (int64_t c : L.n_ea) per += c ? 1 : 0;
@@ -2472,6 +2518,7 @@ cudaError_t sparse_upload(const Plan& p, char* ws, cudaStream_t st, DevPtrs* d) 
   if ((e = upv(ws, s.o_gs_off, s.gs_chain_off, st))) return e;
   if ((e = upv(ws, s.o_gs_col, s.gs_color_off, st))) return e;
   if ((e = cudaMemsetAsync(A.lam, 0, sizeof(double) * 3 * np, st))) return e;
+  if ((e = cudaMemsetAsync(A.mf.F, 0, sizeof(double) * s.front_doubles, st))) return e;  // upper parts stay 0
   int32_t it[10] = {0, 0, 0, 0, 0, 0, 0, 0, 0, 0};  // iters[4] and rmax[3] = 0
   if ((e = cudaMemcpyAsync(A.iters, it, sizeof(it), cudaMemcpyHostToDevice, st))) return e;
   return cudaStreamSynchronize(st);  // the host vectors above are pageable; keep them alive until copied
