@@ -39,8 +39,14 @@ constexpr int MF_NB = 64;          // panel width and tile size of the large-fro
 #define MF_SG 2               // 64-chunks per triangular-solve launch of the large fronts
 #endif
 constexpr int MF_ZC = 16;          // columns per CTA of the per-step lower-triangle zeroing of large fronts
-constexpr int MF_SMALL = 96;       // fronts with f ≤ MF_SMALL are factored in shared memory by one CTA
-constexpr int MF_LEAF_PTS = 12;    // nested dissection stops at regions of ≤ this many points
+#ifndef MF_SMALL_F
+#define MF_SMALL_F 96
+#endif
+#ifndef MF_LEAF_P
+#define MF_LEAF_P 8
+#endif
+constexpr int MF_SMALL = MF_SMALL_F;  // fronts with f ≤ MF_SMALL are factored in shared memory by one CTA
+constexpr int MF_LEAF_PTS = MF_LEAF_P;  // nested dissection stops at regions of ≤ this many points
 constexpr int MF_REFINE = 1;       // iterative-refinement passes per step (default; each gated, see below)
 constexpr double MF_REFINE_TOL = 1e-10;  // a pass runs only if max|r − Sλ| > this · max|r| (refine_gate_kernel)
 
